@@ -1,0 +1,235 @@
+/* gx_b200.h -- C-ABI of the B200-native Ginex data-preparation hot path.
+ *
+ * The reference ("gx", header-only C++20 at /root/reference/proj/include/gx) is
+ * bound by C++ callers; this header is the drop-in boundary a maintainer binds
+ * instead (see INTEGRATION.md for the C++ adapter and the ctypes binding used by
+ * the Python mirror in paper_2208_09151_b200/api.py). Every entry point names the
+ * reference interface it replaces as file:line relative to /root/reference/proj.
+ *
+ * Conventions
+ *  - Plain pointers + sizes only; host pointers unless a name ends in _dev.
+ *  - Node ids are u64 at the boundary (as in the reference, common.hpp:22) and
+ *    u32 on the device; graphs with >= 2^32-1 nodes are rejected (GX_OVERFLOW).
+ *  - Every call returns gx_status. On failure gx_last_error() holds the message
+ *    (thread-local). The status maps 1:1 onto the C++ exception type the
+ *    reference throws at the same point (std::invalid_argument, out_of_range,
+ *    logic_error, runtime_error, overflow_error); the C++ adapter rethrows it.
+ *  - Validation happens before any state mutation, as in the reference
+ *    (feature_cache.hpp:96-112).
+ *  - Handles are opaque; results live in device memory until copied out.
+ */
+#ifndef GX_B200_H
+#define GX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gx_status {
+    GX_OK = 0,
+    GX_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    GX_OUT_OF_RANGE = 2,     /* std::out_of_range */
+    GX_LOGIC_ERROR = 3,      /* std::logic_error */
+    GX_RUNTIME_ERROR = 4,    /* std::runtime_error (I/O, format) */
+    GX_OVERFLOW = 5,         /* std::overflow_error */
+    GX_CUDA_ERROR = 6        /* device failure (no reference counterpart) */
+} gx_status;
+
+/* IoStats (common.hpp:32-45): same field order and meaning. */
+typedef struct gx_iostats {
+    uint64_t pages_read;
+    uint64_t rows_read;
+    uint64_t neighbor_lists_read;
+    uint64_t bytes_read;
+} gx_iostats;
+
+const char* gx_last_error(void);
+const char* gx_version(void);
+
+/* ---- context: one per process per GPU ---------------------------------- */
+typedef struct gx_ctx gx_ctx;
+gx_status gx_ctx_create(int device, gx_ctx** out);
+void gx_ctx_destroy(gx_ctx* ctx);
+gx_status gx_ctx_synchronize(gx_ctx* ctx);
+/* the cudaStream_t all work of this context is ordered on */
+void* gx_ctx_stream(gx_ctx* ctx);
+
+/* ---- primitives (common.hpp:48-61, 90-101) ------------------------------ */
+uint64_t gx_mix64(uint64_t z);
+uint64_t gx_derive_seed(uint64_t base, uint64_t index);
+uint64_t gx_pages_touched(uint64_t lo, uint64_t hi);
+gx_status gx_page_count_for_row(uint64_t row_bytes, uint64_t row_index, uint64_t* pages);
+
+/* ---- graph: GraphFile (graph_store.hpp:106-197), CscGraph (:33-49) ------
+ * The whole CSC (indptr u64[N+1], indices u32[E]) is HBM-resident. */
+typedef struct gx_graph gx_graph;
+/* GraphFile::open (graph_store.hpp:108-133): same header checks and errors. */
+gx_status gx_graph_open(gx_ctx* ctx, const char* path, gx_graph** out);
+/* from a host CSC (CscGraph layout, graph_store.hpp:33-36) */
+gx_status gx_graph_from_csc(gx_ctx* ctx, uint64_t num_nodes, const uint64_t* indptr,
+                            const uint64_t* indices, gx_graph** out);
+/* generate_edges + build_csc on the device (graphgen.hpp:55-70,
+ * graph_store.hpp:53-81): byte-identical CSC to the reference generator. */
+gx_status gx_graph_generate_rmat(gx_ctx* ctx, uint64_t num_nodes, double avg_degree, double a,
+                                 double b, double c, uint64_t edge_seed, gx_graph** out);
+void gx_graph_destroy(gx_graph* g);
+uint64_t gx_graph_num_nodes(const gx_graph* g);
+uint64_t gx_graph_num_edges(const gx_graph* g);
+/* GraphFile::in_degree (graph_store.hpp:138-141) */
+gx_status gx_graph_in_degree(const gx_graph* g, uint64_t v, uint64_t* deg);
+/* copy the CSC back to the host (load_graph, graph_store.hpp:202-215) */
+gx_status gx_graph_copy_csc(const gx_graph* g, uint64_t* indptr, uint64_t* indices);
+/* persist_graph (graph_store.hpp:83-98): writes graph.bin byte-identically */
+gx_status gx_graph_write(const gx_graph* g, const char* path);
+
+/* ---- sampler (sampler.hpp) ---------------------------------------------- */
+typedef struct gx_samples gx_samples; /* S batches: ids + per-layer edges, on device */
+/* superbatch_sample (sampler.hpp:197-243) minus the file writes (see
+ * gx_samples_write_files): batch i is seeded derive_seed(global_seed,
+ * first_global_batch + i). seeds_flat/batch_offsets give S seed lists. */
+gx_status gx_sample_superbatch(gx_graph* g, const uint64_t* seeds_flat,
+                               const uint64_t* batch_offsets, uint64_t n_batches,
+                               const uint32_t* fanouts, uint32_t n_layers, uint64_t global_seed,
+                               uint64_t first_global_batch, gx_samples** out, gx_iostats* io);
+/* sample_batch (sampler.hpp:69-117) with an explicit batch seed. */
+gx_status gx_sample_batch(gx_graph* g, const uint64_t* seeds, uint64_t n_seeds,
+                          const uint32_t* fanouts, uint32_t n_layers, uint64_t batch_seed,
+                          gx_samples** out, gx_iostats* io);
+void gx_samples_destroy(gx_samples* s);
+uint64_t gx_samples_num_batches(const gx_samples* s);
+uint32_t gx_samples_num_layers(const gx_samples* s);
+/* SampleOutput sizes (sampler.hpp:36-40): ids count, seed count, edges per layer */
+gx_status gx_samples_batch_info(const gx_samples* s, uint64_t b, uint64_t* n_ids,
+                                uint64_t* n_seeds, uint64_t* layer_counts);
+gx_status gx_samples_copy_ids(const gx_samples* s, uint64_t b, uint64_t* ids);
+/* (src_local, dst_local) u32 pairs of one layer (LocalEdge, sampler.hpp:34) */
+gx_status gx_samples_copy_edges(const gx_samples* s, uint64_t b, uint32_t layer, uint32_t* pairs);
+/* total sampled edges over all batches/layers */
+uint64_t gx_samples_total_edges(const gx_samples* s);
+/* write ids_{sb}_{i}.bin / adj_{sb}_{i}.bin (sampler.hpp:123-182, FORMATS.md) */
+gx_status gx_samples_write_files(const gx_samples* s, const char* dir, uint64_t sb_index);
+
+/* ---- inspector (changeset.hpp) ------------------------------------------ */
+typedef struct gx_changesets gx_changesets;
+/* precompute_changesets (changeset.hpp:468-484) minus the files: init set =
+ * compute_init_set (:137-153), changesets = simulate_changesets (:228-295).
+ * Trace = S distinct-id lists given flat with offsets[S+1]. */
+gx_status gx_precompute_trace(gx_ctx* ctx, const uint64_t* ids_flat, const uint64_t* offsets,
+                              uint64_t n_iters, uint64_t num_nodes, uint64_t num_entries,
+                              gx_changesets** out);
+/* same, with an explicit init set (simulate_changesets' `init`, :230) */
+gx_status gx_simulate_trace(gx_ctx* ctx, const uint64_t* ids_flat, const uint64_t* offsets,
+                            uint64_t n_iters, uint64_t num_nodes, uint64_t num_entries,
+                            const uint64_t* init, uint64_t n_init, gx_changesets** out);
+/* precompute over a device-resident sampler result (the inspector stage of
+ * the pipeline: no host round trip of the ids trace) */
+gx_status gx_precompute_samples(const gx_samples* s, uint64_t num_nodes, uint64_t num_entries,
+                                gx_changesets** out);
+/* build_access_index (changeset.hpp:124-129): iters[A+1] and ptr[N], byte
+ * layout of AccessIndex including MSB region flags and the dummy tail. */
+gx_status gx_access_index(gx_ctx* ctx, const uint64_t* ids_flat, const uint64_t* offsets,
+                          uint64_t n_iters, uint64_t num_nodes, uint64_t* iters, uint64_t* ptr);
+void gx_changesets_destroy(gx_changesets* cs);
+uint64_t gx_changesets_num_iters(const gx_changesets* cs);
+/* init set in admission (slot) order */
+gx_status gx_changesets_init(const gx_changesets* cs, uint64_t* out, uint64_t* n);
+uint64_t gx_changesets_init_size(const gx_changesets* cs);
+/* Changeset sizes + SimulationResult::misses[i] (changeset.hpp:161-178) */
+gx_status gx_changesets_iter_info(const gx_changesets* cs, uint64_t i, uint64_t* n_in,
+                                  uint64_t* n_out, uint64_t* misses);
+/* in_ids (by position), out_ids (by id), in_positions */
+gx_status gx_changesets_copy_iter(const gx_changesets* cs, uint64_t i, uint64_t* in_ids,
+                                  uint64_t* out_ids, uint64_t* in_positions);
+/* all per-iteration misses (SimulationResult::misses) */
+gx_status gx_changesets_misses(const gx_changesets* cs, uint64_t* misses);
+/* write init_{sb}.bin + update_{sb}_{i}.bin (changeset.hpp:409-454) */
+gx_status gx_changesets_write_files(const gx_changesets* cs, const char* dir, uint64_t sb_index);
+
+/* ---- executor: feature table + FeatureCache (feature_cache.hpp) ---------- */
+typedef struct gx_features gx_features;
+typedef enum gx_backing {
+    GX_BACKING_DEVICE = 0, /* whole table in HBM (fits one B200 up to ~150 GB) */
+    GX_BACKING_HOST = 1    /* pinned host memory, misses read over PCIe by the gather kernel */
+} gx_backing;
+/* FeatureFile::open (graph_store.hpp:282-302) + load of the payload. */
+gx_status gx_features_open(gx_ctx* ctx, const char* path, int backing, gx_features** out);
+/* from host rows (RowMatrix layout, graph_store.hpp:222-234); row_bytes =
+ * dim * scalar_width (scalar_width 4 = the reference format; 2 = fp16 ext.) */
+gx_status gx_features_from_host(gx_ctx* ctx, uint64_t num_nodes, uint32_t dim,
+                                uint32_t scalar_width, const void* rows, int backing,
+                                gx_features** out);
+/* generate the table on the device: feature_value (graphgen.hpp:74-77) */
+gx_status gx_features_generate(gx_ctx* ctx, uint64_t num_nodes, uint32_t dim,
+                               uint64_t value_seed, gx_features** out);
+void gx_features_destroy(gx_features* f);
+uint64_t gx_features_num_nodes(const gx_features* f);
+uint32_t gx_features_dim(const gx_features* f);
+uint64_t gx_features_row_bytes(const gx_features* f);
+/* FeatureFile::read_rows (graph_store.hpp:319-324) into host memory */
+gx_status gx_features_read_rows(gx_features* f, const uint64_t* ids, uint64_t n, void* out,
+                                gx_iostats* io);
+
+/* Gathered batch buffer (RowMatrix, graph_store.hpp:222-234), device resident. */
+typedef struct gx_batch gx_batch;
+gx_status gx_batch_create(gx_ctx* ctx, gx_batch** out);
+void gx_batch_destroy(gx_batch* b);
+uint64_t gx_batch_rows(const gx_batch* b);
+gx_status gx_batch_copy_to_host(const gx_batch* b, void* out);
+void* gx_batch_device_ptr(const gx_batch* b);
+
+typedef struct gx_cache gx_cache;
+/* FeatureCache ctor (feature_cache.hpp:19-37): init ids -> slots 0..k-1. */
+gx_status gx_cache_create(gx_features* f, const uint64_t* init, uint64_t n_init,
+                          uint64_t num_entries, gx_iostats* io, gx_cache** out);
+void gx_cache_destroy(gx_cache* c);
+uint64_t gx_cache_num_entries(const gx_cache* c);
+/* FeatureCache::gather (feature_cache.hpp:58-76) into a device batch */
+gx_status gx_cache_gather(gx_cache* c, const uint64_t* ids, uint64_t n, gx_batch* out,
+                          uint64_t* hits, uint64_t* misses, gx_iostats* io);
+/* FeatureCache::apply_changeset (feature_cache.hpp:89-130) */
+gx_status gx_cache_apply(gx_cache* c, const gx_batch* batch, const uint64_t* ids, uint64_t n_ids,
+                         const uint64_t* in_ids, const uint64_t* in_positions, uint64_t n_in,
+                         const uint64_t* out_ids, uint64_t n_out);
+/* test hooks: contains / cached_row / resident_set (feature_cache.hpp:28-34,119-125) */
+gx_status gx_cache_contains(const gx_cache* c, uint64_t v, int* out);
+gx_status gx_cache_cached_row(const gx_cache* c, uint64_t v, void* out);
+gx_status gx_cache_resident_set(const gx_cache* c, uint64_t* out, uint64_t cap, uint64_t* n);
+
+/* ---- fused device pipeline (TrainingRunner::run_superbatch stages 1-4,
+ * pipeline.hpp:338-377, minus the runtime files and the compute stub) ------
+ * sample -> precompute -> cache init ("switch") -> S x (gather, apply), all on
+ * the device; the ids trace, changesets and gathered batches never leave HBM.
+ * The pipeline owns its buffers and reuses them across superbatches. */
+typedef struct gx_pipeline gx_pipeline;
+typedef struct gx_pipeline_stats {
+    uint64_t sampled_edges;
+    uint64_t gathered_rows;   /* = accesses A = sum |ids_i| */
+    uint64_t total_misses;    /* observed by the gather; equals the inspector's prediction */
+    uint64_t predicted_misses;
+    uint64_t init_size;
+    uint64_t total_in, total_out;
+    gx_iostats sample_io;
+    gx_iostats gather_io;
+    double ms_sample, ms_inspect, ms_switch, ms_gather; /* device-timed stage durations */
+} gx_pipeline_stats;
+gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,
+                             uint32_t n_layers, uint64_t num_entries, gx_pipeline** out);
+void gx_pipeline_destroy(gx_pipeline* p);
+gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat,
+                                 const uint64_t* batch_offsets, uint64_t n_batches,
+                                 uint64_t global_seed, uint64_t first_global_batch,
+                                 uint64_t* misses_per_iter, gx_pipeline_stats* stats);
+/* Optional per-iteration digest of each gathered batch (for end-to-end parity
+ * checks; off by default, costs one extra read of every batch):
+ *   digest_i = sum_k sum_j (w_kj + 1) * mix64(k * W + j)  (mod 2^64)
+ * over the u32 words w_kj (W per row) of row k of iteration i's batch. */
+gx_status gx_pipeline_set_digest(gx_pipeline* p, int enable);
+gx_status gx_pipeline_digests(const gx_pipeline* p, uint64_t* digests_per_iter);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GX_B200_H */

@@ -1,0 +1,464 @@
+// capi.cu -- context, errors, primitives, changeset/sample accessors, runtime
+// file codecs (FORMATS.md "Runtime files") and the fused device pipeline.
+#include <algorithm>
+#include <cstdio>
+#include <fcntl.h>
+#include <unistd.h>
+#include <unordered_set>
+
+#include "gx_internal.cuh"
+
+namespace gx {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+static const char kIdsMagic[8] = {'G', 'X', 'I', 'D', 'S', '0', '0', '1'};
+static const char kAdjMagic[8] = {'G', 'X', 'A', 'D', 'J', '0', '0', '1'};
+static const char kInitMagic[8] = {'G', 'X', 'I', 'N', 'I', 'T', '0', '1'};
+static const char kUpdMagic[8] = {'G', 'X', 'U', 'P', 'D', '0', '0', '1'};
+
+// Little-endian buffered writer with the reference's failure semantics
+// (BinWriter, common.hpp:130-199): throws runtime_error on open/short write.
+struct Writer {
+    FILE* f = nullptr;
+    std::string path;
+    explicit Writer(const std::string& p) : path(p) {
+        f = std::fopen(p.c_str(), "wb");
+        if (!f) fail(GX_RUNTIME_ERROR, "cannot open for write: " + p);
+    }
+    ~Writer() {
+        if (f) std::fclose(f);
+    }
+    void raw(const void* p, size_t n) {
+        if (n && std::fwrite(p, 1, n, f) != n) fail(GX_RUNTIME_ERROR, "short write: " + path);
+    }
+    void u32(uint32_t v) { raw(&v, 4); }
+    void u64(uint64_t v) { raw(&v, 8); }
+    void close() {
+        if (f && std::fclose(f) != 0) {
+            f = nullptr;
+            fail(GX_RUNTIME_ERROR, "close failed: " + path);
+        }
+        f = nullptr;
+    }
+};
+
+static std::string rt_path(const char* dir, const char* stem, uint64_t sb, int64_t i) {
+    std::string p = std::string(dir) + "/" + stem + "_" + std::to_string(sb);
+    if (i >= 0) p += "_" + std::to_string(i);
+    return p + ".bin";
+}
+
+static void d2h_u32_as_u64(const uint32_t* d, uint64_t n, uint64_t* h) {
+    if (!n) return;
+    std::vector<uint32_t> t(n);
+    GX_CUDA(cudaMemcpy(t.data(), d, n * 4, cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < n; ++i) h[i] = t[i];
+}
+
+}  // namespace gx
+
+// ---------------------------------------------------------------------------
+// fused pipeline handle
+// ---------------------------------------------------------------------------
+struct gx_pipeline {
+    gx_graph* g = nullptr;
+    gx_features* f = nullptr;
+    gx_ctx* ctx = nullptr;
+    std::vector<uint32_t> fanouts;
+    uint64_t K = 0;
+    gx_samples samples;
+    gx_changesets cs;
+    gx::DevBuf<uint8_t> cache_rows;
+    gx::DevBuf<int32_t> table;
+    gx::DevBuf<uint8_t> batch;
+    gx::DevBuf<unsigned long long> counters;  // per iteration 8 words
+    gx::DevBuf<unsigned long long> digests;
+    bool digest = false;
+    std::vector<uint64_t> h_digests;
+    cudaEvent_t ev[5] = {};
+};
+
+using namespace gx;
+
+extern "C" {
+
+const char* gx_last_error(void) { return g_last_error.c_str(); }
+const char* gx_version(void) { return "gx_b200 0.1 (sm_100a)"; }
+
+uint64_t gx_mix64(uint64_t z) { return mix64(z); }
+uint64_t gx_derive_seed(uint64_t b, uint64_t i) { return derive_seed(b, i); }
+uint64_t gx_pages_touched(uint64_t lo, uint64_t hi) { return pages_touched(lo, hi); }
+gx_status gx_page_count_for_row(uint64_t w, uint64_t r, uint64_t* pages) {
+    return guard([&] {
+        if (w == 0) fail(GX_INVALID_ARGUMENT, "page_count_for_row: row_bytes must be > 0");
+        *pages = pages_touched(r * w, r * w + w);
+    });
+}
+
+gx_status gx_ctx_create(int device, gx_ctx** out) {
+    return guard([&] {
+        int n = 0;
+        GX_CUDA(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(GX_INVALID_ARGUMENT, "no such CUDA device");
+        GX_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        GX_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            fail(GX_CUDA_ERROR, std::string("gx_b200 is built for sm_100a; found ") + prop.name);
+        auto c = new gx_ctx();
+        c->device = device;
+        c->num_sms = prop.multiProcessorCount;
+        try {
+            GX_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+            c->barrier.alloc(1);
+            GX_CUDA(cudaMemset(c->barrier.p, 0, sizeof(GridBarrier)));
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void gx_ctx_destroy(gx_ctx* c) {
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    cudaStream_t s = c->stream;
+    delete c;
+    if (s) cudaStreamDestroy(s);
+}
+gx_status gx_ctx_synchronize(gx_ctx* c) {
+    return guard([&] { GX_CUDA(cudaStreamSynchronize(c->stream)); });
+}
+void* gx_ctx_stream(gx_ctx* c) { return c ? (void*)c->stream : nullptr; }
+
+// ---- inspector API ---------------------------------------------------------
+
+static std::vector<uint64_t> offsets_vec(const uint64_t* off, uint64_t S) {
+    std::vector<uint64_t> o(off, off + S + 1);
+    for (uint64_t i = 0; i < S; ++i)
+        if (o[i + 1] < o[i]) fail(GX_INVALID_ARGUMENT, "trace offsets must be non-decreasing");
+    if (o[0] != 0) {
+        const uint64_t b = o[0];
+        for (auto& x : o) x -= b;
+    }
+    return o;
+}
+
+gx_status gx_precompute_trace(gx_ctx* ctx, const uint64_t* flat, const uint64_t* off, uint64_t S, uint64_t N,
+                              uint64_t K, gx_changesets** out) {
+    return guard([&] {
+        auto o = offsets_vec(off, S);
+        inspect_fill_from_host(ctx, flat + off[0], o, N);
+        auto cs = new gx_changesets();
+        try {
+            inspect_run(ctx, o, N, K, nullptr, -1, cs);
+        } catch (...) {
+            delete cs;
+            throw;
+        }
+        *out = cs;
+    });
+}
+
+gx_status gx_simulate_trace(gx_ctx* ctx, const uint64_t* flat, const uint64_t* off, uint64_t S, uint64_t N,
+                            uint64_t K, const uint64_t* init, uint64_t n_init, gx_changesets** out) {
+    return guard([&] {
+        auto o = offsets_vec(off, S);
+        inspect_fill_from_host(ctx, flat + off[0], o, N);
+        // build_access_index's checks happen first (duplicates), via the device run
+        // below; init checks in simulate_changesets order (changeset.hpp:238-246)
+        {
+            std::unordered_set<uint64_t> in_trace;
+            std::unordered_set<uint64_t> want(init, init + n_init);
+            for (uint64_t x = 0; x < o[S]; ++x)
+                if (want.count(flat[off[0] + x])) in_trace.insert(flat[off[0] + x]);
+            std::unordered_set<uint64_t> seen;
+            for (uint64_t k = 0; k < n_init; ++k) {
+                if (init[k] >= N) fail(GX_OUT_OF_RANGE, "init id out of range");
+                if (!in_trace.count(init[k]))
+                    fail(GX_LOGIC_ERROR, "init id never appears in the trace (index/trace mismatch)");
+                if (!seen.insert(init[k]).second) fail(GX_LOGIC_ERROR, "duplicate id in init set");
+            }
+            if (n_init > K) fail(GX_INVALID_ARGUMENT, "init set exceeds capacity");
+        }
+        auto cs = new gx_changesets();
+        try {
+            inspect_run(ctx, o, N, K, init, (int64_t)n_init, cs);
+        } catch (...) {
+            delete cs;
+            throw;
+        }
+        *out = cs;
+    });
+}
+
+gx_status gx_precompute_samples(const gx_samples* s, uint64_t N, uint64_t K, gx_changesets** out) {
+    return guard([&] {
+        std::vector<uint64_t> o(s->S + 1, 0);
+        for (uint64_t i = 0; i < s->S; ++i) o[i + 1] = o[i] + s->h_n_ids[i];
+        inspect_fill_from_device(s->ctx, s->ids.p, s->cap_ids, o);
+        auto cs = new gx_changesets();
+        try {
+            inspect_run(s->ctx, o, N, K, nullptr, -1, cs);
+        } catch (...) {
+            delete cs;
+            throw;
+        }
+        *out = cs;
+    });
+}
+
+gx_status gx_access_index(gx_ctx* ctx, const uint64_t* flat, const uint64_t* off, uint64_t S, uint64_t N,
+                          uint64_t* iters, uint64_t* ptr) {
+    return guard([&] {
+        auto o = offsets_vec(off, S);
+        inspect_fill_from_host(ctx, flat + off[0], o, N);
+        access_index_run(ctx, o, N, iters, ptr);
+    });
+}
+
+void gx_changesets_destroy(gx_changesets* cs) { delete cs; }
+uint64_t gx_changesets_num_iters(const gx_changesets* cs) { return cs ? cs->S : 0; }
+uint64_t gx_changesets_init_size(const gx_changesets* cs) { return cs ? cs->n_init : 0; }
+
+gx_status gx_changesets_init(const gx_changesets* cs, uint64_t* out, uint64_t* n) {
+    return guard([&] {
+        if (n) *n = cs->n_init;
+        if (out) d2h_u32_as_u64(cs->init.p, cs->n_init, out);
+    });
+}
+
+gx_status gx_changesets_iter_info(const gx_changesets* cs, uint64_t i, uint64_t* n_in, uint64_t* n_out,
+                                  uint64_t* misses) {
+    return guard([&] {
+        if (i >= cs->S) fail(GX_OUT_OF_RANGE, "iteration index out of range");
+        if (n_in) *n_in = cs->h_in_off[i + 1] - cs->h_in_off[i];
+        if (n_out) *n_out = cs->h_out_off[i + 1] - cs->h_out_off[i];
+        if (misses) *misses = cs->h_misses[i];
+    });
+}
+
+gx_status gx_changesets_copy_iter(const gx_changesets* cs, uint64_t i, uint64_t* in_ids, uint64_t* out_ids,
+                                  uint64_t* in_pos) {
+    return guard([&] {
+        if (i >= cs->S) fail(GX_OUT_OF_RANGE, "iteration index out of range");
+        const uint64_t a = cs->h_in_off[i], ni = cs->h_in_off[i + 1] - a;
+        const uint64_t b = cs->h_out_off[i], no = cs->h_out_off[i + 1] - b;
+        if (in_ids) d2h_u32_as_u64(cs->in_ids.p + a, ni, in_ids);
+        if (in_pos) d2h_u32_as_u64(cs->in_pos.p + a, ni, in_pos);
+        if (out_ids) d2h_u32_as_u64(cs->out_ids.p + b, no, out_ids);
+    });
+}
+
+gx_status gx_changesets_misses(const gx_changesets* cs, uint64_t* misses) {
+    return guard([&] {
+        for (uint64_t i = 0; i < cs->S; ++i) misses[i] = cs->h_misses[i];
+    });
+}
+
+// init_{sb}.bin + update_{sb}_{i}.bin (changeset.hpp:409-454)
+gx_status gx_changesets_write_files(const gx_changesets* cs, const char* dir, uint64_t sb) {
+    return guard([&] {
+        std::vector<uint64_t> init(cs->n_init);
+        d2h_u32_as_u64(cs->init.p, cs->n_init, init.data());
+        {
+            Writer w(rt_path(dir, "init", sb, -1));
+            w.raw(kInitMagic, 8);
+            w.u64(init.size());
+            w.raw(init.data(), init.size() * 8);
+            w.close();
+        }
+        const uint64_t TI = cs->h_in_off[cs->S], TO = cs->h_out_off[cs->S];
+        std::vector<uint64_t> in(TI), pos(TI), outv(TO);
+        d2h_u32_as_u64(cs->in_ids.p, TI, in.data());
+        d2h_u32_as_u64(cs->in_pos.p, TI, pos.data());
+        d2h_u32_as_u64(cs->out_ids.p, TO, outv.data());
+        for (uint64_t i = 0; i < cs->S; ++i) {
+            const uint64_t a = cs->h_in_off[i], ni = cs->h_in_off[i + 1] - a;
+            const uint64_t b = cs->h_out_off[i], no = cs->h_out_off[i + 1] - b;
+            Writer w(rt_path(dir, "update", sb, (int64_t)i));
+            w.raw(kUpdMagic, 8);
+            w.u64(ni);
+            w.raw(in.data() + a, ni * 8);
+            w.u64(no);
+            w.raw(outv.data() + b, no * 8);
+            w.u64(ni);
+            w.raw(pos.data() + a, ni * 8);
+            w.close();
+        }
+    });
+}
+
+// ids_{sb}_{i}.bin + adj_{sb}_{i}.bin (sampler.hpp:123-182)
+gx_status gx_samples_write_files(const gx_samples* s, const char* dir, uint64_t sb) {
+    return guard([&] {
+        for (uint64_t b = 0; b < s->S; ++b) {
+            const uint64_t n = s->h_n_ids[b];
+            std::vector<uint64_t> ids(n);
+            d2h_u32_as_u64(s->ids.p + b * s->cap_ids, n, ids.data());
+            {
+                Writer w(rt_path(dir, "ids", sb, (int64_t)b));
+                w.raw(kIdsMagic, 8);
+                w.u64(n);
+                w.raw(ids.data(), n * 8);
+                w.close();
+            }
+            Writer w(rt_path(dir, "adj", sb, (int64_t)b));
+            w.raw(kAdjMagic, 8);
+            w.u32(s->L);
+            for (uint32_t l = 0; l < s->L; ++l) {
+                const uint64_t c = s->h_layer_count[b * s->L + l];
+                std::vector<uint32_t> pairs(2 * c);
+                if (c)
+                    GX_CUDA(cudaMemcpy(pairs.data(), s->edges.p + b * s->cap_e_batch + s->e_off[l], c * 8,
+                                       cudaMemcpyDeviceToHost));
+                w.u64(c);
+                w.raw(pairs.data(), c * 8);
+            }
+            w.close();
+        }
+    });
+}
+
+// ---- fused pipeline ---------------------------------------------------------
+
+gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts, uint32_t L, uint64_t K,
+                             gx_pipeline** out) {
+    return guard([&] {
+        if (!g || !f) fail(GX_INVALID_ARGUMENT, "null handle");
+        if (f->n != g->n) fail(GX_INVALID_ARGUMENT, "graph and feature files disagree on node count");
+        if (K >= 0x7FFFFFFFull) fail(GX_INVALID_ARGUMENT, "cache capacity exceeds 2^31 - 1 slots");
+        auto p = new gx_pipeline();
+        try {
+            p->g = g;
+            p->f = f;
+            p->ctx = g->ctx;
+            p->fanouts.assign(fanouts, fanouts + L);
+            p->K = K;
+            p->cache_rows.alloc(std::max<uint64_t>(K * f->row_bytes, 16));
+            p->table.alloc(std::max<uint64_t>(g->n, 1));
+            GX_CUDA(cudaMemset(p->table.p, 0xff, std::max<uint64_t>(g->n, 1) * 4));
+            for (auto& e : p->ev) GX_CUDA(cudaEventCreate(&e));
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+void gx_pipeline_destroy(gx_pipeline* p) {
+    if (!p) return;
+    for (auto& e : p->ev)
+        if (e) cudaEventDestroy(e);
+    delete p;
+}
+
+gx_status gx_pipeline_set_digest(gx_pipeline* p, int enable) {
+    return guard([&] { p->digest = enable != 0; });
+}
+
+gx_status gx_pipeline_digests(const gx_pipeline* p, uint64_t* d) {
+    return guard([&] {
+        for (size_t i = 0; i < p->h_digests.size(); ++i) d[i] = p->h_digests[i];
+    });
+}
+
+gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, const uint64_t* batch_off,
+                                 uint64_t S, uint64_t global_seed, uint64_t first_global_batch,
+                                 uint64_t* misses_per_iter, gx_pipeline_stats* stats) {
+    return guard([&] {
+        gx_ctx* ctx = p->ctx;
+        cudaStream_t st = ctx->stream;
+        const uint64_t N = p->g->n;
+        if (S == 0) fail(GX_INVALID_ARGUMENT, "empty superbatch");
+        for (uint64_t b = 0; b < S; ++b) {
+            const uint64_t n = batch_off[b + 1] - batch_off[b];
+            if (n == 0) fail(GX_RUNTIME_ERROR, "superbatch sample failed: sample_batch: seeds are empty");
+            for (uint64_t k = batch_off[b]; k < batch_off[b + 1]; ++k)
+                if (seeds_flat[k] >= N) fail(GX_RUNTIME_ERROR, "superbatch sample failed: seed node out of range");
+        }
+        std::vector<uint64_t> bs(S);
+        for (uint64_t i = 0; i < S; ++i) bs[i] = derive_seed(global_seed, first_global_batch + i);
+        const uint32_t L = (uint32_t)p->fanouts.size();
+        GX_CUDA(cudaEventRecord(p->ev[0], st));
+        // (1) sample
+        sample_run(p->g, seeds_flat, batch_off, S, p->fanouts.data(), L, bs.data(), &p->samples);
+        GX_CUDA(cudaEventRecord(p->ev[1], st));
+        samples_sync_host(&p->samples);
+        // (2) inspect
+        std::vector<uint64_t> o(S + 1, 0);
+        for (uint64_t i = 0; i < S; ++i) o[i + 1] = o[i] + p->samples.h_n_ids[i];
+        inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, o);
+        inspect_run(ctx, o, N, p->K, nullptr, -1, &p->cs);
+        GX_CUDA(cudaEventRecord(p->ev[2], st));
+        // (3) switch: cache init
+        uint64_t maxw = 0;
+        for (uint64_t i = 0; i < S; ++i) maxw = std::max(maxw, o[i + 1] - o[i]);
+        p->batch.reserve(std::max<uint64_t>(maxw * p->f->row_bytes, 16));
+        p->counters.reserve(8 * (S + 1));
+        GX_CUDA(cudaMemsetAsync(p->counters.p, 0, 8 * (S + 1) * 8, st));
+        if (p->digest) {
+            p->digests.reserve(S);
+            GX_CUDA(cudaMemsetAsync(p->digests.p, 0, S * 8, st));
+        }
+        launch_cache_init(ctx, p->cs.init.p, (uint32_t)p->cs.n_init, p->table.p, p->f, p->cache_rows.p,
+                          p->counters.p + 8 * S + 2);
+        GX_CUDA(cudaEventRecord(p->ev[3], st));
+        // (4) main loop: gather + apply (the ids of iteration i are batch i's ids)
+        for (uint64_t i = 0; i < S; ++i) {
+            const uint64_t ni = o[i + 1] - o[i];
+            launch_gather(ctx, ctx->is.trace.p + o[i], ni, p->table.p, p->cache_rows.p, p->f, p->batch.p,
+                          p->counters.p + 8 * i);
+            if (p->digest) launch_digest(ctx, p->batch.p, ni, p->f->row_bytes, p->digests.p + i);
+            const uint64_t a = p->cs.h_in_off[i], b = p->cs.h_out_off[i];
+            launch_apply_slots(ctx, p->cs.in_ids.p + a, p->cs.in_pos.p + a, p->cs.in_slot.p + a,
+                               (uint32_t)(p->cs.h_in_off[i + 1] - a), p->cs.out_ids.p + b,
+                               (uint32_t)(p->cs.h_out_off[i + 1] - b), p->table.p, p->batch.p, p->cache_rows.p,
+                               p->f->row_bytes);
+        }
+        GX_CUDA(cudaEventRecord(p->ev[4], st));
+        // leave the address table clean: every node ever inserted -> -1
+        launch_reset_table(ctx, p->cs.init.p, p->cs.n_init, p->table.p);
+        launch_reset_table(ctx, p->cs.in_ids.p, p->cs.h_in_off[S], p->table.p);
+        std::vector<unsigned long long> cnt(8 * (S + 1));
+        GX_CUDA(cudaMemcpyAsync(cnt.data(), p->counters.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
+        if (p->digest) {
+            p->h_digests.resize(S);
+            GX_CUDA(cudaMemcpyAsync(p->h_digests.data(), p->digests.p, S * 8, cudaMemcpyDeviceToHost, st));
+        }
+        GX_CUDA(cudaStreamSynchronize(st));
+        uint64_t tm = 0, pm = 0;
+        gx_iostats gio{};
+        for (uint64_t i = 0; i < S; ++i) {
+            if (misses_per_iter) misses_per_iter[i] = cnt[8 * i + 1];
+            tm += cnt[8 * i + 1];
+            pm += p->cs.h_misses[i];
+            gio.pages_read += cnt[8 * i + 2];
+            gio.rows_read += cnt[8 * i + 3];
+            gio.bytes_read += cnt[8 * i + 4];
+        }
+        if (stats) {
+            float ms[4];
+            for (int k = 0; k < 4; ++k) GX_CUDA(cudaEventElapsedTime(&ms[k], p->ev[k], p->ev[k + 1]));
+            stats->sampled_edges = gx_samples_total_edges(&p->samples);
+            stats->gathered_rows = o[S];
+            stats->total_misses = tm;
+            stats->predicted_misses = pm;
+            stats->init_size = p->cs.n_init;
+            stats->total_in = p->cs.h_in_off[S];
+            stats->total_out = p->cs.h_out_off[S];
+            stats->sample_io = p->samples.io;
+            stats->gather_io = gio;
+            stats->ms_sample = ms[0];
+            stats->ms_inspect = ms[1];
+            stats->ms_switch = ms[2];
+            stats->ms_gather = ms[3];
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,545 @@
+// executor.cu -- the feature cache of the executor (feature_cache.hpp) on HBM.
+//
+// Cache rows: K x row_bytes in HBM; address table: i32[N] (node -> slot, -1
+// miss); backing store: the whole feature table in HBM or pinned host memory
+// read zero-copy over PCIe (gx_backing). The hot kernels are bandwidth-bound
+// row copies:
+//  * k_gather  (FeatureCache::gather, feature_cache.hpp:58-76): one warp per
+//    row, 16-byte vector loads, several rows in flight per warp; hits read the
+//    cache slot, misses the backing store, misses charged one row,
+//    page_count_for_row pages and row_bytes bytes (graph_store.hpp:308-315).
+//  * k_apply_slots (apply_changeset, feature_cache.hpp:89-130) with the slots
+//    the inspector precomputed; k_apply (API path) recomputes them from this
+//    cache's own free list, exactly as the reference does.
+#include <algorithm>
+
+#include "gx_internal.cuh"
+
+struct gx_cache {
+    gx_features* f = nullptr;
+    gx_ctx* ctx = nullptr;
+    uint64_t K = 0;
+    gx::DevBuf<uint8_t> rows;        // K * row_bytes
+    gx::DevBuf<int32_t> table;       // N
+    gx::DevBuf<uint32_t> free_list;  // K (back = top-1 is the next slot handed out)
+    uint64_t free_top = 0;
+    gx::DevBuf<unsigned long long> counters;  // hits, misses, pages, rows, bytes
+    gx::DevBuf<uint32_t> scratch;             // ids / changeset staging
+    gx::DevBuf<unsigned int> err;
+};
+
+namespace gx {
+
+constexpr int GA_THREADS = 256;
+constexpr int GA_ROWS = 4;  // rows in flight per warp
+
+template <int VEC>
+struct VecT;
+template <>
+struct VecT<16> {
+    using T = uint4;
+};
+template <>
+struct VecT<4> {
+    using T = uint32_t;
+};
+
+__device__ __forceinline__ uint4 ld_nc(const uint4* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_nc(const uint32_t* p) { return __ldg(p); }
+__device__ __forceinline__ void st_na(uint4* p, const uint4& v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w));
+}
+__device__ __forceinline__ void st_na(uint32_t* p, const uint32_t& v) { *p = v; }
+
+// gather: out[k] = row(ids[k]) from cache slot table[ids[k]] or the store.
+// counters: [0] hits [1] misses [2] pages [3] rows [4] bytes (misses only)
+template <int VEC>
+__global__ void __launch_bounds__(GA_THREADS) k_gather(const uint32_t* __restrict__ ids, uint64_t n,
+                                                       const int32_t* __restrict__ table,
+                                                       const uint8_t* __restrict__ cache_rows,
+                                                       const uint8_t* __restrict__ store,
+                                                       uint64_t row_bytes, uint8_t* __restrict__ out,
+                                                       unsigned long long* counters) {
+    using V = typename VecT<VEC>::T;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t nvec = (uint32_t)(row_bytes / VEC);
+    unsigned long long hits = 0, misses = 0, pages = 0;
+    for (uint64_t r0 = warp * GA_ROWS; r0 < n; r0 += nwarps * GA_ROWS) {
+        const V* src[GA_ROWS];
+        V* dst[GA_ROWS];
+        bool valid[GA_ROWS];
+#pragma unroll
+        for (int q = 0; q < GA_ROWS; ++q) {
+            const uint64_t r = r0 + q;
+            valid[q] = r < n;
+            uint32_t v = 0;
+            int32_t s = -1;
+            if (valid[q]) {
+                v = ids[r];
+                s = table[v];
+            }
+            src[q] = reinterpret_cast<const V*>(s >= 0 ? cache_rows + (uint64_t)s * row_bytes
+                                                       : store + (uint64_t)v * row_bytes);
+            dst[q] = reinterpret_cast<V*>(out + r * row_bytes);
+            if (valid[q] && lane == 0) {
+                if (s >= 0) ++hits;
+                else {
+                    ++misses;
+                    pages += pages_touched((uint64_t)v * row_bytes, (uint64_t)(v + 1) * row_bytes);
+                }
+            }
+        }
+        for (uint32_t c = lane; c < nvec; c += 32) {
+            V tmp[GA_ROWS];
+#pragma unroll
+            for (int q = 0; q < GA_ROWS; ++q)
+                if (valid[q]) tmp[q] = ld_nc(src[q] + c);
+#pragma unroll
+            for (int q = 0; q < GA_ROWS; ++q)
+                if (valid[q]) st_na(dst[q] + c, tmp[q]);
+        }
+    }
+    if (lane == 0 && (hits | misses)) {
+        atomicAdd(&counters[0], hits);
+        atomicAdd(&counters[1], misses);
+        atomicAdd(&counters[2], pages);
+        atomicAdd(&counters[3], misses);
+        atomicAdd(&counters[4], misses * row_bytes);
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void warp_copy_row(const uint8_t* src, uint8_t* dst, uint64_t row_bytes) {
+    using V = typename VecT<VEC>::T;
+    const uint32_t nvec = (uint32_t)(row_bytes / VEC);
+    const V* s = reinterpret_cast<const V*>(src);
+    V* d = reinterpret_cast<V*>(dst);
+    for (uint32_t c = threadIdx.x & 31; c < nvec; c += 32) d[c] = s[c];
+}
+
+// Changeset application with precomputed slots (pipeline path).
+template <int VEC>
+__global__ void k_apply_slots(const uint32_t* __restrict__ in_ids, const uint32_t* __restrict__ in_pos,
+                              const uint32_t* __restrict__ in_slot, uint32_t n_in,
+                              const uint32_t* __restrict__ out_ids, uint32_t n_out, int32_t* table,
+                              const uint8_t* __restrict__ batch, uint8_t* cache_rows, uint64_t row_bytes) {
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t m = max(n_in, n_out);
+    for (uint64_t k = warp; k < m; k += nwarps) {
+        if (k < n_out && lane == 0) table[out_ids[k]] = -1;
+        if (k < n_in) {
+            const uint32_t s = in_slot[k];
+            warp_copy_row<VEC>(batch + (uint64_t)in_pos[k] * row_bytes, cache_rows + (uint64_t)s * row_bytes,
+                               row_bytes);
+            if (lane == 0) table[in_ids[k]] = (int32_t)s;
+        }
+    }
+}
+
+// API-path validation (feature_cache.hpp:96-112): any violation -> logic_error.
+__global__ void k_apply_validate(const uint32_t* ids, uint32_t n_ids, const uint32_t* in_ids,
+                                 const uint32_t* in_pos, uint32_t n_in, const uint32_t* out_ids,
+                                 uint32_t n_out, const int32_t* table, uint64_t N, unsigned int* err) {
+    const uint32_t G = gridDim.x * blockDim.x;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_in; k += G) {
+        const uint32_t v = in_ids[k], p = in_pos[k];
+        if (p >= n_ids || ids[p] != v) atomicOr(err, 1u);
+        else if (v >= N) atomicOr(err, 2u);
+        else if (table[v] >= 0) atomicOr(err, 1u);
+    }
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n_out; k += G) {
+        const uint32_t v = out_ids[k];
+        if (v >= N || table[v] < 0) atomicOr(err, 1u);
+    }
+}
+
+// API-path mutation: freed[k] = table[out[k]]; in[k] -> freed[k] or the free
+// list back; surplus freed slots are pushed back in order.
+template <int VEC>
+__global__ void k_apply(const uint32_t* __restrict__ in_ids, const uint32_t* __restrict__ in_pos,
+                        uint32_t n_in, const uint32_t* __restrict__ out_ids, uint32_t n_out, int32_t* table,
+                        uint32_t* free_list, uint64_t top, const uint8_t* __restrict__ batch,
+                        uint8_t* cache_rows, uint64_t row_bytes) {
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t m = max(n_in, n_out);
+    for (uint64_t k = warp; k < m; k += nwarps) {
+        int32_t freed = -1;
+        if (k < n_out) freed = table[out_ids[k]];
+        __syncwarp();
+        if (k < n_out && lane == 0) {
+            table[out_ids[k]] = -1;
+            if (k >= n_in) free_list[top + (k - n_in)] = (uint32_t)freed;
+        }
+        if (k < n_in) {
+            const uint32_t s = k < n_out ? (uint32_t)freed : free_list[top - 1 - (k - n_out)];
+            warp_copy_row<VEC>(batch + (uint64_t)in_pos[k] * row_bytes, cache_rows + (uint64_t)s * row_bytes,
+                               row_bytes);
+            if (lane == 0) table[in_ids[k]] = (int32_t)s;
+        }
+    }
+}
+
+// cache init: slots 0..n-1 <- rows of init ids (FeatureCache ctor, feature_cache.hpp:30-36)
+template <int VEC>
+__global__ void k_cache_init(const uint32_t* __restrict__ init, uint32_t n, int32_t* table,
+                             const uint8_t* __restrict__ store, uint8_t* cache_rows, uint64_t row_bytes,
+                             unsigned long long* pages) {
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    unsigned long long pg = 0;
+    for (uint64_t k = warp; k < n; k += nwarps) {
+        const uint32_t v = init[k];
+        warp_copy_row<VEC>(store + (uint64_t)v * row_bytes, cache_rows + k * row_bytes, row_bytes);
+        if (lane == 0) {
+            table[v] = (int32_t)k;
+            pg += pages_touched((uint64_t)v * row_bytes, (uint64_t)(v + 1) * row_bytes);
+        }
+    }
+    if (lane == 0 && pg) atomicAdd(pages, pg);
+}
+
+__global__ void k_iota_desc(uint32_t* p, uint64_t n, uint64_t K) {
+    // free list [K-1, K-2, ..., K-n]: back() pops ascending from K-n
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = (uint32_t)(K - 1 - i);
+}
+
+__global__ void k_reset_table(const uint32_t* nodes, uint64_t n, int32_t* table) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        table[nodes[i]] = -1;
+}
+
+__global__ void k_resident(const int32_t* table, uint64_t N, uint32_t* out, unsigned int* cnt) {
+    // compaction in id order via a two-level approach is not needed for a test
+    // hook: emit (unordered) and let the host sort.
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < N;
+         v += (uint64_t)gridDim.x * blockDim.x)
+        if (table[v] >= 0) out[atomicAdd(cnt, 1u)] = (uint32_t)v;
+}
+
+static bool vec16(uint64_t row_bytes) { return row_bytes % 16 == 0; }
+
+// digest = sum over u32 words x of (word[x] + 1) * mix64(x)  (mod 2^64)
+__global__ void k_digest(const uint32_t* __restrict__ w, uint64_t nwords, unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < nwords;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        acc += ((unsigned long long)w[x] + 1ull) * mix64(x);
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t row_bytes,
+                   unsigned long long* out) {
+    const uint64_t nw = rows * row_bytes / 4;
+    if (!nw) return;
+    k_digest<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(reinterpret_cast<const uint32_t*>(batch), nw, out);
+    GX_CHECK_LAUNCH();
+}
+
+// Launchers shared with the pipeline.
+void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table, const uint8_t* cache_rows,
+                   const gx_features* f, uint8_t* out, unsigned long long* counters) {
+    if (!n) return;
+    const uint64_t warps_needed = (n + GA_ROWS - 1) / GA_ROWS;
+    const uint64_t blocks = std::min<uint64_t>((warps_needed * 32 + GA_THREADS - 1) / GA_THREADS,
+                                               (uint64_t)ctx->num_sms * 8);
+    if (vec16(f->row_bytes))
+        k_gather<16><<<(unsigned)blocks, GA_THREADS, 0, ctx->stream>>>(ids, n, table, cache_rows, f->rows_dev_view,
+                                                                       f->row_bytes, out, counters);
+    else
+        k_gather<4><<<(unsigned)blocks, GA_THREADS, 0, ctx->stream>>>(ids, n, table, cache_rows, f->rows_dev_view,
+                                                                      f->row_bytes, out, counters);
+    GX_CHECK_LAUNCH();
+}
+
+void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos, const uint32_t* in_slot,
+                        uint32_t n_in, const uint32_t* out_ids, uint32_t n_out, int32_t* table,
+                        const uint8_t* batch, uint8_t* cache_rows, uint64_t row_bytes) {
+    const uint32_t m = std::max(n_in, n_out);
+    if (!m) return;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)m * 32 + 255) / 256, ctx->num_sms * 8);
+    if (vec16(row_bytes))
+        k_apply_slots<16><<<blocks, 256, 0, ctx->stream>>>(in_ids, in_pos, in_slot, n_in, out_ids, n_out, table,
+                                                           batch, cache_rows, row_bytes);
+    else
+        k_apply_slots<4><<<blocks, 256, 0, ctx->stream>>>(in_ids, in_pos, in_slot, n_in, out_ids, n_out, table,
+                                                          batch, cache_rows, row_bytes);
+    GX_CHECK_LAUNCH();
+}
+
+void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table, const gx_features* f,
+                       uint8_t* cache_rows, unsigned long long* pages) {
+    if (!n) return;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)n * 32 + 255) / 256, ctx->num_sms * 8);
+    if (vec16(f->row_bytes))
+        k_cache_init<16><<<blocks, 256, 0, ctx->stream>>>(init, n, table, f->rows_dev_view, cache_rows, f->row_bytes,
+                                                          pages);
+    else
+        k_cache_init<4><<<blocks, 256, 0, ctx->stream>>>(init, n, table, f->rows_dev_view, cache_rows, f->row_bytes,
+                                                         pages);
+    GX_CHECK_LAUNCH();
+}
+
+void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table) {
+    if (!n) return;
+    k_reset_table<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(nodes, n, table);
+    GX_CHECK_LAUNCH();
+}
+
+static void upload_u32(gx_ctx* ctx, gx::DevBuf<uint32_t>& buf, uint64_t off, const uint64_t* h, uint64_t n) {
+    if (!n) return;
+    std::vector<uint32_t> t(n);
+    for (uint64_t i = 0; i < n; ++i) t[i] = (uint32_t)h[i];
+    GX_CUDA(cudaMemcpyAsync(buf.p + off, t.data(), n * 4, cudaMemcpyHostToDevice, ctx->stream));
+    GX_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+}  // namespace gx
+
+using namespace gx;
+
+extern "C" {
+
+gx_status gx_batch_create(gx_ctx* ctx, gx_batch** out) {
+    return guard([&] {
+        auto b = new gx_batch();
+        b->ctx = ctx;
+        *out = b;
+    });
+}
+void gx_batch_destroy(gx_batch* b) { delete b; }
+uint64_t gx_batch_rows(const gx_batch* b) { return b ? b->rows : 0; }
+void* gx_batch_device_ptr(const gx_batch* b) { return b ? b->data.p : nullptr; }
+gx_status gx_batch_copy_to_host(const gx_batch* b, void* out) {
+    return guard([&] {
+        if (b->rows) GX_CUDA(cudaMemcpy(out, b->data.p, b->rows * b->row_bytes, cudaMemcpyDeviceToHost));
+    });
+}
+
+gx_status gx_cache_create(gx_features* f, const uint64_t* init, uint64_t n_init, uint64_t K, gx_iostats* io,
+                          gx_cache** out) {
+    return guard([&] {
+        if (n_init > K) fail(GX_INVALID_ARGUMENT, "init set larger than feature cache capacity");
+        // reference order (feature_cache.hpp:30-36): per id, range then duplicate
+        {
+            std::vector<uint8_t> seen;
+            std::vector<uint64_t> sorted;
+            for (uint64_t k = 0; k < n_init; ++k)
+                if (init[k] >= f->n) {
+                    // a duplicate strictly before the first out-of-range id wins
+                    std::vector<uint64_t> pre(init, init + k);
+                    std::sort(pre.begin(), pre.end());
+                    if (std::adjacent_find(pre.begin(), pre.end()) != pre.end())
+                        fail(GX_INVALID_ARGUMENT, "duplicate init id");
+                    fail(GX_OUT_OF_RANGE, "init id out of range");
+                }
+            sorted.assign(init, init + n_init);
+            std::sort(sorted.begin(), sorted.end());
+            if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+                fail(GX_INVALID_ARGUMENT, "duplicate init id");
+        }
+        if (K >= 0x7FFFFFFFull) fail(GX_INVALID_ARGUMENT, "cache capacity exceeds 2^31 - 1 slots");
+        gx_ctx* ctx = f->ctx;
+        auto c = new gx_cache();
+        try {
+            c->f = f;
+            c->ctx = ctx;
+            c->K = K;
+            c->rows.alloc(std::max<uint64_t>(K * f->row_bytes, 16));
+            c->table.alloc(std::max<uint64_t>(f->n, 1));
+            GX_CUDA(cudaMemsetAsync(c->table.p, 0xff, std::max<uint64_t>(f->n, 1) * 4, ctx->stream));
+            c->free_list.alloc(std::max<uint64_t>(K, 1));
+            c->free_top = K - n_init;
+            if (c->free_top)
+                k_iota_desc<<<ctx->num_sms, 256, 0, ctx->stream>>>(c->free_list.p, c->free_top, K);
+            GX_CHECK_LAUNCH();
+            c->counters.alloc(8);
+            c->err.alloc(1);
+            c->scratch.alloc(std::max<uint64_t>(n_init, 1));
+            upload_u32(ctx, c->scratch, 0, init, n_init);
+            GX_CUDA(cudaMemsetAsync(c->counters.p, 0, 8 * 8, ctx->stream));
+            launch_cache_init(ctx, c->scratch.p, (uint32_t)n_init, c->table.p, f, c->rows.p, c->counters.p + 2);
+            unsigned long long pg = 0;
+            GX_CUDA(cudaMemcpyAsync(&pg, c->counters.p + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
+            GX_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (io) {
+                io->rows_read += n_init;
+                io->pages_read += pg;
+                io->bytes_read += n_init * f->row_bytes;
+            }
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+    });
+}
+
+void gx_cache_destroy(gx_cache* c) { delete c; }
+uint64_t gx_cache_num_entries(const gx_cache* c) { return c ? c->K : 0; }
+
+gx_status gx_cache_gather(gx_cache* c, const uint64_t* ids, uint64_t n, gx_batch* out, uint64_t* hits,
+                          uint64_t* misses, gx_iostats* io) {
+    return guard([&] {
+        gx_ctx* ctx = c->ctx;
+        for (uint64_t k = 0; k < n; ++k)
+            if (ids[k] >= c->f->n) fail(GX_OUT_OF_RANGE, "gather id out of range");
+        c->scratch.reserve(std::max<uint64_t>(n, 1));
+        upload_u32(ctx, c->scratch, 0, ids, n);
+        out->ctx = ctx;
+        out->rows = n;
+        out->row_bytes = c->f->row_bytes;
+        out->data.reserve(std::max<uint64_t>(n * c->f->row_bytes, 16));
+        GX_CUDA(cudaMemsetAsync(c->counters.p, 0, 8 * 8, ctx->stream));
+        launch_gather(ctx, c->scratch.p, n, c->table.p, c->rows.p, c->f, out->data.p, c->counters.p);
+        unsigned long long cnt[5];
+        GX_CUDA(cudaMemcpyAsync(cnt, c->counters.p, 5 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+        GX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (hits) *hits = cnt[0];
+        if (misses) *misses = cnt[1];
+        if (io) {
+            io->pages_read += cnt[2];
+            io->rows_read += cnt[3];
+            io->bytes_read += cnt[4];
+        }
+    });
+}
+
+gx_status gx_cache_apply(gx_cache* c, const gx_batch* batch, const uint64_t* ids, uint64_t n_ids,
+                         const uint64_t* in_ids, const uint64_t* in_pos, uint64_t n_in, const uint64_t* out_ids,
+                         uint64_t n_out) {
+    return guard([&] {
+        gx_ctx* ctx = c->ctx;
+        if (!batch || batch->rows != n_ids || (n_ids && batch->row_bytes != c->f->row_bytes))
+            fail(GX_INVALID_ARGUMENT, "batch buffer does not match ids");
+        // stage ids | in_ids | in_pos | out_ids as u32 (positions beyond u32 are invalid anyway)
+        for (uint64_t k = 0; k < n_in; ++k)
+            if (in_pos[k] >= n_ids) fail(GX_LOGIC_ERROR, "changeset position does not match ids");
+        for (uint64_t k = 0; k < n_out; ++k)
+            if (out_ids[k] >= c->f->n) fail(GX_LOGIC_ERROR, "evicted node is not cached");
+        for (uint64_t k = 0; k < n_in; ++k)
+            if (in_ids[k] >= c->f->n) fail(GX_LOGIC_ERROR, "changeset position does not match ids");
+        const uint64_t tot = n_ids + 2 * n_in + n_out;
+        c->scratch.reserve(std::max<uint64_t>(tot, 1));
+        upload_u32(ctx, c->scratch, 0, ids, n_ids);
+        upload_u32(ctx, c->scratch, n_ids, in_ids, n_in);
+        upload_u32(ctx, c->scratch, n_ids + n_in, in_pos, n_in);
+        upload_u32(ctx, c->scratch, n_ids + 2 * n_in, out_ids, n_out);
+        const uint32_t* d_ids = c->scratch.p;
+        const uint32_t* d_in = c->scratch.p + n_ids;
+        const uint32_t* d_pos = c->scratch.p + n_ids + n_in;
+        const uint32_t* d_out = c->scratch.p + n_ids + 2 * n_in;
+        GX_CUDA(cudaMemsetAsync(c->err.p, 0, 4, ctx->stream));
+        if (n_in || n_out) {
+            k_apply_validate<<<ctx->num_sms, 256, 0, ctx->stream>>>(d_ids, (uint32_t)n_ids, d_in, d_pos,
+                                                                    (uint32_t)n_in, d_out, (uint32_t)n_out,
+                                                                    c->table.p, c->f->n, c->err.p);
+            GX_CHECK_LAUNCH();
+        }
+        unsigned int e = 0;
+        GX_CUDA(cudaMemcpyAsync(&e, c->err.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        GX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (e) fail(GX_LOGIC_ERROR, "invalid changeset for the current cache state");
+        if (n_in > n_out + c->free_top) fail(GX_LOGIC_ERROR, "changeset overflows cache capacity");
+        const uint32_t m = (uint32_t)std::max(n_in, n_out);
+        if (m) {
+            const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)m * 32 + 255) / 256, ctx->num_sms * 8);
+            if (vec16(c->f->row_bytes))
+                k_apply<16><<<blocks, 256, 0, ctx->stream>>>(d_in, d_pos, (uint32_t)n_in, d_out, (uint32_t)n_out,
+                                                             c->table.p, c->free_list.p, c->free_top,
+                                                             batch->data.p, c->rows.p, c->f->row_bytes);
+            else
+                k_apply<4><<<blocks, 256, 0, ctx->stream>>>(d_in, d_pos, (uint32_t)n_in, d_out, (uint32_t)n_out,
+                                                            c->table.p, c->free_list.p, c->free_top,
+                                                            batch->data.p, c->rows.p, c->f->row_bytes);
+            GX_CHECK_LAUNCH();
+        }
+        if (n_in > n_out) c->free_top -= (n_in - n_out);
+        else c->free_top += (n_out - n_in);
+        GX_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+gx_status gx_cache_contains(const gx_cache* c, uint64_t v, int* out) {
+    return guard([&] {
+        if (v >= c->f->n) fail(GX_OUT_OF_RANGE, "node id out of range");
+        int32_t s;
+        GX_CUDA(cudaMemcpy(&s, c->table.p + v, 4, cudaMemcpyDeviceToHost));
+        *out = s >= 0;
+    });
+}
+
+gx_status gx_cache_cached_row(const gx_cache* c, uint64_t v, void* out) {
+    return guard([&] {
+        if (v >= c->f->n) fail(GX_OUT_OF_RANGE, "node id out of range");
+        int32_t s;
+        GX_CUDA(cudaMemcpy(&s, c->table.p + v, 4, cudaMemcpyDeviceToHost));
+        if (s < 0) fail(GX_LOGIC_ERROR, "cached_row on a miss");
+        GX_CUDA(cudaMemcpy(out, c->rows.p + (uint64_t)s * c->f->row_bytes, c->f->row_bytes,
+                           cudaMemcpyDeviceToHost));
+    });
+}
+
+gx_status gx_cache_resident_set(const gx_cache* c, uint64_t* out, uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        gx_ctx* ctx = c->ctx;
+        DevBuf<uint32_t> tmp(std::max<uint64_t>(c->K, 1));
+        DevBuf<unsigned int> cnt(1);
+        GX_CUDA(cudaMemsetAsync(cnt.p, 0, 4, ctx->stream));
+        k_resident<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(c->table.p, c->f->n, tmp.p, cnt.p);
+        GX_CHECK_LAUNCH();
+        unsigned int hc = 0;
+        GX_CUDA(cudaMemcpyAsync(&hc, cnt.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        GX_CUDA(cudaStreamSynchronize(ctx->stream));
+        std::vector<uint32_t> h(hc);
+        if (hc) GX_CUDA(cudaMemcpy(h.data(), tmp.p, hc * 4, cudaMemcpyDeviceToHost));
+        std::sort(h.begin(), h.end());
+        *n = hc;
+        for (uint64_t i = 0; i < hc && i < cap; ++i) out[i] = h[i];
+    });
+}
+
+gx_status gx_features_read_rows(gx_features* f, const uint64_t* ids, uint64_t n, void* out, gx_iostats* io) {
+    return guard([&] {
+        gx_ctx* ctx = f->ctx;
+        for (uint64_t k = 0; k < n; ++k)
+            if (ids[k] >= f->n) fail(GX_OUT_OF_RANGE, "feature row id out of range");
+        DevBuf<uint32_t> d(std::max<uint64_t>(n, 1));
+        upload_u32(ctx, d, 0, ids, n);
+        DevBuf<uint8_t> o(std::max<uint64_t>(n * f->row_bytes, 16));
+        DevBuf<int32_t> none(1);  // table lookup is skipped via an all-miss table below
+        DevBuf<int32_t> table(std::max<uint64_t>(f->n, 1));
+        GX_CUDA(cudaMemsetAsync(table.p, 0xff, std::max<uint64_t>(f->n, 1) * 4, ctx->stream));
+        DevBuf<unsigned long long> cnt(8);
+        GX_CUDA(cudaMemsetAsync(cnt.p, 0, 64, ctx->stream));
+        launch_gather(ctx, d.p, n, table.p, nullptr, f, o.p, cnt.p);
+        unsigned long long h[5];
+        GX_CUDA(cudaMemcpyAsync(h, cnt.p, 40, cudaMemcpyDeviceToHost, ctx->stream));
+        GX_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (n) GX_CUDA(cudaMemcpy(out, o.p, n * f->row_bytes, cudaMemcpyDeviceToHost));
+        if (io) {
+            io->pages_read += h[2];
+            io->rows_read += h[3];
+            io->bytes_read += h[4];
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,241 @@
+// gx_common.cuh -- shared device/host plumbing for the B200 hot path.
+//
+// Error model: internal code throws gx::Error(status, msg); every extern "C"
+// entry point runs inside gx::guard(), which maps it to gx_status and stores
+// the message for gx_last_error() (include/gx_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gx_b200.h"
+
+namespace gx {
+
+struct Error : std::exception {
+    gx_status status;
+    std::string msg;
+    Error(gx_status s, std::string m) : status(s), msg(std::move(m)) {}
+    const char* what() const noexcept override { return msg.c_str(); }
+};
+
+[[noreturn]] inline void fail(gx_status s, const std::string& m) { throw Error(s, m); }
+
+void set_last_error(const std::string& m);
+
+template <class F>
+gx_status guard(F&& f) {
+    try {
+        f();
+        return GX_OK;
+    } catch (const Error& e) {
+        set_last_error(e.msg);
+        return e.status;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return GX_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return GX_RUNTIME_ERROR;
+    }
+}
+
+#define GX_CUDA(call)                                                                       \
+    do {                                                                                    \
+        cudaError_t _e = (call);                                                            \
+        if (_e != cudaSuccess)                                                              \
+            ::gx::fail(GX_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define GX_CHECK_LAUNCH() GX_CUDA(cudaGetLastError())
+
+constexpr uint32_t kNever = 0xFFFFFFFFu;     // "no further access" / empty key
+constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+constexpr uint64_t kPage = 4096;
+
+// ---------------------------------------------------------------------------
+// Device RNG: SplitMix64 as a counter-based generator (common.hpp:68-101).
+// Draw t (0-based) of SplitMix64(seed) == mix64(seed + t*gamma); bounded(n)
+// == umulhi(draw, n). Verified bit-exact against the sequential stream.
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += kGamma;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t derive_seed(uint64_t base, uint64_t index) {
+    return mix64(base ^ mix64(index));
+}
+__device__ __forceinline__ uint64_t draw_bounded(uint64_t seed, uint64_t t, uint64_t n) {
+    return __umul64hi(mix64(seed + t * kGamma), n);
+}
+__host__ __device__ __forceinline__ uint64_t pages_touched(uint64_t lo, uint64_t hi) {
+    return hi <= lo ? 0 : (hi - 1) / kPage - lo / kPage + 1;
+}
+
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+
+// ---------------------------------------------------------------------------
+// Grid-wide barrier for persistent kernels launched cooperatively (all CTAs
+// co-resident). Sense via a monotonically increasing generation counter.
+// ---------------------------------------------------------------------------
+struct GridBarrier {
+    unsigned int count;
+    unsigned int gen;
+};
+
+__device__ __forceinline__ void grid_sync(GridBarrier* b) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = &b->gen;
+        unsigned int g = *vgen;
+        __threadfence();
+        unsigned int arrived = atomicAdd(&b->count, 1u);
+        if (arrived == gridDim.x - 1) {
+            b->count = 0;
+            __threadfence();
+            atomicAdd(&b->gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Warp / block scans
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+    }
+    return v;
+}
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Exclusive block scan; `total` gets the block sum. smem needs 33 T.
+template <class T>
+__device__ __forceinline__ T block_excl_scan(T v, T* smem, T& total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    T inc = warp_incl_scan(v);
+    if (lane == 31) smem[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        T s = lane < nw ? smem[lane] : T(0);
+        T si = warp_incl_scan(s);
+        if (lane < nw) smem[lane] = si - s;
+        if (lane == nw - 1) smem[32] = si;
+    }
+    __syncthreads();
+    T r = inc - v + smem[wid];
+    total = smem[32];
+    __syncthreads();
+    return r;
+}
+
+template <class T>
+__device__ __forceinline__ T block_sum(T v, T* smem) {
+    T tot;
+    block_excl_scan(v, smem, tot);
+    return tot;
+}
+
+// ---------------------------------------------------------------------------
+// RAII device / pinned buffers
+// ---------------------------------------------------------------------------
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    ~DevBuf() { release(); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            n = o.n;
+            o.p = nullptr;
+            o.n = 0;
+        }
+        return *this;
+    }
+    void alloc(size_t count) {
+        release();
+        if (count) {
+            cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+            if (e != cudaSuccess) {
+                p = nullptr;
+                fail(GX_CUDA_ERROR, "cudaMalloc of " + std::to_string(count * sizeof(T)) +
+                                        " bytes failed: " + cudaGetErrorString(e));
+            }
+        }
+        n = count;
+    }
+    // grow-only
+    void reserve(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+template <class T>
+struct PinBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    PinBuf() = default;
+    ~PinBuf() { release(); }
+    PinBuf(const PinBuf&) = delete;
+    PinBuf& operator=(const PinBuf&) = delete;
+    void alloc(size_t count, unsigned flags = cudaHostAllocDefault) {
+        release();
+        if (count) GX_CUDA(cudaHostAlloc(&p, count * sizeof(T), flags));
+        n = count;
+    }
+    void reserve(size_t count) {
+        if (count > n) alloc(count);
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+inline unsigned ceil_div(uint64_t a, uint64_t b) { return (unsigned)((a + b - 1) / b); }
+
+}  // namespace gx

@@ -1,0 +1,137 @@
+// gx_internal.cuh -- definitions behind the opaque C-ABI handles.
+#pragma once
+
+#include "gx_common.cuh"
+
+namespace gx {
+// Sampler scratch (sampler.cu); grow-only, reused across calls.
+struct SampleScratch {
+    DevBuf<uint32_t> F, T, seeds32;
+    DevBuf<uint64_t> dbase, bseed, seed_off;
+    DevBuf<uint32_t> pscan, pdeg, idslot;
+    DevBuf<uint64_t> plo;
+    DevBuf<uint32_t> tsum, tsum2;
+    DevBuf<uint32_t> dslot, drank;
+    DevBuf<unsigned long long> tab[2];
+    uint64_t tab_slots = 0;  // per table, = S * tab_cap
+    DevBuf<unsigned long long> io;
+};
+// Inspector scratch (inspector.cu).
+struct InspectScratch {
+    DevBuf<uint32_t> last;       // N, node-indexed "next access" cursor (kNever when clean)
+    DevBuf<int32_t> node_slot;   // N, -1 when clean
+    uint64_t N = 0;
+    DevBuf<uint32_t> trace, next_use;
+    DevBuf<uint64_t> trace_off;
+    DevBuf<uint32_t> tile_cnt, slot_node, slot_key, hist_new, rh, pkey, out_node, out_slot, c_id,
+        c_ref, in_node, in_pos, chunk_cnt, bm_words, bm_cnt, init_ext, toff, st;
+    DevBuf<int32_t> hist_inc;
+    DevBuf<uint8_t> pmiss;
+};
+}  // namespace gx
+
+struct gx_ctx {
+    int device = 0;
+    int num_sms = 0;
+    cudaStream_t stream = nullptr;
+    gx::DevBuf<gx::GridBarrier> barrier;  // one barrier per context (stream-serialised users)
+    gx::SampleScratch ss;
+    gx::InspectScratch is;
+};
+
+struct gx_graph {
+    gx_ctx* ctx = nullptr;
+    uint64_t n = 0, e = 0;
+    gx::DevBuf<uint64_t> indptr;   // N+1
+    gx::DevBuf<uint32_t> indices;  // E (u32 device ids)
+};
+
+// Sampler output for S batches (SampleOutput x S, sampler.hpp:36-40).
+// Per-batch regions have fixed capacities so every batch can be written in
+// parallel without a device allocator.
+struct gx_samples {
+    gx_ctx* ctx = nullptr;
+    uint64_t S = 0;
+    uint32_t L = 0;
+    std::vector<uint32_t> fanouts;
+    uint64_t cap_ids = 0;                 // ids per batch
+    std::vector<uint64_t> cap_e;          // per layer edge capacity per batch
+    std::vector<uint64_t> e_off;          // per layer offset inside a batch's edge region
+    uint64_t cap_e_batch = 0;             // sum of cap_e
+    gx::DevBuf<uint32_t> ids;             // S * cap_ids
+    gx::DevBuf<uint32_t> n_ids;           // S
+    gx::DevBuf<uint2> edges;              // S * cap_e_batch  (src_local, dst_local)
+    gx::DevBuf<uint32_t> layer_count;     // S * L
+    std::vector<uint32_t> h_n_ids;        // host mirrors, valid after the call
+    std::vector<uint32_t> h_layer_count;
+    std::vector<uint64_t> h_n_seeds;
+    gx_iostats io{};
+};
+
+struct gx_changesets {
+    gx_ctx* ctx = nullptr;
+    uint64_t S = 0, N = 0, K = 0;
+    uint64_t n_init = 0;
+    gx::DevBuf<uint32_t> init;      // n_init (slot order)
+    gx::DevBuf<uint32_t> in_ids;    // total in
+    gx::DevBuf<uint32_t> in_pos;
+    gx::DevBuf<uint32_t> in_slot;   // FeatureCache slot each insertion lands in
+    gx::DevBuf<uint32_t> out_ids;   // total out (sorted per iteration)
+    std::vector<uint64_t> h_in_off, h_out_off, h_misses;  // S+1, S+1, S
+};
+
+struct gx_features {
+    gx_ctx* ctx = nullptr;
+    uint64_t n = 0;
+    uint32_t dim = 0;
+    uint32_t scalar_width = 4;
+    uint64_t row_bytes = 0;
+    int backing = GX_BACKING_DEVICE;
+    gx::DevBuf<uint8_t> dev;       // device backing store
+    gx::PinBuf<uint8_t> host;      // pinned host backing store (mapped)
+    const uint8_t* rows_dev_view = nullptr;  // pointer usable by kernels
+};
+
+struct gx_batch {
+    gx_ctx* ctx = nullptr;
+    uint64_t rows = 0;
+    uint64_t row_bytes = 0;
+    gx::DevBuf<uint8_t> data;
+};
+
+namespace gx {
+
+// Device scratch for one superbatch of sampling; reused across calls.
+struct SampleScratch;
+
+// Internal entry points shared between translation units.
+void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
+                const uint32_t* fanouts, uint32_t L, const uint64_t* batch_seeds,
+                gx_samples* out);
+void samples_sync_host(gx_samples* s);
+
+// Inspector (inspector.cu). The flat u32 trace lives in ctx->is.trace.
+void inspect_fill_from_device(gx_ctx* ctx, const uint32_t* d_ids, uint64_t stride,
+                              const std::vector<uint64_t>& off);
+void inspect_fill_from_host(gx_ctx* ctx, const uint64_t* flat, const std::vector<uint64_t>& off,
+                            uint64_t N);
+void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
+                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out);
+void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t* h_iters,
+                      uint64_t* h_ptr);
+
+// Executor launchers (executor.cu).
+void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table,
+                   const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                   unsigned long long* counters);
+void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos,
+                        const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
+                        uint32_t n_out, int32_t* table, const uint8_t* batch, uint8_t* cache_rows,
+                        uint64_t row_bytes);
+void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table,
+                       const gx_features* f, uint8_t* cache_rows, unsigned long long* pages);
+void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table);
+void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t row_bytes,
+                   unsigned long long* out);
+
+}  // namespace gx

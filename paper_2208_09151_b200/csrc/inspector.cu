@@ -1,0 +1,913 @@
+// inspector.cu -- Belady changesets for a superbatch (changeset.hpp) in ONE
+// persistent, cooperatively launched kernel.
+//
+// Reference: build_access_index (changeset.hpp:61-129), compute_init_set
+// (:137-153), simulate_changesets (:228-295), finish_selection (:198-220).
+// The recurrence
+//     C_{i+1} = the K members of C_i u ids_i with the smallest
+//               (next_access, incumbent-first, node id)
+// is reproduced exactly without sorting candidates:
+//  * next-use per access comes from one backward pass over the trace
+//    (atomicExch on a node-indexed cursor), which is the same quantity as
+//    iters[cursor[v]] & kIterMask in the reference (:268-281); first
+//    occurrences fall out of the same pass and give the init set (:137-153).
+//  * keys live in {i+1..S-1, NEVER}; an incrementally maintained histogram of
+//    incumbent keys plus this iteration's new-candidate histogram yields the
+//    threshold bucket b* and the remainder r with one S-sized scan per
+//    iteration; everything below b* is kept, above b* dropped; inside b*
+//    incumbents precede new candidates and both are ordered by id, so the
+//    cut is an exact radix-select on node ids (3 digit passes).
+//  * out_ids are emitted sorted by id (smem bitonic sort, or an N-bit bitmap
+//    compaction for large sets), in_ids in position order (:211-216).
+//  * the slot each insertion lands in follows FeatureCache exactly
+//    (feature_cache.hpp:114-129): in[k] reuses the slot of out[k], the rest
+//    pop the free list, which (since |out| <= |in|) is always n_res, n_res+1..
+//    so the executor can apply changesets without its own free list.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <unordered_set>
+
+#include "gx_internal.cuh"
+
+namespace gx {
+
+constexpr int IN_THREADS = 1024;
+constexpr uint32_t IN_TILE = IN_THREADS * 4;
+constexpr uint32_t SORT_SMALL = 4096;
+constexpr uint32_t kMaxIters = 4096;
+
+struct IState {
+    uint32_t n_res;
+    uint32_t miss;
+    uint32_t n_out;
+    uint32_t n_c;
+    uint32_t in_total;
+    uint32_t out_total;
+    uint32_t n_first;
+    uint32_t err;
+};
+
+struct IArgs {
+    const uint32_t* __restrict__ trace;
+    const uint32_t* toff;  // S+1
+    uint32_t S, A, K, maxw;
+    uint64_t N;
+    uint32_t* last;
+    int32_t* node_slot;
+    uint32_t* next_use;
+    uint32_t* tile_cnt;
+    uint32_t* slot_node;
+    uint32_t* slot_key;
+    int32_t* hist_inc;   // S+1
+    uint32_t* hist_new;  // S+1
+    uint32_t* rh;        // 3 * 2048
+    uint32_t* pkey;      // maxw
+    uint8_t* pmiss;      // maxw
+    uint32_t* out_node;  // maxw
+    uint32_t* out_slot;  // maxw
+    uint32_t* c_id;      // max(K, maxw)
+    uint32_t* c_ref;
+    uint32_t* in_node;   // maxw
+    uint32_t* in_pos;    // maxw
+    uint32_t* chunk_cnt; // gridDim
+    uint32_t* bm_words;  // nwords
+    uint32_t nwords;
+    uint32_t* bm_cnt;    // gridDim
+    const uint32_t* init_ext;
+    uint32_t n_init_ext;
+    int explicit_init;
+    uint32_t* o_init;
+    uint32_t* o_in_ids;
+    uint32_t* o_in_pos;
+    uint32_t* o_in_slot;
+    uint32_t* o_out_ids;
+    uint32_t* o_misses;   // S
+    uint32_t* o_in_off;   // S+1
+    uint32_t* o_out_off;  // S+1
+    IState* st;
+    GridBarrier* bar;
+};
+
+__device__ __forceinline__ uint32_t bucket_of(uint32_t key, uint32_t S) { return key == kNever ? S : key; }
+
+// warp-aggregated append; returns the slot for pred lanes, undefined otherwise
+__device__ __forceinline__ uint32_t agg_append(uint32_t* ctr, bool pred) {
+    const unsigned active = __activemask();
+    const unsigned m = __ballot_sync(active, pred);
+    const int lane = threadIdx.x & 31;
+    uint32_t base = 0;
+    if (m) {
+        const int leader = __ffs(m) - 1;
+        if (lane == leader) base = atomicAdd(ctr, (uint32_t)__popc(m));
+        base = __shfl_sync(active, base, leader);
+    }
+    return base + __popc(m & ((1u << lane) - 1));
+}
+
+struct ISmem {
+    uint32_t scan[34];
+    uint32_t bc[16];
+    unsigned long long sortbuf[SORT_SMALL];
+    uint32_t toff[kMaxIters + 1];
+    int32_t hinc[kMaxIters + 1];  // per-CTA histogram deltas, flushed with one atomic per bin
+    int32_t hnew[kMaxIters + 1];
+};
+
+__device__ __forceinline__ void hist_flush(int32_t* loc, int32_t* glob, uint32_t n) {
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < n; b += blockDim.x) {
+        const int32_t v = loc[b];
+        if (v) {
+            atomicAdd(&glob[b], v);
+            loc[b] = 0;
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t iter_of(const ISmem& sm, uint32_t S, uint32_t a) {
+    uint32_t lo = 0, hi = S;
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (sm.toff[mid] <= a) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Find the digit bin holding the r-th (1-based) smallest element of a
+// histogram; returns bin and writes the rank left inside that bin.
+__device__ uint32_t hist_select(const uint32_t* h, uint32_t nbins, uint32_t r, uint32_t* r_left,
+                                ISmem& sm) {
+    const uint32_t per = (nbins + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t s = 0;
+    for (uint32_t j = 0; j < per; ++j)
+        if (b0 + j < nbins) s += h[b0 + j];
+    uint32_t tot;
+    uint32_t ex = block_excl_scan(s, sm.scan, tot);
+    if (threadIdx.x == 0) sm.bc[0] = 0xFFFFFFFFu;
+    __syncthreads();
+    if (ex < r && ex + s >= r) {
+        uint32_t c = ex;
+        for (uint32_t j = 0; j < per; ++j) {
+            uint32_t v = b0 + j < nbins ? h[b0 + j] : 0;
+            if (c + v >= r) {
+                sm.bc[0] = b0 + j;
+                sm.bc[1] = r - c;
+                break;
+            }
+            c += v;
+        }
+    }
+    __syncthreads();
+    uint32_t bin = sm.bc[0];
+    *r_left = sm.bc[1];
+    __syncthreads();
+    return bin;
+}
+
+__global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
+    extern __shared__ unsigned char smem_raw[];
+    ISmem& sm = *reinterpret_cast<ISmem*>(smem_raw);
+    const uint32_t S = a.S, K = a.K;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t G = gridDim.x * blockDim.x;
+    const uint32_t gtid = blockIdx.x * blockDim.x + tid;
+    for (uint32_t i = tid; i <= S; i += blockDim.x) {
+        sm.toff[i] = a.toff[i];
+        sm.hinc[i] = 0;
+        sm.hnew[i] = 0;
+    }
+    __syncthreads();
+
+    // ---- next-use: backward pass, one iteration per grid step -------------
+    for (int i = (int)S - 1; i >= 0; --i) {
+        const uint32_t lo = sm.toff[i], hi = sm.toff[i + 1];
+        for (uint32_t x = lo + gtid; x < hi; x += G) {
+            const uint32_t v = a.trace[x];
+            if (v >= a.N) {
+                atomicOr(&a.st->err, 1u);
+                a.next_use[x] = kNever;
+                continue;
+            }
+            const uint32_t old = atomicExch(&a.last[v], (uint32_t)i);
+            if (old == (uint32_t)i) atomicOr(&a.st->err, 2u);
+            a.next_use[x] = old;
+        }
+        grid_sync(a.bar);
+    }
+    if (a.st->err) return;  // host reports the exact reference error
+
+    // ---- init set: first K first-occurrences in trace order ---------------
+    const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
+    if (!a.explicit_init) {
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            uint32_t c = 0;
+            const uint32_t x0 = t * IN_TILE + tid * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t x = x0 + j;
+                if (x < a.A) c += a.last[a.trace[x]] == iter_of(sm, S, x);
+            }
+            uint32_t tot = block_sum(c, sm.scan);
+            if (tid == 0) a.tile_cnt[t] = tot;
+        }
+        grid_sync(a.bar);
+        if (blockIdx.x == 0) {  // exclusive scan of tile counts
+            uint32_t carry = 0;
+            for (uint32_t base = 0; base < ntiles; base += blockDim.x) {
+                const uint32_t t = base + tid;
+                const uint32_t v = t < ntiles ? a.tile_cnt[t] : 0;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan(v, sm.scan, tot);
+                if (t < ntiles) a.tile_cnt[t] = carry + ex;
+                carry += tot;
+            }
+            if (tid == 0) {
+                a.st->n_first = carry;
+                a.st->n_res = min(carry, K);
+            }
+        }
+        grid_sync(a.bar);
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            uint32_t fl[4], it[4], vv[4], c = 0;
+            const uint32_t x0 = t * IN_TILE + tid * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t x = x0 + j;
+                fl[j] = 0;
+                if (x < a.A) {
+                    vv[j] = a.trace[x];
+                    it[j] = iter_of(sm, S, x);
+                    fl[j] = a.last[vv[j]] == it[j];
+                }
+                c += fl[j];
+            }
+            uint32_t tot;
+            uint32_t r = a.tile_cnt[t] + block_excl_scan(c, sm.scan, tot);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (fl[j]) {
+                    if (r < K) {
+                        a.slot_node[r] = vv[j];
+                        a.slot_key[r] = it[j];
+                        a.node_slot[vv[j]] = (int32_t)r;
+                        a.o_init[r] = vv[j];
+                        atomicAdd(&sm.hinc[bucket_of(it[j], S)], 1);
+                    }
+                    ++r;
+                }
+            }
+        }
+    } else {
+        for (uint32_t k = gtid; k < a.n_init_ext; k += G) {
+            const uint32_t v = a.init_ext[k];
+            const uint32_t key = a.last[v];  // first access iteration
+            a.slot_node[k] = v;
+            a.slot_key[k] = key;
+            a.node_slot[v] = (int32_t)k;
+            a.o_init[k] = v;
+            atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
+        }
+        if (gtid == 0) a.st->n_res = a.n_init_ext;
+    }
+    hist_flush(sm.hinc, a.hist_inc, S + 1);
+    grid_sync(a.bar);
+    for (uint32_t x = gtid; x < a.A; x += G) a.last[a.trace[x]] = kNever;  // leave clean
+    if (gtid == 0) {
+        a.o_in_off[0] = 0;
+        a.o_out_off[0] = 0;
+    }
+
+    // ---- the recurrence ------------------------------------------------------
+    for (uint32_t i = 0; i < S; ++i) {
+        const uint32_t base = sm.toff[i];
+        const uint32_t ni = sm.toff[i + 1] - base;
+        // P1: hits refresh their key; misses become candidates
+        {
+            uint32_t hits = 0, miss = 0;
+            for (uint32_t pos = gtid; pos < ni; pos += G) {
+                const uint32_t v = a.trace[base + pos];
+                const uint32_t nu = a.next_use[base + pos];
+                const int32_t s = a.node_slot[v];
+                if (s >= 0) {
+                    a.slot_key[s] = nu;
+                    atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
+                    a.pmiss[pos] = 0;
+                    ++hits;
+                } else {
+                    a.pmiss[pos] = 1;
+                    a.pkey[pos] = nu;
+                    atomicAdd(&sm.hnew[bucket_of(nu, S)], 1);
+                    ++miss;
+                }
+            }
+            hits = block_sum(hits, sm.scan);
+            miss = block_sum(miss, sm.scan);
+            if (tid == 0) {
+                sm.hinc[i] -= (int)hits;
+                if (miss) atomicAdd(&a.st->miss, miss);
+            }
+            hist_flush(sm.hinc, a.hist_inc, S + 1);
+            hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
+        }
+        grid_sync(a.bar);
+
+        // P2 (every CTA, redundantly): ALLIN or CUT; threshold bucket b*
+        const uint32_t m = *(volatile uint32_t*)&a.st->miss;
+        const uint32_t nres = *(volatile uint32_t*)&a.st->n_res;
+        const uint32_t in_total = *(volatile uint32_t*)&a.st->in_total;
+        const uint32_t out_total = *(volatile uint32_t*)&a.st->out_total;
+        const bool cut = (uint64_t)nres + m > K;
+        uint32_t bstar = 0, r = 0, inc_b = 0, new_b = 0;
+        int sel = 0;  // 0 none, 1 select among incumbents of b*, 2 among new of b*
+        if (cut) {
+            if (tid < 32) {
+                uint32_t cum = 0;
+                bool done = false;
+                for (uint32_t b0 = i + 1; b0 <= S && !done; b0 += 32) {
+                    const uint32_t b = b0 + tid;
+                    uint32_t ci = 0, cn = 0;
+                    if (b <= S) {
+                        ci = (uint32_t)((volatile int32_t*)a.hist_inc)[b];
+                        cn = ((volatile uint32_t*)a.hist_new)[b];
+                    }
+                    const uint32_t v = ci + cn;
+                    const uint32_t incl = warp_incl_scan(v) + cum;
+                    const unsigned hit = __ballot_sync(0xffffffffu, b <= S && incl >= K);
+                    if (hit) {
+                        const int ln = __ffs(hit) - 1;
+                        if ((int)tid == ln) {
+                            sm.bc[0] = b;
+                            sm.bc[1] = K - (incl - v);
+                            sm.bc[2] = ci;
+                            sm.bc[3] = cn;
+                        }
+                        done = true;
+                    }
+                    cum = __shfl_sync(0xffffffffu, incl, 31);
+                }
+            }
+            __syncthreads();
+            bstar = sm.bc[0];
+            r = sm.bc[1];
+            inc_b = sm.bc[2];
+            new_b = sm.bc[3];
+            __syncthreads();
+            if (r <= inc_b) sel = (r > 0 && r < inc_b) ? 1 : 0;
+            else sel = (r - inc_b < new_b) ? 2 : 0;
+        }
+        // keep rule inside b*: incumbents kept = min(r, inc_b) smallest ids;
+        // new admitted = max(0, r - inc_b) smallest ids.
+        const uint32_t keep_inc = min(r, inc_b);
+        const uint32_t admit_new = r > inc_b ? r - inc_b : 0;
+        uint32_t thr = 0xFFFFFFFFu;
+
+        if (cut) {
+            // P3: evict buckets > b*; collect selection candidates of b*
+            for (uint32_t s = gtid; s < nres; s += G) {
+                const uint32_t bk = bucket_of(a.slot_key[s], S);
+                const uint32_t v = a.slot_node[s];
+                const bool ev = bk > bstar || (bk == bstar && keep_inc == 0);
+                if (__any_sync(__activemask(), ev)) {
+                    const uint32_t o = agg_append(&a.st->n_out, ev);
+                    if (ev) {
+                        a.out_node[o] = v;
+                        a.out_slot[o] = s;
+                    }
+                }
+                if (sel == 1) {
+                    const bool c = bk == bstar;
+                    if (__any_sync(__activemask(), c)) {
+                        const uint32_t o = agg_append(&a.st->n_c, c);
+                        if (c) {
+                            a.c_id[o] = v;
+                            a.c_ref[o] = s;
+                            atomicAdd(&a.rh[v >> 21], 1u);
+                        }
+                    }
+                }
+            }
+            if (sel == 2) {
+                for (uint32_t pos = gtid; pos < ni; pos += G) {
+                    const bool c = a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar;
+                    if (__any_sync(__activemask(), c)) {
+                        const uint32_t o = agg_append(&a.st->n_c, c);
+                        if (c) {
+                            const uint32_t v = a.trace[base + pos];
+                            a.c_id[o] = v;
+                            a.c_ref[o] = pos;
+                            atomicAdd(&a.rh[v >> 21], 1u);
+                        }
+                    }
+                }
+            }
+            grid_sync(a.bar);
+            if (sel) {
+                const uint32_t nc = *(volatile uint32_t*)&a.st->n_c;
+                uint32_t want = sel == 1 ? keep_inc : admit_new, left;
+                const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const uint32_t v = a.c_id[k];
+                    if ((v >> 21) == d1) atomicAdd(&a.rh[2048 + ((v >> 10) & 2047)], 1u);
+                }
+                grid_sync(a.bar);
+                const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
+                const uint32_t pre = (d1 << 11) | d2;
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const uint32_t v = a.c_id[k];
+                    if ((v >> 10) == pre) atomicAdd(&a.rh[4096 + (v & 1023)], 1u);
+                }
+                grid_sync(a.bar);
+                const uint32_t d3 = hist_select(a.rh + 4096, 1024, left, &left, sm);
+                thr = (pre << 10) | d3;
+            }
+        }
+
+        // P4: per-chunk count of insertions (position order); b* evictions
+        auto in_flag = [&](uint32_t pos) -> bool {
+            if (!a.pmiss[pos]) return false;
+            if (!cut) return true;
+            const uint32_t bk = bucket_of(a.pkey[pos], S);
+            if (bk != bstar) return bk < bstar;
+            if (admit_new == 0) return false;
+            if (sel != 2) return true;
+            return a.trace[base + pos] <= thr;
+        };
+        const uint32_t chunk = (ni + gridDim.x - 1) / gridDim.x;
+        const uint32_t c0 = min(ni, blockIdx.x * chunk), c1 = min(ni, c0 + chunk);
+        {
+            uint32_t c = 0;
+            for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) c += in_flag(pos);
+            c = block_sum(c, sm.scan);
+            if (tid == 0) a.chunk_cnt[blockIdx.x] = c;
+            if (sel == 1) {
+                const uint32_t nc = *(volatile uint32_t*)&a.st->n_c;
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const bool ev = a.c_id[k] > thr;
+                    if (__any_sync(__activemask(), ev)) {
+                        const uint32_t o = agg_append(&a.st->n_out, ev);
+                        if (ev) {
+                            a.out_node[o] = a.c_id[k];
+                            a.out_slot[o] = a.c_ref[k];
+                        }
+                    }
+                }
+            }
+        }
+        grid_sync(a.bar);
+
+        // P5: ordered in-list; sort out-list by node id
+        uint32_t n_in;
+        {
+            uint32_t pre = 0, tot_all = 0;
+            for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
+                const uint32_t v = a.chunk_cnt[c];
+                if (c < blockIdx.x) pre += v;
+                tot_all += v;
+            }
+            pre = block_sum(pre, sm.scan);
+            tot_all = block_sum(tot_all, sm.scan);
+            n_in = tot_all;
+            uint32_t k = pre;
+            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {
+                const uint32_t pos = p0 + tid;
+                const uint32_t f = pos < c1 ? in_flag(pos) : 0;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan(f, sm.scan, tot);
+                if (f) {
+                    a.in_node[k + ex] = a.trace[base + pos];
+                    a.in_pos[k + ex] = pos;
+                }
+                k += tot;
+            }
+        }
+        const uint32_t n_out = *(volatile uint32_t*)&a.st->n_out;
+        if (n_out <= SORT_SMALL) {
+            if (blockIdx.x == 0 && n_out > 1) {
+                uint32_t P = 1;
+                while (P < n_out) P <<= 1;
+                for (uint32_t k = tid; k < P; k += blockDim.x)
+                    sm.sortbuf[k] = k < n_out ? (((unsigned long long)a.out_node[k] << 32) | a.out_slot[k])
+                                              : ~0ull;
+                __syncthreads();
+                for (uint32_t sz = 2; sz <= P; sz <<= 1) {
+                    for (uint32_t st = sz >> 1; st > 0; st >>= 1) {
+                        for (uint32_t k = tid; k < P; k += blockDim.x) {
+                            const uint32_t j = k ^ st;
+                            if (j > k) {
+                                const bool up = (k & sz) == 0;
+                                const unsigned long long x = sm.sortbuf[k], y = sm.sortbuf[j];
+                                if ((x > y) == up) {
+                                    sm.sortbuf[k] = y;
+                                    sm.sortbuf[j] = x;
+                                }
+                            }
+                        }
+                        __syncthreads();
+                    }
+                }
+                for (uint32_t k = tid; k < n_out; k += blockDim.x) {
+                    a.out_node[k] = (uint32_t)(sm.sortbuf[k] >> 32);
+                    a.out_slot[k] = (uint32_t)sm.sortbuf[k];
+                }
+            }
+            grid_sync(a.bar);
+        } else {
+            for (uint32_t k = gtid; k < n_out; k += G) {
+                const uint32_t v = a.out_node[k];
+                atomicOr(&a.bm_words[v >> 5], 1u << (v & 31));
+            }
+            grid_sync(a.bar);
+            const uint32_t wch = (a.nwords + gridDim.x - 1) / gridDim.x;
+            const uint32_t w0 = min(a.nwords, blockIdx.x * wch), w1 = min(a.nwords, w0 + wch);
+            uint32_t c = 0;
+            for (uint32_t w = w0 + tid; w < w1; w += blockDim.x) c += __popc(a.bm_words[w]);
+            c = block_sum(c, sm.scan);
+            if (tid == 0) a.bm_cnt[blockIdx.x] = c;
+            grid_sync(a.bar);
+            uint32_t pre = 0;
+            for (uint32_t cc = tid; cc < blockIdx.x; cc += blockDim.x) pre += a.bm_cnt[cc];
+            pre = block_sum(pre, sm.scan);
+            for (uint32_t p0 = w0; p0 < w1; p0 += blockDim.x) {
+                const uint32_t w = p0 + tid;
+                uint32_t bits = w < w1 ? a.bm_words[w] : 0;
+                uint32_t tot;
+                uint32_t k = pre + block_excl_scan((uint32_t)__popc(bits), sm.scan, tot);
+                if (bits) a.bm_words[w] = 0;
+                while (bits) {
+                    const int b = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const uint32_t v = w * 32 + b;
+                    a.out_node[k] = v;
+                    a.out_slot[k] = (uint32_t)a.node_slot[v];
+                    ++k;
+                }
+                pre += tot;
+            }
+            grid_sync(a.bar);
+        }
+
+        // P6: apply -- slots per FeatureCache rules, state + histogram update
+        for (uint32_t k = gtid; k < n_in; k += G) {
+            const uint32_t v = a.in_node[k];
+            const uint32_t pos = a.in_pos[k];
+            const uint32_t key = a.pkey[pos];
+            uint32_t s;
+            if (k < n_out) {
+                s = a.out_slot[k];
+                const uint32_t u = a.out_node[k];
+                atomicSub(&sm.hinc[bucket_of(a.slot_key[s], S)], 1);
+                a.node_slot[u] = -1;
+                a.o_out_ids[out_total + k] = u;
+            } else {
+                s = nres + (k - n_out);
+            }
+            a.slot_node[s] = v;
+            a.slot_key[s] = key;
+            a.node_slot[v] = (int32_t)s;
+            atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
+            a.o_in_ids[in_total + k] = v;
+            a.o_in_pos[in_total + k] = pos;
+            a.o_in_slot[in_total + k] = s;
+        }
+        hist_flush(sm.hinc, a.hist_inc, S + 1);
+        for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+        for (uint32_t b = gtid; b < 3 * 2048; b += G) a.rh[b] = 0;
+        if (gtid == 0) {
+            if (n_out > n_in) atomicOr(&a.st->err, 4u);
+            a.o_misses[i] = m;
+            a.st->n_res = nres + n_in - n_out;
+            a.st->in_total = in_total + n_in;
+            a.st->out_total = out_total + n_out;
+            a.o_in_off[i + 1] = in_total + n_in;
+            a.o_out_off[i + 1] = out_total + n_out;
+            a.st->miss = 0;
+            a.st->n_out = 0;
+            a.st->n_c = 0;
+        }
+        grid_sync(a.bar);
+    }
+    // leave node_slot clean
+    const uint32_t nfin = a.st->n_res;
+    for (uint32_t s = gtid; s < nfin; s += G) a.node_slot[a.slot_node[s]] = -1;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static InspectScratch& bufs_for(gx_ctx* ctx) { return ctx->is; }
+
+// Exact reference error for an invalid trace (count_pass, changeset.hpp:76-88).
+static void host_trace_error(const std::vector<uint32_t>& flat, const std::vector<uint64_t>& off,
+                             uint64_t N) {
+    std::unordered_set<uint64_t> seen;
+    for (size_t i = 0; i + 1 < off.size(); ++i) {
+        seen.clear();
+        for (uint64_t x = off[i]; x < off[i + 1]; ++x) {
+            if (flat[x] >= N) fail(GX_OUT_OF_RANGE, "trace id out of range");
+            if (!seen.insert(flat[x]).second) fail(GX_LOGIC_ERROR, "duplicate id within one iteration");
+        }
+    }
+    fail(GX_RUNTIME_ERROR, "inspector: invalid trace");
+}
+
+void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
+                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out) {
+    const uint64_t S = off.size() - 1;
+    if (S > kMaxIters) fail(GX_INVALID_ARGUMENT, "at most 4096 iterations per superbatch");
+    if (N >= 0xFFFFFFFFull) fail(GX_OVERFLOW, "num_nodes exceeds the u32 device id range");
+    uint64_t maxw = 1;
+    for (uint64_t i = 0; i < S; ++i) maxw = std::max<uint64_t>(maxw, off[i + 1] - off[i]);
+    const uint64_t A = off[S];
+    if (A >= 0x7FFFFFFFull) fail(GX_INVALID_ARGUMENT, "superbatch trace too large (>= 2^31 accesses)");
+    if (K > 0x7FFFFFFFull) K = std::min<uint64_t>(K, 0x7FFFFFFFull);
+    const uint64_t Keff = std::min<uint64_t>(K, A + 1);  // capacity beyond A is never used
+    cudaStream_t st = ctx->stream;
+    InspectScratch& is = ctx->is;
+    InspectScratch& B = bufs_for(ctx);
+    if (is.N < N) {
+        is.last.alloc(N);
+        is.node_slot.alloc(N);
+        GX_CUDA(cudaMemsetAsync(is.last.p, 0xff, N * 4, st));
+        GX_CUDA(cudaMemsetAsync(is.node_slot.p, 0xff, N * 4, st));
+        is.N = N;
+        B.bm_words.alloc((N + 31) / 32 + 1);
+        GX_CUDA(cudaMemsetAsync(B.bm_words.p, 0, B.bm_words.bytes(), st));
+    }
+    // is.trace holds the flat u32 trace (inspect_fill_*)
+    std::vector<uint32_t> off32(S + 1);
+    for (uint64_t i = 0; i <= S; ++i) off32[i] = (uint32_t)off[i];
+    B.toff.reserve(S + 1);
+    GX_CUDA(cudaMemcpyAsync(B.toff.p, off32.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st));
+    is.next_use.reserve(std::max<uint64_t>(A, 1));
+    const uint64_t ntiles = (A + IN_TILE - 1) / IN_TILE + 1;
+    B.tile_cnt.reserve(ntiles);
+    B.slot_node.reserve(Keff + 1);
+    B.slot_key.reserve(Keff + 1);
+    B.hist_inc.reserve(S + 1);
+    B.hist_new.reserve(S + 1);
+    GX_CUDA(cudaMemsetAsync(B.hist_inc.p, 0, (S + 1) * 4, st));
+    GX_CUDA(cudaMemsetAsync(B.hist_new.p, 0, (S + 1) * 4, st));
+    B.rh.reserve(3 * 2048);
+    GX_CUDA(cudaMemsetAsync(B.rh.p, 0, 3 * 2048 * 4, st));
+    B.pkey.reserve(maxw);
+    B.pmiss.reserve(maxw);
+    B.out_node.reserve(maxw);
+    B.out_slot.reserve(maxw);
+    B.c_id.reserve(std::max(Keff, maxw));
+    B.c_ref.reserve(std::max(Keff, maxw));
+    B.in_node.reserve(maxw);
+    B.in_pos.reserve(maxw);
+    const int grid = ctx->num_sms;
+    B.chunk_cnt.reserve(grid);
+    B.bm_cnt.reserve(grid);
+    B.st.reserve(16);
+    GX_CUDA(cudaMemsetAsync(B.st.p, 0, sizeof(IState), st));
+    static_assert(sizeof(IState) <= 16 * sizeof(uint32_t), "IState fits the scratch words");
+
+    out->ctx = ctx;
+    out->S = S;
+    out->N = N;
+    out->K = K;
+    out->init.reserve(Keff + 1);
+    out->in_ids.reserve(A + 1);
+    out->in_pos.reserve(A + 1);
+    out->in_slot.reserve(A + 1);
+    out->out_ids.reserve(A + 1);
+    DevBuf<uint32_t> d_misses(S + 1), d_in_off(S + 1), d_out_off(S + 1);
+
+    if (n_init_explicit >= 0) {
+        std::vector<uint32_t> i32(std::max<int64_t>(n_init_explicit, 1));
+        for (int64_t k = 0; k < n_init_explicit; ++k) i32[k] = (uint32_t)h_init[k];
+        B.init_ext.reserve(i32.size());
+        GX_CUDA(cudaMemcpyAsync(B.init_ext.p, i32.data(), n_init_explicit * 4, cudaMemcpyHostToDevice, st));
+    }
+
+    IArgs a{};
+    a.trace = is.trace.p;
+    a.toff = B.toff.p;
+    a.S = (uint32_t)S;
+    a.A = (uint32_t)A;
+    a.K = (uint32_t)Keff;
+    a.maxw = (uint32_t)maxw;
+    a.N = N;
+    a.last = is.last.p;
+    a.node_slot = is.node_slot.p;
+    a.next_use = is.next_use.p;
+    a.tile_cnt = B.tile_cnt.p;
+    a.slot_node = B.slot_node.p;
+    a.slot_key = B.slot_key.p;
+    a.hist_inc = B.hist_inc.p;
+    a.hist_new = B.hist_new.p;
+    a.rh = B.rh.p;
+    a.pkey = B.pkey.p;
+    a.pmiss = B.pmiss.p;
+    a.out_node = B.out_node.p;
+    a.out_slot = B.out_slot.p;
+    a.c_id = B.c_id.p;
+    a.c_ref = B.c_ref.p;
+    a.in_node = B.in_node.p;
+    a.in_pos = B.in_pos.p;
+    a.chunk_cnt = B.chunk_cnt.p;
+    a.bm_words = B.bm_words.p;
+    a.nwords = (uint32_t)((N + 31) / 32);
+    a.bm_cnt = B.bm_cnt.p;
+    a.init_ext = n_init_explicit >= 0 ? B.init_ext.p : nullptr;
+    a.n_init_ext = n_init_explicit >= 0 ? (uint32_t)n_init_explicit : 0;
+    a.explicit_init = n_init_explicit >= 0;
+    a.o_init = out->init.p;
+    a.o_in_ids = out->in_ids.p;
+    a.o_in_pos = out->in_pos.p;
+    a.o_in_slot = out->in_slot.p;
+    a.o_out_ids = out->out_ids.p;
+    a.o_misses = d_misses.p;
+    a.o_in_off = d_in_off.p;
+    a.o_out_off = d_out_off.p;
+    a.st = reinterpret_cast<IState*>(B.st.p);
+    a.bar = ctx->barrier.p;
+
+    const size_t smem = sizeof(ISmem);
+    static bool attr = false;
+    if (!attr) {
+        GX_CUDA(cudaFuncSetAttribute(k_inspect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int bps = 0;
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_inspect, IN_THREADS, smem));
+        if (bps < 1) fail(GX_CUDA_ERROR, "inspector kernel cannot be resident");
+        attr = true;
+    }
+    void* args[] = {&a};
+    GX_CUDA(cudaLaunchCooperativeKernel((void*)k_inspect, dim3(grid), dim3(IN_THREADS), args, smem, st));
+    GX_CHECK_LAUNCH();
+
+    IState hs;
+    GX_CUDA(cudaMemcpyAsync(&hs, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
+    std::vector<uint32_t> m32(S + 1), io32(S + 1), oo32(S + 1);
+    GX_CUDA(cudaMemcpyAsync(m32.data(), d_misses.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(io32.data(), d_in_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(oo32.data(), d_out_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    if (hs.err & 3u) {
+        std::vector<uint32_t> flat(A);
+        GX_CUDA(cudaMemcpy(flat.data(), is.trace.p, A * 4, cudaMemcpyDeviceToHost));
+        // the kernel bailed out before touching node_slot; `last` may be dirty
+        GX_CUDA(cudaMemset(is.last.p, 0xff, N * 4));
+        host_trace_error(flat, off, N);
+    }
+    if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");
+    out->n_init = n_init_explicit >= 0 ? (uint64_t)n_init_explicit : std::min<uint64_t>(hs.n_first, Keff);
+    out->h_misses.assign(m32.begin(), m32.begin() + S);
+    out->h_in_off.assign(S + 1, 0);
+    out->h_out_off.assign(S + 1, 0);
+    for (uint64_t i = 0; i <= S; ++i) {
+        out->h_in_off[i] = io32[i];
+        out->h_out_off[i] = oo32[i];
+    }
+    if (S == 0) {
+        out->h_in_off[0] = 0;
+        out->h_out_off[0] = 0;
+    }
+}
+
+void inspect_ensure_trace(gx_ctx* ctx, uint64_t A) { ctx->is.trace.reserve(std::max<uint64_t>(A, 1)); }
+
+__global__ void k_flatten(const uint32_t* __restrict__ ids, uint64_t stride, const uint64_t* __restrict__ off,
+                          uint32_t S, uint32_t* __restrict__ out) {
+    for (uint32_t i = blockIdx.y; i < S; i += gridDim.y) {
+        const uint64_t o = off[i], n = off[i + 1] - o;
+        for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x)
+            out[o + k] = ids[i * stride + k];
+    }
+}
+
+// Flatten S device lists (ids[i*stride .. +n_i)) into ctx->is.trace.
+void inspect_fill_from_device(gx_ctx* ctx, const uint32_t* d_ids, uint64_t stride,
+                              const std::vector<uint64_t>& off) {
+    const uint64_t S = off.size() - 1;
+    inspect_ensure_trace(ctx, off[S]);
+    DevBuf<uint64_t>& d_off = ctx->is.trace_off;
+    d_off.reserve(S + 1);
+    GX_CUDA(cudaMemcpyAsync(d_off.p, off.data(), (S + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
+    if (S && off[S]) {
+        dim3 grid(64, (unsigned)std::min<uint64_t>(S, 65535));
+        k_flatten<<<grid, 256, 0, ctx->stream>>>(d_ids, stride, d_off.p, (uint32_t)S, ctx->is.trace.p);
+        GX_CHECK_LAUNCH();
+    }
+}
+
+// Upload a host u64 trace (validated for range on the host first).
+void inspect_fill_from_host(gx_ctx* ctx, const uint64_t* flat, const std::vector<uint64_t>& off,
+                            uint64_t N) {
+    const uint64_t S = off.size() - 1, A = off[S];
+    std::vector<uint32_t> t32(std::max<uint64_t>(A, 1));
+    bool bad = false;
+    for (uint64_t x = 0; x < A; ++x) {
+        if (flat[x] >= N) {
+            bad = true;
+            break;
+        }
+        t32[x] = (uint32_t)flat[x];
+    }
+    if (bad) {  // exact reference precedence (count_pass order) on the host
+        std::vector<uint32_t> f2(A);
+        for (uint64_t x = 0; x < A; ++x) f2[x] = flat[x] >= N ? 0xFFFFFFFFu : (uint32_t)flat[x];
+        host_trace_error(f2, off, N);
+    }
+    inspect_ensure_trace(ctx, A);
+    GX_CUDA(cudaMemcpyAsync(ctx->is.trace.p, t32.data(), A * 4, cudaMemcpyHostToDevice, ctx->stream));
+    GX_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ---------------------------------------------------------------------------
+// AccessIndex (changeset.hpp:61-129) for parity tests: ptr = exclusive scan of
+// per-node counts; iters in (node, iteration) order; MSB flag on each region
+// start; all-ones dummy tail.
+// ---------------------------------------------------------------------------
+__global__ void k_ai_count(const uint32_t* trace, const uint64_t* off, uint32_t S, uint32_t* stamp,
+                           unsigned long long* counts, uint64_t N, unsigned int* err) {
+    for (uint32_t i = blockIdx.y; i < S; i += gridDim.y) {
+        const uint64_t o = off[i], n = off[i + 1] - o;
+        for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+            const uint32_t v = trace[o + k];
+            if (v >= N) {
+                atomicOr(err, 1u);
+                continue;
+            }
+            if (atomicExch(&stamp[v], i) == i) atomicOr(err, 2u);
+            atomicAdd(&counts[v], 1ull);
+        }
+    }
+}
+__global__ void k_ai_scatter(const uint32_t* trace, uint64_t o, uint64_t n, uint32_t i,
+                             const unsigned long long* ptr, uint32_t* cursor, unsigned long long* iters) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n; k += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = trace[o + k];
+        const uint32_t c = cursor[v]++;  // v appears once per iteration: no race
+        iters[ptr[v] + c] = i;
+    }
+}
+__global__ void k_ai_flags(const unsigned long long* counts, const unsigned long long* ptr, uint64_t N,
+                           unsigned long long* iters, const uint32_t* trace, uint64_t A, uint32_t* stamp,
+                           uint32_t* cursor) {
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < N; v += (uint64_t)gridDim.x * blockDim.x)
+        if (counts[v]) iters[ptr[v]] |= 0x8000000000000000ull;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < A; x += (uint64_t)gridDim.x * blockDim.x) {
+        stamp[trace[x]] = kNever;
+        cursor[trace[x]] = 0;
+    }
+}
+
+void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t* h_iters,
+                      uint64_t* h_ptr) {
+    const uint64_t S = off.size() - 1, A = off[S];
+    cudaStream_t st = ctx->stream;
+    DevBuf<uint32_t> stamp(std::max<uint64_t>(N, 1)), cursor(std::max<uint64_t>(N, 1));
+    DevBuf<unsigned long long> counts(std::max<uint64_t>(N, 1)), ptr(std::max<uint64_t>(N, 1)),
+        iters(A + 1);
+    DevBuf<uint64_t> d_off(S + 1);
+    DevBuf<unsigned int> err(1);
+    GX_CUDA(cudaMemsetAsync(stamp.p, 0xff, stamp.bytes(), st));
+    GX_CUDA(cudaMemsetAsync(cursor.p, 0, cursor.bytes(), st));
+    GX_CUDA(cudaMemsetAsync(counts.p, 0, counts.bytes(), st));
+    GX_CUDA(cudaMemsetAsync(err.p, 0, 4, st));
+    GX_CUDA(cudaMemcpyAsync(d_off.p, off.data(), (S + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (S && A) {
+        dim3 grid(32, (unsigned)std::min<uint64_t>(S, 65535));
+        k_ai_count<<<grid, 256, 0, st>>>(ctx->is.trace.p, d_off.p, (uint32_t)S, stamp.p, counts.p, N, err.p);
+        GX_CHECK_LAUNCH();
+    }
+    unsigned int he = 0;
+    GX_CUDA(cudaMemcpyAsync(&he, err.p, 4, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    if (he) {
+        std::vector<uint32_t> flat(A);
+        GX_CUDA(cudaMemcpy(flat.data(), ctx->is.trace.p, A * 4, cudaMemcpyDeviceToHost));
+        host_trace_error(flat, off, N);
+    }
+    if (N) {
+        size_t tb = 0;
+        cub::DeviceScan::ExclusiveSum(nullptr, tb, counts.p, ptr.p, (int)N, st);
+        DevBuf<uint8_t> tmp(tb + 1);
+        GX_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, counts.p, ptr.p, (int)N, st));
+    }
+    for (uint64_t i = 0; i < S; ++i) {
+        const uint64_t n = off[i + 1] - off[i];
+        if (!n) continue;
+        k_ai_scatter<<<ceil_div(n, 256), 256, 0, st>>>(ctx->is.trace.p, off[i], n, (uint32_t)i, ptr.p,
+                                                        cursor.p, iters.p);
+        GX_CHECK_LAUNCH();
+    }
+    k_ai_flags<<<ctx->num_sms * 4, 256, 0, st>>>(counts.p, ptr.p, N, iters.p, ctx->is.trace.p, A, stamp.p,
+                                                 cursor.p);
+    GX_CHECK_LAUNCH();
+    const unsigned long long dummy = ~0ull;
+    GX_CUDA(cudaMemcpyAsync(iters.p + A, &dummy, 8, cudaMemcpyHostToDevice, st));
+    GX_CUDA(cudaMemcpyAsync(h_iters, iters.p, (A + 1) * 8, cudaMemcpyDeviceToHost, st));
+    if (N) GX_CUDA(cudaMemcpyAsync(h_ptr, ptr.p, N * 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace gx

@@ -1,0 +1,721 @@
+// sampler.cu -- multi-layer uniform neighbour sampling for a whole superbatch
+// in ONE persistent, cooperatively launched kernel (all CTAs co-resident,
+// phases separated by grid barriers).
+//
+// Reference: sample_batch (sampler.hpp:69-117) and superbatch_sample
+// (sampler.hpp:197-243). Output is bit-identical:
+//  * RNG: SplitMix64 per batch seeded derive_seed(global_seed, first+i)
+//    (sampler.hpp:216). Draw t of the sequential stream == mix64(seed+t*gamma),
+//    so the counter of draw j of parent k at layer l is
+//        base_l + excl_scan_k(min(f_l, deg)) + j
+//    and every draw is computed independently.
+//  * Partial Fisher-Yates (sampler.hpp:103-107) on a FRESH copy of the sorted
+//    in-list per parent. Picks are data-independent; the swap chain is
+//    resolved on positions, so only the <= f chosen indices[] entries are read
+//    and lists are never copied (resolve_pos below).
+//  * Discovery-order dedup (sampler.hpp:78-84,108-112): per-batch open-address
+//    table keyed by node id; a candidate child stores (NEW | flat draw
+//    position) and 64-bit atomicMin keeps the first position; pre-existing ids
+//    hold their local id (< NEW) and always win. Winners are ranked by draw
+//    position (block scan + per-tile offsets), giving exactly the reference's
+//    append order; edges are emitted in draw order.
+//  * IoStats (graph_store.hpp:145-154): one list + pages_touched(8 ip[v],
+//    8 ip[v+1]) + 8 deg bytes per expanded parent (no neighbor cache).
+#include <algorithm>
+#include <cooperative_groups.h>
+#include <unordered_set>
+
+#include "gx_internal.cuh"
+
+namespace gx {
+
+constexpr int kMaxLayers = 16;
+constexpr int SB_THREADS = 512;
+constexpr int SB_IPT = 8;
+constexpr uint32_t SB_TILE = SB_THREADS * SB_IPT;
+constexpr uint32_t kNewBit = 0x80000000u;
+constexpr unsigned long long kEmptySlot = ~0ull;
+constexpr uint32_t kMaxBatchesPerLaunch = 4096;
+constexpr int kPickCache = 32;
+
+struct SampArgs {
+    const uint64_t* __restrict__ indptr;
+    const uint32_t* __restrict__ indices;
+    uint64_t N;
+    uint32_t S, L;
+    uint32_t fan[kMaxLayers];
+    const uint64_t* bseed;
+    const uint32_t* seeds;
+    const uint64_t* seed_off;
+    uint32_t* ids;
+    uint64_t cap_ids;
+    uint32_t* n_ids;
+    uint2* edges;
+    uint64_t cap_e_batch;
+    uint64_t e_off[kMaxLayers];
+    uint32_t* layer_count;
+    uint32_t* F;
+    uint32_t* T;
+    uint64_t* dbase;
+    uint32_t* pscan;
+    uint64_t* plo;
+    uint32_t* pdeg;
+    uint32_t* idslot;
+    uint32_t* tsum;
+    uint32_t* tsum2;
+    uint32_t* dslot;
+    uint32_t* drank;
+    uint64_t cap_draw;
+    unsigned long long* tab0;
+    unsigned long long* tab1;
+    uint64_t tab_cap;  // per batch max
+    unsigned long long* io;
+    GridBarrier* bar;
+};
+
+struct SampSmem {
+    uint32_t scan[34];
+    unsigned long long red[34];
+    uint32_t tp[kMaxBatchesPerLaunch + 1];
+};
+
+// tp[0..S] = prefix of ceil(cnt[b] / SB_TILE); returns total tiles.
+__device__ uint32_t build_tiles(const uint32_t* cnt, uint32_t S, SampSmem& sm) {
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < S; base += blockDim.x) {
+        uint32_t b = base + threadIdx.x;
+        uint32_t v = b < S ? (cnt[b] + SB_TILE - 1) / SB_TILE : 0;
+        uint32_t tot;
+        uint32_t ex = block_excl_scan(v, sm.scan, tot);
+        if (b < S) sm.tp[b] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) sm.tp[S] = carry;
+    __syncthreads();
+    return carry;
+}
+
+__device__ __forceinline__ uint32_t tile_batch(const SampSmem& sm, uint32_t S, uint32_t t) {
+    uint32_t lo = 0, hi = S;  // find b: tp[b] <= t < tp[b+1]
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (sm.tp[mid] <= t) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Sum of tile sums of batch b's tiles before tile t (one warp; result to all threads).
+__device__ __forceinline__ uint32_t tile_offset(const uint32_t* tsum, uint32_t first, uint32_t t,
+                                                uint32_t* bcast) {
+    if (threadIdx.x < 32) {
+        uint32_t s = 0;
+        for (uint32_t i = first + threadIdx.x; i < t; i += 32) s += tsum[i];
+        s = warp_sum(s);
+        if (threadIdx.x == 0) *bcast = s;
+    }
+    __syncthreads();
+    uint32_t r = *bcast;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ uint32_t table_insert(unsigned long long* tab, uint32_t H, uint32_t key,
+                                                 uint32_t val) {
+    const unsigned long long ent = ((unsigned long long)key << 32) | val;
+    uint32_t s = hash32(key) & (H - 1);
+    while (true) {
+        unsigned long long cur = tab[s];
+        if (cur == kEmptySlot) {
+            unsigned long long prev = atomicCAS(&tab[s], kEmptySlot, ent);
+            if (prev == kEmptySlot) return s;
+            cur = prev;
+        }
+        if ((uint32_t)(cur >> 32) == key) {
+            if (cur > ent) atomicMin(&tab[s], ent);
+            return s;
+        }
+        s = (s + 1) & (H - 1);
+    }
+}
+
+__device__ __forceinline__ uint32_t pick_at(uint64_t seed, uint64_t t0, uint32_t i, uint32_t deg) {
+    return i + (uint32_t)draw_bounded(seed, t0 + i, (uint64_t)(deg - i));
+}
+
+// Position (within the parent's sorted list) of the child taken at FY step j:
+// P_j[pick_j], where P_j[x] = P_i[i] for the latest i < j with pick_i == x,
+// else x (sampler.hpp:103-107 resolved without materialising the list).
+__device__ __forceinline__ uint32_t resolve_pos(const uint32_t* pk, uint32_t j, uint64_t seed,
+                                                uint64_t t0, uint32_t deg) {
+    uint32_t c = pk[j < kPickCache ? j : 0];
+    if (j >= kPickCache) c = pick_at(seed, t0, j, deg);
+    uint32_t lim = j;
+    while (true) {
+        int found = -1;
+        for (int i = (int)lim - 1; i >= 0; --i) {
+            uint32_t pi = i < kPickCache ? pk[i] : pick_at(seed, t0, (uint32_t)i, deg);
+            if (pi == c) {
+                found = i;
+                break;
+            }
+        }
+        if (found < 0) return c;
+        c = (uint32_t)found;
+        lim = (uint32_t)found;
+    }
+}
+
+__global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
+    extern __shared__ unsigned char smem_raw[];
+    SampSmem& sm = *reinterpret_cast<SampSmem*>(smem_raw);
+    __shared__ uint32_t bcast;
+    const uint32_t S = a.S;
+    const uint32_t tid = threadIdx.x;
+    int cur = 0;
+    uint32_t H = 0;
+
+    for (uint32_t l = 0; l < a.L || l == 0; ++l) {
+        // ---- Phase D: (re)build the per-batch tables with the current ids --
+        // H = nextpow2(2 * max_b F_b * (1 + f_l)) bounds the table load <= 1/2.
+        uint32_t newH;
+        {
+            unsigned long long mx = 0;
+            for (uint32_t b = tid; b < S; b += blockDim.x) {
+                unsigned long long fb = l == 0 ? (a.seed_off[b + 1] - a.seed_off[b]) : a.F[b];
+                unsigned long long need = fb * (1ull + (a.L ? a.fan[l] : 0));
+                mx = max(mx, need);
+            }
+            // block max via the scan buffer
+            for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if ((tid & 31) == 0) sm.red[tid >> 5] = mx;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long m = 0;
+                for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = max(m, sm.red[w]);
+                m = m < a.cap_ids ? m : (unsigned long long)a.cap_ids;
+                unsigned long long h = 1024;
+                while (h < 2 * m) h <<= 1;
+                if (h > a.tab_cap) h = a.tab_cap;
+                sm.red[32] = h;
+            }
+            __syncthreads();
+            newH = (uint32_t)sm.red[32];
+            __syncthreads();
+        }
+        if (l == 0 || newH != H) {
+            unsigned long long* told = cur ? a.tab1 : a.tab0;
+            unsigned long long* tnew = cur ? a.tab0 : a.tab1;
+            if (l == 0) tnew = told;  // tables start clean
+            const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
+            for (uint32_t b = 0; b < S; ++b) {
+                const uint32_t nb = l == 0 ? (uint32_t)(a.seed_off[b + 1] - a.seed_off[b]) : a.F[b];
+                for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + tid; k < nb; k += total_threads) {
+                    const uint64_t gi = (uint64_t)b * a.cap_ids + k;
+                    uint32_t v;
+                    if (l == 0) {
+                        v = a.seeds[a.seed_off[b] + k];
+                        a.ids[gi] = v;
+                    } else {
+                        v = a.ids[gi];
+                        told[(uint64_t)b * a.tab_cap + a.idslot[gi]] = kEmptySlot;
+                    }
+                    a.idslot[gi] = table_insert(tnew + (uint64_t)b * a.tab_cap, newH, v, (uint32_t)k);
+                }
+            }
+            if (l > 0) cur ^= 1;
+            H = newH;
+            if (l == 0) {
+                for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
+                    uint32_t ns = (uint32_t)(a.seed_off[b + 1] - a.seed_off[b]);
+                    a.F[b] = ns;
+                    a.n_ids[b] = ns;
+                    a.dbase[b] = 0;
+                }
+            }
+            grid_sync(a.bar);
+        }
+        if (a.L == 0) break;
+        unsigned long long* tab = cur ? a.tab1 : a.tab0;
+        const uint32_t f = a.fan[l];
+
+        // ---- Phase A: per parent deg/take, IoStats, tile sums of takes ----
+        {
+            uint32_t ntiles = build_tiles(a.F, S, sm);
+            unsigned long long io_pages = 0, io_lists = 0, io_bytes = 0;
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const uint32_t b = tile_batch(sm, S, t);
+                const uint32_t Fb = a.F[b];
+                const uint32_t k0 = (t - sm.tp[b]) * SB_TILE + tid * SB_IPT;
+                uint32_t s = 0;
+#pragma unroll
+                for (int j = 0; j < SB_IPT; ++j) {
+                    const uint32_t k = k0 + j;
+                    if (k < Fb) {
+                        const uint64_t gi = (uint64_t)b * a.cap_ids + k;
+                        const uint32_t v = a.ids[gi];
+                        const uint64_t lo = a.indptr[v], hi = a.indptr[v + 1];
+                        const uint32_t deg = (uint32_t)(hi - lo);
+                        const uint32_t take = min(f, deg);
+                        a.plo[gi] = lo;
+                        a.pdeg[gi] = deg;
+                        a.pscan[gi] = take;
+                        s += take;
+                        io_lists += 1;
+                        io_pages += pages_touched(8 * lo, 8 * hi);
+                        io_bytes += 8ull * deg;
+                    }
+                }
+                uint32_t tot = block_sum(s, sm.scan);
+                if (tid == 0) a.tsum[t] = tot;
+            }
+            io_pages = warp_sum(io_pages);
+            io_lists = warp_sum(io_lists);
+            io_bytes = warp_sum(io_bytes);
+            if ((tid & 31) == 0 && io_lists) {
+                atomicAdd(&a.io[0], io_pages);
+                atomicAdd(&a.io[1], io_lists);
+                atomicAdd(&a.io[2], io_bytes);
+            }
+        }
+        grid_sync(a.bar);
+
+        // ---- Phase E: scan takes -> draw offsets; draw, read child, insert ----
+        {
+            uint32_t ntiles = build_tiles(a.F, S, sm);
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const uint32_t b = tile_batch(sm, S, t);
+                const uint32_t Fb = a.F[b];
+                const uint32_t first = sm.tp[b];
+                const uint32_t toff = tile_offset(a.tsum, first, t, &bcast);
+                if (t == first && tid < 32) {  // batch total T_b
+                    uint32_t s2 = 0;
+                    for (uint32_t i = first + tid; i < sm.tp[b + 1]; i += 32) s2 += a.tsum[i];
+                    s2 = warp_sum(s2);
+                    if (tid == 0) a.T[b] = s2;
+                }
+                const uint32_t k0 = (t - first) * SB_TILE + tid * SB_IPT;
+                uint32_t take[SB_IPT];
+                uint32_t s = 0;
+#pragma unroll
+                for (int j = 0; j < SB_IPT; ++j) {
+                    const uint32_t k = k0 + j;
+                    take[j] = k < Fb ? a.pscan[(uint64_t)b * a.cap_ids + k] : 0;
+                    s += take[j];
+                }
+                uint32_t tot;
+                uint32_t off = toff + block_excl_scan(s, sm.scan, tot);
+                const uint64_t seed = a.bseed[b];
+                const uint64_t dbase = a.dbase[b];
+                unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
+                uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+                uint32_t* bdslot = a.dslot + (uint64_t)b * a.cap_draw;
+                for (int j = 0; j < SB_IPT; ++j) {
+                    const uint32_t k = k0 + j;
+                    const uint32_t tk = take[j];
+                    if (tk) {
+                        const uint64_t gi = (uint64_t)b * a.cap_ids + k;
+                        const uint64_t lo = a.plo[gi];
+                        const uint32_t deg = a.pdeg[gi];
+                        const uint64_t t0 = dbase + off;
+                        uint32_t pk[kPickCache];
+                        const uint32_t nc = min(tk, (uint32_t)kPickCache);
+                        for (uint32_t q = 0; q < nc; ++q) pk[q] = pick_at(seed, t0, q, deg);
+                        for (uint32_t q = 0; q < tk; ++q) {
+                            const uint32_t pos = resolve_pos(pk, q, seed, t0, deg);
+                            const uint32_t child = __ldg(a.indices + lo + pos);
+                            const uint32_t p = off + q;
+                            bedge[p] = make_uint2(child, k);
+                            bdslot[p] = table_insert(btab, H, child, kNewBit | p);
+                        }
+                    }
+                    off += tk;
+                }
+            }
+        }
+        grid_sync(a.bar);
+
+        // ---- Phase F: first-occurrence flags per draw, tile sums ----------
+        {
+            uint32_t ntiles = build_tiles(a.T, S, sm);
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const uint32_t b = tile_batch(sm, S, t);
+                const uint32_t Tb = a.T[b];
+                const uint32_t p0 = (t - sm.tp[b]) * SB_TILE + tid * SB_IPT;
+                const unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
+                const uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+                uint32_t s = 0;
+#pragma unroll
+                for (int j = 0; j < SB_IPT; ++j) {
+                    const uint32_t p = p0 + j;
+                    if (p < Tb) {
+                        const uint64_t gd = (uint64_t)b * a.cap_draw + p;
+                        const unsigned long long e = btab[a.dslot[gd]];
+                        const uint32_t child = bedge[p].x;
+                        const uint32_t fl =
+                            e == (((unsigned long long)child << 32) | (kNewBit | p)) ? 1u : 0u;
+                        a.drank[gd] = fl;
+                        s += fl;
+                    }
+                }
+                uint32_t tot = block_sum(s, sm.scan);
+                if (tid == 0) a.tsum2[t] = tot;
+            }
+        }
+        grid_sync(a.bar);
+
+        // ---- Phase H: rank winners by draw position -> new local ids -------
+        {
+            uint32_t ntiles = build_tiles(a.T, S, sm);
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const uint32_t b = tile_batch(sm, S, t);
+                const uint32_t Tb = a.T[b];
+                const uint32_t first = sm.tp[b];
+                const uint32_t Fb = a.F[b];
+                const uint32_t toff = tile_offset(a.tsum2, first, t, &bcast);
+                if (t == first && tid < 32) {
+                    uint32_t s2 = 0;
+                    for (uint32_t i = first + tid; i < sm.tp[b + 1]; i += 32) s2 += a.tsum2[i];
+                    s2 = warp_sum(s2);
+                    if (tid == 0) a.n_ids[b] = Fb + s2;
+                }
+                const uint32_t p0 = (t - first) * SB_TILE + tid * SB_IPT;
+                uint32_t fl[SB_IPT];
+                uint32_t s = 0;
+#pragma unroll
+                for (int j = 0; j < SB_IPT; ++j) {
+                    const uint32_t p = p0 + j;
+                    fl[j] = p < Tb ? a.drank[(uint64_t)b * a.cap_draw + p] : 0;
+                    s += fl[j];
+                }
+                uint32_t tot;
+                uint32_t r = toff + block_excl_scan(s, sm.scan, tot);
+                unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
+                const uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+#pragma unroll
+                for (int j = 0; j < SB_IPT; ++j) {
+                    if (fl[j]) {
+                        const uint32_t p = p0 + j;
+                        const uint32_t child = bedge[p].x;
+                        const uint32_t local = Fb + r;
+                        const uint32_t slot = a.dslot[(uint64_t)b * a.cap_draw + p];
+                        a.ids[(uint64_t)b * a.cap_ids + local] = child;
+                        a.idslot[(uint64_t)b * a.cap_ids + local] = slot;
+                        btab[slot] = ((unsigned long long)child << 32) | local;
+                        ++r;
+                    }
+                }
+            }
+        }
+        grid_sync(a.bar);
+
+        // ---- Phase I: edge sources -> local ids; per-batch bookkeeping ------
+        {
+            const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
+            for (uint32_t b = 0; b < S; ++b) {
+                const uint32_t Tb = a.T[b];
+                const unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
+                uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+                const uint32_t* bdslot = a.dslot + (uint64_t)b * a.cap_draw;
+                for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + tid; p < Tb; p += total_threads)
+                    bedge[p].x = (uint32_t)btab[bdslot[p]];
+            }
+            for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
+                a.layer_count[(uint64_t)b * a.L + l] = a.T[b];
+                a.dbase[b] += a.T[b];
+                a.F[b] = a.n_ids[b];
+            }
+        }
+        grid_sync(a.bar);
+    }
+
+    // ---- leave the live table clean for the next call -----------------------
+    {
+        unsigned long long* tab = cur ? a.tab1 : a.tab0;
+        const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
+        for (uint32_t b = 0; b < S; ++b) {
+            const uint32_t nb = a.n_ids[b];
+            for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + tid; k < nb; k += total_threads)
+                tab[(uint64_t)b * a.tab_cap + a.idslot[(uint64_t)b * a.cap_ids + k]] = kEmptySlot;
+        }
+    }
+}
+
+static uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t cap) {
+    if (a == 0 || b == 0) return 0;
+    if (a > cap / b) return cap;
+    return std::min(cap, a * b);
+}
+
+void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
+                const uint32_t* fanouts, uint32_t L, const uint64_t* batch_seeds, gx_samples* out) {
+    gx_ctx* ctx = g->ctx;
+    if (L > (uint32_t)kMaxLayers) fail(GX_INVALID_ARGUMENT, "at most 16 layers are supported");
+    if (S > kMaxBatchesPerLaunch)
+        fail(GX_INVALID_ARGUMENT, "at most 4096 batches per sampler launch");
+    uint64_t ns_max = 0, ns_total = batch_off[S];
+    for (uint64_t b = 0; b < S; ++b) ns_max = std::max(ns_max, batch_off[b + 1] - batch_off[b]);
+    const uint64_t N = g->n;
+    // capacities: ids per batch <= min(N, ns * prod(1+f)); edges per layer <= bound_F_l * f_l
+    uint64_t cap_ids = ns_max;
+    std::vector<uint64_t> boundF(L + 1);
+    boundF[0] = ns_max;
+    for (uint32_t l = 0; l < L; ++l)
+        boundF[l + 1] = std::min(std::max(N, ns_max),
+                                 boundF[l] + sat_mul(boundF[l], fanouts[l], 1ull << 40));
+    cap_ids = std::max<uint64_t>(boundF[L], 1);
+    cap_ids = (cap_ids + 3) & ~3ull;
+    out->ctx = ctx;
+    out->S = S;
+    out->L = L;
+    out->fanouts.assign(fanouts, fanouts + L);
+    out->cap_ids = cap_ids;
+    out->cap_e.assign(L, 0);
+    out->e_off.assign(L, 0);
+    uint64_t ce = 0, cap_draw = 1;
+    for (uint32_t l = 0; l < L; ++l) {
+        uint64_t c = sat_mul(std::min(boundF[l], cap_ids), fanouts[l], 1ull << 40);
+        if (c >= (1ull << 31)) fail(GX_INVALID_ARGUMENT, "batch too large: > 2^31 draws per layer");
+        out->e_off[l] = ce;
+        out->cap_e[l] = c;
+        ce += c;
+        cap_draw = std::max(cap_draw, c);
+    }
+    out->cap_e_batch = std::max<uint64_t>(ce, 1);
+    out->ids.reserve(S * cap_ids);
+    out->n_ids.reserve(S);
+    out->edges.reserve(S * out->cap_e_batch);
+    out->layer_count.reserve(std::max<uint64_t>(S * L, 1));
+
+    SampleScratch& ss = ctx->ss;
+    cudaStream_t st = ctx->stream;
+    ss.F.reserve(S);
+    ss.T.reserve(S);
+    ss.dbase.reserve(S);
+    ss.bseed.reserve(S);
+    ss.seed_off.reserve(S + 1);
+    ss.seeds32.reserve(std::max<uint64_t>(ns_total, 1));
+    ss.pscan.reserve(S * cap_ids);
+    ss.pdeg.reserve(S * cap_ids);
+    ss.plo.reserve(S * cap_ids);
+    ss.idslot.reserve(S * cap_ids);
+    const uint64_t max_tiles = S * ((std::max(cap_ids, cap_draw) + SB_TILE - 1) / SB_TILE) + 1;
+    ss.tsum.reserve(max_tiles);
+    ss.tsum2.reserve(max_tiles);
+    ss.dslot.reserve(S * cap_draw);
+    ss.drank.reserve(S * cap_draw);
+    uint64_t tab_cap = 1024;
+    while (tab_cap < 2 * cap_ids) tab_cap <<= 1;
+    if (tab_cap > (1ull << 31)) fail(GX_INVALID_ARGUMENT, "batch too large for the dedup table");
+    if (S * tab_cap > ss.tab_slots) {
+        for (int i = 0; i < 2; ++i) {
+            ss.tab[i].alloc(S * tab_cap);
+            GX_CUDA(cudaMemsetAsync(ss.tab[i].p, 0xff, ss.tab[i].bytes(), st));
+        }
+        ss.tab_slots = S * tab_cap;
+    }
+    ss.io.reserve(4);
+    GX_CUDA(cudaMemsetAsync(ss.io.p, 0, 4 * sizeof(unsigned long long), st));
+
+    // host -> device: seeds (u32), offsets, batch seeds
+    std::vector<uint32_t> s32(std::max<uint64_t>(ns_total, 1));
+    for (uint64_t i = 0; i < ns_total; ++i) s32[i] = (uint32_t)seeds_flat[i];
+    GX_CUDA(cudaMemcpyAsync(ss.seeds32.p, s32.data(), ns_total * 4, cudaMemcpyHostToDevice, st));
+    GX_CUDA(cudaMemcpyAsync(ss.seed_off.p, batch_off, (S + 1) * 8, cudaMemcpyHostToDevice, st));
+    GX_CUDA(cudaMemcpyAsync(ss.bseed.p, batch_seeds, S * 8, cudaMemcpyHostToDevice, st));
+
+    SampArgs a{};
+    a.indptr = g->indptr.p;
+    a.indices = g->indices.p;
+    a.N = N;
+    a.S = (uint32_t)S;
+    a.L = L;
+    for (uint32_t l = 0; l < L; ++l) {
+        a.fan[l] = fanouts[l];
+        a.e_off[l] = out->e_off[l];
+    }
+    a.bseed = ss.bseed.p;
+    a.seeds = ss.seeds32.p;
+    a.seed_off = ss.seed_off.p;
+    a.ids = out->ids.p;
+    a.cap_ids = cap_ids;
+    a.n_ids = out->n_ids.p;
+    a.edges = out->edges.p;
+    a.cap_e_batch = out->cap_e_batch;
+    a.layer_count = out->layer_count.p;
+    a.F = ss.F.p;
+    a.T = ss.T.p;
+    a.dbase = ss.dbase.p;
+    a.pscan = ss.pscan.p;
+    a.plo = ss.plo.p;
+    a.pdeg = ss.pdeg.p;
+    a.idslot = ss.idslot.p;
+    a.tsum = ss.tsum.p;
+    a.tsum2 = ss.tsum2.p;
+    a.dslot = ss.dslot.p;
+    a.drank = ss.drank.p;
+    a.cap_draw = cap_draw;
+    a.tab0 = ss.tab[0].p;
+    a.tab1 = ss.tab[1].p;
+    a.tab_cap = tab_cap;
+    a.io = ss.io.p;
+    a.bar = ctx->barrier.p;
+
+    const size_t smem = sizeof(SampSmem);
+    static int blocks_per_sm = -1;
+    if (blocks_per_sm < 0) {
+        GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_sample, SB_THREADS, smem));
+        if (blocks_per_sm < 1) fail(GX_CUDA_ERROR, "sampler kernel cannot be resident");
+    }
+    dim3 grid(ctx->num_sms * blocks_per_sm), block(SB_THREADS);
+    void* args[] = {&a};
+    GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
+    GX_CHECK_LAUNCH();
+}
+
+void samples_sync_host(gx_samples* s) {
+    cudaStream_t st = s->ctx->stream;
+    s->h_n_ids.resize(s->S);
+    s->h_layer_count.resize(s->S * s->L);
+    unsigned long long io[4];
+    GX_CUDA(cudaMemcpyAsync(s->h_n_ids.data(), s->n_ids.p, s->S * 4, cudaMemcpyDeviceToHost, st));
+    if (s->L)
+        GX_CUDA(cudaMemcpyAsync(s->h_layer_count.data(), s->layer_count.p, s->S * s->L * 4,
+                                cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(io, s->ctx->ss.io.p, 3 * 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaStreamSynchronize(st));
+    s->io.pages_read = io[0];
+    s->io.neighbor_lists_read = io[1];
+    s->io.bytes_read = io[2];
+    s->io.rows_read = 0;
+}
+
+// Host-side seed validation in the reference's order (sampler.hpp:72,80-85):
+// empty -> invalid_argument; per seed in order: >= N -> out_of_range,
+// already seen -> invalid_argument.
+static void validate_seeds(const uint64_t* seeds, uint64_t n, uint64_t N) {
+    if (n == 0) fail(GX_INVALID_ARGUMENT, "sample_batch: seeds are empty");
+    std::unordered_set<uint64_t> seen;
+    seen.reserve(n * 2);
+    for (uint64_t i = 0; i < n; ++i) {
+        if (seeds[i] >= N) fail(GX_OUT_OF_RANGE, "seed node out of range");
+        if (!seen.insert(seeds[i]).second) fail(GX_INVALID_ARGUMENT, "duplicate seed in batch");
+    }
+}
+
+}  // namespace gx
+
+using namespace gx;
+
+extern "C" {
+
+gx_status gx_sample_superbatch(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off,
+                               uint64_t n_batches, const uint32_t* fanouts, uint32_t n_layers,
+                               uint64_t global_seed, uint64_t first_global_batch, gx_samples** out,
+                               gx_iostats* io) {
+    return guard([&] {
+        if (!g || !out) fail(GX_INVALID_ARGUMENT, "null handle");
+        // superbatch_sample wraps any per-batch failure into runtime_error (sampler.hpp:236)
+        for (uint64_t b = 0; b < n_batches; ++b) {
+            try {
+                validate_seeds(seeds_flat + batch_off[b], batch_off[b + 1] - batch_off[b], g->n);
+            } catch (const Error& e) {
+                fail(GX_RUNTIME_ERROR, "superbatch sample failed: " + e.msg);
+            }
+        }
+        std::vector<uint64_t> bs(std::max<uint64_t>(n_batches, 1));
+        for (uint64_t i = 0; i < n_batches; ++i) bs[i] = derive_seed(global_seed, first_global_batch + i);
+        auto s = new gx_samples();
+        try {
+            s->h_n_seeds.resize(n_batches);
+            for (uint64_t b = 0; b < n_batches; ++b) s->h_n_seeds[b] = batch_off[b + 1] - batch_off[b];
+            if (n_batches) {
+                sample_run(g, seeds_flat, batch_off, n_batches, fanouts, n_layers, bs.data(), s);
+                samples_sync_host(s);
+            } else {
+                s->ctx = g->ctx;
+                s->L = n_layers;
+                s->fanouts.assign(fanouts, fanouts + n_layers);
+            }
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        if (io) {
+            io->pages_read += s->io.pages_read;
+            io->neighbor_lists_read += s->io.neighbor_lists_read;
+            io->bytes_read += s->io.bytes_read;
+        }
+        *out = s;
+    });
+}
+
+gx_status gx_sample_batch(gx_graph* g, const uint64_t* seeds, uint64_t n_seeds,
+                          const uint32_t* fanouts, uint32_t n_layers, uint64_t batch_seed,
+                          gx_samples** out, gx_iostats* io) {
+    return guard([&] {
+        if (!g || !out) fail(GX_INVALID_ARGUMENT, "null handle");
+        validate_seeds(seeds, n_seeds, g->n);
+        uint64_t off[2] = {0, n_seeds};
+        auto s = new gx_samples();
+        try {
+            s->h_n_seeds.assign(1, n_seeds);
+            sample_run(g, seeds, off, 1, fanouts, n_layers, &batch_seed, s);
+            samples_sync_host(s);
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        if (io) {
+            io->pages_read += s->io.pages_read;
+            io->neighbor_lists_read += s->io.neighbor_lists_read;
+            io->bytes_read += s->io.bytes_read;
+        }
+        *out = s;
+    });
+}
+
+void gx_samples_destroy(gx_samples* s) { delete s; }
+uint64_t gx_samples_num_batches(const gx_samples* s) { return s ? s->S : 0; }
+uint32_t gx_samples_num_layers(const gx_samples* s) { return s ? s->L : 0; }
+
+gx_status gx_samples_batch_info(const gx_samples* s, uint64_t b, uint64_t* n_ids, uint64_t* n_seeds,
+                                uint64_t* layer_counts) {
+    return guard([&] {
+        if (!s || b >= s->S) fail(GX_OUT_OF_RANGE, "batch index out of range");
+        if (n_ids) *n_ids = s->h_n_ids[b];
+        if (n_seeds) *n_seeds = s->h_n_seeds[b];
+        if (layer_counts)
+            for (uint32_t l = 0; l < s->L; ++l) layer_counts[l] = s->h_layer_count[b * s->L + l];
+    });
+}
+
+gx_status gx_samples_copy_ids(const gx_samples* s, uint64_t b, uint64_t* ids) {
+    return guard([&] {
+        if (!s || b >= s->S) fail(GX_OUT_OF_RANGE, "batch index out of range");
+        const uint64_t n = s->h_n_ids[b];
+        std::vector<uint32_t> tmp(n);
+        GX_CUDA(cudaMemcpy(tmp.data(), s->ids.p + b * s->cap_ids, n * 4, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < n; ++i) ids[i] = tmp[i];
+    });
+}
+
+gx_status gx_samples_copy_edges(const gx_samples* s, uint64_t b, uint32_t layer, uint32_t* pairs) {
+    return guard([&] {
+        if (!s || b >= s->S) fail(GX_OUT_OF_RANGE, "batch index out of range");
+        if (layer >= s->L) fail(GX_OUT_OF_RANGE, "layer index out of range");
+        const uint64_t n = s->h_layer_count[b * s->L + layer];
+        GX_CUDA(cudaMemcpy(pairs, s->edges.p + b * s->cap_e_batch + s->e_off[layer], n * 8,
+                           cudaMemcpyDeviceToHost));
+    });
+}
+
+uint64_t gx_samples_total_edges(const gx_samples* s) {
+    uint64_t t = 0;
+    if (s)
+        for (auto c : s->h_layer_count) t += c;
+    return t;
+}
+
+}  // extern "C"

@@ -1,0 +1,142 @@
+"""GPU parity: the HBM feature cache (executor.cu) vs the C oracle restatement
+of FeatureCache (feature_cache.hpp:19-130) and the reference's KATs
+(test_feature_cache.cpp); plus the fused pipeline end to end."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _feat(n, dim, seed, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    return rng.random((n, dim)).astype(dtype)
+
+
+def test_init_gather_kats(gx, oracle):
+    rows = _feat(20, 8, 1)
+    f = gx.FeatureFile.from_array(rows)
+    io = gx.IoStats()
+    c = gx.FeatureCache(f, [], 4, io)
+    assert not any(c.contains(v) for v in range(20)) and io.rows_read == 0
+    c = gx.FeatureCache(f, [4, 1, 2], 4, io)
+    assert c.contains(4) and c.contains(1) and c.contains(2) and not c.contains(0)
+    assert np.array_equal(c.cached_row(4), rows[4])
+    with pytest.raises(ValueError):
+        gx.FeatureCache(f, [0, 1, 2], 2)
+    with pytest.raises(ValueError):
+        gx.FeatureCache(f, [1, 1], 4)
+    with pytest.raises(IndexError):
+        gx.FeatureCache(f, [25], 4)
+    # straddling rows: 1200-byte rows, prefetch pages = per-row page sum
+    odd = gx.FeatureFile.from_array(_feat(40, 300, 2))
+    io = gx.IoStats()
+    gx.FeatureCache(odd, [0, 3, 17, 33, 39], 8, io)
+    assert io.pages_read == sum(oracle.page_count_for_row(1200, v) for v in [0, 3, 17, 33, 39])
+    assert io.rows_read == 5
+
+
+def test_gather_apply_kats(gx):
+    rows = _feat(10, 6, 3)
+    f = gx.FeatureFile.from_array(rows)
+    c = gx.FeatureCache(f, [0, 1, 4, 6, 7], 5)
+    ids = [0, 2, 5, 7]
+    io = gx.IoStats()
+    b, cnt = c.gather(f, ids, io)
+    assert (cnt.hits, cnt.misses, io.rows_read) == (2, 2, 2)
+    assert np.array_equal(b.numpy(), rows[ids])
+    b2, cnt2 = c.gather(f, [7, 4, 0], gx.IoStats())
+    assert cnt2.misses == 0
+    with pytest.raises(IndexError):
+        c.gather(f, [11])
+    # error paths (test_feature_cache.cpp:153-173), before any mutation
+    with pytest.raises(gx.LogicError):
+        c.apply_changeset(b, ids, gx.Changeset([0], [], [0]))
+    with pytest.raises(gx.LogicError):
+        c.apply_changeset(b, ids, gx.Changeset([], [5], []))
+    with pytest.raises(gx.LogicError):
+        c.apply_changeset(b, ids, gx.Changeset([5], [], [1]))
+    with pytest.raises(gx.LogicError):
+        c.apply_changeset(b, ids, gx.Changeset([2], [], [1]))
+    c.apply_changeset(b, ids, gx.Changeset([2, 5], [0, 6], [1, 2]))
+    assert not c.contains(0) and not c.contains(6)
+    assert np.array_equal(c.cached_row(2), rows[2]) and np.array_equal(c.cached_row(5), rows[5])
+    assert list(c.resident_set()) == [1, 2, 4, 5, 7]
+    # under-full cache draws slots from the free list
+    small = gx.FeatureCache(f, [], 3)
+    b3, _ = small.gather(f, [9, 3])
+    small.apply_changeset(b3, [9, 3], gx.Changeset([9], [], [0]))
+    assert small.contains(9) and np.array_equal(small.cached_row(9), rows[9])
+
+
+@pytest.mark.parametrize("dim,dtype", [(5, np.float32), (128, np.float32), (300, np.float32),
+                                       (64, np.float16), (768, np.float16)])
+def test_replay_matches_oracle(gx, oracle, dim, dtype):
+    """Live replay of simulated changesets (test_feature_cache.cpp:176-221,
+    acceptance c9): gathered bytes, counts, IoStats and slot layout all match."""
+    n = 400
+    rows = _feat(n, dim, 9, dtype)
+    f = gx.FeatureFile.from_array(rows)
+    rng = np.random.default_rng(41)
+    trace = [np.sort(rng.choice(n, size=int(rng.integers(1, 60)), replace=False)).astype(np.uint64)
+             for _ in range(25)]
+    for K in (2, 7, 20, 150):
+        init = oracle.compute_init_set(trace, K, n)
+        sim = oracle.simulate(trace, n, K, init)
+        c = gx.FeatureCache(f, init, K)
+        oc = oracle.cache(rows, init, K)
+        for i, ids in enumerate(trace):
+            io = gx.IoStats()
+            b, cnt = c.gather(f, ids, io)
+            ob, oh, om, oio = oc.gather(ids)
+            got = b.numpy()
+            assert got.tobytes() == ob.tobytes()
+            assert (cnt.hits, cnt.misses) == (oh, om) and om == int(sim["misses"][i])
+            assert (io.pages_read, io.rows_read, io.bytes_read) == (int(oio[0]), int(oio[1]), int(oio[3]))
+            a, z = int(sim["in_off"][i]), int(sim["in_off"][i + 1])
+            p, q = int(sim["out_off"][i]), int(sim["out_off"][i + 1])
+            cs = gx.Changeset(sim["in_ids"][a:z], sim["out_ids"][p:q], sim["in_pos"][a:z])
+            c.apply_changeset(b, ids, cs)
+            oc.apply(ob, ids, cs.in_ids, cs.in_positions, cs.out_ids)
+            assert np.array_equal(c.resident_set(), oc.resident())
+        for v in oc.resident():
+            assert c.cached_row(int(v)).tobytes() == rows[int(v)].tobytes()
+
+
+def test_host_backing_store(gx, oracle):
+    rows = _feat(1000, 64, 4)
+    f = gx.FeatureFile.from_array(rows, backing="host")
+    c = gx.FeatureCache(f, [1, 2, 3], 10)
+    b, cnt = c.gather(f, [5, 1, 999, 3])
+    assert np.array_equal(b.numpy(), rows[[5, 1, 999, 3]]) and cnt.misses == 2
+
+
+def test_pipeline_end_to_end(gx, oracle):
+    """sample -> inspect -> gather/apply on the device == oracle stages composed."""
+    n, dim = 30000, 32
+    ip, ind = oracle.rmat_graph(n, 8.0, 17)
+    g = gx.GraphFile.from_csc(ip, ind)
+    rows = oracle.features(n, dim, 99)
+    f = gx.FeatureFile.from_array(rows)
+    train = oracle.train_ids(n, 2, 0.1)
+    plan = oracle.plan_seed_batches(train, 100, oracle.epoch_seed(2, 0))[:12]
+    K = 3000
+    p = gx.Pipeline(g, f, [5, 5, 5], K, digest=True)
+    st = p.run_superbatch(plan, 2, 0)
+    trace = [oracle.sample_batch(ip, ind, b, [5, 5, 5], oracle.derive_seed(2, i))[0]
+             for i, b in enumerate(plan)]
+    init = oracle.compute_init_set(trace, K, n)
+    sim = oracle.simulate(trace, n, K, init)
+    assert np.array_equal(st.misses, sim["misses"])
+    assert st.total_misses == st.predicted_misses == int(sim["misses"].sum())
+    assert st.gathered_rows == sum(len(t) for t in trace)
+    # gathered bytes of every iteration, via the digest
+    dig = p.digests()
+    for i, ids in enumerate(trace):
+        assert int(dig[i]) == gx.batch_digest(rows[ids.astype(np.int64)])
+    # second superbatch on the same pipeline (buffers reused, tables clean)
+    plan2 = oracle.plan_seed_batches(train, 100, oracle.epoch_seed(2, 0))[12:20]
+    st2 = p.run_superbatch(plan2, 2, 12)
+    trace2 = [oracle.sample_batch(ip, ind, b, [5, 5, 5], oracle.derive_seed(2, 12 + i))[0]
+              for i, b in enumerate(plan2)]
+    init2 = oracle.compute_init_set(trace2, K, n)
+    assert np.array_equal(st2.misses, oracle.simulate(trace2, n, K, init2)["misses"])
