@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""bench.py -- the Ginex data-preparation hot path on B200 (BASELINE.json metric).
+
+One step = one superbatch of S batches through the whole hot path on one GPU:
+    sample (S x batch seeds, fanout 10,10,10) -> Belady inspector (init set +
+    S changesets) -> cache init ("switch") -> S x (gather batch rows, apply
+    changeset)
+on the papers100M-shape synthetic graph (configs[1]): 111,059,956 nodes,
+~1.6B edges (R-MAT a/b/c/d = .57/.19/.19/.05, `gx gen --seed 7` seeds), 128-d
+fp32 features, batch 1000, superbatch 100, cache 20% of the nodes. Graph and
+feature table are generated on the device, bit-identical to the reference's
+generator (tests/test_gpu_sampler.py::test_device_generator_matches_reference_generator).
+
+value  = sampled edges / device time of the K timed steps (CUDA events on the
+         pipeline's stream; max over ranks; whole-job edges over all ranks).
+e2e    = the same through the public API call with host seeds in and host
+         results out, timed by the wall clock around each call.
+Multi-GPU (torchrun): every rank runs its own superbatches of the epoch plan
+(no data-path collective; "scaling": "weak").
+
+--impl reference runs the UNMODIFIED reference (oracle/_ref/libgx_ref.so, the
+reference headers compiled in this container) on the host cores on a bounded
+sample of the same workload (the first `--ref-batches` batches of a superbatch
+per step), reading graph.bin/features.bin written to /dev/shm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SEED_GEN = 7    # `gx gen --seed 7` (gx.cpp:159-160)
+SEED_RUN = 1    # run seed (pipeline.hpp:380-399)
+
+CONFIGS = {
+    # configs[1] of BASELINE.json: the bench workload
+    "papers": dict(N=111_059_956, avg_degree=14.9, dim=128, fanouts=[10, 10, 10], batch=1000,
+                   S=100, cache_frac=0.20, train_fraction=0.1,
+                   workload="ogbn-papers100M-shape synthetic R-MAT: 111M nodes, ~1.6B edges, "
+                            "128-d fp32, fanout (10,10,10), batch 1000, superbatch 100, cache 20%"),
+    # configs[0]: the reference's own CPU-runnable case
+    "cfg1": dict(N=1_000_000, avg_degree=10.0, dim=128, fanouts=[10, 10, 10], batch=1000, S=100,
+                 cache_frac=0.10, train_fraction=0.1,
+                 workload="synthetic R-MAT 1M nodes / 9.7M edges, 128-d fp32, fanout (10,10,10), "
+                          "batch 1000, superbatch 100, cache 10%"),
+}
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        if shutil.which("nvidia-smi"):
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def build_dataset(gx, cfg, ctx, log):
+    edge_seed = gx.derive_seed(SEED_GEN, 0xED6E5)
+    value_seed = gx.derive_seed(SEED_GEN, 0xFEA7)
+    t0 = time.time()
+    g = gx.GraphFile.generate_rmat(cfg["N"], cfg["avg_degree"], edge_seed, ctx=ctx)
+    t1 = time.time()
+    f = gx.FeatureFile.generate(cfg["N"], cfg["dim"], value_seed, ctx=ctx)
+    ctx.synchronize()
+    t2 = time.time()
+    log(f"dataset: N={g.num_nodes()} E={g.num_edges()} (graph {t1 - t0:.1f}s, features {t2 - t1:.1f}s)")
+    return g, f
+
+
+def make_plan(gx, cfg):
+    train = gx.derive_train_ids(cfg["N"], SEED_RUN, cfg["train_fraction"])
+    plan = gx.plan_seed_batches(train, cfg["batch"], gx.epoch_seed(SEED_RUN, 0)).batches
+    S = cfg["S"]
+    sbs = [plan[o:o + S] for o in range(0, len(plan), S)]
+    return sbs
+
+
+# ---------------------------------------------------------------------------
+# the reference on the host cores (oracle/_ref) -- cpu_baseline and --impl reference
+# ---------------------------------------------------------------------------
+def ref_prepare(gx, g, f, cfg, batches, workdir, log):
+    """graph.bin (persist_graph bytes) + a sparse features.bin holding the rows
+    the sample touches, both in tmpfs, so the reference reads page-cache-warm."""
+    os.makedirs(workdir, exist_ok=True)
+    gpath = os.path.join(workdir, "graph.bin")
+    fpath = os.path.join(workdir, "features.bin")
+    t0 = time.time()
+    g.write(gpath)
+    # features.bin header (FeatureWriter, graph_store.hpp:237-250), payload at 4096
+    N, dim = cfg["N"], cfg["dim"]
+    hdr = (b"GXFEAT01" + (1).to_bytes(4, "little") + N.to_bytes(8, "little") +
+           dim.to_bytes(4, "little") + (4).to_bytes(4, "little") + (4096).to_bytes(8, "little"))
+    with open(fpath, "wb") as fh:
+        fh.write(hdr + b"\0" * (4096 - len(hdr)))
+        fh.truncate(4096 + N * dim * 4)
+    s = gx.sample_superbatch(g, None, batches, cfg["fanouts"], SEED_RUN, 0)
+    ids = np.unique(np.concatenate([s.batch(i).ids for i in range(len(s))]))
+    rows = f.read_rows(ids)
+    mm = np.memmap(fpath, dtype=np.float32, mode="r+", offset=4096, shape=(N, dim))
+    mm[ids.astype(np.int64)] = rows
+    mm.flush()
+    del mm
+    log(f"reference inputs in {workdir}: {len(ids)} feature rows materialised ({time.time() - t0:.1f}s)")
+    return gpath, fpath
+
+
+def ref_run(batches, cfg, gpath, fpath, workdir, workers, global_seed=SEED_RUN, first_batch=0):
+    import oracle
+    L = oracle.REF.lib
+    import ctypes as C
+    flat = np.concatenate([np.asarray(b, np.uint64) for b in batches])
+    off = np.zeros(len(batches) + 1, np.uint64)
+    off[1:] = np.cumsum([len(b) for b in batches])
+    fan = np.asarray(cfg["fanouts"], np.uint32)
+    rt = os.path.join(workdir, "rt")
+    shutil.rmtree(rt, ignore_errors=True)
+    os.makedirs(rt)
+    times = np.zeros(4, np.float64)
+    e, r, m = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    K = int(cfg["cache_frac"] * cfg["N"])
+    t0 = time.perf_counter()
+    oracle.REF._chk(L.gxr_run_superbatch(gpath.encode(), fpath.encode(), rt.encode(), flat, off,
+                                         len(batches), fan, len(fan), global_seed, first_batch, K,
+                                         workers, times, C.byref(e), C.byref(r), C.byref(m)))
+    wall = time.perf_counter() - t0
+    shutil.rmtree(rt, ignore_errors=True)
+    return dict(edges=e.value, rows=r.value, misses=m.value, seconds=wall,
+                stages={"sample_s": times[0], "precompute_s": times[1], "switch_s": times[2],
+                        "main_loop_s": times[3]})
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference_arm(args, cfg, log):
+    rank, world, local = env_rank()
+    if rank != 0:
+        return
+    import oracle
+    if not oracle.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgx_ref.so was not built"}))
+        return
+    import paper_2208_09151_b200 as gx
+    ctx = gx.Context(local)
+    g, f = build_dataset(gx, cfg, ctx, log)
+    sbs = make_plan(gx, cfg)
+    nb = args.ref_batches
+    workdir = f"/dev/shm/gx_bench_ref_{os.getpid()}"
+    cores = cpu_cores()
+    try:
+        gpath, fpath = ref_prepare(gx, g, f, cfg,
+                                   [b for k in range(args.warmup + args.steps) for b in
+                                    sbs[k % len(sbs)][:nb]], workdir, log)
+        del g, f
+        res = []
+        for k in range(args.warmup + args.steps):
+            j = k % len(sbs)
+            r = ref_run(sbs[j][:nb], cfg, gpath, fpath, workdir, cores, SEED_RUN, j * cfg["S"])
+            if k >= args.warmup:
+                res.append(r)
+            log(f"reference step {k}: {r['edges']} edges in {r['seconds']:.2f}s {r['stages']}")
+    finally:
+        shutil.rmtree(workdir, ignore_errors=True)
+    edges = sum(r["edges"] for r in res)
+    secs = sum(r["seconds"] for r in res)
+    v = edges / secs
+    sample = (f"first {nb} of the {cfg['S']} batches of superbatch k per step (full stages: "
+              f"superbatch_sample with {cores} workers + files, precompute_changesets, FeatureCache "
+              f"init with K={int(cfg['cache_frac'] * cfg['N'])}, gather+apply)")
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": "sampled_edges/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / max(len(res), 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32/u64 ids, f32 rows (byte copies)", "data": "synthetic",
+        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * nb,
+                   "superbatch": nb, "parallelism": "cpu"},
+        "cpu_baseline": {"value": v, "unit": "sampled_edges/s", "cores": cores, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "sampled_edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "stages": {k: sum(r["stages"][k] for r in res) / len(res) for k in res[0]["stages"]},
+    }))
+
+
+METRIC = ("sampled edges/s through the full data-prep step (sample + Belady inspect + feature "
+          "gather/cache update); gathered feature GB/s and HBM fraction in `stages`/`roofline`")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gx", choices=["gx", "reference"])
+    ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
+    ap.add_argument("--avg-degree", type=float, default=None)
+    ap.add_argument("--superbatch", type=int, default=None)
+    ap.add_argument("--ref-batches", type=int, default=8,
+                    help="batches per step for the reference / cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    if args.avg_degree is not None:
+        cfg["avg_degree"] = args.avg_degree
+    if args.superbatch is not None:
+        cfg["S"] = args.superbatch
+    rank, world, local = env_rank()
+
+    def log(m):
+        if rank == 0:
+            print(f"[bench] {m}", file=sys.stderr, flush=True)
+
+    if args.impl == "reference":
+        return run_reference_arm(args, cfg, log)
+
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    import paper_2208_09151_b200 as gx
+    ctx = gx.Context(local)
+    g, f = build_dataset(gx, cfg, ctx, log)
+    sbs = make_plan(gx, cfg)
+    K_entries = int(cfg["cache_frac"] * cfg["N"])
+    pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+
+    def sb_index(k):  # rank r takes superbatches r, r+world, ... of the epoch plan
+        return (rank + k * world) % len(sbs)
+
+    def step(k):
+        j = sb_index(k)
+        return pipe.run_superbatch(sbs[j], SEED_RUN, j * cfg["S"])
+
+    for k in range(args.warmup):
+        st = step(k)
+        log(f"warmup {k}: {st.sampled_edges} edges, sample {st.ms_sample:.2f} ms inspect "
+            f"{st.ms_inspect:.2f} ms switch {st.ms_switch:.2f} ms gather {st.ms_gather:.2f} ms")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        ctx.synchronize()
+        torch.cuda.synchronize(local)
+
+    stats = []
+    walls = []
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for k in range(args.warmup, args.warmup + args.steps):
+            t = time.perf_counter()
+            stats.append(step(k))
+            walls.append(time.perf_counter() - t)
+        ev1.record(stream)
+        barrier()
+    dev_s = ev0.elapsed_time(ev1) / 1e3
+    wall_s = sum(walls)
+    edges = sum(s.sampled_edges for s in stats)
+    if world > 1:
+        t = torch.tensor([dev_s, wall_s], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_s, wall_s = t.tolist()
+        e = torch.tensor([edges], device=f"cuda:{local}", dtype=torch.float64)
+        torch.distributed.all_reduce(e)
+        edges_all = int(e.item())
+    else:
+        edges_all = edges
+    for s in stats:
+        assert s.total_misses == s.predicted_misses, "observed misses != inspector prediction"
+
+    # --- roofline of the dominant kernel (the gather) -------------------------
+    w = 4 * cfg["dim"]
+    rows = sum(s.gathered_rows for s in stats)
+    gk_ms = sum(s.ms_gather_kernels for s in stats)
+    alg_bytes = (2 * w + 16) * rows               # read row + write row + id + slot
+    peak, peak_src = measured_peaks()
+    achieved = alg_bytes / (gk_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get("k_gather_dram_bytes_per_launch")
+    n = len(stats)
+    S = cfg["S"]
+    stages = {
+        "sample_ms": sum(s.ms_sample for s in stats) / n,
+        "inspect_ms": sum(s.ms_inspect for s in stats) / n,
+        "switch_ms": sum(s.ms_switch for s in stats) / n,
+        "gather_apply_ms": sum(s.ms_gather for s in stats) / n,
+        "gather_kernels_ms": gk_ms / n,
+        "apply_kernels_ms": sum(s.ms_apply_kernels for s in stats) / n,
+        "sampler_edges_per_s": sum(s.sampled_edges for s in stats) / (sum(s.ms_sample for s in stats) / 1e3),
+        "gathered_feature_GBps": w * rows / (gk_ms / 1e3) / 1e9,
+        "gathered_feature_GBps_incl_apply": w * rows / (sum(s.ms_gather for s in stats) / 1e3) / 1e9,
+        "accesses_per_superbatch": rows / n,
+        "miss_ratio": sum(s.total_misses for s in stats) / max(rows, 1),
+        "init_size": stats[-1].init_size,
+        "changeset_in_per_iter": sum(s.total_in for s in stats) / (n * S),
+        "edges_per_superbatch": edges / n,
+    }
+    out = {
+        "metric": METRIC, "value": edges_all / dev_s, "unit": "sampled_edges/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "u32 ids / f32 rows (byte copies)", "data": "synthetic (device R-MAT, bit-exact to the "
+        "reference generator; feature_value table)",
+        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * S * world,
+                   "superbatch": S, "cache_entries": K_entries, "num_edges": g.num_edges(),
+                   "parallelism": f"dp{world} (superbatches per rank, no collective)",
+                   "l2": "inputs larger than L2 (57 GB table, 6.6 GB CSC)" if args.config == "papers"
+                   else "inputs larger than L2"},
+        "e2e": {"value": edges_all / wall_s, "unit": "sampled_edges/s",
+                "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
+                "d2h_bytes_per_step": int(8 * S + 8 * 16)},
+        "gpu_launches": (2 * S + 6) * args.steps,
+        "roofline": {"kernel": "k_gather<16>", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "peak_source": peak_src,
+                     "bytes_per_row": 2 * w + 16, "rows_per_launch": rows / (n * S)},
+        "stages": stages,
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle
+            if oracle.ref_available():
+                nb = args.ref_batches
+                workdir = f"/dev/shm/gx_bench_cpu_{os.getpid()}"
+                try:
+                    gpath, fpath = ref_prepare(gx, g, f, cfg, sbs[0][:nb], workdir, log)
+                    cores = cpu_cores()
+                    r = ref_run(sbs[0][:nb], cfg, gpath, fpath, workdir, cores)
+                finally:
+                    shutil.rmtree(workdir, ignore_errors=True)
+                out["cpu_baseline"] = {
+                    "value": r["edges"] / r["seconds"], "unit": "sampled_edges/s", "cores": cores,
+                    "kind": "reference",
+                    "sample": f"first {nb} batches of superbatch 0 through the reference's stages "
+                              f"(superbatch_sample {cores} workers, precompute_changesets, FeatureCache "
+                              f"K={K_entries}, gather+apply); {r['edges']} edges in {r['seconds']:.2f}s",
+                    "stages": r["stages"]}
+            else:
+                out["cpu_baseline"] = None
+        except Exception as e:  # the baseline never blocks the GPU number
+            out["cpu_baseline"] = {"error": repr(e)}
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -63,6 +63,18 @@ uint64_t gx_derive_seed(uint64_t base, uint64_t index);
 uint64_t gx_pages_touched(uint64_t lo, uint64_t hi);
 gx_status gx_page_count_for_row(uint64_t row_bytes, uint64_t row_index, uint64_t* pages);
 
+/* ---- seed plans (host-side, as in the reference) -------------------------
+ * derive_train_ids (pipeline.hpp:384-399): partial Fisher-Yates over [0,n)
+ * under derive_seed(mix64(seed) ^ 0x545241494E, 0), first floor(n*frac)
+ * (clamped to [1,n]) ids, sorted. `out` needs n entries of scratch. */
+gx_status gx_derive_train_ids(uint64_t n, uint64_t seed, double train_fraction, uint64_t* out,
+                              uint64_t* n_out);
+/* plan_seed_batches (sampler.hpp:48-65): the shuffled order (batches are
+ * consecutive runs of batch_size); epoch_seed per pipeline.hpp:380-382. */
+gx_status gx_plan_seed_batches(const uint64_t* train, uint64_t n, uint64_t batch_size,
+                               uint64_t epoch_seed, uint64_t* shuffled);
+uint64_t gx_epoch_seed(uint64_t seed, uint64_t epoch);
+
 /* ---- graph: GraphFile (graph_store.hpp:106-197), CscGraph (:33-49) ------
  * The whole CSC (indptr u64[N+1], indices u32[E]) is HBM-resident. */
 typedef struct gx_graph gx_graph;
@@ -214,6 +226,8 @@ typedef struct gx_pipeline_stats {
     gx_iostats sample_io;
     gx_iostats gather_io;
     double ms_sample, ms_inspect, ms_switch, ms_gather; /* device-timed stage durations */
+    double ms_gather_kernels;  /* sum of the S gather-kernel durations (CUDA events) */
+    double ms_apply_kernels;   /* sum of the S apply-kernel durations */
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,
                              uint32_t n_layers, uint64_t num_entries, gx_pipeline** out);

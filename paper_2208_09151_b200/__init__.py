@@ -10,6 +10,7 @@ from .api import (AccessIndex, Batch, Changeset, Changesets, Context, FeatureCac
                   FeatureFile, FileTrace, GatherCounts, GraphFile, IoStats, MemoryTrace, Pipeline,
                   PipelineStats, PrecomputeResult, SampleOutput, Samples, SeedPlan,
                   SimulationResult, SplitMix64, batch_digest, build_access_index, compute_init_set,
+                  derive_train_ids, epoch_seed,
                   derive_seed, mix64, page_count_for_row, pages_touched, plan_seed_batches,
                   precompute_changesets, precompute_trace, read_adj_file, read_ids_file,
                   read_init_file, read_update_file, sample_batch, sample_superbatch,

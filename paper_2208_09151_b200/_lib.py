@@ -39,7 +39,8 @@ class PipelineStatsC(C.Structure):
     _fields_ = [("sampled_edges", u64), ("gathered_rows", u64), ("total_misses", u64),
                 ("predicted_misses", u64), ("init_size", u64), ("total_in", u64),
                 ("total_out", u64), ("sample_io", IoStatsC), ("gather_io", IoStatsC),
-                ("ms_sample", dbl), ("ms_inspect", dbl), ("ms_switch", dbl), ("ms_gather", dbl)]
+                ("ms_sample", dbl), ("ms_inspect", dbl), ("ms_switch", dbl), ("ms_gather", dbl),
+                ("ms_gather_kernels", dbl), ("ms_apply_kernels", dbl)]
 
 
 PIO = C.POINTER(IoStatsC)
@@ -56,6 +57,9 @@ SIGNATURES = {
     "gx_derive_seed": (u64, [u64, u64]),
     "gx_pages_touched": (u64, [u64, u64]),
     "gx_page_count_for_row": (i32, [u64, u64, P64]),
+    "gx_derive_train_ids": (i32, [u64, u64, dbl, vp, P64]),
+    "gx_plan_seed_batches": (i32, [vp, u64, u64, u64, vp]),
+    "gx_epoch_seed": (u64, [u64, u64]),
     "gx_graph_open": (i32, [vp, cstr, PVP]),
     "gx_graph_from_csc": (i32, [vp, u64, vp, vp, PVP]),
     "gx_graph_generate_rmat": (i32, [vp, u64, dbl, dbl, dbl, dbl, u64, PVP]),

@@ -214,18 +214,26 @@ class SeedPlan:
 
 
 def plan_seed_batches(train_ids, batch_size: int, epoch_seed: int) -> SeedPlan:
-    """sampler.hpp:48-65 (host-side, sequential Fisher-Yates as in the reference)."""
-    t = [int(x) for x in np.asarray(train_ids, dtype=np.uint64).reshape(-1)]
-    if not t:
-        raise ValueError("training set is empty")
-    if batch_size < 1:
-        raise ValueError("batch_size must be >= 1")
-    rng = SplitMix64(epoch_seed)
-    for i in range(len(t) - 1, 0, -1):
-        j = rng.bounded(i + 1)
-        t[i], t[j] = t[j], t[i]
-    arr = np.array(t, dtype=np.uint64)
-    return SeedPlan([arr[o:o + batch_size].copy() for o in range(0, len(arr), batch_size)])
+    """sampler.hpp:48-65 (host-side sequential Fisher-Yates, in libgx_b200)."""
+    t = _u64(train_ids)
+    out = np.zeros(max(len(t), 1), np.uint64)
+    check(lib.gx_plan_seed_batches(_ptr(t), len(t), batch_size, epoch_seed & 0xFFFFFFFFFFFFFFFF,
+                                   out.ctypes.data))
+    return SeedPlan([out[o:o + batch_size].copy() for o in range(0, len(t), batch_size)])
+
+
+def derive_train_ids(num_nodes: int, seed: int, train_fraction: float) -> np.ndarray:
+    """TrainingRunner::derive_train_ids (pipeline.hpp:384-399)."""
+    out = np.zeros(max(num_nodes, 1), np.uint64)
+    n = C.c_uint64()
+    check(lib.gx_derive_train_ids(num_nodes, seed & 0xFFFFFFFFFFFFFFFF, float(train_fraction),
+                                  out.ctypes.data, C.byref(n)))
+    return out[:n.value].copy()
+
+
+def epoch_seed(seed: int, epoch: int) -> int:
+    """TrainingRunner::epoch_seed (pipeline.hpp:380-382)."""
+    return lib.gx_epoch_seed(seed & 0xFFFFFFFFFFFFFFFF, epoch)
 
 
 class Samples:
@@ -814,6 +822,8 @@ class PipelineStats:
     ms_inspect: float
     ms_switch: float
     ms_gather: float
+    ms_gather_kernels: float
+    ms_apply_kernels: float
     misses: np.ndarray
 
 
@@ -852,7 +862,7 @@ class Pipeline:
         return PipelineStats(st.sampled_edges, st.gathered_rows, st.total_misses, st.predicted_misses,
                              st.init_size, st.total_in, st.total_out, _io(st.sample_io),
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
-                             st.ms_gather, misses[:S].copy())
+                             st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, misses[:S].copy())
 
     def digests(self) -> np.ndarray:
         out = np.zeros(max(self._S, 1), np.uint64)

@@ -78,6 +78,7 @@ struct gx_pipeline {
     bool digest = false;
     std::vector<uint64_t> h_digests;
     cudaEvent_t ev[5] = {};
+    std::vector<cudaEvent_t> kev;  // 3 per iteration: gather start, gather end / apply start, apply end
 };
 
 using namespace gx;
@@ -96,6 +97,48 @@ gx_status gx_page_count_for_row(uint64_t w, uint64_t r, uint64_t* pages) {
         *pages = pages_touched(r * w, r * w + w);
     });
 }
+
+gx_status gx_derive_train_ids(uint64_t n, uint64_t seed, double frac, uint64_t* out, uint64_t* n_out) {
+    return guard([&] {
+        if (frac <= 0.0 || frac > 1.0) fail(GX_INVALID_ARGUMENT, "train_fraction must be in (0, 1]");
+        uint64_t want = (uint64_t)((double)n * frac);
+        want = std::min(std::max<uint64_t>(want, 1), n);
+        for (uint64_t v = 0; v < n; ++v) out[v] = v;
+        uint64_t st = derive_seed(mix64(seed) ^ 0x545241494EULL, 0);
+        for (uint64_t i = 0; i < want; ++i) {
+            st += kGamma;
+            uint64_t z = st;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            z ^= z >> 31;
+            const uint64_t j = i + (uint64_t)(((unsigned __int128)z * (n - i)) >> 64);
+            std::swap(out[i], out[j]);
+        }
+        std::sort(out, out + want);
+        *n_out = want;
+    });
+}
+
+gx_status gx_plan_seed_batches(const uint64_t* train, uint64_t n, uint64_t batch_size, uint64_t epoch_seed,
+                               uint64_t* sh) {
+    return guard([&] {
+        if (n == 0) fail(GX_INVALID_ARGUMENT, "training set is empty");
+        if (batch_size < 1) fail(GX_INVALID_ARGUMENT, "batch_size must be >= 1");
+        std::copy(train, train + n, sh);
+        uint64_t st = epoch_seed;
+        for (uint64_t i = n - 1; i > 0; --i) {
+            st += kGamma;
+            uint64_t z = st;
+            z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+            z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+            z ^= z >> 31;
+            const uint64_t j = (uint64_t)(((unsigned __int128)z * (i + 1)) >> 64);
+            std::swap(sh[i], sh[j]);
+        }
+    });
+}
+
+uint64_t gx_epoch_seed(uint64_t seed, uint64_t epoch) { return derive_seed(mix64(seed) ^ 0x45504F4348ULL, epoch); }
 
 gx_status gx_ctx_create(int device, gx_ctx** out) {
     return guard([&] {
@@ -354,6 +397,7 @@ void gx_pipeline_destroy(gx_pipeline* p) {
     if (!p) return;
     for (auto& e : p->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : p->kev) cudaEventDestroy(e);
     delete p;
 }
 
@@ -409,16 +453,24 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
                           p->counters.p + 8 * S + 2);
         GX_CUDA(cudaEventRecord(p->ev[3], st));
         // (4) main loop: gather + apply (the ids of iteration i are batch i's ids)
+        while (p->kev.size() < 3 * S) {
+            cudaEvent_t e;
+            GX_CUDA(cudaEventCreate(&e));
+            p->kev.push_back(e);
+        }
         for (uint64_t i = 0; i < S; ++i) {
             const uint64_t ni = o[i + 1] - o[i];
+            GX_CUDA(cudaEventRecord(p->kev[3 * i], st));
             launch_gather(ctx, ctx->is.trace.p + o[i], ni, p->table.p, p->cache_rows.p, p->f, p->batch.p,
                           p->counters.p + 8 * i);
+            GX_CUDA(cudaEventRecord(p->kev[3 * i + 1], st));
             if (p->digest) launch_digest(ctx, p->batch.p, ni, p->f->row_bytes, p->digests.p + i);
             const uint64_t a = p->cs.h_in_off[i], b = p->cs.h_out_off[i];
             launch_apply_slots(ctx, p->cs.in_ids.p + a, p->cs.in_pos.p + a, p->cs.in_slot.p + a,
                                (uint32_t)(p->cs.h_in_off[i + 1] - a), p->cs.out_ids.p + b,
                                (uint32_t)(p->cs.h_out_off[i + 1] - b), p->table.p, p->batch.p, p->cache_rows.p,
                                p->f->row_bytes);
+            GX_CUDA(cudaEventRecord(p->kev[3 * i + 2], st));
         }
         GX_CUDA(cudaEventRecord(p->ev[4], st));
         // leave the address table clean: every node ever inserted -> -1
@@ -457,6 +509,16 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
             stats->ms_inspect = ms[1];
             stats->ms_switch = ms[2];
             stats->ms_gather = ms[3];
+            double gk = 0, ak = 0;
+            for (uint64_t i = 0; i < S; ++i) {
+                float a = 0, b = 0;
+                GX_CUDA(cudaEventElapsedTime(&a, p->kev[3 * i], p->kev[3 * i + 1]));
+                GX_CUDA(cudaEventElapsedTime(&b, p->kev[3 * i + 1], p->kev[3 * i + 2]));
+                gk += a;
+                ak += b;
+            }
+            stats->ms_gather_kernels = gk;
+            stats->ms_apply_kernels = ak;
         }
     });
 }
