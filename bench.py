@@ -45,7 +45,8 @@ SEED_RUN = 1    # run seed (pipeline.hpp:380-399)
 
 CONFIGS = {
     # configs[1] of BASELINE.json: the bench workload
-    "papers": dict(N=111_059_956, avg_degree=14.9, dim=128, fanouts=[10, 10, 10], batch=1000,
+    # avg_degree 14.67 pre-dedup -> 1.615B edges after dedup (ogbn-papers100M: 1,615,685,872)
+    "papers": dict(N=111_059_956, avg_degree=14.67, dim=128, fanouts=[10, 10, 10], batch=1000,
                    S=100, cache_frac=0.20, train_fraction=0.1,
                    workload="ogbn-papers100M-shape synthetic R-MAT: 111M nodes, ~1.6B edges, "
                             "128-d fp32, fanout (10,10,10), batch 1000, superbatch 100, cache 20%"),
@@ -143,9 +144,10 @@ def make_plan(gx, cfg):
 # ---------------------------------------------------------------------------
 # the reference on the host cores (oracle/_ref) -- cpu_baseline and --impl reference
 # ---------------------------------------------------------------------------
-def ref_prepare(gx, g, f, cfg, batches, workdir, log):
+def ref_prepare(gx, g, f, cfg, samples, workdir, log):
     """graph.bin (persist_graph bytes) + a sparse features.bin holding the rows
-    the sample touches, both in tmpfs, so the reference reads page-cache-warm."""
+    the sample touches, both in tmpfs, so the reference reads page-cache-warm.
+    samples = [(batches, first_global_batch), ...] exactly as the reference runs them."""
     os.makedirs(workdir, exist_ok=True)
     gpath = os.path.join(workdir, "graph.bin")
     fpath = os.path.join(workdir, "features.bin")
@@ -158,8 +160,11 @@ def ref_prepare(gx, g, f, cfg, batches, workdir, log):
     with open(fpath, "wb") as fh:
         fh.write(hdr + b"\0" * (4096 - len(hdr)))
         fh.truncate(4096 + N * dim * 4)
-    s = gx.sample_superbatch(g, None, batches, cfg["fanouts"], SEED_RUN, 0)
-    ids = np.unique(np.concatenate([s.batch(i).ids for i in range(len(s))]))
+    touched = []
+    for batches, first in samples:
+        s = gx.sample_superbatch(g, None, batches, cfg["fanouts"], SEED_RUN, first)
+        touched += [s.batch(i).ids for i in range(len(s))]
+    ids = np.unique(np.concatenate(touched))
     rows = f.read_rows(ids)
     mm = np.memmap(fpath, dtype=np.float32, mode="r+", offset=4096, shape=(N, dim))
     mm[ids.astype(np.int64)] = rows
@@ -218,8 +223,8 @@ def run_reference_arm(args, cfg, log):
     cores = cpu_cores()
     try:
         gpath, fpath = ref_prepare(gx, g, f, cfg,
-                                   [b for k in range(args.warmup + args.steps) for b in
-                                    sbs[k % len(sbs)][:nb]], workdir, log)
+                                   [(sbs[k % len(sbs)][:nb], (k % len(sbs)) * cfg["S"])
+                                    for k in range(args.warmup + args.steps)], workdir, log)
         del g, f
         res = []
         for k in range(args.warmup + args.steps):
@@ -263,7 +268,7 @@ def main():
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--avg-degree", type=float, default=None)
     ap.add_argument("--superbatch", type=int, default=None)
-    ap.add_argument("--ref-batches", type=int, default=8,
+    ap.add_argument("--ref-batches", type=int, default=16,
                     help="batches per step for the reference / cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -384,7 +389,7 @@ def main():
         "e2e": {"value": edges_all / wall_s, "unit": "sampled_edges/s",
                 "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
                 "d2h_bytes_per_step": int(8 * S + 8 * 16)},
-        "gpu_launches": (2 * S + 6) * args.steps,
+        "gpu_launches": (2 * S + 4) * args.steps,
         "roofline": {"kernel": "k_gather<16>", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
@@ -399,7 +404,7 @@ def main():
                 nb = args.ref_batches
                 workdir = f"/dev/shm/gx_bench_cpu_{os.getpid()}"
                 try:
-                    gpath, fpath = ref_prepare(gx, g, f, cfg, sbs[0][:nb], workdir, log)
+                    gpath, fpath = ref_prepare(gx, g, f, cfg, [(sbs[0][:nb], 0)], workdir, log)
                     cores = cpu_cores()
                     r = ref_run(sbs[0][:nb], cfg, gpath, fpath, workdir, cores)
                 finally:

@@ -71,7 +71,6 @@ struct gx_pipeline {
     gx_samples samples;
     gx_changesets cs;
     gx::DevBuf<uint8_t> cache_rows;
-    gx::DevBuf<int32_t> table;
     gx::DevBuf<uint8_t> batch;
     gx::DevBuf<unsigned long long> counters;  // per iteration 8 words
     gx::DevBuf<unsigned long long> digests;
@@ -382,8 +381,6 @@ gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanout
             p->fanouts.assign(fanouts, fanouts + L);
             p->K = K;
             p->cache_rows.alloc(std::max<uint64_t>(K * f->row_bytes, 16));
-            p->table.alloc(std::max<uint64_t>(g->n, 1));
-            GX_CUDA(cudaMemset(p->table.p, 0xff, std::max<uint64_t>(g->n, 1) * 4));
             for (auto& e : p->ev) GX_CUDA(cudaEventCreate(&e));
         } catch (...) {
             delete p;
@@ -449,7 +446,9 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
             p->digests.reserve(S);
             GX_CUDA(cudaMemsetAsync(p->digests.p, 0, S * 8, st));
         }
-        launch_cache_init(ctx, p->cs.init.p, (uint32_t)p->cs.n_init, p->table.p, p->f, p->cache_rows.p,
+        // the inspector resolved every access's serving slot (is.acc_slot), so
+        // the executor needs no address table on this path
+        launch_cache_init(ctx, p->cs.init.p, (uint32_t)p->cs.n_init, nullptr, p->f, p->cache_rows.p,
                           p->counters.p + 8 * S + 2);
         GX_CUDA(cudaEventRecord(p->ev[3], st));
         // (4) main loop: gather + apply (the ids of iteration i are batch i's ids)
@@ -461,21 +460,18 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
         for (uint64_t i = 0; i < S; ++i) {
             const uint64_t ni = o[i + 1] - o[i];
             GX_CUDA(cudaEventRecord(p->kev[3 * i], st));
-            launch_gather(ctx, ctx->is.trace.p + o[i], ni, p->table.p, p->cache_rows.p, p->f, p->batch.p,
-                          p->counters.p + 8 * i);
+            launch_gather_resolved(ctx, ctx->is.trace.p + o[i], ctx->is.acc_slot.p + o[i], ni,
+                                   p->cache_rows.p, p->f, p->batch.p, p->counters.p + 8 * i);
             GX_CUDA(cudaEventRecord(p->kev[3 * i + 1], st));
             if (p->digest) launch_digest(ctx, p->batch.p, ni, p->f->row_bytes, p->digests.p + i);
             const uint64_t a = p->cs.h_in_off[i], b = p->cs.h_out_off[i];
             launch_apply_slots(ctx, p->cs.in_ids.p + a, p->cs.in_pos.p + a, p->cs.in_slot.p + a,
                                (uint32_t)(p->cs.h_in_off[i + 1] - a), p->cs.out_ids.p + b,
-                               (uint32_t)(p->cs.h_out_off[i + 1] - b), p->table.p, p->batch.p, p->cache_rows.p,
+                               (uint32_t)(p->cs.h_out_off[i + 1] - b), nullptr, p->batch.p, p->cache_rows.p,
                                p->f->row_bytes);
             GX_CUDA(cudaEventRecord(p->kev[3 * i + 2], st));
         }
         GX_CUDA(cudaEventRecord(p->ev[4], st));
-        // leave the address table clean: every node ever inserted -> -1
-        launch_reset_table(ctx, p->cs.init.p, p->cs.n_init, p->table.p);
-        launch_reset_table(ctx, p->cs.in_ids.p, p->cs.h_in_off[S], p->table.p);
         std::vector<unsigned long long> cnt(8 * (S + 1));
         GX_CUDA(cudaMemcpyAsync(cnt.data(), p->counters.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
         if (p->digest) {

@@ -58,62 +58,76 @@ __device__ __forceinline__ void st_na(uint4* p, const uint4& v) {
 }
 __device__ __forceinline__ void st_na(uint32_t* p, const uint32_t& v) { *p = v; }
 
-// gather: out[k] = row(ids[k]) from cache slot table[ids[k]] or the store.
-// counters: [0] hits [1] misses [2] pages [3] rows [4] bytes (misses only)
-template <int VEC>
-__global__ void __launch_bounds__(GA_THREADS) k_gather(const uint32_t* __restrict__ ids, uint64_t n,
-                                                       const int32_t* __restrict__ table,
-                                                       const uint8_t* __restrict__ cache_rows,
-                                                       const uint8_t* __restrict__ store,
-                                                       uint64_t row_bytes, uint8_t* __restrict__ out,
-                                                       unsigned long long* counters) {
+// Row gather with pre-resolved sources: row k of `out` = cache slot slots[k]
+// or, when slots[k] == kNever (a miss), row ids[k] of the backing store.
+// A warp moves R rows per step: lanes 0..R-1 fetch the rows' metadata
+// (coalesced), the row base pointers are broadcast by shuffles and every lane
+// issues R independent 16-byte loads before the R stores, so R x row_bytes per
+// warp are in flight with no dependent index chain on the data path.
+// counters: [0] hits [1] misses [2] pages [3] rows [4] bytes (misses only,
+// graph_store.hpp:308-315).
+template <int VEC, int R>
+__global__ void __launch_bounds__(GA_THREADS, 5) k_gather_rows(const uint32_t* __restrict__ ids,
+                                                               const uint32_t* __restrict__ slots, uint32_t n,
+                                                               const uint8_t* __restrict__ cache_rows,
+                                                               const uint8_t* __restrict__ store,
+                                                               uint32_t row_bytes, uint8_t* __restrict__ out,
+                                                               unsigned long long* counters) {
     using V = typename VecT<VEC>::T;
     const uint32_t lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t nvec = (uint32_t)(row_bytes / VEC);
-    unsigned long long hits = 0, misses = 0, pages = 0;
-    for (uint64_t r0 = warp * GA_ROWS; r0 < n; r0 += nwarps * GA_ROWS) {
-        const V* src[GA_ROWS];
-        V* dst[GA_ROWS];
-        bool valid[GA_ROWS];
-#pragma unroll
-        for (int q = 0; q < GA_ROWS; ++q) {
-            const uint64_t r = r0 + q;
-            valid[q] = r < n;
-            uint32_t v = 0;
-            int32_t s = -1;
-            if (valid[q]) {
-                v = ids[r];
-                s = table[v];
-            }
-            src[q] = reinterpret_cast<const V*>(s >= 0 ? cache_rows + (uint64_t)s * row_bytes
-                                                       : store + (uint64_t)v * row_bytes);
-            dst[q] = reinterpret_cast<V*>(out + r * row_bytes);
-            if (valid[q] && lane == 0) {
-                if (s >= 0) ++hits;
-                else {
-                    ++misses;
-                    pages += pages_touched((uint64_t)v * row_bytes, (uint64_t)(v + 1) * row_bytes);
-                }
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nvec = row_bytes / VEC;
+    uint32_t hits = 0, misses = 0, pages = 0;
+    for (uint32_t r0 = warp * R; r0 < n; r0 += nwarps * R) {
+        const uint32_t nr = min(n - r0, (uint32_t)R);
+        const uint8_t* src = nullptr;
+        if (lane < nr) {
+            const uint32_t v = __ldg(ids + r0 + lane);
+            const uint32_t s = __ldg(slots + r0 + lane);
+            if (s != kNever) {
+                src = cache_rows + (uint64_t)s * row_bytes;
+                ++hits;
+            } else {
+                src = store + (uint64_t)v * row_bytes;
+                ++misses;
+                pages += (uint32_t)pages_touched((uint64_t)v * row_bytes, (uint64_t)v * row_bytes + row_bytes);
             }
         }
-        for (uint32_t c = lane; c < nvec; c += 32) {
-            V tmp[GA_ROWS];
+        V* dst = reinterpret_cast<V*>(out + (uint64_t)r0 * row_bytes);
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < nvec; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            V tmp[R];
 #pragma unroll
-            for (int q = 0; q < GA_ROWS; ++q)
-                if (valid[q]) tmp[q] = ld_nc(src[q] + c);
+            for (int q = 0; q < R; ++q) {
+                const V* sq = reinterpret_cast<const V*>(__shfl_sync(0xffffffffu, (unsigned long long)src, q));
+                if (q < (int)nr && c < nvec) tmp[q] = ld_nc(sq + c);
+            }
 #pragma unroll
-            for (int q = 0; q < GA_ROWS; ++q)
-                if (valid[q]) st_na(dst[q] + c, tmp[q]);
+            for (int q = 0; q < R; ++q)
+                if (q < (int)nr && c < nvec) st_na(dst + q * nvec + c, tmp[q]);
         }
     }
+    hits = warp_sum(hits);
+    misses = warp_sum(misses);
+    pages = warp_sum(pages);
     if (lane == 0 && (hits | misses)) {
-        atomicAdd(&counters[0], hits);
-        atomicAdd(&counters[1], misses);
-        atomicAdd(&counters[2], pages);
-        atomicAdd(&counters[3], misses);
-        atomicAdd(&counters[4], misses * row_bytes);
+        atomicAdd(&counters[0], (unsigned long long)hits);
+        atomicAdd(&counters[1], (unsigned long long)misses);
+        atomicAdd(&counters[2], (unsigned long long)pages);
+        atomicAdd(&counters[3], (unsigned long long)misses);
+        atomicAdd(&counters[4], (unsigned long long)misses * row_bytes);
+    }
+}
+
+// Address-table resolution for the API path: slots[k] = table[ids[k]] (or kNever).
+__global__ void k_resolve(const uint32_t* __restrict__ ids, uint64_t n, const int32_t* __restrict__ table,
+                          uint32_t* __restrict__ slots) {
+    for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < n;
+         k += (uint64_t)gridDim.x * blockDim.x) {
+        const int32_t s = table[ids[k]];
+        slots[k] = s >= 0 ? (uint32_t)s : kNever;
     }
 }
 
@@ -137,12 +151,12 @@ __global__ void k_apply_slots(const uint32_t* __restrict__ in_ids, const uint32_
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t m = max(n_in, n_out);
     for (uint64_t k = warp; k < m; k += nwarps) {
-        if (k < n_out && lane == 0) table[out_ids[k]] = -1;
+        if (table && k < n_out && lane == 0) table[out_ids[k]] = -1;
         if (k < n_in) {
             const uint32_t s = in_slot[k];
             warp_copy_row<VEC>(batch + (uint64_t)in_pos[k] * row_bytes, cache_rows + (uint64_t)s * row_bytes,
                                row_bytes);
-            if (lane == 0) table[in_ids[k]] = (int32_t)s;
+            if (table && lane == 0) table[in_ids[k]] = (int32_t)s;
         }
     }
 }
@@ -205,7 +219,7 @@ __global__ void k_cache_init(const uint32_t* __restrict__ init, uint32_t n, int3
         const uint32_t v = init[k];
         warp_copy_row<VEC>(store + (uint64_t)v * row_bytes, cache_rows + k * row_bytes, row_bytes);
         if (lane == 0) {
-            table[v] = (int32_t)k;
+            if (table) table[v] = (int32_t)k;
             pg += pages_touched((uint64_t)v * row_bytes, (uint64_t)(v + 1) * row_bytes);
         }
     }
@@ -254,19 +268,39 @@ void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t ro
 }
 
 // Launchers shared with the pipeline.
+template <int VEC, int R>
+static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
+                               const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                               unsigned long long* counters) {
+    static int bps = 0;
+    if (!bps) {
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_gather_rows<VEC, R>, GA_THREADS, 0));
+        bps = std::max(bps, 1);
+    }
+    const uint64_t warps_needed = (n + R - 1) / R;
+    const uint64_t blocks_needed = (warps_needed * 32 + GA_THREADS - 1) / GA_THREADS;
+    const uint64_t blocks = std::min<uint64_t>(blocks_needed, (uint64_t)ctx->num_sms * bps);
+    k_gather_rows<VEC, R><<<(unsigned)blocks, GA_THREADS, 0, ctx->stream>>>(
+        ids, slots, (uint32_t)n, cache_rows, f->rows_dev_view, (uint32_t)f->row_bytes, out, counters);
+    GX_CHECK_LAUNCH();
+}
+
+void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
+                            const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                            unsigned long long* counters) {
+    if (!n) return;
+    if (vec16(f->row_bytes)) gather_rows_launch<16, 4>(ctx, ids, slots, n, cache_rows, f, out, counters);
+    else gather_rows_launch<4, 4>(ctx, ids, slots, n, cache_rows, f, out, counters);
+}
+
 void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table, const uint8_t* cache_rows,
                    const gx_features* f, uint8_t* out, unsigned long long* counters) {
     if (!n) return;
-    const uint64_t warps_needed = (n + GA_ROWS - 1) / GA_ROWS;
-    const uint64_t blocks = std::min<uint64_t>((warps_needed * 32 + GA_THREADS - 1) / GA_THREADS,
-                                               (uint64_t)ctx->num_sms * 8);
-    if (vec16(f->row_bytes))
-        k_gather<16><<<(unsigned)blocks, GA_THREADS, 0, ctx->stream>>>(ids, n, table, cache_rows, f->rows_dev_view,
-                                                                       f->row_bytes, out, counters);
-    else
-        k_gather<4><<<(unsigned)blocks, GA_THREADS, 0, ctx->stream>>>(ids, n, table, cache_rows, f->rows_dev_view,
-                                                                      f->row_bytes, out, counters);
+    DevBuf<uint32_t>& slots = ctx->resolve_slots;  // API path only
+    slots.reserve(n);
+    k_resolve<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ids, n, table, slots.p);
     GX_CHECK_LAUNCH();
+    launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, f, out, counters);
 }
 
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos, const uint32_t* in_slot,

@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -201,9 +202,10 @@ struct DevBuf {
         }
         n = count;
     }
-    // grow-only
+    // grow-only, with 25% headroom so per-superbatch size jitter does not
+    // re-allocate (cudaMalloc/cudaFree stall the stream)
     void reserve(size_t count) {
-        if (count > n) alloc(count);
+        if (count > n) alloc(std::max(count + count / 4, n + n / 4) + 64);
     }
     void release() {
         if (p) cudaFree(p);

@@ -21,12 +21,14 @@ struct InspectScratch {
     DevBuf<uint32_t> last;       // N, node-indexed "next access" cursor (kNever when clean)
     DevBuf<int32_t> node_slot;   // N, -1 when clean
     uint64_t N = 0;
-    DevBuf<uint32_t> trace, next_use;
+    DevBuf<uint32_t> trace, next_use, acc_slot;
     DevBuf<uint64_t> trace_off;
     DevBuf<uint32_t> tile_cnt, slot_node, slot_key, hist_new, rh, pkey, out_node, out_slot, c_id,
         c_ref, in_node, in_pos, chunk_cnt, bm_words, bm_cnt, init_ext, toff, st;
     DevBuf<int32_t> hist_inc;
     DevBuf<uint8_t> pmiss;
+    DevBuf<uint32_t> o_misses, o_in_off, o_out_off;  // per-iteration outputs (S+1)
+    std::vector<uint32_t> h_m, h_io, h_oo;
 };
 }  // namespace gx
 
@@ -37,6 +39,7 @@ struct gx_ctx {
     gx::DevBuf<gx::GridBarrier> barrier;  // one barrier per context (stream-serialised users)
     gx::SampleScratch ss;
     gx::InspectScratch is;
+    gx::DevBuf<uint32_t> resolve_slots;  // executor API path scratch
 };
 
 struct gx_graph {
@@ -124,6 +127,10 @@ void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N,
 void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table,
                    const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
                    unsigned long long* counters);
+// gather with the serving slot of every row already resolved (kNever = miss)
+void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
+                            const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                            unsigned long long* counters);
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos,
                         const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
                         uint32_t n_out, int32_t* table, const uint8_t* batch, uint8_t* cache_rows,

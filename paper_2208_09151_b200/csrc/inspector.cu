@@ -64,6 +64,7 @@ struct IArgs {
     uint32_t* rh;        // 3 * 2048
     uint32_t* pkey;      // maxw
     uint8_t* pmiss;      // maxw
+    uint32_t* acc_slot;  // A: cache slot serving each access at gather time (kNever = miss)
     uint32_t* out_node;  // maxw
     uint32_t* out_slot;  // maxw
     uint32_t* c_id;      // max(K, maxw)
@@ -296,9 +297,11 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                     a.slot_key[s] = nu;
                     atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
                     a.pmiss[pos] = 0;
+                    a.acc_slot[base + pos] = (uint32_t)s;
                     ++hits;
                 } else {
                     a.pmiss[pos] = 1;
+                    a.acc_slot[base + pos] = kNever;
                     a.pkey[pos] = nu;
                     atomicAdd(&sm.hnew[bucket_of(nu, S)], 1);
                     ++miss;
@@ -678,7 +681,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     out->in_pos.reserve(A + 1);
     out->in_slot.reserve(A + 1);
     out->out_ids.reserve(A + 1);
-    DevBuf<uint32_t> d_misses(S + 1), d_in_off(S + 1), d_out_off(S + 1);
+    B.o_misses.reserve(S + 1);
+    B.o_in_off.reserve(S + 1);
+    B.o_out_off.reserve(S + 1);
+    DevBuf<uint32_t>&d_misses = B.o_misses, &d_in_off = B.o_in_off, &d_out_off = B.o_out_off;
 
     if (n_init_explicit >= 0) {
         std::vector<uint32_t> i32(std::max<int64_t>(n_init_explicit, 1));
@@ -706,6 +712,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.rh = B.rh.p;
     a.pkey = B.pkey.p;
     a.pmiss = B.pmiss.p;
+    is.acc_slot.reserve(std::max<uint64_t>(A, 1));
+    a.acc_slot = is.acc_slot.p;
     a.out_node = B.out_node.p;
     a.out_slot = B.out_slot.p;
     a.c_id = B.c_id.p;
@@ -745,7 +753,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
 
     IState hs;
     GX_CUDA(cudaMemcpyAsync(&hs, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
-    std::vector<uint32_t> m32(S + 1), io32(S + 1), oo32(S + 1);
+    std::vector<uint32_t>&m32 = B.h_m, &io32 = B.h_io, &oo32 = B.h_oo;
+    m32.resize(S + 1);
+    io32.resize(S + 1);
+    oo32.resize(S + 1);
     GX_CUDA(cudaMemcpyAsync(m32.data(), d_misses.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(io32.data(), d_in_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(oo32.data(), d_out_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
