@@ -299,8 +299,10 @@ def main():
     pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
+    from paper_2208_09151_b200.shard import assign_superbatches
+
     def sb_index(k):  # rank r takes superbatches r, r+world, ... of the epoch plan
-        return (rank + k * world) % len(sbs)
+        return assign_superbatches(len(sbs), rank, world, 1, start=k)[0]
 
     def step(k):
         j = sb_index(k)

@@ -1,0 +1,135 @@
+"""GPU: the reference's own recorded acceptance numbers (proj/test_output.txt,
+tests/golden/acceptance_kats.json) reproduced end to end by the CUDA path, plus
+the golden fixtures generated from the reference build."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+KATS = json.load(open(os.path.join(HERE, "golden", "acceptance_kats.json")))
+G = np.load(os.path.join(HERE, "golden", "reference_golden.npz"))
+
+
+def test_golden_samples_on_device(gx):
+    g = gx.GraphFile.from_csc(G["g_indptr"], G["g_indices"])
+    for t in G["sample_cases"]:
+        fan = [int(x) for x in G[f"s{t}_fan"]]
+        io = gx.IoStats()
+        out = gx.sample_batch(g, None, G[f"s{t}_seeds"], fan, int(G[f"s{t}_bs"]), io)
+        assert np.array_equal(out.ids, G[f"s{t}_ids"])
+        for l in range(len(fan)):
+            assert np.array_equal(out.layers[l], G[f"s{t}_l{l}"])
+        want = G[f"s{t}_io"]
+        assert (io.pages_read, io.neighbor_lists_read, io.bytes_read) == (int(want[0]), int(want[2]), int(want[3]))
+    # the device generator reproduces generate_dataset's graph and feature table
+    g2 = gx.GraphFile.generate_rmat(2000, 8.0, 61)
+    ip, ind = g2.to_csc()
+    assert np.array_equal(ip, G["g_indptr"]) and np.array_equal(ind, G["g_indices"])
+    f = gx.FeatureFile.generate(2000, 16, 62)
+    assert np.array_equal(f.read_rows(np.arange(2000)), G["g_features"])
+
+
+def test_golden_files_on_device(gx, tmp_path):
+    g = gx.GraphFile.from_csc(G["g_indptr"], G["g_indices"])
+    batches = [np.arange(i * 40, i * 40 + 40, dtype=np.uint64) for i in range(3)]
+    gx.superbatch_sample(g, None, batches, [4, 4], 123, 5, 9, str(tmp_path))
+    for i in range(3):
+        for stem in ("ids", "adj"):
+            got = open(tmp_path / f"{stem}_9_{i}.bin", "rb").read()
+            assert got == G[f"file_{stem}_{i}"].tobytes(), (stem, i)
+
+
+def test_golden_changesets_on_device(gx):
+    for t in G["cs_cases"]:
+        flat, off = G[f"c{t}_flat"], G[f"c{t}_off"]
+        tr = [flat[int(off[i]):int(off[i + 1])] for i in range(len(off) - 1)]
+        n = int(G[f"c{t}_n"])
+        ix = gx.build_access_index(tr, n)
+        assert np.array_equal(ix.iters, G[f"c{t}_iters"]) and np.array_equal(ix.ptr, G[f"c{t}_ptr"])
+        for K in G[f"c{t}_caps"]:
+            K = int(K)
+            cs = gx.precompute_trace(tr, n, K)
+            assert np.array_equal(cs.init_set(), G[f"c{t}_K{K}_init"])
+            assert np.array_equal(cs.misses(), G[f"c{t}_K{K}_misses"])
+            io, oo = G[f"c{t}_K{K}_in_off"], G[f"c{t}_K{K}_out_off"]
+            for i in range(len(tr)):
+                c = cs.changeset(i)
+                a, b = int(io[i]), int(io[i + 1])
+                assert np.array_equal(c.in_ids, G[f"c{t}_K{K}_in_ids"][a:b])
+                assert np.array_equal(c.in_positions, G[f"c{t}_K{K}_in_pos"][a:b])
+                a, b = int(oo[i]), int(oo[i + 1])
+                assert np.array_equal(c.out_ids, G[f"c{t}_K{K}_out_ids"][a:b])
+
+
+def test_dp_optimality_on_device(gx):
+    from tests.golden.make_golden import make_trace
+    for t, K, want in G["dp"]:
+        t, K, want = int(t), int(K), int(want)
+        tr = make_trace(2 + t % 7, 1 + t % 6, 4, 4000 + t)
+        r = gx.simulate_changesets(None, tr, K, [], num_nodes=2 + t % 7)
+        assert r.total_misses() == want  # acceptance c2: Belady == exhaustive optimum
+
+
+def test_acceptance_c3_miss_ratios_on_device(gx):
+    k = KATS["c3_belady_miss_ratio"]
+    n = k["num_nodes"]
+    g = gx.GraphFile.generate_rmat(n, k["avg_degree"], k["edge_seed"])
+    sums = np.zeros(4)
+    for seed in (1, 2, 3):
+        rng = gx.SplitMix64(gx.derive_seed(seed, 0x7261))
+        pool = list(range(n))
+        train = []
+        for i in range(64 * 512):
+            j = i + rng.bounded(n - i)
+            pool[i], pool[j] = pool[j], pool[i]
+            train.append(pool[i])
+        plan = gx.plan_seed_batches(train, 512, gx.derive_seed(seed, 1)).batches
+        s = gx.sample_superbatch(g, None, plan, [10, 10, 10], seed, 100)
+        trace = [s.batch(i).ids for i in range(len(s))]
+        acc = sum(len(t) for t in trace)
+        for c, K in enumerate(k["capacities"]):
+            sums[c] += gx.precompute_trace(trace, n, K).misses().sum() / acc
+    assert [f"{x / 3:.6f}" for x in sums] == k["miss_ratio"]
+
+
+def _run(gx, g, f, cfg, num_entries):
+    train = gx.derive_train_ids(g.num_nodes(), cfg["seed"], cfg["train_fraction"])
+    plan = gx.plan_seed_batches(train, cfg["batch"], gx.epoch_seed(cfg["seed"], 0)).batches
+    S = cfg["superbatch"]
+    p = gx.Pipeline(g, f, cfg["fanouts"], num_entries)
+    out = []
+    for j, o in enumerate(range(0, len(plan), S)):
+        out.append(p.run_superbatch(plan[o:o + S], cfg["seed"], o))
+    return out
+
+
+def test_acceptance_c6_aligned_pages_on_device(gx):
+    k = KATS["c6_aligned_pages"]
+    g = gx.GraphFile.generate_rmat(k["num_nodes"], k["avg_degree"], k["edge_seed"])
+    f = gx.FeatureFile.generate(k["num_nodes"], k["dim"], k["value_seed"])
+    st = _run(gx, g, f, k, k["cache"])
+    assert sum(s.gather_io.pages_read for s in st) == k["pages"]
+    assert sum(s.total_misses for s in st) == k["misses"]
+
+
+def test_acceptance_c7_pages_on_device(gx):
+    k = KATS["c7_pages"]
+    g = gx.GraphFile.generate_rmat(k["num_nodes"], k["avg_degree"], k["edge_seed"])
+    f = gx.FeatureFile.generate(k["num_nodes"], k["dim"], 72)
+    st = _run(gx, g, f, k, 0)
+    assert sum(s.gather_io.pages_read for s in st) == k["gather_pages"]
+    assert sum(s.sample_io.pages_read for s in st) == k["sample_pages"]
+
+
+def test_survey_cfg1_superbatch_on_device(gx):
+    k = KATS["survey_cfg1"]
+    g = gx.GraphFile.generate_rmat(1_000_000, 10.0, gx.derive_seed(7, 0xED6E5))
+    assert g.num_edges() == k["num_edges"]
+    f = gx.FeatureFile.generate(1_000_000, 128, gx.derive_seed(7, 0xFEA7))
+    train = gx.derive_train_ids(1_000_000, 1, 0.1)
+    plan = gx.plan_seed_batches(train, 1000, gx.epoch_seed(1, 0)).batches
+    st = gx.Pipeline(g, f, [10, 10, 10], 100_000).run_superbatch(plan[:100], 1, 0)
+    assert (st.gathered_rows, st.sampled_edges, st.total_misses) == (k["accesses"], k["sampled_edges"], k["misses"])
