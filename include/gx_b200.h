@@ -191,6 +191,8 @@ void gx_batch_destroy(gx_batch* b);
 uint64_t gx_batch_rows(const gx_batch* b);
 gx_status gx_batch_copy_to_host(const gx_batch* b, void* out);
 void* gx_batch_device_ptr(const gx_batch* b);
+/* load host rows into a batch (e.g. a RowMatrix handed to apply_changeset) */
+gx_status gx_batch_upload(gx_batch* b, const void* rows, uint64_t n_rows, uint64_t row_bytes);
 
 typedef struct gx_cache gx_cache;
 /* FeatureCache ctor (feature_cache.hpp:19-37): init ids -> slots 0..k-1. */

@@ -104,6 +104,7 @@ SIGNATURES = {
     "gx_batch_rows": (u64, [vp]),
     "gx_batch_copy_to_host": (i32, [vp, vp]),
     "gx_batch_device_ptr": (vp, [vp]),
+    "gx_batch_upload": (i32, [vp, vp, u64, u64]),
     "gx_cache_create": (i32, [vp, vp, u64, u64, PIO, PVP]),
     "gx_cache_destroy": (None, [vp]),
     "gx_cache_num_entries": (u64, [vp]),

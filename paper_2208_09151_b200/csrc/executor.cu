@@ -361,6 +361,15 @@ gx_status gx_batch_create(gx_ctx* ctx, gx_batch** out) {
 void gx_batch_destroy(gx_batch* b) { delete b; }
 uint64_t gx_batch_rows(const gx_batch* b) { return b ? b->rows : 0; }
 void* gx_batch_device_ptr(const gx_batch* b) { return b ? b->data.p : nullptr; }
+gx_status gx_batch_upload(gx_batch* b, const void* rows, uint64_t n, uint64_t row_bytes) {
+    return guard([&] {
+        b->rows = n;
+        b->row_bytes = row_bytes;
+        b->data.reserve(std::max<uint64_t>(n * row_bytes, 16));
+        if (n) GX_CUDA(cudaMemcpy(b->data.p, rows, n * row_bytes, cudaMemcpyHostToDevice));
+    });
+}
+
 gx_status gx_batch_copy_to_host(const gx_batch* b, void* out) {
     return guard([&] {
         if (b->rows) GX_CUDA(cudaMemcpy(out, b->data.p, b->rows * b->row_bytes, cudaMemcpyDeviceToHost));
