@@ -12,6 +12,7 @@
 //    the inspector precomputed; k_apply (API path) recomputes them from this
 //    cache's own free list, exactly as the reference does.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gx_internal.cuh"
 
@@ -66,8 +67,13 @@ __device__ __forceinline__ void st_na(uint32_t* p, const uint32_t& v) { *p = v; 
 // warp are in flight with no dependent index chain on the data path.
 // counters: [0] hits [1] misses [2] pages [3] rows [4] bytes (misses only,
 // graph_store.hpp:308-315).
+template <int R>
+struct GatherOcc {
+    static constexpr int value = R >= 8 ? 3 : (R >= 4 ? 5 : 8);
+};
+
 template <int VEC, int R>
-__global__ void __launch_bounds__(GA_THREADS, 5) k_gather_rows(const uint32_t* __restrict__ ids,
+__global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_gather_rows(const uint32_t* __restrict__ ids,
                                                                const uint32_t* __restrict__ slots, uint32_t n,
                                                                const uint8_t* __restrict__ cache_rows,
                                                                const uint8_t* __restrict__ store,
@@ -113,6 +119,156 @@ __global__ void __launch_bounds__(GA_THREADS, 5) k_gather_rows(const uint32_t* _
     misses = warp_sum(misses);
     pages = warp_sum(pages);
     if (lane == 0 && (hits | misses)) {
+        atomicAdd(&counters[0], (unsigned long long)hits);
+        atomicAdd(&counters[1], (unsigned long long)misses);
+        atomicAdd(&counters[2], (unsigned long long)pages);
+        atomicAdd(&counters[3], (unsigned long long)misses);
+        atomicAdd(&counters[4], (unsigned long long)misses * row_bytes);
+    }
+}
+
+// TMA variant of the row gather: every thread moves whole rows with the bulk
+// copy engine, global -> its own smem row buffer (cp.async.bulk + mbarrier
+// complete_tx) -> global (cp.async.bulk bulk_group). Bytes in flight are
+// bounded by shared memory (blockDim x row_bytes per CTA), not registers.
+// Requires row_bytes % 16 == 0 and 16-byte aligned rows.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__global__ void __launch_bounds__(128) k_gather_tma(const uint32_t* __restrict__ ids,
+                                                    const uint32_t* __restrict__ slots, uint32_t n,
+                                                    const uint8_t* __restrict__ cache_rows,
+                                                    const uint8_t* __restrict__ store, uint32_t row_bytes,
+                                                    uint8_t* __restrict__ out, unsigned long long* counters) {
+    extern __shared__ __align__(128) unsigned char sbuf[];
+    __shared__ __align__(8) unsigned long long bars[128];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t bar = smem_u32(&bars[tid]);
+    const uint32_t buf = smem_u32(sbuf + (size_t)tid * row_bytes);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    uint32_t phase = 0;
+    uint32_t hits = 0, misses = 0, pages = 0;
+    for (uint32_t r = blockIdx.x * blockDim.x + tid; r < n; r += gridDim.x * blockDim.x) {
+        const uint32_t v = __ldg(ids + r);
+        const uint32_t s = __ldg(slots + r);
+        const uint8_t* src;
+        if (s != kNever) {
+            src = cache_rows + (uint64_t)s * row_bytes;
+            ++hits;
+        } else {
+            src = store + (uint64_t)v * row_bytes;
+            ++misses;
+            pages += (uint32_t)pages_touched((uint64_t)v * row_bytes, (uint64_t)v * row_bytes + row_bytes);
+        }
+        // the previous row's store must have finished reading the buffer
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(buf),
+            "l"(src), "r"(row_bytes), "r"(bar)
+            : "memory");
+        asm volatile(
+            "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(bar),
+            "r"(phase)
+            : "memory");
+        phase ^= 1;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + (uint64_t)r * row_bytes),
+                     "r"(buf), "r"(row_bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    hits = warp_sum(hits);
+    misses = warp_sum(misses);
+    pages = warp_sum(pages);
+    if ((tid & 31) == 0 && (hits | misses)) {
+        atomicAdd(&counters[0], (unsigned long long)hits);
+        atomicAdd(&counters[1], (unsigned long long)misses);
+        atomicAdd(&counters[2], (unsigned long long)pages);
+        atomicAdd(&counters[3], (unsigned long long)misses);
+        atomicAdd(&counters[4], (unsigned long long)misses * row_bytes);
+    }
+}
+
+// 2-deep per-thread pipeline: the load of row j+1 is in flight while row j is
+// stored, so each thread keeps two rows moving.
+__device__ __forceinline__ const uint8_t* gather_src(const uint32_t* ids, const uint32_t* slots, uint32_t r,
+                                                     const uint8_t* cache_rows, const uint8_t* store,
+                                                     uint32_t row_bytes, uint32_t& hits, uint32_t& misses,
+                                                     uint32_t& pages) {
+    const uint32_t v = __ldg(ids + r);
+    const uint32_t s = __ldg(slots + r);
+    if (s != kNever) {
+        ++hits;
+        return cache_rows + (uint64_t)s * row_bytes;
+    }
+    ++misses;
+    pages += (uint32_t)pages_touched((uint64_t)v * row_bytes, (uint64_t)v * row_bytes + row_bytes);
+    return store + (uint64_t)v * row_bytes;
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t buf, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(buf),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(bar),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* dst, uint32_t buf, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(buf), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict__ ids,
+                                                     const uint32_t* __restrict__ slots, uint32_t n,
+                                                     const uint8_t* __restrict__ cache_rows,
+                                                     const uint8_t* __restrict__ store, uint32_t row_bytes,
+                                                     uint8_t* __restrict__ out, unsigned long long* counters) {
+    extern __shared__ __align__(128) unsigned char sbuf[];
+    __shared__ __align__(8) unsigned long long bars[2 * 128];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t bar0 = smem_u32(&bars[2 * tid]), bar1 = bar0 + 8;
+    const uint32_t buf0 = smem_u32(sbuf + (size_t)(2 * tid) * row_bytes), buf1 = buf0 + row_bytes;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    uint32_t hits = 0, misses = 0, pages = 0;
+    const uint32_t step = gridDim.x * blockDim.x;
+    uint32_t r = blockIdx.x * blockDim.x + tid;
+    uint32_t ph0 = 0, ph1 = 0;
+    if (r < n) bulk_load(buf0, gather_src(ids, slots, r, cache_rows, store, row_bytes, hits, misses, pages), row_bytes, bar0);
+    for (uint32_t j = 0; r < n; ++j, r += step) {
+        const uint32_t nx = r + step;
+        const bool odd = j & 1;
+        if (nx < n) {  // prefetch the next row into the other buffer
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            bulk_load(odd ? buf0 : buf1, gather_src(ids, slots, nx, cache_rows, store, row_bytes, hits, misses, pages),
+                      row_bytes, odd ? bar0 : bar1);
+        }
+        if (odd) {
+            bar_wait(bar1, ph1);
+            ph1 ^= 1;
+            bulk_store(out + (uint64_t)r * row_bytes, buf1, row_bytes);
+        } else {
+            bar_wait(bar0, ph0);
+            ph0 ^= 1;
+            bulk_store(out + (uint64_t)r * row_bytes, buf0, row_bytes);
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    hits = warp_sum(hits);
+    misses = warp_sum(misses);
+    pages = warp_sum(pages);
+    if ((tid & 31) == 0 && (hits | misses)) {
         atomicAdd(&counters[0], (unsigned long long)hits);
         atomicAdd(&counters[1], (unsigned long long)misses);
         atomicAdd(&counters[2], (unsigned long long)pages);
@@ -289,8 +445,46 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
                             const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
                             unsigned long long* counters) {
     if (!n) return;
-    if (vec16(f->row_bytes)) gather_rows_launch<16, 4>(ctx, ids, slots, n, cache_rows, f, out, counters);
-    else gather_rows_launch<4, 4>(ctx, ids, slots, n, cache_rows, f, out, counters);
+    // Variant (tuning knob GX_GATHER_R): 1 = TMA bulk, 2 rows in flight per
+    // thread (default); 0 = TMA bulk, 1 row per thread; 2/4/8 = LDG/STG with
+    // that many rows per warp. TMA needs 16-byte rows whose buffers fit smem.
+    static const int R = [] {
+        const char* e = std::getenv("GX_GATHER_R");
+        const int r = e ? std::atoi(e) : 1;
+        return (r == 0 || r == 1 || r == 2 || r == 4 || r == 8) ? r : 1;
+    }();
+    static const int budget = [] {  // shared memory per CTA for row buffers (KB)
+        const char* e = std::getenv("GX_GATHER_SMEM_KB");
+        const int kb = e ? std::atoi(e) : 96;
+        return std::min(std::max(kb, 16), 200) * 1024;
+    }();
+    const uint64_t rb = f->row_bytes;
+    const int depth = R == 1 ? 2 : 1;
+    if (vec16(rb) && R <= 1 && (uint64_t)depth * 32 * rb <= (uint64_t)budget) {
+        static int tpb[2] = {0, 0}, bps[2] = {0, 0};
+        static uint64_t last_rb[2] = {0, 0};
+        const int d = depth - 1;
+        if (last_rb[d] != rb) {  // threads per CTA: one (or two) row buffers per thread
+            last_rb[d] = rb;
+            tpb[d] = (int)std::min<uint64_t>(128, budget / (depth * rb)) & ~31;
+            const int smem = tpb[d] * depth * (int)rb;
+            auto kfn = depth == 2 ? k_gather_tma2 : k_gather_tma;
+            GX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[d], kfn, tpb[d], smem));
+            bps[d] = std::max(bps[d], 1);
+        }
+        const uint64_t blocks = std::min<uint64_t>((n + tpb[d] - 1) / tpb[d], (uint64_t)ctx->num_sms * bps[d]);
+        auto kfn = depth == 2 ? k_gather_tma2 : k_gather_tma;
+        kfn<<<(unsigned)blocks, tpb[d], (size_t)tpb[d] * depth * rb, ctx->stream>>>(
+            ids, slots, (uint32_t)n, cache_rows, f->rows_dev_view, (uint32_t)rb, out, counters);
+        GX_CHECK_LAUNCH();
+    } else if (vec16(rb)) {
+        if (R == 2) gather_rows_launch<16, 2>(ctx, ids, slots, n, cache_rows, f, out, counters);
+        else if (R == 8) gather_rows_launch<16, 8>(ctx, ids, slots, n, cache_rows, f, out, counters);
+        else gather_rows_launch<16, 4>(ctx, ids, slots, n, cache_rows, f, out, counters);
+    } else {
+        gather_rows_launch<4, 4>(ctx, ids, slots, n, cache_rows, f, out, counters);
+    }
 }
 
 void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table, const uint8_t* cache_rows,

@@ -112,7 +112,11 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b) {
             __threadfence();
             atomicAdd(&b->gen, 1u);
         } else {
-            while (*vgen == g) __nanosleep(20);
+            unsigned ns = 32;
+            while (*vgen == g) {
+                __nanosleep(ns);
+                if (ns < 256) ns <<= 1;
+            }
         }
         __threadfence();
     }

@@ -28,6 +28,11 @@ struct InspectScratch {
     DevBuf<int32_t> hist_inc;
     DevBuf<uint8_t> pmiss;
     DevBuf<uint32_t> o_misses, o_in_off, o_out_off;  // per-iteration outputs (S+1)
+    DevBuf<unsigned long long> bits;  // N * ceil(S/64) iteration bitmask, clean between calls
+    uint64_t bits_words = 0;
+    DevBuf<uint8_t> isfirst;
+    DevBuf<int32_t> init_pos;         // N, -1 when clean (explicit-init API path)
+    uint64_t init_pos_n = 0;
     std::vector<uint32_t> h_m, h_io, h_oo;
 };
 }  // namespace gx

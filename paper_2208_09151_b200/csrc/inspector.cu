@@ -65,13 +65,19 @@ struct IArgs {
     uint32_t* pkey;      // maxw
     uint8_t* pmiss;      // maxw
     uint32_t* acc_slot;  // A: cache slot serving each access at gather time (kNever = miss)
+    unsigned long long* bits;  // N * W per-node iteration bitmask (use_bits)
+    uint32_t W;
+    int use_bits;
+    uint8_t* isfirst;    // A
+    uint32_t* chunk_miss;  // gridDim
+    uint32_t* chunk_in;    // gridDim
+    const int32_t* init_pos;  // N: slot of an explicit init id, -1 otherwise
     uint32_t* out_node;  // maxw
     uint32_t* out_slot;  // maxw
     uint32_t* c_id;      // max(K, maxw)
     uint32_t* c_ref;
     uint32_t* in_node;   // maxw
     uint32_t* in_pos;    // maxw
-    uint32_t* chunk_cnt; // gridDim
     uint32_t* bm_words;  // nwords
     uint32_t nwords;
     uint32_t* bm_cnt;    // gridDim
@@ -104,6 +110,12 @@ __device__ __forceinline__ uint32_t agg_append(uint32_t* ctr, bool pred) {
         base = __shfl_sync(active, base, leader);
     }
     return base + __popc(m & ((1u << lane) - 1));
+}
+
+// explicit init ids -> their slot (set=1) or back to -1 (set=0)
+__global__ void k_init_pos(const uint32_t* init, uint32_t n, int32_t* pos, int set) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        pos[init[k]] = set ? (int32_t)k : -1;
 }
 
 struct ISmem {
@@ -182,41 +194,102 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         sm.hnew[i] = 0;
     }
     __syncthreads();
+    const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
 
-    // ---- next-use: backward pass, one iteration per grid step -------------
-    for (int i = (int)S - 1; i >= 0; --i) {
-        const uint32_t lo = sm.toff[i], hi = sm.toff[i + 1];
-        for (uint32_t x = lo + gtid; x < hi; x += G) {
+    // ---- next use and first occurrence of every access ---------------------
+    if (a.use_bits) {
+        // per-node bitmask of the iterations it appears in: set, read, clear
+        // (3 grid steps instead of one per iteration)
+        for (uint32_t x = gtid; x < a.A; x += G) {
             const uint32_t v = a.trace[x];
             if (v >= a.N) {
                 atomicOr(&a.st->err, 1u);
-                a.next_use[x] = kNever;
                 continue;
             }
-            const uint32_t old = atomicExch(&a.last[v], (uint32_t)i);
-            if (old == (uint32_t)i) atomicOr(&a.st->err, 2u);
-            a.next_use[x] = old;
+            const uint32_t i = iter_of(sm, S, x);
+            const unsigned long long bit = 1ull << (i & 63);
+            const unsigned long long old = atomicOr(&a.bits[(uint64_t)v * a.W + (i >> 6)], bit);
+            if (old & bit) atomicOr(&a.st->err, 2u);
         }
         grid_sync(a.bar);
-    }
-    if (a.st->err) return;  // host reports the exact reference error
-
-    // ---- init set: first K first-occurrences in trace order ---------------
-    const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
-    if (!a.explicit_init) {
+        if (a.st->err) return;  // host reports the exact reference error
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t x = x0 + j;
-                if (x < a.A) c += a.last[a.trace[x]] == iter_of(sm, S, x);
+                if (x < a.A) {
+                    const uint32_t v = a.trace[x];
+                    const uint32_t i = iter_of(sm, S, x);
+                    const unsigned long long* w = a.bits + (uint64_t)v * a.W;
+                    uint32_t nu = kNever, first = kNever;
+                    for (uint32_t q = 0; q < a.W; ++q) {
+                        const unsigned long long word = w[q];
+                        if (first == kNever && word) first = q * 64 + __ffsll((long long)word) - 1;
+                        if (q >= (i >> 6)) {
+                            const unsigned long long above =
+                                q == (i >> 6) ? ((i & 63) == 63 ? 0ull : word & (~0ull << ((i & 63) + 1))) : word;
+                            if (above) {
+                                nu = q * 64 + __ffsll((long long)above) - 1;
+                                break;
+                            }
+                        }
+                    }
+                    a.next_use[x] = nu;
+                    const uint8_t f = first == i;
+                    a.isfirst[x] = f;
+                    c += f;
+                }
             }
-            uint32_t tot = block_sum(c, sm.scan);
+            const uint32_t tot = block_sum(c, sm.scan);
             if (tid == 0) a.tile_cnt[t] = tot;
         }
         grid_sync(a.bar);
-        if (blockIdx.x == 0) {  // exclusive scan of tile counts
+        for (uint32_t x = gtid; x < a.A; x += G) {  // leave the bitmask clean
+            unsigned long long* w = a.bits + (uint64_t)a.trace[x] * a.W;
+            for (uint32_t q = 0; q < a.W; ++q) w[q] = 0;
+        }
+    } else {
+        // large S: backward pass with a node-indexed cursor, one grid step per iteration
+        for (int i = (int)S - 1; i >= 0; --i) {
+            const uint32_t lo = sm.toff[i], hi = sm.toff[i + 1];
+            for (uint32_t x = lo + gtid; x < hi; x += G) {
+                const uint32_t v = a.trace[x];
+                if (v >= a.N) {
+                    atomicOr(&a.st->err, 1u);
+                    a.next_use[x] = kNever;
+                    continue;
+                }
+                const uint32_t old = atomicExch(&a.last[v], (uint32_t)i);
+                if (old == (uint32_t)i) atomicOr(&a.st->err, 2u);
+                a.next_use[x] = old;
+            }
+            grid_sync(a.bar);
+        }
+        if (a.st->err) return;
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            uint32_t c = 0;
+            const uint32_t x0 = t * IN_TILE + tid * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t x = x0 + j;
+                if (x < a.A) {
+                    const uint8_t f = a.last[a.trace[x]] == iter_of(sm, S, x);
+                    a.isfirst[x] = f;
+                    c += f;
+                }
+            }
+            const uint32_t tot = block_sum(c, sm.scan);
+            if (tid == 0) a.tile_cnt[t] = tot;
+        }
+        grid_sync(a.bar);
+        for (uint32_t x = gtid; x < a.A; x += G) a.last[a.trace[x]] = kNever;  // leave clean
+    }
+
+    // ---- init set: first K first-occurrences in trace order (changeset.hpp:137-153)
+    if (!a.explicit_init) {
+        if (blockIdx.x == 0) {  // exclusive scan of the tile counts
             uint32_t carry = 0;
             for (uint32_t base = 0; base < ntiles; base += blockDim.x) {
                 const uint32_t t = base + tid;
@@ -233,17 +306,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            uint32_t fl[4], it[4], vv[4], c = 0;
+            uint32_t fl[4], c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t x = x0 + j;
-                fl[j] = 0;
-                if (x < a.A) {
-                    vv[j] = a.trace[x];
-                    it[j] = iter_of(sm, S, x);
-                    fl[j] = a.last[vv[j]] == it[j];
-                }
+                fl[j] = x < a.A ? a.isfirst[x] : 0;
                 c += fl[j];
             }
             uint32_t tot;
@@ -252,206 +320,266 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             for (int j = 0; j < 4; ++j) {
                 if (fl[j]) {
                     if (r < K) {
-                        a.slot_node[r] = vv[j];
-                        a.slot_key[r] = it[j];
-                        a.node_slot[vv[j]] = (int32_t)r;
-                        a.o_init[r] = vv[j];
-                        atomicAdd(&sm.hinc[bucket_of(it[j], S)], 1);
+                        const uint32_t x = x0 + j;
+                        const uint32_t v = a.trace[x];
+                        const uint32_t it = iter_of(sm, S, x);
+                        a.slot_node[r] = v;
+                        a.slot_key[r] = it;
+                        a.node_slot[v] = (int32_t)r;
+                        a.o_init[r] = v;
+                        atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                     }
                     ++r;
                 }
             }
         }
     } else {
-        for (uint32_t k = gtid; k < a.n_init_ext; k += G) {
-            const uint32_t v = a.init_ext[k];
-            const uint32_t key = a.last[v];  // first access iteration
-            a.slot_node[k] = v;
-            a.slot_key[k] = key;
-            a.node_slot[v] = (int32_t)k;
-            a.o_init[k] = v;
-            atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
+        // explicit init (simulate_changesets' `init`): key = first access iteration
+        for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const uint32_t x0 = t * IN_TILE + tid * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t x = x0 + j;
+                if (x < a.A && a.isfirst[x]) {
+                    const uint32_t v = a.trace[x];
+                    const int32_t k = a.init_pos[v];
+                    if (k >= 0) {
+                        const uint32_t it = iter_of(sm, S, x);
+                        a.slot_node[k] = v;
+                        a.slot_key[k] = it;
+                        a.node_slot[v] = k;
+                        a.o_init[k] = v;
+                        atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
+                    }
+                }
+            }
         }
         if (gtid == 0) a.st->n_res = a.n_init_ext;
     }
     hist_flush(sm.hinc, a.hist_inc, S + 1);
-    grid_sync(a.bar);
-    for (uint32_t x = gtid; x < a.A; x += G) a.last[a.trace[x]] = kNever;  // leave clean
     if (gtid == 0) {
         a.o_in_off[0] = 0;
         a.o_out_off[0] = 0;
     }
+    grid_sync(a.bar);
 
-    // ---- the recurrence ------------------------------------------------------
+    // ---- the recurrence -------------------------------------------------------
+    // State counters are double-buffered by iteration parity: iteration i reads
+    // st[i&1] and CTA 0 writes st[(i+1)&1] in the iteration's last grid step.
     for (uint32_t i = 0; i < S; ++i) {
+        IState* cs = a.st + (i & 1);
+        IState* ns = a.st + ((i + 1) & 1);
         const uint32_t base = sm.toff[i];
         const uint32_t ni = sm.toff[i + 1] - base;
-        // P1: hits refresh their key; misses become candidates
+        const uint32_t chunk = (ni + gridDim.x - 1) / gridDim.x;
+        const uint32_t c0 = min(ni, blockIdx.x * chunk), c1 = min(ni, c0 + chunk);
+        const uint32_t nres = *(volatile uint32_t*)&cs->n_res;
+        const uint32_t in_total = *(volatile uint32_t*)&cs->in_total;
+        const uint32_t out_total = *(volatile uint32_t*)&cs->out_total;
+
+        // P1 (this CTA's contiguous chunk of positions): hits refresh their
+        // key, misses become candidates; per-chunk miss counts
         {
-            uint32_t hits = 0, miss = 0;
-            for (uint32_t pos = gtid; pos < ni; pos += G) {
+            uint32_t miss = 0;
+            for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) {
                 const uint32_t v = a.trace[base + pos];
                 const uint32_t nu = a.next_use[base + pos];
                 const int32_t s = a.node_slot[v];
                 if (s >= 0) {
                     a.slot_key[s] = nu;
                     atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
+                    atomicSub(&sm.hinc[i], 1);
                     a.pmiss[pos] = 0;
                     a.acc_slot[base + pos] = (uint32_t)s;
-                    ++hits;
                 } else {
                     a.pmiss[pos] = 1;
-                    a.acc_slot[base + pos] = kNever;
                     a.pkey[pos] = nu;
+                    a.acc_slot[base + pos] = kNever;
                     atomicAdd(&sm.hnew[bucket_of(nu, S)], 1);
                     ++miss;
                 }
             }
-            hits = block_sum(hits, sm.scan);
             miss = block_sum(miss, sm.scan);
-            if (tid == 0) {
-                sm.hinc[i] -= (int)hits;
-                if (miss) atomicAdd(&a.st->miss, miss);
-            }
+            if (tid == 0) a.chunk_miss[blockIdx.x] = miss;
             hist_flush(sm.hinc, a.hist_inc, S + 1);
             hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
         }
         grid_sync(a.bar);
 
-        // P2 (every CTA, redundantly): ALLIN or CUT; threshold bucket b*
-        const uint32_t m = *(volatile uint32_t*)&a.st->miss;
-        const uint32_t nres = *(volatile uint32_t*)&a.st->n_res;
-        const uint32_t in_total = *(volatile uint32_t*)&a.st->in_total;
-        const uint32_t out_total = *(volatile uint32_t*)&a.st->out_total;
-        const bool cut = (uint64_t)nres + m > K;
-        uint32_t bstar = 0, r = 0, inc_b = 0, new_b = 0;
-        int sel = 0;  // 0 none, 1 select among incumbents of b*, 2 among new of b*
-        if (cut) {
-            if (tid < 32) {
-                uint32_t cum = 0;
-                bool done = false;
-                for (uint32_t b0 = i + 1; b0 <= S && !done; b0 += 32) {
-                    const uint32_t b = b0 + tid;
-                    uint32_t ci = 0, cn = 0;
-                    if (b <= S) {
-                        ci = (uint32_t)((volatile int32_t*)a.hist_inc)[b];
-                        cn = ((volatile uint32_t*)a.hist_new)[b];
-                    }
-                    const uint32_t v = ci + cn;
-                    const uint32_t incl = warp_incl_scan(v) + cum;
-                    const unsigned hit = __ballot_sync(0xffffffffu, b <= S && incl >= K);
-                    if (hit) {
-                        const int ln = __ffs(hit) - 1;
-                        if ((int)tid == ln) {
-                            sm.bc[0] = b;
-                            sm.bc[1] = K - (incl - v);
-                            sm.bc[2] = ci;
-                            sm.bc[3] = cn;
-                        }
-                        done = true;
-                    }
-                    cum = __shfl_sync(0xffffffffu, incl, 31);
-                }
+        uint32_t m, mpre;  // misses this iteration, misses in earlier chunks
+        {
+            uint32_t pre = 0, tot = 0;
+            for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
+                const uint32_t v = a.chunk_miss[c];
+                if (c < blockIdx.x) pre += v;
+                tot += v;
             }
-            __syncthreads();
-            bstar = sm.bc[0];
-            r = sm.bc[1];
-            inc_b = sm.bc[2];
-            new_b = sm.bc[3];
-            __syncthreads();
-            if (r <= inc_b) sel = (r > 0 && r < inc_b) ? 1 : 0;
-            else sel = (r - inc_b < new_b) ? 2 : 0;
+            mpre = block_sum(pre, sm.scan);
+            m = block_sum(tot, sm.scan);
         }
+        const bool cut = (uint64_t)nres + m > K;
+
+        if (!cut) {
+            // ALLIN fast path: keep = |cand| (changeset.hpp:284), every miss is
+            // admitted in position order into the next free slots (no evictions)
+            uint32_t k = mpre;
+            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {
+                const uint32_t pos = p0 + tid;
+                const uint32_t f = pos < c1 ? a.pmiss[pos] : 0;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan(f, sm.scan, tot);
+                if (f) {
+                    const uint32_t r = k + ex, s = nres + r;
+                    const uint32_t v = a.trace[base + pos];
+                    const uint32_t key = a.pkey[pos];
+                    a.slot_node[s] = v;
+                    a.slot_key[s] = key;
+                    a.node_slot[v] = (int32_t)s;
+                    atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
+                    a.o_in_ids[in_total + r] = v;
+                    a.o_in_pos[in_total + r] = pos;
+                    a.o_in_slot[in_total + r] = s;
+                }
+                k += tot;
+            }
+            hist_flush(sm.hinc, a.hist_inc, S + 1);
+            for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+            if (gtid == 0) {
+                a.o_misses[i] = m;
+                ns->n_res = nres + m;
+                ns->in_total = in_total + m;
+                ns->out_total = out_total;
+                ns->n_out = 0;
+                ns->n_c = 0;
+                a.o_in_off[i + 1] = in_total + m;
+                a.o_out_off[i + 1] = out_total;
+            }
+            grid_sync(a.bar);
+            continue;
+        }
+
+        // CUT: threshold bucket b* over keys in (i, S] (every CTA, redundantly)
+        uint32_t bstar = 0, r = 0, inc_b = 0, new_b = 0;
+        if (tid < 32) {
+            uint32_t cum = 0;
+            bool done = false;
+            for (uint32_t b0 = i + 1; b0 <= S && !done; b0 += 32) {
+                const uint32_t b = b0 + tid;
+                uint32_t ci = 0, cn = 0;
+                if (b <= S) {
+                    ci = (uint32_t)((volatile int32_t*)a.hist_inc)[b];
+                    cn = ((volatile uint32_t*)a.hist_new)[b];
+                }
+                const uint32_t v = ci + cn;
+                const uint32_t incl = warp_incl_scan(v) + cum;
+                const unsigned hit = __ballot_sync(0xffffffffu, b <= S && incl >= K);
+                if (hit) {
+                    const int ln = __ffs(hit) - 1;
+                    if ((int)tid == ln) {
+                        sm.bc[0] = b;
+                        sm.bc[1] = K - (incl - v);
+                        sm.bc[2] = ci;
+                        sm.bc[3] = cn;
+                    }
+                    done = true;
+                }
+                cum = __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+        bstar = sm.bc[0];
+        r = sm.bc[1];
+        inc_b = sm.bc[2];
+        new_b = sm.bc[3];
+        __syncthreads();
+        int sel = 0;  // 1: select among incumbents of b*, 2: among new candidates of b*
+        if (r <= inc_b) sel = (r > 0 && r < inc_b) ? 1 : 0;
+        else sel = (r - inc_b < new_b) ? 2 : 0;
         // keep rule inside b*: incumbents kept = min(r, inc_b) smallest ids;
-        // new admitted = max(0, r - inc_b) smallest ids.
+        // new admitted = max(0, r - inc_b) smallest ids (finish_selection order)
         const uint32_t keep_inc = min(r, inc_b);
         const uint32_t admit_new = r > inc_b ? r - inc_b : 0;
         uint32_t thr = 0xFFFFFFFFu;
 
-        if (cut) {
-            // P3: evict buckets > b*; collect selection candidates of b*
-            for (uint32_t s = gtid; s < nres; s += G) {
-                const uint32_t bk = bucket_of(a.slot_key[s], S);
-                const uint32_t v = a.slot_node[s];
-                const bool ev = bk > bstar || (bk == bstar && keep_inc == 0);
-                if (__any_sync(__activemask(), ev)) {
-                    const uint32_t o = agg_append(&a.st->n_out, ev);
-                    if (ev) {
-                        a.out_node[o] = v;
-                        a.out_slot[o] = s;
-                    }
+        // P3: evict buckets > b*; collect the selection candidates of b*
+        for (uint32_t s = gtid; s < nres; s += G) {
+            const uint32_t bk = bucket_of(a.slot_key[s], S);
+            const uint32_t v = a.slot_node[s];
+            const bool ev = bk > bstar || (bk == bstar && keep_inc == 0);
+            if (__any_sync(__activemask(), ev)) {
+                const uint32_t o = agg_append(&cs->n_out, ev);
+                if (ev) {
+                    a.out_node[o] = v;
+                    a.out_slot[o] = s;
                 }
-                if (sel == 1) {
-                    const bool c = bk == bstar;
-                    if (__any_sync(__activemask(), c)) {
-                        const uint32_t o = agg_append(&a.st->n_c, c);
-                        if (c) {
-                            a.c_id[o] = v;
-                            a.c_ref[o] = s;
-                            atomicAdd(&a.rh[v >> 21], 1u);
-                        }
+            }
+            if (sel == 1) {
+                const bool c = bk == bstar;
+                if (__any_sync(__activemask(), c)) {
+                    const uint32_t o = agg_append(&cs->n_c, c);
+                    if (c) {
+                        a.c_id[o] = v;
+                        a.c_ref[o] = s;
+                        atomicAdd(&a.rh[v >> 21], 1u);
                     }
                 }
             }
-            if (sel == 2) {
-                for (uint32_t pos = gtid; pos < ni; pos += G) {
-                    const bool c = a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar;
-                    if (__any_sync(__activemask(), c)) {
-                        const uint32_t o = agg_append(&a.st->n_c, c);
-                        if (c) {
-                            const uint32_t v = a.trace[base + pos];
-                            a.c_id[o] = v;
-                            a.c_ref[o] = pos;
-                            atomicAdd(&a.rh[v >> 21], 1u);
-                        }
+        }
+        if (sel == 2) {
+            for (uint32_t pos = gtid; pos < ni; pos += G) {
+                const bool c = a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar;
+                if (__any_sync(__activemask(), c)) {
+                    const uint32_t o = agg_append(&cs->n_c, c);
+                    if (c) {
+                        const uint32_t v = a.trace[base + pos];
+                        a.c_id[o] = v;
+                        a.c_ref[o] = pos;
+                        atomicAdd(&a.rh[v >> 21], 1u);
                     }
                 }
+            }
+        }
+        grid_sync(a.bar);
+        if (sel) {  // exact radix select of the cut id (11/11/10-bit digits)
+            const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+            uint32_t want = sel == 1 ? keep_inc : admit_new, left;
+            const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
+            for (uint32_t k = gtid; k < nc; k += G) {
+                const uint32_t v = a.c_id[k];
+                if ((v >> 21) == d1) atomicAdd(&a.rh[2048 + ((v >> 10) & 2047)], 1u);
             }
             grid_sync(a.bar);
-            if (sel) {
-                const uint32_t nc = *(volatile uint32_t*)&a.st->n_c;
-                uint32_t want = sel == 1 ? keep_inc : admit_new, left;
-                const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
-                for (uint32_t k = gtid; k < nc; k += G) {
-                    const uint32_t v = a.c_id[k];
-                    if ((v >> 21) == d1) atomicAdd(&a.rh[2048 + ((v >> 10) & 2047)], 1u);
-                }
-                grid_sync(a.bar);
-                const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
-                const uint32_t pre = (d1 << 11) | d2;
-                for (uint32_t k = gtid; k < nc; k += G) {
-                    const uint32_t v = a.c_id[k];
-                    if ((v >> 10) == pre) atomicAdd(&a.rh[4096 + (v & 1023)], 1u);
-                }
-                grid_sync(a.bar);
-                const uint32_t d3 = hist_select(a.rh + 4096, 1024, left, &left, sm);
-                thr = (pre << 10) | d3;
+            const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
+            const uint32_t pre = (d1 << 11) | d2;
+            for (uint32_t k = gtid; k < nc; k += G) {
+                const uint32_t v = a.c_id[k];
+                if ((v >> 10) == pre) atomicAdd(&a.rh[4096 + (v & 1023)], 1u);
             }
+            grid_sync(a.bar);
+            const uint32_t d3 = hist_select(a.rh + 4096, 1024, left, &left, sm);
+            thr = (pre << 10) | d3;
         }
 
         // P4: per-chunk count of insertions (position order); b* evictions
         auto in_flag = [&](uint32_t pos) -> bool {
             if (!a.pmiss[pos]) return false;
-            if (!cut) return true;
             const uint32_t bk = bucket_of(a.pkey[pos], S);
             if (bk != bstar) return bk < bstar;
             if (admit_new == 0) return false;
             if (sel != 2) return true;
             return a.trace[base + pos] <= thr;
         };
-        const uint32_t chunk = (ni + gridDim.x - 1) / gridDim.x;
-        const uint32_t c0 = min(ni, blockIdx.x * chunk), c1 = min(ni, c0 + chunk);
         {
             uint32_t c = 0;
             for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) c += in_flag(pos);
             c = block_sum(c, sm.scan);
-            if (tid == 0) a.chunk_cnt[blockIdx.x] = c;
+            if (tid == 0) a.chunk_in[blockIdx.x] = c;
             if (sel == 1) {
-                const uint32_t nc = *(volatile uint32_t*)&a.st->n_c;
+                const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
                 for (uint32_t k = gtid; k < nc; k += G) {
                     const bool ev = a.c_id[k] > thr;
                     if (__any_sync(__activemask(), ev)) {
-                        const uint32_t o = agg_append(&a.st->n_out, ev);
+                        const uint32_t o = agg_append(&cs->n_out, ev);
                         if (ev) {
                             a.out_node[o] = a.c_id[k];
                             a.out_slot[o] = a.c_ref[k];
@@ -462,12 +590,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
 
-        // P5: ordered in-list; sort out-list by node id
+        // P5: ordered in-list; out-list sorted by node id
         uint32_t n_in;
         {
             uint32_t pre = 0, tot_all = 0;
             for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
-                const uint32_t v = a.chunk_cnt[c];
+                const uint32_t v = a.chunk_in[c];
                 if (c < blockIdx.x) pre += v;
                 tot_all += v;
             }
@@ -487,7 +615,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                 k += tot;
             }
         }
-        const uint32_t n_out = *(volatile uint32_t*)&a.st->n_out;
+        const uint32_t n_out = *(volatile uint32_t*)&cs->n_out;
         if (n_out <= SORT_SMALL) {
             if (blockIdx.x == 0 && n_out > 1) {
                 uint32_t P = 1;
@@ -582,20 +710,20 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         if (gtid == 0) {
             if (n_out > n_in) atomicOr(&a.st->err, 4u);
             a.o_misses[i] = m;
-            a.st->n_res = nres + n_in - n_out;
-            a.st->in_total = in_total + n_in;
-            a.st->out_total = out_total + n_out;
+            ns->n_res = nres + n_in - n_out;
+            ns->in_total = in_total + n_in;
+            ns->out_total = out_total + n_out;
+            ns->n_out = 0;
+            ns->n_c = 0;
             a.o_in_off[i + 1] = in_total + n_in;
             a.o_out_off[i + 1] = out_total + n_out;
-            a.st->miss = 0;
-            a.st->n_out = 0;
-            a.st->n_c = 0;
         }
         grid_sync(a.bar);
     }
     // leave node_slot clean
-    const uint32_t nfin = a.st->n_res;
+    const uint32_t nfin = a.st[S & 1].n_res;
     for (uint32_t s = gtid; s < nfin; s += G) a.node_slot[a.slot_node[s]] = -1;
+    if (gtid == 0) a.st->n_res = nfin;  // final resident count for the host
 }
 
 // ---------------------------------------------------------------------------
@@ -666,11 +794,20 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.in_node.reserve(maxw);
     B.in_pos.reserve(maxw);
     const int grid = ctx->num_sms;
-    B.chunk_cnt.reserve(grid);
+    B.chunk_cnt.reserve(2 * grid);
     B.bm_cnt.reserve(grid);
     B.st.reserve(16);
-    GX_CUDA(cudaMemsetAsync(B.st.p, 0, sizeof(IState), st));
-    static_assert(sizeof(IState) <= 16 * sizeof(uint32_t), "IState fits the scratch words");
+    GX_CUDA(cudaMemsetAsync(B.st.p, 0, 2 * sizeof(IState), st));
+    static_assert(2 * sizeof(IState) <= 16 * sizeof(uint32_t), "2 IStates fit the scratch words");
+    B.isfirst.reserve(std::max<uint64_t>(A, 1));
+    // per-node iteration bitmask (next use in 3 grid steps) when it fits the budget
+    const uint64_t W = (S + 63) / 64;
+    const bool use_bits = S > 0 && N * W * 8 <= (8ull << 30);
+    if (use_bits && is.bits_words < N * W) {
+        is.bits.alloc(N * W);
+        GX_CUDA(cudaMemsetAsync(is.bits.p, 0, N * W * 8, st));
+        is.bits_words = N * W;
+    }
 
     out->ctx = ctx;
     out->S = S;
@@ -691,6 +828,14 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         for (int64_t k = 0; k < n_init_explicit; ++k) i32[k] = (uint32_t)h_init[k];
         B.init_ext.reserve(i32.size());
         GX_CUDA(cudaMemcpyAsync(B.init_ext.p, i32.data(), n_init_explicit * 4, cudaMemcpyHostToDevice, st));
+        if (is.init_pos_n < N) {
+            is.init_pos.alloc(N);
+            GX_CUDA(cudaMemsetAsync(is.init_pos.p, 0xff, N * 4, st));
+            is.init_pos_n = N;
+        }
+        if (n_init_explicit)
+            k_init_pos<<<ctx->num_sms, 256, 0, st>>>(B.init_ext.p, (uint32_t)n_init_explicit, is.init_pos.p, 1);
+        GX_CHECK_LAUNCH();
     }
 
     IArgs a{};
@@ -720,7 +865,13 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.c_ref = B.c_ref.p;
     a.in_node = B.in_node.p;
     a.in_pos = B.in_pos.p;
-    a.chunk_cnt = B.chunk_cnt.p;
+    a.chunk_miss = B.chunk_cnt.p;
+    a.chunk_in = B.chunk_cnt.p + grid;
+    a.isfirst = B.isfirst.p;
+    a.bits = use_bits ? is.bits.p : nullptr;
+    a.W = (uint32_t)W;
+    a.use_bits = use_bits;
+    a.init_pos = n_init_explicit >= 0 ? is.init_pos.p : nullptr;
     a.bm_words = B.bm_words.p;
     a.nwords = (uint32_t)((N + 31) / 32);
     a.bm_cnt = B.bm_cnt.p;
@@ -751,6 +902,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     GX_CUDA(cudaLaunchCooperativeKernel((void*)k_inspect, dim3(grid), dim3(IN_THREADS), args, smem, st));
     GX_CHECK_LAUNCH();
 
+    if (n_init_explicit > 0)
+        k_init_pos<<<ctx->num_sms, 256, 0, st>>>(B.init_ext.p, (uint32_t)n_init_explicit, is.init_pos.p, 0);
     IState hs;
     GX_CUDA(cudaMemcpyAsync(&hs, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
     std::vector<uint32_t>&m32 = B.h_m, &io32 = B.h_io, &oo32 = B.h_oo;
@@ -764,8 +917,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     if (hs.err & 3u) {
         std::vector<uint32_t> flat(A);
         GX_CUDA(cudaMemcpy(flat.data(), is.trace.p, A * 4, cudaMemcpyDeviceToHost));
-        // the kernel bailed out before touching node_slot; `last` may be dirty
+        // the kernel bailed out before touching node_slot; `last`/`bits` may be dirty
         GX_CUDA(cudaMemset(is.last.p, 0xff, N * 4));
+        if (use_bits) GX_CUDA(cudaMemset(is.bits.p, 0, N * W * 8));
         host_trace_error(flat, off, N);
     }
     if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");

@@ -166,6 +166,58 @@ __device__ __forceinline__ uint32_t resolve_pos(const uint32_t* pk, uint32_t j, 
     }
 }
 
+// Positions of a parent's tk draws (partial Fisher-Yates, sampler.hpp:103-107)
+// written as (position, parent) into out[0..tk). Fast path (tk <= 16): picks in
+// registers; a 64-bit filter over the low pick bits proves most picks
+// collision-free (then the child sits at the picked position), the rest
+// resolve the swap chain exactly over the register array.
+__device__ __forceinline__ void draw_positions(uint32_t tk, uint64_t seed, uint64_t t0, uint32_t deg,
+                                               uint2* out, uint32_t parent) {
+    constexpr int MAXT = 16;
+    if (tk <= MAXT) {
+        uint32_t pk[MAXT];
+#pragma unroll
+        for (int q = 0; q < MAXT; ++q) pk[q] = (uint32_t)q < tk ? pick_at(seed, t0, q, deg) : 0xFFFFFFFFu;
+        unsigned long long filt = 0;
+#pragma unroll
+        for (int q = 0; q < MAXT; ++q) {
+            if ((uint32_t)q < tk) {
+                uint32_t c = pk[q];
+                const unsigned long long bit = 1ull << (c & 63);
+                if (filt & bit) {
+                    int lim = q;
+                    while (true) {
+                        int found = -1;
+#pragma unroll
+                        for (int i = 0; i < MAXT; ++i)
+                            if (i < lim && pk[i] == c) found = i;  // latest i < lim
+                        if (found < 0) break;
+                        c = (uint32_t)found;
+                        lim = found;
+                    }
+                }
+                filt |= bit;
+                out[q] = make_uint2(c, parent);
+            }
+        }
+    } else {
+        uint32_t pk[kPickCache];
+        for (uint32_t q = 0; q < (uint32_t)kPickCache; ++q) pk[q] = pick_at(seed, t0, q, deg);
+        for (uint32_t q = 0; q < tk; ++q) out[q] = make_uint2(resolve_pos(pk, q, seed, t0, deg), parent);
+    }
+}
+
+// Clear the first H entries of each of the S per-batch tables (16-byte stores).
+__device__ __forceinline__ void clear_region(unsigned long long* tab, uint64_t tab_cap, uint32_t H, uint32_t S) {
+    const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
+    const uint64_t per = H / 2;  // ulonglong2 per batch (H is a power of two >= 1024)
+    const ulonglong2 e = make_ulonglong2(kEmptySlot, kEmptySlot);
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < (uint64_t)S * per; x += total_threads) {
+        const uint64_t b = x / per, o = x - b * per;
+        reinterpret_cast<ulonglong2*>(tab + b * tab_cap)[o] = e;
+    }
+}
+
 __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
     extern __shared__ unsigned char smem_raw[];
     SampSmem& sm = *reinterpret_cast<SampSmem*>(smem_raw);
@@ -218,12 +270,14 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                         a.ids[gi] = v;
                     } else {
                         v = a.ids[gi];
-                        told[(uint64_t)b * a.tab_cap + a.idslot[gi]] = kEmptySlot;
                     }
                     a.idslot[gi] = table_insert(tnew + (uint64_t)b * a.tab_cap, newH, v, (uint32_t)k);
                 }
             }
-            if (l > 0) cur ^= 1;
+            if (l > 0) {  // the previous layer's table is dead: bulk-clear its used region
+                clear_region(told, a.tab_cap, H, S);
+                cur ^= 1;
+            }
             H = newH;
             if (l == 0) {
                 for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
@@ -310,27 +364,30 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                 unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
                 uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
                 uint32_t* bdslot = a.dslot + (uint64_t)b * a.cap_draw;
+                const uint32_t d_begin = off;  // this thread's first draw
+                // E1 (per parent, registers only): FY positions of every draw,
+                // staged as (position, parent) in the edge slot.
                 for (int j = 0; j < SB_IPT; ++j) {
-                    const uint32_t k = k0 + j;
                     const uint32_t tk = take[j];
                     if (tk) {
-                        const uint64_t gi = (uint64_t)b * a.cap_ids + k;
-                        const uint64_t lo = a.plo[gi];
-                        const uint32_t deg = a.pdeg[gi];
-                        const uint64_t t0 = dbase + off;
-                        uint32_t pk[kPickCache];
-                        const uint32_t nc = min(tk, (uint32_t)kPickCache);
-                        for (uint32_t q = 0; q < nc; ++q) pk[q] = pick_at(seed, t0, q, deg);
-                        for (uint32_t q = 0; q < tk; ++q) {
-                            const uint32_t pos = resolve_pos(pk, q, seed, t0, deg);
-                            const uint32_t child = __ldg(a.indices + lo + pos);
-                            const uint32_t p = off + q;
-                            bedge[p] = make_uint2(child, k);
-                            bdslot[p] = table_insert(btab, H, child, kNewBit | p);
-                        }
+                        const uint64_t gi = (uint64_t)b * a.cap_ids + k0 + j;
+                        draw_positions(tk, seed, dbase + off, a.pdeg[gi], bedge + off, k0 + j);
                     }
                     off += tk;
                 }
+                (void)d_begin;
+                __syncthreads();  // the tile's staged draws are visible to the whole CTA
+                // E2 (per draw): child read, edge, dedup insert -- one draw per
+                // thread so the random reads and atomics of a tile overlap.
+                const uint32_t tile_d0 = toff, tile_d1 = toff + tot;
+                for (uint32_t p = tile_d0 + tid; p < tile_d1; p += blockDim.x) {
+                    const uint2 st = bedge[p];
+                    const uint64_t lo = a.plo[(uint64_t)b * a.cap_ids + st.y];
+                    const uint32_t child = __ldg(a.indices + lo + st.x);
+                    bedge[p] = make_uint2(child, st.y);
+                    bdslot[p] = table_insert(btab, H, child, kNewBit | p);
+                }
+                __syncthreads();
             }
         }
         grid_sync(a.bar);
@@ -429,16 +486,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
         grid_sync(a.bar);
     }
 
-    // ---- leave the live table clean for the next call -----------------------
-    {
-        unsigned long long* tab = cur ? a.tab1 : a.tab0;
-        const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
-        for (uint32_t b = 0; b < S; ++b) {
-            const uint32_t nb = a.n_ids[b];
-            for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + tid; k < nb; k += total_threads)
-                tab[(uint64_t)b * a.tab_cap + a.idslot[(uint64_t)b * a.cap_ids + k]] = kEmptySlot;
-        }
-    }
+    // ---- leave the live table clean for the next call (coalesced bulk clear) ----
+    clear_region(cur ? a.tab1 : a.tab0, a.tab_cap, H, S);
 }
 
 static uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t cap) {
