@@ -392,7 +392,7 @@ def main():
                 "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
                 "d2h_bytes_per_step": int(8 * S + 8 * 16)},
         "gpu_launches": (2 * S + 4) * args.steps,
-        "roofline": {"kernel": "k_gather<16>", "bound": "hbm", "achieved": achieved, "peak": peak,
+        "roofline": {"kernel": "k_gather_tma2 (TMA bulk row gather)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
                      "bytes_per_row": 2 * w + 16, "rows_per_launch": rows / (n * S)},

@@ -449,7 +449,7 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
         // the inspector resolved every access's serving slot (is.acc_slot), so
         // the executor needs no address table on this path
         launch_cache_init(ctx, p->cs.init.p, (uint32_t)p->cs.n_init, nullptr, p->f, p->cache_rows.p,
-                          p->counters.p + 8 * S + 2);
+                          p->counters.p + 8 * S);
         GX_CUDA(cudaEventRecord(p->ev[3], st));
         // (4) main loop: gather + apply (the ids of iteration i are batch i's ids)
         while (p->kev.size() < 3 * S) {

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_gather_rows
         const uint8_t* src = nullptr;
         if (lane < nr) {
             const uint32_t v = __ldg(ids + r0 + lane);
-            const uint32_t s = __ldg(slots + r0 + lane);
+            const uint32_t s = slots ? __ldg(slots + r0 + lane) : kNever;
             if (s != kNever) {
                 src = cache_rows + (uint64_t)s * row_bytes;
                 ++hits;
@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(128) k_gather_tma(const uint32_t* __restrict__
     uint32_t hits = 0, misses = 0, pages = 0;
     for (uint32_t r = blockIdx.x * blockDim.x + tid; r < n; r += gridDim.x * blockDim.x) {
         const uint32_t v = __ldg(ids + r);
-        const uint32_t s = __ldg(slots + r);
+        const uint32_t s = slots ? __ldg(slots + r) : kNever;
         const uint8_t* src;
         if (s != kNever) {
             src = cache_rows + (uint64_t)s * row_bytes;
@@ -200,7 +200,7 @@ __device__ __forceinline__ const uint8_t* gather_src(const uint32_t* ids, const 
                                                      uint32_t row_bytes, uint32_t& hits, uint32_t& misses,
                                                      uint32_t& pages) {
     const uint32_t v = __ldg(ids + r);
-    const uint32_t s = __ldg(slots + r);
+    const uint32_t s = slots ? __ldg(slots + r) : kNever;
     if (s != kNever) {
         ++hits;
         return cache_rows + (uint64_t)s * row_bytes;
@@ -362,26 +362,6 @@ __global__ void k_apply(const uint32_t* __restrict__ in_ids, const uint32_t* __r
     }
 }
 
-// cache init: slots 0..n-1 <- rows of init ids (FeatureCache ctor, feature_cache.hpp:30-36)
-template <int VEC>
-__global__ void k_cache_init(const uint32_t* __restrict__ init, uint32_t n, int32_t* table,
-                             const uint8_t* __restrict__ store, uint8_t* cache_rows, uint64_t row_bytes,
-                             unsigned long long* pages) {
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t lane = threadIdx.x & 31;
-    unsigned long long pg = 0;
-    for (uint64_t k = warp; k < n; k += nwarps) {
-        const uint32_t v = init[k];
-        warp_copy_row<VEC>(store + (uint64_t)v * row_bytes, cache_rows + k * row_bytes, row_bytes);
-        if (lane == 0) {
-            if (table) table[v] = (int32_t)k;
-            pg += pages_touched((uint64_t)v * row_bytes, (uint64_t)(v + 1) * row_bytes);
-        }
-    }
-    if (lane == 0 && pg) atomicAdd(pages, pg);
-}
-
 __global__ void k_iota_desc(uint32_t* p, uint64_t n, uint64_t K) {
     // free list [K-1, K-2, ..., K-n]: back() pops ascending from K-n
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -512,17 +492,22 @@ void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_
     GX_CHECK_LAUNCH();
 }
 
+// FeatureCache ctor prefetch (feature_cache.hpp:30-36): cache slot k <- row
+// init[k] of the store, i.e. an all-miss gather into the slot array (the TMA
+// gather kernel), plus the address table when the caller keeps one.
+__global__ void k_set_table(const uint32_t* __restrict__ init, uint32_t n, int32_t* table) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        table[init[k]] = (int32_t)k;
+}
+
 void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table, const gx_features* f,
-                       uint8_t* cache_rows, unsigned long long* pages) {
+                       uint8_t* cache_rows, unsigned long long* counters) {
     if (!n) return;
-    const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)n * 32 + 255) / 256, ctx->num_sms * 8);
-    if (vec16(f->row_bytes))
-        k_cache_init<16><<<blocks, 256, 0, ctx->stream>>>(init, n, table, f->rows_dev_view, cache_rows, f->row_bytes,
-                                                          pages);
-    else
-        k_cache_init<4><<<blocks, 256, 0, ctx->stream>>>(init, n, table, f->rows_dev_view, cache_rows, f->row_bytes,
-                                                         pages);
-    GX_CHECK_LAUNCH();
+    launch_gather_resolved(ctx, init, nullptr, n, nullptr, f, cache_rows, counters);
+    if (table) {
+        k_set_table<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(init, n, table);
+        GX_CHECK_LAUNCH();
+    }
 }
 
 void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table) {
@@ -612,7 +597,7 @@ gx_status gx_cache_create(gx_features* f, const uint64_t* init, uint64_t n_init,
             c->scratch.alloc(std::max<uint64_t>(n_init, 1));
             upload_u32(ctx, c->scratch, 0, init, n_init);
             GX_CUDA(cudaMemsetAsync(c->counters.p, 0, 8 * 8, ctx->stream));
-            launch_cache_init(ctx, c->scratch.p, (uint32_t)n_init, c->table.p, f, c->rows.p, c->counters.p + 2);
+            launch_cache_init(ctx, c->scratch.p, (uint32_t)n_init, c->table.p, f, c->rows.p, c->counters.p);
             unsigned long long pg = 0;
             GX_CUDA(cudaMemcpyAsync(&pg, c->counters.p + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
             GX_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -140,8 +140,9 @@ void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_
                         const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
                         uint32_t n_out, int32_t* table, const uint8_t* batch, uint8_t* cache_rows,
                         uint64_t row_bytes);
+// counters: 5 words as for the gather (init rows are charged as misses)
 void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table,
-                       const gx_features* f, uint8_t* cache_rows, unsigned long long* pages);
+                       const gx_features* f, uint8_t* cache_rows, unsigned long long* counters);
 void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table);
 void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t row_bytes,
                    unsigned long long* out);
