@@ -50,6 +50,11 @@ CONFIGS = {
                    S=100, cache_frac=0.20, train_fraction=0.1,
                    workload="ogbn-papers100M-shape synthetic R-MAT: 111M nodes, ~1.6B edges, "
                             "128-d fp32, fanout (10,10,10), batch 1000, superbatch 100, cache 20%"),
+    # configs[2]: com-friendster shape, 256-d features (1 KB rows, 67 GB table); K unspecified -> 10 %
+    "friendster": dict(N=65_608_366, avg_degree=27.9, dim=256, fanouts=[10, 10, 10], batch=1000,
+                       S=100, cache_frac=0.10, train_fraction=0.1,
+                       workload="com-friendster-shape synthetic R-MAT: 65.6M nodes, ~1.8B edges, "
+                                "256-d fp32, fanout (10,10,10), batch 1000, superbatch 100, cache 10%"),
     # configs[0]: the reference's own CPU-runnable case
     "cfg1": dict(N=1_000_000, avg_degree=10.0, dim=128, fanouts=[10, 10, 10], batch=1000, S=100,
                  cache_frac=0.10, train_fraction=0.1,

@@ -196,7 +196,7 @@ gx_status gx_precompute_trace(gx_ctx* ctx, const uint64_t* flat, const uint64_t*
         inspect_fill_from_host(ctx, flat + off[0], o, N);
         auto cs = new gx_changesets();
         try {
-            inspect_run(ctx, o, N, K, nullptr, -1, cs);
+            inspect_run(ctx, o, N, K, nullptr, -1, cs, false);
         } catch (...) {
             delete cs;
             throw;
@@ -228,7 +228,7 @@ gx_status gx_simulate_trace(gx_ctx* ctx, const uint64_t* flat, const uint64_t* o
         }
         auto cs = new gx_changesets();
         try {
-            inspect_run(ctx, o, N, K, init, (int64_t)n_init, cs);
+            inspect_run(ctx, o, N, K, init, (int64_t)n_init, cs, false);
         } catch (...) {
             delete cs;
             throw;
@@ -244,7 +244,7 @@ gx_status gx_precompute_samples(const gx_samples* s, uint64_t N, uint64_t K, gx_
         inspect_fill_from_device(s->ctx, s->ids.p, s->cap_ids, o);
         auto cs = new gx_changesets();
         try {
-            inspect_run(s->ctx, o, N, K, nullptr, -1, cs);
+            inspect_run(s->ctx, o, N, K, nullptr, -1, cs, true);
         } catch (...) {
             delete cs;
             throw;
@@ -434,7 +434,7 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
         std::vector<uint64_t> o(S + 1, 0);
         for (uint64_t i = 0; i < S; ++i) o[i + 1] = o[i] + p->samples.h_n_ids[i];
         inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, o);
-        inspect_run(ctx, o, N, p->K, nullptr, -1, &p->cs);
+        inspect_run(ctx, o, N, p->K, nullptr, -1, &p->cs, true);
         GX_CUDA(cudaEventRecord(p->ev[2], st));
         // (3) switch: cache init
         uint64_t maxw = 0;

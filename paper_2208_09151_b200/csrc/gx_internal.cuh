@@ -123,8 +123,9 @@ void inspect_fill_from_device(gx_ctx* ctx, const uint32_t* d_ids, uint64_t strid
                               const std::vector<uint64_t>& off);
 void inspect_fill_from_host(gx_ctx* ctx, const uint64_t* flat, const std::vector<uint64_t>& off,
                             uint64_t N);
+// trusted: the trace comes from the sampler (ids < N, distinct per iteration)
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
-                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out);
+                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted);
 void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t* h_iters,
                       uint64_t* h_ptr);
 

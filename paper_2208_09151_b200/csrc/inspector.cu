@@ -72,6 +72,7 @@ struct IArgs {
     uint32_t* chunk_miss;  // gridDim
     uint32_t* chunk_in;    // gridDim
     const int32_t* init_pos;  // N: slot of an explicit init id, -1 otherwise
+    int trusted;              // trace produced by the sampler (ids < N, distinct per iteration)
     uint32_t* out_node;  // maxw
     uint32_t* out_slot;  // maxw
     uint32_t* c_id;      // max(K, maxw)
@@ -118,6 +119,43 @@ __global__ void k_init_pos(const uint32_t* init, uint32_t n, int32_t* pos, int s
         pos[init[k]] = set ? (int32_t)k : -1;
 }
 
+// Block-staged append: entries are staged in shared memory (warp-aggregated
+// shared atomics) and published with ONE global atomic per >= 1024 entries,
+// so grid-wide list building never serializes on a single global counter.
+struct Stage {
+    unsigned long long* buf;  // 2048 staged (a << 32 | b) pairs
+    uint32_t* cnt;            // shared counter
+};
+__device__ __forceinline__ void stage_put(Stage st, bool pred, uint32_t a, uint32_t b) {
+    const unsigned active = __activemask();
+    const unsigned m = __ballot_sync(active, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(st.cnt, (uint32_t)__popc(m));
+    base = __shfl_sync(active, base, leader);
+    if (pred) st.buf[base + __popc(m & ((1u << lane) - 1))] = ((unsigned long long)a << 32) | b;
+}
+// Called by the whole CTA after __syncthreads; flushes when `force` or when
+// another round could overflow the 2048-entry stage.
+__device__ __forceinline__ void stage_flush(Stage st, uint32_t* gcnt, uint32_t* ga, uint32_t* gb, bool force,
+                                            uint32_t* bcast) {
+    const uint32_t n = *st.cnt;
+    __syncthreads();  // every thread has read n before anyone appends again
+    if (n == 0 || (!force && n < 1024)) return;
+    if (threadIdx.x == 0) *bcast = atomicAdd(gcnt, n);
+    __syncthreads();
+    const uint32_t base = *bcast;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const unsigned long long e = st.buf[k];
+        ga[base + k] = (uint32_t)(e >> 32);
+        gb[base + k] = (uint32_t)e;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *st.cnt = 0;
+    __syncthreads();
+}
+
 struct ISmem {
     uint32_t scan[34];
     uint32_t bc[16];
@@ -125,6 +163,7 @@ struct ISmem {
     uint32_t toff[kMaxIters + 1];
     int32_t hinc[kMaxIters + 1];  // per-CTA histogram deltas, flushed with one atomic per bin
     int32_t hnew[kMaxIters + 1];
+    int32_t rh[2048];             // per-CTA radix-select digit histogram
 };
 
 __device__ __forceinline__ void hist_flush(int32_t* loc, int32_t* glob, uint32_t n) {
@@ -181,22 +220,17 @@ __device__ uint32_t hist_select(const uint32_t* h, uint32_t nbins, uint32_t r, u
     return bin;
 }
 
-__global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
-    extern __shared__ unsigned char smem_raw[];
-    ISmem& sm = *reinterpret_cast<ISmem*>(smem_raw);
-    const uint32_t S = a.S, K = a.K;
+// Next use of every access (and, with `firsts`, the first-occurrence flags
+// and their per-tile counts, plus the reference's trace checks: ids < N and
+// distinct per iteration, count_pass changeset.hpp:76-88). Small S: per-node
+// iteration bitmask (3 grid steps); large S: backward pass, one grid step per
+// iteration. Returns false if the trace is invalid (host reports the error).
+__device__ bool next_use_pass(const IArgs& a, ISmem& sm, bool firsts) {
+    const uint32_t S = a.S;
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x * blockDim.x;
     const uint32_t gtid = blockIdx.x * blockDim.x + tid;
-    for (uint32_t i = tid; i <= S; i += blockDim.x) {
-        sm.toff[i] = a.toff[i];
-        sm.hinc[i] = 0;
-        sm.hnew[i] = 0;
-    }
-    __syncthreads();
     const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
-
-    // ---- next use and first occurrence of every access ---------------------
     if (a.use_bits) {
         // per-node bitmask of the iterations it appears in: set, read, clear
         // (3 grid steps instead of one per iteration)
@@ -212,7 +246,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             if (old & bit) atomicOr(&a.st->err, 2u);
         }
         grid_sync(a.bar);
-        if (a.st->err) return;  // host reports the exact reference error
+        if (a.st->err) return false;  // host reports the exact reference error
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
@@ -238,12 +272,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                     }
                     a.next_use[x] = nu;
                     const uint8_t f = first == i;
-                    a.isfirst[x] = f;
+                    if (firsts) a.isfirst[x] = f;
                     c += f;
                 }
             }
             const uint32_t tot = block_sum(c, sm.scan);
-            if (tid == 0) a.tile_cnt[t] = tot;
+            if (firsts && tid == 0) a.tile_cnt[t] = tot;
         }
         grid_sync(a.bar);
         for (uint32_t x = gtid; x < a.A; x += G) {  // leave the bitmask clean
@@ -267,7 +301,52 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             }
             grid_sync(a.bar);
         }
-        if (a.st->err) return;
+        if (a.st->err) return false;
+        for (uint32_t t = blockIdx.x; firsts && t < ntiles; t += gridDim.x) {
+            uint32_t c = 0;
+            const uint32_t x0 = t * IN_TILE + tid * 4;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t x = x0 + j;
+                if (x < a.A) {
+                    const uint8_t f = a.last[a.trace[x]] == iter_of(sm, S, x);
+                    a.isfirst[x] = f;
+                    c += f;
+                }
+            }
+            const uint32_t tot = block_sum(c, sm.scan);
+            if (tid == 0) a.tile_cnt[t] = tot;
+        }
+        grid_sync(a.bar);
+        for (uint32_t x = gtid; x < a.A; x += G) a.last[a.trace[x]] = kNever;  // leave clean
+    }
+
+    return true;
+}
+
+__global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
+    extern __shared__ unsigned char smem_raw[];
+    ISmem& sm = *reinterpret_cast<ISmem*>(smem_raw);
+    const uint32_t S = a.S, K = a.K;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t G = gridDim.x * blockDim.x;
+    const uint32_t gtid = blockIdx.x * blockDim.x + tid;
+    for (uint32_t i = tid; i <= S; i += blockDim.x) {
+        sm.toff[i] = a.toff[i];
+        sm.hinc[i] = 0;
+        sm.hnew[i] = 0;
+    }
+    for (uint32_t i = tid; i < 2048; i += blockDim.x) sm.rh[i] = 0;
+    __syncthreads();
+    const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
+
+    // ---- first occurrences, next use ---------------------------------------
+    bool have_next = false;
+    if (a.trusted) {
+        // sampler-produced trace: ids < N and distinct per iteration by
+        // construction; first occurrences by one atomicMin pass
+        for (uint32_t x = gtid; x < a.A; x += G) atomicMin(&a.last[a.trace[x]], iter_of(sm, S, x));
+        grid_sync(a.bar);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
@@ -285,6 +364,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
         for (uint32_t x = gtid; x < a.A; x += G) a.last[a.trace[x]] = kNever;  // leave clean
+    } else {
+        if (!next_use_pass(a, sm, true)) return;
+        have_next = true;
     }
 
     // ---- init set: first K first-occurrences in trace order (changeset.hpp:137-153)
@@ -363,6 +445,25 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     }
     grid_sync(a.bar);
 
+    // Every distinct node fits (init = all of them): the recurrence keeps them
+    // all and never misses or evicts (keep = |cand| <= K at every iteration,
+    // changeset.hpp:284), so the changesets are empty and each access is
+    // served by its init slot.
+    const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
+    if (allfit) {
+        for (uint32_t x = gtid; x < a.A; x += G) a.acc_slot[x] = (uint32_t)a.node_slot[a.trace[x]];
+        for (uint32_t i = gtid; i < S; i += G) {
+            a.o_misses[i] = 0;
+            a.o_in_off[i + 1] = 0;
+            a.o_out_off[i + 1] = 0;
+        }
+        grid_sync(a.bar);
+        const uint32_t n0 = a.st->n_res;
+        for (uint32_t s = gtid; s < n0; s += G) a.node_slot[a.slot_node[s]] = -1;
+        return;
+    }
+    if (!have_next) next_use_pass(a, sm, false);
+
     // ---- the recurrence -------------------------------------------------------
     // State counters are double-buffered by iteration parity: iteration i reads
     // st[i&1] and CTA 0 writes st[(i+1)&1] in the iteration's last grid step.
@@ -380,7 +481,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         // P1 (this CTA's contiguous chunk of positions): hits refresh their
         // key, misses become candidates; per-chunk miss counts
         {
-            uint32_t miss = 0;
+            uint32_t miss = 0, hits = 0;
             for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) {
                 const uint32_t v = a.trace[base + pos];
                 const uint32_t nu = a.next_use[base + pos];
@@ -388,7 +489,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                 if (s >= 0) {
                     a.slot_key[s] = nu;
                     atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
-                    atomicSub(&sm.hinc[i], 1);
+                    ++hits;
                     a.pmiss[pos] = 0;
                     a.acc_slot[base + pos] = (uint32_t)s;
                 } else {
@@ -400,7 +501,11 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                 }
             }
             miss = block_sum(miss, sm.scan);
-            if (tid == 0) a.chunk_miss[blockIdx.x] = miss;
+            hits = block_sum(hits, sm.scan);
+            if (tid == 0) {
+                a.chunk_miss[blockIdx.x] = miss;
+                sm.hinc[i] -= (int32_t)hits;  // all incumbents keyed i are exactly the hits
+            }
             hist_flush(sm.hinc, a.hist_inc, S + 1);
             hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
         }
@@ -501,60 +606,92 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         const uint32_t admit_new = r > inc_b ? r - inc_b : 0;
         uint32_t thr = 0xFFFFFFFFu;
 
-        // P3: evict buckets > b*; collect the selection candidates of b*
-        for (uint32_t s = gtid; s < nres; s += G) {
-            const uint32_t bk = bucket_of(a.slot_key[s], S);
-            const uint32_t v = a.slot_node[s];
-            const bool ev = bk > bstar || (bk == bstar && keep_inc == 0);
-            if (__any_sync(__activemask(), ev)) {
-                const uint32_t o = agg_append(&cs->n_out, ev);
-                if (ev) {
-                    a.out_node[o] = v;
-                    a.out_slot[o] = s;
-                }
+        // P3: evict buckets > b*. Selection inside b* is an exact radix select
+        // on node ids (11/11/10-bit digits). For incumbents (sel 1) the first
+        // digit histogram is taken straight from the slot scan; only members
+        // whose first digit equals the cut digit are materialised (P3b), the
+        // ones above it are evicted there and then.
+        const Stage st_ev{sm.sortbuf, &sm.bc[8]}, st_c{sm.sortbuf + 2048, &sm.bc[9]};
+        if (tid == 0) {
+            sm.bc[8] = 0;
+            sm.bc[9] = 0;
+        }
+        __syncthreads();
+        for (uint32_t s0 = blockIdx.x * blockDim.x; s0 < nres; s0 += G) {  // CTA-uniform trip count
+            const uint32_t s = s0 + tid;
+            bool ev = false;
+            uint32_t v = 0;
+            if (s < nres) {
+                const uint32_t bk = bucket_of(a.slot_key[s], S);
+                ev = bk > bstar || (bk == bstar && keep_inc == 0);
+                if (ev || (sel == 1 && bk == bstar)) v = a.slot_node[s];
+                if (sel == 1 && bk == bstar) atomicAdd(&sm.rh[v >> 21], 1);
             }
-            if (sel == 1) {
-                const bool c = bk == bstar;
-                if (__any_sync(__activemask(), c)) {
-                    const uint32_t o = agg_append(&cs->n_c, c);
-                    if (c) {
-                        a.c_id[o] = v;
-                        a.c_ref[o] = s;
-                        atomicAdd(&a.rh[v >> 21], 1u);
-                    }
+            stage_put(st_ev, ev, v, s);
+            __syncthreads();
+            stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+        }
+        if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
+            for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < ni; p0 += G) {
+                const uint32_t pos = p0 + tid;
+                bool c = false;
+                uint32_t v = 0;
+                if (pos < ni && a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar) {
+                    c = true;
+                    v = a.trace[base + pos];
+                    atomicAdd(&sm.rh[v >> 21], 1);
                 }
+                stage_put(st_c, c, v, pos);
+                __syncthreads();
+                stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
             }
         }
-        if (sel == 2) {
-            for (uint32_t pos = gtid; pos < ni; pos += G) {
-                const bool c = a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar;
-                if (__any_sync(__activemask(), c)) {
-                    const uint32_t o = agg_append(&cs->n_c, c);
-                    if (c) {
-                        const uint32_t v = a.trace[base + pos];
-                        a.c_id[o] = v;
-                        a.c_ref[o] = pos;
-                        atomicAdd(&a.rh[v >> 21], 1u);
-                    }
-                }
-            }
-        }
+        __syncthreads();
+        stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
+        stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
+        if (sel) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
         grid_sync(a.bar);
-        if (sel) {  // exact radix select of the cut id (11/11/10-bit digits)
-            const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+        if (sel) {
             uint32_t want = sel == 1 ? keep_inc : admit_new, left;
             const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
-            for (uint32_t k = gtid; k < nc; k += G) {
-                const uint32_t v = a.c_id[k];
-                if ((v >> 21) == d1) atomicAdd(&a.rh[2048 + ((v >> 10) & 2047)], 1u);
+            if (sel == 1) {
+                // P3b: first digit above the cut -> evicted; equal -> candidates
+                for (uint32_t s0 = blockIdx.x * blockDim.x; s0 < nres; s0 += G) {
+                    const uint32_t s = s0 + tid;
+                    bool ev = false, c = false;
+                    uint32_t v = 0;
+                    if (s < nres && bucket_of(a.slot_key[s], S) == bstar) {
+                        v = a.slot_node[s];
+                        ev = (v >> 21) > d1;
+                        c = (v >> 21) == d1;
+                        if (c) atomicAdd(&sm.rh[(v >> 10) & 2047], 1);
+                    }
+                    stage_put(st_ev, ev, v, s);
+                    stage_put(st_c, c, v, s);
+                    __syncthreads();
+                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                    stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
+                }
+                __syncthreads();
+                stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
+                stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
+            } else {
+                const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const uint32_t v = a.c_id[k];
+                    if ((v >> 21) == d1) atomicAdd(&sm.rh[(v >> 10) & 2047], 1);
+                }
             }
+            hist_flush(sm.rh, (int32_t*)a.rh + 2048, 2048);
             grid_sync(a.bar);
+            const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
             const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
             const uint32_t pre = (d1 << 11) | d2;
             for (uint32_t k = gtid; k < nc; k += G) {
                 const uint32_t v = a.c_id[k];
-                if ((v >> 10) == pre) atomicAdd(&a.rh[4096 + (v & 1023)], 1u);
+                if ((v >> 10) == pre) atomicAdd(&sm.rh[v & 1023], 1);
             }
+            hist_flush(sm.rh, (int32_t*)a.rh + 4096, 1024);
             grid_sync(a.bar);
             const uint32_t d3 = hist_select(a.rh + 4096, 1024, left, &left, sm);
             thr = (pre << 10) | d3;
@@ -576,16 +713,16 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             if (tid == 0) a.chunk_in[blockIdx.x] = c;
             if (sel == 1) {
                 const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
-                for (uint32_t k = gtid; k < nc; k += G) {
-                    const bool ev = a.c_id[k] > thr;
-                    if (__any_sync(__activemask(), ev)) {
-                        const uint32_t o = agg_append(&cs->n_out, ev);
-                        if (ev) {
-                            a.out_node[o] = a.c_id[k];
-                            a.out_slot[o] = a.c_ref[k];
-                        }
-                    }
+                const Stage st_ev{sm.sortbuf, &sm.bc[8]};
+                for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < nc; k0 += G) {
+                    const uint32_t k = k0 + tid;
+                    const bool ev = k < nc && a.c_id[k] > thr;
+                    stage_put(st_ev, ev, ev ? a.c_id[k] : 0, ev ? a.c_ref[k] : 0);
+                    __syncthreads();
+                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
                 }
+                __syncthreads();
+                stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
             }
         }
         grid_sync(a.bar);
@@ -747,7 +884,7 @@ static void host_trace_error(const std::vector<uint32_t>& flat, const std::vecto
 }
 
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
-                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out) {
+                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted) {
     const uint64_t S = off.size() - 1;
     if (S > kMaxIters) fail(GX_INVALID_ARGUMENT, "at most 4096 iterations per superbatch");
     if (N >= 0xFFFFFFFFull) fail(GX_OVERFLOW, "num_nodes exceeds the u32 device id range");
@@ -802,7 +939,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.isfirst.reserve(std::max<uint64_t>(A, 1));
     // per-node iteration bitmask (next use in 3 grid steps) when it fits the budget
     const uint64_t W = (S + 63) / 64;
-    const bool use_bits = S > 0 && N * W * 8 <= (8ull << 30);
+    const bool use_bits = S > 0 && W <= 2 && N * W * 8 <= (8ull << 30);
     if (use_bits && is.bits_words < N * W) {
         is.bits.alloc(N * W);
         GX_CUDA(cudaMemsetAsync(is.bits.p, 0, N * W * 8, st));
@@ -871,6 +1008,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.bits = use_bits ? is.bits.p : nullptr;
     a.W = (uint32_t)W;
     a.use_bits = use_bits;
+    a.trusted = trusted && n_init_explicit < 0;
     a.init_pos = n_init_explicit >= 0 ? is.init_pos.p : nullptr;
     a.bm_words = B.bm_words.p;
     a.nwords = (uint32_t)((N + 31) / 32);

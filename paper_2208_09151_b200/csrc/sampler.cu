@@ -36,6 +36,7 @@ constexpr uint32_t SB_TILE = SB_THREADS * SB_IPT;
 constexpr uint32_t kNewBit = 0x80000000u;
 constexpr unsigned long long kEmptySlot = ~0ull;
 constexpr uint32_t kMaxBatchesPerLaunch = 4096;
+constexpr uint64_t kChunk = 128;  // batches per sampler launch
 constexpr int kPickCache = 32;
 
 struct SampArgs {
@@ -500,8 +501,6 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
                 const uint32_t* fanouts, uint32_t L, const uint64_t* batch_seeds, gx_samples* out) {
     gx_ctx* ctx = g->ctx;
     if (L > (uint32_t)kMaxLayers) fail(GX_INVALID_ARGUMENT, "at most 16 layers are supported");
-    if (S > kMaxBatchesPerLaunch)
-        fail(GX_INVALID_ARGUMENT, "at most 4096 batches per sampler launch");
     uint64_t ns_max = 0, ns_total = batch_off[S];
     for (uint64_t b = 0; b < S; ++b) ns_max = std::max(ns_max, batch_off[b + 1] - batch_off[b]);
     const uint64_t N = g->n;
@@ -536,32 +535,36 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     out->edges.reserve(S * out->cap_e_batch);
     out->layer_count.reserve(std::max<uint64_t>(S * L, 1));
 
+    // Scratch is sized for one launch of at most kChunk batches; larger
+    // superbatches run as consecutive launches into the same output (batches
+    // are independent, sampler.hpp:216).
+    const uint64_t CH = std::min<uint64_t>(S, kChunk);
     SampleScratch& ss = ctx->ss;
     cudaStream_t st = ctx->stream;
-    ss.F.reserve(S);
-    ss.T.reserve(S);
-    ss.dbase.reserve(S);
+    ss.F.reserve(CH);
+    ss.T.reserve(CH);
+    ss.dbase.reserve(CH);
     ss.bseed.reserve(S);
     ss.seed_off.reserve(S + 1);
     ss.seeds32.reserve(std::max<uint64_t>(ns_total, 1));
-    ss.pscan.reserve(S * cap_ids);
-    ss.pdeg.reserve(S * cap_ids);
-    ss.plo.reserve(S * cap_ids);
-    ss.idslot.reserve(S * cap_ids);
-    const uint64_t max_tiles = S * ((std::max(cap_ids, cap_draw) + SB_TILE - 1) / SB_TILE) + 1;
+    ss.pscan.reserve(CH * cap_ids);
+    ss.pdeg.reserve(CH * cap_ids);
+    ss.plo.reserve(CH * cap_ids);
+    ss.idslot.reserve(CH * cap_ids);
+    const uint64_t max_tiles = CH * ((std::max(cap_ids, cap_draw) + SB_TILE - 1) / SB_TILE) + 1;
     ss.tsum.reserve(max_tiles);
     ss.tsum2.reserve(max_tiles);
-    ss.dslot.reserve(S * cap_draw);
-    ss.drank.reserve(S * cap_draw);
+    ss.dslot.reserve(CH * cap_draw);
+    ss.drank.reserve(CH * cap_draw);
     uint64_t tab_cap = 1024;
     while (tab_cap < 2 * cap_ids) tab_cap <<= 1;
     if (tab_cap > (1ull << 31)) fail(GX_INVALID_ARGUMENT, "batch too large for the dedup table");
-    if (S * tab_cap > ss.tab_slots) {
+    if (CH * tab_cap > ss.tab_slots) {
         for (int i = 0; i < 2; ++i) {
-            ss.tab[i].alloc(S * tab_cap);
+            ss.tab[i].alloc(CH * tab_cap);
             GX_CUDA(cudaMemsetAsync(ss.tab[i].p, 0xff, ss.tab[i].bytes(), st));
         }
-        ss.tab_slots = S * tab_cap;
+        ss.tab_slots = CH * tab_cap;
     }
     ss.io.reserve(4);
     GX_CUDA(cudaMemsetAsync(ss.io.p, 0, 4 * sizeof(unsigned long long), st));
@@ -577,21 +580,14 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     a.indptr = g->indptr.p;
     a.indices = g->indices.p;
     a.N = N;
-    a.S = (uint32_t)S;
     a.L = L;
     for (uint32_t l = 0; l < L; ++l) {
         a.fan[l] = fanouts[l];
         a.e_off[l] = out->e_off[l];
     }
-    a.bseed = ss.bseed.p;
     a.seeds = ss.seeds32.p;
-    a.seed_off = ss.seed_off.p;
-    a.ids = out->ids.p;
     a.cap_ids = cap_ids;
-    a.n_ids = out->n_ids.p;
-    a.edges = out->edges.p;
     a.cap_e_batch = out->cap_e_batch;
-    a.layer_count = out->layer_count.p;
     a.F = ss.F.p;
     a.T = ss.T.p;
     a.dbase = ss.dbase.p;
@@ -618,9 +614,19 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         if (blocks_per_sm < 1) fail(GX_CUDA_ERROR, "sampler kernel cannot be resident");
     }
     dim3 grid(ctx->num_sms * blocks_per_sm), block(SB_THREADS);
-    void* args[] = {&a};
-    GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
-    GX_CHECK_LAUNCH();
+    for (uint64_t c0 = 0; c0 < S; c0 += CH) {
+        const uint64_t nb = std::min(CH, S - c0);
+        a.S = (uint32_t)nb;
+        a.bseed = ss.bseed.p + c0;
+        a.seed_off = ss.seed_off.p + c0;  // global offsets into the flat seed array
+        a.ids = out->ids.p + c0 * cap_ids;
+        a.n_ids = out->n_ids.p + c0;
+        a.edges = out->edges.p + c0 * out->cap_e_batch;
+        a.layer_count = out->layer_count.p + c0 * L;
+        void* args[] = {&a};
+        GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
+        GX_CHECK_LAUNCH();
+    }
 }
 
 void samples_sync_host(gx_samples* s) {

@@ -140,3 +140,29 @@ def test_pipeline_end_to_end(gx, oracle):
               for i, b in enumerate(plan2)]
     init2 = oracle.compute_init_set(trace2, K, n)
     assert np.array_equal(st2.misses, oracle.simulate(trace2, n, K, init2)["misses"])
+
+
+def test_pipeline_all_distinct_nodes_fit(gx, oracle):
+    """K >= distinct nodes of the superbatch: init = every node, no misses, empty
+    changesets (the inspector's all-fit shortcut) -- bytes still exact."""
+    n, dim = 8000, 16
+    ip, ind = oracle.rmat_graph(n, 6.0, 5)
+    g = gx.GraphFile.from_csc(ip, ind)
+    rows = oracle.features(n, dim, 4)
+    f = gx.FeatureFile.from_array(rows)
+    plan = oracle.plan_seed_batches(oracle.train_ids(n, 3, 0.2), 50, oracle.epoch_seed(3, 0))[:10]
+    trace = [oracle.sample_batch(ip, ind, b, [4, 4], oracle.derive_seed(3, i))[0] for i, b in enumerate(plan)]
+    for K in (n, len(np.unique(np.concatenate(trace)))):
+        p = gx.Pipeline(g, f, [4, 4], K, digest=True)
+        st = p.run_superbatch(plan, 3, 0)
+        sim = oracle.simulate(trace, n, K, oracle.compute_init_set(trace, K, n))
+        assert np.array_equal(st.misses, sim["misses"]) and st.total_misses == 0
+        assert st.total_in == 0 and st.total_out == 0
+        dig = p.digests()
+        for i, ids in enumerate(trace):
+            assert int(dig[i]) == gx.batch_digest(rows[ids.astype(np.int64)])
+    # one node short of all-fit: the general path, still exact
+    K = len(np.unique(np.concatenate(trace))) - 1
+    st = gx.Pipeline(g, f, [4, 4], K).run_superbatch(plan, 3, 0)
+    sim = oracle.simulate(trace, n, K, oracle.compute_init_set(trace, K, n))
+    assert np.array_equal(st.misses, sim["misses"])

@@ -128,3 +128,21 @@ def test_device_generator_matches_reference_generator(oracle, gx):
         g = gx.GraphFile.generate_rmat(n, deg, seed)
         gip, gind = g.to_csc()
         assert np.array_equal(ip, gip) and np.array_equal(ind, gind)
+
+
+def test_superbatch_spanning_several_launches(oracle, gx):
+    """> 128 batches run as consecutive sampler launches into one output."""
+    ip, ind = oracle.rmat_graph(5000, 6.0, 21)
+    g = gx.GraphFile.from_csc(ip, ind)
+    rng = np.random.default_rng(9)
+    batches = [rng.choice(5000, size=int(rng.integers(1, 12)), replace=False).astype(np.uint64)
+               for _ in range(300)]
+    io = gx.IoStats()
+    s = gx.sample_superbatch(g, None, batches, [3, 3], 17, 1000, io)
+    tot = np.zeros(4, np.uint64)
+    for i in range(0, 300, 7):
+        want = oracle.sample_batch(ip, ind, batches[i], [3, 3], oracle.derive_seed(17, 1000 + i))
+        _same(want, s.batch(i))
+    for i in range(300):
+        tot += oracle.sample_batch(ip, ind, batches[i], [3, 3], oracle.derive_seed(17, 1000 + i))[2]
+    assert (io.pages_read, io.neighbor_lists_read) == (int(tot[0]), int(tot[2]))
