@@ -276,6 +276,8 @@ def main():
     ap.add_argument("--ref-batches", type=int, default=16,
                     help="batches per step for the reference / cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sync", action="store_true",
+                    help="no overlap: each superbatch's executor finishes before the next sampler starts")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.avg_degree is not None:
@@ -313,10 +315,36 @@ def main():
         j = sb_index(k)
         return pipe.run_superbatch(sbs[j], SEED_RUN, j * cfg["S"])
 
-    for k in range(args.warmup):
-        st = step(k)
-        log(f"warmup {k}: {st.sampled_edges} edges, sample {st.ms_sample:.2f} ms inspect "
+    exec_stream = torch.cuda.ExternalStream(pipe.exec_stream, device=torch.device("cuda", local))
+
+    def submit(k):
+        j = sb_index(k)
+        return pipe.submit(sbs[j], SEED_RUN, j * cfg["S"])
+
+    def run_steps(k0, n, on_stats, ev_start=None, ev_end=None):
+        """Superbatch k's executor overlaps superbatch k+1's sampler/inspector
+        (two in flight); --sync runs them back to back."""
+        if ev_start is not None:
+            ev_start.record(stream)
+        prev = None
+        for k in range(k0, k0 + n):
+            t = submit(k)
+            if args.sync:
+                on_stats(pipe.wait(t))
+                continue
+            if prev is not None:
+                on_stats(pipe.wait(prev))
+            prev = t
+        if ev_end is not None:
+            ev_end.record(exec_stream)
+        if prev is not None:
+            on_stats(pipe.wait(prev))
+
+    def log_warm(st):
+        log(f"warmup: {st.sampled_edges} edges, sample {st.ms_sample:.2f} ms inspect "
             f"{st.ms_inspect:.2f} ms switch {st.ms_switch:.2f} ms gather {st.ms_gather:.2f} ms")
+
+    run_steps(0, args.warmup, log_warm)
 
     def barrier():
         if world > 1:
@@ -325,20 +353,15 @@ def main():
         torch.cuda.synchronize(local)
 
     stats = []
-    walls = []
     barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
-        ev0.record(stream)
-        for k in range(args.warmup, args.warmup + args.steps):
-            t = time.perf_counter()
-            stats.append(step(k))
-            walls.append(time.perf_counter() - t)
-        ev1.record(stream)
+        t_wall = time.perf_counter()
+        run_steps(args.warmup, args.steps, stats.append, ev0, ev1)
+        wall_s = time.perf_counter() - t_wall
         barrier()
     dev_s = ev0.elapsed_time(ev1) / 1e3
-    wall_s = sum(walls)
     edges = sum(s.sampled_edges for s in stats)
     if world > 1:
         t = torch.tensor([dev_s, wall_s], device=f"cuda:{local}", dtype=torch.float64)

@@ -238,6 +238,22 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat,
                                  const uint64_t* batch_offsets, uint64_t n_batches,
                                  uint64_t global_seed, uint64_t first_global_batch,
                                  uint64_t* misses_per_iter, gx_pipeline_stats* stats);
+/* Asynchronous, double-buffered form. submit() runs the sampler and the
+ * inspector of a superbatch on the context stream and queues its executor
+ * (cache init + S x gather/apply) on the pipeline's own stream, returning
+ * without waiting for it, so the executor of superbatch k overlaps the
+ * sampler/inspector of k+1 (the reference overlaps sample(k+1) with
+ * precompute(k), pipeline.hpp:299-315). At most two superbatches may be in
+ * flight; wait(ticket) returns that superbatch's results. gx_pipeline_superbatch
+ * is submit + wait. */
+gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat,
+                             const uint64_t* batch_offsets, uint64_t n_batches,
+                             uint64_t global_seed, uint64_t first_global_batch, uint64_t* ticket);
+gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per_iter,
+                           gx_pipeline_stats* stats);
+/* the cudaStream_t the executor of this pipeline runs on */
+void* gx_pipeline_exec_stream(gx_pipeline* p);
+
 /* Optional per-iteration digest of each gathered batch (for end-to-end parity
  * checks; off by default, costs one extra read of every batch):
  *   digest_i = sum_k sum_j (w_kj + 1) * mix64(k * W + j)  (mod 2^64)

@@ -116,6 +116,9 @@ SIGNATURES = {
     "gx_pipeline_create": (i32, [vp, vp, vp, u32, u64, PVP]),
     "gx_pipeline_destroy": (None, [vp]),
     "gx_pipeline_superbatch": (i32, [vp, vp, vp, u64, u64, u64, vp, C.POINTER(PipelineStatsC)]),
+    "gx_pipeline_submit": (i32, [vp, vp, vp, u64, u64, u64, P64]),
+    "gx_pipeline_wait": (i32, [vp, u64, vp, C.POINTER(PipelineStatsC)]),
+    "gx_pipeline_exec_stream": (vp, [vp]),
     "gx_pipeline_set_digest": (i32, [vp, i32]),
     "gx_pipeline_digests": (i32, [vp, vp]),
 }

@@ -844,6 +844,7 @@ class Pipeline:
         if digest:
             check(lib.gx_pipeline_set_digest(h, 1))
         self._S = 0
+        self._sizes = {}
 
     def __del__(self):
         if getattr(self, "h", None):
@@ -851,18 +852,33 @@ class Pipeline:
             self.h = None
 
     def run_superbatch(self, batches, global_seed: int, first_global_batch: int) -> PipelineStats:
+        """Synchronous: one superbatch end to end (gx_pipeline_superbatch)."""
+        return self.wait(self.submit(batches, global_seed, first_global_batch))
+
+    def submit(self, batches, global_seed: int, first_global_batch: int) -> int:
+        """Sampler + inspector now, executor queued on the pipeline stream;
+        returns a ticket. At most two superbatches may be in flight."""
         flat, off = _flatten(batches)
-        S = len(off) - 1
+        t = C.c_uint64()
+        check(lib.gx_pipeline_submit(self.h, flat.ctypes.data, off.ctypes.data, len(off) - 1,
+                                     global_seed & 0xFFFFFFFFFFFFFFFF, first_global_batch, C.byref(t)))
+        self._sizes[t.value] = len(off) - 1
+        return t.value
+
+    def wait(self, ticket: int) -> PipelineStats:
+        S = self._sizes.pop(ticket)
         misses = np.zeros(max(S, 1), np.uint64)
         st = PipelineStatsC()
-        check(lib.gx_pipeline_superbatch(self.h, flat.ctypes.data, off.ctypes.data, S,
-                                         global_seed & 0xFFFFFFFFFFFFFFFF, first_global_batch,
-                                         misses.ctypes.data, C.byref(st)))
+        check(lib.gx_pipeline_wait(self.h, ticket, misses.ctypes.data, C.byref(st)))
         self._S = S
         return PipelineStats(st.sampled_edges, st.gathered_rows, st.total_misses, st.predicted_misses,
                              st.init_size, st.total_in, st.total_out, _io(st.sample_io),
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
                              st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, misses[:S].copy())
+
+    @property
+    def exec_stream(self) -> int:
+        return lib.gx_pipeline_exec_stream(self.h)
 
     def digests(self) -> np.ndarray:
         out = np.zeros(max(self._S, 1), np.uint64)

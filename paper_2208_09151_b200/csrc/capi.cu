@@ -60,8 +60,24 @@ static void d2h_u32_as_u64(const uint32_t* d, uint64_t n, uint64_t* h) {
 }  // namespace gx
 
 // ---------------------------------------------------------------------------
-// fused pipeline handle
+// fused pipeline handle: two superbatch slots in flight. The sampler and the
+// inspector run on the context stream; the executor of a slot runs on the
+// pipeline's own stream, so executor(k) overlaps sampler/inspector(k+1).
 // ---------------------------------------------------------------------------
+struct PipeSlot {
+    bool pending = false;
+    uint64_t S = 0;
+    gx_changesets cs;
+    gx::DevBuf<uint32_t> trace, acc_slot;  // swapped with ctx->is while the inspector runs
+    gx::DevBuf<unsigned long long> counters, digests;
+    gx::PinBuf<unsigned long long> h_cnt, h_dig;
+    std::vector<uint64_t> o;  // trace offsets
+    uint64_t sampled_edges = 0;
+    gx_iostats sample_io{};
+    cudaEvent_t ev[6] = {};  // A: start, sampled, inspected; B: exec start, switched, done
+    std::vector<cudaEvent_t> kev;
+};
+
 struct gx_pipeline {
     gx_graph* g = nullptr;
     gx_features* f = nullptr;
@@ -69,15 +85,13 @@ struct gx_pipeline {
     std::vector<uint32_t> fanouts;
     uint64_t K = 0;
     gx_samples samples;
-    gx_changesets cs;
     gx::DevBuf<uint8_t> cache_rows;
     gx::DevBuf<uint8_t> batch;
-    gx::DevBuf<unsigned long long> counters;  // per iteration 8 words
-    gx::DevBuf<unsigned long long> digests;
+    cudaStream_t exec = nullptr;
+    PipeSlot slot[2];
+    uint64_t submitted = 0;
     bool digest = false;
     std::vector<uint64_t> h_digests;
-    cudaEvent_t ev[5] = {};
-    std::vector<cudaEvent_t> kev;  // 3 per iteration: gather start, gather end / apply start, apply end
 };
 
 using namespace gx;
@@ -381,9 +395,11 @@ gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanout
             p->fanouts.assign(fanouts, fanouts + L);
             p->K = K;
             p->cache_rows.alloc(std::max<uint64_t>(K * f->row_bytes, 16));
-            for (auto& e : p->ev) GX_CUDA(cudaEventCreate(&e));
+            GX_CUDA(cudaStreamCreateWithFlags(&p->exec, cudaStreamNonBlocking));
+            for (auto& sl : p->slot)
+                for (auto& e : sl.ev) GX_CUDA(cudaEventCreate(&e));
         } catch (...) {
-            delete p;
+            gx_pipeline_destroy(p);
             throw;
         }
         *out = p;
@@ -392,9 +408,14 @@ gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanout
 
 void gx_pipeline_destroy(gx_pipeline* p) {
     if (!p) return;
-    for (auto& e : p->ev)
-        if (e) cudaEventDestroy(e);
-    for (auto& e : p->kev) cudaEventDestroy(e);
+    if (p->exec) cudaStreamSynchronize(p->exec);
+    if (p->ctx) cudaStreamSynchronize(p->ctx->stream);
+    for (auto& sl : p->slot) {
+        for (auto& e : sl.ev)
+            if (e) cudaEventDestroy(e);
+        for (auto& e : sl.kev) cudaEventDestroy(e);
+    }
+    if (p->exec) cudaStreamDestroy(p->exec);
     delete p;
 }
 
@@ -408,12 +429,13 @@ gx_status gx_pipeline_digests(const gx_pipeline* p, uint64_t* d) {
     });
 }
 
-gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, const uint64_t* batch_off,
-                                 uint64_t S, uint64_t global_seed, uint64_t first_global_batch,
-                                 uint64_t* misses_per_iter, gx_pipeline_stats* stats) {
+void* gx_pipeline_exec_stream(gx_pipeline* p) { return p ? (void*)p->exec : nullptr; }
+
+gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
+                             uint64_t global_seed, uint64_t first_global_batch, uint64_t* ticket) {
     return guard([&] {
         gx_ctx* ctx = p->ctx;
-        cudaStream_t st = ctx->stream;
+        cudaStream_t A = ctx->stream, B = p->exec;
         const uint64_t N = p->g->n;
         if (S == 0) fail(GX_INVALID_ARGUMENT, "empty superbatch");
         for (uint64_t b = 0; b < S; ++b) {
@@ -422,84 +444,128 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
             for (uint64_t k = batch_off[b]; k < batch_off[b + 1]; ++k)
                 if (seeds_flat[k] >= N) fail(GX_RUNTIME_ERROR, "superbatch sample failed: seed node out of range");
         }
+        const uint64_t t = p->submitted;
+        PipeSlot& sl = p->slot[t & 1];
+        if (sl.pending) fail(GX_LOGIC_ERROR, "two superbatches already in flight: wait for the older one first");
         std::vector<uint64_t> bs(S);
         for (uint64_t i = 0; i < S; ++i) bs[i] = derive_seed(global_seed, first_global_batch + i);
         const uint32_t L = (uint32_t)p->fanouts.size();
-        GX_CUDA(cudaEventRecord(p->ev[0], st));
+        // this slot's buffers were last read by its previous executor (already waited)
+        GX_CUDA(cudaEventRecord(sl.ev[0], A));
         // (1) sample
         sample_run(p->g, seeds_flat, batch_off, S, p->fanouts.data(), L, bs.data(), &p->samples);
-        GX_CUDA(cudaEventRecord(p->ev[1], st));
-        samples_sync_host(&p->samples);
-        // (2) inspect
-        std::vector<uint64_t> o(S + 1, 0);
-        for (uint64_t i = 0; i < S; ++i) o[i + 1] = o[i] + p->samples.h_n_ids[i];
-        inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, o);
-        inspect_run(ctx, o, N, p->K, nullptr, -1, &p->cs, true);
-        GX_CUDA(cudaEventRecord(p->ev[2], st));
-        // (3) switch: cache init
-        uint64_t maxw = 0;
-        for (uint64_t i = 0; i < S; ++i) maxw = std::max(maxw, o[i + 1] - o[i]);
-        p->batch.reserve(std::max<uint64_t>(maxw * p->f->row_bytes, 16));
-        p->counters.reserve(8 * (S + 1));
-        GX_CUDA(cudaMemsetAsync(p->counters.p, 0, 8 * (S + 1) * 8, st));
-        if (p->digest) {
-            p->digests.reserve(S);
-            GX_CUDA(cudaMemsetAsync(p->digests.p, 0, S * 8, st));
+        GX_CUDA(cudaEventRecord(sl.ev[1], A));
+        samples_sync_host(&p->samples);  // host needs |ids_i| (stream A only)
+        sl.sampled_edges = gx_samples_total_edges(&p->samples);
+        sl.sample_io = p->samples.io;
+        sl.S = S;
+        // (2) inspect into this slot's trace / acc_slot / changesets
+        sl.o.assign(S + 1, 0);
+        for (uint64_t i = 0; i < S; ++i) sl.o[i + 1] = sl.o[i] + p->samples.h_n_ids[i];
+        std::swap(ctx->is.trace, sl.trace);
+        std::swap(ctx->is.acc_slot, sl.acc_slot);
+        try {
+            inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, sl.o);
+            inspect_run(ctx, sl.o, N, p->K, nullptr, -1, &sl.cs, true);
+        } catch (...) {
+            std::swap(ctx->is.trace, sl.trace);
+            std::swap(ctx->is.acc_slot, sl.acc_slot);
+            throw;
         }
-        // the inspector resolved every access's serving slot (is.acc_slot), so
-        // the executor needs no address table on this path
-        launch_cache_init(ctx, p->cs.init.p, (uint32_t)p->cs.n_init, nullptr, p->f, p->cache_rows.p,
-                          p->counters.p + 8 * S);
-        GX_CUDA(cudaEventRecord(p->ev[3], st));
-        // (4) main loop: gather + apply (the ids of iteration i are batch i's ids)
-        while (p->kev.size() < 3 * S) {
+        std::swap(ctx->is.trace, sl.trace);
+        std::swap(ctx->is.acc_slot, sl.acc_slot);
+        GX_CUDA(cudaEventRecord(sl.ev[2], A));
+        // (3)+(4) executor on stream B, after the inspector and the previous executor
+        GX_CUDA(cudaStreamWaitEvent(B, sl.ev[2], 0));
+        GX_CUDA(cudaEventRecord(sl.ev[3], B));
+        uint64_t maxw = 0;
+        for (uint64_t i = 0; i < S; ++i) maxw = std::max(maxw, sl.o[i + 1] - sl.o[i]);
+        p->batch.reserve(std::max<uint64_t>(maxw * p->f->row_bytes, 16));
+        sl.counters.reserve(8 * (S + 1));
+        sl.h_cnt.reserve(8 * (S + 1));
+        GX_CUDA(cudaMemsetAsync(sl.counters.p, 0, 8 * (S + 1) * 8, B));
+        if (p->digest) {
+            sl.digests.reserve(S);
+            sl.h_dig.reserve(S);
+            GX_CUDA(cudaMemsetAsync(sl.digests.p, 0, S * 8, B));
+        }
+        while (sl.kev.size() < 3 * S) {
             cudaEvent_t e;
             GX_CUDA(cudaEventCreate(&e));
-            p->kev.push_back(e);
+            sl.kev.push_back(e);
         }
-        for (uint64_t i = 0; i < S; ++i) {
-            const uint64_t ni = o[i + 1] - o[i];
-            GX_CUDA(cudaEventRecord(p->kev[3 * i], st));
-            launch_gather_resolved(ctx, ctx->is.trace.p + o[i], ctx->is.acc_slot.p + o[i], ni,
-                                   p->cache_rows.p, p->f, p->batch.p, p->counters.p + 8 * i);
-            GX_CUDA(cudaEventRecord(p->kev[3 * i + 1], st));
-            if (p->digest) launch_digest(ctx, p->batch.p, ni, p->f->row_bytes, p->digests.p + i);
-            const uint64_t a = p->cs.h_in_off[i], b = p->cs.h_out_off[i];
-            launch_apply_slots(ctx, p->cs.in_ids.p + a, p->cs.in_pos.p + a, p->cs.in_slot.p + a,
-                               (uint32_t)(p->cs.h_in_off[i + 1] - a), p->cs.out_ids.p + b,
-                               (uint32_t)(p->cs.h_out_off[i + 1] - b), nullptr, p->batch.p, p->cache_rows.p,
-                               p->f->row_bytes);
-            GX_CUDA(cudaEventRecord(p->kev[3 * i + 2], st));
+        ctx->launch_stream = B;
+        try {
+            // (3) switch: the init rows into slots 0..n_init-1 (the inspector
+            // resolved every access's serving slot, so no address table here)
+            launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
+                              sl.counters.p + 8 * S);
+            GX_CUDA(cudaEventRecord(sl.ev[4], B));
+            // (4) main loop: gather + apply
+            for (uint64_t i = 0; i < S; ++i) {
+                const uint64_t ni = sl.o[i + 1] - sl.o[i];
+                GX_CUDA(cudaEventRecord(sl.kev[3 * i], B));
+                launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], ni, p->cache_rows.p, p->f,
+                                       p->batch.p, sl.counters.p + 8 * i);
+                GX_CUDA(cudaEventRecord(sl.kev[3 * i + 1], B));
+                if (p->digest) launch_digest(ctx, p->batch.p, ni, p->f->row_bytes, sl.digests.p + i);
+                const uint64_t a = sl.cs.h_in_off[i], b = sl.cs.h_out_off[i];
+                launch_apply_slots(ctx, sl.cs.in_ids.p + a, sl.cs.in_pos.p + a, sl.cs.in_slot.p + a,
+                                   (uint32_t)(sl.cs.h_in_off[i + 1] - a), sl.cs.out_ids.p + b,
+                                   (uint32_t)(sl.cs.h_out_off[i + 1] - b), nullptr, p->batch.p, p->cache_rows.p,
+                                   p->f->row_bytes);
+                GX_CUDA(cudaEventRecord(sl.kev[3 * i + 2], B));
+            }
+        } catch (...) {
+            ctx->launch_stream = nullptr;
+            throw;
         }
-        GX_CUDA(cudaEventRecord(p->ev[4], st));
-        std::vector<unsigned long long> cnt(8 * (S + 1));
-        GX_CUDA(cudaMemcpyAsync(cnt.data(), p->counters.p, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
-        if (p->digest) {
-            p->h_digests.resize(S);
-            GX_CUDA(cudaMemcpyAsync(p->h_digests.data(), p->digests.p, S * 8, cudaMemcpyDeviceToHost, st));
-        }
-        GX_CUDA(cudaStreamSynchronize(st));
+        ctx->launch_stream = nullptr;
+        GX_CUDA(cudaMemcpyAsync(sl.h_cnt.p, sl.counters.p, 8 * (S + 1) * 8, cudaMemcpyDeviceToHost, B));
+        if (p->digest) GX_CUDA(cudaMemcpyAsync(sl.h_dig.p, sl.digests.p, S * 8, cudaMemcpyDeviceToHost, B));
+        GX_CUDA(cudaEventRecord(sl.ev[5], B));
+        // the next submit reuses the context stream's scratch: it may start as
+        // soon as the inspector is done; slot reuse is guarded by `pending`
+        sl.pending = true;
+        *ticket = t;
+        p->submitted = t + 1;
+    });
+}
+
+gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per_iter, gx_pipeline_stats* stats) {
+    return guard([&] {
+        PipeSlot& sl = p->slot[ticket & 1];
+        if (!sl.pending || ticket + 2 < p->submitted || ticket >= p->submitted)
+            fail(GX_INVALID_ARGUMENT, "unknown or already completed pipeline ticket");
+        GX_CUDA(cudaEventSynchronize(sl.ev[5]));
+        sl.pending = false;
+        const uint64_t S = sl.S;
+        const unsigned long long* cnt = sl.h_cnt.p;
         uint64_t tm = 0, pm = 0;
         gx_iostats gio{};
         for (uint64_t i = 0; i < S; ++i) {
             if (misses_per_iter) misses_per_iter[i] = cnt[8 * i + 1];
             tm += cnt[8 * i + 1];
-            pm += p->cs.h_misses[i];
+            pm += sl.cs.h_misses[i];
             gio.pages_read += cnt[8 * i + 2];
             gio.rows_read += cnt[8 * i + 3];
             gio.bytes_read += cnt[8 * i + 4];
         }
+        if (p->digest) p->h_digests.assign(sl.h_dig.p, sl.h_dig.p + S);
         if (stats) {
-            float ms[4];
-            for (int k = 0; k < 4; ++k) GX_CUDA(cudaEventElapsedTime(&ms[k], p->ev[k], p->ev[k + 1]));
-            stats->sampled_edges = gx_samples_total_edges(&p->samples);
-            stats->gathered_rows = o[S];
+            float ms[5];
+            GX_CUDA(cudaEventElapsedTime(&ms[0], sl.ev[0], sl.ev[1]));  // sample
+            GX_CUDA(cudaEventElapsedTime(&ms[1], sl.ev[1], sl.ev[2]));  // inspect
+            GX_CUDA(cudaEventElapsedTime(&ms[2], sl.ev[3], sl.ev[4]));  // switch (executor stream)
+            GX_CUDA(cudaEventElapsedTime(&ms[3], sl.ev[4], sl.ev[5]));  // gather + apply
+            stats->sampled_edges = sl.sampled_edges;
+            stats->gathered_rows = sl.o[S];
             stats->total_misses = tm;
             stats->predicted_misses = pm;
-            stats->init_size = p->cs.n_init;
-            stats->total_in = p->cs.h_in_off[S];
-            stats->total_out = p->cs.h_out_off[S];
-            stats->sample_io = p->samples.io;
+            stats->init_size = sl.cs.n_init;
+            stats->total_in = sl.cs.h_in_off[S];
+            stats->total_out = sl.cs.h_out_off[S];
+            stats->sample_io = sl.sample_io;
             stats->gather_io = gio;
             stats->ms_sample = ms[0];
             stats->ms_inspect = ms[1];
@@ -508,8 +574,8 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
             double gk = 0, ak = 0;
             for (uint64_t i = 0; i < S; ++i) {
                 float a = 0, b = 0;
-                GX_CUDA(cudaEventElapsedTime(&a, p->kev[3 * i], p->kev[3 * i + 1]));
-                GX_CUDA(cudaEventElapsedTime(&b, p->kev[3 * i + 1], p->kev[3 * i + 2]));
+                GX_CUDA(cudaEventElapsedTime(&a, sl.kev[3 * i], sl.kev[3 * i + 1]));
+                GX_CUDA(cudaEventElapsedTime(&b, sl.kev[3 * i + 1], sl.kev[3 * i + 2]));
                 gk += a;
                 ak += b;
             }
@@ -517,6 +583,15 @@ gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, con
             stats->ms_apply_kernels = ak;
         }
     });
+}
+
+gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, const uint64_t* batch_off,
+                                 uint64_t S, uint64_t global_seed, uint64_t first_global_batch,
+                                 uint64_t* misses_per_iter, gx_pipeline_stats* stats) {
+    uint64_t t = 0;
+    gx_status st = gx_pipeline_submit(p, seeds_flat, batch_off, S, global_seed, first_global_batch, &t);
+    if (st != GX_OK) return st;
+    return gx_pipeline_wait(p, t, misses_per_iter, stats);
 }
 
 }  // extern "C"

@@ -399,7 +399,7 @@ void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t ro
                    unsigned long long* out) {
     const uint64_t nw = rows * row_bytes / 4;
     if (!nw) return;
-    k_digest<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(reinterpret_cast<const uint32_t*>(batch), nw, out);
+    k_digest<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(reinterpret_cast<const uint32_t*>(batch), nw, out);
     GX_CHECK_LAUNCH();
 }
 
@@ -416,7 +416,7 @@ static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t*
     const uint64_t warps_needed = (n + R - 1) / R;
     const uint64_t blocks_needed = (warps_needed * 32 + GA_THREADS - 1) / GA_THREADS;
     const uint64_t blocks = std::min<uint64_t>(blocks_needed, (uint64_t)ctx->num_sms * bps);
-    k_gather_rows<VEC, R><<<(unsigned)blocks, GA_THREADS, 0, ctx->stream>>>(
+    k_gather_rows<VEC, R><<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(
         ids, slots, (uint32_t)n, cache_rows, f->rows_dev_view, (uint32_t)f->row_bytes, out, counters);
     GX_CHECK_LAUNCH();
 }
@@ -455,7 +455,7 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         }
         const uint64_t blocks = std::min<uint64_t>((n + tpb[d] - 1) / tpb[d], (uint64_t)ctx->num_sms * bps[d]);
         auto kfn = depth == 2 ? k_gather_tma2 : k_gather_tma;
-        kfn<<<(unsigned)blocks, tpb[d], (size_t)tpb[d] * depth * rb, ctx->stream>>>(
+        kfn<<<(unsigned)blocks, tpb[d], (size_t)tpb[d] * depth * rb, lstream(ctx)>>>(
             ids, slots, (uint32_t)n, cache_rows, f->rows_dev_view, (uint32_t)rb, out, counters);
         GX_CHECK_LAUNCH();
     } else if (vec16(rb)) {
@@ -472,7 +472,7 @@ void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* 
     if (!n) return;
     DevBuf<uint32_t>& slots = ctx->resolve_slots;  // API path only
     slots.reserve(n);
-    k_resolve<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(ids, n, table, slots.p);
+    k_resolve<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(ids, n, table, slots.p);
     GX_CHECK_LAUNCH();
     launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, f, out, counters);
 }
@@ -484,10 +484,10 @@ void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_
     if (!m) return;
     const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)m * 32 + 255) / 256, ctx->num_sms * 8);
     if (vec16(row_bytes))
-        k_apply_slots<16><<<blocks, 256, 0, ctx->stream>>>(in_ids, in_pos, in_slot, n_in, out_ids, n_out, table,
+        k_apply_slots<16><<<blocks, 256, 0, lstream(ctx)>>>(in_ids, in_pos, in_slot, n_in, out_ids, n_out, table,
                                                            batch, cache_rows, row_bytes);
     else
-        k_apply_slots<4><<<blocks, 256, 0, ctx->stream>>>(in_ids, in_pos, in_slot, n_in, out_ids, n_out, table,
+        k_apply_slots<4><<<blocks, 256, 0, lstream(ctx)>>>(in_ids, in_pos, in_slot, n_in, out_ids, n_out, table,
                                                           batch, cache_rows, row_bytes);
     GX_CHECK_LAUNCH();
 }
@@ -505,14 +505,14 @@ void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* t
     if (!n) return;
     launch_gather_resolved(ctx, init, nullptr, n, nullptr, f, cache_rows, counters);
     if (table) {
-        k_set_table<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(init, n, table);
+        k_set_table<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(init, n, table);
         GX_CHECK_LAUNCH();
     }
 }
 
 void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table) {
     if (!n) return;
-    k_reset_table<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(nodes, n, table);
+    k_reset_table<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(nodes, n, table);
     GX_CHECK_LAUNCH();
 }
 

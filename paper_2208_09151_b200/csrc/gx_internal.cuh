@@ -45,7 +45,11 @@ struct gx_ctx {
     gx::SampleScratch ss;
     gx::InspectScratch is;
     gx::DevBuf<uint32_t> resolve_slots;  // executor API path scratch
+    cudaStream_t launch_stream = nullptr;  // executor launches go here when set (pipeline stream)
 };
+
+// stream the executor launchers use
+inline cudaStream_t lstream(const gx_ctx* c) { return c->launch_stream ? c->launch_stream : c->stream; }
 
 struct gx_graph {
     gx_ctx* ctx = nullptr;

@@ -32,7 +32,7 @@
 
 namespace gx {
 
-constexpr int IN_THREADS = 1024;
+constexpr int IN_THREADS = 512;  // half an SM: the executor shares the SMs
 constexpr uint32_t IN_TILE = IN_THREADS * 4;
 constexpr uint32_t SORT_SMALL = 4096;
 constexpr uint32_t kMaxIters = 4096;

@@ -23,6 +23,7 @@
 //    8 ip[v+1]) + 8 deg bytes per expanded parent (no neighbor cache).
 #include <algorithm>
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <unordered_set>
 
 #include "gx_internal.cuh"
@@ -538,7 +539,12 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     // Scratch is sized for one launch of at most kChunk batches; larger
     // superbatches run as consecutive launches into the same output (batches
     // are independent, sampler.hpp:216).
-    const uint64_t CH = std::min<uint64_t>(S, kChunk);
+    static const uint64_t chunk = [] {  // batches per launch (GX_SAMPLER_CHUNK)
+        const char* e = std::getenv("GX_SAMPLER_CHUNK");
+        const long v = e ? std::atol(e) : (long)kChunk;
+        return (uint64_t)std::min<long>(std::max<long>(v, 1), (long)kMaxBatchesPerLaunch);
+    }();
+    const uint64_t CH = std::min<uint64_t>(S, chunk);
     SampleScratch& ss = ctx->ss;
     cudaStream_t st = ctx->stream;
     ss.F.reserve(CH);
@@ -613,7 +619,13 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_sample, SB_THREADS, smem));
         if (blocks_per_sm < 1) fail(GX_CUDA_ERROR, "sampler kernel cannot be resident");
     }
-    dim3 grid(ctx->num_sms * blocks_per_sm), block(SB_THREADS);
+    // CTAs per SM (GX_SAMPLER_BPS, default 1): one leaves half of each SM's
+    // register file to the executor's gather CTAs running on the other stream
+    static const int bps_use = [] {
+        const char* e = std::getenv("GX_SAMPLER_BPS");
+        return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    dim3 grid(ctx->num_sms * std::min(bps_use, blocks_per_sm)), block(SB_THREADS);
     for (uint64_t c0 = 0; c0 < S; c0 += CH) {
         const uint64_t nb = std::min(CH, S - c0);
         a.S = (uint32_t)nb;

@@ -166,3 +166,39 @@ def test_pipeline_all_distinct_nodes_fit(gx, oracle):
     st = gx.Pipeline(g, f, [4, 4], K).run_superbatch(plan, 3, 0)
     sim = oracle.simulate(trace, n, K, oracle.compute_init_set(trace, K, n))
     assert np.array_equal(st.misses, sim["misses"])
+
+
+def test_pipeline_async_overlap_matches_sync(gx, oracle):
+    """submit/wait with two superbatches in flight gives the same per-superbatch
+    results (misses, digests) as running them one at a time."""
+    n, dim = 20000, 32
+    ip, ind = oracle.rmat_graph(n, 8.0, 23)
+    g = gx.GraphFile.from_csc(ip, ind)
+    rows = oracle.features(n, dim, 7)
+    f = gx.FeatureFile.from_array(rows)
+    plan = oracle.plan_seed_batches(oracle.train_ids(n, 4, 0.2), 64, oracle.epoch_seed(4, 0))
+    sbs = [plan[o:o + 6] for o in range(0, 36, 6)]
+    K = 2500
+    sync = gx.Pipeline(g, f, [5, 5], K, digest=True)
+    want = []
+    for j, sb in enumerate(sbs):
+        st = sync.run_superbatch(sb, 4, 6 * j)
+        want.append((st.misses.copy(), sync.digests().copy()))
+    asyn = gx.Pipeline(g, f, [5, 5], K, digest=True)
+    got, prev = [], None
+    for j, sb in enumerate(sbs):
+        t = asyn.submit(sb, 4, 6 * j)
+        if prev is not None:
+            st = asyn.wait(prev)
+            got.append((st.misses.copy(), asyn.digests().copy()))
+        prev = t
+    st = asyn.wait(prev)
+    got.append((st.misses.copy(), asyn.digests().copy()))
+    for (m1, d1), (m2, d2) in zip(want, got):
+        assert np.array_equal(m1, m2) and np.array_equal(d1, d2)
+    with pytest.raises(gx.LogicError):
+        t0 = asyn.submit(sbs[0], 4, 0)
+        t1 = asyn.submit(sbs[1], 4, 6)
+        asyn.submit(sbs[2], 4, 12)  # a third in flight is refused
+    asyn.wait(t0)
+    asyn.wait(t1)
