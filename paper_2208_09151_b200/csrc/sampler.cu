@@ -28,11 +28,24 @@
 
 #include "gx_internal.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace gx {
 
 constexpr int kMaxLayers = 16;
 constexpr int SB_THREADS = 512;
-constexpr int SB_IPT = 8;
+constexpr int SB_IPT = 2;
+#ifndef GX_E_UNROLL
+#define GX_E_UNROLL 4
+#endif
+#ifndef GX_E_LOADFIRST
+#define GX_E_LOADFIRST 1
+#endif
+#ifdef GX_SB_MINB
+#define GX_SB_BOUNDS __launch_bounds__(SB_THREADS, GX_SB_MINB)
+#else
+#define GX_SB_BOUNDS __launch_bounds__(SB_THREADS)
+#endif
 constexpr uint32_t SB_TILE = SB_THREADS * SB_IPT;
 constexpr uint32_t kNewBit = 0x80000000u;
 constexpr unsigned long long kEmptySlot = ~0ull;
@@ -73,13 +86,54 @@ struct SampArgs {
     uint64_t tab_cap;  // per batch max
     unsigned long long* io;
     GridBarrier* bar;
+    unsigned long long* trace;  // optional phase timestamps (GX_SAMPLER_TRACE)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE_STAMP(a, l, ph)                                                  \
+    do {                                                                       \
+        if ((a).trace && blockIdx.x == 0 && threadIdx.x == 0)                  \
+            (a).trace[1 + (l) * 8 + (ph)] = gtimer() - (a).trace[0];           \
+    } while (0)
 
 struct SampSmem {
     uint32_t scan[34];
     unsigned long long red[34];
     uint32_t tp[kMaxBatchesPerLaunch + 1];
+    uint32_t px[kMaxBatchesPerLaunch + 1];  // raw per-batch item prefix (flattened loops)
 };
+
+// px[0..S] = prefix of per-batch item counts (seeds of batch b when
+// seed_off != nullptr, else cnt[b]); returns the total. Lets a phase spread
+// (batch, item) pairs over the whole grid instead of looping batch by batch.
+__device__ uint32_t build_prefix(const uint32_t* cnt, const uint64_t* seed_off, uint32_t S, SampSmem& sm) {
+    uint32_t carry = 0;
+    for (uint32_t base = 0; base < S; base += blockDim.x) {
+        const uint32_t b = base + threadIdx.x;
+        uint32_t v = 0;
+        if (b < S) v = seed_off ? (uint32_t)(seed_off[b + 1] - seed_off[b]) : cnt[b];
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan(v, sm.scan, tot);
+        if (b < S) sm.px[b] = carry + ex;
+        carry += tot;
+    }
+    if (threadIdx.x == 0) sm.px[S] = carry;
+    __syncthreads();
+    return carry;
+}
+__device__ __forceinline__ uint32_t prefix_batch(const SampSmem& sm, uint32_t S, uint32_t x) {
+    uint32_t lo = 0, hi = S;  // b: px[b] <= x < px[b+1]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sm.px[mid] <= x) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
 
 // tp[0..S] = prefix of ceil(cnt[b] / SB_TILE); returns total tiles.
 __device__ uint32_t build_tiles(const uint32_t* cnt, uint32_t S, SampSmem& sm) {
@@ -127,7 +181,7 @@ __device__ __forceinline__ uint32_t table_insert(unsigned long long* tab, uint32
     const unsigned long long ent = ((unsigned long long)key << 32) | val;
     uint32_t s = hash32(key) & (H - 1);
     while (true) {
-        unsigned long long cur = tab[s];
+        unsigned long long cur = __ldcg(tab + s);  // never trust a stale L1 line
         if (cur == kEmptySlot) {
             unsigned long long prev = atomicCAS(&tab[s], kEmptySlot, ent);
             if (prev == kEmptySlot) return s;
@@ -135,6 +189,30 @@ __device__ __forceinline__ uint32_t table_insert(unsigned long long* tab, uint32
         }
         if ((uint32_t)(cur >> 32) == key) {
             if (cur > ent) atomicMin(&tab[s], ent);
+            return s;
+        }
+        s = (s + 1) & (H - 1);
+    }
+}
+
+// Insert for a draw: CAS first (one round trip when the slot is free).
+// *prior = the key's value before this insert: a local id (< kNewBit) when the
+// child was already in ids -- final for this layer, so the edge resolves now --
+// else kEmpty32 / another draw's (NEW | position).
+constexpr uint32_t kResolved = 0x80000000u;  // dslot flag: edge source known at insert time
+__device__ __forceinline__ uint32_t table_insert_draw(unsigned long long* tab, uint32_t H, uint32_t key,
+                                                      uint32_t val, uint32_t* prior) {
+    const unsigned long long ent = ((unsigned long long)key << 32) | val;
+    uint32_t s = hash32(key) & (H - 1);
+    while (true) {
+        const unsigned long long cur = atomicCAS(&tab[s], kEmptySlot, ent);
+        if (cur == kEmptySlot) {
+            *prior = kEmpty32;
+            return s;
+        }
+        if ((uint32_t)(cur >> 32) == key) {
+            if (cur > ent) atomicMin(&tab[s], ent);
+            *prior = (uint32_t)cur;
             return s;
         }
         s = (s + 1) & (H - 1);
@@ -220,7 +298,7 @@ __device__ __forceinline__ void clear_region(unsigned long long* tab, uint64_t t
     }
 }
 
-__global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
+__global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
     extern __shared__ unsigned char smem_raw[];
     SampSmem& sm = *reinterpret_cast<SampSmem*>(smem_raw);
     __shared__ uint32_t bcast;
@@ -228,6 +306,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
     const uint32_t tid = threadIdx.x;
     int cur = 0;
     uint32_t H = 0;
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[0] = gtimer();
 
     for (uint32_t l = 0; l < a.L || l == 0; ++l) {
         // ---- Phase D: (re)build the per-batch tables with the current ids --
@@ -262,19 +341,19 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
             unsigned long long* tnew = cur ? a.tab0 : a.tab1;
             if (l == 0) tnew = told;  // tables start clean
             const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
-            for (uint32_t b = 0; b < S; ++b) {
-                const uint32_t nb = l == 0 ? (uint32_t)(a.seed_off[b + 1] - a.seed_off[b]) : a.F[b];
-                for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + tid; k < nb; k += total_threads) {
-                    const uint64_t gi = (uint64_t)b * a.cap_ids + k;
-                    uint32_t v;
-                    if (l == 0) {
-                        v = a.seeds[a.seed_off[b] + k];
-                        a.ids[gi] = v;
-                    } else {
-                        v = a.ids[gi];
-                    }
-                    a.idslot[gi] = table_insert(tnew + (uint64_t)b * a.tab_cap, newH, v, (uint32_t)k);
+            const uint32_t tot = build_prefix(a.F, l == 0 ? a.seed_off : nullptr, S, sm);
+            for (uint32_t x = blockIdx.x * blockDim.x + tid; x < tot; x += (uint32_t)total_threads) {
+                const uint32_t b = prefix_batch(sm, S, x);
+                const uint32_t k = x - sm.px[b];
+                const uint64_t gi = (uint64_t)b * a.cap_ids + k;
+                uint32_t v;
+                if (l == 0) {
+                    v = a.seeds[a.seed_off[b] + k];
+                    a.ids[gi] = v;
+                } else {
+                    v = a.ids[gi];
                 }
+                table_insert(tnew + (uint64_t)b * a.tab_cap, newH, v, k);
             }
             if (l > 0) {  // the previous layer's table is dead: bulk-clear its used region
                 clear_region(told, a.tab_cap, H, S);
@@ -290,6 +369,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                 }
             }
             grid_sync(a.bar);
+            TRACE_STAMP(a, l, 0);
         }
         if (a.L == 0) break;
         unsigned long long* tab = cur ? a.tab1 : a.tab0;
@@ -335,6 +415,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
             }
         }
         grid_sync(a.bar);
+        TRACE_STAMP(a, l, 1);
 
         // ---- Phase E: scan takes -> draw offsets; draw, read child, insert ----
         {
@@ -382,17 +463,84 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                 // E2 (per draw): child read, edge, dedup insert -- one draw per
                 // thread so the random reads and atomics of a tile overlap.
                 const uint32_t tile_d0 = toff, tile_d1 = toff + tot;
-                for (uint32_t p = tile_d0 + tid; p < tile_d1; p += blockDim.x) {
-                    const uint2 st = bedge[p];
-                    const uint64_t lo = a.plo[(uint64_t)b * a.cap_ids + st.y];
-                    const uint32_t child = __ldg(a.indices + lo + st.x);
-                    bedge[p] = make_uint2(child, st.y);
-                    bdslot[p] = table_insert(btab, H, child, kNewBit | p);
+                constexpr int U = GX_E_UNROLL;  // draws per thread in flight
+                for (uint32_t q0 = tile_d0 + tid; q0 < tile_d1; q0 += U * blockDim.x) {
+                    uint2 st[U];
+                    uint32_t child[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t p = q0 + j * blockDim.x;
+                        if (p < tile_d1) st[j] = bedge[p];
+                    }
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t p = q0 + j * blockDim.x;
+                        if (p < tile_d1) {
+                            const uint64_t lo = a.plo[(uint64_t)b * a.cap_ids + st[j].y];
+                            child[j] = __ldg(a.indices + lo + st[j].x);
+                        }
+                    }
+                    // first probes of all U draws back to back, then resolve
+                    uint32_t slot[U];
+                    unsigned long long got[U];
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t p = q0 + j * blockDim.x;
+                        if (p < tile_d1) {
+                            slot[j] = hash32(child[j]) & (H - 1);
+#if GX_E_LOADFIRST
+                            got[j] = __ldcg(&btab[slot[j]]);
+#else
+                            got[j] = atomicCAS(&btab[slot[j]], kEmptySlot,
+                                               ((unsigned long long)child[j] << 32) | (kNewBit | p));
+#endif
+                        }
+                    }
+#if GX_E_LOADFIRST
+                    // claim the empty first slots (a match needs no CAS; most repeats of a hub stop here)
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t p = q0 + j * blockDim.x;
+                        if (p < tile_d1 && got[j] == kEmptySlot)
+                            got[j] = atomicCAS(&btab[slot[j]], kEmptySlot,
+                                               ((unsigned long long)child[j] << 32) | (kNewBit | p));
+                    }
+#endif
+#pragma unroll
+                    for (int j = 0; j < U; ++j) {
+                        const uint32_t p = q0 + j * blockDim.x;
+                        if (p < tile_d1) {
+                            const unsigned long long ent = ((unsigned long long)child[j] << 32) | (kNewBit | p);
+                            uint32_t sl = slot[j], prior;
+                            unsigned long long cur = got[j];
+                            while (true) {
+                                if (cur == kEmptySlot) {
+                                    prior = kEmpty32;
+                                    break;
+                                }
+                                if ((uint32_t)(cur >> 32) == child[j]) {
+                                    if (cur > ent) atomicMin(&btab[sl], ent);
+                                    prior = (uint32_t)cur;
+                                    break;
+                                }
+                                sl = (sl + 1) & (H - 1);
+                                cur = atomicCAS(&btab[sl], kEmptySlot, ent);
+                            }
+                            if (prior < kNewBit) {  // child already in ids: its local id is final
+                                bedge[p] = make_uint2(prior, st[j].y);
+                                bdslot[p] = sl | kResolved;
+                            } else {
+                                bedge[p] = make_uint2(child[j], st[j].y);
+                                bdslot[p] = sl;
+                            }
+                        }
+                    }
                 }
                 __syncthreads();
             }
         }
         grid_sync(a.bar);
+        TRACE_STAMP(a, l, 2);
 
         // ---- Phase F: first-occurrence flags per draw, tile sums ----------
         {
@@ -409,10 +557,13 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                     const uint32_t p = p0 + j;
                     if (p < Tb) {
                         const uint64_t gd = (uint64_t)b * a.cap_draw + p;
-                        const unsigned long long e = btab[a.dslot[gd]];
-                        const uint32_t child = bedge[p].x;
-                        const uint32_t fl =
-                            e == (((unsigned long long)child << 32) | (kNewBit | p)) ? 1u : 0u;
+                        const uint32_t ds = a.dslot[gd];
+                        uint32_t fl = 0;
+                        if (!(ds & kResolved)) {
+                            const unsigned long long e = btab[ds];
+                            const uint32_t child = bedge[p].x;
+                            fl = e == (((unsigned long long)child << 32) | (kNewBit | p)) ? 1u : 0u;
+                        }
                         a.drank[gd] = fl;
                         s += fl;
                     }
@@ -422,6 +573,7 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
             }
         }
         grid_sync(a.bar);
+        TRACE_STAMP(a, l, 3);
 
         // ---- Phase H: rank winners by draw position -> new local ids -------
         {
@@ -450,7 +602,8 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                 uint32_t tot;
                 uint32_t r = toff + block_excl_scan(s, sm.scan, tot);
                 unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
-                const uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+                uint2* bedge_w = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+                const uint2* bedge = bedge_w;
 #pragma unroll
                 for (int j = 0; j < SB_IPT; ++j) {
                     if (fl[j]) {
@@ -459,25 +612,29 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
                         const uint32_t local = Fb + r;
                         const uint32_t slot = a.dslot[(uint64_t)b * a.cap_draw + p];
                         a.ids[(uint64_t)b * a.cap_ids + local] = child;
-                        a.idslot[(uint64_t)b * a.cap_ids + local] = slot;
                         btab[slot] = ((unsigned long long)child << 32) | local;
+                        bedge_w[p].x = local;
                         ++r;
                     }
                 }
             }
         }
         grid_sync(a.bar);
+        TRACE_STAMP(a, l, 4);
 
         // ---- Phase I: edge sources -> local ids; per-batch bookkeeping ------
         {
             const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
-            for (uint32_t b = 0; b < S; ++b) {
-                const uint32_t Tb = a.T[b];
-                const unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
-                uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
-                const uint32_t* bdslot = a.dslot + (uint64_t)b * a.cap_draw;
-                for (uint64_t p = (uint64_t)blockIdx.x * blockDim.x + tid; p < Tb; p += total_threads)
-                    bedge[p].x = (uint32_t)btab[bdslot[p]];
+            const uint32_t tot = build_prefix(a.T, nullptr, S, sm);
+            for (uint32_t x = blockIdx.x * blockDim.x + tid; x < tot; x += (uint32_t)total_threads) {
+                const uint32_t b = prefix_batch(sm, S, x);
+                const uint32_t p = x - sm.px[b];
+                const uint64_t gd = (uint64_t)b * a.cap_draw + p;
+                const uint32_t ds = a.dslot[gd];
+                // resolved at insert time or written by the winner: nothing to do
+                if (!(ds & kResolved) && !a.drank[gd])
+                    a.edges[(uint64_t)b * a.cap_e_batch + a.e_off[l] + p].x =
+                        (uint32_t)tab[(uint64_t)b * a.tab_cap + ds];
             }
             for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
                 a.layer_count[(uint64_t)b * a.L + l] = a.T[b];
@@ -486,10 +643,215 @@ __global__ void __launch_bounds__(SB_THREADS) k_sample(SampArgs a) {
             }
         }
         grid_sync(a.bar);
+        TRACE_STAMP(a, l, 5);
     }
 
     // ---- leave the live table clean for the next call (coalesced bulk clear) ----
     clear_region(cur ? a.tab1 : a.tab0, a.tab_cap, H, S);
+    if (a.trace && blockIdx.x == 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) a.trace[127] = gtimer() - a.trace[0];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Cluster sampler: one thread-block cluster (CS CTAs on CS SMs) owns a batch at
+// a time and walks the batches of the launch independently of the other
+// clusters. All synchronisation is the hardware cluster barrier; per-CTA
+// partial sums are exchanged through distributed shared memory; the batch's
+// dedup table is the cluster's private region in global memory, and since only
+// gridDim/CS batches are live at once their tables stay L2-resident. Same
+// phases and bit-exact outputs as k_sample (sampler.hpp:69-117).
+// ---------------------------------------------------------------------------
+constexpr int SC_THREADS = 512;
+
+struct ClSmem {
+    uint32_t scan[34];
+    uint32_t part[4];       // partials published to the cluster
+    uint32_t bc[4];
+    unsigned long long red[34];
+};
+
+// sum over ranks < r (and total) of part[idx] published by every CTA of the cluster
+__device__ __forceinline__ void cluster_prefix(cg::cluster_group& cl, ClSmem& sm, int idx, uint32_t CS,
+                                               uint32_t* before, uint32_t* total) {
+    if (threadIdx.x == 0) {
+        uint32_t b = 0, t = 0;
+        for (uint32_t r = 0; r < CS; ++r) {
+            const uint32_t* rp = cl.map_shared_rank(sm.part, r);
+            const uint32_t v = rp[idx];
+            if (r < cl.block_rank()) b += v;
+            t += v;
+        }
+        sm.bc[0] = b;
+        sm.bc[1] = t;
+    }
+    __syncthreads();
+    *before = sm.bc[0];
+    *total = sm.bc[1];
+    __syncthreads();
+}
+
+template <int CS>
+__global__ void __launch_bounds__(SC_THREADS) k_sample_cl(SampArgs a) {
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ ClSmem sm;
+    const uint32_t rank = cl.block_rank();
+    const uint32_t cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    const uint32_t tid = threadIdx.x, T = blockDim.x;
+    const uint32_t ct = rank * T + tid, CT = CS * T;
+    unsigned long long* tabs[2] = {a.tab0 + (uint64_t)cid * a.tab_cap, a.tab1 + (uint64_t)cid * a.tab_cap};
+    unsigned long long io_pages = 0, io_lists = 0, io_bytes = 0;
+
+    for (uint32_t b = cid; b < a.S; b += ncl) {
+        const uint64_t ibase = (uint64_t)b * a.cap_ids;
+        const uint32_t ns = (uint32_t)(a.seed_off[b + 1] - a.seed_off[b]);
+        const uint64_t seed = a.bseed[b];
+        uint32_t F = ns;
+        uint64_t dbase = 0;
+        uint32_t H = 0;
+        int cur = 0;
+        for (uint32_t l = 0; l < a.L || l == 0; ++l) {
+            // ---- table (re)build: H = nextpow2(2 * min(cap, F (1 + f_l))) ----
+            const unsigned long long need0 = (unsigned long long)F * (1ull + (a.L ? a.fan[l] : 0));
+            const unsigned long long need = need0 < a.cap_ids ? need0 : (unsigned long long)a.cap_ids;
+            uint32_t newH = 1024;
+            while (newH < 2 * need) newH <<= 1;
+            if (newH > a.tab_cap) newH = (uint32_t)a.tab_cap;
+            if (l == 0 || newH != H) {
+                unsigned long long* told = tabs[cur];
+                unsigned long long* tnew = l == 0 ? told : tabs[cur ^ 1];
+                if (l > 0)
+                    for (uint32_t x = ct; x < H; x += CT) told[x] = kEmptySlot;
+                for (uint32_t k = ct; k < F; k += CT) {
+                    uint32_t v;
+                    if (l == 0) {
+                        v = a.seeds[a.seed_off[b] + k];
+                        a.ids[ibase + k] = v;
+                    } else {
+                        v = __ldcg(a.ids + ibase + k);
+                    }
+                    table_insert(tnew, newH, v, k);
+                }
+                if (l > 0) cur ^= 1;
+                H = newH;
+                cl.sync();
+            }
+            if (a.L == 0) break;
+            unsigned long long* tab = tabs[cur];
+            const uint32_t f = a.fan[l];
+            uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
+            uint32_t* bdslot = a.dslot + (uint64_t)b * a.cap_draw;
+            uint32_t* bdrank = a.drank + (uint64_t)b * a.cap_draw;
+
+            // ---- A: per parent deg/take (this CTA's contiguous chunk), IoStats ----
+            const uint32_t pch = (F + CS - 1) / CS;
+            const uint32_t k0 = min(F, rank * pch), k1 = min(F, k0 + pch);
+            uint32_t csum = 0;
+            for (uint32_t k = k0 + tid; k < k1; k += T) {
+                const uint64_t gi = ibase + k;
+                const uint32_t v = __ldcg(a.ids + gi);  // written by other CTAs of the cluster
+                const uint64_t lo = a.indptr[v], hi = a.indptr[v + 1];
+                const uint32_t deg = (uint32_t)(hi - lo);
+                const uint32_t take = min(f, deg);
+                a.plo[gi] = lo;
+                a.pdeg[gi] = deg;
+                a.pscan[gi] = take;
+                csum += take;
+                io_lists += 1;
+                io_pages += pages_touched(8 * lo, 8 * hi);
+                io_bytes += 8ull * deg;
+            }
+            csum = block_sum(csum, sm.scan);
+            if (tid == 0) sm.part[0] = csum;
+            cl.sync();
+            uint32_t doff, Tb;
+            cluster_prefix(cl, sm, 0, CS, &doff, &Tb);
+
+            // ---- E: positions per parent, then one draw per thread ----------------
+            for (uint32_t r0 = k0; r0 < k1; r0 += T * 4) {
+                uint32_t take[4], s = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t k = r0 + tid * 4 + j;
+                    take[j] = k < k1 ? a.pscan[ibase + k] : 0;
+                    s += take[j];
+                }
+                uint32_t tot;
+                uint32_t off = doff + block_excl_scan(s, sm.scan, tot);
+                const uint32_t d0 = doff;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (take[j]) {
+                        const uint32_t k = r0 + tid * 4 + j;
+                        draw_positions(take[j], seed, dbase + off, a.pdeg[ibase + k], bedge + off, k);
+                    }
+                    off += take[j];
+                }
+                __syncthreads();
+                for (uint32_t p = d0 + tid; p < d0 + tot; p += T) {
+                    const uint2 st = bedge[p];
+                    const uint32_t child = __ldg(a.indices + a.plo[ibase + st.y] + st.x);
+                    bedge[p] = make_uint2(child, st.y);
+                    bdslot[p] = table_insert(tab, H, child, kNewBit | p);
+                }
+                doff += tot;
+                __syncthreads();
+            }
+            cl.sync();  // every insert of the layer is in the table
+
+            // ---- F/H: first-occurrence winners ranked by draw position -------------
+            const uint32_t dch = (Tb + CS - 1) / CS;
+            const uint32_t p0 = min(Tb, rank * dch), p1 = min(Tb, p0 + dch);
+            uint32_t wsum = 0;
+            for (uint32_t p = p0 + tid; p < p1; p += T) {
+                const uint32_t child = __ldcg(&bedge[p].x);
+                const uint32_t fl =
+                    __ldcg(tab + __ldcg(bdslot + p)) == (((unsigned long long)child << 32) | (kNewBit | p)) ? 1u : 0u;
+                bdrank[p] = fl;
+                wsum += fl;
+            }
+            wsum = block_sum(wsum, sm.scan);
+            if (tid == 0) sm.part[1] = wsum;
+            cl.sync();
+            uint32_t wbefore, wtot;
+            cluster_prefix(cl, sm, 1, CS, &wbefore, &wtot);
+            uint32_t rk = wbefore;
+            for (uint32_t q0 = p0; q0 < p1; q0 += T) {
+                const uint32_t p = q0 + tid;
+                const uint32_t fl = p < p1 ? bdrank[p] : 0;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan(fl, sm.scan, tot);
+                if (fl) {
+                    const uint32_t child = __ldcg(&bedge[p].x);
+                    const uint32_t local = F + rk + ex;
+                    a.ids[ibase + local] = child;
+                    tab[__ldcg(bdslot + p)] = ((unsigned long long)child << 32) | local;
+                }
+                rk += tot;
+            }
+            cl.sync();
+            // ---- I: edge sources -> local ids --------------------------------------
+            for (uint32_t p = ct; p < Tb; p += CT) bedge[p].x = (uint32_t)__ldcg(tab + __ldcg(bdslot + p));
+            if (ct == 0) a.layer_count[(uint64_t)b * a.L + l] = Tb;
+            dbase += Tb;
+            F += wtot;
+            cl.sync();
+        }
+        // leave this cluster's table clean for its next batch
+        unsigned long long* tab = tabs[cur];
+        for (uint32_t x = ct; x < H; x += CT) tab[x] = kEmptySlot;
+        if (ct == 0) a.n_ids[b] = F;
+        cl.sync();
+    }
+    io_pages = warp_sum(io_pages);
+    io_lists = warp_sum(io_lists);
+    io_bytes = warp_sum(io_bytes);
+    if ((tid & 31) == 0 && io_lists) {
+        atomicAdd(&a.io[0], io_pages);
+        atomicAdd(&a.io[1], io_lists);
+        atomicAdd(&a.io[2], io_bytes);
+    }
 }
 
 static uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t cap) {
@@ -611,6 +973,13 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     a.tab_cap = tab_cap;
     a.io = ss.io.p;
     a.bar = ctx->barrier.p;
+    static const bool trace = std::getenv("GX_SAMPLER_TRACE") != nullptr;
+    static DevBuf<unsigned long long> tbuf;
+    if (trace) {
+        tbuf.reserve(128);
+        GX_CUDA(cudaMemsetAsync(tbuf.p, 0, 128 * 8, st));
+        a.trace = tbuf.p;
+    }
 
     const size_t smem = sizeof(SampSmem);
     static int blocks_per_sm = -1;
@@ -626,6 +995,46 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
     dim3 grid(ctx->num_sms * std::min(bps_use, blocks_per_sm)), block(SB_THREADS);
+    // cluster sampler (GX_SAMPLER_CLUSTER = 8 or 16 CTAs per batch; 0 = grid-wide kernel)
+    static const int cs = [] {
+        const char* e = std::getenv("GX_SAMPLER_CLUSTER");
+        const int v = e ? std::atoi(e) : 0;  // measured slower than the grid kernel at B=1000
+        return (v == 8 || v == 16) ? v : 0;
+    }();
+    if (cs) {
+        static bool attr = false;
+        if (!attr) {
+            GX_CUDA(cudaFuncSetAttribute(k_sample_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            attr = true;
+        }
+        const uint32_t ncl = std::max(1, ctx->num_sms / cs);
+        for (uint64_t c0 = 0; c0 < S; c0 += CH) {
+            const uint64_t nb = std::min(CH, S - c0);
+            a.S = (uint32_t)nb;
+            a.bseed = ss.bseed.p + c0;
+            a.seed_off = ss.seed_off.p + c0;
+            a.ids = out->ids.p + c0 * cap_ids;
+            a.n_ids = out->n_ids.p + c0;
+            a.edges = out->edges.p + c0 * out->cap_e_batch;
+            a.layer_count = out->layer_count.p + c0 * L;
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(ncl * cs);
+            lc.blockDim = dim3(SC_THREADS);
+            lc.dynamicSmemBytes = 0;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            if (cs == 16) GX_CUDA(cudaLaunchKernelEx(&lc, k_sample_cl<16>, a));
+            else GX_CUDA(cudaLaunchKernelEx(&lc, k_sample_cl<8>, a));
+            GX_CHECK_LAUNCH();
+        }
+        return;
+    }
     for (uint64_t c0 = 0; c0 < S; c0 += CH) {
         const uint64_t nb = std::min(CH, S - c0);
         a.S = (uint32_t)nb;
@@ -638,6 +1047,23 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         void* args[] = {&a};
         GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
         GX_CHECK_LAUNCH();
+        if (trace) {
+            unsigned long long h[128];
+            GX_CUDA(cudaMemcpyAsync(h, tbuf.p, sizeof h, cudaMemcpyDeviceToHost, st));
+            GX_CUDA(cudaStreamSynchronize(st));
+            const char* names[6] = {"D", "A", "E", "F", "H", "I"};
+            unsigned long long prev = 0;
+            std::string line = "[sampler trace us]";
+            for (uint32_t l = 0; l < std::max<uint32_t>(L, 1); ++l)
+                for (int ph = 0; ph < 6; ++ph) {
+                    const unsigned long long t = h[1 + l * 8 + ph];
+                    if (!t) continue;
+                    line += " L" + std::to_string(l) + names[ph] + "=" + std::to_string((t - prev) / 1000.0).substr(0, 6);
+                    prev = t;
+                }
+            line += " end=" + std::to_string((h[127] - prev) / 1000.0).substr(0, 6);
+            fprintf(stderr, "%s\n", line.c_str());
+        }
     }
 }
 
