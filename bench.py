@@ -419,7 +419,7 @@ def main():
         "e2e": {"value": edges_all / wall_s, "unit": "sampled_edges/s",
                 "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
                 "d2h_bytes_per_step": int(8 * S + 8 * 16)},
-        "gpu_launches": (2 * S + 4) * args.steps,
+        "gpu_launches": int(sum(s.kernel_launches for s in stats)),
         "roofline": {"kernel": "k_gather_tma2 (TMA bulk row gather)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,

@@ -230,6 +230,8 @@ typedef struct gx_pipeline_stats {
     double ms_sample, ms_inspect, ms_switch, ms_gather; /* device-timed stage durations */
     double ms_gather_kernels;  /* sum of the S gather-kernel durations (CUDA events) */
     double ms_apply_kernels;   /* sum of the S apply-kernel durations */
+    uint64_t kernel_launches;  /* this library's kernel launches for the superbatch
+                                  (sampler, inspector, cache init, gathers, non-empty applies) */
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,
                              uint32_t n_layers, uint64_t num_entries, gx_pipeline** out);
@@ -253,6 +255,16 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
                            gx_pipeline_stats* stats);
 /* the cudaStream_t the executor of this pipeline runs on */
 void* gx_pipeline_exec_stream(gx_pipeline* p);
+/* Device pointer to iteration i's gathered rows (|ids_i| x row_bytes, the
+ * RowMatrix of feature_cache.hpp:58 kept in HBM) of a waited-for superbatch.
+ * Valid until the slot is resubmitted (ticket + 2). The executor keeps the whole
+ * superbatch's batches resident (rows of iteration i at row offset
+ * sum_{j<i}|ids_j|) when they fit GX_BATCH_BUDGET_MB (default 24 GiB per slot);
+ * otherwise it reuses one iteration-sized buffer and only the last iteration is
+ * readable (GX_LOGIC_ERROR for the others). host_out (nullable) additionally
+ * receives a copy of the rows. */
+gx_status gx_pipeline_batch(gx_pipeline* p, uint64_t ticket, uint64_t i, const void** rows,
+                            uint64_t* n_rows, void* host_out);
 
 /* Optional per-iteration digest of each gathered batch (for end-to-end parity
  * checks; off by default, costs one extra read of every batch):

@@ -40,7 +40,8 @@ class PipelineStatsC(C.Structure):
                 ("predicted_misses", u64), ("init_size", u64), ("total_in", u64),
                 ("total_out", u64), ("sample_io", IoStatsC), ("gather_io", IoStatsC),
                 ("ms_sample", dbl), ("ms_inspect", dbl), ("ms_switch", dbl), ("ms_gather", dbl),
-                ("ms_gather_kernels", dbl), ("ms_apply_kernels", dbl)]
+                ("ms_gather_kernels", dbl), ("ms_apply_kernels", dbl),
+                ("kernel_launches", u64)]
 
 
 PIO = C.POINTER(IoStatsC)
@@ -119,6 +120,7 @@ SIGNATURES = {
     "gx_pipeline_submit": (i32, [vp, vp, vp, u64, u64, u64, P64]),
     "gx_pipeline_wait": (i32, [vp, u64, vp, C.POINTER(PipelineStatsC)]),
     "gx_pipeline_exec_stream": (vp, [vp]),
+    "gx_pipeline_batch": (i32, [vp, u64, u64, C.POINTER(vp), P64, vp]),
     "gx_pipeline_set_digest": (i32, [vp, i32]),
     "gx_pipeline_digests": (i32, [vp, vp]),
 }

@@ -824,6 +824,7 @@ class PipelineStats:
     ms_gather: float
     ms_gather_kernels: float
     ms_apply_kernels: float
+    kernel_launches: int
     misses: np.ndarray
 
 
@@ -844,6 +845,7 @@ class Pipeline:
         if digest:
             check(lib.gx_pipeline_set_digest(h, 1))
         self._S = 0
+        self._last = -1
         self._sizes = {}
 
     def __del__(self):
@@ -871,10 +873,25 @@ class Pipeline:
         st = PipelineStatsC()
         check(lib.gx_pipeline_wait(self.h, ticket, misses.ctypes.data, C.byref(st)))
         self._S = S
+        self._last = ticket
         return PipelineStats(st.sampled_edges, st.gathered_rows, st.total_misses, st.predicted_misses,
                              st.init_size, st.total_in, st.total_out, _io(st.sample_io),
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
-                             st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, misses[:S].copy())
+                             st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, st.kernel_launches,
+                             misses[:S].copy())
+
+    def batch(self, i: int, ticket: Optional[int] = None) -> np.ndarray:
+        """Iteration i's gathered rows of a waited-for superbatch (default: the
+        last one waited for) -- a host copy of the device-resident batch
+        (gx_pipeline_batch)."""
+        ticket = self._last if ticket is None else ticket
+        n = C.c_uint64()
+        check(lib.gx_pipeline_batch(self.h, ticket, i, None, C.byref(n), None))
+        f = self.features
+        out = np.empty((n.value, f.dim()), dtype=f.dtype)
+        if n.value:
+            check(lib.gx_pipeline_batch(self.h, ticket, i, None, None, out.ctypes.data))
+        return out
 
     @property
     def exec_stream(self) -> int:

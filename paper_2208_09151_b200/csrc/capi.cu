@@ -72,7 +72,16 @@ struct PipeSlot {
     gx::DevBuf<unsigned long long> counters, digests;
     gx::PinBuf<unsigned long long> h_cnt, h_dig;
     std::vector<uint64_t> o;  // trace offsets
+    // gathered rows: every iteration's batch at row o[i] (whole superbatch
+    // resident: `full`), or one iteration-sized buffer reused per iteration
+    gx::DevBuf<uint8_t> batch;
+    bool full = false;
+    gx::DevBuf<uint32_t> d_off;  // o[] on the device (segment-mode miss charging)
+    gx::PinBuf<uint32_t> h_off;
+    uint64_t nseg = 0;     // gather launches (segments of iterations)
+    uint64_t ticket = ~0ull;
     uint64_t sampled_edges = 0;
+    uint64_t launches = 0;  // this library's kernels launched for the superbatch
     gx_iostats sample_io{};
     cudaEvent_t ev[6] = {};  // A: start, sampled, inspected; B: exec start, switched, done
     std::vector<cudaEvent_t> kev;
@@ -86,7 +95,6 @@ struct gx_pipeline {
     uint64_t K = 0;
     gx_samples samples;
     gx::DevBuf<uint8_t> cache_rows;
-    gx::DevBuf<uint8_t> batch;
     cudaStream_t exec = nullptr;
     PipeSlot slot[2];
     uint64_t submitted = 0;
@@ -447,6 +455,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         const uint64_t t = p->submitted;
         PipeSlot& sl = p->slot[t & 1];
         if (sl.pending) fail(GX_LOGIC_ERROR, "two superbatches already in flight: wait for the older one first");
+        const uint64_t launches0 = gx::g_kernel_launches.load(std::memory_order_relaxed);
         std::vector<uint64_t> bs(S);
         for (uint64_t i = 0; i < S; ++i) bs[i] = derive_seed(global_seed, first_global_batch + i);
         const uint32_t L = (uint32_t)p->fanouts.size();
@@ -480,7 +489,15 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         GX_CUDA(cudaEventRecord(sl.ev[3], B));
         uint64_t maxw = 0;
         for (uint64_t i = 0; i < S; ++i) maxw = std::max(maxw, sl.o[i + 1] - sl.o[i]);
-        p->batch.reserve(std::max<uint64_t>(maxw * p->f->row_bytes, 16));
+        const uint64_t rb = p->f->row_bytes;
+        // whole superbatch resident when it fits the per-slot budget (GX_BATCH_BUDGET_MB)
+        static const uint64_t budget = (uint64_t)std::max(0, gx::env_int("GX_BATCH_BUDGET_MB", 24576)) << 20;
+        sl.full = sl.o[S] * rb <= budget;
+        sl.batch.reserve(std::max<uint64_t>((sl.full ? sl.o[S] : maxw) * rb, 16));
+        sl.h_off.reserve(S + 1);
+        sl.d_off.reserve(S + 1);
+        for (uint64_t i = 0; i <= S; ++i) sl.h_off.p[i] = (uint32_t)sl.o[i];
+        GX_CUDA(cudaMemcpyAsync(sl.d_off.p, sl.h_off.p, (S + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, B));
         sl.counters.reserve(8 * (S + 1));
         sl.h_cnt.reserve(8 * (S + 1));
         GX_CUDA(cudaMemsetAsync(sl.counters.p, 0, 8 * (S + 1) * 8, B));
@@ -501,21 +518,38 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
                               sl.counters.p + 8 * S);
             GX_CUDA(cudaEventRecord(sl.ev[4], B));
-            // (4) main loop: gather + apply
-            for (uint64_t i = 0; i < S; ++i) {
-                const uint64_t ni = sl.o[i + 1] - sl.o[i];
-                GX_CUDA(cudaEventRecord(sl.kev[3 * i], B));
-                launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], ni, p->cache_rows.p, p->f,
-                                       p->batch.p, sl.counters.p + 8 * i);
-                GX_CUDA(cudaEventRecord(sl.kev[3 * i + 1], B));
-                if (p->digest) launch_digest(ctx, p->batch.p, ni, p->f->row_bytes, sl.digests.p + i);
-                const uint64_t a = sl.cs.h_in_off[i], b = sl.cs.h_out_off[i];
-                launch_apply_slots(ctx, sl.cs.in_ids.p + a, sl.cs.in_pos.p + a, sl.cs.in_slot.p + a,
-                                   (uint32_t)(sl.cs.h_in_off[i + 1] - a), sl.cs.out_ids.p + b,
-                                   (uint32_t)(sl.cs.h_out_off[i + 1] - b), nullptr, p->batch.p, p->cache_rows.p,
-                                   p->f->row_bytes);
-                GX_CUDA(cudaEventRecord(sl.kev[3 * i + 2], B));
+            // (4) main loop. Iterations whose changesets are empty do not mutate
+            // the cache, so with the whole superbatch resident a run of them is
+            // gathered by one launch (segment), then the last one's changeset applied.
+            auto empty_cs = [&](uint64_t i) {
+                return sl.cs.h_in_off[i + 1] == sl.cs.h_in_off[i] && sl.cs.h_out_off[i + 1] == sl.cs.h_out_off[i];
+            };
+            auto rows_of = [&](uint64_t i) { return sl.batch.p + (sl.full ? sl.o[i] * rb : 0); };
+            uint64_t nseg = 0;
+            for (uint64_t i = 0; i < S;) {
+                uint64_t e = i;  // segment [i, e]
+                if (sl.full)
+                    while (e + 1 < S && empty_cs(e)) ++e;
+                GX_CUDA(cudaEventRecord(sl.kev[3 * nseg], B));
+                launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], sl.o[e + 1] - sl.o[i],
+                                       p->cache_rows.p, p->f, rows_of(i), sl.counters.p + 8 * i, sl.d_off.p + i,
+                                       (uint32_t)(e - i + 1));
+                GX_CUDA(cudaEventRecord(sl.kev[3 * nseg + 1], B));
+                if (p->digest)
+                    for (uint64_t k = i; k <= e; ++k)
+                        launch_digest(ctx, rows_of(k), sl.o[k + 1] - sl.o[k], rb, sl.digests.p + k);
+                if (!empty_cs(e)) {
+                    const uint64_t a = sl.cs.h_in_off[e], b = sl.cs.h_out_off[e];
+                    launch_apply_slots(ctx, sl.cs.in_ids.p + a, sl.cs.in_pos.p + a, sl.cs.in_slot.p + a,
+                                       (uint32_t)(sl.cs.h_in_off[e + 1] - a), sl.cs.out_ids.p + b,
+                                       (uint32_t)(sl.cs.h_out_off[e + 1] - b), nullptr, rows_of(e),
+                                       p->cache_rows.p, rb);
+                }
+                GX_CUDA(cudaEventRecord(sl.kev[3 * nseg + 2], B));
+                ++nseg;
+                i = e + 1;
             }
+            sl.nseg = nseg;
         } catch (...) {
             ctx->launch_stream = nullptr;
             throw;
@@ -524,9 +558,11 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         GX_CUDA(cudaMemcpyAsync(sl.h_cnt.p, sl.counters.p, 8 * (S + 1) * 8, cudaMemcpyDeviceToHost, B));
         if (p->digest) GX_CUDA(cudaMemcpyAsync(sl.h_dig.p, sl.digests.p, S * 8, cudaMemcpyDeviceToHost, B));
         GX_CUDA(cudaEventRecord(sl.ev[5], B));
+        sl.launches = gx::g_kernel_launches.load(std::memory_order_relaxed) - launches0;
         // the next submit reuses the context stream's scratch: it may start as
         // soon as the inspector is done; slot reuse is guarded by `pending`
         sl.pending = true;
+        sl.ticket = t;
         *ticket = t;
         p->submitted = t + 1;
     });
@@ -543,13 +579,15 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
         const unsigned long long* cnt = sl.h_cnt.p;
         uint64_t tm = 0, pm = 0;
         gx_iostats gio{};
+        // per iteration (segment-mode gathers): [1] misses, [2] pages; a miss
+        // reads one row of row_bytes (feature_cache.hpp:66-71)
         for (uint64_t i = 0; i < S; ++i) {
             if (misses_per_iter) misses_per_iter[i] = cnt[8 * i + 1];
             tm += cnt[8 * i + 1];
             pm += sl.cs.h_misses[i];
             gio.pages_read += cnt[8 * i + 2];
-            gio.rows_read += cnt[8 * i + 3];
-            gio.bytes_read += cnt[8 * i + 4];
+            gio.rows_read += cnt[8 * i + 1];
+            gio.bytes_read += cnt[8 * i + 1] * p->f->row_bytes;
         }
         if (p->digest) p->h_digests.assign(sl.h_dig.p, sl.h_dig.p + S);
         if (stats) {
@@ -572,7 +610,7 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             stats->ms_switch = ms[2];
             stats->ms_gather = ms[3];
             double gk = 0, ak = 0;
-            for (uint64_t i = 0; i < S; ++i) {
+            for (uint64_t i = 0; i < sl.nseg; ++i) {
                 float a = 0, b = 0;
                 GX_CUDA(cudaEventElapsedTime(&a, sl.kev[3 * i], sl.kev[3 * i + 1]));
                 GX_CUDA(cudaEventElapsedTime(&b, sl.kev[3 * i + 1], sl.kev[3 * i + 2]));
@@ -581,6 +619,28 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             }
             stats->ms_gather_kernels = gk;
             stats->ms_apply_kernels = ak;
+            stats->kernel_launches = sl.launches;
+        }
+    });
+}
+
+gx_status gx_pipeline_batch(gx_pipeline* p, uint64_t ticket, uint64_t i, const void** rows, uint64_t* n_rows,
+                            void* host_out) {
+    return guard([&] {
+        if (!p) fail(GX_INVALID_ARGUMENT, "null pipeline");
+        const PipeSlot& sl = p->slot[ticket & 1];
+        if (sl.ticket != ticket || sl.pending)
+            fail(GX_LOGIC_ERROR, "batches are readable after wait(ticket) until that slot is resubmitted");
+        if (i >= sl.S) fail(GX_OUT_OF_RANGE, "iteration index out of range");
+        if (!sl.full && i + 1 != sl.S)
+            fail(GX_LOGIC_ERROR, "superbatch exceeded GX_BATCH_BUDGET_MB: only the last iteration's rows are resident");
+        const uint8_t* src = sl.batch.p + (sl.full ? sl.o[i] * p->f->row_bytes : 0);
+        const uint64_t n = sl.o[i + 1] - sl.o[i];
+        if (rows) *rows = src;
+        if (n_rows) *n_rows = n;
+        if (host_out && n) {
+            GX_CUDA(cudaMemcpyAsync(host_out, src, n * p->f->row_bytes, cudaMemcpyDeviceToHost, p->exec));
+            GX_CUDA(cudaStreamSynchronize(p->exec));
         }
     });
 }

@@ -4,6 +4,8 @@
 // entry point runs inside gx::guard(), which maps it to gx_status and stores
 // the message for gx_last_error() (include/gx_b200.h).
 #pragma once
+#include <cstdlib>
+#include <atomic>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -18,6 +20,13 @@
 #include "gx_b200.h"
 
 namespace gx {
+
+// Tuning knob from the environment (read once per call site); def when unset.
+inline int env_int(const char* name, int def) {
+    const char* e = std::getenv(name);
+    return (e && *e) ? std::atoi(e) : def;
+}
+
 
 struct Error : std::exception {
     gx_status status;
@@ -54,7 +63,14 @@ gx_status guard(F&& f) {
             ::gx::fail(GX_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(_e)); \
     } while (0)
 
-#define GX_CHECK_LAUNCH() GX_CUDA(cudaGetLastError())
+// Every launch of one of this library's kernels is followed by GX_CHECK_LAUNCH(),
+// which also counts it (gx_pipeline_stats.kernel_launches).
+inline std::atomic<uint64_t> g_kernel_launches{0};
+#define GX_CHECK_LAUNCH()                                                  \
+    do {                                                                   \
+        ::gx::g_kernel_launches.fetch_add(1, std::memory_order_relaxed); \
+        GX_CUDA(cudaGetLastError());                                       \
+    } while (0)
 
 constexpr uint32_t kNever = 0xFFFFFFFFu;     // "no further access" / empty key
 constexpr uint32_t kEmpty32 = 0xFFFFFFFFu;

@@ -138,9 +138,12 @@ void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* 
                    const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
                    unsigned long long* counters);
 // gather with the serving slot of every row already resolved (kNever = miss)
+// seg_off != nullptr: segment mode -- rows of nseg consecutive iterations
+// (absolute offsets seg_off[0..nseg]); misses/pages are charged per iteration
+// into counters[8 * it + 1 / + 2] (executor.cu, SegInfo).
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
                             const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
-                            unsigned long long* counters);
+                            unsigned long long* counters, const uint32_t* seg_off = nullptr, uint32_t nseg = 0);
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos,
                         const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
                         uint32_t n_out, int32_t* table, const uint8_t* batch, uint8_t* cache_rows,

@@ -930,7 +930,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.c_ref.reserve(std::max(Keff, maxw));
     B.in_node.reserve(maxw);
     B.in_pos.reserve(maxw);
-    const int grid = ctx->num_sms;
+    static const int grid_knob = env_int("GX_INSPECT_CTAS", 0);  // CTAs (0 = one per SM)
+    const int grid = grid_knob > 0 ? std::min(grid_knob, ctx->num_sms) : ctx->num_sms;
     B.chunk_cnt.reserve(2 * grid);
     B.bm_cnt.reserve(grid);
     B.st.reserve(16);
@@ -1040,8 +1041,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     GX_CUDA(cudaLaunchCooperativeKernel((void*)k_inspect, dim3(grid), dim3(IN_THREADS), args, smem, st));
     GX_CHECK_LAUNCH();
 
-    if (n_init_explicit > 0)
+    if (n_init_explicit > 0) {
         k_init_pos<<<ctx->num_sms, 256, 0, st>>>(B.init_ext.p, (uint32_t)n_init_explicit, is.init_pos.p, 0);
+        GX_CHECK_LAUNCH();
+    }
     IState hs;
     GX_CUDA(cudaMemcpyAsync(&hs, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
     std::vector<uint32_t>&m32 = B.h_m, &io32 = B.h_io, &oo32 = B.h_oo;

@@ -994,7 +994,9 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         const char* e = std::getenv("GX_SAMPLER_BPS");
         return e ? std::max(1, std::atoi(e)) : 1;
     }();
-    dim3 grid(ctx->num_sms * std::min(bps_use, blocks_per_sm)), block(SB_THREADS);
+    static const int ctas_knob = env_int("GX_SAMPLER_CTAS", 0);  // explicit CTA count (0 = per-SM rule)
+    const int ctas_max = ctx->num_sms * std::min(bps_use, blocks_per_sm);
+    dim3 grid(ctas_knob > 0 ? std::min(ctas_knob, ctas_max) : ctas_max), block(SB_THREADS);
     // cluster sampler (GX_SAMPLER_CLUSTER = 8 or 16 CTAs per batch; 0 = grid-wide kernel)
     static const int cs = [] {
         const char* e = std::getenv("GX_SAMPLER_CLUSTER");
