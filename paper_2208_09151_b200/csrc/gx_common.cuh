@@ -21,10 +21,28 @@
 
 namespace gx {
 
+// Global nanosecond timer (phase tracing: GX_SAMPLER_TRACE, GX_INSPECT_TRACE).
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
 // Tuning knob from the environment (read once per call site); def when unset.
 inline int env_int(const char* name, int def) {
     const char* e = std::getenv(name);
     return (e && *e) ? std::atoi(e) : def;
+}
+
+// Persistent grid-barrier kernels (sampler, inspector) are sized to be fully
+// co-resident (occupancy query x SMs). GX_COOP=1 launches them with
+// cudaLaunchCooperativeKernel; 0 uses an ordinary launch, which lets them share
+// SMs with the executor stream's gathers -- safe because nothing those kernels
+// wait on depends on this grid, so CTAs not yet resident are scheduled as
+// the gather CTAs retire.
+inline bool coop_launch() {
+    static const bool v = env_int("GX_COOP", 1) != 0;
+    return v;
 }
 
 

@@ -23,6 +23,7 @@
 //    (feature_cache.hpp:114-129): in[k] reuses the slot of out[k], the rest
 //    pop the free list, which (since |out| <= |in|) is always n_res, n_res+1..
 //    so the executor can apply changesets without its own free list.
+#include <cstdio>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -49,6 +50,7 @@ struct IState {
 };
 
 struct IArgs {
+    unsigned long long* tstamp;  // optional phase timestamps (GX_INSPECT_TRACE), 64 slots
     const uint32_t* __restrict__ trace;
     const uint32_t* toff;  // S+1
     uint32_t S, A, K, maxw;
@@ -96,6 +98,13 @@ struct IArgs {
     IState* st;
     GridBarrier* bar;
 };
+
+// block 0 / thread 0 records the time since kernel start into slot k (after a grid barrier)
+#define ISTAMP(a, k)                                                         \
+    do {                                                                     \
+        if ((a).tstamp && blockIdx.x == 0 && threadIdx.x == 0)               \
+            (a).tstamp[k] = gtimer() - (a).tstamp[0];                        \
+    } while (0)
 
 __device__ __forceinline__ uint32_t bucket_of(uint32_t key, uint32_t S) { return key == kNever ? S : key; }
 
@@ -156,14 +165,22 @@ __device__ __forceinline__ void stage_flush(Stage st, uint32_t* gcnt, uint32_t* 
     __syncthreads();
 }
 
+// Shared memory of k_inspect<CAP>: per-iteration arrays sized for CAP
+// iterations (the host picks the smallest CAP >= S), so a small superbatch's
+// inspector leaves room on each SM for the executor's gather CTAs.
+template <uint32_t CAP>
 struct ISmem {
+    // smem bitonic-sort limit; the buffer also holds two 2048-entry staging
+    // areas (block-staged appends: sortbuf, sortbuf + 2048)
+    static constexpr uint32_t kSort = SORT_SMALL;
+    static_assert(kSort >= 4096, "two 2048-entry Stage buffers live in sortbuf");
     uint32_t scan[34];
     uint32_t bc[16];
-    unsigned long long sortbuf[SORT_SMALL];
-    uint32_t toff[kMaxIters + 1];
-    int32_t hinc[kMaxIters + 1];  // per-CTA histogram deltas, flushed with one atomic per bin
-    int32_t hnew[kMaxIters + 1];
-    int32_t rh[2048];             // per-CTA radix-select digit histogram
+    unsigned long long sortbuf[kSort];
+    uint32_t toff[CAP + 1];
+    int32_t hinc[CAP + 1];  // per-CTA histogram deltas, flushed with one atomic per bin
+    int32_t hnew[CAP + 1];
+    int32_t rh[2048];       // per-CTA radix-select digit histogram
 };
 
 __device__ __forceinline__ void hist_flush(int32_t* loc, int32_t* glob, uint32_t n) {
@@ -178,7 +195,8 @@ __device__ __forceinline__ void hist_flush(int32_t* loc, int32_t* glob, uint32_t
     __syncthreads();
 }
 
-__device__ __forceinline__ uint32_t iter_of(const ISmem& sm, uint32_t S, uint32_t a) {
+template <class SM>
+__device__ __forceinline__ uint32_t iter_of(const SM& sm, uint32_t S, uint32_t a) {
     uint32_t lo = 0, hi = S;
     while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
@@ -190,8 +208,8 @@ __device__ __forceinline__ uint32_t iter_of(const ISmem& sm, uint32_t S, uint32_
 
 // Find the digit bin holding the r-th (1-based) smallest element of a
 // histogram; returns bin and writes the rank left inside that bin.
-__device__ uint32_t hist_select(const uint32_t* h, uint32_t nbins, uint32_t r, uint32_t* r_left,
-                                ISmem& sm) {
+template <class SM>
+__device__ uint32_t hist_select(const uint32_t* h, uint32_t nbins, uint32_t r, uint32_t* r_left, SM& sm) {
     const uint32_t per = (nbins + blockDim.x - 1) / blockDim.x;
     const uint32_t b0 = threadIdx.x * per;
     uint32_t s = 0;
@@ -225,7 +243,8 @@ __device__ uint32_t hist_select(const uint32_t* h, uint32_t nbins, uint32_t r, u
 // distinct per iteration, count_pass changeset.hpp:76-88). Small S: per-node
 // iteration bitmask (3 grid steps); large S: backward pass, one grid step per
 // iteration. Returns false if the trace is invalid (host reports the error).
-__device__ bool next_use_pass(const IArgs& a, ISmem& sm, bool firsts) {
+template <class SM>
+__device__ bool next_use_pass(const IArgs& a, SM& sm, bool firsts) {
     const uint32_t S = a.S;
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x * blockDim.x;
@@ -324,9 +343,11 @@ __device__ bool next_use_pass(const IArgs& a, ISmem& sm, bool firsts) {
     return true;
 }
 
+template <uint32_t CAP>
 __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     extern __shared__ unsigned char smem_raw[];
-    ISmem& sm = *reinterpret_cast<ISmem*>(smem_raw);
+    using SM = ISmem<CAP>;
+    SM& sm = *reinterpret_cast<SM*>(smem_raw);
     const uint32_t S = a.S, K = a.K;
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x * blockDim.x;
@@ -337,6 +358,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         sm.hnew[i] = 0;
     }
     for (uint32_t i = tid; i < 2048; i += blockDim.x) sm.rh[i] = 0;
+    if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[0] = gtimer();
     __syncthreads();
     const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
 
@@ -347,6 +369,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         // construction; first occurrences by one atomicMin pass
         for (uint32_t x = gtid; x < a.A; x += G) atomicMin(&a.last[a.trace[x]], iter_of(sm, S, x));
         grid_sync(a.bar);
+        ISTAMP(a, 1);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
@@ -363,10 +386,13 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             if (tid == 0) a.tile_cnt[t] = tot;
         }
         grid_sync(a.bar);
-        for (uint32_t x = gtid; x < a.A; x += G) a.last[a.trace[x]] = kNever;  // leave clean
+        ISTAMP(a, 2);
+        // `last` is cleaned (or, all-fit, reused as the node -> slot map) by the
+        // init pass below, which visits every first occurrence exactly once
     } else {
         if (!next_use_pass(a, sm, true)) return;
         have_next = true;
+        ISTAMP(a, 2);
     }
 
     // ---- init set: first K first-occurrences in trace order (changeset.hpp:137-153)
@@ -387,6 +413,10 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             }
         }
         grid_sync(a.bar);
+        ISTAMP(a, 3);
+        // all-fit on a trusted trace: `last` (first iteration per node) becomes the
+        // node -> slot map, so node_slot is never touched; otherwise clean `last`
+        const bool fit = a.trusted && *(volatile uint32_t*)&a.st->n_first <= K;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t fl[4], c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
@@ -401,16 +431,18 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 if (fl[j]) {
+                    const uint32_t x = x0 + j;
+                    const uint32_t v = a.trace[x];
                     if (r < K) {
-                        const uint32_t x = x0 + j;
-                        const uint32_t v = a.trace[x];
                         const uint32_t it = iter_of(sm, S, x);
                         a.slot_node[r] = v;
                         a.slot_key[r] = it;
-                        a.node_slot[v] = (int32_t)r;
+                        if (fit) a.last[v] = r;
+                        else a.node_slot[v] = (int32_t)r;
                         a.o_init[r] = v;
                         atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                     }
+                    if (a.trusted && !fit) a.last[v] = kNever;
                     ++r;
                 }
             }
@@ -424,6 +456,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                 const uint32_t x = x0 + j;
                 if (x < a.A && a.isfirst[x]) {
                     const uint32_t v = a.trace[x];
+                    if (a.trusted) a.last[v] = kNever;  // leave clean
                     const int32_t k = a.init_pos[v];
                     if (k >= 0) {
                         const uint32_t it = iter_of(sm, S, x);
@@ -444,6 +477,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         a.o_out_off[0] = 0;
     }
     grid_sync(a.bar);
+    ISTAMP(a, 4);
 
     // Every distinct node fits (init = all of them): the recurrence keeps them
     // all and never misses or evicts (keep = |cand| <= K at every iteration,
@@ -451,18 +485,25 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     // served by its init slot.
     const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
     if (allfit) {
-        for (uint32_t x = gtid; x < a.A; x += G) a.acc_slot[x] = (uint32_t)a.node_slot[a.trace[x]];
+        // node -> slot map: `last` on the trusted path (see the init pass), else node_slot
+        uint32_t* const slot_of = a.trusted ? a.last : reinterpret_cast<uint32_t*>(a.node_slot);
+        for (uint32_t x = gtid; x < a.A; x += G) a.acc_slot[x] = slot_of[a.trace[x]];
         for (uint32_t i = gtid; i < S; i += G) {
             a.o_misses[i] = 0;
             a.o_in_off[i + 1] = 0;
             a.o_out_off[i + 1] = 0;
         }
         grid_sync(a.bar);
+        ISTAMP(a, 5);
         const uint32_t n0 = a.st->n_res;
-        for (uint32_t s = gtid; s < n0; s += G) a.node_slot[a.slot_node[s]] = -1;
+        for (uint32_t s = gtid; s < n0; s += G) slot_of[a.slot_node[s]] = kNever;  // == -1: clean either map
         return;
     }
     if (!have_next) next_use_pass(a, sm, false);
+    if (a.tstamp) {  // tracing only: the recurrence needs no barrier here
+        grid_sync(a.bar);
+        ISTAMP(a, 6);
+    }
 
     // ---- the recurrence -------------------------------------------------------
     // State counters are double-buffered by iteration parity: iteration i reads
@@ -753,7 +794,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
             }
         }
         const uint32_t n_out = *(volatile uint32_t*)&cs->n_out;
-        if (n_out <= SORT_SMALL) {
+        if (n_out <= SM::kSort) {
             if (blockIdx.x == 0 && n_out > 1) {
                 uint32_t P = 1;
                 while (P < n_out) P <<= 1;
@@ -857,6 +898,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
     }
+    ISTAMP(a, 7);
     // leave node_slot clean
     const uint32_t nfin = a.st[S & 1].n_res;
     for (uint32_t s = gtid; s < nfin; s += G) a.node_slot[a.slot_node[s]] = -1;
@@ -1027,18 +1069,34 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.o_out_off = d_out_off.p;
     a.st = reinterpret_cast<IState*>(B.st.p);
     a.bar = ctx->barrier.p;
+    static const bool tracing = std::getenv("GX_INSPECT_TRACE") != nullptr;
+    static DevBuf<unsigned long long> tbuf;
+    static PinBuf<unsigned long long> htb;
+    a.tstamp = nullptr;
+    if (tracing) {
+        tbuf.reserve(64);
+        htb.reserve(64);
+        GX_CUDA(cudaMemsetAsync(tbuf.p, 0, 64 * 8, st));
+        a.tstamp = tbuf.p;
+    }
 
-    const size_t smem = sizeof(ISmem);
-    static bool attr = false;
-    if (!attr) {
-        GX_CUDA(cudaFuncSetAttribute(k_inspect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // smallest iteration capacity that holds S (shared memory scales with it)
+    const int ci = S <= 128 ? 0 : S <= 512 ? 1 : 2;
+    void* const kfns[3] = {(void*)k_inspect<128>, (void*)k_inspect<512>, (void*)k_inspect<kMaxIters>};
+    const size_t smems[3] = {sizeof(ISmem<128>), sizeof(ISmem<512>), sizeof(ISmem<kMaxIters>)};
+    static bool attr[3] = {false, false, false};
+    if (!attr[ci]) {
+        GX_CUDA(cudaFuncSetAttribute(kfns[ci], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[ci]));
         int bps = 0;
-        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_inspect, IN_THREADS, smem));
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfns[ci], IN_THREADS, smems[ci]));
         if (bps < 1) fail(GX_CUDA_ERROR, "inspector kernel cannot be resident");
-        attr = true;
+        attr[ci] = true;
     }
     void* args[] = {&a};
-    GX_CUDA(cudaLaunchCooperativeKernel((void*)k_inspect, dim3(grid), dim3(IN_THREADS), args, smem, st));
+    if (coop_launch())
+        GX_CUDA(cudaLaunchCooperativeKernel(kfns[ci], dim3(grid), dim3(IN_THREADS), args, smems[ci], st));
+    else
+        GX_CUDA(cudaLaunchKernel(kfns[ci], dim3(grid), dim3(IN_THREADS), args, smems[ci], st));
     GX_CHECK_LAUNCH();
 
     if (n_init_explicit > 0) {
@@ -1054,7 +1112,14 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     GX_CUDA(cudaMemcpyAsync(m32.data(), d_misses.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(io32.data(), d_in_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(oo32.data(), d_out_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
+    if (tracing) GX_CUDA(cudaMemcpyAsync(htb.p, tbuf.p, 64 * 8, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
+    if (tracing) {
+        std::fprintf(stderr, "[inspect trace us] A=%llu S=%llu", (unsigned long long)A, (unsigned long long)S);
+        for (int k = 1; k < 8; ++k)
+            if (htb.p[k]) std::fprintf(stderr, " s%d=%.1f", k, htb.p[k] / 1e3);
+        std::fprintf(stderr, "\n");
+    }
     if (hs.err & 3u) {
         std::vector<uint32_t> flat(A);
         GX_CUDA(cudaMemcpy(flat.data(), is.trace.p, A * 4, cudaMemcpyDeviceToHost));

@@ -89,11 +89,6 @@ struct SampArgs {
     unsigned long long* trace;  // optional phase timestamps (GX_SAMPLER_TRACE)
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
 #define TRACE_STAMP(a, l, ph)                                                  \
     do {                                                                       \
         if ((a).trace && blockIdx.x == 0 && threadIdx.x == 0)                  \
@@ -1047,7 +1042,8 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         a.edges = out->edges.p + c0 * out->cap_e_batch;
         a.layer_count = out->layer_count.p + c0 * L;
         void* args[] = {&a};
-        GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
+        if (coop_launch()) GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
+        else GX_CUDA(cudaLaunchKernel((void*)k_sample, grid, block, args, smem, st));
         GX_CHECK_LAUNCH();
         if (trace) {
             unsigned long long h[128];
