@@ -276,8 +276,11 @@ def main():
     ap.add_argument("--ref-batches", type=int, default=16,
                     help="batches per step for the reference / cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sync", action="store_true",
-                    help="no overlap: each superbatch's executor finishes before the next sampler starts")
+    ap.add_argument("--overlap", action="store_true",
+                    help="two superbatches in flight: superbatch k's executor overlaps k+1's sampler/"
+                         "inspector (slower on B200 at papers shape: the HBM-bound gather stretches the "
+                         "barrier-bound inspector, DESIGN.md §6); default runs them back to back")
+    ap.add_argument("--sync", action="store_true", help="(default) back-to-back superbatches")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.avg_degree is not None:
@@ -322,14 +325,14 @@ def main():
         return pipe.submit(sbs[j], SEED_RUN, j * cfg["S"])
 
     def run_steps(k0, n, on_stats, ev_start=None, ev_end=None):
-        """Superbatch k's executor overlaps superbatch k+1's sampler/inspector
-        (two in flight); --sync runs them back to back."""
+        """Back to back (default), or with --overlap superbatch k's executor
+        overlaps superbatch k+1's sampler/inspector (two in flight)."""
         if ev_start is not None:
             ev_start.record(stream)
         prev = None
         for k in range(k0, k0 + n):
             t = submit(k)
-            if args.sync:
+            if not args.overlap:
                 on_stats(pipe.wait(t))
                 continue
             if prev is not None:
@@ -413,6 +416,7 @@ def main():
         "reference generator; feature_value table)",
         "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * S * world,
                    "superbatch": S, "cache_entries": K_entries, "num_edges": g.num_edges(),
+                   "pipeline": "overlap (2 superbatches in flight)" if args.overlap else "serial superbatches",
                    "parallelism": f"dp{world} (superbatches per rank, no collective)",
                    "l2": "inputs larger than L2 (57 GB table, 6.6 GB CSC)" if args.config == "papers"
                    else "inputs larger than L2"},
@@ -423,7 +427,9 @@ def main():
         "roofline": {"kernel": "k_gather_tma2 (TMA bulk row gather)", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
-                     "bytes_per_row": 2 * w + 16, "rows_per_launch": rows / (n * S)},
+                     "bytes_per_row": 2 * w + 16,
+                     "rows_per_launch": rows / max(1, sum(s.gather_launches for s in stats)),
+                     "alg_bytes_per_launch": alg_bytes / max(1, sum(s.gather_launches for s in stats))},
         "stages": stages,
         "clocks": clk.summary(),
     }

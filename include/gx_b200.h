@@ -232,6 +232,7 @@ typedef struct gx_pipeline_stats {
     double ms_apply_kernels;   /* sum of the S apply-kernel durations */
     uint64_t kernel_launches;  /* this library's kernel launches for the superbatch
                                   (sampler, inspector, cache init, gathers, non-empty applies) */
+    uint64_t gather_launches;  /* gather launches: one per run of iterations with empty changesets */
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,
                              uint32_t n_layers, uint64_t num_entries, gx_pipeline** out);

@@ -41,7 +41,7 @@ class PipelineStatsC(C.Structure):
                 ("total_out", u64), ("sample_io", IoStatsC), ("gather_io", IoStatsC),
                 ("ms_sample", dbl), ("ms_inspect", dbl), ("ms_switch", dbl), ("ms_gather", dbl),
                 ("ms_gather_kernels", dbl), ("ms_apply_kernels", dbl),
-                ("kernel_launches", u64)]
+                ("kernel_launches", u64), ("gather_launches", u64)]
 
 
 PIO = C.POINTER(IoStatsC)

@@ -825,6 +825,7 @@ class PipelineStats:
     ms_gather_kernels: float
     ms_apply_kernels: float
     kernel_launches: int
+    gather_launches: int
     misses: np.ndarray
 
 
@@ -878,7 +879,7 @@ class Pipeline:
                              st.init_size, st.total_in, st.total_out, _io(st.sample_io),
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
                              st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, st.kernel_launches,
-                             misses[:S].copy())
+                             st.gather_launches, misses[:S].copy())
 
     def batch(self, i: int, ticket: Optional[int] = None) -> np.ndarray:
         """Iteration i's gathered rows of a waited-for superbatch (default: the

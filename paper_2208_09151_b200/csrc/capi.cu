@@ -620,6 +620,7 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             stats->ms_gather_kernels = gk;
             stats->ms_apply_kernels = ak;
             stats->kernel_launches = sl.launches;
+            stats->gather_launches = sl.nseg;
         }
     });
 }
