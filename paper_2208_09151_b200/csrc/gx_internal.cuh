@@ -15,6 +15,7 @@ struct SampleScratch {
     DevBuf<unsigned long long> tab[2];
     uint64_t tab_slots = 0;  // per table, = S * tab_cap
     DevBuf<unsigned long long> io;
+    DevBuf<uint32_t> tctr;  // dynamic tile counters (4 per layer), zeroed by the kernel
 };
 // Inspector scratch (inspector.cu).
 struct InspectScratch {

@@ -86,6 +86,7 @@ struct SampArgs {
     uint64_t tab_cap;  // per batch max
     unsigned long long* io;
     GridBarrier* bar;
+    uint32_t* tctr;             // dynamic tile counters, 4 per layer (zeroed at kernel start)
     unsigned long long* trace;  // optional phase timestamps (GX_SAMPLER_TRACE)
 };
 
@@ -100,6 +101,8 @@ struct SampSmem {
     unsigned long long red[34];
     uint32_t tp[kMaxBatchesPerLaunch + 1];
     uint32_t px[kMaxBatchesPerLaunch + 1];  // raw per-batch item prefix (flattened loops)
+    unsigned long long plo_s[SB_TILE];      // phase E: list offsets of the tile's parents
+    uint32_t tnext;                         // dynamically scheduled tile (broadcast)
 };
 
 // px[0..S] = prefix of per-batch item counts (seeds of batch b when
@@ -302,6 +305,9 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
     int cur = 0;
     uint32_t H = 0;
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[0] = gtimer();
+    // tile counters: first used after several grid barriers
+    if (blockIdx.x == 0)
+        for (uint32_t i = threadIdx.x; i < 4 * kMaxLayers; i += blockDim.x) a.tctr[i] = 0;
 
     for (uint32_t l = 0; l < a.L || l == 0; ++l) {
         // ---- Phase D: (re)build the per-batch tables with the current ids --
@@ -415,7 +421,13 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
         // ---- Phase E: scan takes -> draw offsets; draw, read child, insert ----
         {
             uint32_t ntiles = build_tiles(a.F, S, sm);
-            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            // tiles carry very different draw counts: hand them out dynamically
+            // (consecutive tiles -> the CTAs share a few batches' tables in L2)
+            for (;;) {
+                if (tid == 0) sm.tnext = atomicAdd(&a.tctr[4 * l], 1u);
+                __syncthreads();
+                const uint32_t t = sm.tnext;
+                if (t >= ntiles) break;
                 const uint32_t b = tile_batch(sm, S, t);
                 const uint32_t Fb = a.F[b];
                 const uint32_t first = sm.tp[b];
@@ -443,21 +455,31 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
                 uint32_t* bdslot = a.dslot + (uint64_t)b * a.cap_draw;
                 const uint32_t d_begin = off;  // this thread's first draw
+                long long c_e1 = 0;
+                if (a.trace && tid == 0) c_e1 = clock64();
                 // E1 (per parent, registers only): FY positions of every draw,
-                // staged as (position, parent) in the edge slot.
+                // staged as (position, parent) in the edge slot; the parents'
+                // list offsets go to shared memory for E2.
                 for (int j = 0; j < SB_IPT; ++j) {
                     const uint32_t tk = take[j];
                     if (tk) {
                         const uint64_t gi = (uint64_t)b * a.cap_ids + k0 + j;
+                        sm.plo_s[tid * SB_IPT + j] = a.plo[gi];
                         draw_positions(tk, seed, dbase + off, a.pdeg[gi], bedge + off, k0 + j);
                     }
                     off += tk;
                 }
                 (void)d_begin;
                 __syncthreads();  // the tile's staged draws are visible to the whole CTA
+                long long c_e2 = 0;
+                if (a.trace && tid == 0 && l < 8) {
+                    c_e2 = clock64();
+                    atomicAdd(&a.trace[100 + 2 * l], (unsigned long long)(c_e2 - c_e1));
+                }
                 // E2 (per draw): child read, edge, dedup insert -- one draw per
                 // thread so the random reads and atomics of a tile overlap.
                 const uint32_t tile_d0 = toff, tile_d1 = toff + tot;
+                const uint32_t tile_k0 = (t - first) * SB_TILE;  // the tile's first parent
                 constexpr int U = GX_E_UNROLL;  // draws per thread in flight
                 for (uint32_t q0 = tile_d0 + tid; q0 < tile_d1; q0 += U * blockDim.x) {
                     uint2 st[U];
@@ -470,10 +492,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
                         const uint32_t p = q0 + j * blockDim.x;
-                        if (p < tile_d1) {
-                            const uint64_t lo = a.plo[(uint64_t)b * a.cap_ids + st[j].y];
-                            child[j] = __ldg(a.indices + lo + st[j].x);
-                        }
+                        if (p < tile_d1) child[j] = __ldg(a.indices + sm.plo_s[st[j].y - tile_k0] + st[j].x);
                     }
                     // first probes of all U draws back to back, then resolve
                     uint32_t slot[U];
@@ -532,6 +551,8 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                     }
                 }
                 __syncthreads();
+                if (a.trace && tid == 0 && l < 8)
+                    atomicAdd(&a.trace[101 + 2 * l], (unsigned long long)(clock64() - c_e2));
             }
         }
         grid_sync(a.bar);
@@ -930,6 +951,7 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         ss.tab_slots = CH * tab_cap;
     }
     ss.io.reserve(4);
+    ss.tctr.reserve(4 * kMaxLayers);
     GX_CUDA(cudaMemsetAsync(ss.io.p, 0, 4 * sizeof(unsigned long long), st));
 
     // host -> device: seeds (u32), offsets, batch seeds
@@ -967,6 +989,7 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     a.tab1 = ss.tab[1].p;
     a.tab_cap = tab_cap;
     a.io = ss.io.p;
+    a.tctr = ss.tctr.p;
     a.bar = ctx->barrier.p;
     static const bool trace = std::getenv("GX_SAMPLER_TRACE") != nullptr;
     static DevBuf<unsigned long long> tbuf;
@@ -1060,6 +1083,11 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
                     prev = t;
                 }
             line += " end=" + std::to_string((h[127] - prev) / 1000.0).substr(0, 6);
+            // E1/E2 split: cycles summed over CTAs / CTAs / SM clock (~1.9 GHz) = us per CTA
+            for (uint32_t l = 0; l < std::min<uint32_t>(L, 8); ++l)
+                line += " L" + std::to_string(l) + "E1/E2(us/CTA)=" +
+                        std::to_string(h[100 + 2 * l] / (double)grid.x / 1965.0).substr(0, 6) + "/" +
+                        std::to_string(h[101 + 2 * l] / (double)grid.x / 1965.0).substr(0, 6);
             fprintf(stderr, "%s\n", line.c_str());
         }
     }

@@ -22,7 +22,9 @@ def main():
     ap.add_argument("--config", default="papers", choices=sorted(bench.CONFIGS))
     ap.add_argument("--superbatches", default="1,10,50,100,250,500")
     ap.add_argument("--cache", default="5,10,20,35,50")
-    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2,
+                    help="untimed superbatches per point (>= 2: the pipeline alternates two buffer slots)")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import paper_2208_09151_b200 as gx
@@ -37,10 +39,10 @@ def main():
         pipe = gx.Pipeline(g, f, cfg["fanouts"], K)
         for S in [int(x) for x in args.superbatches.split(",")]:
             sts = []
-            for k in range(1 + args.steps):
+            for k in range(args.warmup + args.steps):
                 o = (k * S) % max(len(plan) - S, 1)
                 st = pipe.run_superbatch(plan[o:o + S], bench.SEED_RUN, o)
-                if k:
+                if k >= args.warmup:
                     sts.append(st)
             ms = sum(s.ms_sample + s.ms_inspect + s.ms_switch + s.ms_gather for s in sts) / len(sts)
             edges = sum(s.sampled_edges for s in sts) / len(sts)
