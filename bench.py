@@ -78,32 +78,62 @@ def measured_peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+    """SM clock + throttle-reason sampling during the timed region
+    (B200_PROFILING.md recipe). NVML every 5 ms (the timed region of a few
+    superbatches lasts tens of ms); nvidia-smi polling when NVML is absent."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason* (HwSlowdown, HwThermal, SwThermal, SwPowerCap)
 
     def __init__(self, device):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, [4 bools])
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            idx = int(vis.split(",")[device]) if vis and vis.split(",")[0].isdigit() else device
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self._nvml = pynvml
+        except Exception:
+            self._nvml = None
+
+    def _sample_nvml(self):
+        n = self._nvml
+        sm = n.nvmlDeviceGetClockInfo(self._h, n.NVML_CLOCK_SM)
+        mx = n.nvmlDeviceGetMaxClockInfo(self._h, n.NVML_CLOCK_SM)
+        try:
+            r = n.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            r = n.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        return (float(sm), float(mx), [bool(r & b) for b in self.BITS])
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        v = [x.strip() for x in out.split(",")]
+        num = lambda x: float(x) if x.replace(".", "").isdigit() else None  # noqa: E731
+        return (num(v[0]), num(v[1]), [x.lower() == "active" for x in v[2:6]])
 
     def _run(self):
-        while not self._stop.is_set():
+        period = 0.005 if self._nvml else 0.2
+        while True:
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                self.samples.append(self._sample_nvml() if self._nvml else self._sample_smi())
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            if self._stop.wait(period):
+                break
 
     def __enter__(self):
-        if shutil.which("nvidia-smi"):
+        if self._nvml or shutil.which("nvidia-smi"):
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -116,16 +146,15 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
-                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        sm = [x[0] for x in self.samples if x[0] is not None]
+        mx = [x[1] for x in self.samples if x[1] is not None]
+        reasons = sorted({self.NAMES[k] for x in self.samples for k in range(4) if x[2][k]})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "source": "nvml 5 ms" if self._nvml else "nvidia-smi"}
 
 
-def build_dataset(gx, cfg, ctx, log):
+def build_dataset(gx, cfg, ctx, log, backing="device", ssd_dir=None):
     edge_seed = gx.derive_seed(SEED_GEN, 0xED6E5)
     value_seed = gx.derive_seed(SEED_GEN, 0xFEA7)
     t0 = time.time()
@@ -135,6 +164,15 @@ def build_dataset(gx, cfg, ctx, log):
     ctx.synchronize()
     t2 = time.time()
     log(f"dataset: N={g.num_nodes()} E={g.num_edges()} (graph {t1 - t0:.1f}s, features {t2 - t1:.1f}s)")
+    if backing == "file":
+        # the SSD tier: features.bin on storage, the table leaves HBM
+        path = os.path.join(ssd_dir, f"gx_bench_features_{os.getpid()}.bin")
+        f.write(path)
+        del f
+        f = gx.FeatureFile.open(path, "file", ctx=ctx)
+        os.unlink(path)  # the open descriptor keeps the inode readable
+        log(f"features.bin written to {ssd_dir} ({time.time() - t2:.1f}s), "
+            f"O_DIRECT={f.storage_stats().direct}")
     return g, f
 
 
@@ -281,6 +319,10 @@ def main():
                          "inspector (slower on B200 at papers shape: the HBM-bound gather stretches the "
                          "barrier-bound inspector, DESIGN.md §6); default runs them back to back")
     ap.add_argument("--sync", action="store_true", help="(default) back-to-back superbatches")
+    ap.add_argument("--backing", default="device", choices=["device", "file"],
+                    help="feature backing store: HBM-resident table (default) or the SSD tier "
+                         "(features.bin on storage, misses read with O_DIRECT into pinned staging)")
+    ap.add_argument("--ssd-dir", default=os.environ.get("GX_SSD_DIR", "/tmp"))
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.avg_degree is not None:
@@ -303,7 +345,7 @@ def main():
         dist.init_process_group("nccl")
     import paper_2208_09151_b200 as gx
     ctx = gx.Context(local)
-    g, f = build_dataset(gx, cfg, ctx, log)
+    g, f = build_dataset(gx, cfg, ctx, log, args.backing, args.ssd_dir)
     sbs = make_plan(gx, cfg)
     K_entries = int(cfg["cache_frac"] * cfg["N"])
     pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries)
@@ -379,7 +421,7 @@ def main():
         assert s.total_misses == s.predicted_misses, "observed misses != inspector prediction"
 
     # --- roofline of the dominant kernel (the gather) -------------------------
-    w = 4 * cfg["dim"]
+    w = f.row_bytes()
     rows = sum(s.gathered_rows for s in stats)
     gk_ms = sum(s.ms_gather_kernels for s in stats)
     alg_bytes = (2 * w + 16) * rows               # read row + write row + id + slot
@@ -408,6 +450,19 @@ def main():
         "changeset_in_per_iter": sum(s.total_in for s in stats) / (n * S),
         "edges_per_superbatch": edges / n,
     }
+    if args.backing == "file":
+        sm = sum(s.ms_storage for s in stats)
+        sb = sum(s.storage_bytes for s in stats)
+        srows = sum(s.storage_rows for s in stats)
+        fs = f.storage_stats()
+        stages.update({
+            "storage_ms": sm / n, "storage_rows_per_superbatch": srows / n,
+            "storage_bytes_per_superbatch": sb / n,
+            "storage_GBps": sb / (sm / 1e3) / 1e9 if sm else None,
+            "storage_row_GBps": srows * w / (sm / 1e3) / 1e9 if sm else None,
+            "storage_preads_per_s": fs.preads / (fs.read_ms / 1e3) if fs.read_ms else None,
+            "storage_direct": fs.direct, "storage_threads": fs.threads,
+            "storage_dir": args.ssd_dir})
     out = {
         "metric": METRIC, "value": edges_all / dev_s, "unit": "sampled_edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
@@ -417,6 +472,7 @@ def main():
         "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * S * world,
                    "superbatch": S, "cache_entries": K_entries, "num_edges": g.num_edges(),
                    "pipeline": "overlap (2 superbatches in flight)" if args.overlap else "serial superbatches",
+                   "backing": args.backing,
                    "parallelism": f"dp{world} (superbatches per rank, no collective)",
                    "l2": "inputs larger than L2 (57 GB table, 6.6 GB CSC)" if args.config == "papers"
                    else "inputs larger than L2"},

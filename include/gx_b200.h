@@ -164,10 +164,33 @@ gx_status gx_changesets_write_files(const gx_changesets* cs, const char* dir, ui
 typedef struct gx_features gx_features;
 typedef enum gx_backing {
     GX_BACKING_DEVICE = 0, /* whole table in HBM (fits one B200 up to ~150 GB) */
-    GX_BACKING_HOST = 1    /* pinned host memory, misses read over PCIe by the gather kernel */
+    GX_BACKING_HOST = 1,   /* pinned host memory, misses read over PCIe by the gather kernel */
+    GX_BACKING_FILE = 2    /* the 'SSD' tier: features.bin stays on storage; the rows a
+                              superbatch misses (cache init + changeset misses) are read with
+                              pread (O_DIRECT when the filesystem allows it, whole 4 KB pages)
+                              by a host thread pool into pinned staging and copied to HBM on a
+                              side stream (FeatureFile::read_row, graph_store.hpp:308-315) */
 } gx_backing;
-/* FeatureFile::open (graph_store.hpp:282-302) + load of the payload. */
+/* FeatureFile::open (graph_store.hpp:282-302) + load of the payload (DEVICE,
+ * HOST) or an open descriptor only (FILE). With GX_BACKING_FILE, ctx may be
+ * NULL: the handle then serves gx_features_read_rows from the host only. */
 gx_status gx_features_open(gx_ctx* ctx, const char* path, int backing, gx_features** out);
+/* FeatureWriter (graph_store.hpp:237-250): writes features.bin (36-byte header,
+ * payload at 4096) from a DEVICE or HOST backed table. */
+gx_status gx_features_write(const gx_features* f, const char* path);
+/* Storage-tier counters of a GX_BACKING_FILE table since open (physical reads;
+ * the reference's page accounting stays in gx_iostats). direct = 1 when reads
+ * bypass the page cache (O_DIRECT). */
+typedef struct gx_storage_stats {
+    uint64_t rows;        /* rows delivered */
+    uint64_t preads;      /* pread calls (one per coalesced page run) */
+    uint64_t bytes;       /* bytes read from storage (whole pages) */
+    uint64_t h2d_bytes;   /* bytes copied pinned -> HBM */
+    double read_ms;       /* wall time of the host read phase (all workers) */
+    uint32_t threads;     /* reader threads */
+    int32_t direct;       /* 1 = O_DIRECT, 0 = buffered fallback */
+} gx_storage_stats;
+gx_status gx_features_storage_stats(const gx_features* f, gx_storage_stats* out);
 /* from host rows (RowMatrix layout, graph_store.hpp:222-234); row_bytes =
  * dim * scalar_width (scalar_width 4 = the reference format; 2 = fp16 ext.) */
 gx_status gx_features_from_host(gx_ctx* ctx, uint64_t num_nodes, uint32_t dim,
@@ -233,6 +256,10 @@ typedef struct gx_pipeline_stats {
     uint64_t kernel_launches;  /* this library's kernel launches for the superbatch
                                   (sampler, inspector, cache init, gathers, non-empty applies) */
     uint64_t gather_launches;  /* gather launches: one per run of iterations with empty changesets */
+    /* GX_BACKING_FILE only (zero otherwise): the superbatch's storage reads */
+    double ms_storage;         /* wall time of the host read phase (pread + staging) */
+    uint64_t storage_rows;     /* rows read: cache init + changeset misses */
+    uint64_t storage_bytes;    /* bytes read from storage (whole pages) */
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,
                              uint32_t n_layers, uint64_t num_entries, gx_pipeline** out);

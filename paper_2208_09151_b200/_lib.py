@@ -41,7 +41,13 @@ class PipelineStatsC(C.Structure):
                 ("total_out", u64), ("sample_io", IoStatsC), ("gather_io", IoStatsC),
                 ("ms_sample", dbl), ("ms_inspect", dbl), ("ms_switch", dbl), ("ms_gather", dbl),
                 ("ms_gather_kernels", dbl), ("ms_apply_kernels", dbl),
-                ("kernel_launches", u64), ("gather_launches", u64)]
+                ("kernel_launches", u64), ("gather_launches", u64),
+                ("ms_storage", dbl), ("storage_rows", u64), ("storage_bytes", u64)]
+
+
+class StorageStatsC(C.Structure):
+    _fields_ = [("rows", u64), ("preads", u64), ("bytes", u64), ("h2d_bytes", u64), ("read_ms", dbl),
+                ("threads", u32), ("direct", i32)]
 
 
 PIO = C.POINTER(IoStatsC)
@@ -93,6 +99,8 @@ SIGNATURES = {
     "gx_changesets_misses": (i32, [vp, vp]),
     "gx_changesets_write_files": (i32, [vp, cstr, u64]),
     "gx_features_open": (i32, [vp, cstr, i32, PVP]),
+    "gx_features_write": (i32, [vp, cstr]),
+    "gx_features_storage_stats": (i32, [vp, vp]),
     "gx_features_from_host": (i32, [vp, u64, u32, u32, vp, i32, PVP]),
     "gx_features_generate": (i32, [vp, u64, u32, u64, PVP]),
     "gx_features_destroy": (None, [vp]),

@@ -18,7 +18,7 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (IoStatsC, LogicError, PipelineStatsC, CudaError, check, lib)  # noqa: F401
+from ._lib import (IoStatsC, LogicError, PipelineStatsC, StorageStatsC, CudaError, check, lib)  # noqa: F401
 
 # ---------------------------------------------------------------------------
 # primitives (common.hpp)
@@ -632,14 +632,30 @@ def precompute_changesets(trace: FileTrace, num_nodes: int, num_entries: int, ou
 # ---------------------------------------------------------------------------
 # executor (feature_cache.hpp) and the feature table (graph_store.hpp:217-333)
 # ---------------------------------------------------------------------------
-BACKING = {"device": 0, "host": 1}
+BACKING = {"device": 0, "host": 1, "file": 2}
+
+
+@dataclasses.dataclass
+class StorageStats:
+    """gx_storage_stats: physical reads of a file-backed table since open."""
+    rows: int
+    preads: int
+    bytes: int
+    h2d_bytes: int
+    read_ms: float
+    threads: int
+    direct: bool
 
 
 class FeatureFile:
-    """FeatureFile (graph_store.hpp:280-333): the table lives in HBM ("device")
-    or in pinned host memory ("host", misses read over PCIe by the kernel)."""
+    """FeatureFile (graph_store.hpp:280-333): the table lives in HBM ("device"),
+    in pinned host memory ("host", misses read over PCIe by the kernel) or stays
+    in features.bin ("file": the SSD tier -- missed rows are read with pread,
+    O_DIRECT where the filesystem allows it, into pinned staging and copied to
+    HBM on a side stream). A file-backed table opened with ctx=None serves
+    read_rows from the host alone."""
 
-    def __init__(self, handle, ctx: Context, dtype=np.float32):
+    def __init__(self, handle, ctx: Optional[Context], dtype=np.float32):
         self.h = handle
         self.ctx = ctx
         self.dtype = dtype
@@ -651,9 +667,10 @@ class FeatureFile:
 
     @staticmethod
     def open(path: str, backing: str = "device", ctx: Optional[Context] = None) -> "FeatureFile":
-        c = _ctx(ctx)
+        c = ctx if (ctx is not None or backing == "file") else _ctx(ctx)
         h = C.c_void_p()
-        check(lib.gx_features_open(c.h, os.fspath(path).encode(), BACKING[backing], C.byref(h)))
+        check(lib.gx_features_open(c.h if c is not None else None, os.fspath(path).encode(),
+                                   BACKING[backing], C.byref(h)))
         f = FeatureFile(h, c)
         if f.row_bytes() == 2 * f.dim():
             f.dtype = np.float16
@@ -688,6 +705,16 @@ class FeatureFile:
 
     def row_bytes(self) -> int:
         return lib.gx_features_row_bytes(self.h)
+
+    def write(self, path: str) -> None:
+        """FeatureWriter (graph_store.hpp:237-250): features.bin of this table."""
+        check(lib.gx_features_write(self.h, os.fspath(path).encode()))
+
+    def storage_stats(self) -> StorageStats:
+        st = StorageStatsC()
+        check(lib.gx_features_storage_stats(self.h, C.byref(st)))
+        return StorageStats(st.rows, st.preads, st.bytes, st.h2d_bytes, st.read_ms, st.threads,
+                            bool(st.direct))
 
     def read_rows(self, ids, stats: Optional[IoStats] = None) -> np.ndarray:
         """FeatureFile::read_rows (graph_store.hpp:319-324)."""
@@ -827,6 +854,9 @@ class PipelineStats:
     kernel_launches: int
     gather_launches: int
     misses: np.ndarray
+    ms_storage: float = 0.0      # file-backed tables: host read phase of the superbatch
+    storage_rows: int = 0
+    storage_bytes: int = 0
 
 
 def _io(c: IoStatsC) -> IoStats:
@@ -879,7 +909,8 @@ class Pipeline:
                              st.init_size, st.total_in, st.total_out, _io(st.sample_io),
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
                              st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, st.kernel_launches,
-                             st.gather_launches, misses[:S].copy())
+                             st.gather_launches, misses[:S].copy(), st.ms_storage, st.storage_rows,
+                             st.storage_bytes)
 
     def batch(self, i: int, ticket: Optional[int] = None) -> np.ndarray:
         """Iteration i's gathered rows of a waited-for superbatch (default: the

@@ -83,6 +83,11 @@ struct PipeSlot {
     uint64_t sampled_edges = 0;
     uint64_t launches = 0;  // this library's kernels launched for the superbatch
     gx_iostats sample_io{};
+    // GX_BACKING_FILE: miss ids (access order) and their staged rows
+    gx::DevBuf<uint32_t> miss_ids;
+    gx::DevBuf<uint8_t> stage;
+    double ms_storage = 0;
+    uint64_t storage_rows = 0, storage_bytes = 0;
     cudaEvent_t ev[6] = {};  // A: start, sampled, inspected; B: exec start, switched, done
     std::vector<cudaEvent_t> kev;
 };
@@ -394,6 +399,7 @@ gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanout
     return guard([&] {
         if (!g || !f) fail(GX_INVALID_ARGUMENT, "null handle");
         if (f->n != g->n) fail(GX_INVALID_ARGUMENT, "graph and feature files disagree on node count");
+        if (!f->ctx) fail(GX_INVALID_ARGUMENT, "feature table was opened without a context");
         if (K >= 0x7FFFFFFFull) fail(GX_INVALID_ARGUMENT, "cache capacity exceeds 2^31 - 1 slots");
         auto p = new gx_pipeline();
         try {
@@ -483,6 +489,9 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         }
         std::swap(ctx->is.trace, sl.trace);
         std::swap(ctx->is.acc_slot, sl.acc_slot);
+        // storage tier: the accesses the cache will miss read staged rows
+        const bool file = p->f->backing == GX_BACKING_FILE;
+        const uint64_t n_miss = file ? stage_misses(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.miss_ids, A) : 0;
         GX_CUDA(cudaEventRecord(sl.ev[2], A));
         // (3)+(4) executor on stream B, after the inspector and the previous executor
         GX_CUDA(cudaStreamWaitEvent(B, sl.ev[2], 0));
@@ -515,9 +524,25 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         try {
             // (3) switch: the init rows into slots 0..n_init-1 (the inspector
             // resolved every access's serving slot, so no address table here)
-            launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
-                              sl.counters.p + 8 * S);
-            GX_CUDA(cudaEventRecord(sl.ev[4], B));
+            const uint8_t* store = p->f->rows_dev_view;
+            sl.ms_storage = 0;
+            sl.storage_rows = sl.storage_bytes = 0;
+            if (file) {
+                // the init rows land in their slots, the misses in this slot's
+                // staging rows, both read from storage while B drains
+                const uint64_t r0 = p->f->file->rows.load(), b0 = p->f->file->bytes.load();
+                sl.ms_storage += stage_fetch(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B);
+                GX_CUDA(cudaEventRecord(sl.ev[4], B));
+                sl.stage.reserve(std::max<uint64_t>(n_miss * rb, 16));
+                sl.ms_storage += stage_fetch(p->f, sl.miss_ids.p, n_miss, sl.stage.p, B);
+                store = sl.stage.p;
+                sl.storage_rows = p->f->file->rows.load() - r0;
+                sl.storage_bytes = p->f->file->bytes.load() - b0;
+            } else {
+                launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
+                                  sl.counters.p + 8 * S);
+                GX_CUDA(cudaEventRecord(sl.ev[4], B));
+            }
             // (4) main loop. Iterations whose changesets are empty do not mutate
             // the cache, so with the whole superbatch resident a run of them is
             // gathered by one launch (segment), then the last one's changeset applied.
@@ -532,8 +557,8 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                     while (e + 1 < S && empty_cs(e)) ++e;
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg], B));
                 launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], sl.o[e + 1] - sl.o[i],
-                                       p->cache_rows.p, p->f, rows_of(i), sl.counters.p + 8 * i, sl.d_off.p + i,
-                                       (uint32_t)(e - i + 1));
+                                       p->cache_rows.p, store, rb, rows_of(i), sl.counters.p + 8 * i,
+                                       sl.d_off.p + i, (uint32_t)(e - i + 1));
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg + 1], B));
                 if (p->digest)
                     for (uint64_t k = i; k <= e; ++k)
@@ -621,6 +646,9 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             stats->ms_apply_kernels = ak;
             stats->kernel_launches = sl.launches;
             stats->gather_launches = sl.nseg;
+            stats->ms_storage = sl.ms_storage;
+            stats->storage_rows = sl.storage_rows;
+            stats->storage_bytes = sl.storage_bytes;
         }
     });
 }

@@ -60,7 +60,8 @@ __device__ __forceinline__ void st_na(uint4* p, const uint4& v) {
 __device__ __forceinline__ void st_na(uint32_t* p, const uint32_t& v) { *p = v; }
 
 // Row gather with pre-resolved sources: row k of `out` = cache slot slots[k]
-// or, when slots[k] == kNever (a miss), row ids[k] of the backing store.
+// or, for a miss, row ids[k] of the backing store (slots[k] == kNever) or row
+// slots[k] & ~kStageFlag of the staged rows the storage tier delivered.
 // A warp moves R rows per step: lanes 0..R-1 fetch the rows' metadata
 // (coalesced), the row base pointers are broadcast by shuffles and every lane
 // issues R independent 16-byte loads before the R stores, so R x row_bytes per
@@ -115,11 +116,11 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_gather_rows
         if (lane < nr) {
             const uint32_t v = __ldg(ids + r0 + lane);
             const uint32_t s = slots ? __ldg(slots + r0 + lane) : kNever;
-            if (s != kNever) {
+            if (s < kStageFlag) {
                 src = cache_rows + (uint64_t)s * row_bytes;
                 if (!sg.off) ++hits;
-            } else {
-                src = store + (uint64_t)v * row_bytes;
+            } else {  // miss: backing row v, or staged row (s & ~kStageFlag)
+                src = store + (uint64_t)(s == kNever ? v : (s & ~kStageFlag)) * row_bytes;
                 const uint32_t pg =
                     (uint32_t)pages_touched((uint64_t)v * row_bytes, (uint64_t)v * row_bytes + row_bytes);
                 if (sg.off) {
@@ -163,7 +164,7 @@ __device__ __forceinline__ const uint8_t* gather_src(const uint32_t* ids, const 
                                                      uint32_t& pages, const SegInfo& sg) {
     const uint32_t v = __ldg(ids + r);
     const uint32_t s = slots ? __ldg(slots + r) : kNever;
-    if (s != kNever) {
+    if (s < kStageFlag) {
         if (!sg.off) ++hits;
         return cache_rows + (uint64_t)s * row_bytes;
     }
@@ -174,7 +175,7 @@ __device__ __forceinline__ const uint8_t* gather_src(const uint32_t* ids, const 
         ++misses;
         pages += pg;
     }
-    return store + (uint64_t)v * row_bytes;
+    return store + (uint64_t)(s == kNever ? v : (s & ~kStageFlag)) * row_bytes;
 }
 
 // TMA variant of the row gather: every thread moves whole rows with the bulk
@@ -491,7 +492,7 @@ void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t ro
 // Launchers shared with the pipeline.
 template <int VEC, int R>
 static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
-                               const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                               const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
                                unsigned long long* counters, SegInfo sg = {nullptr, 0, nullptr}) {
     static int bps = 0;
     if (!bps) {
@@ -502,12 +503,12 @@ static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t*
     const uint64_t blocks_needed = (warps_needed * 32 + GA_THREADS - 1) / GA_THREADS;
     const uint64_t blocks = std::min<uint64_t>(blocks_needed, (uint64_t)ctx->num_sms * bps);
     k_gather_rows<VEC, R><<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(
-        ids, slots, (uint32_t)n, cache_rows, f->rows_dev_view, (uint32_t)f->row_bytes, out, counters, sg);
+        ids, slots, (uint32_t)n, cache_rows, store, (uint32_t)rb, out, counters, sg);
     GX_CHECK_LAUNCH();
 }
 
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
-                            const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                            const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
                             unsigned long long* counters, const uint32_t* seg_off, uint32_t nseg) {
     if (!n) return;
     const SegInfo sg{seg_off, seg_off ? nseg : 0u, counters};
@@ -524,7 +525,6 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         const int kb = e ? std::atoi(e) : 96;
         return std::min(std::max(kb, 16), 200) * 1024;
     }();
-    const uint64_t rb = f->row_bytes;
     static const int ring = env_int("GX_GATHER_D", 0);  // 3/4/6: k_gather_ring<D> (experimental)
     if (vec16(rb) && R == 1 && (ring == 3 || ring == 4 || ring == 6) && (uint64_t)ring * 32 * rb <= (uint64_t)budget) {
         static int tpb = 0, bpsm = 0;
@@ -542,7 +542,7 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         const uint64_t cap = ctas_knob > 0 ? (uint64_t)ctas_knob : (uint64_t)ctx->num_sms * bpsm;
         const uint64_t blocks = std::min<uint64_t>((n + tpb - 1) / tpb, cap);
         kfn<<<(unsigned)blocks, tpb, (size_t)tpb * ring * rb, lstream(ctx)>>>(ids, slots, (uint32_t)n, cache_rows,
-                                                                            f->rows_dev_view, (uint32_t)rb, out,
+                                                                            store, (uint32_t)rb, out,
                                                                             counters, sg);
         GX_CHECK_LAUNCH();
         return;
@@ -566,25 +566,32 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         const uint64_t blocks = std::min<uint64_t>((n + tpb[d] - 1) / tpb[d], cap);
         auto kfn = depth == 2 ? k_gather_tma2 : k_gather_tma;
         kfn<<<(unsigned)blocks, tpb[d], (size_t)tpb[d] * depth * rb, lstream(ctx)>>>(
-            ids, slots, (uint32_t)n, cache_rows, f->rows_dev_view, (uint32_t)rb, out, counters, sg);
+            ids, slots, (uint32_t)n, cache_rows, store, (uint32_t)rb, out, counters, sg);
         GX_CHECK_LAUNCH();
     } else if (vec16(rb)) {
-        if (R == 2) gather_rows_launch<16, 2>(ctx, ids, slots, n, cache_rows, f, out, counters, sg);
-        else if (R == 8) gather_rows_launch<16, 8>(ctx, ids, slots, n, cache_rows, f, out, counters, sg);
-        else gather_rows_launch<16, 4>(ctx, ids, slots, n, cache_rows, f, out, counters, sg);
+        if (R == 2) gather_rows_launch<16, 2>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
+        else if (R == 8) gather_rows_launch<16, 8>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
+        else gather_rows_launch<16, 4>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
     } else {
-        gather_rows_launch<4, 4>(ctx, ids, slots, n, cache_rows, f, out, counters, sg);
+        gather_rows_launch<4, 4>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
     }
 }
 
 void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table, const uint8_t* cache_rows,
-                   const gx_features* f, uint8_t* out, unsigned long long* counters) {
+                   gx_features* f, uint8_t* out, unsigned long long* counters) {
     if (!n) return;
     DevBuf<uint32_t>& slots = ctx->resolve_slots;  // API path only
     slots.reserve(n);
     k_resolve<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(ids, n, table, slots.p);
     GX_CHECK_LAUNCH();
-    launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, f, out, counters);
+    const uint8_t* store = f->rows_dev_view;
+    if (f->backing == GX_BACKING_FILE) {  // misses come from the storage tier
+        const uint64_t m = stage_misses(ctx, ids, slots.p, n, ctx->stage_ids, lstream(ctx));
+        ctx->stage_rows.reserve(std::max<uint64_t>(m * f->row_bytes, 16));
+        if (m) stage_fetch(f, ctx->stage_ids.p, m, ctx->stage_rows.p, lstream(ctx));
+        store = ctx->stage_rows.p;
+    }
+    launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, store, f->row_bytes, out, counters);
 }
 
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos, const uint32_t* in_slot,
@@ -610,13 +617,20 @@ __global__ void k_set_table(const uint32_t* __restrict__ init, uint32_t n, int32
         table[init[k]] = (int32_t)k;
 }
 
-void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table, const gx_features* f,
+void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table, gx_features* f,
                        uint8_t* cache_rows, unsigned long long* counters) {
     if (!n) return;
-    // one large all-miss gather: the 8-rows-per-warp LDG/STG kernel measured
-    // faster than the bulk-copy kernel here (1.05 vs 1.35 ms, 6.2M x 512 B rows)
-    if (vec16(f->row_bytes)) gather_rows_launch<16, 8>(ctx, init, nullptr, n, nullptr, f, cache_rows, counters);
-    else launch_gather_resolved(ctx, init, nullptr, n, nullptr, f, cache_rows, counters);
+    if (f->backing == GX_BACKING_FILE) {
+        // the storage tier writes the init rows straight into their slots
+        stage_fetch(f, init, n, cache_rows, lstream(ctx));
+    } else if (vec16(f->row_bytes)) {
+        // one large all-miss gather: the 8-rows-per-warp LDG/STG kernel measured
+        // faster than the bulk-copy kernel here (1.05 vs 1.35 ms, 6.2M x 512 B rows)
+        gather_rows_launch<16, 8>(ctx, init, nullptr, n, nullptr, f->rows_dev_view, f->row_bytes, cache_rows,
+                                  counters);
+    } else {
+        launch_gather_resolved(ctx, init, nullptr, n, nullptr, f->rows_dev_view, f->row_bytes, cache_rows, counters);
+    }
     if (table) {
         k_set_table<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(init, n, table);
         GX_CHECK_LAUNCH();
@@ -691,6 +705,7 @@ gx_status gx_cache_create(gx_features* f, const uint64_t* init, uint64_t n_init,
                 fail(GX_INVALID_ARGUMENT, "duplicate init id");
         }
         if (K >= 0x7FFFFFFFull) fail(GX_INVALID_ARGUMENT, "cache capacity exceeds 2^31 - 1 slots");
+        if (!f->ctx) fail(GX_INVALID_ARGUMENT, "feature table was opened without a context");
         gx_ctx* ctx = f->ctx;
         auto c = new gx_cache();
         try {
@@ -714,6 +729,11 @@ gx_status gx_cache_create(gx_features* f, const uint64_t* init, uint64_t n_init,
             unsigned long long pg = 0;
             GX_CUDA(cudaMemcpyAsync(&pg, c->counters.p + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
             GX_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (f->backing == GX_BACKING_FILE) {  // the storage tier does not run the gather's counters
+                pg = 0;
+                for (uint64_t k = 0; k < n_init; ++k)
+                    pg += pages_touched(init[k] * f->row_bytes, init[k] * f->row_bytes + f->row_bytes);
+            }
             if (io) {
                 io->rows_read += n_init;
                 io->pages_read += pg;
@@ -856,6 +876,16 @@ gx_status gx_features_read_rows(gx_features* f, const uint64_t* ids, uint64_t n,
         gx_ctx* ctx = f->ctx;
         for (uint64_t k = 0; k < n; ++k)
             if (ids[k] >= f->n) fail(GX_OUT_OF_RANGE, "feature row id out of range");
+        if (f->backing == GX_BACKING_FILE) {  // straight from storage into the caller's buffer
+            f->file->read_rows(ids, n, (uint8_t*)out);
+            if (io) {
+                for (uint64_t k = 0; k < n; ++k)
+                    io->pages_read += pages_touched(ids[k] * f->row_bytes, ids[k] * f->row_bytes + f->row_bytes);
+                io->rows_read += n;
+                io->bytes_read += n * f->row_bytes;
+            }
+            return;
+        }
         DevBuf<uint32_t> d(std::max<uint64_t>(n, 1));
         upload_u32(ctx, d, 0, ids, n);
         DevBuf<uint8_t> o(std::max<uint64_t>(n * f->row_bytes, 16));

@@ -443,6 +443,14 @@ gx_status gx_features_open(gx_ctx* ctx, const char* path, int backing, gx_featur
             ft->row_bytes = (uint64_t)ft->dim * ft->scalar_width;
             if (fsz < poff + ft->n * ft->row_bytes)
                 fail(GX_RUNTIME_ERROR, std::string("truncated feature file: ") + path);
+            if (backing == GX_BACKING_FILE) {  // the storage tier: rows stay in the file
+                check_nodes_u32(ft->n);
+                ft->backing = GX_BACKING_FILE;
+                ft->file.reset(new RowReader(path, poff, ft->row_bytes, ft->n));
+                *out = ft;
+                return;
+            }
+            if (!ctx) fail(GX_INVALID_ARGUMENT, "a device or host backed table needs a context");
             features_alloc(ft, backing);
             const uint64_t bytes = ft->n * ft->row_bytes;
             if (backing == GX_BACKING_HOST) {
@@ -468,6 +476,8 @@ gx_status gx_features_open(gx_ctx* ctx, const char* path, int backing, gx_featur
 gx_status gx_features_from_host(gx_ctx* ctx, uint64_t n, uint32_t dim, uint32_t sw, const void* rows,
                                 int backing, gx_features** out) {
     return guard([&] {
+        if (backing == GX_BACKING_FILE)
+            fail(GX_INVALID_ARGUMENT, "GX_BACKING_FILE tables are opened from features.bin (gx_features_open)");
         if (sw != 4 && sw != 2) fail(GX_INVALID_ARGUMENT, "scalar_width must be 4 or 2");
         if (dim < 1) fail(GX_INVALID_ARGUMENT, "dim must be >= 1");
         check_nodes_u32(n);
@@ -512,6 +522,39 @@ gx_status gx_features_generate(gx_ctx* ctx, uint64_t n, uint32_t dim, uint64_t v
             throw;
         }
         *out = ft;
+    });
+}
+
+gx_status gx_features_write(const gx_features* f, const char* path) {
+    return guard([&] {
+        if (!f) fail(GX_INVALID_ARGUMENT, "null handle");
+        if (f->backing == GX_BACKING_FILE) fail(GX_INVALID_ARGUMENT, "table is already file backed");
+        // FeatureWriter (graph_store.hpp:237-250): magic, u32 version, u64 n,
+        // u32 dim, u32 scalar_width, u64 payload offset (4096), zero padding
+        File out(path, O_WRONLY | O_CREAT | O_TRUNC);
+        unsigned char hdr[kPage] = {};
+        std::memcpy(hdr, kFeatMagic, 8);
+        const uint32_t ver = 1;
+        const uint64_t poff = kPage;
+        std::memcpy(hdr + 8, &ver, 4);
+        std::memcpy(hdr + 12, &f->n, 8);
+        std::memcpy(hdr + 20, &f->dim, 4);
+        std::memcpy(hdr + 24, &f->scalar_width, 4);
+        std::memcpy(hdr + 28, &poff, 8);
+        out.write_all(hdr, kPage);
+        const uint64_t bytes = f->n * f->row_bytes;
+        if (f->backing == GX_BACKING_HOST) {
+            if (bytes) out.write_all(f->host.p, bytes);
+            return;
+        }
+        const uint64_t CH = 1ull << 28;
+        PinBuf<uint8_t> pin;
+        pin.alloc(std::min(bytes, CH) + 1);
+        for (uint64_t o = 0; o < bytes; o += CH) {
+            const uint64_t c = std::min(CH, bytes - o);
+            GX_CUDA(cudaMemcpy(pin.p, f->dev.p + o, c, cudaMemcpyDeviceToHost));
+            out.write_all(pin.p, c);
+        }
     });
 }
 

@@ -1,7 +1,45 @@
 // gx_internal.cuh -- definitions behind the opaque C-ABI handles.
 #pragma once
 
+#include <atomic>
+#include <memory>
+
 #include "gx_common.cuh"
+
+namespace gx {
+// The 'SSD' tier (storage.cu): a features.bin payload read with pread in whole
+// 4 KB pages (O_DIRECT when the filesystem allows it) by a host thread pool.
+struct RowReader {
+    std::string path;
+    int fd = -1;
+    bool direct = false;
+    uint64_t poff = 0, rb = 0, n = 0, fsize = 0;
+    unsigned threads = 1;
+    uint64_t run_cap = 0;    // bytes per pread (coalesced page run)
+    uint64_t gap_pages = 0;  // merge runs separated by at most this many unneeded pages
+    std::atomic<uint64_t> rows{0}, preads{0}, bytes{0}, h2d{0}, read_ns{0};
+    RowReader(const char* path, uint64_t payload_off, uint64_t row_bytes, uint64_t n_rows);
+    ~RowReader();
+    // dst + q * rb <- row sorted[q] for q in [0, n); sorted ascending (runs coalesce)
+    void read_sorted(const uint32_t* sorted, uint64_t n, uint8_t* dst);
+    // any order (host-only API path): sorts a copy
+    void read_rows(const uint64_t* ids, uint64_t n, uint8_t* dst);
+  private:
+    void read_range(const uint32_t* sorted, uint64_t lo, uint64_t hi, uint8_t* dst, uint8_t* bounce);
+    void pread_full(uint8_t* dst, uint64_t len, uint64_t off, uint64_t need);
+};
+// Device-side staging scratch of one features handle (storage.cu).
+struct StageScratch {
+    DevBuf<uint32_t> keys, keys_alt, vals, vals_alt;
+    DevBuf<uint8_t> cub_tmp;
+    DevBuf<uint8_t> land[2];
+    PinBuf<uint8_t> pin[2];
+    PinBuf<uint32_t> h_sorted;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr}, ev_ready = nullptr;
+    ~StageScratch();
+};
+}  // namespace gx
 
 namespace gx {
 // Sampler scratch (sampler.cu); grow-only, reused across calls.
@@ -46,6 +84,8 @@ struct gx_ctx {
     gx::SampleScratch ss;
     gx::InspectScratch is;
     gx::DevBuf<uint32_t> resolve_slots;  // executor API path scratch
+    gx::DevBuf<uint32_t> stage_ids;      // API path: miss ids staged from storage
+    gx::DevBuf<uint8_t> stage_rows;      // API path: their rows
     cudaStream_t launch_stream = nullptr;  // executor launches go here when set (pipeline stream)
 };
 
@@ -103,6 +143,8 @@ struct gx_features {
     gx::DevBuf<uint8_t> dev;       // device backing store
     gx::PinBuf<uint8_t> host;      // pinned host backing store (mapped)
     const uint8_t* rows_dev_view = nullptr;  // pointer usable by kernels
+    std::unique_ptr<gx::RowReader> file;     // GX_BACKING_FILE
+    std::unique_ptr<gx::StageScratch> stage;
 };
 
 struct gx_batch {
@@ -136,14 +178,14 @@ void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N,
 
 // Executor launchers (executor.cu).
 void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table,
-                   const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                   const uint8_t* cache_rows, gx_features* f, uint8_t* out,
                    unsigned long long* counters);
 // gather with the serving slot of every row already resolved (kNever = miss)
 // seg_off != nullptr: segment mode -- rows of nseg consecutive iterations
 // (absolute offsets seg_off[0..nseg]); misses/pages are charged per iteration
 // into counters[8 * it + 1 / + 2] (executor.cu, SegInfo).
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
-                            const uint8_t* cache_rows, const gx_features* f, uint8_t* out,
+                            const uint8_t* cache_rows, const uint8_t* store, uint64_t row_bytes, uint8_t* out,
                             unsigned long long* counters, const uint32_t* seg_off = nullptr, uint32_t nseg = 0);
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos,
                         const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
@@ -151,9 +193,25 @@ void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_
                         uint64_t row_bytes);
 // counters: 5 words as for the gather (init rows are charged as misses)
 void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table,
-                       const gx_features* f, uint8_t* cache_rows, unsigned long long* counters);
+                       gx_features* f, uint8_t* cache_rows, unsigned long long* counters);
 void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table);
 void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t row_bytes,
                    unsigned long long* out);
+
+// Storage tier (storage.cu). A slot value with kStageFlag set (and != kNever)
+// is a miss whose row was staged: the gather reads row (slot & ~kStageFlag)
+// of the store pointer it is given and charges the miss to ids[k] as usual.
+constexpr uint32_t kStageFlag = 0x80000000u;
+// d_out row j <- feature row d_ids[j] from storage, for j in [0, n). Sorts the
+// requests by id on `s`, reads page runs on the host into pinned chunks,
+// copies them to HBM on the features' copy stream and scatters them to their
+// rows on `s`; returns when everything is enqueued (work on `s` after the call
+// sees the rows). Returns the host read wall time in ms.
+double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s);
+// Misses of a resolved access list: miss_ids[r] = ids[k] for the r-th k with
+// slots[k] == kNever (access order), slots[k] := kStageFlag | r. Returns the
+// count (synchronises `s`).
+uint64_t stage_misses(gx_ctx* ctx, const uint32_t* ids, uint32_t* slots, uint64_t n, DevBuf<uint32_t>& miss_ids,
+                      cudaStream_t s);
 
 }  // namespace gx
