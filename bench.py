@@ -55,6 +55,13 @@ CONFIGS = {
                        S=100, cache_frac=0.10, train_fraction=0.1,
                        workload="com-friendster-shape synthetic R-MAT: 65.6M nodes, ~1.8B edges, "
                                 "256-d fp32, fanout (10,10,10), batch 1000, superbatch 100, cache 10%"),
+    # configs[3]: MAG240M paper-subgraph shape, 768-d fp16 (scalar_width 2 extension): the
+    # 187 GB table exceeds one B200, so it runs row-partitioned over >= 2 GPUs (--features
+    # partitioned) -- 1.30B edges after dedup at avg_degree 10.75 pre-dedup
+    "mag240m": dict(N=121_751_666, avg_degree=10.75, dim=768, dtype="fp16", fanouts=[10, 10, 10],
+                    batch=1000, S=100, cache_frac=0.10, train_fraction=0.1, min_gpus_partitioned=2,
+                    workload="MAG240M-shape paper subgraph synthetic R-MAT: 122M nodes, ~1.3B edges, "
+                             "768-d fp16, fanout (10,10,10), batch 1000, superbatch 100, cache 10%"),
     # configs[0]: the reference's own CPU-runnable case
     "cfg1": dict(N=1_000_000, avg_degree=10.0, dim=128, fanouts=[10, 10, 10], batch=1000, S=100,
                  cache_frac=0.10, train_fraction=0.1,
@@ -154,13 +161,17 @@ class Clocks:
                 "source": "nvml 5 ms" if self._nvml else "nvidia-smi"}
 
 
-def build_dataset(gx, cfg, ctx, log, backing="device", ssd_dir=None):
+def build_dataset(gx, cfg, ctx, log, backing="device", ssd_dir=None, comm=None):
     edge_seed = gx.derive_seed(SEED_GEN, 0xED6E5)
     value_seed = gx.derive_seed(SEED_GEN, 0xFEA7)
+    dtype = np.float16 if cfg.get("dtype") == "fp16" else np.float32
     t0 = time.time()
     g = gx.GraphFile.generate_rmat(cfg["N"], cfg["avg_degree"], edge_seed, ctx=ctx)
     t1 = time.time()
-    f = gx.FeatureFile.generate(cfg["N"], cfg["dim"], value_seed, ctx=ctx)
+    if comm is not None:   # row-partitioned: this rank generates only its own rows
+        f = gx.FeatureFile.partitioned_generate(cfg["N"], cfg["dim"], value_seed, comm, ctx, dtype=dtype)
+    else:
+        f = gx.FeatureFile.generate(cfg["N"], cfg["dim"], value_seed, ctx=ctx, dtype=dtype)
     ctx.synchronize()
     t2 = time.time()
     log(f"dataset: N={g.num_nodes()} E={g.num_edges()} (graph {t1 - t0:.1f}s, features {t2 - t1:.1f}s)")
@@ -323,6 +334,10 @@ def main():
                     help="feature backing store: HBM-resident table (default) or the SSD tier "
                          "(features.bin on storage, misses read with O_DIRECT into pinned staging)")
     ap.add_argument("--ssd-dir", default=os.environ.get("GX_SSD_DIR", "/tmp"))
+    ap.add_argument("--features", default="replicated", choices=["replicated", "partitioned"],
+                    help="replicated: every rank holds the whole table (no data-path collective); "
+                         "partitioned: rows split over the ranks, cache init + misses fetched from "
+                         "their owners by NCCL all-to-all (SURVEY.md 8e)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     if args.avg_degree is not None:
@@ -345,7 +360,19 @@ def main():
         dist.init_process_group("nccl")
     import paper_2208_09151_b200 as gx
     ctx = gx.Context(local)
-    g, f = build_dataset(gx, cfg, ctx, log, args.backing, args.ssd_dir)
+    comm = None
+    if args.features == "partitioned":
+        uid = [gx.Comm.unique_id() if rank == 0 else None]
+        if world > 1:
+            torch.distributed.broadcast_object_list(uid, src=0)
+        comm = gx.Comm.nccl(ctx, uid[0], world, rank)
+    elif cfg.get("min_gpus_partitioned"):
+        msg = (f"config {args.config} needs its table row-partitioned over >= "
+               f"{cfg['min_gpus_partitioned']} GPUs (--features partitioned)")
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "unavailable": msg}))
+        return
+    g, f = build_dataset(gx, cfg, ctx, log, args.backing, args.ssd_dir, comm)
     sbs = make_plan(gx, cfg)
     K_entries = int(cfg["cache_frac"] * cfg["N"])
     pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries)
@@ -450,6 +477,13 @@ def main():
         "changeset_in_per_iter": sum(s.total_in for s in stats) / (n * S),
         "edges_per_superbatch": edges / n,
     }
+    if comm is not None:
+        xs = f.exchange_stats()
+        stages.update({
+            "exchange_ms": sum(s.ms_storage for s in stats) / n,
+            "exchange_rows_per_superbatch": sum(s.storage_rows for s in stats) / n,
+            "exchange_bytes_sent_total": xs.bytes_sent, "exchange_rows_remote_total": xs.rows_remote,
+            "exchange_calls": xs.calls})
     if args.backing == "file":
         sm = sum(s.ms_storage for s in stats)
         sb = sum(s.storage_bytes for s in stats)
@@ -473,7 +507,10 @@ def main():
                    "superbatch": S, "cache_entries": K_entries, "num_edges": g.num_edges(),
                    "pipeline": "overlap (2 superbatches in flight)" if args.overlap else "serial superbatches",
                    "backing": args.backing,
-                   "parallelism": f"dp{world} (superbatches per rank, no collective)",
+                   "parallelism": (f"dp{world} (superbatches per rank, no collective)" if comm is None else
+                                   f"dp{world} superbatches x {world}-way row-partitioned features "
+                                   "(NCCL all-to-all for cache init + misses)"),
+                   "features": args.features,
                    "l2": "inputs larger than L2 (57 GB table, 6.6 GB CSC)" if args.config == "papers"
                    else "inputs larger than L2"},
         "e2e": {"value": edges_all / wall_s, "unit": "sampled_edges/s",
@@ -489,7 +526,7 @@ def main():
         "stages": stages,
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and comm is None:
         try:
             import oracle
             if oracle.ref_available():

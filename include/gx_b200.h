@@ -165,6 +165,8 @@ typedef struct gx_features gx_features;
 typedef enum gx_backing {
     GX_BACKING_DEVICE = 0, /* whole table in HBM (fits one B200 up to ~150 GB) */
     GX_BACKING_HOST = 1,   /* pinned host memory, misses read over PCIe by the gather kernel */
+    GX_BACKING_PARTITIONED = 3, /* row-partitioned across ranks (gx_features_partitioned_*): rows
+                              of other ranks are fetched by a variable all-to-all (NCCL) */
     GX_BACKING_FILE = 2    /* the 'SSD' tier: features.bin stays on storage; the rows a
                               superbatch misses (cache init + changeset misses) are read with
                               pread (O_DIRECT when the filesystem allows it, whole 4 KB pages)
@@ -199,6 +201,10 @@ gx_status gx_features_from_host(gx_ctx* ctx, uint64_t num_nodes, uint32_t dim,
 /* generate the table on the device: feature_value (graphgen.hpp:74-77) */
 gx_status gx_features_generate(gx_ctx* ctx, uint64_t num_nodes, uint32_t dim,
                                uint64_t value_seed, gx_features** out);
+/* fp16 extension (scalar_width 2, cfg4 MAG240M-shape): element = the fp16
+ * round-to-nearest-even of feature_value */
+gx_status gx_features_generate_fp16(gx_ctx* ctx, uint64_t num_nodes, uint32_t dim, uint64_t value_seed,
+                                    gx_features** out);
 void gx_features_destroy(gx_features* f);
 uint64_t gx_features_num_nodes(const gx_features* f);
 uint32_t gx_features_dim(const gx_features* f);
@@ -206,6 +212,48 @@ uint64_t gx_features_row_bytes(const gx_features* f);
 /* FeatureFile::read_rows (graph_store.hpp:319-324) into host memory */
 gx_status gx_features_read_rows(gx_features* f, const uint64_t* ids, uint64_t n, void* out,
                                 gx_iostats* io);
+
+/* ---- multi-GPU: row-partitioned feature table -----------
+ * The reference is single-process (its only parallelism is a thread pool,
+ * sampler.hpp:205-235); this is the B200 extension north_star asks for. One
+ * process per GPU (or, for tests, one host thread per rank). Rank r of P owns
+ * feature rows [N*r/P, N*(r+1)/P) in its HBM. Every row a rank's cache needs
+ * from the backing store (cache init, changeset misses) is fetched by ONE
+ * variable all-to-all per request set: per-owner request lists (u32 local ids)
+ * out, rows back, as grouped NCCL send/recv over NVLink/NVSwitch; the owner
+ * serves them with the row-gather kernel. Collective: every rank must make
+ * the same sequence of calls that touch a partitioned table (pipeline
+ * superbatches, cache create/gather), with empty request sets where it has none. */
+typedef struct gx_comm gx_comm;
+#define GX_COMM_ID_BYTES 128
+/* a fresh NCCL unique id (rank 0 creates it, the caller broadcasts the bytes) */
+gx_status gx_comm_unique_id(void* id_out);
+/* NCCL communicator over this context's GPU (libnccl.so.2 resolved at run time) */
+gx_status gx_comm_init_nccl(gx_ctx* ctx, const void* id, int nranks, int rank, gx_comm** out);
+/* in-process transport: nranks contexts (one per host thread; they may share a
+ * GPU), peer copies through the CUDA runtime; outs[r] belongs to ctxs[r] */
+gx_status gx_comm_init_local(gx_ctx* const* ctxs, int nranks, gx_comm** outs);
+void gx_comm_destroy(gx_comm* c);
+int gx_comm_rank(const gx_comm* c);
+int gx_comm_size(const gx_comm* c);
+/* rows [lo, hi) owned by `rank` */
+gx_status gx_partition_bounds(uint64_t num_nodes, int nranks, int rank, uint64_t* lo, uint64_t* hi);
+/* this rank's partition from its own rows (host, (hi-lo) x row_bytes), from
+ * features.bin (reads only this rank's rows) or generated (feature_value) */
+gx_status gx_features_partitioned_from_host(gx_ctx* ctx, gx_comm* comm, uint64_t num_nodes, uint32_t dim,
+                                            uint32_t scalar_width, const void* local_rows, gx_features** out);
+gx_status gx_features_partitioned_open(gx_ctx* ctx, gx_comm* comm, const char* path, gx_features** out);
+gx_status gx_features_partitioned_generate(gx_ctx* ctx, gx_comm* comm, uint64_t num_nodes, uint32_t dim,
+                                           uint32_t scalar_width, uint64_t value_seed, gx_features** out);
+typedef struct gx_exchange_stats {
+    uint64_t calls;           /* all-to-all request sets served */
+    uint64_t rows_requested;  /* rows this rank asked for (own partition included) */
+    uint64_t rows_remote;     /* of those, rows owned by other ranks */
+    uint64_t rows_served;     /* rows this rank sent to requesters (itself included) */
+    uint64_t bytes_sent;      /* ids + rows this rank put on the wire to other ranks */
+    double ms;                /* host wall time inside the exchanges */
+} gx_exchange_stats;
+gx_status gx_features_exchange_stats(const gx_features* f, gx_exchange_stats* out);
 
 /* Gathered batch buffer (RowMatrix, graph_store.hpp:222-234), device resident. */
 typedef struct gx_batch gx_batch;

@@ -45,6 +45,11 @@ class PipelineStatsC(C.Structure):
                 ("ms_storage", dbl), ("storage_rows", u64), ("storage_bytes", u64)]
 
 
+class ExchangeStatsC(C.Structure):
+    _fields_ = [("calls", u64), ("rows_requested", u64), ("rows_remote", u64), ("rows_served", u64),
+                ("bytes_sent", u64), ("ms", dbl)]
+
+
 class StorageStatsC(C.Structure):
     _fields_ = [("rows", u64), ("preads", u64), ("bytes", u64), ("h2d_bytes", u64), ("read_ms", dbl),
                 ("threads", u32), ("direct", i32)]
@@ -100,6 +105,18 @@ SIGNATURES = {
     "gx_changesets_write_files": (i32, [vp, cstr, u64]),
     "gx_features_open": (i32, [vp, cstr, i32, PVP]),
     "gx_features_write": (i32, [vp, cstr]),
+    "gx_features_generate_fp16": (i32, [vp, u64, u32, u64, PVP]),
+    "gx_comm_unique_id": (i32, [vp]),
+    "gx_comm_init_nccl": (i32, [vp, vp, i32, i32, PVP]),
+    "gx_comm_init_local": (i32, [vp, i32, vp]),
+    "gx_comm_destroy": (None, [vp]),
+    "gx_comm_rank": (i32, [vp]),
+    "gx_comm_size": (i32, [vp]),
+    "gx_partition_bounds": (i32, [u64, i32, i32, P64, P64]),
+    "gx_features_partitioned_from_host": (i32, [vp, vp, u64, u32, u32, vp, PVP]),
+    "gx_features_partitioned_open": (i32, [vp, vp, cstr, PVP]),
+    "gx_features_partitioned_generate": (i32, [vp, vp, u64, u32, u32, u64, PVP]),
+    "gx_features_exchange_stats": (i32, [vp, vp]),
     "gx_features_storage_stats": (i32, [vp, vp]),
     "gx_features_from_host": (i32, [vp, u64, u32, u32, vp, i32, PVP]),
     "gx_features_generate": (i32, [vp, u64, u32, u64, PVP]),

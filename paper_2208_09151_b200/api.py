@@ -18,7 +18,8 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
-from ._lib import (IoStatsC, LogicError, PipelineStatsC, StorageStatsC, CudaError, check, lib)  # noqa: F401
+from ._lib import (ExchangeStatsC, IoStatsC, LogicError, PipelineStatsC, StorageStatsC, CudaError, check,  # noqa: F401
+                   lib)
 
 # ---------------------------------------------------------------------------
 # primitives (common.hpp)
@@ -635,6 +636,67 @@ def precompute_changesets(trace: FileTrace, num_nodes: int, num_entries: int, ou
 BACKING = {"device": 0, "host": 1, "file": 2}
 
 
+def partition_bounds(num_nodes: int, nranks: int, rank: int) -> tuple:
+    """Rows [lo, hi) rank `rank` of `nranks` owns: [N*r/P, N*(r+1)/P)."""
+    lo, hi = C.c_uint64(), C.c_uint64()
+    check(lib.gx_partition_bounds(num_nodes, nranks, rank, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
+class Comm:
+    """Communicator of a row-partitioned feature table: NCCL (one process per
+    GPU) or the in-process hub (one host thread per rank, for tests)."""
+
+    def __init__(self, handle, ctx: Context):
+        self.h = handle
+        self.ctx = ctx
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib.gx_comm_destroy(self.h)
+            self.h = None
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib.gx_comm_unique_id(buf))
+        return bytes(buf)
+
+    @staticmethod
+    def nccl(ctx: Context, uid: bytes, nranks: int, rank: int) -> "Comm":
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib.gx_comm_init_nccl(ctx.h, buf, nranks, rank, C.byref(h)))
+        return Comm(h, ctx)
+
+    @staticmethod
+    def local(ctxs: Sequence[Context]) -> List["Comm"]:
+        n = len(ctxs)
+        arr = (C.c_void_p * n)(*[c.h.value if isinstance(c.h, C.c_void_p) else c.h for c in ctxs])
+        outs = (C.c_void_p * n)()
+        check(lib.gx_comm_init_local(arr, n, outs))
+        return [Comm(C.c_void_p(outs[r]), ctxs[r]) for r in range(n)]
+
+    @property
+    def rank(self) -> int:
+        return lib.gx_comm_rank(self.h)
+
+    @property
+    def size(self) -> int:
+        return lib.gx_comm_size(self.h)
+
+
+@dataclasses.dataclass
+class ExchangeStats:
+    """gx_exchange_stats: all-to-all traffic of a partitioned table."""
+    calls: int
+    rows_requested: int
+    rows_remote: int
+    rows_served: int
+    bytes_sent: int
+    ms: float
+
+
 @dataclasses.dataclass
 class StorageStats:
     """gx_storage_stats: physical reads of a file-backed table since open."""
@@ -690,12 +752,63 @@ class FeatureFile:
         return FeatureFile(h, c, rows.dtype.type)
 
     @staticmethod
-    def generate(num_nodes: int, dim: int, value_seed: int, ctx: Optional[Context] = None) -> "FeatureFile":
-        """feature_value table (graphgen.hpp:74-77) generated in HBM."""
+    def generate(num_nodes: int, dim: int, value_seed: int, ctx: Optional[Context] = None,
+                 dtype=np.float32) -> "FeatureFile":
+        """feature_value table (graphgen.hpp:74-77) generated in HBM; dtype
+        float16 = the scalar_width 2 extension (fp16 of the same values)."""
         c = _ctx(ctx)
         h = C.c_void_p()
+        if np.dtype(dtype) == np.float16:
+            check(lib.gx_features_generate_fp16(c.h, num_nodes, dim, value_seed, C.byref(h)))
+            return FeatureFile(h, c, np.float16)
         check(lib.gx_features_generate(c.h, num_nodes, dim, value_seed, C.byref(h)))
         return FeatureFile(h, c)
+
+    # -- row-partitioned tables (include/gx_b200.h, SURVEY.md §8e) ----------
+    @staticmethod
+    def partitioned_from_array(local_rows: np.ndarray, num_nodes: int, comm: "Comm",
+                               ctx: Optional[Context] = None) -> "FeatureFile":
+        """This rank's rows [lo, hi) of an N-row table partitioned over comm."""
+        c = ctx if ctx is not None else comm.ctx
+        rows = np.ascontiguousarray(local_rows)
+        lo, hi = partition_bounds(num_nodes, comm.size, comm.rank)
+        if rows.shape[0] != hi - lo:
+            raise ValueError(f"rank {comm.rank} owns rows [{lo}, {hi}), got {rows.shape[0]}")
+        h = C.c_void_p()
+        check(lib.gx_features_partitioned_from_host(c.h, comm.h, num_nodes, rows.shape[1], rows.dtype.itemsize,
+                                                    _ptr(rows.reshape(-1)) if rows.size else None,
+                                                    C.byref(h)))
+        f = FeatureFile(h, c, rows.dtype.type)
+        f.comm = comm
+        return f
+
+    @staticmethod
+    def partitioned_open(path: str, comm: "Comm", ctx: Optional[Context] = None) -> "FeatureFile":
+        """This rank's rows of features.bin (only those bytes are read)."""
+        c = ctx if ctx is not None else comm.ctx
+        h = C.c_void_p()
+        check(lib.gx_features_partitioned_open(c.h, comm.h, os.fspath(path).encode(), C.byref(h)))
+        f = FeatureFile(h, c)
+        if f.row_bytes() == 2 * f.dim():
+            f.dtype = np.float16
+        f.comm = comm
+        return f
+
+    @staticmethod
+    def partitioned_generate(num_nodes: int, dim: int, value_seed: int, comm: "Comm",
+                             ctx: Optional[Context] = None, dtype=np.float32) -> "FeatureFile":
+        c = ctx if ctx is not None else comm.ctx
+        sw = np.dtype(dtype).itemsize
+        h = C.c_void_p()
+        check(lib.gx_features_partitioned_generate(c.h, comm.h, num_nodes, dim, sw, value_seed, C.byref(h)))
+        f = FeatureFile(h, c, np.dtype(dtype).type)
+        f.comm = comm
+        return f
+
+    def exchange_stats(self) -> "ExchangeStats":
+        st = ExchangeStatsC()
+        check(lib.gx_features_exchange_stats(self.h, C.byref(st)))
+        return ExchangeStats(st.calls, st.rows_requested, st.rows_remote, st.rows_served, st.bytes_sent, st.ms)
 
     def num_nodes(self) -> int:
         return lib.gx_features_num_nodes(self.h)

@@ -490,7 +490,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         std::swap(ctx->is.trace, sl.trace);
         std::swap(ctx->is.acc_slot, sl.acc_slot);
         // storage tier: the accesses the cache will miss read staged rows
-        const bool file = p->f->backing == GX_BACKING_FILE;
+        const bool file = staged_backing(p->f);
         const uint64_t n_miss = file ? stage_misses(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.miss_ids, A) : 0;
         GX_CUDA(cudaEventRecord(sl.ev[2], A));
         // (3)+(4) executor on stream B, after the inspector and the previous executor
@@ -530,14 +530,19 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             if (file) {
                 // the init rows land in their slots, the misses in this slot's
                 // staging rows, both read from storage while B drains
-                const uint64_t r0 = p->f->file->rows.load(), b0 = p->f->file->bytes.load();
-                sl.ms_storage += stage_fetch(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B);
+                // (partitioned tables: two all-to-alls with the other ranks)
+                const bool f_file = p->f->file != nullptr;
+                const uint64_t r0 = f_file ? p->f->file->rows.load() : p->f->xstats.rows_requested;
+                const uint64_t b0 = f_file ? p->f->file->bytes.load() : p->f->xstats.bytes_sent;
+                sl.cs.init.reserve(1);
+                sl.miss_ids.reserve(1);
+                sl.ms_storage += fetch_rows(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
                 sl.stage.reserve(std::max<uint64_t>(n_miss * rb, 16));
-                sl.ms_storage += stage_fetch(p->f, sl.miss_ids.p, n_miss, sl.stage.p, B);
+                sl.ms_storage += fetch_rows(p->f, sl.miss_ids.p, n_miss, sl.stage.p, B);
                 store = sl.stage.p;
-                sl.storage_rows = p->f->file->rows.load() - r0;
-                sl.storage_bytes = p->f->file->bytes.load() - b0;
+                sl.storage_rows = (f_file ? p->f->file->rows.load() : p->f->xstats.rows_requested) - r0;
+                sl.storage_bytes = (f_file ? p->f->file->bytes.load() : p->f->xstats.bytes_sent) - b0;
             } else {
                 launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
                                   sl.counters.p + 8 * S);

@@ -12,6 +12,7 @@
 //    the inspector precomputed; k_apply (API path) recomputes them from this
 //    cache's own free list, exactly as the reference does.
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 
 #include "gx_internal.cuh"
@@ -494,11 +495,11 @@ template <int VEC, int R>
 static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
                                const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
                                unsigned long long* counters, SegInfo sg = {nullptr, 0, nullptr}) {
-    static int bps = 0;
-    if (!bps) {
-        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_gather_rows<VEC, R>, GA_THREADS, 0));
-        bps = std::max(bps, 1);
-    }
+    static const int bps = [] {
+        int b = 0;
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gather_rows<VEC, R>, GA_THREADS, 0));
+        return std::max(b, 1);
+    }();
     const uint64_t warps_needed = (n + R - 1) / R;
     const uint64_t blocks_needed = (warps_needed * 32 + GA_THREADS - 1) / GA_THREADS;
     const uint64_t blocks = std::min<uint64_t>(blocks_needed, (uint64_t)ctx->num_sms * bps);
@@ -526,6 +527,8 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         return std::min(std::max(kb, 16), 200) * 1024;
     }();
     static const int ring = env_int("GX_GATHER_D", 0);  // 3/4/6: k_gather_ring<D> (experimental)
+    static std::mutex cfg_mu;  // launch-config caches below are shared by every context / host thread
+    std::lock_guard<std::mutex> cfg_lock(cfg_mu);
     if (vec16(rb) && R == 1 && (ring == 3 || ring == 4 || ring == 6) && (uint64_t)ring * 32 * rb <= (uint64_t)budget) {
         static int tpb = 0, bpsm = 0;
         static uint64_t last = 0;
@@ -579,16 +582,23 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
 
 void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* table, const uint8_t* cache_rows,
                    gx_features* f, uint8_t* out, unsigned long long* counters) {
-    if (!n) return;
+    if (!n) {
+        if (f->backing == GX_BACKING_PARTITIONED) {  // still take part in the exchange
+            ctx->stage_ids.reserve(1);
+            fetch_rows(f, ctx->stage_ids.p, 0, nullptr, lstream(ctx));
+        }
+        return;
+    }
     DevBuf<uint32_t>& slots = ctx->resolve_slots;  // API path only
     slots.reserve(n);
     k_resolve<<<ctx->num_sms * 4, 256, 0, lstream(ctx)>>>(ids, n, table, slots.p);
     GX_CHECK_LAUNCH();
     const uint8_t* store = f->rows_dev_view;
-    if (f->backing == GX_BACKING_FILE) {  // misses come from the storage tier
+    if (staged_backing(f)) {  // misses come from the storage tier / the owning ranks
         const uint64_t m = stage_misses(ctx, ids, slots.p, n, ctx->stage_ids, lstream(ctx));
         ctx->stage_rows.reserve(std::max<uint64_t>(m * f->row_bytes, 16));
-        if (m) stage_fetch(f, ctx->stage_ids.p, m, ctx->stage_rows.p, lstream(ctx));
+        ctx->stage_ids.reserve(1);
+        fetch_rows(f, ctx->stage_ids.p, m, ctx->stage_rows.p, lstream(ctx));
         store = ctx->stage_rows.p;
     }
     launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, store, f->row_bytes, out, counters);
@@ -619,10 +629,11 @@ __global__ void k_set_table(const uint32_t* __restrict__ init, uint32_t n, int32
 
 void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table, gx_features* f,
                        uint8_t* cache_rows, unsigned long long* counters) {
-    if (!n) return;
-    if (f->backing == GX_BACKING_FILE) {
-        // the storage tier writes the init rows straight into their slots
-        stage_fetch(f, init, n, cache_rows, lstream(ctx));
+    if (staged_backing(f)) {
+        // the storage tier / the owners write the init rows straight into their slots
+        fetch_rows(f, init, n, cache_rows, lstream(ctx));
+    } else if (!n) {
+        return;
     } else if (vec16(f->row_bytes)) {
         // one large all-miss gather: the 8-rows-per-warp LDG/STG kernel measured
         // faster than the bulk-copy kernel here (1.05 vs 1.35 ms, 6.2M x 512 B rows)
@@ -729,7 +740,7 @@ gx_status gx_cache_create(gx_features* f, const uint64_t* init, uint64_t n_init,
             unsigned long long pg = 0;
             GX_CUDA(cudaMemcpyAsync(&pg, c->counters.p + 2, 8, cudaMemcpyDeviceToHost, ctx->stream));
             GX_CUDA(cudaStreamSynchronize(ctx->stream));
-            if (f->backing == GX_BACKING_FILE) {  // the storage tier does not run the gather's counters
+            if (staged_backing(f)) {  // the staged tiers do not run the gather's counters
                 pg = 0;
                 for (uint64_t k = 0; k < n_init; ++k)
                     pg += pages_touched(init[k] * f->row_bytes, init[k] * f->row_bytes + f->row_bytes);
@@ -876,6 +887,8 @@ gx_status gx_features_read_rows(gx_features* f, const uint64_t* ids, uint64_t n,
         gx_ctx* ctx = f->ctx;
         for (uint64_t k = 0; k < n; ++k)
             if (ids[k] >= f->n) fail(GX_OUT_OF_RANGE, "feature row id out of range");
+        if (f->backing == GX_BACKING_PARTITIONED)
+            fail(GX_INVALID_ARGUMENT, "read_rows on a partitioned table: rows are served collectively (cache/pipeline)");
         if (f->backing == GX_BACKING_FILE) {  // straight from storage into the caller's buffer
             f->file->read_rows(ids, n, (uint8_t*)out);
             if (io) {

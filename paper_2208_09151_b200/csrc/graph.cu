@@ -13,6 +13,8 @@
 #include <fcntl.h>
 #include <unistd.h>
 
+#include <cuda_fp16.h>
+
 #include "gx_internal.cuh"
 
 namespace gx {
@@ -248,15 +250,27 @@ static void generate_rmat(gx_graph* g, uint64_t N, double avg, double a, double 
 }
 
 // feature_value (graphgen.hpp:74-77) for a whole table.
-__global__ void k_features(float* out, uint64_t n, uint32_t dim, uint64_t vseed) {
+// Rows [node0, node0 + n) of the table; fp16 extension: __float2half_rn of the value.
+template <class T>
+__global__ void k_features(T* out, uint64_t n, uint32_t dim, uint64_t vseed, uint64_t node0) {
     const uint64_t total = n * dim;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t node = i / dim;
-        const uint32_t col = (uint32_t)(i - node * dim);
-        const uint64_t h = mix64(vseed ^ mix64(node * 0x10001ULL + col));
-        out[i] = (float)(h >> 40) * 0x1.0p-24f;
+        const uint64_t r = i / dim;
+        const uint32_t col = (uint32_t)(i - r * dim);
+        const uint64_t h = mix64(vseed ^ mix64((node0 + r) * 0x10001ULL + col));
+        const float v = (float)(h >> 40) * 0x1.0p-24f;
+        if constexpr (sizeof(T) == 2) out[i] = __float2half_rn(v);
+        else out[i] = v;
     }
+}
+
+void launch_features(uint8_t* out, uint64_t n, uint32_t dim, uint32_t sw, uint64_t vseed, uint64_t node0,
+                     int num_sms, cudaStream_t s) {
+    if (!n) return;
+    if (sw == 2) k_features<__half><<<num_sms * 8, 256, 0, s>>>((__half*)out, n, dim, vseed, node0);
+    else k_features<float><<<num_sms * 8, 256, 0, s>>>((float*)out, n, dim, vseed, node0);
+    GX_CHECK_LAUNCH();
 }
 
 static void features_alloc(gx_features* f, int backing) {
@@ -514,8 +528,7 @@ gx_status gx_features_generate(gx_ctx* ctx, uint64_t n, uint32_t dim, uint64_t v
             ft->scalar_width = 4;
             ft->row_bytes = (uint64_t)dim * 4;
             features_alloc(ft, GX_BACKING_DEVICE);
-            k_features<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>((float*)ft->dev.p, n, dim, vseed);
-            GX_CHECK_LAUNCH();
+            launch_features(ft->dev.p, n, dim, 4, vseed, 0, ctx->num_sms, ctx->stream);
             GX_CUDA(cudaStreamSynchronize(ctx->stream));
         } catch (...) {
             delete ft;
@@ -555,6 +568,28 @@ gx_status gx_features_write(const gx_features* f, const char* path) {
             GX_CUDA(cudaMemcpy(pin.p, f->dev.p + o, c, cudaMemcpyDeviceToHost));
             out.write_all(pin.p, c);
         }
+    });
+}
+
+gx_status gx_features_generate_fp16(gx_ctx* ctx, uint64_t n, uint32_t dim, uint64_t vseed, gx_features** out) {
+    return guard([&] {
+        if (dim < 1) fail(GX_INVALID_ARGUMENT, "dim must be >= 1");
+        check_nodes_u32(n);
+        auto ft = new gx_features();
+        try {
+            ft->ctx = ctx;
+            ft->n = n;
+            ft->dim = dim;
+            ft->scalar_width = 2;
+            ft->row_bytes = (uint64_t)dim * 2;
+            features_alloc(ft, GX_BACKING_DEVICE);
+            launch_features(ft->dev.p, n, dim, 2, vseed, 0, ctx->num_sms, ctx->stream);
+            GX_CUDA(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+            delete ft;
+            throw;
+        }
+        *out = ft;
     });
 }
 

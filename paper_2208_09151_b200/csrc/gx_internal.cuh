@@ -28,6 +28,13 @@ struct RowReader {
     void read_range(const uint32_t* sorted, uint64_t lo, uint64_t hi, uint8_t* dst, uint8_t* bounce);
     void pread_full(uint8_t* dst, uint64_t len, uint64_t off, uint64_t need);
 };
+// Exchange scratch of a partitioned features handle (comm.cu).
+struct PartScratch {
+    DevBuf<uint32_t> keys, keys_alt, vals, vals_alt, send_ids, recv_ids;
+    DevBuf<unsigned long long> counts;
+    DevBuf<uint8_t> cub_tmp, send_rows, recv_rows;
+    DevBuf<unsigned long long> dummy;
+};
 // Device-side staging scratch of one features handle (storage.cu).
 struct StageScratch {
     DevBuf<uint32_t> keys, keys_alt, vals, vals_alt;
@@ -145,6 +152,11 @@ struct gx_features {
     const uint8_t* rows_dev_view = nullptr;  // pointer usable by kernels
     std::unique_ptr<gx::RowReader> file;     // GX_BACKING_FILE
     std::unique_ptr<gx::StageScratch> stage;
+    // GX_BACKING_PARTITIONED: this rank's rows [part_lo, part_hi) in `dev`
+    gx_comm* comm = nullptr;
+    uint64_t part_lo = 0, part_hi = 0;
+    std::unique_ptr<gx::PartScratch> part;
+    gx_exchange_stats xstats{};
 };
 
 struct gx_batch {
@@ -213,5 +225,24 @@ double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d
 // count (synchronises `s`).
 uint64_t stage_misses(gx_ctx* ctx, const uint32_t* ids, uint32_t* slots, uint64_t n, DevBuf<uint32_t>& miss_ids,
                       cudaStream_t s);
+// Row-partitioned table (comm.cu): the same contract as stage_fetch, served by
+// the owners through one variable all-to-all. Collective (call on every rank,
+// also with n == 0).
+double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s);
+// storage tiers that deliver rows through staging (FILE, PARTITIONED)
+inline bool staged_backing(const gx_features* f) {
+    return f->backing == GX_BACKING_FILE || f->backing == GX_BACKING_PARTITIONED;
+}
+// d_out row j <- feature row d_ids[j] through the table's staged tier
+inline double fetch_rows(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s) {
+    return f->backing == GX_BACKING_PARTITIONED ? part_fetch(f, d_ids, n, d_out, s)
+                                                : stage_fetch(f, d_ids, n, d_out, s);
+}
+// feature_value rows [node0, node0 + n) (graph.cu), scalar_width 4 or 2
+void launch_features(uint8_t* out, uint64_t n, uint32_t dim, uint32_t sw, uint64_t vseed, uint64_t node0,
+                     int num_sms, cudaStream_t s);
+// k_scatter_rows launcher (storage.cu): out row dst_idx[q] <- src row q
+void launch_scatter_rows(const uint8_t* src, const uint32_t* dst_idx, uint64_t cnt, uint8_t* out, uint64_t rb,
+                         int num_sms, cudaStream_t s);
 
 }  // namespace gx

@@ -184,6 +184,15 @@ __global__ void k_scatter_rows(const uint8_t* __restrict__ land, const uint32_t*
     }
 }
 
+void launch_scatter_rows(const uint8_t* src, const uint32_t* dst_idx, uint64_t cnt, uint8_t* out, uint64_t rb,
+                         int num_sms, cudaStream_t s) {
+    if (!cnt) return;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((cnt * 32 + 255) / 256, (uint64_t)num_sms * 8);
+    if (rb % 16 == 0) k_scatter_rows<16><<<blocks, 256, 0, s>>>(src, dst_idx, cnt, out, rb);
+    else k_scatter_rows<4><<<blocks, 256, 0, s>>>(src, dst_idx, cnt, out, rb);
+    GX_CHECK_LAUNCH();
+}
+
 static int key_bits(uint64_t n) {
     int b = 1;
     while (b < 32 && (1ull << b) < n) ++b;
@@ -252,10 +261,7 @@ double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d
         GX_CUDA(cudaEventRecord(st.ev_h2d[b], st.copy));
         f->file->h2d.fetch_add(cnt * rb, std::memory_order_relaxed);
         GX_CUDA(cudaStreamWaitEvent(s, st.ev_h2d[b], 0));
-        const unsigned blocks = (unsigned)std::min<uint64_t>((cnt * 32 + 255) / 256, (uint64_t)ctx->num_sms * 8);
-        if (rb % 16 == 0) k_scatter_rows<16><<<blocks, 256, 0, s>>>(st.land[b].p, perm + c0, cnt, d_out, rb);
-        else k_scatter_rows<4><<<blocks, 256, 0, s>>>(st.land[b].p, perm + c0, cnt, d_out, rb);
-        GX_CHECK_LAUNCH();
+        launch_scatter_rows(st.land[b].p, perm + c0, cnt, d_out, rb, ctx->num_sms, s);
         GX_CUDA(cudaEventRecord(st.ev_free[b], s));
         used[b] = true;
     }
