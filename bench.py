@@ -365,7 +365,14 @@ def main():
         uid = [gx.Comm.unique_id() if rank == 0 else None]
         if world > 1:
             torch.distributed.broadcast_object_list(uid, src=0)
-        comm = gx.Comm.nccl(ctx, uid[0], world, rank)
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)  # NCCL's version banner goes to stderr: stdout carries only the JSON line
+        try:
+            comm = gx.Comm.nccl(ctx, uid[0], world, rank)
+        finally:
+            os.dup2(saved, 1)
+            os.close(saved)
     elif cfg.get("min_gpus_partitioned"):
         msg = (f"config {args.config} needs its table row-partitioned over >= "
                f"{cfg['min_gpus_partitioned']} GPUs (--features partitioned)")

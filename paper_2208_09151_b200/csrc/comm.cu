@@ -278,6 +278,45 @@ __global__ void k_local_ids(const uint32_t* __restrict__ ids, const uint32_t* __
         out[q] = (uint32_t)(ids[perm[q]] - b.lo[owner[q]]);
 }
 
+// out row perm[q] <- local row ids[q] (a rank's own requests), 16-byte
+// vectors, R rows in flight per warp
+template <int VEC>
+__global__ void k_gather_scatter(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ perm, uint64_t n,
+                                 const uint8_t* __restrict__ store, uint8_t* __restrict__ out, uint64_t rb) {
+    using V = typename std::conditional<VEC == 16, uint4, uint32_t>::type;
+    constexpr int R = 4;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31, nvec = (uint32_t)(rb / VEC);
+    for (uint64_t q0 = warp * R; q0 < n; q0 += nwarps * R) {
+        const V* src[R];
+        V* dst[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const uint64_t q = q0 + k < n ? q0 + k : q0;
+            src[k] = reinterpret_cast<const V*>(store + (uint64_t)__ldg(ids + q) * rb);
+            dst[k] = reinterpret_cast<V*>(out + (uint64_t)__ldg(perm + q) * rb);
+        }
+        for (uint32_t c = lane; c < nvec; c += 32) {
+            V t[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) t[k] = src[k][c];
+#pragma unroll
+            for (int k = 0; k < R; ++k)
+                if (q0 + k < n) dst[k][c] = t[k];
+        }
+    }
+}
+
+static void launch_gather_scatter(const uint32_t* ids, const uint32_t* perm, uint64_t n, const uint8_t* store,
+                                  uint8_t* out, uint64_t rb, int num_sms, cudaStream_t s) {
+    if (!n) return;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((n * 8 + 255) / 256, (uint64_t)num_sms * 8);
+    if (rb % 16 == 0) k_gather_scatter<16><<<blocks, 256, 0, s>>>(ids, perm, n, store, out, rb);
+    else k_gather_scatter<4><<<blocks, 256, 0, s>>>(ids, perm, n, store, out, rb);
+    GX_CHECK_LAUNCH();
+}
+
 static Bounds make_bounds(uint64_t N, int P) {
     Bounds b{};
     b.P = P;
@@ -290,6 +329,7 @@ double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_
     gx_ctx* ctx = f->ctx;
     Transport& T = *f->comm->t;
     const int P = T.size;
+    if (P == 1 && n == 0) return 0.0;  // nothing to exchange with nobody
     const uint64_t rb = f->row_bytes;
     if (!f->part) f->part.reset(new PartScratch());
     PartScratch& x = *f->part;
@@ -328,24 +368,30 @@ double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_
         GX_CUDA(cudaStreamSynchronize(s));
         for (int p = 0; p < P; ++p) scnt[p] = h[p];
     }
-    // (2) counts, then ids
+    // (2) counts, then ids. This rank's own requests never touch the network:
+    // they are served straight from the local partition (step 3a).
     T.counts(scnt.data(), rcnt.data(), s);
+    const int me = T.rank;
     std::vector<uint64_t> soff(P + 1, 0), roff(P + 1, 0);
     for (int p = 0; p < P; ++p) {
         soff[p + 1] = soff[p] + scnt[p];
-        roff[p + 1] = roff[p] + rcnt[p];
+        roff[p + 1] = roff[p] + (p == me ? 0 : rcnt[p]);
     }
-    const uint64_t nrecv = roff[P];
+    const uint64_t nrecv = roff[P];  // rows other ranks asked this rank for
     x.recv_ids.reserve(nrecv + 1);
     std::vector<uint64_t> sb(P), so(P), rbb(P), ro(P);
     for (int p = 0; p < P; ++p) {
-        sb[p] = scnt[p] * 4;
+        sb[p] = p == me ? 0 : scnt[p] * 4;
         so[p] = soff[p] * 4;
-        rbb[p] = rcnt[p] * 4;
+        rbb[p] = p == me ? 0 : rcnt[p] * 4;
         ro[p] = roff[p] * 4;
     }
-    T.alltoallv((const uint8_t*)x.send_ids.p, so.data(), sb.data(), (uint8_t*)x.recv_ids.p, ro.data(), rbb.data(), s);
-    // (3) serve the requests from this rank's partition (local ids)
+    if (P > 1)
+        T.alltoallv((const uint8_t*)x.send_ids.p, so.data(), sb.data(), (uint8_t*)x.recv_ids.p, ro.data(), rbb.data(),
+                    s);
+    // (3a) own requests: local row -> request position in one pass
+    launch_gather_scatter(x.send_ids.p + soff[me], perm + soff[me], scnt[me], f->dev.p, d_out, rb, ctx->num_sms, s);
+    // (3b) serve the other ranks' requests from this rank's partition (local ids)
     x.send_rows.reserve(std::max<uint64_t>(nrecv * rb, 16));
     x.dummy.reserve(8);
     if (nrecv) {
@@ -359,23 +405,27 @@ double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_
         }
         ctx->launch_stream = saved;
     }
-    // (4) rows back, in request-grouped order; scatter to their requests
+    // (4) rows back into their request-grouped slots; scatter to their requests
+    const uint64_t n_remote = n - scnt[me];
     x.recv_rows.reserve(std::max<uint64_t>(n * rb, 16));
     for (int p = 0; p < P; ++p) {
-        sb[p] = rcnt[p] * rb;  // rows go back to whoever asked
+        sb[p] = p == me ? 0 : rcnt[p] * rb;  // rows go back to whoever asked
         so[p] = roff[p] * rb;
-        rbb[p] = scnt[p] * rb;
+        rbb[p] = p == me ? 0 : scnt[p] * rb;
         ro[p] = soff[p] * rb;
     }
-    T.alltoallv(x.send_rows.p, so.data(), sb.data(), x.recv_rows.p, ro.data(), rbb.data(), s);
-    launch_scatter_rows(x.recv_rows.p, perm, n, d_out, rb, ctx->num_sms, s);
+    if (P > 1) {
+        T.alltoallv(x.send_rows.p, so.data(), sb.data(), x.recv_rows.p, ro.data(), rbb.data(), s);
+        launch_scatter_rows(x.recv_rows.p, perm, soff[me], d_out, rb, ctx->num_sms, s);
+        const uint64_t tail = soff[me] + scnt[me];
+        launch_scatter_rows(x.recv_rows.p + tail * rb, perm + tail, n - tail, d_out, rb, ctx->num_sms, s);
+    }
     // counters
-    const int me = T.rank;
     f->xstats.calls += 1;
     f->xstats.rows_requested += n;
-    f->xstats.rows_remote += n - scnt[me];
-    f->xstats.rows_served += nrecv;
-    f->xstats.bytes_sent += (n - scnt[me]) * 4 + (nrecv - rcnt[me]) * rb;
+    f->xstats.rows_remote += n_remote;
+    f->xstats.rows_served += nrecv + scnt[me];
+    f->xstats.bytes_sent += n_remote * 4 + nrecv * rb;
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     f->xstats.ms += ms;
     return ms;
