@@ -98,7 +98,7 @@ __device__ __forceinline__ void charge_miss_seg(const SegInfo& sg, uint32_t r, u
     atomicAdd(&sg.counters[8 * lo + 2], (unsigned long long)pages);
 }
 
-template <int VEC, int R>
+template <int VEC, int R, bool STAGED>
 __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_gather_rows(const uint32_t* __restrict__ ids,
                                                                const uint32_t* __restrict__ slots, uint32_t n,
                                                                const uint8_t* __restrict__ cache_rows,
@@ -117,11 +117,11 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_gather_rows
         if (lane < nr) {
             const uint32_t v = __ldg(ids + r0 + lane);
             const uint32_t s = slots ? __ldg(slots + r0 + lane) : kNever;
-            if (s < kStageFlag) {
+            if (STAGED ? s < kStageFlag : s != kNever) {
                 src = cache_rows + (uint64_t)s * row_bytes;
                 if (!sg.off) ++hits;
             } else {  // miss: backing row v, or staged row (s & ~kStageFlag)
-                src = store + (uint64_t)(s == kNever ? v : (s & ~kStageFlag)) * row_bytes;
+                src = store + (uint64_t)(STAGED ? (s == kNever ? v : (s & ~kStageFlag)) : v) * row_bytes;
                 const uint32_t pg =
                     (uint32_t)pages_touched((uint64_t)v * row_bytes, (uint64_t)v * row_bytes + row_bytes);
                 if (sg.off) {
@@ -159,16 +159,19 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_gather_rows
     }
 }
 
+// STAGED: the store is a staging buffer (storage tier / partition exchange)
+// and a miss reads row (slot & ~kStageFlag) of it; otherwise a miss reads row
+// ids[k] of the backing table. Separate instantiations: the extra select on
+// the (cold) miss path measurably slows the all-hit gather when compiled in
+// (4.1 vs 2.9 ms per papers superbatch), so the HBM-backed path never sees it.
+template <bool STAGED>
 __device__ __forceinline__ const uint8_t* gather_src(const uint32_t* ids, const uint32_t* slots, uint32_t r,
                                                      const uint8_t* cache_rows, const uint8_t* store,
                                                      uint32_t row_bytes, uint32_t& hits, uint32_t& misses,
                                                      uint32_t& pages, const SegInfo& sg) {
-    // Both loads are issued up front even though a hit never uses the id:
-    // measured at papers shape, moving the id load onto the miss path makes
-    // the all-hit gather 30% slower (3.9 vs 2.9 ms per superbatch).
     const uint32_t v = __ldg(ids + r);
     const uint32_t s = slots ? __ldg(slots + r) : kNever;
-    if (s < kStageFlag) {
+    if (STAGED ? s < kStageFlag : s != kNever) {
         if (!sg.off) ++hits;
         return cache_rows + (uint64_t)s * row_bytes;
     }
@@ -179,7 +182,7 @@ __device__ __forceinline__ const uint8_t* gather_src(const uint32_t* ids, const 
         ++misses;
         pages += pg;
     }
-    return store + (uint64_t)(s == kNever ? v : (s & ~kStageFlag)) * row_bytes;
+    return store + (uint64_t)(STAGED ? (s == kNever ? v : (s & ~kStageFlag)) : v) * row_bytes;
 }
 
 // TMA variant of the row gather: every thread moves whole rows with the bulk
@@ -191,6 +194,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+template <bool STAGED>
 __global__ void __launch_bounds__(128) k_gather_tma(const uint32_t* __restrict__ ids,
                                                     const uint32_t* __restrict__ slots, uint32_t n,
                                                     const uint8_t* __restrict__ cache_rows,
@@ -207,7 +211,7 @@ __global__ void __launch_bounds__(128) k_gather_tma(const uint32_t* __restrict__
     uint32_t phase = 0;
     uint32_t hits = 0, misses = 0, pages = 0;
     for (uint32_t r = blockIdx.x * blockDim.x + tid; r < n; r += gridDim.x * blockDim.x) {
-        const uint8_t* src = gather_src(ids, slots, r, cache_rows, store, row_bytes, hits, misses, pages, sg);
+        const uint8_t* src = gather_src<STAGED>(ids, slots, r, cache_rows, store, row_bytes, hits, misses, pages, sg);
         // the previous row's store must have finished reading the buffer
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(row_bytes) : "memory");
@@ -258,6 +262,7 @@ __device__ __forceinline__ void bulk_store(void* dst, uint32_t buf, uint32_t byt
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
+template <bool STAGED>
 __global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict__ ids,
                                                      const uint32_t* __restrict__ slots, uint32_t n,
                                                      const uint8_t* __restrict__ cache_rows,
@@ -276,13 +281,13 @@ __global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict_
     const uint32_t step = gridDim.x * blockDim.x;
     uint32_t r = blockIdx.x * blockDim.x + tid;
     uint32_t ph0 = 0, ph1 = 0;
-    if (r < n) bulk_load(buf0, gather_src(ids, slots, r, cache_rows, store, row_bytes, hits, misses, pages, sg), row_bytes, bar0);
+    if (r < n) bulk_load(buf0, gather_src<STAGED>(ids, slots, r, cache_rows, store, row_bytes, hits, misses, pages, sg), row_bytes, bar0);
     for (uint32_t j = 0; r < n; ++j, r += step) {
         const uint32_t nx = r + step;
         const bool odd = j & 1;
         if (nx < n) {  // prefetch the next row into the other buffer
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            bulk_load(odd ? buf0 : buf1, gather_src(ids, slots, nx, cache_rows, store, row_bytes, hits, misses, pages, sg),
+            bulk_load(odd ? buf0 : buf1, gather_src<STAGED>(ids, slots, nx, cache_rows, store, row_bytes, hits, misses, pages, sg),
                       row_bytes, odd ? bar0 : bar1);
         }
         if (odd) {
@@ -334,7 +339,7 @@ __global__ void __launch_bounds__(256) k_gather_ring(const uint32_t* __restrict_
         const uint64_t r = r0 + k * step;
         if (r < n)
             bulk_load(buf_base + k * row_bytes,
-                      gather_src(ids, slots, (uint32_t)r, cache_rows, store, row_bytes, hits, misses, pages, sg),
+                      gather_src<false>(ids, slots, (uint32_t)r, cache_rows, store, row_bytes, hits, misses, pages, sg),
                       row_bytes, bar_base + 8 * k);
     }
     uint32_t b = 0, par = 0;  // buffer of row j, and its barrier parity ((j / D) & 1)
@@ -346,7 +351,7 @@ __global__ void __launch_bounds__(256) k_gather_ring(const uint32_t* __restrict_
         if (rn < n) {
             asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             bulk_load(buf_base + bn * row_bytes,
-                      gather_src(ids, slots, (uint32_t)rn, cache_rows, store, row_bytes, hits, misses, pages, sg),
+                      gather_src<false>(ids, slots, (uint32_t)rn, cache_rows, store, row_bytes, hits, misses, pages, sg),
                       row_bytes, bar_base + 8 * bn);
         }
         if (++b == D) {
@@ -494,26 +499,26 @@ void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t ro
 }
 
 // Launchers shared with the pipeline.
-template <int VEC, int R>
+template <int VEC, int R, bool STAGED = false>
 static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
                                const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
                                unsigned long long* counters, SegInfo sg = {nullptr, 0, nullptr}) {
     static const int bps = [] {
         int b = 0;
-        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gather_rows<VEC, R>, GA_THREADS, 0));
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_gather_rows<VEC, R, STAGED>, GA_THREADS, 0));
         return std::max(b, 1);
     }();
     const uint64_t warps_needed = (n + R - 1) / R;
     const uint64_t blocks_needed = (warps_needed * 32 + GA_THREADS - 1) / GA_THREADS;
     const uint64_t blocks = std::min<uint64_t>(blocks_needed, (uint64_t)ctx->num_sms * bps);
-    k_gather_rows<VEC, R><<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(
+    k_gather_rows<VEC, R, STAGED><<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(
         ids, slots, (uint32_t)n, cache_rows, store, (uint32_t)rb, out, counters, sg);
     GX_CHECK_LAUNCH();
 }
 
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
                             const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
-                            unsigned long long* counters, const uint32_t* seg_off, uint32_t nseg) {
+                            unsigned long long* counters, const uint32_t* seg_off, uint32_t nseg, bool staged) {
     if (!n) return;
     const SegInfo sg{seg_off, seg_off ? nseg : 0u, counters};
     // Variant (tuning knob GX_GATHER_R): 1 = TMA bulk, 2 rows in flight per
@@ -532,7 +537,8 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
     static const int ring = env_int("GX_GATHER_D", 0);  // 3/4/6: k_gather_ring<D> (experimental)
     static std::mutex cfg_mu;  // launch-config caches below are shared by every context / host thread
     std::lock_guard<std::mutex> cfg_lock(cfg_mu);
-    if (vec16(rb) && R == 1 && (ring == 3 || ring == 4 || ring == 6) && (uint64_t)ring * 32 * rb <= (uint64_t)budget) {
+    if (!staged && vec16(rb) && R == 1 && (ring == 3 || ring == 4 || ring == 6) &&
+        (uint64_t)ring * 32 * rb <= (uint64_t)budget) {
         static int tpb = 0, bpsm = 0;
         static uint64_t last = 0;
         auto kfn = ring == 3 ? k_gather_ring<3> : ring == 4 ? k_gather_ring<4> : k_gather_ring<6>;
@@ -555,29 +561,35 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
     }
     const int depth = R == 1 ? 2 : 1;
     if (vec16(rb) && R <= 1 && (uint64_t)depth * 32 * rb <= (uint64_t)budget) {
-        static int tpb[2] = {0, 0}, bps[2] = {0, 0};
-        static uint64_t last_rb[2] = {0, 0};
-        const int d = depth - 1;
+        // launch config per (depth, staged), cached for the last row size
+        static int tpb[4] = {0, 0, 0, 0}, bps[4] = {0, 0, 0, 0};
+        static uint64_t last_rb[4] = {0, 0, 0, 0};
+        const int d = (depth - 1) + 2 * (int)staged;
+        using KFn = void (*)(const uint32_t*, const uint32_t*, uint32_t, const uint8_t*, const uint8_t*, uint32_t,
+                             uint8_t*, unsigned long long*, SegInfo);
+        const KFn kfn = depth == 2 ? (staged ? (KFn)k_gather_tma2<true> : (KFn)k_gather_tma2<false>)
+                                   : (staged ? (KFn)k_gather_tma<true> : (KFn)k_gather_tma<false>);
         if (last_rb[d] != rb) {  // threads per CTA: one (or two) row buffers per thread
-            last_rb[d] = rb;
             tpb[d] = (int)std::min<uint64_t>(128, budget / (depth * rb)) & ~31;
             const int smem = tpb[d] * depth * (int)rb;
-            auto kfn = depth == 2 ? k_gather_tma2 : k_gather_tma;
             GX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[d], kfn, tpb[d], smem));
             bps[d] = std::max(bps[d], 1);
+            last_rb[d] = rb;
         }
         static const int ctas_knob = env_int("GX_GATHER_CTAS", 0);  // cap on CTAs (0 = all resident)
         const uint64_t cap = ctas_knob > 0 ? (uint64_t)ctas_knob : (uint64_t)ctx->num_sms * bps[d];
         const uint64_t blocks = std::min<uint64_t>((n + tpb[d] - 1) / tpb[d], cap);
-        auto kfn = depth == 2 ? k_gather_tma2 : k_gather_tma;
         kfn<<<(unsigned)blocks, tpb[d], (size_t)tpb[d] * depth * rb, lstream(ctx)>>>(
             ids, slots, (uint32_t)n, cache_rows, store, (uint32_t)rb, out, counters, sg);
         GX_CHECK_LAUNCH();
     } else if (vec16(rb)) {
-        if (R == 2) gather_rows_launch<16, 2>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
+        if (staged) gather_rows_launch<16, 4, true>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
+        else if (R == 2) gather_rows_launch<16, 2>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
         else if (R == 8) gather_rows_launch<16, 8>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
         else gather_rows_launch<16, 4>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
+    } else if (staged) {
+        gather_rows_launch<4, 4, true>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
     } else {
         gather_rows_launch<4, 4>(ctx, ids, slots, n, cache_rows, store, rb, out, counters, sg);
     }
@@ -604,7 +616,8 @@ void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* 
         fetch_rows(f, ctx->stage_ids.p, m, ctx->stage_rows.p, lstream(ctx));
         store = ctx->stage_rows.p;
     }
-    launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, store, f->row_bytes, out, counters);
+    launch_gather_resolved(ctx, ids, slots.p, n, cache_rows, store, f->row_bytes, out, counters, nullptr, 0,
+                           staged_backing(f));
 }
 
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos, const uint32_t* in_slot,

@@ -193,12 +193,14 @@ void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* 
                    const uint8_t* cache_rows, gx_features* f, uint8_t* out,
                    unsigned long long* counters);
 // gather with the serving slot of every row already resolved (kNever = miss)
+// staged: `store` is a staging buffer addressed by flagged slots (kStageFlag).
 // seg_off != nullptr: segment mode -- rows of nseg consecutive iterations
 // (absolute offsets seg_off[0..nseg]); misses/pages are charged per iteration
 // into counters[8 * it + 1 / + 2] (executor.cu, SegInfo).
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
                             const uint8_t* cache_rows, const uint8_t* store, uint64_t row_bytes, uint8_t* out,
-                            unsigned long long* counters, const uint32_t* seg_off = nullptr, uint32_t nseg = 0);
+                            unsigned long long* counters, const uint32_t* seg_off = nullptr, uint32_t nseg = 0,
+                            bool staged = false);
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos,
                         const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
                         uint32_t n_out, int32_t* table, const uint8_t* batch, uint8_t* cache_rows,
