@@ -565,7 +565,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg], B));
                 launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], sl.o[e + 1] - sl.o[i],
                                        p->cache_rows.p, store, rb, rows_of(i), sl.counters.p + 8 * i,
-                                       sl.d_off.p + i, (uint32_t)(e - i + 1), file);
+                                       sl.d_off.p + i, (uint32_t)(e - i + 1), file && n_miss > 0);
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg + 1], B));
                 if (p->digest)
                     for (uint64_t k = i; k <= e; ++k)
