@@ -354,12 +354,15 @@ struct RowMatrix {
     std::span<const float> row(std::size_t k) const { return {data.data() + k * dim, dim}; }
 };
 
-// graph_store.hpp:280-333 (payload in HBM)
+// graph_store.hpp:280-333. Default: payload loaded into HBM. GX_BACKING_FILE
+// keeps the reference's storage model (rows stay in features.bin; misses are
+// read with O_DIRECT page runs into pinned staging, the SSD tier);
+// GX_BACKING_HOST keeps them in pinned host memory.
 class FeatureFile {
 public:
-    static FeatureFile open(const std::filesystem::path& path) {
+    static FeatureFile open(const std::filesystem::path& path, int backing = GX_BACKING_DEVICE) {
         gx_features* f = nullptr;
-        check(gx_features_open(context(), path.string().c_str(), GX_BACKING_DEVICE, &f));
+        check(gx_features_open(context(), path.string().c_str(), backing, &f));
         return FeatureFile(f);
     }
     std::uint64_t num_nodes() const { return gx_features_num_nodes(f_.get()); }
