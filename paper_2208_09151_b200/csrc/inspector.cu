@@ -366,19 +366,29 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     bool have_next = false;
     if (a.trusted) {
         // sampler-produced trace: ids < N and distinct per iteration by
-        // construction; first occurrences by one atomicMin pass
-        for (uint32_t x = gtid; x < a.A; x += G) atomicMin(&a.last[a.trace[x]], iter_of(sm, S, x));
+        // construction; first occurrences by one atomicMin pass over access
+        // indices (the trace is iteration-major, so the smallest access index
+        // of a node is its first iteration's access). Each access keeps its
+        // node's first access index (next_use doubles as that array until the
+        // next-use pass, which the all-fit path never runs).
+        for (uint32_t x = gtid; x < a.A; x += G) atomicMin(&a.last[a.trace[x]], x);
         grid_sync(a.bar);
         ISTAMP(a, 1);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
             const uint32_t x0 = t * IN_TILE + tid * 4;
+            uint32_t v[4], fx[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = x0 + j < a.A ? a.trace[x0 + j] : 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) fx[j] = x0 + j < a.A ? a.last[v[j]] : 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t x = x0 + j;
                 if (x < a.A) {
-                    const uint8_t f = a.last[a.trace[x]] == iter_of(sm, S, x);
+                    const uint8_t f = fx[j] == x;
                     a.isfirst[x] = f;
+                    a.next_use[x] = fx[j];
                     c += f;
                 }
             }
@@ -387,8 +397,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
         ISTAMP(a, 2);
-        // `last` is cleaned (or, all-fit, reused as the node -> slot map) by the
-        // init pass below, which visits every first occurrence exactly once
+        // `last` is cleaned by the init pass below, which visits every first
+        // occurrence exactly once
     } else {
         if (!next_use_pass(a, sm, true)) return;
         have_next = true;
@@ -414,8 +424,9 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
         ISTAMP(a, 3);
-        // all-fit on a trusted trace: `last` (first iteration per node) becomes the
-        // node -> slot map, so node_slot is never touched; otherwise clean `last`
+        // all-fit on a trusted trace: a first occurrence's slot goes straight to
+        // its access (acc_slot), the other accesses copy it from there below,
+        // and node_slot is never touched
         const bool fit = a.trusted && *(volatile uint32_t*)&a.st->n_first <= K;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t fl[4], c = 0;
@@ -437,12 +448,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                         const uint32_t it = iter_of(sm, S, x);
                         a.slot_node[r] = v;
                         a.slot_key[r] = it;
-                        if (fit) a.last[v] = r;
+                        if (fit) a.acc_slot[x] = r;
                         else a.node_slot[v] = (int32_t)r;
                         a.o_init[r] = v;
                         atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                     }
-                    if (a.trusted && !fit) a.last[v] = kNever;
+                    if (a.trusted) a.last[v] = kNever;  // leave clean
                     ++r;
                 }
             }
@@ -485,9 +496,18 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     // served by its init slot.
     const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
     if (allfit) {
-        // node -> slot map: `last` on the trusted path (see the init pass), else node_slot
-        uint32_t* const slot_of = a.trusted ? a.last : reinterpret_cast<uint32_t*>(a.node_slot);
-        for (uint32_t x = gtid; x < a.A; x += G) a.acc_slot[x] = slot_of[a.trace[x]];
+        if (a.trusted) {
+            // the first occurrence of each access's node already holds the slot
+            // (init pass); the lookups stay inside the A-sized acc_slot array
+            // instead of the N-sized node arrays
+            for (uint32_t x = gtid; x < a.A; x += G) {
+                const uint32_t fx = a.next_use[x];
+                if (fx != x) a.acc_slot[x] = a.acc_slot[fx];
+            }
+        } else {
+            const int32_t* const slot_of = a.node_slot;
+            for (uint32_t x = gtid; x < a.A; x += G) a.acc_slot[x] = (uint32_t)slot_of[a.trace[x]];
+        }
         for (uint32_t i = gtid; i < S; i += G) {
             a.o_misses[i] = 0;
             a.o_in_off[i + 1] = 0;
@@ -495,8 +515,10 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         grid_sync(a.bar);
         ISTAMP(a, 5);
-        const uint32_t n0 = a.st->n_res;
-        for (uint32_t s = gtid; s < n0; s += G) slot_of[a.slot_node[s]] = kNever;  // == -1: clean either map
+        if (!a.trusted) {
+            const uint32_t n0 = a.st->n_res;
+            for (uint32_t s = gtid; s < n0; s += G) a.node_slot[a.slot_node[s]] = -1;  // leave clean
+        }
         return;
     }
     if (!have_next) next_use_pass(a, sm, false);

@@ -34,9 +34,21 @@ namespace gx {
 
 constexpr int kMaxLayers = 16;
 constexpr int SB_THREADS = 512;
-constexpr int SB_IPT = 2;
+#ifndef GX_SB_IPT
+#define GX_SB_IPT 2
+#endif
+constexpr int SB_IPT = GX_SB_IPT;
 #ifndef GX_E_UNROLL
 #define GX_E_UNROLL 4
+#endif
+#ifndef GX_TABLE_SLACK  // table slots >= entry bound << SLACK (1: load <= 1/2)
+#define GX_TABLE_SLACK 1
+#endif
+#ifndef GX_TABLE_BY_DRAWS
+#define GX_TABLE_BY_DRAWS 0
+#endif
+#ifndef GX_I_UNROLL
+#define GX_I_UNROLL 4
 #endif
 #ifndef GX_E_LOADFIRST
 #define GX_E_LOADFIRST 1
@@ -47,6 +59,13 @@ constexpr int SB_IPT = 2;
 #define GX_SB_BOUNDS __launch_bounds__(SB_THREADS)
 #endif
 constexpr uint32_t SB_TILE = SB_THREADS * SB_IPT;
+// draws per thread in the per-draw tile phases F and H (more independent
+// loads in flight per thread than the per-parent tiles of A/E)
+#ifndef GX_SB_DIPT
+#define GX_SB_DIPT 4
+#endif
+constexpr int SB_DIPT = GX_SB_DIPT;
+constexpr uint32_t SB_DTILE = SB_THREADS * SB_DIPT;
 constexpr uint32_t kNewBit = 0x80000000u;
 constexpr unsigned long long kEmptySlot = ~0ull;
 constexpr uint32_t kMaxBatchesPerLaunch = 4096;
@@ -133,12 +152,13 @@ __device__ __forceinline__ uint32_t prefix_batch(const SampSmem& sm, uint32_t S,
     return lo;
 }
 
-// tp[0..S] = prefix of ceil(cnt[b] / SB_TILE); returns total tiles.
+// tp[0..S] = prefix of ceil(cnt[b] / TILE); returns total tiles.
+template <uint32_t TILE = SB_TILE>
 __device__ uint32_t build_tiles(const uint32_t* cnt, uint32_t S, SampSmem& sm) {
     uint32_t carry = 0;
     for (uint32_t base = 0; base < S; base += blockDim.x) {
         uint32_t b = base + threadIdx.x;
-        uint32_t v = b < S ? (cnt[b] + SB_TILE - 1) / SB_TILE : 0;
+        uint32_t v = b < S ? (cnt[b] + TILE - 1) / TILE : 0;
         uint32_t tot;
         uint32_t ex = block_excl_scan(v, sm.scan, tot);
         if (b < S) sm.tp[b] = carry + ex;
@@ -311,13 +331,25 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 
     for (uint32_t l = 0; l < a.L || l == 0; ++l) {
         // ---- Phase D: (re)build the per-batch tables with the current ids --
-        // H = nextpow2(2 * max_b F_b * (1 + f_l)) bounds the table load <= 1/2.
+        // H = nextpow2(2 * max_b(entries bound)) keeps the load <= 1/2.
+        auto phase_d = [&](bool by_draws) {
         uint32_t newH;
         {
             unsigned long long mx = 0;
+            // entries the layer's table can hold: the ids so far plus at most
+            // one per draw -- after phase A the draw count T_b is known (tile
+            // sums of takes), before it (layer 0) bound it by F_b * f
+            if (by_draws) build_tiles(a.F, S, sm);
             for (uint32_t b = tid; b < S; b += blockDim.x) {
                 unsigned long long fb = l == 0 ? (a.seed_off[b + 1] - a.seed_off[b]) : a.F[b];
-                unsigned long long need = fb * (1ull + (a.L ? a.fan[l] : 0));
+                unsigned long long need;
+                if (by_draws) {
+                    unsigned long long tb = 0;
+                    for (uint32_t i = sm.tp[b]; i < sm.tp[b + 1]; ++i) tb += a.tsum[i];
+                    need = fb + tb;
+                } else {
+                    need = fb * (1ull + (a.L ? a.fan[l] : 0));
+                }
                 mx = max(mx, need);
             }
             // block max via the scan buffer
@@ -329,7 +361,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = max(m, sm.red[w]);
                 m = m < a.cap_ids ? m : (unsigned long long)a.cap_ids;
                 unsigned long long h = 1024;
-                while (h < 2 * m) h <<= 1;
+                while (h < (m << GX_TABLE_SLACK)) h <<= 1;
                 if (h > a.tab_cap) h = a.tab_cap;
                 sm.red[32] = h;
             }
@@ -372,8 +404,13 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
             grid_sync(a.bar);
             TRACE_STAMP(a, l, 0);
         }
+        };
+        // GX_TABLE_BY_DRAWS=1 sizes layers >= 1 by the actual draw count (phase A
+        // first): tables about half as large, but measured slower at papers shape
+        // (phase E 1.22 vs 1.11 ms: the higher load costs more probes than the
+        // smaller footprint saves), so the default sizes by F_b * (1 + f).
+        if (l == 0 || !GX_TABLE_BY_DRAWS) phase_d(false);
         if (a.L == 0) break;
-        unsigned long long* tab = cur ? a.tab1 : a.tab0;
         const uint32_t f = a.fan[l];
 
         // ---- Phase A: per parent deg/take, IoStats, tile sums of takes ----
@@ -417,6 +454,9 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
         }
         grid_sync(a.bar);
         TRACE_STAMP(a, l, 1);
+
+        if (l > 0 && GX_TABLE_BY_DRAWS) phase_d(true);
+        unsigned long long* tab = cur ? a.tab1 : a.tab0;
 
         // ---- Phase E: scan takes -> draw offsets; draw, read child, insert ----
         {
@@ -560,16 +600,16 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 
         // ---- Phase F: first-occurrence flags per draw, tile sums ----------
         {
-            uint32_t ntiles = build_tiles(a.T, S, sm);
+            uint32_t ntiles = build_tiles<SB_DTILE>(a.T, S, sm);
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const uint32_t b = tile_batch(sm, S, t);
                 const uint32_t Tb = a.T[b];
-                const uint32_t p0 = (t - sm.tp[b]) * SB_TILE + tid * SB_IPT;
+                const uint32_t p0 = (t - sm.tp[b]) * SB_DTILE + tid * SB_DIPT;
                 const unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
                 const uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
                 uint32_t s = 0;
 #pragma unroll
-                for (int j = 0; j < SB_IPT; ++j) {
+                for (int j = 0; j < SB_DIPT; ++j) {
                     const uint32_t p = p0 + j;
                     if (p < Tb) {
                         const uint64_t gd = (uint64_t)b * a.cap_draw + p;
@@ -593,7 +633,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 
         // ---- Phase H: rank winners by draw position -> new local ids -------
         {
-            uint32_t ntiles = build_tiles(a.T, S, sm);
+            uint32_t ntiles = build_tiles<SB_DTILE>(a.T, S, sm);
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const uint32_t b = tile_batch(sm, S, t);
                 const uint32_t Tb = a.T[b];
@@ -606,11 +646,11 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                     s2 = warp_sum(s2);
                     if (tid == 0) a.n_ids[b] = Fb + s2;
                 }
-                const uint32_t p0 = (t - first) * SB_TILE + tid * SB_IPT;
-                uint32_t fl[SB_IPT];
+                const uint32_t p0 = (t - first) * SB_DTILE + tid * SB_DIPT;
+                uint32_t fl[SB_DIPT];
                 uint32_t s = 0;
 #pragma unroll
-                for (int j = 0; j < SB_IPT; ++j) {
+                for (int j = 0; j < SB_DIPT; ++j) {
                     const uint32_t p = p0 + j;
                     fl[j] = p < Tb ? a.drank[(uint64_t)b * a.cap_draw + p] : 0;
                     s += fl[j];
@@ -621,7 +661,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 uint2* bedge_w = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
                 const uint2* bedge = bedge_w;
 #pragma unroll
-                for (int j = 0; j < SB_IPT; ++j) {
+                for (int j = 0; j < SB_DIPT; ++j) {
                     if (fl[j]) {
                         const uint32_t p = p0 + j;
                         const uint32_t child = bedge[p].x;
@@ -642,15 +682,35 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
         {
             const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
             const uint32_t tot = build_prefix(a.T, nullptr, S, sm);
-            for (uint32_t x = blockIdx.x * blockDim.x + tid; x < tot; x += (uint32_t)total_threads) {
-                const uint32_t b = prefix_batch(sm, S, x);
-                const uint32_t p = x - sm.px[b];
-                const uint64_t gd = (uint64_t)b * a.cap_draw + p;
-                const uint32_t ds = a.dslot[gd];
-                // resolved at insert time or written by the winner: nothing to do
-                if (!(ds & kResolved) && !a.drank[gd])
-                    a.edges[(uint64_t)b * a.cap_e_batch + a.e_off[l] + p].x =
-                        (uint32_t)tab[(uint64_t)b * a.tab_cap + ds];
+            // IU draws per thread in flight: their slot/flag loads, then their
+            // table reads, then the stores (the chain is latency-bound otherwise)
+            constexpr int IU = GX_I_UNROLL;
+            const uint32_t T_all = (uint32_t)total_threads;
+            for (uint32_t x0 = blockIdx.x * blockDim.x + tid; x0 < tot; x0 += IU * T_all) {
+                uint64_t gd[IU], tb[IU], eo[IU];
+                uint32_t ds[IU], rk[IU];
+#pragma unroll
+                for (int j = 0; j < IU; ++j) {
+                    const uint32_t x = x0 + j * T_all;
+                    ds[j] = kResolved;
+                    rk[j] = 1;
+                    if (x < tot) {
+                        const uint32_t b = prefix_batch(sm, S, x);
+                        const uint32_t p = x - sm.px[b];
+                        gd[j] = (uint64_t)b * a.cap_draw + p;
+                        tb[j] = (uint64_t)b * a.tab_cap;
+                        eo[j] = (uint64_t)b * a.cap_e_batch + a.e_off[l] + p;
+                        ds[j] = a.dslot[gd[j]];
+                        rk[j] = a.drank[gd[j]];
+                    }
+                }
+                uint32_t val[IU];
+#pragma unroll
+                for (int j = 0; j < IU; ++j)  // resolved at insert time or a winner: nothing to do
+                    if (!(ds[j] & kResolved) && !rk[j]) val[j] = (uint32_t)tab[tb[j] + ds[j]];
+#pragma unroll
+                for (int j = 0; j < IU; ++j)
+                    if (!(ds[j] & kResolved) && !rk[j]) a.edges[eo[j]].x = val[j];
             }
             for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
                 a.layer_count[(uint64_t)b * a.L + l] = a.T[b];
