@@ -479,9 +479,15 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         for (uint64_t i = 0; i < S; ++i) sl.o[i + 1] = sl.o[i] + p->samples.h_n_ids[i];
         std::swap(ctx->is.trace, sl.trace);
         std::swap(ctx->is.acc_slot, sl.acc_slot);
+        // all-fit superbatches fuse the cache fill with the first uses when the
+        // whole superbatch is resident in HBM and the backing table is too
+        const uint64_t rb = p->f->row_bytes;
+        static const uint64_t budget = (uint64_t)std::max(0, gx::env_int("GX_BATCH_BUDGET_MB", 24576)) << 20;
+        const bool resident = sl.o[S] * rb <= budget;
+        const bool mark = resident && !staged_backing(p->f) && p->f->rows_dev_view && gather_can_skip_first(rb);
         try {
             inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, sl.o);
-            inspect_run(ctx, sl.o, N, p->K, nullptr, -1, &sl.cs, true);
+            inspect_run(ctx, sl.o, N, p->K, nullptr, -1, &sl.cs, true, mark);
         } catch (...) {
             std::swap(ctx->is.trace, sl.trace);
             std::swap(ctx->is.acc_slot, sl.acc_slot);
@@ -498,10 +504,9 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         GX_CUDA(cudaEventRecord(sl.ev[3], B));
         uint64_t maxw = 0;
         for (uint64_t i = 0; i < S; ++i) maxw = std::max(maxw, sl.o[i + 1] - sl.o[i]);
-        const uint64_t rb = p->f->row_bytes;
         // whole superbatch resident when it fits the per-slot budget (GX_BATCH_BUDGET_MB)
-        static const uint64_t budget = (uint64_t)std::max(0, gx::env_int("GX_BATCH_BUDGET_MB", 24576)) << 20;
-        sl.full = sl.o[S] * rb <= budget;
+        sl.full = resident;
+        const bool fused = sl.cs.first_marked;  // implies all-fit (no changesets) and resident
         sl.batch.reserve(std::max<uint64_t>((sl.full ? sl.o[S] : maxw) * rb, 16));
         sl.h_off.reserve(S + 1);
         sl.d_off.reserve(S + 1);
@@ -543,6 +548,12 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 store = sl.stage.p;
                 sl.storage_rows = (f_file ? p->f->file->rows.load() : p->f->xstats.rows_requested) - r0;
                 sl.storage_bytes = (f_file ? p->f->file->bytes.load() : p->f->xstats.bytes_sent) - b0;
+            } else if (fused) {
+                // the switch fused with every init node's first use: one read of
+                // the backing row, written to its slot and to its first batch row
+                launch_fill_first(ctx, sl.cs.init.p, sl.cs.first_acc.p, (uint32_t)sl.cs.n_init, p->f->rows_dev_view,
+                                  rb, p->cache_rows.p, sl.batch.p);
+                GX_CUDA(cudaEventRecord(sl.ev[4], B));
             } else {
                 launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
                                   sl.counters.p + 8 * S);
@@ -558,14 +569,24 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             };
             auto rows_of = [&](uint64_t i) { return sl.batch.p + (sl.full ? sl.o[i] * rb : 0); };
             uint64_t nseg = 0;
-            for (uint64_t i = 0; i < S;) {
+            if (fused) {  // one launch: every access that is not a first use
+                GX_CUDA(cudaEventRecord(sl.kev[0], B));
+                launch_gather_resolved(ctx, sl.cs.rest_x.p, sl.cs.rest_slot.p, sl.cs.n_rest, p->cache_rows.p,
+                                       store, rb, sl.batch.p, sl.counters.p + 8 * S, nullptr, 0, false, true);
+                GX_CUDA(cudaEventRecord(sl.kev[1], B));
+                if (p->digest)
+                    for (uint64_t k = 0; k < S; ++k)
+                        launch_digest(ctx, rows_of(k), sl.o[k + 1] - sl.o[k], rb, sl.digests.p + k);
+                GX_CUDA(cudaEventRecord(sl.kev[2], B));
+            }
+            for (uint64_t i = fused ? S : 0; i < S;) {
                 uint64_t e = i;  // segment [i, e]
                 if (sl.full)
                     while (e + 1 < S && empty_cs(e)) ++e;
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg], B));
                 launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], sl.o[e + 1] - sl.o[i],
                                        p->cache_rows.p, store, rb, rows_of(i), sl.counters.p + 8 * i,
-                                       sl.d_off.p + i, (uint32_t)(e - i + 1), file && n_miss > 0);
+                                       sl.d_off.p + i, (uint32_t)(e - i + 1), file && n_miss > 0, fused);
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg + 1], B));
                 if (p->digest)
                     for (uint64_t k = i; k <= e; ++k)
@@ -581,7 +602,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 ++nseg;
                 i = e + 1;
             }
-            sl.nseg = nseg;
+            sl.nseg = fused ? 1 : nseg;
         } catch (...) {
             ctx->launch_stream = nullptr;
             throw;

@@ -262,7 +262,9 @@ __device__ __forceinline__ void bulk_store(void* dst, uint32_t buf, uint32_t byt
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
-template <bool STAGED>
+// DSTIDX: row k goes to batch row ids[k] (the fused all-fit gather: a dense
+// list of the accesses that are not an init node's first use).
+template <bool STAGED, bool DSTIDX = false>
 __global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict__ ids,
                                                      const uint32_t* __restrict__ slots, uint32_t n,
                                                      const uint8_t* __restrict__ cache_rows,
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict_
     uint32_t r = blockIdx.x * blockDim.x + tid;
     uint32_t ph0 = 0, ph1 = 0;
     if (r < n) bulk_load(buf0, gather_src<STAGED>(ids, slots, r, cache_rows, store, row_bytes, hits, misses, pages, sg), row_bytes, bar0);
-    for (uint32_t j = 0; r < n; ++j, r += step) {
+    for (uint32_t j = 0; r < n; ++j) {
         const uint32_t nx = r + step;
         const bool odd = j & 1;
         if (nx < n) {  // prefetch the next row into the other buffer
@@ -290,15 +292,17 @@ __global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict_
             bulk_load(odd ? buf0 : buf1, gather_src<STAGED>(ids, slots, nx, cache_rows, store, row_bytes, hits, misses, pages, sg),
                       row_bytes, odd ? bar0 : bar1);
         }
+        const uint64_t dr = DSTIDX ? (uint64_t)__ldg(ids + r) : (uint64_t)r;
         if (odd) {
             bar_wait(bar1, ph1);
             ph1 ^= 1;
-            bulk_store(out + (uint64_t)r * row_bytes, buf1, row_bytes);
+            bulk_store(out + dr * row_bytes, buf1, row_bytes);
         } else {
             bar_wait(bar0, ph0);
             ph0 ^= 1;
-            bulk_store(out + (uint64_t)r * row_bytes, buf0, row_bytes);
+            bulk_store(out + dr * row_bytes, buf0, row_bytes);
         }
+        r = nx;
     }
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     hits = warp_sum(hits);
@@ -370,6 +374,135 @@ __global__ void __launch_bounds__(256) k_gather_ring(const uint32_t* __restrict_
         atomicAdd(&counters[3], (unsigned long long)misses);
         atomicAdd(&counters[4], (unsigned long long)misses * row_bytes);
     }
+}
+
+// Fused cache fill for an all-fit superbatch (the "switch" and the first use of
+// every init node in one pass): init slot r <- backing row init[r], and the
+// same bytes to the batch row of the slot's first use, first_acc[r]. R rows
+// in flight per warp, 16-byte loads, two 16-byte stores per load.
+template <int R>
+__global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fill_first(const uint32_t* __restrict__ init,
+                                                               const uint32_t* __restrict__ first_acc, uint32_t n,
+                                                               const uint8_t* __restrict__ store, uint32_t row_bytes,
+                                                               uint8_t* __restrict__ cache_rows,
+                                                               uint8_t* __restrict__ batch) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t nvec = row_bytes / 16;
+    for (uint32_t r0 = warp * R; r0 < n; r0 += nwarps * R) {
+        const uint32_t nr = min(n - r0, (uint32_t)R);
+        const uint8_t* src = nullptr;
+        uint8_t* dst2 = nullptr;
+        if (lane < nr) {
+            src = store + (uint64_t)__ldg(init + r0 + lane) * row_bytes;
+            dst2 = batch + (uint64_t)__ldg(first_acc + r0 + lane) * row_bytes;
+        }
+        uint4* dst1 = reinterpret_cast<uint4*>(cache_rows + (uint64_t)r0 * row_bytes);
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < nvec; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            uint4 tmp[R];
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const uint4* sq = reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, (unsigned long long)src, q));
+                if (q < (int)nr && c < nvec) tmp[q] = ld_nc(sq + c);
+            }
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                uint4* dq = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, (unsigned long long)dst2, q));
+                if (q < (int)nr && c < nvec) {
+                    st_na(dst1 + q * nvec + c, tmp[q]);
+                    st_na(dq + c, tmp[q]);
+                }
+            }
+        }
+    }
+}
+
+static int gather_smem_budget();
+
+// Bulk-copy form of the fused fill: each thread moves whole rows through its
+// own two smem buffers (load of row j+1 in flight while row j is stored), and
+// every row is stored twice from the same buffer (cache slot, batch row).
+__global__ void __launch_bounds__(128) k_fill_first_tma(const uint32_t* __restrict__ init,
+                                                        const uint32_t* __restrict__ first_acc, uint32_t n,
+                                                        const uint8_t* __restrict__ store, uint32_t row_bytes,
+                                                        uint8_t* __restrict__ cache_rows, uint8_t* __restrict__ batch) {
+    extern __shared__ __align__(128) unsigned char sbuf[];
+    __shared__ __align__(8) unsigned long long bars[2 * 128];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t bar0 = smem_u32(&bars[2 * tid]), bar1 = bar0 + 8;
+    const uint32_t buf0 = smem_u32(sbuf + (size_t)(2 * tid) * row_bytes), buf1 = buf0 + row_bytes;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    const uint32_t step = gridDim.x * blockDim.x;
+    uint32_t r = blockIdx.x * blockDim.x + tid;
+    uint32_t ph0 = 0, ph1 = 0;
+    if (r < n) bulk_load(buf0, store + (uint64_t)__ldg(init + r) * row_bytes, row_bytes, bar0);
+    for (uint32_t j = 0; r < n; ++j, r += step) {
+        const uint32_t nx = r + step;
+        const bool odd = j & 1;
+        if (nx < n) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            bulk_load(odd ? buf0 : buf1, store + (uint64_t)__ldg(init + nx) * row_bytes, row_bytes, odd ? bar0 : bar1);
+        }
+        const uint64_t x = __ldg(first_acc + r);
+        const uint32_t buf = odd ? buf1 : buf0;
+        if (odd) {
+            bar_wait(bar1, ph1);
+            ph1 ^= 1;
+        } else {
+            bar_wait(bar0, ph0);
+            ph0 ^= 1;
+        }
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(cache_rows + (uint64_t)r * row_bytes),
+                     "r"(buf), "r"(row_bytes) : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(batch + x * row_bytes),
+                     "r"(buf), "r"(row_bytes) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_acc, uint32_t n,
+                       const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch) {
+    if (!n) return;
+    if (rb % 16) fail(GX_INVALID_ARGUMENT, "fused fill needs 16-byte rows");
+    static const int tma = env_int("GX_FILL_TMA", 0);  // bulk-copy form: 1.85 vs 1.67 ms (LDG/STG) at papers shape
+    if (tma && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget()) {
+        static int tpb = 0, bpsm = 0;
+        static uint64_t last = 0;
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lk(mu);
+        if (last != rb) {
+            tpb = (int)std::min<uint64_t>(128, gather_smem_budget() / (2 * rb)) & ~31;
+            const int smem = tpb * 2 * (int)rb;
+            GX_CUDA(cudaFuncSetAttribute(k_fill_first_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_fill_first_tma, tpb, smem));
+            bpsm = std::max(bpsm, 1);
+            last = rb;
+        }
+        const uint64_t blocks = std::min<uint64_t>((n + tpb - 1) / tpb, (uint64_t)ctx->num_sms * bpsm);
+        k_fill_first_tma<<<(unsigned)blocks, tpb, (size_t)tpb * 2 * rb, lstream(ctx)>>>(init, first_acc, n, store,
+                                                                                      (uint32_t)rb, cache_rows, batch);
+        GX_CHECK_LAUNCH();
+        return;
+    }
+    constexpr int R = 8;
+    static const int bps = [] {
+        int b = 0;
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fill_first<R>, GA_THREADS, 0));
+        return std::max(b, 1);
+    }();
+    const uint64_t warps_needed = (n + R - 1) / R;
+    const uint64_t blocks = std::min<uint64_t>((warps_needed * 32 + GA_THREADS - 1) / GA_THREADS,
+                                               (uint64_t)ctx->num_sms * bps);
+    k_fill_first<R><<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(init, first_acc, n, store, (uint32_t)rb,
+                                                                      cache_rows, batch);
+    GX_CHECK_LAUNCH();
 }
 
 // Address-table resolution for the API path: slots[k] = table[ids[k]] (or kNever).
@@ -516,24 +649,41 @@ static void gather_rows_launch(gx_ctx* ctx, const uint32_t* ids, const uint32_t*
     GX_CHECK_LAUNCH();
 }
 
-void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
-                            const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
-                            unsigned long long* counters, const uint32_t* seg_off, uint32_t nseg, bool staged) {
-    if (!n) return;
-    const SegInfo sg{seg_off, seg_off ? nseg : 0u, counters};
-    // Variant (tuning knob GX_GATHER_R): 1 = TMA bulk, 2 rows in flight per
-    // thread (default); 0 = TMA bulk, 1 row per thread; 2/4/8 = LDG/STG with
-    // that many rows per warp. TMA needs 16-byte rows whose buffers fit smem.
+static int gather_variant() {
     static const int R = [] {
         const char* e = std::getenv("GX_GATHER_R");
         const int r = e ? std::atoi(e) : 1;
         return (r == 0 || r == 1 || r == 2 || r == 4 || r == 8) ? r : 1;
     }();
+    return R;
+}
+static int gather_smem_budget() {
     static const int budget = [] {  // shared memory per CTA for row buffers (KB)
         const char* e = std::getenv("GX_GATHER_SMEM_KB");
         const int kb = e ? std::atoi(e) : 96;
         return std::min(std::max(kb, 16), 200) * 1024;
     }();
+    return budget;
+}
+
+// the pipeline may fuse the fill with the first uses only when the gather that
+// will serve the rest is the bulk-copy kernel (its DSTIDX instantiation)
+bool gather_can_skip_first(uint64_t rb) {
+    static const bool on = env_int("GX_FUSED_FILL", 1) != 0;
+    return on && vec16(rb) && gather_variant() == 1 && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget();
+}
+
+void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
+                            const uint8_t* cache_rows, const uint8_t* store, uint64_t rb, uint8_t* out,
+                            unsigned long long* counters, const uint32_t* seg_off, uint32_t nseg, bool staged,
+                            bool skip_first) {
+    if (!n) return;
+    const SegInfo sg{seg_off, seg_off ? nseg : 0u, counters};
+    // Variant (tuning knob GX_GATHER_R): 1 = TMA bulk, 2 rows in flight per
+    // thread (default); 0 = TMA bulk, 1 row per thread; 2/4/8 = LDG/STG with
+    // that many rows per warp. TMA needs 16-byte rows whose buffers fit smem.
+    const int R = gather_variant();
+    const int budget = gather_smem_budget();
     static const int ring = env_int("GX_GATHER_D", 0);  // 3/4/6: k_gather_ring<D> (experimental)
     static std::mutex cfg_mu;  // launch-config caches below are shared by every context / host thread
     std::lock_guard<std::mutex> cfg_lock(cfg_mu);
@@ -560,15 +710,19 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         return;
     }
     const int depth = R == 1 ? 2 : 1;
+    if (skip_first && (staged || !gather_can_skip_first(rb)))
+        fail(GX_LOGIC_ERROR, "the fused all-fit gather needs the bulk-copy kernel");
     if (vec16(rb) && R <= 1 && (uint64_t)depth * 32 * rb <= (uint64_t)budget) {
         // launch config per (depth, staged), cached for the last row size
-        static int tpb[4] = {0, 0, 0, 0}, bps[4] = {0, 0, 0, 0};
-        static uint64_t last_rb[4] = {0, 0, 0, 0};
-        const int d = (depth - 1) + 2 * (int)staged;
+        static int tpb[6] = {0, 0, 0, 0, 0, 0}, bps[6] = {0, 0, 0, 0, 0, 0};
+        static uint64_t last_rb[6] = {0, 0, 0, 0, 0, 0};
+        const bool skip = skip_first && depth == 2 && !staged;
+        const int d = skip ? 4 : (depth - 1) + 2 * (int)staged;
         using KFn = void (*)(const uint32_t*, const uint32_t*, uint32_t, const uint8_t*, const uint8_t*, uint32_t,
                              uint8_t*, unsigned long long*, SegInfo);
-        const KFn kfn = depth == 2 ? (staged ? (KFn)k_gather_tma2<true> : (KFn)k_gather_tma2<false>)
-                                   : (staged ? (KFn)k_gather_tma<true> : (KFn)k_gather_tma<false>);
+        const KFn kfn = skip ? (KFn)k_gather_tma2<false, true>
+                        : depth == 2 ? (staged ? (KFn)k_gather_tma2<true> : (KFn)k_gather_tma2<false>)
+                                     : (staged ? (KFn)k_gather_tma<true> : (KFn)k_gather_tma<false>);
         if (last_rb[d] != rb) {  // threads per CTA: one (or two) row buffers per thread
             tpb[d] = (int)std::min<uint64_t>(128, budget / (depth * rb)) & ~31;
             const int smem = tpb[d] * depth * (int)rb;

@@ -137,6 +137,10 @@ struct gx_changesets {
     gx::DevBuf<uint32_t> in_pos;
     gx::DevBuf<uint32_t> in_slot;   // FeatureCache slot each insertion lands in
     gx::DevBuf<uint32_t> out_ids;   // total out (sorted per iteration)
+    gx::DevBuf<uint32_t> first_acc; // all-fit: access index of each init slot's first use
+    gx::DevBuf<uint32_t> rest_x, rest_slot;  // all-fit: the other accesses and their slots
+    uint64_t n_rest = 0;
+    bool first_marked = false;      // first_acc / rest_* valid (pipeline only)
     std::vector<uint64_t> h_in_off, h_out_off, h_misses;  // S+1, S+1, S
 };
 
@@ -184,7 +188,8 @@ void inspect_fill_from_host(gx_ctx* ctx, const uint64_t* flat, const std::vector
                             uint64_t N);
 // trusted: the trace comes from the sampler (ids < N, distinct per iteration)
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
-                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted);
+                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
+                 bool mark_first = false);
 void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t* h_iters,
                       uint64_t* h_ptr);
 
@@ -200,7 +205,7 @@ void launch_gather(gx_ctx* ctx, const uint32_t* ids, uint64_t n, const int32_t* 
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
                             const uint8_t* cache_rows, const uint8_t* store, uint64_t row_bytes, uint8_t* out,
                             unsigned long long* counters, const uint32_t* seg_off = nullptr, uint32_t nseg = 0,
-                            bool staged = false);
+                            bool staged = false, bool skip_first = false);
 void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_pos,
                         const uint32_t* in_slot, uint32_t n_in, const uint32_t* out_ids,
                         uint32_t n_out, int32_t* table, const uint8_t* batch, uint8_t* cache_rows,
@@ -216,6 +221,14 @@ void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t ro
 // is a miss whose row was staged: the gather reads row (slot & ~kStageFlag)
 // of the store pointer it is given and charges the miss to ids[k] as usual.
 constexpr uint32_t kStageFlag = 0x80000000u;
+// All-fit pipeline superbatches: the fused fill (launch_fill_first) serves the
+// first use of every init slot; the other accesses come as a dense list
+// (rest_x: batch row, rest_slot: cache slot) served by the gather's DSTIDX form
+// (skip_first = true: ids = rest_x, slots = rest_slot).
+constexpr uint32_t kFirstFlag = 0x40000000u;  // inspector-internal mark of a first use
+void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_acc, uint32_t n,
+                       const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch);
+bool gather_can_skip_first(uint64_t rb);
 // d_out row j <- feature row d_ids[j] from storage, for j in [0, n). Sorts the
 // requests by id on `s`, reads page runs on the host into pinned chunks,
 // copies them to HBM on the features' copy stream and scatters them to their

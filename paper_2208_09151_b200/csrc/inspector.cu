@@ -88,6 +88,9 @@ struct IArgs {
     uint32_t n_init_ext;
     int explicit_init;
     uint32_t* o_init;
+    uint32_t* o_first;   // all-fit + mark_first: access index of each init slot's first use
+    uint32_t* o_rest_x;  // all-fit + mark_first: accesses that are not a first use (dense) ...
+    uint32_t* o_rest_slot;  // ... and their cache slots
     uint32_t* o_in_ids;
     uint32_t* o_in_pos;
     uint32_t* o_in_slot;
@@ -448,8 +451,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
                         const uint32_t it = iter_of(sm, S, x);
                         a.slot_node[r] = v;
                         a.slot_key[r] = it;
-                        if (fit) a.acc_slot[x] = r;
-                        else a.node_slot[v] = (int32_t)r;
+                        if (fit) {
+                            a.acc_slot[x] = r;
+                            if (a.o_first) a.o_first[r] = x;
+                        } else {
+                            a.node_slot[v] = (int32_t)r;
+                        }
                         a.o_init[r] = v;
                         atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                     }
@@ -496,7 +503,31 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     // served by its init slot.
     const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
     if (allfit) {
-        if (a.trusted) {
+        if (a.trusted && a.o_first) {
+            // fused executor: the non-first accesses as a dense list (rank =
+            // position minus the first uses before it: tile_cnt + in-tile scan)
+            for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                uint32_t nf[4], c = 0;
+                const uint32_t x0 = t * IN_TILE + tid * 4;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint32_t x = x0 + j;
+                    nf[j] = x < a.A ? (a.isfirst[x] ? 0u : 1u) : 0u;
+                    c += nf[j];
+                }
+                uint32_t tot;
+                uint32_t k = t * IN_TILE - a.tile_cnt[t] + block_excl_scan(c, sm.scan, tot);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (nf[j]) {
+                        const uint32_t x = x0 + j;
+                        a.o_rest_x[k] = x;
+                        a.o_rest_slot[k] = a.acc_slot[a.next_use[x]] & ~kFirstFlag;
+                        ++k;
+                    }
+                }
+            }
+        } else if (a.trusted) {
             // the first occurrence of each access's node already holds the slot
             // (init pass); the lookups stay inside the A-sized acc_slot array
             // instead of the N-sized node arrays
@@ -948,7 +979,8 @@ static void host_trace_error(const std::vector<uint32_t>& flat, const std::vecto
 }
 
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
-                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted) {
+                 const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
+                 bool mark_first) {
     const uint64_t S = off.size() - 1;
     if (S > kMaxIters) fail(GX_INVALID_ARGUMENT, "at most 4096 iterations per superbatch");
     if (N >= 0xFFFFFFFFull) fail(GX_OVERFLOW, "num_nodes exceeds the u32 device id range");
@@ -1082,6 +1114,16 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.n_init_ext = n_init_explicit >= 0 ? (uint32_t)n_init_explicit : 0;
     a.explicit_init = n_init_explicit >= 0;
     a.o_init = out->init.p;
+    a.o_first = nullptr;
+    a.o_rest_x = a.o_rest_slot = nullptr;
+    if (mark_first && a.trusted) {
+        out->first_acc.reserve(Keff + 1);
+        out->rest_x.reserve(A + 1);
+        out->rest_slot.reserve(A + 1);
+        a.o_first = out->first_acc.p;
+        a.o_rest_x = out->rest_x.p;
+        a.o_rest_slot = out->rest_slot.p;
+    }
     a.o_in_ids = out->in_ids.p;
     a.o_in_pos = out->in_pos.p;
     a.o_in_slot = out->in_slot.p;
@@ -1152,6 +1194,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     }
     if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");
     out->n_init = n_init_explicit >= 0 ? (uint64_t)n_init_explicit : std::min<uint64_t>(hs.n_first, Keff);
+    // all-fit with marks: first uses carry kFirstFlag in acc_slot, first_acc is valid
+    out->first_marked = a.o_first != nullptr && hs.n_first <= Keff;
+    out->n_rest = out->first_marked ? A - hs.n_first : 0;
     out->h_misses.assign(m32.begin(), m32.begin() + S);
     out->h_in_off.assign(S + 1, 0);
     out->h_out_off.assign(S + 1, 0);
