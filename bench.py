@@ -454,11 +454,14 @@ def main():
     for s in stats:
         assert s.total_misses == s.predicted_misses, "observed misses != inspector prediction"
 
-    # --- roofline of the dominant kernel (the gather) -------------------------
+    # --- rooflines: the gather (the north star's bandwidth kernel) and every stage --
     w = f.row_bytes()
-    rows = sum(s.gathered_rows for s in stats)
+    n = len(stats)
+    rows = sum(s.gathered_rows for s in stats)                # accesses A
+    rows_g = sum(s.gather_kernel_rows for s in stats)         # rows the gather launches moved
     gk_ms = sum(s.ms_gather_kernels for s in stats)
-    alg_bytes = (2 * w + 16) * rows               # read row + write row + id + slot
+    g_row = 2 * w + 8                                         # read row + write row + u32 id + u32 slot
+    alg_bytes = g_row * rows_g
     peak, peak_src = measured_peaks()
     achieved = alg_bytes / (gk_ms / 1e3) / 1e9
     traffic = None
@@ -466,7 +469,33 @@ def main():
     if os.path.exists(tp):
         with open(tp) as fh:
             traffic = json.load(fh).get("k_gather_dram_bytes_per_launch")
-    n = len(stats)
+    step_ms = 1e3 * dev_s / args.steps
+
+    def line(kernel, ms_tot, bytes_tot, bytes_formula, bound="hbm"):
+        ms = ms_tot / n
+        a = bytes_tot / (ms_tot / 1e3) / 1e9 if ms_tot else None
+        return {"kernel": kernel, "ms_per_superbatch": ms, "share_of_step": ms / step_ms, "bound": bound,
+                "achieved_GBps": a, "peak_GBps": peak, "frac": a / peak if a else None,
+                "alg_bytes_per_superbatch": bytes_tot / n, "alg_bytes": bytes_formula}
+
+    fused = any(s.fused_fill for s in stats)
+    lists = sum(s.sample_io.neighbor_lists_read for s in stats)
+    C = sum(s.total_in + s.total_out for s in stats)
+    fills = sum(s.fill_rows for s in stats)
+    rooflines = [
+        line("k_sample (stage: sampler)", sum(s.ms_sample for s in stats),
+             24 * lists + 16 * edges + 8 * rows, "24*P + 16*E + 8*U (SURVEY 8d; P = parents expanded)",
+             "latency (dependent indptr -> indices -> dedup-table chains, grid barriers)"),
+        line("k_flatten + k_inspect (stage: inspector)", sum(s.ms_inspect for s in stats),
+             24 * rows + 16 * C + 8 * fills, "24*A + 16*C + 8*|init| (SURVEY 8d)",
+             "latency (random node-array atomics, grid barriers)"),
+        line("k_fill_first (switch fused with first uses)" if fused else "k_gather_rows<16,8> (switch: cache init)",
+             sum(s.ms_switch for s in stats), (3 * w + 8 if fused else 2 * w + 4) * fills,
+             "(3w + 8) per init row: read row, write slot + first batch row, 2 ids" if fused
+             else "(2w + 4) per init row: read row, write slot, id"),
+        line("k_gather_tma2 (bulk-copy row gather)", gk_ms, alg_bytes,
+             "(2w + 8) per row: read row, write row, u32 id + u32 slot"),
+    ]
     S = cfg["S"]
     stages = {
         "sample_ms": sum(s.ms_sample for s in stats) / n,
@@ -476,8 +505,10 @@ def main():
         "gather_kernels_ms": gk_ms / n,
         "apply_kernels_ms": sum(s.ms_apply_kernels for s in stats) / n,
         "sampler_edges_per_s": sum(s.sampled_edges for s in stats) / (sum(s.ms_sample for s in stats) / 1e3),
-        "gathered_feature_GBps": w * rows / (gk_ms / 1e3) / 1e9,
-        "gathered_feature_GBps_incl_apply": w * rows / (sum(s.ms_gather for s in stats) / 1e3) / 1e9,
+        # feature bytes assembled into batches per second of executor time (switch + gather + apply)
+        "gathered_feature_GBps": w * rows / (sum(s.ms_switch + s.ms_gather for s in stats) / 1e3) / 1e9,
+        "gather_kernel_rows_per_superbatch": rows_g / n,
+        "fused_fill": fused,
         "accesses_per_superbatch": rows / n,
         "miss_ratio": sum(s.total_misses for s in stats) / max(rows, 1),
         "init_size": stats[-1].init_size,
@@ -524,12 +555,15 @@ def main():
                 "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
                 "d2h_bytes_per_step": int(8 * S + 8 * 16)},
         "gpu_launches": int(sum(s.kernel_launches for s in stats)),
-        "roofline": {"kernel": "k_gather_tma2 (TMA bulk row gather)", "bound": "hbm", "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+        "roofline": {"kernel": "k_gather_tma2 (bulk-copy row gather)", "bound": "hbm", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "peak_source": peak_src,
-                     "bytes_per_row": 2 * w + 16,
-                     "rows_per_launch": rows / max(1, sum(s.gather_launches for s in stats)),
-                     "alg_bytes_per_launch": alg_bytes / max(1, sum(s.gather_launches for s in stats))},
+                     "bytes_per_row": g_row,
+                     "rows_per_launch": rows_g / max(1, sum(s.gather_launches for s in stats)),
+                     "alg_bytes_per_launch": alg_bytes / max(1, sum(s.gather_launches for s in stats)),
+                     "note": ("all-fit superbatches: the switch kernel also writes each init node's first-use "
+                              "batch row, the gather moves the other accesses" if fused else None)},
+        "rooflines": rooflines,
         "stages": stages,
         "clocks": clk.summary(),
     }

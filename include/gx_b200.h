@@ -308,6 +308,13 @@ typedef struct gx_pipeline_stats {
     double ms_storage;         /* wall time of the host read phase (pread + staging) */
     uint64_t storage_rows;     /* rows read: cache init + changeset misses */
     uint64_t storage_bytes;    /* bytes read from storage (whole pages) */
+    /* executor kernel work, for roofline accounting */
+    uint64_t fill_rows;        /* rows the switch wrote into cache slots (= init_size) */
+    uint64_t gather_kernel_rows; /* rows the gather launches moved (all accesses, or with
+                                    fused_fill the accesses that are not an init node's first use) */
+    uint32_t fused_fill;       /* 1: all-fit superbatch, the switch also wrote each init node's
+                                  first-use batch row */
+    uint32_t reserved0;
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,
                              uint32_t n_layers, uint64_t num_entries, gx_pipeline** out);

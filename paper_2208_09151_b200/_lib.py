@@ -42,7 +42,8 @@ class PipelineStatsC(C.Structure):
                 ("ms_sample", dbl), ("ms_inspect", dbl), ("ms_switch", dbl), ("ms_gather", dbl),
                 ("ms_gather_kernels", dbl), ("ms_apply_kernels", dbl),
                 ("kernel_launches", u64), ("gather_launches", u64),
-                ("ms_storage", dbl), ("storage_rows", u64), ("storage_bytes", u64)]
+                ("ms_storage", dbl), ("storage_rows", u64), ("storage_bytes", u64),
+                ("fill_rows", u64), ("gather_kernel_rows", u64), ("fused_fill", u32), ("reserved0", u32)]
 
 
 class ExchangeStatsC(C.Structure):

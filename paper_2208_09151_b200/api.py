@@ -970,6 +970,9 @@ class PipelineStats:
     ms_storage: float = 0.0      # file-backed tables: host read phase of the superbatch
     storage_rows: int = 0
     storage_bytes: int = 0
+    fill_rows: int = 0           # rows the switch wrote (init set)
+    gather_kernel_rows: int = 0  # rows the gather launches moved
+    fused_fill: bool = False     # all-fit: the switch also wrote each init node's first batch row
 
 
 def _io(c: IoStatsC) -> IoStats:
@@ -1023,7 +1026,7 @@ class Pipeline:
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
                              st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, st.kernel_launches,
                              st.gather_launches, misses[:S].copy(), st.ms_storage, st.storage_rows,
-                             st.storage_bytes)
+                             st.storage_bytes, st.fill_rows, st.gather_kernel_rows, bool(st.fused_fill))
 
     def batch(self, i: int, ticket: Optional[int] = None) -> np.ndarray:
         """Iteration i's gathered rows of a waited-for superbatch (default: the

@@ -88,6 +88,8 @@ struct PipeSlot {
     gx::DevBuf<uint8_t> stage;
     double ms_storage = 0;
     uint64_t storage_rows = 0, storage_bytes = 0;
+    bool fused = false;
+    uint64_t gather_rows = 0;
     cudaEvent_t ev[6] = {};  // A: start, sampled, inspected; B: exec start, switched, done
     std::vector<cudaEvent_t> kev;
 };
@@ -507,6 +509,8 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         // whole superbatch resident when it fits the per-slot budget (GX_BATCH_BUDGET_MB)
         sl.full = resident;
         const bool fused = sl.cs.first_marked;  // implies all-fit (no changesets) and resident
+        sl.fused = fused;
+        sl.gather_rows = fused ? sl.cs.n_rest : sl.o[S];
         sl.batch.reserve(std::max<uint64_t>((sl.full ? sl.o[S] : maxw) * rb, 16));
         sl.h_off.reserve(S + 1);
         sl.d_off.reserve(S + 1);
@@ -674,6 +678,10 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             stats->ms_apply_kernels = ak;
             stats->kernel_launches = sl.launches;
             stats->gather_launches = sl.nseg;
+            stats->fill_rows = sl.cs.n_init;
+            stats->gather_kernel_rows = sl.gather_rows;
+            stats->fused_fill = sl.fused ? 1u : 0u;
+            stats->reserved0 = 0;
             stats->ms_storage = sl.ms_storage;
             stats->storage_rows = sl.storage_rows;
             stats->storage_bytes = sl.storage_bytes;

@@ -53,7 +53,9 @@ def main():
                    "ms_inspect": sum(s.ms_inspect for s in sts) / len(sts),
                    "ms_switch": sum(s.ms_switch for s in sts) / len(sts),
                    "ms_gather_apply": sum(s.ms_gather for s in sts) / len(sts),
-                   "gathered_GBps": rows * 4 * cfg["dim"] / (sum(s.ms_gather_kernels for s in sts) / len(sts) / 1e3) / 1e9,
+                   # feature bytes assembled per second of executor time (switch + gather + apply)
+                   "gathered_GBps": rows * 4 * cfg["dim"] / (sum(s.ms_switch + s.ms_gather for s in sts) / len(sts) / 1e3) / 1e9,
+                   "fused_fill": any(s.fused_fill for s in sts),
                    "miss_ratio": sum(s.total_misses for s in sts) / max(sum(s.gathered_rows for s in sts), 1),
                    "changeset_in_per_iter": sum(s.total_in for s in sts) / (len(sts) * S),
                    "observed_eq_predicted": all(s.total_misses == s.predicted_misses for s in sts)}
