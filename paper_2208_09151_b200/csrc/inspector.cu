@@ -27,6 +27,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <mutex>
 #include <unordered_set>
 
 #include "gx_internal.cuh"
@@ -346,8 +347,17 @@ __device__ bool next_use_pass(const IArgs& a, SM& sm, bool firsts) {
     return true;
 }
 
-template <uint32_t CAP>
-__global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
+// The inspector is two cooperative launches over one body. PART 0 (first uses,
+// init set, and the whole all-fit case) runs two 512-thread CTAs per SM: its
+// passes are random node-array accesses that want warps in flight (1.04 vs
+// 1.15 ms at papers shape). PART 1 (next use + the Belady recurrence, skipped
+// when everything fit) runs one CTA per SM: it is grid-barrier bound, and a
+// larger grid makes every barrier dearer (cfg1: 5.07 vs 5.62 ms).
+#ifndef GX_IN_FRONT_BPS
+#define GX_IN_FRONT_BPS 2
+#endif
+template <uint32_t CAP, int PART>
+__device__ __forceinline__ void inspect_body(IArgs& a) {
     extern __shared__ unsigned char smem_raw[];
     using SM = ISmem<CAP>;
     SM& sm = *reinterpret_cast<SM*>(smem_raw);
@@ -364,6 +374,7 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[0] = gtimer();
     __syncthreads();
     const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
+    if (PART == 0) {
 
     // ---- first occurrences, next use ---------------------------------------
     bool have_next = false;
@@ -552,6 +563,12 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
         }
         return;
     }
+    return;  // not all-fit: PART 1 continues
+    }
+    // PART 1
+    if (*(volatile uint32_t*)&a.st->err) return;  // PART 0 found a bad trace (the host reports it)
+    if (!a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K) return;  // all-fit: done
+    const bool have_next = !a.trusted;  // untrusted traces computed next use in PART 0
     if (!have_next) next_use_pass(a, sm, false);
     if (a.tstamp) {  // tracing only: the recurrence needs no barrier here
         grid_sync(a.bar);
@@ -958,6 +975,15 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect(IArgs a) {
     if (gtid == 0) a.st->n_res = nfin;  // final resident count for the host
 }
 
+template <uint32_t CAP>
+__global__ void __launch_bounds__(IN_THREADS, GX_IN_FRONT_BPS) k_inspect(IArgs a) {
+    inspect_body<CAP, 0>(a);
+}
+template <uint32_t CAP>
+__global__ void __launch_bounds__(IN_THREADS, 1) k_inspect_rec(IArgs a) {
+    inspect_body<CAP, 1>(a);
+}
+
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
@@ -1027,9 +1053,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.in_node.reserve(maxw);
     B.in_pos.reserve(maxw);
     static const int grid_knob = env_int("GX_INSPECT_CTAS", 0);  // CTAs (0 = one per SM)
-    const int grid = grid_knob > 0 ? std::min(grid_knob, ctx->num_sms) : ctx->num_sms;
-    B.chunk_cnt.reserve(2 * grid);
-    B.bm_cnt.reserve(grid);
+    const int grid = grid_knob > 0 ? std::min(grid_knob, ctx->num_sms) : ctx->num_sms;  // PART 1 (recurrence)
+    const int grid0 = ctx->num_sms * GX_IN_FRONT_BPS;                                      // PART 0
+    B.chunk_cnt.reserve(2 * std::max(grid, grid0));
+    B.bm_cnt.reserve(std::max(grid, grid0));
     B.st.reserve(16);
     GX_CUDA(cudaMemsetAsync(B.st.p, 0, 2 * sizeof(IState), st));
     static_assert(2 * sizeof(IState) <= 16 * sizeof(uint32_t), "2 IStates fit the scratch words");
@@ -1100,7 +1127,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.in_node = B.in_node.p;
     a.in_pos = B.in_pos.p;
     a.chunk_miss = B.chunk_cnt.p;
-    a.chunk_in = B.chunk_cnt.p + grid;
+    a.chunk_in = B.chunk_cnt.p + std::max(grid, grid0);
     a.isfirst = B.isfirst.p;
     a.bits = use_bits ? is.bits.p : nullptr;
     a.W = (uint32_t)W;
@@ -1147,21 +1174,33 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     // smallest iteration capacity that holds S (shared memory scales with it)
     const int ci = S <= 128 ? 0 : S <= 512 ? 1 : 2;
     void* const kfns[3] = {(void*)k_inspect<128>, (void*)k_inspect<512>, (void*)k_inspect<kMaxIters>};
+    void* const rfns[3] = {(void*)k_inspect_rec<128>, (void*)k_inspect_rec<512>, (void*)k_inspect_rec<kMaxIters>};
     const size_t smems[3] = {sizeof(ISmem<128>), sizeof(ISmem<512>), sizeof(ISmem<kMaxIters>)};
-    static bool attr[3] = {false, false, false};
-    if (!attr[ci]) {
-        GX_CUDA(cudaFuncSetAttribute(kfns[ci], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[ci]));
-        int bps = 0;
-        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfns[ci], IN_THREADS, smems[ci]));
-        if (bps < 1) fail(GX_CUDA_ERROR, "inspector kernel cannot be resident");
-        attr[ci] = true;
+    static int bps0[3] = {0, 0, 0};
+    static std::mutex attr_mu;
+    {
+        std::lock_guard<std::mutex> lk(attr_mu);
+        if (!bps0[ci]) {
+            int b1 = 0, b0 = 0;
+            GX_CUDA(cudaFuncSetAttribute(kfns[ci], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[ci]));
+            GX_CUDA(cudaFuncSetAttribute(rfns[ci], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[ci]));
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b0, kfns[ci], IN_THREADS, smems[ci]));
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, rfns[ci], IN_THREADS, smems[ci]));
+            if (b1 < 1 || b0 < 1) fail(GX_CUDA_ERROR, "inspector kernel cannot be resident");
+            bps0[ci] = std::min(b0, GX_IN_FRONT_BPS);
+        }
     }
+    const int g0 = std::min(grid0, ctx->num_sms * bps0[ci]);
     void* args[] = {&a};
-    if (coop_launch())
-        GX_CUDA(cudaLaunchCooperativeKernel(kfns[ci], dim3(grid), dim3(IN_THREADS), args, smems[ci], st));
-    else
-        GX_CUDA(cudaLaunchKernel(kfns[ci], dim3(grid), dim3(IN_THREADS), args, smems[ci], st));
-    GX_CHECK_LAUNCH();
+    for (int part = 0; part < 2; ++part) {
+        void* fn = part ? rfns[ci] : kfns[ci];
+        const int g = part ? grid : g0;
+        if (coop_launch())
+            GX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(IN_THREADS), args, smems[ci], st));
+        else
+            GX_CUDA(cudaLaunchKernel(fn, dim3(g), dim3(IN_THREADS), args, smems[ci], st));
+        GX_CHECK_LAUNCH();
+    }
 
     if (n_init_explicit > 0) {
         k_init_pos<<<ctx->num_sms, 256, 0, st>>>(B.init_ext.p, (uint32_t)n_init_explicit, is.init_pos.p, 0);
