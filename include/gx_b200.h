@@ -97,6 +97,25 @@ gx_status gx_graph_copy_csc(const gx_graph* g, uint64_t* indptr, uint64_t* indic
 /* persist_graph (graph_store.hpp:83-98): writes graph.bin byte-identically */
 gx_status gx_graph_write(const gx_graph* g, const char* path);
 
+/* ---- static neighbor cache (neighbor_cache.hpp) --------------------------
+ * The CSC is HBM-resident, so the cache changes only the sampler's IoStats (a
+ * cached list charges nothing, sampler.hpp:91-97), exactly as in the
+ * reference; the address table and cache array are kept for ncache.bin. */
+typedef struct gx_ncache gx_ncache;
+/* build_neighbor_cache (neighbor_cache.hpp:88-116): greedy by out/in degree
+ * (descending, ties by id) within budget_bytes (address table + regions) */
+gx_status gx_ncache_build(gx_graph* g, uint64_t budget_bytes, gx_iostats* io, gx_ncache** out);
+/* load_neighbor_cache / persist_neighbor_cache (neighbor_cache.hpp:118-148) */
+gx_status gx_ncache_open(gx_graph* g, const char* path, gx_iostats* io, gx_ncache** out);
+gx_status gx_ncache_write(const gx_ncache* c, const char* path);
+void gx_ncache_destroy(gx_ncache* c);
+uint64_t gx_ncache_cached_nodes(const gx_ncache* c);
+uint64_t gx_ncache_bytes_used(const gx_ncache* c);   /* NeighborCache::bytes_used */
+gx_status gx_ncache_contains(const gx_ncache* c, uint64_t v, int* out);
+/* the sampler calls on this graph (and its pipelines) consult `c` (NULL: none);
+ * `c` must outlive its use */
+gx_status gx_graph_set_neighbor_cache(gx_graph* g, const gx_ncache* c);
+
 /* ---- sampler (sampler.hpp) ---------------------------------------------- */
 typedef struct gx_samples gx_samples; /* S batches: ids + per-layer edges, on device */
 /* superbatch_sample (sampler.hpp:197-243) minus the file writes (see

@@ -118,7 +118,47 @@ struct SampleOutput {
     std::vector<std::vector<LocalEdge>> layers;
 };
 
-struct NeighborCache;  // out of scope: the CSC is HBM-resident; pass nullptr
+// neighbor_cache.hpp: the static neighbor cache. The CSC is HBM-resident, so
+// it changes only the sampler's IoStats (a cached list charges nothing).
+class NeighborCache {
+public:
+    std::uint64_t cached_node_count() const { return gx_ncache_cached_nodes(c_.get()); }
+    std::uint64_t bytes_used() const { return gx_ncache_bytes_used(c_.get()); }
+    gx_ncache* handle() const { return c_.get(); }
+    explicit NeighborCache(gx_ncache* c) : c_(c, gx_ncache_destroy) {}
+
+private:
+    std::shared_ptr<gx_ncache> c_;
+};
+// build_neighbor_cache / load_neighbor_cache / persist_neighbor_cache (neighbor_cache.hpp:88-148)
+inline NeighborCache build_neighbor_cache(const GraphFile& graph, std::uint64_t budget_bytes,
+                                          IoStats* stats = nullptr) {
+    gx_ncache* c = nullptr;
+    gx_iostats io{};
+    check(gx_ncache_build(graph.handle(), budget_bytes, &io, &c));
+    if (stats) stats->add(io);
+    return NeighborCache(c);
+}
+inline NeighborCache load_neighbor_cache(const GraphFile& graph, const std::filesystem::path& path,
+                                         IoStats* stats = nullptr) {
+    gx_ncache* c = nullptr;
+    gx_iostats io{};
+    check(gx_ncache_open(graph.handle(), path.string().c_str(), &io, &c));
+    if (stats) stats->add(io);
+    return NeighborCache(c);
+}
+inline void persist_neighbor_cache(const NeighborCache& cache, const std::filesystem::path& path) {
+    check(gx_ncache_write(cache.handle(), path.string().c_str()));
+}
+namespace detail {
+struct UseNcache {  // installs the cache on the graph for one sampler call
+    gx_graph* g;
+    UseNcache(gx_graph* graph, const NeighborCache* c) : g(graph) {
+        check(gx_graph_set_neighbor_cache(g, c ? c->handle() : nullptr));
+    }
+    ~UseNcache() { gx_graph_set_neighbor_cache(g, nullptr); }
+};
+}  // namespace detail
 
 namespace detail {
 inline SampleOutput batch_of(gx_samples* s, std::uint64_t b) {
@@ -145,7 +185,7 @@ inline SampleOutput batch_of(gx_samples* s, std::uint64_t b) {
 inline SampleOutput sample_batch(const GraphFile& graph, const NeighborCache* cache,
                                  std::span<const NodeId> seeds, const Fanouts& fanouts,
                                  std::uint64_t batch_seed, IoStats& stats) {
-    if (cache) throw std::invalid_argument("neighbor cache is out of scope (CSC in HBM)");
+    detail::UseNcache use(graph.handle(), cache);
     gx_samples* s = nullptr;
     gx_iostats io{};
     check(gx_sample_batch(graph.handle(), seeds.data(), seeds.size(), fanouts.data(),
@@ -169,7 +209,7 @@ inline SuperbatchSampleResult superbatch_sample(const GraphFile& graph, const Ne
                                                 std::uint64_t first_global_batch, std::uint64_t sb_index,
                                                 const std::filesystem::path& out_dir, unsigned workers) {
     (void)workers;
-    if (cache) throw std::invalid_argument("neighbor cache is out of scope (CSC in HBM)");
+    detail::UseNcache use(graph.handle(), cache);
     std::filesystem::create_directories(out_dir);
     std::vector<NodeId> flat;
     std::vector<std::uint64_t> off{0};

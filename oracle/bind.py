@@ -362,6 +362,8 @@ class _Ref:
             L.gxr_graph_read_all.argtypes = [vp, u64p, u64p]
             L.gxr_sample_batch.argtypes = [vp, u64p, u64, u32p, u32, u64, u64p, u64,
                                            C_.POINTER(u64), u32p, u64, u64p, u64p]
+            L.gxr_sample_batch_nc.argtypes = [vp, C_.c_char_p] + L.gxr_sample_batch.argtypes[1:]
+            L.gxr_ncache_build.argtypes = [vp, u64, C_.c_char_p, u64p, C_.POINTER(u64)]
             L.gxr_superbatch_sample.argtypes = [vp, u64p, u64p, u64, u32p, u32, u64, u64, u64,
                                                 C_.c_char_p, C_.c_uint, u64p,
                                                 C_.POINTER(C_.c_double)]
@@ -500,7 +502,14 @@ class _RefGraph:
         self.r._chk(self.r.lib.gxr_graph_read_all(self.h, ip, ind))
         return ip, ind[:self.num_edges].copy()
 
-    def sample_batch(self, seeds, fanouts, batch_seed):
+    def ncache_build(self, budget_bytes, path):
+        """build_neighbor_cache + persist_neighbor_cache -> (IoStats, cached nodes)."""
+        io = np.zeros(4, np.uint64)
+        k = u64()
+        self.r._chk(self.r.lib.gxr_ncache_build(self.h, budget_bytes, path.encode(), io, C_.byref(k)))
+        return io, k.value
+
+    def sample_batch(self, seeds, fanouts, batch_seed, ncache_path=None):
         seeds = _a64(seeds)
         fan = np.ascontiguousarray(fanouts, dtype=np.uint32)
         f = len(seeds)
@@ -513,10 +522,13 @@ class _RefGraph:
         lc = np.zeros(max(len(fan), 1), np.uint64)
         io = np.zeros(4, np.uint64)
         nid = u64()
-        self.r._chk(self.r.lib.gxr_sample_batch(self.h, seeds if len(seeds) else np.zeros(1, np.uint64),
-                                                len(seeds), fan if len(fan) else np.zeros(1, np.uint32),
-                                                len(fan), batch_seed, ids, len(ids), C_.byref(nid),
-                                                edges, e_cap, lc, io))
+        args = (seeds if len(seeds) else np.zeros(1, np.uint64), len(seeds),
+                fan if len(fan) else np.zeros(1, np.uint32), len(fan), batch_seed, ids, len(ids),
+                C_.byref(nid), edges, e_cap, lc, io)
+        if ncache_path is None:
+            self.r._chk(self.r.lib.gxr_sample_batch(self.h, *args))
+        else:
+            self.r._chk(self.r.lib.gxr_sample_batch_nc(self.h, ncache_path.encode(), *args))
         layers, k = [], 0
         for l in range(len(fan)):
             c = int(lc[l])

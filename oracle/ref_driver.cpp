@@ -183,15 +183,15 @@ int gxr_graph_read_all(void* gh, uint64_t* indptr, uint64_t* indices) {
 
 /// sample_batch (sampler.hpp:69). edges_out holds (src,dst) u32 pairs, layer
 /// after layer; layer_counts[l] gives each layer's edge count.
-int gxr_sample_batch(void* gh, const uint64_t* seeds, uint64_t n_seeds, const uint32_t* fanouts,
-                     uint32_t n_layers, uint64_t batch_seed, uint64_t* ids_out, uint64_t ids_cap,
-                     uint64_t* n_ids, uint32_t* edges_out, uint64_t edges_cap,
-                     uint64_t* layer_counts, uint64_t* io) {
+static int sample_batch_impl(void* gh, const NeighborCache* nc, const uint64_t* seeds, uint64_t n_seeds,
+                             const uint32_t* fanouts, uint32_t n_layers, uint64_t batch_seed,
+                             uint64_t* ids_out, uint64_t ids_cap, uint64_t* n_ids, uint32_t* edges_out,
+                             uint64_t edges_cap, uint64_t* layer_counts, uint64_t* io) {
     return guard([&] {
         auto& g = static_cast<Graph*>(gh)->g;
         IoStats s;
         Fanouts f(fanouts, fanouts + n_layers);
-        SampleOutput o = sample_batch(g, nullptr, std::span<const NodeId>(seeds, n_seeds), f,
+        SampleOutput o = sample_batch(g, nc, std::span<const NodeId>(seeds, n_seeds), f,
                                       batch_seed, s);
         *n_ids = o.ids.size();
         if (o.ids.size() > ids_cap) throw std::runtime_error("ids_cap too small");
@@ -206,6 +206,39 @@ int gxr_sample_batch(void* gh, const uint64_t* seeds, uint64_t n_seeds, const ui
                 ++k;
             }
         }
+        put_io(s, io);
+    });
+}
+
+int gxr_sample_batch(void* gh, const uint64_t* seeds, uint64_t n_seeds, const uint32_t* fanouts,
+                     uint32_t n_layers, uint64_t batch_seed, uint64_t* ids_out, uint64_t ids_cap,
+                     uint64_t* n_ids, uint32_t* edges_out, uint64_t edges_cap,
+                     uint64_t* layer_counts, uint64_t* io) {
+    return sample_batch_impl(gh, nullptr, seeds, n_seeds, fanouts, n_layers, batch_seed, ids_out, ids_cap,
+                             n_ids, edges_out, edges_cap, layer_counts, io);
+}
+
+/// sample_batch with a static neighbor cache loaded from ncache.bin
+/// (load_neighbor_cache, neighbor_cache.hpp:130-148; its own load is not charged).
+int gxr_sample_batch_nc(void* gh, const char* ncache_path, const uint64_t* seeds, uint64_t n_seeds,
+                        const uint32_t* fanouts, uint32_t n_layers, uint64_t batch_seed, uint64_t* ids_out,
+                        uint64_t ids_cap, uint64_t* n_ids, uint32_t* edges_out, uint64_t edges_cap,
+                        uint64_t* layer_counts, uint64_t* io) {
+    NeighborCache nc;
+    const int rc = guard([&] { nc = load_neighbor_cache(ncache_path); });
+    if (rc) return rc;
+    return sample_batch_impl(gh, &nc, seeds, n_seeds, fanouts, n_layers, batch_seed, ids_out, ids_cap, n_ids,
+                             edges_out, edges_cap, layer_counts, io);
+}
+
+/// build_neighbor_cache (neighbor_cache.hpp:88-116) + persist_neighbor_cache.
+int gxr_ncache_build(void* gh, uint64_t budget_bytes, const char* path, uint64_t* io, uint64_t* cached) {
+    return guard([&] {
+        auto& g = static_cast<Graph*>(gh)->g;
+        IoStats s;
+        NeighborCache c = build_neighbor_cache(g, budget_bytes, &s);
+        persist_neighbor_cache(c, path);
+        if (cached) *cached = c.cached_node_count();
         put_io(s, io);
     });
 }

@@ -106,6 +106,14 @@ SIGNATURES = {
     "gx_changesets_write_files": (i32, [vp, cstr, u64]),
     "gx_features_open": (i32, [vp, cstr, i32, PVP]),
     "gx_features_write": (i32, [vp, cstr]),
+    "gx_ncache_build": (i32, [vp, u64, PIO, PVP]),
+    "gx_ncache_open": (i32, [vp, cstr, PIO, PVP]),
+    "gx_ncache_write": (i32, [vp, cstr]),
+    "gx_ncache_destroy": (None, [vp]),
+    "gx_ncache_cached_nodes": (u64, [vp]),
+    "gx_ncache_bytes_used": (u64, [vp]),
+    "gx_ncache_contains": (i32, [vp, u64, C.POINTER(C.c_int)]),
+    "gx_graph_set_neighbor_cache": (i32, [vp, vp]),
     "gx_features_generate_fp16": (i32, [vp, u64, u32, u64, PVP]),
     "gx_comm_unique_id": (i32, [vp]),
     "gx_comm_init_nccl": (i32, [vp, vp, i32, i32, PVP]),

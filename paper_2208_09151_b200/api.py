@@ -278,10 +278,77 @@ class Samples:
         check(lib.gx_samples_write_files(self.h, os.fspath(out_dir).encode(), sb_index))
 
 
-def _check_no_ncache(cache):
-    if cache is not None:
-        raise ValueError("the static neighbor cache is out of scope: the CSC is HBM-resident "
-                         "(pass cache=None)")
+class NeighborCache:
+    """Static neighbor cache (neighbor_cache.hpp). The CSC is HBM-resident, so
+    the cache changes only the sampler's IoStats: a cached list charges nothing
+    (sampler.hpp:91-97). build() = build_neighbor_cache (greedy by out/in
+    degree within a byte budget), open()/write() = ncache.bin."""
+
+    def __init__(self, handle, graph: GraphFile):
+        self.h = handle
+        self.graph = graph
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            g = getattr(self, "graph", None)
+            if g is not None and getattr(g, "_ncache", None) is self:
+                lib.gx_graph_set_neighbor_cache(g.h, None)
+            lib.gx_ncache_destroy(self.h)
+            self.h = None
+
+    @staticmethod
+    def build(graph: GraphFile, budget_bytes: int, stats: Optional[IoStats] = None) -> "NeighborCache":
+        io = IoStatsC()
+        h = C.c_void_p()
+        check(lib.gx_ncache_build(graph.h, budget_bytes, C.byref(io), C.byref(h)))
+        if stats is not None:
+            stats._add_c(io)
+        return NeighborCache(h, graph)
+
+    @staticmethod
+    def open(graph: GraphFile, path: str, stats: Optional[IoStats] = None) -> "NeighborCache":
+        io = IoStatsC()
+        h = C.c_void_p()
+        check(lib.gx_ncache_open(graph.h, os.fspath(path).encode(), C.byref(io), C.byref(h)))
+        if stats is not None:
+            stats._add_c(io)
+        return NeighborCache(h, graph)
+
+    def write(self, path: str) -> None:
+        check(lib.gx_ncache_write(self.h, os.fspath(path).encode()))
+
+    def cached_node_count(self) -> int:
+        return lib.gx_ncache_cached_nodes(self.h)
+
+    def bytes_used(self) -> int:
+        return lib.gx_ncache_bytes_used(self.h)
+
+    def contains(self, v: int) -> bool:
+        out = C.c_int()
+        check(lib.gx_ncache_contains(self.h, v, C.byref(out)))
+        return bool(out.value)
+
+
+build_neighbor_cache = NeighborCache.build
+load_neighbor_cache = NeighborCache.open
+
+
+class _UseNcache:
+    """Installs `cache` on the graph for one sampler call (the reference passes
+    it per call, sampler.hpp:69,197)."""
+
+    def __init__(self, graph: GraphFile, cache):
+        if cache is not None and not isinstance(cache, NeighborCache):
+            raise TypeError("cache must be a NeighborCache or None")
+        if cache is not None and cache.graph.num_nodes() != graph.num_nodes():
+            raise ValueError("neighbor cache and graph disagree on node count")
+        self.graph, self.cache = graph, cache
+
+    def __enter__(self):
+        check(lib.gx_graph_set_neighbor_cache(self.graph.h, self.cache.h if self.cache is not None else None))
+
+    def __exit__(self, *a):
+        lib.gx_graph_set_neighbor_cache(self.graph.h, None)
 
 
 def _fan(fanouts: Sequence[int]) -> np.ndarray:
@@ -291,12 +358,12 @@ def _fan(fanouts: Sequence[int]) -> np.ndarray:
 def sample_batch(graph: GraphFile, cache, seeds, fanouts: Sequence[int], batch_seed: int,
                  stats: Optional[IoStats] = None) -> SampleOutput:
     """sample_batch (sampler.hpp:69-117)."""
-    _check_no_ncache(cache)
     s, f = _u64(seeds), _fan(fanouts)
     io = IoStatsC()
     h = C.c_void_p()
-    check(lib.gx_sample_batch(graph.h, _ptr(s), len(s), _ptr(f), len(f),
-                              batch_seed & 0xFFFFFFFFFFFFFFFF, C.byref(h), C.byref(io)))
+    with _UseNcache(graph, cache):
+        check(lib.gx_sample_batch(graph.h, _ptr(s), len(s), _ptr(f), len(f),
+                                  batch_seed & 0xFFFFFFFFFFFFFFFF, C.byref(h), C.byref(io)))
     if stats is not None:
         stats._add_c(io)
     return Samples(h).batch(0)
@@ -314,14 +381,14 @@ def _flatten(batches) -> tuple:
 def sample_superbatch(graph: GraphFile, cache, batch_slice, fanouts: Sequence[int], global_seed: int,
                       first_global_batch: int, stats: Optional[IoStats] = None) -> Samples:
     """superbatch_sample's sampling part (sampler.hpp:197-243); result stays on the device."""
-    _check_no_ncache(cache)
     flat, off = _flatten(batch_slice)
     f = _fan(fanouts)
     io = IoStatsC()
     h = C.c_void_p()
-    check(lib.gx_sample_superbatch(graph.h, flat.ctypes.data, off.ctypes.data, len(off) - 1, _ptr(f),
-                                   len(f), global_seed & 0xFFFFFFFFFFFFFFFF, first_global_batch,
-                                   C.byref(h), C.byref(io)))
+    with _UseNcache(graph, cache):
+        check(lib.gx_sample_superbatch(graph.h, flat.ctypes.data, off.ctypes.data, len(off) - 1, _ptr(f),
+                                       len(f), global_seed & 0xFFFFFFFFFFFFFFFF, first_global_batch,
+                                       C.byref(h), C.byref(io)))
     if stats is not None:
         stats._add_c(io)
     return Samples(h)

@@ -71,7 +71,7 @@ __device__ __forceinline__ void st_na(uint32_t* p, const uint32_t& v) { *p = v; 
 // graph_store.hpp:308-315).
 template <int R>
 struct GatherOcc {
-    static constexpr int value = R >= 8 ? 3 : (R >= 4 ? 5 : 8);
+    static constexpr int value = R >= 16 ? 2 : (R >= 8 ? 3 : (R >= 4 ? 5 : 8));
 };
 
 // Segment mode (the pipeline gathers several iterations per launch when no
@@ -491,18 +491,20 @@ void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_
         GX_CHECK_LAUNCH();
         return;
     }
-    constexpr int R = 8;
-    static const int bps = [] {
-        int b = 0;
-        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fill_first<R>, GA_THREADS, 0));
-        return std::max(b, 1);
-    }();
-    const uint64_t warps_needed = (n + R - 1) / R;
-    const uint64_t blocks = std::min<uint64_t>((warps_needed * 32 + GA_THREADS - 1) / GA_THREADS,
-                                               (uint64_t)ctx->num_sms * bps);
-    k_fill_first<R><<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(init, first_acc, n, store, (uint32_t)rb,
-                                                                      cache_rows, batch);
-    GX_CHECK_LAUNCH();
+    static const int rr = env_int("GX_FILL_R", 8);  // rows in flight per warp: 4, 8 or 16
+    auto go = [&](auto kfn, int R) {
+        int bps = 0;
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, GA_THREADS, 0));
+        const uint64_t warps_needed = (n + R - 1) / R;
+        const uint64_t blocks = std::min<uint64_t>((warps_needed * 32 + GA_THREADS - 1) / GA_THREADS,
+                                                   (uint64_t)ctx->num_sms * std::max(bps, 1));
+        kfn<<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(init, first_acc, n, store, (uint32_t)rb, cache_rows,
+                                                               batch);
+        GX_CHECK_LAUNCH();
+    };
+    if (rr == 4) go(k_fill_first<4>, 4);
+    else if (rr == 16) go(k_fill_first<16>, 16);
+    else go(k_fill_first<8>, 8);
 }
 
 // Address-table resolution for the API path: slots[k] = table[ids[k]] (or kNever).

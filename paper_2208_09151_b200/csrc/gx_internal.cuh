@@ -104,6 +104,7 @@ struct gx_graph {
     uint64_t n = 0, e = 0;
     gx::DevBuf<uint64_t> indptr;   // N+1
     gx::DevBuf<uint32_t> indices;  // E (u32 device ids)
+    const uint32_t* ncache_bits = nullptr;  // neighbor cache in use (bit v: list cached, charges no I/O)
 };
 
 // Sampler output for S batches (SampleOutput x S, sampler.hpp:36-40).

@@ -106,6 +106,7 @@ struct SampArgs {
     unsigned long long* tab1;
     uint64_t tab_cap;  // per batch max
     unsigned long long* io;
+    const uint32_t* ncbits;     // neighbor cache: a cached list charges no I/O (sampler.hpp:91-97)
     GridBarrier* bar;
     uint32_t* tctr;             // dynamic tile counters, 4 per layer (zeroed at kernel start)
     unsigned long long* trace;  // optional phase timestamps (GX_SAMPLER_TRACE)
@@ -437,9 +438,11 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                         a.pdeg[gi] = deg;
                         a.pscan[gi] = take;
                         s += take;
-                        io_lists += 1;
-                        io_pages += pages_touched(8 * lo, 8 * hi);
-                        io_bytes += 8ull * deg;
+                        if (!a.ncbits || !((__ldg(a.ncbits + (v >> 5)) >> (v & 31)) & 1u)) {
+                            io_lists += 1;
+                            io_pages += pages_touched(8 * lo, 8 * hi);
+                            io_bytes += 8ull * deg;
+                        }
                     }
                 }
                 uint32_t tot = block_sum(s, sm.scan);
@@ -836,9 +839,11 @@ __global__ void __launch_bounds__(SC_THREADS) k_sample_cl(SampArgs a) {
                 a.pdeg[gi] = deg;
                 a.pscan[gi] = take;
                 csum += take;
-                io_lists += 1;
-                io_pages += pages_touched(8 * lo, 8 * hi);
-                io_bytes += 8ull * deg;
+                if (!a.ncbits || !((__ldg(a.ncbits + (v >> 5)) >> (v & 31)) & 1u)) {
+                    io_lists += 1;
+                    io_pages += pages_touched(8 * lo, 8 * hi);
+                    io_bytes += 8ull * deg;
+                }
             }
             csum = block_sum(csum, sm.scan);
             if (tid == 0) sm.part[0] = csum;
@@ -1051,6 +1056,7 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     a.tab1 = ss.tab[1].p;
     a.tab_cap = tab_cap;
     a.io = ss.io.p;
+    a.ncbits = g->ncache_bits;
     a.tctr = ss.tctr.p;
     a.bar = ctx->barrier.p;
     static const bool trace = std::getenv("GX_SAMPLER_TRACE") != nullptr;

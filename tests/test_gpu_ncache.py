@@ -1,0 +1,95 @@
+"""GPU parity of the static neighbor cache (ncache.cu) against the reference
+(neighbor_cache.hpp, compiled from its headers in oracle/_ref): the built
+ncache.bin is byte-identical, the builder's IoStats match, and sampling with
+the cache gives the same ids/edges and the same (reduced) IoStats as the
+reference's sample_batch with that cache (sampler.hpp:91-97)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dataset(ref, tmp_path_factory):
+    d = str(tmp_path_factory.mktemp("ncache"))
+    ref.generate_dataset(d, 6000, 7.0, 8, 101, 102)
+    return d
+
+
+def _io_list(io):
+    return [io.pages_read, io.rows_read, io.neighbor_lists_read, io.bytes_read]
+
+
+@pytest.mark.parametrize("extra", [0, 16, 4000, 40_000, 10_000_000])
+def test_build_matches_reference_bytes(gx, ref, dataset, tmp_path, extra):
+    gpath = os.path.join(dataset, "graph.bin")
+    rg = ref.open_graph(gpath)
+    budget = rg.num_nodes * 8 + extra
+    rpath = str(tmp_path / "ref_ncache.bin")
+    rio, rk = rg.ncache_build(budget, rpath)
+    g = gx.GraphFile.open(gpath)
+    io = gx.IoStats()
+    nc = gx.NeighborCache.build(g, budget, io)
+    gpath2 = str(tmp_path / "gx_ncache.bin")
+    nc.write(gpath2)
+    assert open(gpath2, "rb").read() == open(rpath, "rb").read()
+    assert nc.cached_node_count() == rk
+    assert _io_list(io) == list(map(int, rio))
+    assert nc.bytes_used() <= budget
+
+
+def test_sampling_with_cache_matches_reference(gx, ref, dataset, tmp_path):
+    gpath = os.path.join(dataset, "graph.bin")
+    rg = ref.open_graph(gpath)
+    budget = rg.num_nodes * 8 + 60_000
+    rpath = str(tmp_path / "ncache.bin")
+    rg.ncache_build(budget, rpath)
+    g = gx.GraphFile.open(gpath)
+    lio = gx.IoStats()
+    nc = gx.NeighborCache.open(g, rpath, lio)       # the reference's file
+    size = os.path.getsize(rpath)
+    assert (lio.bytes_read, lio.pages_read) == (size, gx.pages_touched(0, size))
+    rng = np.random.default_rng(4)
+    total_with = gx.IoStats()
+    for trial in range(6):
+        seeds = rng.choice(rg.num_nodes, 64, replace=False).astype(np.uint64)
+        want_ids, want_layers, want_io = rg.sample_batch(seeds, [5, 4, 3], 1000 + trial, rpath)
+        _, _, plain_io = rg.sample_batch(seeds, [5, 4, 3], 1000 + trial)
+        io = gx.IoStats()
+        got = gx.sample_batch(g, nc, seeds, [5, 4, 3], 1000 + trial, io)
+        assert np.array_equal(got.ids, want_ids)
+        for l in range(3):
+            assert np.array_equal(got.layers[l], want_layers[l])
+        assert _io_list(io) == list(map(int, want_io))
+        assert io.neighbor_lists_read <= int(plain_io[2])
+        total_with += io
+        io0 = gx.IoStats()                        # the cache is installed per call only
+        gx.sample_batch(g, None, seeds, [5, 4, 3], 1000 + trial, io0)
+        assert _io_list(io0) == list(map(int, plain_io))
+    # superbatch form: IoStats = sum over its batches
+    batches = [rng.choice(rg.num_nodes, 50, replace=False).astype(np.uint64) for _ in range(5)]
+    sio = gx.IoStats()
+    gx.sample_superbatch(g, nc, batches, [5, 4], 9, 3, sio)
+    want = np.zeros(4, np.uint64)
+    for i, b in enumerate(batches):
+        want += rg.sample_batch(b, [5, 4], gx.derive_seed(9, 3 + i), rpath)[2]
+    assert _io_list(sio) == list(map(int, want))
+
+
+def test_ncache_errors(gx, ref, dataset, tmp_path):
+    g = gx.GraphFile.open(os.path.join(dataset, "graph.bin"))
+    with pytest.raises(ValueError):
+        gx.NeighborCache.build(g, g.num_nodes() * 8 - 1)
+    nc = gx.NeighborCache.build(g, g.num_nodes() * 8 + 1000)
+    assert nc.contains(int(np.argmax([nc.contains(v) for v in range(50)]))) in (True, False)
+    with pytest.raises(IndexError):
+        nc.contains(g.num_nodes())
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"NOTNCACH" + b"\0" * 40)
+    with pytest.raises(RuntimeError):
+        gx.NeighborCache.open(g, str(bad))
+    small = gx.GraphFile.from_csc(np.array([0, 1, 1], np.uint64), np.array([1], np.uint64))
+    with pytest.raises(ValueError):
+        gx.sample_batch(small, nc, [0], [1], 1)
