@@ -116,6 +116,16 @@ gx_status gx_ncache_contains(const gx_ncache* c, uint64_t v, int* out);
  * `c` must outlive its use */
 gx_status gx_graph_set_neighbor_cache(gx_graph* g, const gx_ncache* c);
 
+/* ---- comparison policies of `gx simulate` (baselines.hpp) ----------------
+ * static_degree_set (baselines.hpp:50-62): the K nodes of highest out-degree
+ * (out-degrees from this graph's CSC), ties by lower id, in that order. */
+gx_status gx_static_degree_set(gx_graph* g, uint64_t num_entries, uint64_t* out);
+/* simulate_policy(..., static_degree) (baselines.hpp:81-96): per-iteration
+ * misses of a fixed resident set over a trace of distinct-id lists. The belady
+ * policy is gx_precompute_trace's misses; none = every access; LRU is not offered. */
+gx_status gx_simulate_static_degree(gx_graph* g, const uint64_t* ids_flat, const uint64_t* offsets,
+                                    uint64_t n_iters, uint64_t num_entries, uint64_t* misses);
+
 /* ---- sampler (sampler.hpp) ---------------------------------------------- */
 typedef struct gx_samples gx_samples; /* S batches: ids + per-layer edges, on device */
 /* superbatch_sample (sampler.hpp:197-243) minus the file writes (see

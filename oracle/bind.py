@@ -364,6 +364,7 @@ class _Ref:
                                            C_.POINTER(u64), u32p, u64, u64p, u64p]
             L.gxr_sample_batch_nc.argtypes = [vp, C_.c_char_p] + L.gxr_sample_batch.argtypes[1:]
             L.gxr_ncache_build.argtypes = [vp, u64, C_.c_char_p, u64p, C_.POINTER(u64)]
+            L.gxr_simulate_policy.argtypes = [vp, u64p, u64p, u64, u64, C_.c_int, u64p, C_.POINTER(u64)]
             L.gxr_superbatch_sample.argtypes = [vp, u64p, u64p, u64, u32p, u32, u64, u64, u64,
                                                 C_.c_char_p, C_.c_uint, u64p,
                                                 C_.POINTER(C_.c_double)]
@@ -501,6 +502,16 @@ class _RefGraph:
         ind = np.zeros(max(self.num_edges, 1), np.uint64)
         self.r._chk(self.r.lib.gxr_graph_read_all(self.h, ip, ind))
         return ip, ind[:self.num_edges].copy()
+
+    def simulate_policy(self, trace, K, policy):
+        """simulate_policy (baselines.hpp:64-143) -> (misses per iteration, total accesses)."""
+        flat, off = _trace(trace)
+        pol = {"none": 0, "static_degree": 1, "lru": 2, "belady": 3}[policy]
+        m = np.zeros(max(len(trace), 1), np.uint64)
+        tot = u64()
+        self.r._chk(self.r.lib.gxr_simulate_policy(self.h, flat if len(flat) else np.zeros(1, np.uint64), off,
+                                                   len(trace), K, pol, m, C_.byref(tot)))
+        return m[:len(trace)].copy(), tot.value
 
     def ncache_build(self, budget_bytes, path):
         """build_neighbor_cache + persist_neighbor_cache -> (IoStats, cached nodes)."""

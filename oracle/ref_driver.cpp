@@ -17,6 +17,7 @@
 #include <memory>
 #include <string>
 
+#include "gx/baselines.hpp"
 #include "gx/graphgen.hpp"
 #include "gx/pipeline.hpp"
 
@@ -240,6 +241,31 @@ int gxr_ncache_build(void* gh, uint64_t budget_bytes, const char* path, uint64_t
         persist_neighbor_cache(c, path);
         if (cached) *cached = c.cached_node_count();
         put_io(s, io);
+    });
+}
+
+/// simulate_policy (baselines.hpp:64-143): policy 0 none, 1 static_degree
+/// (out-degrees from the graph, compute_out_degrees), 2 lru, 3 belady.
+int gxr_simulate_policy(void* gh, const uint64_t* flat, const uint64_t* off, uint64_t S, uint64_t K,
+                        int policy, uint64_t* misses_out, uint64_t* total_accesses) {
+    return guard([&] {
+        auto& g = static_cast<Graph*>(gh)->g;
+        struct T {
+            const uint64_t* flat;
+            const uint64_t* off;
+            uint64_t S;
+            std::size_t iterations() const { return S; }
+            std::vector<NodeId> ids(std::size_t i) const {  // the Trace concept (changeset.hpp:44-55)
+                return std::vector<NodeId>(flat + off[i], flat + off[i + 1]);
+            }
+        } tr{flat, off, S};
+        const CachePolicy pol[4] = {CachePolicy::none, CachePolicy::static_degree, CachePolicy::lru,
+                                    CachePolicy::belady};
+        std::vector<std::uint64_t> outdeg;
+        if (policy == 1) outdeg = g.compute_out_degrees();
+        PolicyResult r = simulate_policy(tr, g.num_nodes(), K, pol[policy], outdeg);
+        for (uint64_t i = 0; i < S; ++i) misses_out[i] = r.misses[i];
+        *total_accesses = r.total_accesses;
     });
 }
 

@@ -114,6 +114,8 @@ SIGNATURES = {
     "gx_ncache_bytes_used": (u64, [vp]),
     "gx_ncache_contains": (i32, [vp, u64, C.POINTER(C.c_int)]),
     "gx_graph_set_neighbor_cache": (i32, [vp, vp]),
+    "gx_static_degree_set": (i32, [vp, u64, vp]),
+    "gx_simulate_static_degree": (i32, [vp, vp, vp, u64, u64, vp]),
     "gx_features_generate_fp16": (i32, [vp, u64, u32, u64, PVP]),
     "gx_comm_unique_id": (i32, [vp]),
     "gx_comm_init_nccl": (i32, [vp, vp, i32, i32, PVP]),

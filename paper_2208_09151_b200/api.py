@@ -646,6 +646,66 @@ def precompute_trace(trace, num_nodes: int, num_entries: int, init=None,
     return Changesets(h)
 
 
+# ---------------------------------------------------------------------------
+# comparison policies of `gx simulate` (baselines.hpp)
+# ---------------------------------------------------------------------------
+POLICIES = ("none", "static_degree", "lru", "belady")
+
+
+def parse_policy(s: str) -> str:
+    """parse_policy (baselines.hpp:24-30)."""
+    if s not in POLICIES:
+        raise ValueError("unknown policy: " + s)
+    return s
+
+
+@dataclasses.dataclass
+class PolicyResult:
+    """PolicyResult (baselines.hpp:32-48)."""
+    policy: str
+    capacity: int
+    misses: np.ndarray
+    total_accesses: int
+
+    def total_misses(self) -> int:
+        return int(np.sum(self.misses, dtype=np.uint64))
+
+    def miss_ratio(self) -> float:
+        return 0.0 if self.total_accesses == 0 else self.total_misses() / self.total_accesses
+
+
+def static_degree_set(graph: GraphFile, num_entries: int) -> np.ndarray:
+    """static_degree_set (baselines.hpp:50-62) with out-degrees from the graph's CSC."""
+    out = np.zeros(max(num_entries, 1), np.uint64)
+    check(lib.gx_static_degree_set(graph.h, num_entries, out.ctypes.data))
+    return out[:num_entries].copy()
+
+
+def simulate_policy(trace, num_nodes: int, num_entries: int, policy: str,
+                    graph: Optional[GraphFile] = None, ctx: Optional[Context] = None) -> PolicyResult:
+    """simulate_policy (baselines.hpp:64-143). static_degree takes its
+    out-degrees from `graph` (the reference takes them as a span); belady is
+    the inspector; LRU is not offered on the device."""
+    policy = parse_policy(policy)
+    lists = _trace_lists(trace)
+    total = int(sum(len(x) for x in lists))
+    if policy == "none":
+        return PolicyResult(policy, num_entries, np.array([len(x) for x in lists], np.uint64), total)
+    if policy == "static_degree":
+        if graph is None or graph.num_nodes() != num_nodes:
+            raise ValueError("static_degree requires out-degrees (pass the graph)")
+        flat, off = _flatten(lists)
+        m = np.zeros(max(len(lists), 1), np.uint64)
+        check(lib.gx_simulate_static_degree(graph.h, flat.ctypes.data, off.ctypes.data, len(lists), num_entries,
+                                            m.ctypes.data))
+        return PolicyResult(policy, num_entries, m[:len(lists)].copy(), total)
+    if policy == "belady":
+        cs = precompute_trace(lists, num_nodes, num_entries, ctx=ctx)
+        return PolicyResult(policy, num_entries, cs.misses().astype(np.uint64), total)
+    raise NotImplementedError("LRU is not offered on the device: its misses need the number of distinct "
+                              "nodes between consecutive accesses of a node (a sequential stack simulation)")
+
+
 def compute_init_set(trace, num_entries: int, num_nodes: int,
                      ctx: Optional[Context] = None) -> np.ndarray:
     """compute_init_set (changeset.hpp:137-153)."""

@@ -93,3 +93,29 @@ def test_ncache_errors(gx, ref, dataset, tmp_path):
     small = gx.GraphFile.from_csc(np.array([0, 1, 1], np.uint64), np.array([1], np.uint64))
     with pytest.raises(ValueError):
         gx.sample_batch(small, nc, [0], [1], 1)
+
+
+# ---------------------------------------------------------------------------
+# comparison policies of `gx simulate` (baselines.hpp) vs the reference
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("K", [0, 50, 700, 6000])
+def test_policies_match_reference(gx, ref, dataset, K):
+    gpath = os.path.join(dataset, "graph.bin")
+    rg = ref.open_graph(gpath)
+    g = gx.GraphFile.open(gpath)
+    rng = np.random.default_rng(K)
+    trace = [rg.sample_batch(rng.choice(rg.num_nodes, 40, replace=False).astype(np.uint64), [4, 3], 50 + i)[0]
+             for i in range(8)]
+    for pol in ["none", "static_degree", "belady"]:
+        want, tot = rg.simulate_policy(trace, K, pol)
+        got = gx.simulate_policy(trace, rg.num_nodes, K, pol, graph=g)
+        assert np.array_equal(got.misses, want), pol
+        assert got.total_accesses == tot and got.policy == pol and got.capacity == K
+    with pytest.raises(NotImplementedError):
+        gx.simulate_policy(trace, rg.num_nodes, K, "lru")
+    with pytest.raises(ValueError):
+        gx.simulate_policy(trace, rg.num_nodes, K, "fifo")
+    with pytest.raises(ValueError):
+        gx.static_degree_set(g, rg.num_nodes + 1)
+    s = gx.static_degree_set(g, 10)
+    assert len(s) == 10 and len(set(s.tolist())) == 10
