@@ -382,7 +382,7 @@ def main():
     g, f = build_dataset(gx, cfg, ctx, log, args.backing, args.ssd_dir, comm)
     sbs = make_plan(gx, cfg)
     K_entries = int(cfg["cache_frac"] * cfg["N"])
-    pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries)
+    pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries, overlap=args.overlap)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
     from paper_2208_09151_b200.shard import assign_superbatches
@@ -401,16 +401,15 @@ def main():
         return pipe.submit(sbs[j], SEED_RUN, j * cfg["S"])
 
     def run_steps(k0, n, on_stats, ev_start=None, ev_end=None):
-        """Back to back (default), or with --overlap superbatch k's executor
-        overlaps superbatch k+1's sampler/inspector (two in flight)."""
+        """Two superbatches in flight: superbatch k+1 is submitted before k is
+        waited for, so the host prepares k+1 while the GPU runs k. The GPU
+        stages run back to back (default) or, with --overlap, k+1's
+        sampler/inspector concurrently with k's executor."""
         if ev_start is not None:
             ev_start.record(stream)
         prev = None
         for k in range(k0, k0 + n):
             t = submit(k)
-            if not args.overlap:
-                on_stats(pipe.wait(t))
-                continue
             if prev is not None:
                 on_stats(pipe.wait(prev))
             prev = t
@@ -543,7 +542,8 @@ def main():
         "reference generator; feature_value table)",
         "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * S * world,
                    "superbatch": S, "cache_entries": K_entries, "num_edges": g.num_edges(),
-                   "pipeline": "overlap (2 superbatches in flight)" if args.overlap else "serial superbatches",
+                   "pipeline": ("2 superbatches in flight, GPU stages concurrent" if args.overlap else
+                                "2 superbatches in flight, GPU stages back to back"),
                    "backing": args.backing,
                    "parallelism": (f"dp{world} (superbatches per rank, no collective)" if comm is None else
                                    f"dp{world} superbatches x {world}-way row-partitioned features "

@@ -365,6 +365,11 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat,
                              uint64_t global_seed, uint64_t first_global_batch, uint64_t* ticket);
 gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per_iter,
                            gx_pipeline_stats* stats);
+/* With two superbatches in flight, 0 (default): the GPU runs superbatch k+1's
+ * sampler after k's executor (stages back to back; only the host preparation
+ * of k+1 overlaps k); 1: k+1's sampler/inspector run concurrently with k's
+ * executor. */
+gx_status gx_pipeline_set_overlap(gx_pipeline* p, int concurrent);
 /* the cudaStream_t the executor of this pipeline runs on */
 void* gx_pipeline_exec_stream(gx_pipeline* p);
 /* Device pointer to iteration i's gathered rows (|ids_i| x row_bytes, the

@@ -1110,7 +1110,10 @@ class Pipeline:
     """sample -> precompute -> cache init -> S x (gather, apply) on one GPU."""
 
     def __init__(self, graph: GraphFile, features: FeatureFile, fanouts: Sequence[int],
-                 num_entries: int, digest: bool = False):
+                 num_entries: int, digest: bool = False, overlap: bool = False):
+        """overlap: with two superbatches in flight (submit/wait), let superbatch
+        k+1's sampler and inspector run concurrently with k's executor instead
+        of after it (gx_pipeline_set_overlap)."""
         f = _fan(fanouts)
         h = C.c_void_p()
         check(lib.gx_pipeline_create(graph.h, features.h, _ptr(f), len(f), num_entries, C.byref(h)))
@@ -1118,6 +1121,8 @@ class Pipeline:
         self.graph, self.features = graph, features
         if digest:
             check(lib.gx_pipeline_set_digest(h, 1))
+        if overlap:
+            check(lib.gx_pipeline_set_overlap(h, 1))
         self._S = 0
         self._last = -1
         self._sizes = {}

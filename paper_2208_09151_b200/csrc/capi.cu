@@ -106,6 +106,11 @@ struct gx_pipeline {
     PipeSlot slot[2];
     uint64_t submitted = 0;
     bool digest = false;
+    // 0 (default): a superbatch's sampler waits for the previous superbatch's
+    // executor -- the GPU runs the stages back to back while the host prepares
+    // the next submission; 1: they run concurrently (measured slower at papers
+    // shape: the HBM-bound gather stretches the latency-bound sampler/inspector)
+    int overlap = 0;
     std::vector<uint64_t> h_digests;
 };
 
@@ -435,6 +440,13 @@ void gx_pipeline_destroy(gx_pipeline* p) {
     delete p;
 }
 
+gx_status gx_pipeline_set_overlap(gx_pipeline* p, int concurrent) {
+    return guard([&] {
+        if (!p) fail(GX_INVALID_ARGUMENT, "null pipeline");
+        p->overlap = concurrent != 0;
+    });
+}
+
 gx_status gx_pipeline_set_digest(gx_pipeline* p, int enable) {
     return guard([&] { p->digest = enable != 0; });
 }
@@ -468,6 +480,8 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         for (uint64_t i = 0; i < S; ++i) bs[i] = derive_seed(global_seed, first_global_batch + i);
         const uint32_t L = (uint32_t)p->fanouts.size();
         // this slot's buffers were last read by its previous executor (already waited)
+        const PipeSlot& prev = p->slot[(t + 1) & 1];
+        if (!p->overlap && prev.pending) GX_CUDA(cudaStreamWaitEvent(A, prev.ev[5], 0));
         GX_CUDA(cudaEventRecord(sl.ev[0], A));
         // (1) sample
         sample_run(p->g, seeds_flat, batch_off, S, p->fanouts.data(), L, bs.data(), &p->samples);
