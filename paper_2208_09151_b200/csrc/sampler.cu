@@ -415,6 +415,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
         if (l == 0 || !GX_TABLE_BY_DRAWS) phase_d(false);
         if (a.L == 0) break;
         const uint32_t f = a.fan[l];
+        const bool last_layer = l + 1 == a.L;
 
         // ---- Phase A: per parent deg/take, IoStats, tile sums of takes ----
         {
@@ -671,9 +672,16 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                         const uint32_t p = p0 + j;
                         const uint32_t child = bedge[p].x;
                         const uint32_t local = Fb + r;
-                        const uint32_t slot = a.dslot[(uint64_t)b * a.cap_draw + p];
                         a.ids[(uint64_t)b * a.cap_ids + local] = child;
-                        btab[slot] = ((unsigned long long)child << 32) | local;
+                        if (last_layer) {
+                            // the table is never read again by node: the winner's
+                            // local id goes to its own draw slot (coalesced), and
+                            // phase I follows the table's winning position there
+                            a.drank[(uint64_t)b * a.cap_draw + p] = local;
+                        } else {
+                            const uint32_t slot = a.dslot[(uint64_t)b * a.cap_draw + p];
+                            btab[slot] = ((unsigned long long)child << 32) | local;
+                        }
                         bedge_w[p].x = local;
                         ++r;
                     }
@@ -693,7 +701,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
             const uint32_t T_all = (uint32_t)total_threads;
             for (uint32_t x0 = blockIdx.x * blockDim.x + tid; x0 < tot; x0 += IU * T_all) {
                 uint64_t gd[IU], tb[IU], eo[IU];
-                uint32_t ds[IU], rk[IU];
+                uint32_t ds[IU], rk[IU], x_p[IU];
 #pragma unroll
                 for (int j = 0; j < IU; ++j) {
                     const uint32_t x = x0 + j * T_all;
@@ -702,6 +710,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                     if (x < tot) {
                         const uint32_t b = prefix_batch(sm, S, x);
                         const uint32_t p = x - sm.px[b];
+                        x_p[j] = p;
                         gd[j] = (uint64_t)b * a.cap_draw + p;
                         tb[j] = (uint64_t)b * a.tab_cap;
                         eo[j] = (uint64_t)b * a.cap_e_batch + a.e_off[l] + p;
@@ -713,6 +722,11 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 #pragma unroll
                 for (int j = 0; j < IU; ++j)  // resolved at insert time or a winner: nothing to do
                     if (!(ds[j] & kResolved) && !rk[j]) val[j] = (uint32_t)tab[tb[j] + ds[j]];
+                if (last_layer) {  // val = the winner's draw position: its local id sits in drank
+#pragma unroll
+                    for (int j = 0; j < IU; ++j)
+                        if (!(ds[j] & kResolved) && !rk[j]) val[j] = a.drank[gd[j] - x_p[j] + (val[j] & ~kNewBit)];
+                }
 #pragma unroll
                 for (int j = 0; j < IU; ++j)
                     if (!(ds[j] & kResolved) && !rk[j]) a.edges[eo[j]].x = val[j];
