@@ -66,6 +66,8 @@ struct SampleScratch {
 struct InspectScratch {
     DevBuf<uint32_t> last;       // N, node-indexed "next access" cursor (kNever when clean)
     DevBuf<int32_t> node_slot;   // N, -1 when clean
+    DevBuf<uint32_t> firstx;     // N, epoch-encoded first access (trusted traces)
+    uint64_t fx_base = 0;        // last epoch handed out
     uint64_t N = 0;
     DevBuf<uint32_t> trace, next_use, acc_slot;
     DevBuf<uint64_t> trace_off;

@@ -57,6 +57,8 @@ struct IArgs {
     uint32_t S, A, K, maxw;
     uint64_t N;
     uint32_t* last;
+    uint32_t* firstx;   // N: epoch-encoded first access (trusted path), never cleaned
+    uint32_t fx_epoch;  // this call's epoch E: firstx[v] = E - (first access index of v)
     int32_t* node_slot;
     uint32_t* next_use;
     uint32_t* tile_cnt;
@@ -385,7 +387,9 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         // of a node is its first iteration's access). Each access keeps its
         // node's first access index (next_use doubles as that array until the
         // next-use pass, which the all-fit path never runs).
-        for (uint32_t x = gtid; x < a.A; x += G) atomicMin(&a.last[a.trace[x]], x);
+        // (epoch-encoded, atomicMax of E - x: entries older than this call are
+        // below E - A, so the array never needs cleaning -- no scattered writes)
+        for (uint32_t x = gtid; x < a.A; x += G) atomicMax(&a.firstx[a.trace[x]], a.fx_epoch - x);
         grid_sync(a.bar);
         ISTAMP(a, 1);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -395,7 +399,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) v[j] = x0 + j < a.A ? a.trace[x0 + j] : 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) fx[j] = x0 + j < a.A ? a.last[v[j]] : 0;
+            for (int j = 0; j < 4; ++j) fx[j] = x0 + j < a.A ? a.fx_epoch - a.firstx[v[j]] : 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t x = x0 + j;
@@ -411,8 +415,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         }
         grid_sync(a.bar);
         ISTAMP(a, 2);
-        // `last` is cleaned by the init pass below, which visits every first
-        // occurrence exactly once
+
     } else {
         if (!next_use_pass(a, sm, true)) return;
         have_next = true;
@@ -459,9 +462,12 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     const uint32_t x = x0 + j;
                     const uint32_t v = a.trace[x];
                     if (r < K) {
-                        const uint32_t it = iter_of(sm, S, x);
-                        a.slot_node[r] = v;
-                        a.slot_key[r] = it;
+                        if (!(fit && a.trusted)) {  // recurrence state (and the untrusted cleanup)
+                            const uint32_t it = iter_of(sm, S, x);
+                            a.slot_node[r] = v;
+                            a.slot_key[r] = it;
+                            atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
+                        }
                         if (fit) {
                             a.acc_slot[x] = r;
                             if (a.o_first) a.o_first[r] = x;
@@ -469,9 +475,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                             a.node_slot[v] = (int32_t)r;
                         }
                         a.o_init[r] = v;
-                        atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                     }
-                    if (a.trusted) a.last[v] = kNever;  // leave clean
                     ++r;
                 }
             }
@@ -1021,6 +1025,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     InspectScratch& B = bufs_for(ctx);
     if (is.N < N) {
         is.last.alloc(N);
+        is.firstx.alloc(N);
+        GX_CUDA(cudaMemsetAsync(is.firstx.p, 0, N * 4, st));
+        is.fx_base = 0;
         is.node_slot.alloc(N);
         GX_CUDA(cudaMemsetAsync(is.last.p, 0xff, N * 4, st));
         GX_CUDA(cudaMemsetAsync(is.node_slot.p, 0xff, N * 4, st));
@@ -1108,6 +1115,16 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.maxw = (uint32_t)maxw;
     a.N = N;
     a.last = is.last.p;
+    a.firstx = is.firstx.p;
+    a.fx_epoch = 0;
+    if (trusted && n_init_explicit < 0) {
+        if (is.fx_base + A + 1 > 0xFFFFFFFFull) {  // epoch space exhausted: start over
+            GX_CUDA(cudaMemsetAsync(is.firstx.p, 0, N * 4, st));
+            is.fx_base = 0;
+        }
+        is.fx_base += A + 1;
+        a.fx_epoch = (uint32_t)is.fx_base;
+    }
     a.node_slot = is.node_slot.p;
     a.next_use = is.next_use.p;
     a.tile_cnt = B.tile_cnt.p;
