@@ -602,9 +602,15 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 if (sl.full)
                     while (e + 1 < S && empty_cs(e)) ++e;
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg], B));
+                // a one-iteration segment charges its misses through the kernel's
+                // per-warp counters (the iteration's counter block has the same
+                // layout); per-miss atomics on one iteration's two counters
+                // serialise at L2 (cfg1: 3.4 -> 2.1 ms of gather per superbatch)
+                const bool one = e == i;
                 launch_gather_resolved(ctx, sl.trace.p + sl.o[i], sl.acc_slot.p + sl.o[i], sl.o[e + 1] - sl.o[i],
                                        p->cache_rows.p, store, rb, rows_of(i), sl.counters.p + 8 * i,
-                                       sl.d_off.p + i, (uint32_t)(e - i + 1), file && n_miss > 0, fused);
+                                       one ? nullptr : sl.d_off.p + i, one ? 0u : (uint32_t)(e - i + 1),
+                                       file && n_miss > 0, false);
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg + 1], B));
                 if (p->digest)
                     for (uint64_t k = i; k <= e; ++k)
