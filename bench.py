@@ -322,6 +322,7 @@ def main():
     ap.add_argument("--config", default="papers", choices=sorted(CONFIGS))
     ap.add_argument("--avg-degree", type=float, default=None)
     ap.add_argument("--superbatch", type=int, default=None)
+    ap.add_argument("--cache-frac", type=float, default=None, help="cache entries as a fraction of the nodes")
     ap.add_argument("--ref-batches", type=int, default=16,
                     help="batches per step for the reference / cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -344,6 +345,8 @@ def main():
         cfg["avg_degree"] = args.avg_degree
     if args.superbatch is not None:
         cfg["S"] = args.superbatch
+    if args.cache_frac is not None:
+        cfg["cache_frac"] = args.cache_frac
     rank, world, local = env_rank()
 
     def log(m):

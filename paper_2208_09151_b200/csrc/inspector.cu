@@ -112,6 +112,17 @@ struct IArgs {
             (a).tstamp[k] = gtimer() - (a).tstamp[0];                        \
     } while (0)
 
+// per-phase time of the recurrence (GX_INSPECT_TRACE): slot 15 = last mark,
+// 16 + k = accumulated ns of phase k, 30/31 = ALLIN / cut iterations
+#define IPHASE(a, k)                                                         \
+    do {                                                                     \
+        if ((a).tstamp && blockIdx.x == 0 && threadIdx.x == 0) {             \
+            const unsigned long long _t = gtimer();                          \
+            if ((k) > 0) (a).tstamp[16 + (k)] += _t - (a).tstamp[15];        \
+            (a).tstamp[15] = _t;                                             \
+        }                                                                    \
+    } while (0)
+
 __device__ __forceinline__ uint32_t bucket_of(uint32_t key, uint32_t S) { return key == kNever ? S : key; }
 
 // warp-aggregated append; returns the slot for pred lanes, undefined otherwise
@@ -583,6 +594,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     // State counters are double-buffered by iteration parity: iteration i reads
     // st[i&1] and CTA 0 writes st[(i+1)&1] in the iteration's last grid step.
     for (uint32_t i = 0; i < S; ++i) {
+        IPHASE(a, 0);
         IState* cs = a.st + (i & 1);
         IState* ns = a.st + ((i + 1) & 1);
         const uint32_t base = sm.toff[i];
@@ -625,6 +637,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
         }
         grid_sync(a.bar);
+        IPHASE(a, 1);
 
         uint32_t m, mpre;  // misses this iteration, misses in earlier chunks
         {
@@ -675,8 +688,11 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 a.o_out_off[i + 1] = out_total;
             }
             grid_sync(a.bar);
+            IPHASE(a, 2);
+            if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[30] += 1;
             continue;
         }
+        if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[31] += 1;
 
         // CUT: threshold bucket b* over keys in (i, S] (every CTA, redundantly)
         uint32_t bstar = 0, r = 0, inc_b = 0, new_b = 0;
@@ -766,6 +782,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         if (sel) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
         grid_sync(a.bar);
+        IPHASE(a, 3);
         if (sel) {
             uint32_t want = sel == 1 ? keep_inc : admit_new, left;
             const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
@@ -811,6 +828,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             const uint32_t d3 = hist_select(a.rh + 4096, 1024, left, &left, sm);
             thr = (pre << 10) | d3;
         }
+        IPHASE(a, 4);
 
         // P4: per-chunk count of insertions (position order); b* evictions
         auto in_flag = [&](uint32_t pos) -> bool {
@@ -841,6 +859,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             }
         }
         grid_sync(a.bar);
+        IPHASE(a, 5);
 
         // P5: ordered in-list; out-list sorted by node id
         uint32_t n_in;
@@ -933,6 +952,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             grid_sync(a.bar);
         }
 
+        IPHASE(a, 6);
         // P6: apply -- slots per FeatureCache rules, state + histogram update
         for (uint32_t k = gtid; k < n_in; k += G) {
             const uint32_t v = a.in_node[k];
@@ -971,6 +991,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             a.o_out_off[i + 1] = out_total + n_out;
         }
         grid_sync(a.bar);
+        IPHASE(a, 7);
     }
     ISTAMP(a, 7);
     // leave node_slot clean
@@ -1238,6 +1259,11 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         std::fprintf(stderr, "[inspect trace us] A=%llu S=%llu", (unsigned long long)A, (unsigned long long)S);
         for (int k = 1; k < 8; ++k)
             if (htb.p[k]) std::fprintf(stderr, " s%d=%.1f", k, htb.p[k] / 1e3);
+        if (htb.p[30] + htb.p[31]) {
+            std::fprintf(stderr, " | allin=%llu cut=%llu phases(us):", htb.p[30], htb.p[31]);
+            const char* nm[8] = {"", "P1", "allin", "P3", "select", "P4", "P5", "P6"};
+            for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.1f", nm[k], htb.p[16 + k] / 1e3);
+        }
         std::fprintf(stderr, "\n");
     }
     if (hs.err & 3u) {
