@@ -179,9 +179,14 @@ namespace gx {
 struct SampleScratch;
 
 // Internal entry points shared between translation units.
-void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
+// firstx != nullptr (pipeline): also fill the inspector's first-use array with
+// keys (b << 21 | local) under epoch fx_epoch; returns whether it did
+bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
                 const uint32_t* fanouts, uint32_t L, const uint64_t* batch_seeds,
-                gx_samples* out);
+                gx_samples* out, uint32_t* firstx = nullptr, uint32_t fx_epoch = 0);
+// reserve an epoch of `keyrange` keys in the first-use array (allocated and
+// zeroed for N nodes on first use, reset when the epochs wrap)
+uint32_t inspect_reserve_epoch(gx_ctx* ctx, uint64_t N, uint64_t keyrange);
 void samples_sync_host(gx_samples* s);
 
 // Inspector (inspector.cu). The flat u32 trace lives in ctx->is.trace.
@@ -190,9 +195,10 @@ void inspect_fill_from_device(gx_ctx* ctx, const uint32_t* d_ids, uint64_t strid
 void inspect_fill_from_host(gx_ctx* ctx, const uint64_t* flat, const std::vector<uint64_t>& off,
                             uint64_t N);
 // trusted: the trace comes from the sampler (ids < N, distinct per iteration)
+// presampled_epoch != 0: the sampler already filled firstx with (b << 21 | local) keys
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
                  const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
-                 bool mark_first = false);
+                 bool mark_first = false, uint32_t presampled_epoch = 0);
 void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t* h_iters,
                       uint64_t* h_ptr);
 

@@ -59,6 +59,7 @@ struct IArgs {
     uint32_t* last;
     uint32_t* firstx;   // N: epoch-encoded first access (trusted path), never cleaned
     uint32_t fx_epoch;  // this call's epoch E: firstx[v] = E - (first access index of v)
+    int fx_sampled;     // the sampler filled firstx with keys (iteration << 21 | position)
     int32_t* node_slot;
     uint32_t* next_use;
     uint32_t* tile_cnt;
@@ -400,8 +401,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         // next-use pass, which the all-fit path never runs).
         // (epoch-encoded, atomicMax of E - x: entries older than this call are
         // below E - A, so the array never needs cleaning -- no scattered writes)
-        for (uint32_t x = gtid; x < a.A; x += G) atomicMax(&a.firstx[a.trace[x]], a.fx_epoch - x);
-        grid_sync(a.bar);
+        if (!a.fx_sampled) {
+            for (uint32_t x = gtid; x < a.A; x += G) atomicMax(&a.firstx[a.trace[x]], a.fx_epoch - x);
+            grid_sync(a.bar);
+        }
         ISTAMP(a, 1);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
@@ -411,6 +414,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             for (int j = 0; j < 4; ++j) v[j] = x0 + j < a.A ? a.trace[x0 + j] : 0;
 #pragma unroll
             for (int j = 0; j < 4; ++j) fx[j] = x0 + j < a.A ? a.fx_epoch - a.firstx[v[j]] : 0;
+            if (a.fx_sampled) {  // key (iteration << 21 | position) -> access index
+#pragma unroll
+                for (int j = 0; j < 4; ++j) fx[j] = sm.toff[fx[j] >> 21] + (fx[j] & 0x1FFFFFu);
+            }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t x = x0 + j;
@@ -1029,9 +1036,35 @@ static void host_trace_error(const std::vector<uint32_t>& flat, const std::vecto
     fail(GX_RUNTIME_ERROR, "inspector: invalid trace");
 }
 
+static void ensure_node_arrays(gx_ctx* ctx, uint64_t N) {
+    InspectScratch& is = ctx->is;
+    cudaStream_t st = ctx->stream;
+    if (is.N < N) {
+        is.last.alloc(N);
+        is.firstx.alloc(N);
+        GX_CUDA(cudaMemsetAsync(is.firstx.p, 0, N * 4, st));
+        is.fx_base = 0;
+        is.node_slot.alloc(N);
+        GX_CUDA(cudaMemsetAsync(is.last.p, 0xff, N * 4, st));
+        GX_CUDA(cudaMemsetAsync(is.node_slot.p, 0xff, N * 4, st));
+        is.N = N;
+    }
+}
+
+uint32_t inspect_reserve_epoch(gx_ctx* ctx, uint64_t N, uint64_t keyrange) {
+    ensure_node_arrays(ctx, N);
+    InspectScratch& is = ctx->is;
+    if (is.fx_base + keyrange + 1 > 0xFFFFFFFFull) {  // epoch space exhausted: start over
+        GX_CUDA(cudaMemsetAsync(is.firstx.p, 0, N * 4, ctx->stream));
+        is.fx_base = 0;
+    }
+    is.fx_base += keyrange + 1;
+    return (uint32_t)is.fx_base;
+}
+
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
                  const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
-                 bool mark_first) {
+                 bool mark_first, uint32_t presampled_epoch) {
     const uint64_t S = off.size() - 1;
     if (S > kMaxIters) fail(GX_INVALID_ARGUMENT, "at most 4096 iterations per superbatch");
     if (N >= 0xFFFFFFFFull) fail(GX_OVERFLOW, "num_nodes exceeds the u32 device id range");
@@ -1044,18 +1077,11 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     cudaStream_t st = ctx->stream;
     InspectScratch& is = ctx->is;
     InspectScratch& B = bufs_for(ctx);
-    if (is.N < N) {
-        is.last.alloc(N);
-        is.firstx.alloc(N);
-        GX_CUDA(cudaMemsetAsync(is.firstx.p, 0, N * 4, st));
-        is.fx_base = 0;
-        is.node_slot.alloc(N);
-        GX_CUDA(cudaMemsetAsync(is.last.p, 0xff, N * 4, st));
-        GX_CUDA(cudaMemsetAsync(is.node_slot.p, 0xff, N * 4, st));
-        is.N = N;
+    if (B.bm_words.n < (N + 31) / 32 + 1) {
         B.bm_words.alloc((N + 31) / 32 + 1);
         GX_CUDA(cudaMemsetAsync(B.bm_words.p, 0, B.bm_words.bytes(), st));
     }
+    ensure_node_arrays(ctx, N);
     // is.trace holds the flat u32 trace (inspect_fill_*)
     std::vector<uint32_t> off32(S + 1);
     for (uint64_t i = 0; i <= S; ++i) off32[i] = (uint32_t)off[i];
@@ -1138,13 +1164,14 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.last = is.last.p;
     a.firstx = is.firstx.p;
     a.fx_epoch = 0;
+    a.fx_sampled = 0;
     if (trusted && n_init_explicit < 0) {
-        if (is.fx_base + A + 1 > 0xFFFFFFFFull) {  // epoch space exhausted: start over
-            GX_CUDA(cudaMemsetAsync(is.firstx.p, 0, N * 4, st));
-            is.fx_base = 0;
+        if (presampled_epoch) {
+            a.fx_epoch = presampled_epoch;
+            a.fx_sampled = 1;
+        } else {
+            a.fx_epoch = inspect_reserve_epoch(ctx, N, A);
         }
-        is.fx_base += A + 1;
-        a.fx_epoch = (uint32_t)is.fx_base;
     }
     a.node_slot = is.node_slot.p;
     a.next_use = is.next_use.p;

@@ -107,6 +107,10 @@ struct SampArgs {
     uint64_t tab_cap;  // per batch max
     unsigned long long* io;
     const uint32_t* ncbits;     // neighbor cache: a cached list charges no I/O (sampler.hpp:91-97)
+    // the inspector's first-use array, filled as ids are discovered (pipeline):
+    // firstx[v] = max(firstx[v], fx_epoch - ((batch0 + b) << 21 | local))
+    uint32_t* firstx;
+    uint32_t fx_epoch, batch0;
     GridBarrier* bar;
     uint32_t* tctr;             // dynamic tile counters, 4 per layer (zeroed at kernel start)
     unsigned long long* trace;  // optional phase timestamps (GX_SAMPLER_TRACE)
@@ -386,6 +390,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 if (l == 0) {
                     v = a.seeds[a.seed_off[b] + k];
                     a.ids[gi] = v;
+                    if (a.firstx) atomicMax(&a.firstx[v], a.fx_epoch - (((a.batch0 + b) << 21) | k));
                 } else {
                     v = a.ids[gi];
                 }
@@ -673,6 +678,8 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                         const uint32_t child = bedge[p].x;
                         const uint32_t local = Fb + r;
                         a.ids[(uint64_t)b * a.cap_ids + local] = child;
+                        if (a.firstx)  // fire-and-forget: overlaps the latency-bound phases
+                            atomicMax(&a.firstx[child], a.fx_epoch - (((a.batch0 + b) << 21) | local));
                         if (last_layer) {
                             // the table is never read again by node: the winner's
                             // local id goes to its own draw slot (coalesced), and
@@ -957,8 +964,9 @@ static uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t cap) {
     return std::min(cap, a * b);
 }
 
-void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
-                const uint32_t* fanouts, uint32_t L, const uint64_t* batch_seeds, gx_samples* out) {
+bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
+                const uint32_t* fanouts, uint32_t L, const uint64_t* batch_seeds, gx_samples* out,
+                uint32_t* firstx, uint32_t fx_epoch) {
     gx_ctx* ctx = g->ctx;
     if (L > (uint32_t)kMaxLayers) fail(GX_INVALID_ARGUMENT, "at most 16 layers are supported");
     uint64_t ns_max = 0, ns_total = batch_off[S];
@@ -1071,6 +1079,10 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     a.tab_cap = tab_cap;
     a.io = ss.io.p;
     a.ncbits = g->ncache_bits;
+    // first-use keys (b << 21 | local) need local ids below 2^21 and S <= 2048
+    const bool fx_ok = firstx && cap_ids <= (1ull << 21) && S <= 2048;
+    a.firstx = fx_ok ? firstx : nullptr;
+    a.fx_epoch = fx_epoch;
     a.tctr = ss.tctr.p;
     a.bar = ctx->barrier.p;
     static const bool trace = std::getenv("GX_SAMPLER_TRACE") != nullptr;
@@ -1134,7 +1146,7 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
             else GX_CUDA(cudaLaunchKernelEx(&lc, k_sample_cl<8>, a));
             GX_CHECK_LAUNCH();
         }
-        return;
+        return false;  // the cluster sampler does not fill the first-use array
     }
     for (uint64_t c0 = 0; c0 < S; c0 += CH) {
         const uint64_t nb = std::min(CH, S - c0);
@@ -1145,6 +1157,7 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         a.n_ids = out->n_ids.p + c0;
         a.edges = out->edges.p + c0 * out->cap_e_batch;
         a.layer_count = out->layer_count.p + c0 * L;
+        a.batch0 = (uint32_t)c0;
         void* args[] = {&a};
         if (coop_launch()) GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
         else GX_CUDA(cudaLaunchKernel((void*)k_sample, grid, block, args, smem, st));
@@ -1172,6 +1185,7 @@ void sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
             fprintf(stderr, "%s\n", line.c_str());
         }
     }
+    return fx_ok;
 }
 
 void samples_sync_host(gx_samples* s) {
