@@ -70,7 +70,9 @@ constexpr int SB_DIPT = GX_SB_DIPT;
 constexpr uint32_t SB_DTILE = SB_THREADS * SB_DIPT;
 constexpr uint32_t kNewBit = 0x80000000u;
 constexpr unsigned long long kEmptySlot = ~0ull;
-constexpr uint32_t kMaxBatchesPerLaunch = 4096;
+// batches per launch cap: sizes SampSmem's prefix arrays, and a small SampSmem
+// leaves the SM's unified L1/shared array to L1 (spills, read-only loads)
+constexpr uint32_t kMaxBatchesPerLaunch = 512;
 constexpr uint64_t kChunk = 128;  // batches per sampler launch
 constexpr int kPickCache = 32;
 
@@ -1097,6 +1099,9 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     static int blocks_per_sm = -1;
     if (blocks_per_sm < 0) {
         GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        static const int carve = env_int("GX_SAMPLER_CARVEOUT", -1);  // % of the array as shared memory
+        if (carve >= 0)
+            GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
         GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_sample, SB_THREADS, smem));
         if (blocks_per_sm < 1) fail(GX_CUDA_ERROR, "sampler kernel cannot be resident");
     }
