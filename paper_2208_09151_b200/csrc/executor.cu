@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fill_first(
     }
 }
 
-static int gather_smem_budget();
+static int gather_smem_budget(uint64_t rb);
 
 // Bulk-copy form of the fused fill: each thread moves whole rows through its
 // own two smem buffers (load of row j+1 in flight while row j is stored), and
@@ -472,13 +472,13 @@ void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_
     if (!n) return;
     if (rb % 16) fail(GX_INVALID_ARGUMENT, "fused fill needs 16-byte rows");
     static const int tma = env_int("GX_FILL_TMA", 0);  // bulk-copy form: 1.85 vs 1.67 ms (LDG/STG) at papers shape
-    if (tma && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget()) {
+    if (tma && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget(rb)) {
         static int tpb = 0, bpsm = 0;
         static uint64_t last = 0;
         static std::mutex mu;
         std::lock_guard<std::mutex> lk(mu);
         if (last != rb) {
-            tpb = (int)std::min<uint64_t>(128, gather_smem_budget() / (2 * rb)) & ~31;
+            tpb = (int)std::min<uint64_t>(128, gather_smem_budget(rb) / (2 * rb)) & ~31;
             const int smem = tpb * 2 * (int)rb;
             GX_CUDA(cudaFuncSetAttribute(k_fill_first_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
             GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_fill_first_tma, tpb, smem));
@@ -659,20 +659,21 @@ static int gather_variant() {
     }();
     return R;
 }
-static int gather_smem_budget() {
-    static const int budget = [] {  // shared memory per CTA for row buffers (KB)
-        const char* e = std::getenv("GX_GATHER_SMEM_KB");
-        const int kb = e ? std::atoi(e) : 96;
-        return std::min(std::max(kb, 16), 200) * 1024;
-    }();
-    return budget;
+// shared memory per CTA for the bulk-copy row buffers: three full warps with
+// two rows in flight each (96 KB at 512-byte rows -> two CTAs per SM; 192 KB at
+// 1 KB rows -> one; measured at friendster shape: 0.98 vs 0.88 of peak against
+// a fixed 96 KB, whose 48-thread CTAs leave half a warp idle)
+static int gather_smem_budget(uint64_t rb = 512) {
+    static const int knob = env_int("GX_GATHER_SMEM_KB", 0);
+    if (knob > 0) return std::min(std::max(knob, 16), 200) * 1024;
+    return (int)std::min<uint64_t>(200 * 1024, std::max<uint64_t>(16 * 1024, 96 * 2 * rb));
 }
 
 // the pipeline may fuse the fill with the first uses only when the gather that
 // will serve the rest is the bulk-copy kernel (its DSTIDX instantiation)
 bool gather_can_skip_first(uint64_t rb) {
     static const bool on = env_int("GX_FUSED_FILL", 1) != 0;
-    return on && vec16(rb) && gather_variant() == 1 && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget();
+    return on && vec16(rb) && gather_variant() == 1 && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget(rb);
 }
 
 void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
@@ -685,7 +686,7 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
     // thread (default); 0 = TMA bulk, 1 row per thread; 2/4/8 = LDG/STG with
     // that many rows per warp. TMA needs 16-byte rows whose buffers fit smem.
     const int R = gather_variant();
-    const int budget = gather_smem_budget();
+    const int budget = gather_smem_budget(rb);
     static const int ring = env_int("GX_GATHER_D", 0);  // 3/4/6: k_gather_ring<D> (experimental)
     static std::mutex cfg_mu;  // launch-config caches below are shared by every context / host thread
     std::lock_guard<std::mutex> cfg_lock(cfg_mu);

@@ -61,7 +61,10 @@ def test_file_read_rows_matches_reference(gx, ref, tmp_path, knobs, dim, cfg):
     assert (hits, misses) == (0, len(ids))
     assert [io.pages_read, io.rows_read, io.neighbor_lists_read, io.bytes_read] == list(map(int, rio))
     st = f.storage_stats()
-    assert st.rows == len(ids) and st.preads >= 1 and st.bytes % 4096 in (0, (4096 + n * dim * 4) % 4096)
+    assert st.rows == len(ids) and st.preads >= 1
+    # whole pages, except reads that stop at EOF (one per reader thread that reaches it)
+    tail = (4096 + n * dim * 4) % 4096
+    assert any((st.bytes - k * tail) % 4096 == 0 for k in range(st.threads + 1))
     # coalescing: never more preads than rows, never fewer than the distinct page runs need
     assert st.preads <= len(ids)
 
