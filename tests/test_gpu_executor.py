@@ -277,3 +277,25 @@ def test_pipeline_batch_budget_fallback(oracle):
     env = dict(os.environ, GX_BATCH_BUDGET_MB="0", PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("K", [200, 3000])       # changesets every iteration / all-fit (fused fill)
+def test_pipeline_fp16_768(gx, oracle, K):
+    """scalar_width 2 extension (configs[3], MAG240M shape: 768-d fp16 rows of
+    1536 bytes) through the whole pipeline: batches byte-identical to the rows."""
+    n, dim = 4000, 768
+    ip, ind = oracle.rmat_graph(n, 6.0, 23)
+    rows = oracle.features(n, dim, 24).astype(np.float16)
+    g = gx.GraphFile.from_csc(ip, ind)
+    f = gx.FeatureFile.from_array(rows)
+    assert f.row_bytes() == 1536
+    train = oracle.train_ids(n, 1, 0.3)
+    plan = oracle.plan_seed_batches(train, 40, oracle.epoch_seed(1, 0))[:8]
+    p = gx.Pipeline(g, f, [5, 3], K, digest=True)
+    st = p.run_superbatch(plan, 1, 0)
+    trace = [oracle.sample_batch(ip, ind, b, [5, 3], oracle.derive_seed(1, i))[0] for i, b in enumerate(plan)]
+    sim = oracle.simulate(trace, n, K, oracle.compute_init_set(trace, K, n))
+    assert np.array_equal(st.misses, sim["misses"])
+    for i, ids in enumerate(trace):
+        assert np.array_equal(p.batch(i), rows[ids.astype(np.int64)])
+    assert st.fused_fill == (K >= len(np.unique(np.concatenate(trace))))
