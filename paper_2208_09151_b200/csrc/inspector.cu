@@ -755,6 +755,34 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             sm.bc[9] = 0;
         }
         __syncthreads();
+        // PI slots per thread per pass, their keys loaded together (the scan
+        // covers every resident slot, so it is latency-bound otherwise); the
+        // stage takes at most 2 x blockDim entries between flushes
+        if (nres >= 8u * G) {  // large caches: PI slots per thread per pass
+        constexpr int PI = 8;
+        for (uint32_t s0 = blockIdx.x * blockDim.x * PI; s0 < nres; s0 += G * PI) {  // CTA-uniform trip count
+            uint32_t bk[PI];
+#pragma unroll
+            for (int j = 0; j < PI; ++j) {
+                const uint32_t s = s0 + j * blockDim.x + tid;
+                bk[j] = s < nres ? bucket_of(a.slot_key[s], S) : 0u;  // bucket 0 <= i < b*: kept
+            }
+#pragma unroll
+            for (int j = 0; j < PI; ++j) {
+                const uint32_t s = s0 + j * blockDim.x + tid;
+                const bool ev = s < nres && (bk[j] > bstar || (bk[j] == bstar && keep_inc == 0));
+                const bool mem = s < nres && sel == 1 && bk[j] == bstar;
+                uint32_t v = 0;
+                if (ev || mem) v = a.slot_node[s];
+                if (mem) atomicAdd(&sm.rh[v >> 21], 1);
+                stage_put(st_ev, ev, v, s);
+                if (j & 1) {
+                    __syncthreads();
+                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                }
+            }
+        }
+        } else {  // small caches: one slot per thread per pass keeps every CTA busy
         for (uint32_t s0 = blockIdx.x * blockDim.x; s0 < nres; s0 += G) {  // CTA-uniform trip count
             const uint32_t s = s0 + tid;
             bool ev = false;
@@ -768,6 +796,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             stage_put(st_ev, ev, v, s);
             __syncthreads();
             stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+        }
         }
         if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
             for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < ni; p0 += G) {
@@ -795,6 +824,36 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
             if (sel == 1) {
                 // P3b: first digit above the cut -> evicted; equal -> candidates
+                if (nres >= 8u * G) {
+                constexpr int PI = 8;
+                for (uint32_t s0 = blockIdx.x * blockDim.x * PI; s0 < nres; s0 += G * PI) {
+                    bool inb[PI];
+#pragma unroll
+                    for (int j = 0; j < PI; ++j) {
+                        const uint32_t s = s0 + j * blockDim.x + tid;
+                        inb[j] = s < nres && bucket_of(a.slot_key[s], S) == bstar;
+                    }
+#pragma unroll
+                    for (int j = 0; j < PI; ++j) {
+                        const uint32_t s = s0 + j * blockDim.x + tid;
+                        bool ev = false, c = false;
+                        uint32_t v = 0;
+                        if (inb[j]) {
+                            v = a.slot_node[s];
+                            ev = (v >> 21) > d1;
+                            c = (v >> 21) == d1;
+                            if (c) atomicAdd(&sm.rh[(v >> 10) & 2047], 1);
+                        }
+                        stage_put(st_ev, ev, v, s);
+                        stage_put(st_c, c, v, s);
+                        if (j & 1) {
+                            __syncthreads();
+                            stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                            stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
+                        }
+                    }
+                }
+                } else {
                 for (uint32_t s0 = blockIdx.x * blockDim.x; s0 < nres; s0 += G) {
                     const uint32_t s = s0 + tid;
                     bool ev = false, c = false;
@@ -810,6 +869,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     __syncthreads();
                     stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
                     stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
+                }
                 }
                 __syncthreads();
                 stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
