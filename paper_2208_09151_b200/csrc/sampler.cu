@@ -709,36 +709,38 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
             constexpr int IU = GX_I_UNROLL;
             const uint32_t T_all = (uint32_t)total_threads;
             for (uint32_t x0 = blockIdx.x * blockDim.x + tid; x0 < tot; x0 += IU * T_all) {
-                uint64_t gd[IU], tb[IU], eo[IU];
-                uint32_t ds[IU], rk[IU], x_p[IU];
+                // per item only (batch, position) and the two loaded words stay
+                // live; addresses are recomputed (64-bit address arrays spilled)
+                uint32_t bb[IU], pp[IU], ds[IU], rk[IU];
 #pragma unroll
                 for (int j = 0; j < IU; ++j) {
                     const uint32_t x = x0 + j * T_all;
                     ds[j] = kResolved;
                     rk[j] = 1;
+                    bb[j] = 0;
+                    pp[j] = 0;
                     if (x < tot) {
-                        const uint32_t b = prefix_batch(sm, S, x);
-                        const uint32_t p = x - sm.px[b];
-                        x_p[j] = p;
-                        gd[j] = (uint64_t)b * a.cap_draw + p;
-                        tb[j] = (uint64_t)b * a.tab_cap;
-                        eo[j] = (uint64_t)b * a.cap_e_batch + a.e_off[l] + p;
-                        ds[j] = a.dslot[gd[j]];
-                        rk[j] = a.drank[gd[j]];
+                        bb[j] = prefix_batch(sm, S, x);
+                        pp[j] = x - sm.px[bb[j]];
+                        const uint64_t gd = (uint64_t)bb[j] * a.cap_draw + pp[j];
+                        ds[j] = a.dslot[gd];
+                        rk[j] = a.drank[gd];
                     }
                 }
                 uint32_t val[IU];
 #pragma unroll
                 for (int j = 0; j < IU; ++j)  // resolved at insert time or a winner: nothing to do
-                    if (!(ds[j] & kResolved) && !rk[j]) val[j] = (uint32_t)tab[tb[j] + ds[j]];
+                    if (!(ds[j] & kResolved) && !rk[j]) val[j] = (uint32_t)tab[(uint64_t)bb[j] * a.tab_cap + ds[j]];
                 if (last_layer) {  // val = the winner's draw position: its local id sits in drank
 #pragma unroll
                     for (int j = 0; j < IU; ++j)
-                        if (!(ds[j] & kResolved) && !rk[j]) val[j] = a.drank[gd[j] - x_p[j] + (val[j] & ~kNewBit)];
+                        if (!(ds[j] & kResolved) && !rk[j])
+                            val[j] = a.drank[(uint64_t)bb[j] * a.cap_draw + (val[j] & ~kNewBit)];
                 }
 #pragma unroll
                 for (int j = 0; j < IU; ++j)
-                    if (!(ds[j] & kResolved) && !rk[j]) a.edges[eo[j]].x = val[j];
+                    if (!(ds[j] & kResolved) && !rk[j])
+                        a.edges[(uint64_t)bb[j] * a.cap_e_batch + a.e_off[l] + pp[j]].x = val[j];
             }
             for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
                 a.layer_count[(uint64_t)b * a.L + l] = a.T[b];
