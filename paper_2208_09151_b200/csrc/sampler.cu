@@ -39,7 +39,7 @@ constexpr int SB_THREADS = 512;
 #endif
 constexpr int SB_IPT = GX_SB_IPT;
 #ifndef GX_E_UNROLL
-#define GX_E_UNROLL 4
+#define GX_E_UNROLL 3  // draws in flight per thread in phase E (swept 2-6 at 64 registers: 3 best)
 #endif
 #ifndef GX_TABLE_SLACK  // table slots >= entry bound << SLACK (1: load <= 1/2)
 #define GX_TABLE_SLACK 1
