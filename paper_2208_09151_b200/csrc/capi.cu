@@ -581,8 +581,6 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                                   sl.counters.p + 8 * S);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
             }
-            static const int dbg_sync = gx::env_int("GX_SYNC_BEFORE_GATHER", 0);  // experiment knob
-            if (dbg_sync) GX_CUDA(cudaStreamSynchronize(B));
             // (4) main loop. Iterations whose changesets are empty do not mutate
             // the cache, so with the whole superbatch resident a run of them is
             // gathered by one launch (segment), then the last one's changeset applied.
