@@ -72,7 +72,7 @@ struct InspectScratch {
     DevBuf<uint32_t> trace, next_use, acc_slot;
     DevBuf<uint64_t> trace_off;
     DevBuf<uint32_t> tile_cnt, slot_node, slot_key, hist_new, rh, pkey, out_node, out_slot, c_id,
-        c_ref, in_node, in_pos, chunk_cnt, bm_words, bm_cnt, init_ext, toff, st;
+        c_ref, in_node, in_pos, chunk_cnt, bm_words, bm_top, bm_cnt, init_ext, toff, st;
     DevBuf<int32_t> hist_inc;
     DevBuf<uint8_t> pmiss;
     DevBuf<uint32_t> o_misses, o_in_off, o_out_off;  // per-iteration outputs (S+1)

@@ -87,6 +87,8 @@ struct IArgs {
     uint32_t* in_pos;    // maxw
     uint32_t* bm_words;  // nwords
     uint32_t nwords;
+    uint32_t* bm_top;    // ntop = ceil(nwords / 32): bit w set iff bm_words[w] != 0
+    uint32_t ntop;
     uint32_t* bm_cnt;    // gridDim
     const uint32_t* init_ext;
     uint32_t n_init_ext;
@@ -984,7 +986,53 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 }
             }
             grid_sync(a.bar);
-        } else {
+        } else if ((uint64_t)n_out * 32 < a.nwords) {
+            // sparse outs (large N): two-level bitmap -- bit v of bm_words per
+            // out node, bit w of bm_top per non-empty word, so the ordered walk
+            // touches N/1024 summary words plus the occupied words instead of
+            // all N/32 words (S = 500 at 5 %: P5 67 -> ~45 us per cut iteration)
+            for (uint32_t k = gtid; k < n_out; k += G) {
+                const uint32_t v = a.out_node[k];
+                atomicOr(&a.bm_words[v >> 5], 1u << (v & 31));
+                atomicOr(&a.bm_top[v >> 10], 1u << ((v >> 5) & 31));
+            }
+            grid_sync(a.bar);
+            const uint32_t tch = (a.ntop + gridDim.x - 1) / gridDim.x;
+            const uint32_t t0 = min(a.ntop, blockIdx.x * tch), t1 = min(a.ntop, t0 + tch);
+            uint32_t c = 0;
+            for (uint32_t t = t0 + tid; t < t1; t += blockDim.x)
+                for (uint32_t tb = a.bm_top[t]; tb; tb &= tb - 1) c += __popc(a.bm_words[t * 32 + (__ffs(tb) - 1)]);
+            c = block_sum(c, sm.scan);
+            if (tid == 0) a.bm_cnt[blockIdx.x] = c;
+            grid_sync(a.bar);
+            uint32_t pre = 0;
+            for (uint32_t cc = tid; cc < blockIdx.x; cc += blockDim.x) pre += a.bm_cnt[cc];
+            pre = block_sum(pre, sm.scan);
+            for (uint32_t p0 = t0; p0 < t1; p0 += blockDim.x) {
+                const uint32_t t = p0 + tid;
+                const uint32_t tb0 = t < t1 ? a.bm_top[t] : 0;
+                uint32_t cnt = 0;
+                for (uint32_t tb = tb0; tb; tb &= tb - 1) cnt += __popc(a.bm_words[t * 32 + (__ffs(tb) - 1)]);
+                uint32_t tot;
+                uint32_t k = pre + block_excl_scan(cnt, sm.scan, tot);
+                if (tb0) a.bm_top[t] = 0;
+                for (uint32_t tb = tb0; tb; tb &= tb - 1) {
+                    const uint32_t w = t * 32 + (__ffs(tb) - 1);
+                    uint32_t bits = a.bm_words[w];
+                    a.bm_words[w] = 0;
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const uint32_t v = w * 32 + b;
+                        a.out_node[k] = v;
+                        a.out_slot[k] = (uint32_t)a.node_slot[v];
+                        ++k;
+                    }
+                }
+                pre += tot;
+            }
+            grid_sync(a.bar);
+        } else {  // dense outs: one flat pass over the N-bit bitmap
             for (uint32_t k = gtid; k < n_out; k += G) {
                 const uint32_t v = a.out_node[k];
                 atomicOr(&a.bm_words[v >> 5], 1u << (v & 31));
@@ -1140,6 +1188,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     if (B.bm_words.n < (N + 31) / 32 + 1) {
         B.bm_words.alloc((N + 31) / 32 + 1);
         GX_CUDA(cudaMemsetAsync(B.bm_words.p, 0, B.bm_words.bytes(), st));
+        B.bm_top.alloc((N + 1023) / 1024 + 1);
+        GX_CUDA(cudaMemsetAsync(B.bm_top.p, 0, B.bm_top.bytes(), st));
     }
     ensure_node_arrays(ctx, N);
     // is.trace holds the flat u32 trace (inspect_fill_*)
@@ -1261,6 +1311,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.init_pos = n_init_explicit >= 0 ? is.init_pos.p : nullptr;
     a.bm_words = B.bm_words.p;
     a.nwords = (uint32_t)((N + 31) / 32);
+    a.bm_top = B.bm_top.p;
+    a.ntop = (uint32_t)((N + 1023) / 1024);
     a.bm_cnt = B.bm_cnt.p;
     a.init_ext = n_init_explicit >= 0 ? B.init_ext.p : nullptr;
     a.n_init_ext = n_init_explicit >= 0 ? (uint32_t)n_init_explicit : 0;
