@@ -234,7 +234,6 @@ constexpr uint32_t kStageFlag = 0x80000000u;
 // first use of every init slot; the other accesses come as a dense list
 // (rest_x: batch row, rest_slot: cache slot) served by the gather's DSTIDX form
 // (skip_first = true: ids = rest_x, slots = rest_slot).
-constexpr uint32_t kFirstFlag = 0x40000000u;  // inspector-internal mark of a first use
 void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_acc, uint32_t n,
                        const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch);
 bool gather_can_skip_first(uint64_t rb);

@@ -557,7 +557,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     if (nf[j]) {
                         const uint32_t x = x0 + j;
                         a.o_rest_x[k] = x;
-                        a.o_rest_slot[k] = a.acc_slot[a.next_use[x]] & ~kFirstFlag;
+                        a.o_rest_slot[k] = a.acc_slot[a.next_use[x]];
                         ++k;
                     }
                 }
@@ -1415,7 +1415,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     }
     if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");
     out->n_init = n_init_explicit >= 0 ? (uint64_t)n_init_explicit : std::min<uint64_t>(hs.n_first, Keff);
-    // all-fit with marks: first uses carry kFirstFlag in acc_slot, first_acc is valid
+    // all-fit with marks: first_acc and the rest lists are valid
     out->first_marked = a.o_first != nullptr && hs.n_first <= Keff;
     out->n_rest = out->first_marked ? A - hs.n_first : 0;
     out->h_misses.assign(m32.begin(), m32.begin() + S);
