@@ -257,8 +257,22 @@ __device__ __forceinline__ void bar_wait(uint32_t bar, uint32_t phase) {
         "r"(phase)
         : "memory");
 }
+#ifndef GX_STORE_EVICT_FIRST
+#define GX_STORE_EVICT_FIRST 1
+#endif
+// Gathered rows are written once and not read again by this step: with an L2
+// evict-first policy they do not push the cache rows out of L2 (a small cache,
+// e.g. cfg1's 51 MB, then stays L2-resident across iterations).
 __device__ __forceinline__ void bulk_store(void* dst, uint32_t buf, uint32_t bytes) {
+#if GX_STORE_EVICT_FIRST
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(dst), "r"(buf),
+                 "r"(bytes), "l"(pol)
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(buf), "r"(bytes) : "memory");
+#endif
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
 
