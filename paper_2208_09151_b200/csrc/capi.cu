@@ -504,7 +504,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         const uint64_t rb = p->f->row_bytes;
         static const uint64_t budget = (uint64_t)std::max(0, gx::env_int("GX_BATCH_BUDGET_MB", 24576)) << 20;
         const bool resident = sl.o[S] * rb <= budget;
-        const bool mark = resident && !staged_backing(p->f) && p->f->rows_dev_view && gather_can_skip_first(rb);
+        const bool mark = resident && (staged_backing(p->f) || p->f->rows_dev_view) && gather_can_skip_first(rb);
         try {
             inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, sl.o);
             inspect_run(ctx, sl.o, N, p->K, nullptr, -1, &sl.cs, true, mark, presampled ? fx_epoch : 0);
@@ -517,7 +517,10 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         std::swap(ctx->is.acc_slot, sl.acc_slot);
         // storage tier: the accesses the cache will miss read staged rows
         const bool file = staged_backing(p->f);
-        const uint64_t n_miss = file ? stage_misses(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.miss_ids, A) : 0;
+        // (an all-fit superbatch has no misses, and with the fused executor its
+        // acc_slot only holds the first uses -- nothing to stage)
+        const uint64_t n_miss =
+            file && !sl.cs.first_marked ? stage_misses(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.miss_ids, A) : 0;
         GX_CUDA(cudaEventRecord(sl.ev[2], A));
         // (3)+(4) executor on stream B, after the inspector and the previous executor
         GX_CUDA(cudaStreamWaitEvent(B, sl.ev[2], 0));
@@ -563,7 +566,9 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 const uint64_t b0 = f_file ? p->f->file->bytes.load() : p->f->xstats.bytes_sent;
                 sl.cs.init.reserve(1);
                 sl.miss_ids.reserve(1);
-                sl.ms_storage += fetch_rows(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B);
+                // all-fit (fused): each init row also lands in its first batch row
+                sl.ms_storage += fetch_rows(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B,
+                                            fused ? sl.batch.p : nullptr, fused ? sl.cs.first_acc.p : nullptr);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
                 sl.stage.reserve(std::max<uint64_t>(n_miss * rb, 16));
                 sl.ms_storage += fetch_rows(p->f, sl.miss_ids.p, n_miss, sl.stage.p, B);

@@ -282,7 +282,8 @@ __global__ void k_local_ids(const uint32_t* __restrict__ ids, const uint32_t* __
 // vectors, R rows in flight per warp
 template <int VEC>
 __global__ void k_gather_scatter(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ perm, uint64_t n,
-                                 const uint8_t* __restrict__ store, uint8_t* __restrict__ out, uint64_t rb) {
+                                 const uint8_t* __restrict__ store, uint8_t* __restrict__ out, uint64_t rb,
+                                 uint8_t* __restrict__ out2, const uint32_t* __restrict__ idx2) {
     using V = typename std::conditional<VEC == 16, uint4, uint32_t>::type;
     constexpr int R = 4;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -291,11 +292,14 @@ __global__ void k_gather_scatter(const uint32_t* __restrict__ ids, const uint32_
     for (uint64_t q0 = warp * R; q0 < n; q0 += nwarps * R) {
         const V* src[R];
         V* dst[R];
+        V* dst2[R];
 #pragma unroll
         for (int k = 0; k < R; ++k) {
             const uint64_t q = q0 + k < n ? q0 + k : q0;
+            const uint32_t j = __ldg(perm + q);
             src[k] = reinterpret_cast<const V*>(store + (uint64_t)__ldg(ids + q) * rb);
-            dst[k] = reinterpret_cast<V*>(out + (uint64_t)__ldg(perm + q) * rb);
+            dst[k] = reinterpret_cast<V*>(out + (uint64_t)j * rb);
+            dst2[k] = out2 ? reinterpret_cast<V*>(out2 + (uint64_t)__ldg(idx2 + j) * rb) : nullptr;
         }
         for (uint32_t c = lane; c < nvec; c += 32) {
             V t[R];
@@ -303,17 +307,21 @@ __global__ void k_gather_scatter(const uint32_t* __restrict__ ids, const uint32_
             for (int k = 0; k < R; ++k) t[k] = src[k][c];
 #pragma unroll
             for (int k = 0; k < R; ++k)
-                if (q0 + k < n) dst[k][c] = t[k];
+                if (q0 + k < n) {
+                    dst[k][c] = t[k];
+                    if (out2) dst2[k][c] = t[k];
+                }
         }
     }
 }
 
 static void launch_gather_scatter(const uint32_t* ids, const uint32_t* perm, uint64_t n, const uint8_t* store,
-                                  uint8_t* out, uint64_t rb, int num_sms, cudaStream_t s) {
+                                  uint8_t* out, uint64_t rb, int num_sms, cudaStream_t s, uint8_t* out2,
+                                  const uint32_t* idx2) {
     if (!n) return;
     const unsigned blocks = (unsigned)std::min<uint64_t>((n * 8 + 255) / 256, (uint64_t)num_sms * 8);
-    if (rb % 16 == 0) k_gather_scatter<16><<<blocks, 256, 0, s>>>(ids, perm, n, store, out, rb);
-    else k_gather_scatter<4><<<blocks, 256, 0, s>>>(ids, perm, n, store, out, rb);
+    if (rb % 16 == 0) k_gather_scatter<16><<<blocks, 256, 0, s>>>(ids, perm, n, store, out, rb, out2, idx2);
+    else k_gather_scatter<4><<<blocks, 256, 0, s>>>(ids, perm, n, store, out, rb, out2, idx2);
     GX_CHECK_LAUNCH();
 }
 
@@ -324,7 +332,8 @@ static Bounds make_bounds(uint64_t N, int P) {
     return b;
 }
 
-double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s) {
+double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s,
+                  uint8_t* out2, const uint32_t* idx2) {
     const auto t0 = std::chrono::steady_clock::now();
     gx_ctx* ctx = f->ctx;
     Transport& T = *f->comm->t;
@@ -390,7 +399,8 @@ double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_
         T.alltoallv((const uint8_t*)x.send_ids.p, so.data(), sb.data(), (uint8_t*)x.recv_ids.p, ro.data(), rbb.data(),
                     s);
     // (3a) own requests: local row -> request position in one pass
-    launch_gather_scatter(x.send_ids.p + soff[me], perm + soff[me], scnt[me], f->dev.p, d_out, rb, ctx->num_sms, s);
+    launch_gather_scatter(x.send_ids.p + soff[me], perm + soff[me], scnt[me], f->dev.p, d_out, rb, ctx->num_sms, s,
+                          out2, idx2);
     // (3b) serve the other ranks' requests from this rank's partition (local ids)
     x.send_rows.reserve(std::max<uint64_t>(nrecv * rb, 16));
     x.dummy.reserve(8);
@@ -416,9 +426,9 @@ double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_
     }
     if (P > 1) {
         T.alltoallv(x.send_rows.p, so.data(), sb.data(), x.recv_rows.p, ro.data(), rbb.data(), s);
-        launch_scatter_rows(x.recv_rows.p, perm, soff[me], d_out, rb, ctx->num_sms, s);
+        launch_scatter_rows(x.recv_rows.p, perm, soff[me], d_out, rb, ctx->num_sms, s, out2, idx2);
         const uint64_t tail = soff[me] + scnt[me];
-        launch_scatter_rows(x.recv_rows.p + tail * rb, perm + tail, n - tail, d_out, rb, ctx->num_sms, s);
+        launch_scatter_rows(x.recv_rows.p + tail * rb, perm + tail, n - tail, d_out, rb, ctx->num_sms, s, out2, idx2);
     }
     // counters
     f->xstats.calls += 1;

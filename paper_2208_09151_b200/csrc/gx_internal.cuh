@@ -242,7 +242,9 @@ bool gather_can_skip_first(uint64_t rb);
 // copies them to HBM on the features' copy stream and scatters them to their
 // rows on `s`; returns when everything is enqueued (work on `s` after the call
 // sees the rows). Returns the host read wall time in ms.
-double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s);
+// out2/idx2 (optional): row j also goes to out2 row idx2[j]
+double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s,
+                   uint8_t* out2 = nullptr, const uint32_t* idx2 = nullptr);
 // Misses of a resolved access list: miss_ids[r] = ids[k] for the r-th k with
 // slots[k] == kNever (access order), slots[k] := kStageFlag | r. Returns the
 // count (synchronises `s`).
@@ -251,21 +253,23 @@ uint64_t stage_misses(gx_ctx* ctx, const uint32_t* ids, uint32_t* slots, uint64_
 // Row-partitioned table (comm.cu): the same contract as stage_fetch, served by
 // the owners through one variable all-to-all. Collective (call on every rank,
 // also with n == 0).
-double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s);
+double part_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s,
+                  uint8_t* out2 = nullptr, const uint32_t* idx2 = nullptr);
 // storage tiers that deliver rows through staging (FILE, PARTITIONED)
 inline bool staged_backing(const gx_features* f) {
     return f->backing == GX_BACKING_FILE || f->backing == GX_BACKING_PARTITIONED;
 }
 // d_out row j <- feature row d_ids[j] through the table's staged tier
-inline double fetch_rows(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s) {
-    return f->backing == GX_BACKING_PARTITIONED ? part_fetch(f, d_ids, n, d_out, s)
-                                                : stage_fetch(f, d_ids, n, d_out, s);
+inline double fetch_rows(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s,
+                         uint8_t* out2 = nullptr, const uint32_t* idx2 = nullptr) {
+    return f->backing == GX_BACKING_PARTITIONED ? part_fetch(f, d_ids, n, d_out, s, out2, idx2)
+                                                : stage_fetch(f, d_ids, n, d_out, s, out2, idx2);
 }
 // feature_value rows [node0, node0 + n) (graph.cu), scalar_width 4 or 2
 void launch_features(uint8_t* out, uint64_t n, uint32_t dim, uint32_t sw, uint64_t vseed, uint64_t node0,
                      int num_sms, cudaStream_t s);
 // k_scatter_rows launcher (storage.cu): out row dst_idx[q] <- src row q
 void launch_scatter_rows(const uint8_t* src, const uint32_t* dst_idx, uint64_t cnt, uint8_t* out, uint64_t rb,
-                         int num_sms, cudaStream_t s);
+                         int num_sms, cudaStream_t s, uint8_t* out2 = nullptr, const uint32_t* idx2 = nullptr);
 
 }  // namespace gx

@@ -170,26 +170,35 @@ __global__ void k_iota32(uint32_t* p, uint64_t n) {
 }
 
 // out row dst_idx[q] <- landing row q (one warp per row, 16-byte vectors).
+// out2 != nullptr: the row also goes to out2 row idx2[dst_idx[q]] (the
+// fused all-fit executor: an init row's slot and its first batch row)
 template <int VEC>
 __global__ void k_scatter_rows(const uint8_t* __restrict__ land, const uint32_t* __restrict__ dst_idx, uint64_t cnt,
-                               uint8_t* __restrict__ out, uint64_t rb) {
+                               uint8_t* __restrict__ out, uint64_t rb, uint8_t* __restrict__ out2,
+                               const uint32_t* __restrict__ idx2) {
     using V = typename std::conditional<VEC == 16, uint4, uint32_t>::type;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t lane = threadIdx.x & 31, nvec = (uint32_t)(rb / VEC);
     for (uint64_t q = warp; q < cnt; q += nwarps) {
+        const uint32_t j = __ldg(dst_idx + q);
         const V* s = reinterpret_cast<const V*>(land + q * rb);
-        V* d = reinterpret_cast<V*>(out + (uint64_t)__ldg(dst_idx + q) * rb);
-        for (uint32_t c = lane; c < nvec; c += 32) d[c] = s[c];
+        V* d = reinterpret_cast<V*>(out + (uint64_t)j * rb);
+        V* d2 = out2 ? reinterpret_cast<V*>(out2 + (uint64_t)__ldg(idx2 + j) * rb) : nullptr;
+        for (uint32_t c = lane; c < nvec; c += 32) {
+            const V v = s[c];
+            d[c] = v;
+            if (d2) d2[c] = v;
+        }
     }
 }
 
 void launch_scatter_rows(const uint8_t* src, const uint32_t* dst_idx, uint64_t cnt, uint8_t* out, uint64_t rb,
-                         int num_sms, cudaStream_t s) {
+                         int num_sms, cudaStream_t s, uint8_t* out2, const uint32_t* idx2) {
     if (!cnt) return;
     const unsigned blocks = (unsigned)std::min<uint64_t>((cnt * 32 + 255) / 256, (uint64_t)num_sms * 8);
-    if (rb % 16 == 0) k_scatter_rows<16><<<blocks, 256, 0, s>>>(src, dst_idx, cnt, out, rb);
-    else k_scatter_rows<4><<<blocks, 256, 0, s>>>(src, dst_idx, cnt, out, rb);
+    if (rb % 16 == 0) k_scatter_rows<16><<<blocks, 256, 0, s>>>(src, dst_idx, cnt, out, rb, out2, idx2);
+    else k_scatter_rows<4><<<blocks, 256, 0, s>>>(src, dst_idx, cnt, out, rb, out2, idx2);
     GX_CHECK_LAUNCH();
 }
 
@@ -199,7 +208,8 @@ static int key_bits(uint64_t n) {
     return b;
 }
 
-double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s) {
+double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d_out, cudaStream_t s,
+                   uint8_t* out2, const uint32_t* idx2) {
     if (!n) return 0.0;
     if (!f->file || !f->ctx) fail(GX_INVALID_ARGUMENT, "stage_fetch needs a GX_BACKING_FILE table with a context");
     gx_ctx* ctx = f->ctx;
@@ -261,7 +271,7 @@ double stage_fetch(gx_features* f, const uint32_t* d_ids, uint64_t n, uint8_t* d
         GX_CUDA(cudaEventRecord(st.ev_h2d[b], st.copy));
         f->file->h2d.fetch_add(cnt * rb, std::memory_order_relaxed);
         GX_CUDA(cudaStreamWaitEvent(s, st.ev_h2d[b], 0));
-        launch_scatter_rows(st.land[b].p, perm + c0, cnt, d_out, rb, ctx->num_sms, s);
+        launch_scatter_rows(st.land[b].p, perm + c0, cnt, d_out, rb, ctx->num_sms, s, out2, idx2);
         GX_CUDA(cudaEventRecord(st.ev_free[b], s));
         used[b] = true;
     }
