@@ -35,7 +35,11 @@
 namespace gx {
 
 constexpr int IN_THREADS = 512;  // half an SM: the executor shares the SMs
-constexpr uint32_t IN_TILE = IN_THREADS * 4;
+#ifndef GX_IN_IPT
+#define GX_IN_IPT 4
+#endif
+constexpr int IN_IPT = GX_IN_IPT;  // accesses per thread per tile (loads in flight)
+constexpr uint32_t IN_TILE = IN_THREADS * IN_IPT;
 constexpr uint32_t SORT_SMALL = 4096;
 constexpr uint32_t kMaxIters = 4096;
 
@@ -288,9 +292,9 @@ __device__ bool next_use_pass(const IArgs& a, SM& sm, bool firsts) {
         if (a.st->err) return false;  // host reports the exact reference error
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
-            const uint32_t x0 = t * IN_TILE + tid * 4;
+            const uint32_t x0 = t * IN_TILE + tid * IN_IPT;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < IN_IPT; ++j) {
                 const uint32_t x = x0 + j;
                 if (x < a.A) {
                     const uint32_t v = a.trace[x];
@@ -343,9 +347,9 @@ __device__ bool next_use_pass(const IArgs& a, SM& sm, bool firsts) {
         if (a.st->err) return false;
         for (uint32_t t = blockIdx.x; firsts && t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
-            const uint32_t x0 = t * IN_TILE + tid * 4;
+            const uint32_t x0 = t * IN_TILE + tid * IN_IPT;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < IN_IPT; ++j) {
                 const uint32_t x = x0 + j;
                 if (x < a.A) {
                     const uint8_t f = a.last[a.trace[x]] == iter_of(sm, S, x);
@@ -410,18 +414,18 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         ISTAMP(a, 1);
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
             uint32_t c = 0;
-            const uint32_t x0 = t * IN_TILE + tid * 4;
-            uint32_t v[4], fx[4];
+            const uint32_t x0 = t * IN_TILE + tid * IN_IPT;
+            uint32_t v[IN_IPT], fx[IN_IPT];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = x0 + j < a.A ? a.trace[x0 + j] : 0;
+            for (int j = 0; j < IN_IPT; ++j) v[j] = x0 + j < a.A ? a.trace[x0 + j] : 0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) fx[j] = x0 + j < a.A ? a.fx_epoch - a.firstx[v[j]] : 0;
+            for (int j = 0; j < IN_IPT; ++j) fx[j] = x0 + j < a.A ? a.fx_epoch - a.firstx[v[j]] : 0;
             if (a.fx_sampled) {  // key (iteration << 21 | position) -> access index
 #pragma unroll
-                for (int j = 0; j < 4; ++j) fx[j] = sm.toff[fx[j] >> 21] + (fx[j] & 0x1FFFFFu);
+                for (int j = 0; j < IN_IPT; ++j) fx[j] = sm.toff[fx[j] >> 21] + (fx[j] & 0x1FFFFFu);
             }
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < IN_IPT; ++j) {
                 const uint32_t x = x0 + j;
                 if (x < a.A) {
                     const uint8_t f = fx[j] == x;
@@ -466,10 +470,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         // and node_slot is never touched
         const bool fit = a.trusted && *(volatile uint32_t*)&a.st->n_first <= K;
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            uint32_t fl[4], c = 0;
-            const uint32_t x0 = t * IN_TILE + tid * 4;
+            uint32_t fl[IN_IPT], c = 0;
+            const uint32_t x0 = t * IN_TILE + tid * IN_IPT;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < IN_IPT; ++j) {
                 const uint32_t x = x0 + j;
                 fl[j] = x < a.A ? a.isfirst[x] : 0;
                 c += fl[j];
@@ -477,7 +481,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             uint32_t tot;
             uint32_t r = a.tile_cnt[t] + block_excl_scan(c, sm.scan, tot);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < IN_IPT; ++j) {
                 if (fl[j]) {
                     const uint32_t x = x0 + j;
                     const uint32_t v = a.trace[x];
@@ -503,9 +507,9 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     } else {
         // explicit init (simulate_changesets' `init`): key = first access iteration
         for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const uint32_t x0 = t * IN_TILE + tid * 4;
+            const uint32_t x0 = t * IN_TILE + tid * IN_IPT;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < IN_IPT; ++j) {
                 const uint32_t x = x0 + j;
                 if (x < a.A && a.isfirst[x]) {
                     const uint32_t v = a.trace[x];
@@ -542,10 +546,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             // fused executor: the non-first accesses as a dense list (rank =
             // position minus the first uses before it: tile_cnt + in-tile scan)
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                uint32_t nf[4], c = 0;
-                const uint32_t x0 = t * IN_TILE + tid * 4;
+                uint32_t nf[IN_IPT], c = 0;
+                const uint32_t x0 = t * IN_TILE + tid * IN_IPT;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < IN_IPT; ++j) {
                     const uint32_t x = x0 + j;
                     nf[j] = x < a.A ? (a.isfirst[x] ? 0u : 1u) : 0u;
                     c += nf[j];
@@ -553,7 +557,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 uint32_t tot;
                 uint32_t k = t * IN_TILE - a.tile_cnt[t] + block_excl_scan(c, sm.scan, tot);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < IN_IPT; ++j) {
                     if (nf[j]) {
                         const uint32_t x = x0 + j;
                         a.o_rest_x[k] = x;
