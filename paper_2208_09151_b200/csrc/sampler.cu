@@ -33,7 +33,10 @@ namespace cg = cooperative_groups;
 namespace gx {
 
 constexpr int kMaxLayers = 16;
-constexpr int SB_THREADS = 512;
+#ifndef GX_SB_THREADS
+#define GX_SB_THREADS 256  // 256 x 4 CTAs/SM: 1.96 vs 2.00 ms (512 x 2), 1.98 (128 x 8), 2.14 (1024 x 1)
+#endif
+constexpr int SB_THREADS = GX_SB_THREADS;
 #ifndef GX_SB_IPT
 #define GX_SB_IPT 1  // parents per thread per tile (512-parent tiles: 2.00 vs 2.11 ms against 2)
 #endif
@@ -53,11 +56,11 @@ constexpr int SB_IPT = GX_SB_IPT;
 #ifndef GX_E_LOADFIRST
 #define GX_E_LOADFIRST 1
 #endif
-// Two 512-thread CTAs per SM (64 registers, a few spills): twice the warps to
-// hide the dependent random reads; measured 2.60 vs 2.86 ms per papers
-// superbatch against one CTA per SM at 128 registers.
+// 1024 threads per SM at 64 registers (a few spills): twice the warps of the
+// 128-register build to hide the dependent random reads (measured 2.60 vs
+// 2.86 ms per papers superbatch), split into four 256-thread CTAs.
 #ifndef GX_SB_MINB
-#define GX_SB_MINB 2
+#define GX_SB_MINB (1024 / GX_SB_THREADS)
 #endif
 #define GX_SB_BOUNDS __launch_bounds__(SB_THREADS, GX_SB_MINB)
 constexpr uint32_t SB_TILE = SB_THREADS * SB_IPT;
