@@ -465,7 +465,7 @@ def main():
     g_row = 2 * w + 8                                         # read row + write row + u32 id + u32 slot
     alg_bytes = g_row * rows_g
     peak, peak_src = measured_peaks()
-    achieved = alg_bytes / (gk_ms / 1e3) / 1e9
+    achieved = alg_bytes / (gk_ms / 1e3) / 1e9 if gk_ms and alg_bytes else 0.0
     traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
@@ -481,6 +481,8 @@ def main():
                 "alg_bytes_per_superbatch": bytes_tot / n, "alg_bytes": bytes_formula}
 
     fused = any(s.fused_fill for s in stats)
+    fan = any(s.fan_out for s in stats)
+    staged = args.backing == "file" or comm is not None
     lists = sum(s.sample_io.neighbor_lists_read for s in stats)
     C = sum(s.total_in + s.total_out for s in stats)
     fills = sum(s.fill_rows for s in stats)
@@ -491,13 +493,39 @@ def main():
         line("k_flatten + k_inspect (stage: inspector)", sum(s.ms_inspect for s in stats),
              24 * rows + 16 * C + 8 * fills, "24*A + 16*C + 8*|init| (SURVEY 8d)",
              "latency (random node-array atomics, grid barriers)"),
-        line("k_fill_first (switch fused with first uses)" if fused else "k_gather_rows<16,8> (switch: cache init)",
-             sum(s.ms_switch for s in stats), (3 * w + 8 if fused else 2 * w + 4) * fills,
-             "(3w + 8) per init row: read row, write slot + first batch row, 2 ids" if fused
-             else "(2w + 4) per init row: read row, write slot, id"),
-        line("k_gather_tma2 (bulk-copy row gather)", gk_ms, alg_bytes,
-             "(2w + 8) per row: read row, write row, u32 id + u32 slot"),
     ]
+    fan_kernel = fan_bytes = fan_ms = None
+    if fan and not staged:      # switch + every access in one kernel
+        fan_kernel = "k_fan_rows (switch fanned out to every access)"
+        fan_ms = sum(s.ms_switch for s in stats)
+        fan_bytes = (2 * w + 8) * fills + (w + 4) * rows
+        rooflines.append(line(fan_kernel, fan_ms, fan_bytes,
+                              "(2w + 8) per init row (read row, write slot, id + offset) + (w + 4) per access "
+                              "(write batch row, list entry)"))
+    elif fan:                   # staged tiers: the filled cache fans out
+        rooflines.append(line("switch (storage / exchange scatter into slots)", sum(s.ms_switch for s in stats),
+                              (w + 4) * fills, "(w + 4) per init row: write slot, id (device side)"))
+        fan_kernel = "k_fan_rows (cache rows fanned out to every access)"
+        fan_ms = gk_ms
+        fan_bytes = (w + 4) * fills + (w + 4) * rows
+        rooflines.append(line(fan_kernel, fan_ms, fan_bytes,
+                              "(w + 4) per init row (read slot row, offset) + (w + 4) per access "
+                              "(write batch row, list entry)"))
+    else:
+        rooflines += [
+            line("k_fill_first (switch fused with first uses)" if fused else "k_gather_rows<16,8> (switch: cache init)",
+                 sum(s.ms_switch for s in stats), (3 * w + 8 if fused else 2 * w + 4) * fills,
+                 "(3w + 8) per init row: read row, write slot + first batch row, 2 ids" if fused
+                 else "(2w + 4) per init row: read row, write slot, id"),
+            line("k_gather_tma2 (bulk-copy row gather)", gk_ms, alg_bytes,
+                 "(2w + 8) per row: read row, write row, u32 id + u32 slot"),
+        ]
+    if fan:                     # the headline roofline is the fan-out kernel
+        achieved = fan_bytes / (fan_ms / 1e3) / 1e9
+        traffic = None
+        if os.path.exists(tp):
+            with open(tp) as fh:
+                traffic = json.load(fh).get("k_fan_dram_bytes_per_launch")
     S = cfg["S"]
     stages = {
         "sample_ms": sum(s.ms_sample for s in stats) / n,
@@ -511,6 +539,7 @@ def main():
         "gathered_feature_GBps": w * rows / (sum(s.ms_switch + s.ms_gather for s in stats) / 1e3) / 1e9,
         "gather_kernel_rows_per_superbatch": rows_g / n,
         "fused_fill": fused,
+        "fan_out": fan,
         "accesses_per_superbatch": rows / n,
         "miss_ratio": sum(s.total_misses for s in stats) / max(rows, 1),
         "init_size": stats[-1].init_size,
@@ -558,14 +587,22 @@ def main():
                 "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
                 "d2h_bytes_per_step": int(8 * S + 8 * 16)},
         "gpu_launches": int(sum(s.kernel_launches for s in stats)),
-        "roofline": {"kernel": "k_gather_tma2 (bulk-copy row gather)", "bound": "hbm", "achieved": achieved,
-                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "peak_source": peak_src,
-                     "bytes_per_row": g_row,
-                     "rows_per_launch": rows_g / max(1, sum(s.gather_launches for s in stats)),
-                     "alg_bytes_per_launch": alg_bytes / max(1, sum(s.gather_launches for s in stats)),
-                     "note": ("all-fit superbatches: the switch kernel also writes each init node's first-use "
-                              "batch row, the gather moves the other accesses" if fused else None)},
+        "roofline": ({"kernel": fan_kernel, "bound": "hbm", "achieved": achieved,
+                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                      "peak_source": peak_src,
+                      "init_rows_per_launch": fills / n, "accesses_per_launch": rows / n,
+                      "alg_bytes_per_launch": fan_bytes / n,
+                      "note": "all-fit superbatches: one launch per superbatch reads each init row once and "
+                              "writes it to its cache slot and to the batch row of every access of its node"}
+                     if fan else
+                     {"kernel": "k_gather_tma2 (bulk-copy row gather)", "bound": "hbm", "achieved": achieved,
+                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                      "peak_source": peak_src,
+                      "bytes_per_row": g_row,
+                      "rows_per_launch": rows_g / max(1, sum(s.gather_launches for s in stats)),
+                      "alg_bytes_per_launch": alg_bytes / max(1, sum(s.gather_launches for s in stats)),
+                      "note": ("all-fit superbatches: the switch kernel also writes each init node's first-use "
+                               "batch row, the gather moves the other accesses" if fused else None)}),
         "rooflines": rooflines,
         "stages": stages,
         "clocks": clk.summary(),

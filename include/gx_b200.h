@@ -339,10 +339,12 @@ typedef struct gx_pipeline_stats {
     uint64_t storage_bytes;    /* bytes read from storage (whole pages) */
     /* executor kernel work, for roofline accounting */
     uint64_t fill_rows;        /* rows the switch wrote into cache slots (= init_size) */
-    uint64_t gather_kernel_rows; /* rows the gather launches moved (all accesses, or with
-                                    fused_fill the accesses that are not an init node's first use) */
-    uint32_t fused_fill;       /* 1: all-fit superbatch, the switch also wrote each init node's
-                                  first-use batch row */
+    uint64_t gather_kernel_rows; /* rows the gather launches moved (all accesses; fused_fill 1:
+                                    the accesses that are not an init node's first use; fused_fill 2:
+                                    0, or all accesses fanned out from the cache on staged tiers) */
+    uint32_t fused_fill;       /* all-fit superbatch: 1 = the switch also wrote each init node's
+                                  first-use batch row; 2 = fan-out: each init row was read once and
+                                  written to its slot and to every batch row of its node */
     uint32_t reserved0;
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,

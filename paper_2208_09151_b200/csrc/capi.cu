@@ -504,7 +504,12 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         const uint64_t rb = p->f->row_bytes;
         static const uint64_t budget = (uint64_t)std::max(0, gx::env_int("GX_BATCH_BUDGET_MB", 24576)) << 20;
         const bool resident = sl.o[S] * rb <= budget;
-        const bool mark = resident && (staged_backing(p->f) || p->f->rows_dev_view) && gather_can_skip_first(rb);
+        // fan-out form (default): each init row read once, written to its slot
+        // and every batch row of its node; GX_FANOUT=0: fill + first use, then
+        // a gather of the other accesses from the cache
+        static const bool fan = gx::env_int("GX_FANOUT", 1) != 0;
+        const bool src_ok = staged_backing(p->f) || p->f->rows_dev_view;
+        const int mark = !resident || !src_ok ? 0 : fan && rb % 16 == 0 ? 2 : gather_can_skip_first(rb) ? 1 : 0;
         try {
             inspect_fill_from_device(ctx, p->samples.ids.p, p->samples.cap_ids, sl.o);
             inspect_run(ctx, sl.o, N, p->K, nullptr, -1, &sl.cs, true, mark, presampled ? fx_epoch : 0);
@@ -531,7 +536,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         sl.full = resident;
         const bool fused = sl.cs.first_marked;  // implies all-fit (no changesets) and resident
         sl.fused = fused;
-        sl.gather_rows = fused ? sl.cs.n_rest : sl.o[S];
+        sl.gather_rows = fused ? (sl.cs.fan ? (file ? sl.o[S] : 0) : sl.cs.n_rest) : sl.o[S];
         sl.batch.reserve(std::max<uint64_t>((sl.full ? sl.o[S] : maxw) * rb, 16));
         sl.h_off.reserve(S + 1);
         sl.d_off.reserve(S + 1);
@@ -567,14 +572,22 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 sl.cs.init.reserve(1);
                 sl.miss_ids.reserve(1);
                 // all-fit (fused): each init row also lands in its first batch row
+                // (fan-out form: the cache rows fan out to all batch rows below)
+                const bool dual = fused && !sl.cs.fan;
                 sl.ms_storage += fetch_rows(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B,
-                                            fused ? sl.batch.p : nullptr, fused ? sl.cs.first_acc.p : nullptr);
+                                            dual ? sl.batch.p : nullptr, dual ? sl.cs.first_acc.p : nullptr);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
                 sl.stage.reserve(std::max<uint64_t>(n_miss * rb, 16));
                 sl.ms_storage += fetch_rows(p->f, sl.miss_ids.p, n_miss, sl.stage.p, B);
                 store = sl.stage.p;
                 sl.storage_rows = (f_file ? p->f->file->rows.load() : p->f->xstats.rows_requested) - r0;
                 sl.storage_bytes = (f_file ? p->f->file->bytes.load() : p->f->xstats.bytes_sent) - b0;
+            } else if (fused && sl.cs.fan) {
+                // the switch fused with every access: one read of each backing
+                // row, written to its slot and to all batch rows of its node
+                launch_fan_rows(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, p->f->rows_dev_view, rb, p->cache_rows.p,
+                                sl.cs.fan_off.p, sl.cs.fan_list.p, sl.batch.p);
+                GX_CUDA(cudaEventRecord(sl.ev[4], B));
             } else if (fused) {
                 // the switch fused with every init node's first use: one read of
                 // the backing row, written to its slot and to its first batch row
@@ -596,8 +609,16 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             uint64_t nseg = 0;
             if (fused) {  // one launch: every access that is not a first use
                 GX_CUDA(cudaEventRecord(sl.kev[0], B));
-                launch_gather_resolved(ctx, sl.cs.rest_x.p, sl.cs.rest_slot.p, sl.cs.n_rest, p->cache_rows.p,
-                                       store, rb, sl.batch.p, sl.counters.p + 8 * S, nullptr, 0, false, true);
+                if (sl.cs.fan) {
+                    // staged tiers: the filled cache rows fan out to the batch
+                    // rows (device-backed tables did this in the switch)
+                    if (file)
+                        launch_fan_rows(ctx, nullptr, (uint32_t)sl.cs.n_init, p->cache_rows.p, rb, nullptr,
+                                        sl.cs.fan_off.p, sl.cs.fan_list.p, sl.batch.p);
+                } else {
+                    launch_gather_resolved(ctx, sl.cs.rest_x.p, sl.cs.rest_slot.p, sl.cs.n_rest, p->cache_rows.p,
+                                           store, rb, sl.batch.p, sl.counters.p + 8 * S, nullptr, 0, false, true);
+                }
                 GX_CUDA(cudaEventRecord(sl.kev[1], B));
                 if (p->digest)
                     for (uint64_t k = 0; k < S; ++k)
@@ -707,7 +728,7 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             stats->gather_launches = sl.nseg;
             stats->fill_rows = sl.cs.n_init;
             stats->gather_kernel_rows = sl.gather_rows;
-            stats->fused_fill = sl.fused ? 1u : 0u;
+            stats->fused_fill = sl.fused ? (sl.cs.fan ? 2u : 1u) : 0u;
             stats->reserved0 = 0;
             stats->ms_storage = sl.ms_storage;
             stats->storage_rows = sl.storage_rows;

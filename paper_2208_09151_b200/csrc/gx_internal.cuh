@@ -142,8 +142,13 @@ struct gx_changesets {
     gx::DevBuf<uint32_t> out_ids;   // total out (sorted per iteration)
     gx::DevBuf<uint32_t> first_acc; // all-fit: access index of each init slot's first use
     gx::DevBuf<uint32_t> rest_x, rest_slot;  // all-fit: the other accesses and their slots
+    // all-fit, fan-out form: the accesses of init slot r are
+    // fan_list[fan_off[r] .. fan_off[r + 1]) (first use included)
+    gx::DevBuf<uint32_t> fan_cnt, fan_rank, fan_off, fan_list;
+    gx::DevBuf<uint8_t> cub_tmp;
     uint64_t n_rest = 0;
-    bool first_marked = false;      // first_acc / rest_* valid (pipeline only)
+    bool first_marked = false;      // first_acc / rest_* (or fan_*) valid (pipeline only)
+    bool fan = false;               // fan_off / fan_list valid
     std::vector<uint64_t> h_in_off, h_out_off, h_misses;  // S+1, S+1, S
 };
 
@@ -198,7 +203,7 @@ void inspect_fill_from_host(gx_ctx* ctx, const uint64_t* flat, const std::vector
 // presampled_epoch != 0: the sampler already filled firstx with (b << 21 | local) keys
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
                  const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
-                 bool mark_first = false, uint32_t presampled_epoch = 0);
+                 int mark_first = 0, uint32_t presampled_epoch = 0);
 void access_index_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t* h_iters,
                       uint64_t* h_ptr);
 
@@ -236,6 +241,12 @@ constexpr uint32_t kStageFlag = 0x80000000u;
 // (skip_first = true: ids = rest_x, slots = rest_slot).
 void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_acc, uint32_t n,
                        const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch);
+// Fan-out form (mark_first = 2): each init row is read once and written to its
+// cache slot (cache_rows != nullptr) and to every batch row of its accesses,
+// batch row fan_list[j] for j in [off[r], off[r + 1]). idx == nullptr: source
+// row r is row r of `src` (the staged tiers fan out from the filled cache).
+void launch_fan_rows(gx_ctx* ctx, const uint32_t* idx, uint32_t n, const uint8_t* src, uint64_t rb,
+                     uint8_t* cache_rows, const uint32_t* off, const uint32_t* list, uint8_t* batch);
 bool gather_can_skip_first(uint64_t rb);
 // d_out row j <- feature row d_ids[j] from storage, for j in [0, n). Sorts the
 // requests by id on `s`, reads page runs on the host into pinned chunks,

@@ -101,6 +101,8 @@ struct IArgs {
     uint32_t* o_first;   // all-fit + mark_first: access index of each init slot's first use
     uint32_t* o_rest_x;  // all-fit + mark_first: accesses that are not a first use (dense) ...
     uint32_t* o_rest_slot;  // ... and their cache slots
+    uint32_t* o_fan_cnt;    // all-fit + fan-out marks: accesses per init slot (K + 1) ...
+    uint32_t* o_fan_rank;   // ... and each access's rank among its slot's accesses (A)
     uint32_t* o_in_ids;
     uint32_t* o_in_pos;
     uint32_t* o_in_slot;
@@ -495,6 +497,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         if (fit) {
                             a.acc_slot[x] = r;
                             if (a.o_first) a.o_first[r] = x;
+                            if (a.o_fan_cnt) {  // the first use is rank 0 of its slot
+                                a.o_fan_cnt[r] = 1;
+                                a.o_fan_rank[x] = 0;
+                            }
                         } else {
                             a.node_slot[v] = (int32_t)r;
                         }
@@ -542,7 +548,18 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     // served by its init slot.
     const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
     if (allfit) {
-        if (a.trusted && a.o_first) {
+        if (a.trusted && a.o_fan_cnt) {
+            // fan-out executor: every other access takes the next rank of its
+            // slot (L2-resident counters: K words); the host turns the counts
+            // into offsets and places each access at off[slot] + rank
+            for (uint32_t x = gtid; x < a.A; x += G) {
+                if (a.isfirst[x]) continue;
+                const uint32_t s = a.acc_slot[a.next_use[x]];
+                a.acc_slot[x] = s;
+                a.o_fan_rank[x] = atomicAdd(&a.o_fan_cnt[s], 1u);
+            }
+            if (gtid == 0) a.o_fan_cnt[*(volatile uint32_t*)&a.st->n_first] = 0;  // scan sentinel
+        } else if (a.trusted && a.o_first) {
             // fused executor: the non-first accesses as a dense list (rank =
             // position minus the first uses before it: tile_cnt + in-tile scan)
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -1174,9 +1191,16 @@ uint32_t inspect_reserve_epoch(gx_ctx* ctx, uint64_t N, uint64_t keyrange) {
     return (uint32_t)is.fx_base;
 }
 
+// fan-out lists: access x goes to position off[slot(x)] + rank(x) of its slot's list
+__global__ void k_fan_place(const uint32_t* __restrict__ acc_slot, const uint32_t* __restrict__ rank,
+                            const uint32_t* __restrict__ off, uint32_t A, uint32_t* __restrict__ list) {
+    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < A; x += gridDim.x * blockDim.x)
+        list[__ldg(off + __ldg(acc_slot + x)) + __ldg(rank + x)] = x;
+}
+
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
                  const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
-                 bool mark_first, uint32_t presampled_epoch) {
+                 int mark_first, uint32_t presampled_epoch) {
     const uint64_t S = off.size() - 1;
     if (S > kMaxIters) fail(GX_INVALID_ARGUMENT, "at most 4096 iterations per superbatch");
     if (N >= 0xFFFFFFFFull) fail(GX_OVERFLOW, "num_nodes exceeds the u32 device id range");
@@ -1324,7 +1348,13 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.o_init = out->init.p;
     a.o_first = nullptr;
     a.o_rest_x = a.o_rest_slot = nullptr;
-    if (mark_first && a.trusted) {
+    a.o_fan_cnt = a.o_fan_rank = nullptr;
+    if (mark_first == 2 && a.trusted) {
+        out->fan_cnt.reserve(Keff + 1);
+        out->fan_rank.reserve(A + 1);
+        a.o_fan_cnt = out->fan_cnt.p;
+        a.o_fan_rank = out->fan_rank.p;
+    } else if (mark_first && a.trusted) {
         out->first_acc.reserve(Keff + 1);
         out->rest_x.reserve(A + 1);
         out->rest_slot.reserve(A + 1);
@@ -1419,9 +1449,24 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     }
     if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");
     out->n_init = n_init_explicit >= 0 ? (uint64_t)n_init_explicit : std::min<uint64_t>(hs.n_first, Keff);
-    // all-fit with marks: first_acc and the rest lists are valid
-    out->first_marked = a.o_first != nullptr && hs.n_first <= Keff;
+    // all-fit with marks: first_acc and the rest lists (or the fan-out lists) are valid
+    out->first_marked = (a.o_first != nullptr || a.o_fan_cnt != nullptr) && hs.n_first <= Keff;
+    out->fan = out->first_marked && a.o_fan_cnt != nullptr;
     out->n_rest = out->first_marked ? A - hs.n_first : 0;
+    if (out->fan) {  // slot -> its accesses: offsets by a scan of the counts, then placement
+        const uint32_t n = (uint32_t)hs.n_first;
+        out->fan_off.reserve((uint64_t)n + 1);
+        out->fan_list.reserve(A + 1);
+        size_t tb = 0;
+        GX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
+        out->cub_tmp.reserve(tb + 16);
+        GX_CUDA(cub::DeviceScan::ExclusiveSum(out->cub_tmp.p, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
+        if (A) {
+            k_fan_place<<<ctx->num_sms * 4, 256, 0, st>>>(is.acc_slot.p, out->fan_rank.p, out->fan_off.p,
+                                                         (uint32_t)A, out->fan_list.p);
+            GX_CHECK_LAUNCH();
+        }
+    }
     out->h_misses.assign(m32.begin(), m32.begin() + S);
     out->h_in_off.assign(S + 1, 0);
     out->h_out_off.assign(S + 1, 0);

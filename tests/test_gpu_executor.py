@@ -299,3 +299,48 @@ def test_pipeline_fp16_768(gx, oracle, K):
     for i, ids in enumerate(trace):
         assert np.array_equal(p.batch(i), rows[ids.astype(np.int64)])
     assert st.fused_fill == (K >= len(np.unique(np.concatenate(trace))))
+
+
+@pytest.mark.parametrize("fanout", [1, 0])
+def test_allfit_fan_out_forms(gx, oracle, fanout):
+    """All-fit superbatch through both fused executors: the fan-out form (each
+    init row read once, written to its slot and to every batch row of its node;
+    64 iterations over a 500-node graph, so hub slots own more than 32 batch rows
+    and the per-warp list spans more than one 32-entry window) and the older
+    fill-first + rest-gather form (GX_FANOUT=0, in a subprocess). Batches must
+    be byte-identical to the rows of the oracle's trace."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import textwrap
+    n, dim, S = 500, 32, 64
+    code = textwrap.dedent(f"""
+        import json, numpy as np
+        import paper_2208_09151_b200 as gx
+        from oracle import C as oracle
+        ip, ind = oracle.rmat_graph({n}, 8.0, 31)
+        rows = oracle.features({n}, {dim}, 32)
+        g = gx.GraphFile.from_csc(ip, ind)
+        f = gx.FeatureFile.from_array(rows)
+        train = oracle.train_ids({n}, 1, 0.9)
+        plan = [train[(7 * i) % (len(train) - 20):][:20] for i in range({S})]
+        p = gx.Pipeline(g, f, [6, 4], {n}, digest=True)
+        st = p.run_superbatch(plan, 3, 0)
+        trace = [oracle.sample_batch(ip, ind, b, [6, 4], oracle.derive_seed(3, i))[0] for i, b in enumerate(plan)]
+        flat = np.concatenate(trace)
+        hub = int(np.bincount(flat.astype(np.int64)).max())
+        ok = all(np.array_equal(p.batch(i), rows[ids.astype(np.int64)]) for i, ids in enumerate(trace))
+        dig = p.digests()
+        ok = ok and all(int(dig[i]) == gx.batch_digest(rows[trace[i].astype(np.int64)]) for i in range(0, {S}, 9))
+        print(json.dumps({{"ok": bool(ok), "fused": bool(st.fused_fill), "fan": bool(st.fan_out), "hub": hub,
+                          "misses": int(st.total_misses), "init": int(st.init_size),
+                          "distinct": int(len(np.unique(flat)))}}))
+    """)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GX_FANOUT=str(fanout), PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["ok"] and res["fused"] and res["fan"] == bool(fanout), res
+    assert res["hub"] > 32 and res["misses"] == 0 and res["init"] == res["distinct"], res
