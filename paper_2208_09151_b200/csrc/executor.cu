@@ -436,13 +436,31 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fill_first(
 
 // Fan-out executor for an all-fit superbatch: every init row is read ONCE and
 // written to its cache slot and to the batch rows of ALL its accesses
-// (list[off[r] .. off[r + 1]), first use included), so no access re-reads the
+// (list[off[r - 1] .. off[r]), first use included), so no access re-reads the
 // cache: (2w + 8) bytes per init row + (w + 4) per access instead of
 // (3w + 8) per init row + (2w + 8) per other access (fill + gather).
 // A warp takes R slots; the slots' lists are contiguous in `list`, so one
 // coalesced load brings the first 32 destinations of all R slots into lanes.
+#ifndef GX_FAN_OCC
+#define GX_FAN_OCC 0  // CTAs per SM for __launch_bounds__ (0: the gather's GatherOcc<R>)
+#endif
+#ifndef GX_FAN_EF
+#define GX_FAN_EF 0   // L2 evict-first policy on the batch-row stores
+#endif
+#ifndef GX_FAN_PF
+#define GX_FAN_PF 0   // prefetch the next group's offsets / ids / list window
+#endif
+__device__ __forceinline__ void st_fan(uint4* p, const uint4& v, uint64_t pol) {
+#if GX_FAN_EF
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
+                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol));
+#else
+    (void)pol;
+    st_na(p, v);
+#endif
+}
 template <int R>
-__global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fan_rows(
+__global__ void __launch_bounds__(GA_THREADS, GX_FAN_OCC ? GX_FAN_OCC : GatherOcc<R>::value) k_fan_rows(
     const uint32_t* __restrict__ idx, uint32_t n, const uint8_t* __restrict__ src, uint32_t row_bytes,
     uint8_t* __restrict__ cache_rows, const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
     uint8_t* __restrict__ batch) {
@@ -450,15 +468,43 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fan_rows(
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t nvec = row_bytes / 16;
-    for (uint32_t r0 = warp * R; r0 < n; r0 += nwarps * R) {
-        const uint32_t nr = min(n - r0, (uint32_t)R);
-        const uint8_t* sp = nullptr;
-        uint32_t o = 0;
-        if (lane < nr) sp = src + (uint64_t)(idx ? __ldg(idx + r0 + lane) : r0 + lane) * row_bytes;
-        if (lane <= nr) o = __ldg(off + r0 + lane);
+    const uint32_t step = nwarps * R;
+    uint64_t pol = 0;
+#if GX_FAN_EF
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    auto nr_of = [&](uint32_t g0) { return g0 < n ? min(n - g0, (uint32_t)R) : 0u; };
+    // group metadata: source row (lanes < nr), offsets (lanes <= nr), first 32 list entries
+    auto meta = [&](uint32_t g0, const uint8_t*& sp, uint32_t& o) {
+        const uint32_t nr = nr_of(g0);
+        sp = lane < nr ? src + (uint64_t)(idx ? __ldg(idx + g0 + lane) : g0 + lane) * row_bytes : nullptr;
+        o = lane <= nr && nr && g0 + lane ? __ldg(off + g0 + lane - 1) : 0u;  // slot s: [off[s-1], off[s])
+    };
+    auto window = [&](uint32_t o, uint32_t nr) {
+        const uint32_t bs = __shfl_sync(0xffffffffu, o, 0), en = __shfl_sync(0xffffffffu, o, nr);
+        return bs + lane < en ? __ldg(list + bs + lane) : 0u;
+    };
+    uint32_t r0 = warp * R;
+    const uint8_t* sp;
+    uint32_t o;
+    meta(r0, sp, o);
+#if GX_FAN_PF
+    const uint8_t* sp_n;
+    uint32_t o_n;
+    meta(r0 + step, sp_n, o_n);
+    uint32_t d = window(o, nr_of(r0));
+#endif
+    for (; r0 < n; r0 += step) {
+        const uint32_t nr = nr_of(r0);
+#if GX_FAN_PF
+        const uint32_t d_n = window(o_n, nr_of(r0 + step));
+        const uint8_t* sp_nn;
+        uint32_t o_nn;
+        meta(r0 + 2 * step, sp_nn, o_nn);
+#else
+        const uint32_t d = window(o, nr);
+#endif
         const uint32_t base = __shfl_sync(0xffffffffu, o, 0);
-        const uint32_t end = __shfl_sync(0xffffffffu, o, nr);
-        const uint32_t d = base + lane < end ? __ldg(list + base + lane) : 0u;
 #pragma unroll 1
         for (uint32_t c0 = 0; c0 < nvec; c0 += 32) {
             const uint32_t c = c0 + lane;
@@ -472,7 +518,7 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fan_rows(
                 uint4* dst1 = reinterpret_cast<uint4*>(cache_rows + (uint64_t)r0 * row_bytes);
 #pragma unroll
                 for (int q = 0; q < R; ++q)
-                    if (q < (int)nr && c < nvec) st_na(dst1 + q * nvec + c, tmp[q]);
+                    if (q < (int)nr && c < nvec) st_fan(dst1 + q * nvec + c, tmp[q], pol);
             }
 #pragma unroll
             for (int q = 0; q < R; ++q) {
@@ -481,10 +527,19 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fan_rows(
                 for (uint32_t j = b; j < e; ++j) {
                     const uint32_t v = __shfl_sync(0xffffffffu, d, (j - base) & 31);
                     const uint32_t x = j - base < 32 ? v : __ldg(list + j);
-                    if (c < nvec) st_na(reinterpret_cast<uint4*>(batch + (uint64_t)x * row_bytes) + c, tmp[q]);
+                    if (c < nvec) st_fan(reinterpret_cast<uint4*>(batch + (uint64_t)x * row_bytes) + c, tmp[q], pol);
                 }
             }
         }
+#if GX_FAN_PF
+        sp = sp_n;
+        o = o_n;
+        d = d_n;
+        sp_n = sp_nn;
+        o_n = o_nn;
+#else
+        meta(r0 + step, sp, o);
+#endif
     }
 }
 
@@ -518,7 +573,9 @@ __global__ void __launch_bounds__(FT_WARPS * 32) k_fan_tma(const uint32_t* __res
     // first 32 list entries are prefetched one or two groups ahead, so the
     // off -> list -> store chain never stalls the store phase
     auto nr_of = [&](uint32_t g0) { return g0 < n ? min(n - g0, (uint32_t)R) : 0u; };
-    auto ld_off = [&](uint32_t g0) { return lane <= nr_of(g0) && g0 < n ? __ldg(off + g0 + lane) : 0u; };
+    auto ld_off = [&](uint32_t g0) {
+        return lane <= nr_of(g0) && g0 < n && g0 + lane ? __ldg(off + g0 + lane - 1) : 0u;
+    };
     auto ld_id = [&](uint32_t g0) {
         return lane < nr_of(g0) ? (idx ? __ldg(idx + g0 + lane) : g0 + lane) : 0u;
     };

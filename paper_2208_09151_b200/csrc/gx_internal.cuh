@@ -143,8 +143,8 @@ struct gx_changesets {
     gx::DevBuf<uint32_t> first_acc; // all-fit: access index of each init slot's first use
     gx::DevBuf<uint32_t> rest_x, rest_slot;  // all-fit: the other accesses and their slots
     // all-fit, fan-out form: the accesses of init slot r are
-    // fan_list[fan_off[r] .. fan_off[r + 1]) (first use included)
-    gx::DevBuf<uint32_t> fan_cnt, fan_rank, fan_off, fan_list;
+    // fan_list[r ? fan_off[r - 1] : 0 .. fan_off[r]) (first use included)
+    gx::DevBuf<uint32_t> fan_cnt, fan_off, fan_list;
     gx::DevBuf<uint8_t> cub_tmp;
     uint64_t n_rest = 0;
     bool first_marked = false;      // first_acc / rest_* (or fan_*) valid (pipeline only)
@@ -243,7 +243,7 @@ void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_
                        const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch);
 // Fan-out form (mark_first = 2): each init row is read once and written to its
 // cache slot (cache_rows != nullptr) and to every batch row of its accesses,
-// batch row fan_list[j] for j in [off[r], off[r + 1]). idx == nullptr: source
+// batch row fan_list[j] for j in [r ? off[r - 1] : 0, off[r]). idx == nullptr: source
 // row r is row r of `src` (the staged tiers fan out from the filled cache).
 void launch_fan_rows(gx_ctx* ctx, const uint32_t* idx, uint32_t n, const uint8_t* src, uint64_t rb,
                      uint8_t* cache_rows, const uint32_t* off, const uint32_t* list, uint8_t* batch);

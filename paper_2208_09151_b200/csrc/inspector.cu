@@ -101,8 +101,7 @@ struct IArgs {
     uint32_t* o_first;   // all-fit + mark_first: access index of each init slot's first use
     uint32_t* o_rest_x;  // all-fit + mark_first: accesses that are not a first use (dense) ...
     uint32_t* o_rest_slot;  // ... and their cache slots
-    uint32_t* o_fan_cnt;    // all-fit + fan-out marks: accesses per init slot (K + 1) ...
-    uint32_t* o_fan_rank;   // ... and each access's rank among its slot's accesses (A)
+    uint32_t* o_fan_cnt;    // all-fit + fan-out marks: accesses per init slot (K + 1)
     uint32_t* o_in_ids;
     uint32_t* o_in_pos;
     uint32_t* o_in_slot;
@@ -497,10 +496,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         if (fit) {
                             a.acc_slot[x] = r;
                             if (a.o_first) a.o_first[r] = x;
-                            if (a.o_fan_cnt) {  // the first use is rank 0 of its slot
-                                a.o_fan_cnt[r] = 1;
-                                a.o_fan_rank[x] = 0;
-                            }
+                            if (a.o_fan_cnt) a.o_fan_cnt[r] = 1;  // the first use
                         } else {
                             a.node_slot[v] = (int32_t)r;
                         }
@@ -549,14 +545,14 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
     if (allfit) {
         if (a.trusted && a.o_fan_cnt) {
-            // fan-out executor: every other access takes the next rank of its
-            // slot (L2-resident counters: K words); the host turns the counts
-            // into offsets and places each access at off[slot] + rank
+            // fan-out executor: every other access counts into its slot
+            // (fire-and-forget reductions on K L2-resident words) and records
+            // its slot; the host scans the counts and places the accesses
             for (uint32_t x = gtid; x < a.A; x += G) {
                 if (a.isfirst[x]) continue;
                 const uint32_t s = a.acc_slot[a.next_use[x]];
                 a.acc_slot[x] = s;
-                a.o_fan_rank[x] = atomicAdd(&a.o_fan_cnt[s], 1u);
+                atomicAdd(&a.o_fan_cnt[s], 1u);
             }
             if (gtid == 0) a.o_fan_cnt[*(volatile uint32_t*)&a.st->n_first] = 0;  // scan sentinel
         } else if (a.trusted && a.o_first) {
@@ -1191,11 +1187,15 @@ uint32_t inspect_reserve_epoch(gx_ctx* ctx, uint64_t N, uint64_t keyrange) {
     return (uint32_t)is.fx_base;
 }
 
-// fan-out lists: access x goes to position off[slot(x)] + rank(x) of its slot's list
-__global__ void k_fan_place(const uint32_t* __restrict__ acc_slot, const uint32_t* __restrict__ rank,
-                            const uint32_t* __restrict__ off, uint32_t A, uint32_t* __restrict__ list) {
+// fan-out lists: access x takes the next position of its slot's range; off[s]
+// (the range start after the scan) ends as the range end, i.e. the start of
+// slot s + 1 -- the fan-out kernel reads slot s as [off[s - 1], off[s]).
+// The order inside a slot's range is arbitrary: every entry is a distinct
+// batch row that receives the same bytes.
+__global__ void k_fan_place(const uint32_t* __restrict__ acc_slot, uint32_t* __restrict__ off, uint32_t A,
+                            uint32_t* __restrict__ list) {
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < A; x += gridDim.x * blockDim.x)
-        list[__ldg(off + __ldg(acc_slot + x)) + __ldg(rank + x)] = x;
+        list[atomicAdd(off + __ldg(acc_slot + x), 1u)] = x;
 }
 
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
@@ -1348,12 +1348,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.o_init = out->init.p;
     a.o_first = nullptr;
     a.o_rest_x = a.o_rest_slot = nullptr;
-    a.o_fan_cnt = a.o_fan_rank = nullptr;
+    a.o_fan_cnt = nullptr;
     if (mark_first == 2 && a.trusted) {
         out->fan_cnt.reserve(Keff + 1);
-        out->fan_rank.reserve(A + 1);
         a.o_fan_cnt = out->fan_cnt.p;
-        a.o_fan_rank = out->fan_rank.p;
     } else if (mark_first && a.trusted) {
         out->first_acc.reserve(Keff + 1);
         out->rest_x.reserve(A + 1);
@@ -1462,8 +1460,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         out->cub_tmp.reserve(tb + 16);
         GX_CUDA(cub::DeviceScan::ExclusiveSum(out->cub_tmp.p, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
         if (A) {
-            k_fan_place<<<ctx->num_sms * 4, 256, 0, st>>>(is.acc_slot.p, out->fan_rank.p, out->fan_off.p,
-                                                         (uint32_t)A, out->fan_list.p);
+            k_fan_place<<<ctx->num_sms * 4, 256, 0, st>>>(is.acc_slot.p, out->fan_off.p, (uint32_t)A,
+                                                         out->fan_list.p);
             GX_CHECK_LAUNCH();
         }
     }
