@@ -77,7 +77,7 @@ def main():
         for d in rs:
             lines.append(f"| {d['kernel'][:40]} | " + " | ".join(
                 f"{d[l][0]} {d[l][1]}".strip() if l in d else "" for l in labels) + " |")
-            if "gather" in d["kernel"] and "DRAM read" in d:
+            if ("gather" in d["kernel"] or "fan_rows" in d["kernel"]) and "DRAM read" in d:
                 def mb(x):
                     v, u = float(x[0]), x[1]
                     return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1}.get(u, 1)
@@ -87,10 +87,14 @@ def main():
     for k, v in traffic.items():
         print(k, sum(v) / len(v))
     if traffic:
-        k = next((x for x in traffic if x.startswith("k_gather_tma2")), max(traffic, key=lambda x: len(traffic[x])))
-        json.dump({"kernel": k, "k_gather_dram_bytes_per_launch": sum(traffic[k]) / len(traffic[k]),
-                   "launches_captured": len(traffic[k]), "source": [os.path.basename(r) for r in reps]},
-                  open(os.path.join(here, "traffic_papers.json"), "w"), indent=1)
+        out = {"source": [os.path.basename(r) for r in reps]}
+        for key, pre in (("k_gather", "k_gather_tma2"), ("k_fan", "k_fan_rows")):
+            k = next((x for x in traffic if x.startswith(pre)), None)
+            if k:
+                out[key + "_kernel"] = k
+                out[key + "_dram_bytes_per_launch"] = sum(traffic[k]) / len(traffic[k])
+                out[key + "_launches_captured"] = len(traffic[k])
+        json.dump(out, open(os.path.join(here, "traffic_papers.json"), "w"), indent=1)
 
 
 if __name__ == "__main__":
