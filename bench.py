@@ -498,19 +498,20 @@ def main():
     if fan and not staged:      # switch + every access in one kernel
         fan_kernel = "k_fan_rows (switch fanned out to every access)"
         fan_ms = sum(s.ms_switch for s in stats)
-        fan_bytes = (2 * w + 8) * fills + (w + 4) * rows
+        fan_bytes = (3 * w + 12) * fills + (w + 4) * (rows - fills)
         rooflines.append(line(fan_kernel, fan_ms, fan_bytes,
-                              "(2w + 8) per init row (read row, write slot, id + offset) + (w + 4) per access "
-                              "(write batch row, list entry)"))
+                              "(3w + 12) per init row (read row, write slot + first-use row, id + first + range "
+                              "end) + (w + 4) per other access (write batch row, list entry)"))
     elif fan:                   # staged tiers: the filled cache fans out
         rooflines.append(line("switch (storage / exchange scatter into slots)", sum(s.ms_switch for s in stats),
-                              (w + 4) * fills, "(w + 4) per init row: write slot, id (device side)"))
-        fan_kernel = "k_fan_rows (cache rows fanned out to every access)"
+                              (2 * w + 8) * fills, "(2w + 8) per init row: write slot + first-use row, 2 ids "
+                              "(device side)"))
+        fan_kernel = "k_fan_rows (cache rows fanned out to the other accesses)"
         fan_ms = gk_ms
-        fan_bytes = (w + 4) * fills + (w + 4) * rows
+        fan_bytes = (w + 4) * fills + (w + 4) * (rows - fills)
         rooflines.append(line(fan_kernel, fan_ms, fan_bytes,
-                              "(w + 4) per init row (read slot row, offset) + (w + 4) per access "
-                              "(write batch row, list entry)"))
+                              "<= (w + 4) per init row (read slot row if it has other accesses, range end) + "
+                              "(w + 4) per other access (write batch row, list entry)"))
     else:
         rooflines += [
             line("k_fill_first (switch fused with first uses)" if fused else "k_gather_rows<16,8> (switch: cache init)",
@@ -593,7 +594,9 @@ def main():
                       "init_rows_per_launch": fills / n, "accesses_per_launch": rows / n,
                       "alg_bytes_per_launch": fan_bytes / n,
                       "note": "all-fit superbatches: one launch per superbatch reads each init row once and "
-                              "writes it to its cache slot and to the batch row of every access of its node"}
+                              "writes it to its cache slot and to the batch row of every access of its node"
+                              if not staged else "staged tier: the scatter filled slots + first-use rows; the "
+                              "cache rows fan out to the other accesses"}
                      if fan else
                      {"kernel": "k_gather_tma2 (bulk-copy row gather)", "bound": "hbm", "achieved": achieved,
                       "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

@@ -536,7 +536,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         sl.full = resident;
         const bool fused = sl.cs.first_marked;  // implies all-fit (no changesets) and resident
         sl.fused = fused;
-        sl.gather_rows = fused ? (sl.cs.fan ? (file ? sl.o[S] : 0) : sl.cs.n_rest) : sl.o[S];
+        sl.gather_rows = fused ? (sl.cs.fan ? (file ? sl.cs.n_rest : 0) : sl.cs.n_rest) : sl.o[S];
         sl.batch.reserve(std::max<uint64_t>((sl.full ? sl.o[S] : maxw) * rb, 16));
         sl.h_off.reserve(S + 1);
         sl.d_off.reserve(S + 1);
@@ -572,8 +572,8 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 sl.cs.init.reserve(1);
                 sl.miss_ids.reserve(1);
                 // all-fit (fused): each init row also lands in its first batch row
-                // (fan-out form: the cache rows fan out to all batch rows below)
-                const bool dual = fused && !sl.cs.fan;
+                // (fan-out form: the cache rows then fan out to the other accesses)
+                const bool dual = fused;
                 sl.ms_storage += fetch_rows(p->f, sl.cs.init.p, sl.cs.n_init, p->cache_rows.p, B,
                                             dual ? sl.batch.p : nullptr, dual ? sl.cs.first_acc.p : nullptr);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
@@ -586,7 +586,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 // the switch fused with every access: one read of each backing
                 // row, written to its slot and to all batch rows of its node
                 launch_fan_rows(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, p->f->rows_dev_view, rb, p->cache_rows.p,
-                                sl.cs.fan_off.p, sl.cs.fan_list.p, sl.batch.p);
+                                sl.cs.first_acc.p, sl.cs.fan_off.p, sl.cs.fan_list.p, sl.batch.p);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
             } else if (fused) {
                 // the switch fused with every init node's first use: one read of
@@ -613,7 +613,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                     // staged tiers: the filled cache rows fan out to the batch
                     // rows (device-backed tables did this in the switch)
                     if (file)
-                        launch_fan_rows(ctx, nullptr, (uint32_t)sl.cs.n_init, p->cache_rows.p, rb, nullptr,
+                        launch_fan_rows(ctx, nullptr, (uint32_t)sl.cs.n_init, p->cache_rows.p, rb, nullptr, nullptr,
                                         sl.cs.fan_off.p, sl.cs.fan_list.p, sl.batch.p);
                 } else {
                     launch_gather_resolved(ctx, sl.cs.rest_x.p, sl.cs.rest_slot.p, sl.cs.n_rest, p->cache_rows.p,

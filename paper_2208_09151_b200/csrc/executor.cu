@@ -435,76 +435,42 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fill_first(
 }
 
 // Fan-out executor for an all-fit superbatch: every init row is read ONCE and
-// written to its cache slot and to the batch rows of ALL its accesses
-// (list[off[r - 1] .. off[r]), first use included), so no access re-reads the
-// cache: (2w + 8) bytes per init row + (w + 4) per access instead of
-// (3w + 8) per init row + (2w + 8) per other access (fill + gather).
-// A warp takes R slots; the slots' lists are contiguous in `list`, so one
+// written to its cache slot, to the batch row of its first use first[r] and to
+// the batch rows of its other accesses list[off[r - 1] .. off[r]), so no access
+// re-reads the cache: (3w + 12) bytes per init row + (w + 4) per other access
+// instead of (3w + 8) per init row + (2w + 8) per other access (fill + gather).
+// A warp takes R consecutive slots: their lists are one contiguous run, so one
 // coalesced load brings the first 32 destinations of all R slots into lanes.
-#ifndef GX_FAN_OCC
-#define GX_FAN_OCC 0  // CTAs per SM for __launch_bounds__ (0: the gather's GatherOcc<R>)
-#endif
-#ifndef GX_FAN_EF
-#define GX_FAN_EF 0   // L2 evict-first policy on the batch-row stores
-#endif
-#ifndef GX_FAN_PF
-#define GX_FAN_PF 0   // prefetch the next group's offsets / ids / list window
-#endif
-__device__ __forceinline__ void st_fan(uint4* p, const uint4& v, uint64_t pol) {
-#if GX_FAN_EF
-    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x),
-                 "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol));
-#else
-    (void)pol;
-    st_na(p, v);
-#endif
-}
+// Measured and removed: a bulk-copy form (lanes issue cp.async.bulk stores of
+// their destinations from smem row buffers, the next group's loads in flight:
+// 2.94 vs 2.85 ms), 64-register builds, L2 evict-first stores, prefetching the
+// next group's offsets and list window (2.85-2.93 ms).
 template <int R>
-__global__ void __launch_bounds__(GA_THREADS, GX_FAN_OCC ? GX_FAN_OCC : GatherOcc<R>::value) k_fan_rows(
+__global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fan_rows(
     const uint32_t* __restrict__ idx, uint32_t n, const uint8_t* __restrict__ src, uint32_t row_bytes,
-    uint8_t* __restrict__ cache_rows, const uint32_t* __restrict__ off, const uint32_t* __restrict__ list,
-    uint8_t* __restrict__ batch) {
+    uint8_t* __restrict__ cache_rows, const uint32_t* __restrict__ first, const uint32_t* __restrict__ off,
+    const uint32_t* __restrict__ list, uint8_t* __restrict__ batch) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     const uint32_t nvec = row_bytes / 16;
-    const uint32_t step = nwarps * R;
-    uint64_t pol = 0;
-#if GX_FAN_EF
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-#endif
-    auto nr_of = [&](uint32_t g0) { return g0 < n ? min(n - g0, (uint32_t)R) : 0u; };
-    // group metadata: source row (lanes < nr), offsets (lanes <= nr), first 32 list entries
-    auto meta = [&](uint32_t g0, const uint8_t*& sp, uint32_t& o) {
-        const uint32_t nr = nr_of(g0);
-        sp = lane < nr ? src + (uint64_t)(idx ? __ldg(idx + g0 + lane) : g0 + lane) * row_bytes : nullptr;
-        o = lane <= nr && nr && g0 + lane ? __ldg(off + g0 + lane - 1) : 0u;  // slot s: [off[s-1], off[s])
-    };
-    auto window = [&](uint32_t o, uint32_t nr) {
-        const uint32_t bs = __shfl_sync(0xffffffffu, o, 0), en = __shfl_sync(0xffffffffu, o, nr);
-        return bs + lane < en ? __ldg(list + bs + lane) : 0u;
-    };
-    uint32_t r0 = warp * R;
-    const uint8_t* sp;
-    uint32_t o;
-    meta(r0, sp, o);
-#if GX_FAN_PF
-    const uint8_t* sp_n;
-    uint32_t o_n;
-    meta(r0 + step, sp_n, o_n);
-    uint32_t d = window(o, nr_of(r0));
-#endif
-    for (; r0 < n; r0 += step) {
-        const uint32_t nr = nr_of(r0);
-#if GX_FAN_PF
-        const uint32_t d_n = window(o_n, nr_of(r0 + step));
-        const uint8_t* sp_nn;
-        uint32_t o_nn;
-        meta(r0 + 2 * step, sp_nn, o_nn);
-#else
-        const uint32_t d = window(o, nr);
-#endif
-        const uint32_t base = __shfl_sync(0xffffffffu, o, 0);
+    for (uint32_t r0 = warp * R; r0 < n; r0 += nwarps * R) {
+        const uint32_t nr = min(n - r0, (uint32_t)R);
+        // lanes < nr: source row and first-use row of slot r0 + lane;
+        // lanes <= nr: range ends (slot s: [off[s - 1], off[s]))
+        const uint8_t* sp = nullptr;
+        uint8_t* fp = nullptr;
+        if (lane < nr) {
+            sp = src + (uint64_t)(idx ? __ldg(idx + r0 + lane) : r0 + lane) * row_bytes;
+            if (first) fp = batch + (uint64_t)__ldg(first + r0 + lane) * row_bytes;
+        }
+        const uint32_t o = lane <= nr && r0 + lane ? __ldg(off + r0 + lane - 1) : 0u;
+        const uint32_t base = __shfl_sync(0xffffffffu, o, 0), end = __shfl_sync(0xffffffffu, o, nr);
+        // rows to read: all (a first use or a cache slot to write), else only
+        // slots with other accesses (staged tiers: the slots are already filled)
+        const uint32_t o_next = __shfl_down_sync(0xffffffffu, o, 1);
+        const uint32_t need = __ballot_sync(0xffffffffu, lane < nr && (first || cache_rows || o_next > o));
+        const uint32_t d = base + lane < end ? __ldg(list + base + lane) : 0u;
 #pragma unroll 1
         for (uint32_t c0 = 0; c0 < nvec; c0 += 32) {
             const uint32_t c = c0 + lane;
@@ -512,13 +478,15 @@ __global__ void __launch_bounds__(GA_THREADS, GX_FAN_OCC ? GX_FAN_OCC : GatherOc
 #pragma unroll
             for (int q = 0; q < R; ++q) {
                 const uint4* sq = reinterpret_cast<const uint4*>(__shfl_sync(0xffffffffu, (unsigned long long)sp, q));
-                if (q < (int)nr && c < nvec) tmp[q] = ld_nc(sq + c);
+                if (((need >> q) & 1) && c < nvec) tmp[q] = ld_nc(sq + c);
             }
-            if (cache_rows) {
-                uint4* dst1 = reinterpret_cast<uint4*>(cache_rows + (uint64_t)r0 * row_bytes);
 #pragma unroll
-                for (int q = 0; q < R; ++q)
-                    if (q < (int)nr && c < nvec) st_fan(dst1 + q * nvec + c, tmp[q], pol);
+            for (int q = 0; q < R; ++q) {
+                uint4* fq = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, (unsigned long long)fp, q));
+                if (q < (int)nr && c < nvec) {
+                    if (cache_rows) st_na(reinterpret_cast<uint4*>(cache_rows + (uint64_t)(r0 + q) * row_bytes) + c, tmp[q]);
+                    if (fq) st_na(fq + c, tmp[q]);
+                }
             }
 #pragma unroll
             for (int q = 0; q < R; ++q) {
@@ -527,148 +495,18 @@ __global__ void __launch_bounds__(GA_THREADS, GX_FAN_OCC ? GX_FAN_OCC : GatherOc
                 for (uint32_t j = b; j < e; ++j) {
                     const uint32_t v = __shfl_sync(0xffffffffu, d, (j - base) & 31);
                     const uint32_t x = j - base < 32 ? v : __ldg(list + j);
-                    if (c < nvec) st_fan(reinterpret_cast<uint4*>(batch + (uint64_t)x * row_bytes) + c, tmp[q], pol);
+                    if (c < nvec) st_na(reinterpret_cast<uint4*>(batch + (uint64_t)x * row_bytes) + c, tmp[q]);
                 }
             }
         }
-#if GX_FAN_PF
-        sp = sp_n;
-        o = o_n;
-        d = d_n;
-        sp_n = sp_nn;
-        o_n = o_nn;
-#else
-        meta(r0 + step, sp, o);
-#endif
     }
-}
-
-// Bulk-copy form: a warp owns two smem buffers of R rows. Lanes 0..R-1 load
-// the group's rows with cp.async.bulk (one mbarrier per row), the next group's
-// loads are issued before this group's stores, and every lane issues the bulk
-// stores of its destinations (lane l: list entries l, l + 32, ...), so a
-// group's ~3R batch-row writes leave in one instruction round and the loads
-// never wait behind them. The R cache slots are contiguous: one bulk store.
-constexpr int FT_WARPS = 4;
-template <int R>
-__global__ void __launch_bounds__(FT_WARPS * 32) k_fan_tma(const uint32_t* __restrict__ idx, uint32_t n,
-                                                           const uint8_t* __restrict__ src, uint32_t row_bytes,
-                                                           uint8_t* __restrict__ cache_rows,
-                                                           const uint32_t* __restrict__ off,
-                                                           const uint32_t* __restrict__ list,
-                                                           uint8_t* __restrict__ batch) {
-    extern __shared__ __align__(128) unsigned char sbuf[];
-    __shared__ __align__(8) unsigned long long bars[FT_WARPS * 2 * R];
-    const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const uint32_t warp = blockIdx.x * FT_WARPS + wib, nwarps = gridDim.x * FT_WARPS;
-    const uint32_t buf0 = smem_u32(sbuf + (size_t)wib * 2 * R * row_bytes);
-    const uint32_t bar0 = smem_u32(&bars[wib * 2 * R]);
-    if (lane < 2 * R) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8 * lane));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncwarp();
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    const uint32_t step = nwarps * R;
-    // per group: offsets (lanes 0..nr), source ids (lanes 0..nr-1) and the
-    // first 32 list entries are prefetched one or two groups ahead, so the
-    // off -> list -> store chain never stalls the store phase
-    auto nr_of = [&](uint32_t g0) { return g0 < n ? min(n - g0, (uint32_t)R) : 0u; };
-    auto ld_off = [&](uint32_t g0) {
-        return lane <= nr_of(g0) && g0 < n && g0 + lane ? __ldg(off + g0 + lane - 1) : 0u;
-    };
-    auto ld_id = [&](uint32_t g0) {
-        return lane < nr_of(g0) ? (idx ? __ldg(idx + g0 + lane) : g0 + lane) : 0u;
-    };
-    auto ld_list = [&](uint32_t o, uint32_t g0) {
-        const uint32_t bs = __shfl_sync(0xffffffffu, o, 0), en = __shfl_sync(0xffffffffu, o, nr_of(g0));
-        return bs + lane < en ? __ldg(list + bs + lane) : 0u;
-    };
-    auto issue = [&](uint32_t g0, uint32_t id, uint32_t b) {
-        if (lane < nr_of(g0))
-            bulk_load(buf0 + (b * R + lane) * row_bytes, src + (uint64_t)id * row_bytes, row_bytes,
-                      bar0 + 8 * (b * R + lane));
-    };
-    uint32_t r0 = warp * R;
-    if (r0 >= n) return;
-    issue(r0, ld_id(r0), 0);
-    uint32_t o_c = ld_off(r0);
-    uint32_t o_n = ld_off(r0 + step), id_n = ld_id(r0 + step);
-    uint32_t x_c = ld_list(o_c, r0);
-    for (uint32_t it = 0; r0 < n; ++it, r0 += step) {
-        const uint32_t b = it & 1, ph = (it >> 1) & 1;
-        const uint32_t nr = nr_of(r0), r1 = r0 + step, r2 = r1 + step;
-        if (r1 < n) {
-            // buffer b^1 is free once this lane's stores from it have read smem
-            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            __syncwarp();
-            issue(r1, id_n, b ^ 1);
-        }
-        const uint32_t o_nn = ld_off(r2), id_nn = ld_id(r2);
-        const uint32_t x_n = ld_list(o_n, r1);
-        uint32_t oq[R + 1];
-#pragma unroll
-        for (int k = 0; k <= R; ++k) oq[k] = __shfl_sync(0xffffffffu, o_c, k);
-        const uint32_t base = oq[0], end = __shfl_sync(0xffffffffu, o_c, nr);
-        for (uint32_t j = base + lane; j < end; j += 32) {
-            const uint32_t x = j - base < 32 ? x_c : __ldg(list + j);
-            uint32_t q = 0;
-#pragma unroll
-            for (int k = 1; k < R; ++k) q += (k < (int)nr && oq[k] <= j) ? 1u : 0u;
-            const uint32_t slot = b * R + q;
-            bar_wait(bar0 + 8 * slot, ph);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
-                             batch + (uint64_t)x * row_bytes),
-                         "r"(buf0 + slot * row_bytes), "r"(row_bytes), "l"(pol)
-                         : "memory");
-        }
-        if (cache_rows && lane == 0) {
-            for (uint32_t q = 0; q < nr; ++q) bar_wait(bar0 + 8 * (b * R + q), ph);
-            asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
-                             cache_rows + (uint64_t)r0 * row_bytes),
-                         "r"(buf0 + b * R * row_bytes), "r"(nr * row_bytes), "l"(pol)
-                         : "memory");
-        }
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-        o_c = o_n;
-        o_n = o_nn;
-        id_n = id_nn;
-        x_c = x_n;
-    }
-    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 void launch_fan_rows(gx_ctx* ctx, const uint32_t* idx, uint32_t n, const uint8_t* src, uint64_t rb,
-                     uint8_t* cache_rows, const uint32_t* off, const uint32_t* list, uint8_t* batch) {
+                     uint8_t* cache_rows, const uint32_t* first, const uint32_t* off, const uint32_t* list,
+                     uint8_t* batch) {
     if (!n) return;
     if (rb % 16) fail(GX_INVALID_ARGUMENT, "fan-out fill needs 16-byte rows");
-    static const int tma = env_int("GX_FAN_TMA", 0);  // bulk-copy form: 2.94-2.96 vs 2.85 ms (LDG/STG) at papers shape
-    static const int tr = env_int("GX_FAN_TR", 8);  // rows per warp group: 4, 8 or 16
-    auto go_tma = [&](auto kfn, int TR) {
-        const uint64_t smem = (uint64_t)FT_WARPS * 2 * TR * rb;
-        if (smem > 200 * 1024) return false;
-        static uint64_t last[3] = {0, 0, 0};
-        static int bpsm[3] = {0, 0, 0};
-        static std::mutex mu;
-        const int k = TR == 4 ? 0 : TR == 8 ? 1 : 2;
-        std::lock_guard<std::mutex> lk(mu);
-        if (last[k] != rb) {
-            GX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm[k], kfn, FT_WARPS * 32, smem));
-            bpsm[k] = std::max(bpsm[k], 1);
-            last[k] = rb;
-        }
-        const uint64_t groups = (n + TR - 1) / TR;
-        const uint64_t blocks =
-            std::min<uint64_t>((groups + FT_WARPS - 1) / FT_WARPS, (uint64_t)ctx->num_sms * bpsm[k]);
-        kfn<<<(unsigned)blocks, FT_WARPS * 32, smem, lstream(ctx)>>>(idx, n, src, (uint32_t)rb, cache_rows, off, list,
-                                                                    batch);
-        GX_CHECK_LAUNCH();
-        return true;
-    };
-    if (tma) {
-        if (tr == 4 ? go_tma(k_fan_tma<4>, 4) : tr == 16 ? go_tma(k_fan_tma<16>, 16) : go_tma(k_fan_tma<8>, 8))
-            return;
-    }
     static const int rr = env_int("GX_FAN_R", 8);  // slots per warp: 4, 8 or 16
     auto go = [&](auto kfn, int R) {
         int bps = 0;
@@ -676,8 +514,8 @@ void launch_fan_rows(gx_ctx* ctx, const uint32_t* idx, uint32_t n, const uint8_t
         const uint64_t warps_needed = (n + R - 1) / R;
         const uint64_t blocks = std::min<uint64_t>((warps_needed * 32 + GA_THREADS - 1) / GA_THREADS,
                                                    (uint64_t)ctx->num_sms * std::max(bps, 1));
-        kfn<<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(idx, n, src, (uint32_t)rb, cache_rows, off, list,
-                                                               batch);
+        kfn<<<(unsigned)blocks, GA_THREADS, 0, lstream(ctx)>>>(idx, n, src, (uint32_t)rb, cache_rows, first, off,
+                                                               list, batch);
         GX_CHECK_LAUNCH();
     };
     if (rr == 4) go(k_fan_rows<4>, 4);

@@ -142,8 +142,8 @@ struct gx_changesets {
     gx::DevBuf<uint32_t> out_ids;   // total out (sorted per iteration)
     gx::DevBuf<uint32_t> first_acc; // all-fit: access index of each init slot's first use
     gx::DevBuf<uint32_t> rest_x, rest_slot;  // all-fit: the other accesses and their slots
-    // all-fit, fan-out form: the accesses of init slot r are
-    // fan_list[r ? fan_off[r - 1] : 0 .. fan_off[r]) (first use included)
+    // all-fit, fan-out form: init slot r serves first_acc[r] and the accesses
+    // fan_list[r ? fan_off[r - 1] : 0 .. fan_off[r])
     gx::DevBuf<uint32_t> fan_cnt, fan_off, fan_list;
     gx::DevBuf<uint8_t> cub_tmp;
     uint64_t n_rest = 0;
@@ -242,11 +242,14 @@ constexpr uint32_t kStageFlag = 0x80000000u;
 void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_acc, uint32_t n,
                        const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch);
 // Fan-out form (mark_first = 2): each init row is read once and written to its
-// cache slot (cache_rows != nullptr) and to every batch row of its accesses,
-// batch row fan_list[j] for j in [r ? off[r - 1] : 0, off[r]). idx == nullptr: source
-// row r is row r of `src` (the staged tiers fan out from the filled cache).
+// cache slot (cache_rows != nullptr), to the batch row of its first use
+// first[r] and to batch rows list[j] for j in [r ? off[r - 1] : 0, off[r]).
+// idx == nullptr: source row r is row r of `src`; first == nullptr: no
+// first-use rows (the staged tiers fan out from the filled cache to the other
+// accesses only, reading just the slots that have any).
 void launch_fan_rows(gx_ctx* ctx, const uint32_t* idx, uint32_t n, const uint8_t* src, uint64_t rb,
-                     uint8_t* cache_rows, const uint32_t* off, const uint32_t* list, uint8_t* batch);
+                     uint8_t* cache_rows, const uint32_t* first, const uint32_t* off, const uint32_t* list,
+                     uint8_t* batch);
 bool gather_can_skip_first(uint64_t rb);
 // d_out row j <- feature row d_ids[j] from storage, for j in [0, n). Sorts the
 // requests by id on `s`, reads page runs on the host into pinned chunks,

@@ -496,7 +496,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         if (fit) {
                             a.acc_slot[x] = r;
                             if (a.o_first) a.o_first[r] = x;
-                            if (a.o_fan_cnt) a.o_fan_cnt[r] = 1;  // the first use
+                            if (a.o_fan_cnt) a.o_fan_cnt[r] = 0;  // the other accesses are counted below
                         } else {
                             a.node_slot[v] = (int32_t)r;
                         }
@@ -544,18 +544,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     // served by its init slot.
     const bool allfit = !a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K;
     if (allfit) {
-        if (a.trusted && a.o_fan_cnt) {
-            // fan-out executor: every other access counts into its slot
-            // (fire-and-forget reductions on K L2-resident words) and records
-            // its slot; the host scans the counts and places the accesses
-            for (uint32_t x = gtid; x < a.A; x += G) {
-                if (a.isfirst[x]) continue;
-                const uint32_t s = a.acc_slot[a.next_use[x]];
-                a.acc_slot[x] = s;
-                atomicAdd(&a.o_fan_cnt[s], 1u);
-            }
-            if (gtid == 0) a.o_fan_cnt[*(volatile uint32_t*)&a.st->n_first] = 0;  // scan sentinel
-        } else if (a.trusted && a.o_first) {
+        if (a.trusted && a.o_first) {
             // fused executor: the non-first accesses as a dense list (rank =
             // position minus the first uses before it: tile_cnt + in-tile scan)
             for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
@@ -573,8 +562,12 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 for (int j = 0; j < IN_IPT; ++j) {
                     if (nf[j]) {
                         const uint32_t x = x0 + j;
+                        const uint32_t s = a.acc_slot[a.next_use[x]];
                         a.o_rest_x[k] = x;
-                        a.o_rest_slot[k] = a.acc_slot[a.next_use[x]];
+                        a.o_rest_slot[k] = s;
+                        // fan-out form: count into the slot (fire-and-forget
+                        // reductions on K L2-resident words)
+                        if (a.o_fan_cnt) atomicAdd(&a.o_fan_cnt[s], 1u);
                         ++k;
                     }
                 }
@@ -1187,15 +1180,15 @@ uint32_t inspect_reserve_epoch(gx_ctx* ctx, uint64_t N, uint64_t keyrange) {
     return (uint32_t)is.fx_base;
 }
 
-// fan-out lists: access x takes the next position of its slot's range; off[s]
-// (the range start after the scan) ends as the range end, i.e. the start of
-// slot s + 1 -- the fan-out kernel reads slot s as [off[s - 1], off[s]).
-// The order inside a slot's range is arbitrary: every entry is a distinct
-// batch row that receives the same bytes.
-__global__ void k_fan_place(const uint32_t* __restrict__ acc_slot, uint32_t* __restrict__ off, uint32_t A,
-                            uint32_t* __restrict__ list) {
-    for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < A; x += gridDim.x * blockDim.x)
-        list[atomicAdd(off + __ldg(acc_slot + x), 1u)] = x;
+// fan-out lists: each access that is not a first use (the dense rest list)
+// takes the next position of its slot's range; off[s] (the range start after
+// the scan) ends as the range end, i.e. the start of slot s + 1 -- the fan-out
+// kernel reads slot s as [off[s - 1], off[s]). The order inside a range is
+// arbitrary: every entry is a distinct batch row that receives the same bytes.
+__global__ void k_fan_place(const uint32_t* __restrict__ rest_x, const uint32_t* __restrict__ rest_slot,
+                            uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ list) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        list[atomicAdd(off + __ldg(rest_slot + k), 1u)] = __ldg(rest_x + k);
 }
 
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
@@ -1352,7 +1345,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     if (mark_first == 2 && a.trusted) {
         out->fan_cnt.reserve(Keff + 1);
         a.o_fan_cnt = out->fan_cnt.p;
-    } else if (mark_first && a.trusted) {
+    }
+    if (mark_first && a.trusted) {
         out->first_acc.reserve(Keff + 1);
         out->rest_x.reserve(A + 1);
         out->rest_slot.reserve(A + 1);
@@ -1451,17 +1445,19 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     out->first_marked = (a.o_first != nullptr || a.o_fan_cnt != nullptr) && hs.n_first <= Keff;
     out->fan = out->first_marked && a.o_fan_cnt != nullptr;
     out->n_rest = out->first_marked ? A - hs.n_first : 0;
-    if (out->fan) {  // slot -> its accesses: offsets by a scan of the counts, then placement
+    if (out->fan) {  // slot -> its other accesses: offsets by a scan of the counts, then placement
         const uint32_t n = (uint32_t)hs.n_first;
+        const uint64_t nr = out->n_rest;
         out->fan_off.reserve((uint64_t)n + 1);
-        out->fan_list.reserve(A + 1);
+        out->fan_list.reserve(nr + 1);
+        GX_CUDA(cudaMemsetAsync(out->fan_cnt.p + n, 0, 4, st));  // scan sentinel
         size_t tb = 0;
         GX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
         out->cub_tmp.reserve(tb + 16);
         GX_CUDA(cub::DeviceScan::ExclusiveSum(out->cub_tmp.p, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
-        if (A) {
-            k_fan_place<<<ctx->num_sms * 4, 256, 0, st>>>(is.acc_slot.p, out->fan_off.p, (uint32_t)A,
-                                                         out->fan_list.p);
+        if (nr) {
+            k_fan_place<<<ctx->num_sms * 4, 256, 0, st>>>(out->rest_x.p, out->rest_slot.p, out->fan_off.p,
+                                                         (uint32_t)nr, out->fan_list.p);
             GX_CHECK_LAUNCH();
         }
     }
