@@ -524,7 +524,7 @@ def main():
     if fan:                     # the headline roofline is the fan-out kernel
         achieved = fan_bytes / (fan_ms / 1e3) / 1e9
         traffic = None
-        if os.path.exists(tp):
+        if os.path.exists(tp) and not staged:   # captured on the device-backed fan-out
             with open(tp) as fh:
                 traffic = json.load(fh).get("k_fan_dram_bytes_per_launch")
     S = cfg["S"]
