@@ -482,15 +482,12 @@ __global__ void __launch_bounds__(GA_THREADS, GatherOcc<R>::value) k_fan_rows(
             }
 #pragma unroll
             for (int q = 0; q < R; ++q) {
+                if (q >= (int)nr) break;
                 uint4* fq = reinterpret_cast<uint4*>(__shfl_sync(0xffffffffu, (unsigned long long)fp, q));
-                if (q < (int)nr && c < nvec) {
+                if (c < nvec) {
                     if (cache_rows) st_na(reinterpret_cast<uint4*>(cache_rows + (uint64_t)(r0 + q) * row_bytes) + c, tmp[q]);
                     if (fq) st_na(fq + c, tmp[q]);
                 }
-            }
-#pragma unroll
-            for (int q = 0; q < R; ++q) {
-                if (q >= (int)nr) break;
                 const uint32_t b = __shfl_sync(0xffffffffu, o, q), e = __shfl_sync(0xffffffffu, o, q + 1);
                 for (uint32_t j = b; j < e; ++j) {
                     const uint32_t v = __shfl_sync(0xffffffffu, d, (j - base) & 31);
