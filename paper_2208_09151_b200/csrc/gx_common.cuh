@@ -230,6 +230,8 @@ struct DevBuf {
     }
     void alloc(size_t count) {
         release();
+        static const bool trace = std::getenv("GX_ALLOC_TRACE") != nullptr;  // growth diagnostics
+        if (trace && count) std::fprintf(stderr, "[gx alloc] %zu bytes\n", count * sizeof(T));
         if (count) {
             cudaError_t e = cudaMalloc(&p, count * sizeof(T));
             if (e != cudaSuccess) {

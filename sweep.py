@@ -23,8 +23,9 @@ def main():
     ap.add_argument("--superbatches", default="1,10,50,100,250,500")
     ap.add_argument("--cache", default="5,10,20,35,50")
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--warmup", type=int, default=2,
-                    help="untimed superbatches per point (>= 2: the pipeline alternates two buffer slots)")
+    ap.add_argument("--warmup", type=int, default=4,
+                    help="untimed superbatches per point: each of the pipeline's two buffer slots grows to "
+                         "the point's sizes (device buffers are grow-only) before the timed steps")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import paper_2208_09151_b200 as gx
