@@ -82,6 +82,7 @@ struct InspectScratch {
     DevBuf<int32_t> init_pos;         // N, -1 when clean (explicit-init API path)
     uint64_t init_pos_n = 0;
     std::vector<uint32_t> h_m, h_io, h_oo;
+    gx::PinBuf<uint8_t> h_pin;  // pinned landing area of the post-inspector readback (one sync)
 };
 }  // namespace gx
 
@@ -128,6 +129,7 @@ struct gx_samples {
     std::vector<uint32_t> h_n_ids;        // host mirrors, valid after the call
     std::vector<uint32_t> h_layer_count;
     std::vector<uint64_t> h_n_seeds;
+    gx::PinBuf<uint32_t> h_pin;  // pinned landing area of samples_sync_host (one sync)
     gx_iostats io{};
 };
 

@@ -1409,17 +1409,26 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         k_init_pos<<<ctx->num_sms, 256, 0, st>>>(B.init_ext.p, (uint32_t)n_init_explicit, is.init_pos.p, 0);
         GX_CHECK_LAUNCH();
     }
-    IState hs;
-    GX_CUDA(cudaMemcpyAsync(&hs, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
+    // one pinned landing area: the copies stay asynchronous and the host waits
+    // once (pageable destinations cost a round trip each)
     std::vector<uint32_t>&m32 = B.h_m, &io32 = B.h_io, &oo32 = B.h_oo;
     m32.resize(S + 1);
     io32.resize(S + 1);
     oo32.resize(S + 1);
-    GX_CUDA(cudaMemcpyAsync(m32.data(), d_misses.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(io32.data(), d_in_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(oo32.data(), d_out_off.p, (S + 1) * 4, cudaMemcpyDeviceToHost, st));
+    const size_t hs_bytes = (sizeof(IState) + 15) / 16 * 16, arr_bytes = (S + 1) * 4;
+    B.h_pin.reserve(hs_bytes + 3 * arr_bytes);
+    uint8_t* hp = B.h_pin.p;
+    GX_CUDA(cudaMemcpyAsync(hp, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp + hs_bytes, d_misses.p, arr_bytes, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp + hs_bytes + arr_bytes, d_in_off.p, arr_bytes, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp + hs_bytes + 2 * arr_bytes, d_out_off.p, arr_bytes, cudaMemcpyDeviceToHost, st));
     if (tracing) GX_CUDA(cudaMemcpyAsync(htb.p, tbuf.p, 64 * 8, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
+    IState hs;
+    std::memcpy(&hs, hp, sizeof(IState));
+    std::memcpy(m32.data(), hp + hs_bytes, arr_bytes);
+    std::memcpy(io32.data(), hp + hs_bytes + arr_bytes, arr_bytes);
+    std::memcpy(oo32.data(), hp + hs_bytes + 2 * arr_bytes, arr_bytes);
     if (tracing) {
         std::fprintf(stderr, "[inspect trace us] A=%llu S=%llu", (unsigned long long)A, (unsigned long long)S);
         for (int k = 1; k < 8; ++k)

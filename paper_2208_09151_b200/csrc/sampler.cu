@@ -1202,13 +1202,19 @@ void samples_sync_host(gx_samples* s) {
     cudaStream_t st = s->ctx->stream;
     s->h_n_ids.resize(s->S);
     s->h_layer_count.resize(s->S * s->L);
-    unsigned long long io[4];
-    GX_CUDA(cudaMemcpyAsync(s->h_n_ids.data(), s->n_ids.p, s->S * 4, cudaMemcpyDeviceToHost, st));
-    if (s->L)
-        GX_CUDA(cudaMemcpyAsync(s->h_layer_count.data(), s->layer_count.p, s->S * s->L * 4,
-                                cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(io, s->ctx->ss.io.p, 3 * 8, cudaMemcpyDeviceToHost, st));
+    // one pinned landing area [io u64 x3 | n_ids S | layer_count S*L]: the
+    // copies stay asynchronous and the host waits once
+    const size_t nl = s->S * s->L;
+    s->h_pin.reserve(6 + s->S + nl);
+    uint32_t* hp = s->h_pin.p;
+    GX_CUDA(cudaMemcpyAsync(hp, s->ctx->ss.io.p, 3 * 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp + 6, s->n_ids.p, s->S * 4, cudaMemcpyDeviceToHost, st));
+    if (nl) GX_CUDA(cudaMemcpyAsync(hp + 6 + s->S, s->layer_count.p, nl * 4, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
+    unsigned long long io[3];
+    std::memcpy(io, hp, sizeof(io));
+    std::memcpy(s->h_n_ids.data(), hp + 6, s->S * 4);
+    if (nl) std::memcpy(s->h_layer_count.data(), hp + 6 + s->S, nl * 4);
     s->io.pages_read = io[0];
     s->io.neighbor_lists_read = io[1];
     s->io.bytes_read = io[2];
