@@ -83,14 +83,6 @@ struct InspectScratch {
     uint64_t init_pos_n = 0;
     std::vector<uint32_t> h_m, h_io, h_oo;
     gx::PinBuf<uint8_t> h_pin;  // pinned landing area of the post-inspector readback (one sync)
-    gx::PinBuf<uint8_t> h_up;   // pinned source of the per-call offset uploads
-    cudaEvent_t up_done = nullptr;  // recorded after the last upload from h_up
-    InspectScratch() = default;
-    InspectScratch(const InspectScratch&) = delete;
-    InspectScratch& operator=(const InspectScratch&) = delete;
-    ~InspectScratch() {
-        if (up_done) cudaEventDestroy(up_done);
-    }
 };
 }  // namespace gx
 

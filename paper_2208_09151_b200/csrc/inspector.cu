@@ -1140,20 +1140,6 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect_rec(IArgs a) {
 
 static InspectScratch& bufs_for(gx_ctx* ctx) { return ctx->is; }
 
-// Small per-call host->device uploads (offset arrays) go through one pinned
-// buffer: a pageable source may make the copy wait for the stream. The buffer
-// is rewritten only after the previous upload from it has executed.
-static void upload_small(InspectScratch& is, void* dst, const void* src, size_t bytes, cudaStream_t st) {
-    if (is.up_done)
-        GX_CUDA(cudaEventSynchronize(is.up_done));
-    else
-        GX_CUDA(cudaEventCreateWithFlags(&is.up_done, cudaEventDisableTiming));
-    is.h_up.reserve(bytes);
-    std::memcpy(is.h_up.p, src, bytes);
-    GX_CUDA(cudaMemcpyAsync(dst, is.h_up.p, bytes, cudaMemcpyHostToDevice, st));
-    GX_CUDA(cudaEventRecord(is.up_done, st));
-}
-
 // Exact reference error for an invalid trace (count_pass, changeset.hpp:76-88).
 static void host_trace_error(const std::vector<uint32_t>& flat, const std::vector<uint64_t>& off,
                              uint64_t N) {
@@ -1231,7 +1217,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     std::vector<uint32_t> off32(S + 1);
     for (uint64_t i = 0; i <= S; ++i) off32[i] = (uint32_t)off[i];
     B.toff.reserve(S + 1);
-    upload_small(is, B.toff.p, off32.data(), (S + 1) * 4, st);
+    GX_CUDA(cudaMemcpyAsync(B.toff.p, off32.data(), (S + 1) * 4, cudaMemcpyHostToDevice, st));
     is.next_use.reserve(std::max<uint64_t>(A, 1));
     const uint64_t ntiles = (A + IN_TILE - 1) / IN_TILE + 1;
     B.tile_cnt.reserve(ntiles);
@@ -1515,7 +1501,7 @@ void inspect_fill_from_device(gx_ctx* ctx, const uint32_t* d_ids, uint64_t strid
     inspect_ensure_trace(ctx, off[S]);
     DevBuf<uint64_t>& d_off = ctx->is.trace_off;
     d_off.reserve(S + 1);
-    upload_small(ctx->is, d_off.p, off.data(), (S + 1) * 8, ctx->stream);
+    GX_CUDA(cudaMemcpyAsync(d_off.p, off.data(), (S + 1) * 8, cudaMemcpyHostToDevice, ctx->stream));
     if (S && off[S]) {
         dim3 grid(64, (unsigned)std::min<uint64_t>(S, 65535));
         k_flatten<<<grid, 256, 0, ctx->stream>>>(d_ids, stride, d_off.p, (uint32_t)S, ctx->is.trace.p);
