@@ -387,6 +387,7 @@ class _Ref:
                                            C_.POINTER(u64), u64p]
             L.gxr_cache_apply.argtypes = [vp, vp, u64, u32, u64p, u64, u64p, u64p, u64, u64p, u64]
             L.gxr_cache_resident.argtypes = [vp, u64p, u64, C_.POINTER(u64)]
+            L.gxr_cache_row.argtypes = [vp, u64, vp]
             L.gxr_run_superbatch.argtypes = [C_.c_char_p, C_.c_char_p, C_.c_char_p, u64p, u64p, u64,
                                              u32p, u32, u64, u64, u64, C_.c_uint,
                                              np.ctypeslib.ndpointer(np.float64), C_.POINTER(u64),
@@ -620,6 +621,11 @@ class _RefCache:
         k = u64()
         self.r._chk(self.r.lib.gxr_cache_resident(self.h, out, len(out), C_.byref(k)))
         return out[:k.value].copy()
+
+    def row(self, v, dim):
+        out = np.zeros(dim, np.float32)
+        self.r._chk(self.r.lib.gxr_cache_row(self.h, int(v), out.ctypes.data))
+        return out
 
 
 C = _Oracle(oracle_lib_path)

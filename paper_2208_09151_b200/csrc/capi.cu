@@ -491,6 +491,10 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                                            &p->samples, fx_epoch ? ctx->is.firstx.p : nullptr, fx_epoch);
         GX_CUDA(cudaEventRecord(sl.ev[1], A));
         samples_sync_host(&p->samples);  // host needs |ids_i| (stream A only)
+        // duplicate seeds are found by the sampler's layer-0 table build; the
+        // reference's sample_batch throws and superbatch_sample rethrows it as
+        // runtime_error (sampler.hpp:83, 236). Nothing downstream ran yet.
+        if (p->samples.dup_seed) fail(GX_RUNTIME_ERROR, "superbatch sample failed: duplicate seed in batch");
         sl.sampled_edges = gx_samples_total_edges(&p->samples);
         sl.sample_io = p->samples.io;
         sl.S = S;

@@ -12,6 +12,8 @@
 //    the inspector precomputed; k_apply (API path) recomputes them from this
 //    cache's own free list, exactly as the reference does.
 #include <algorithm>
+#include <array>
+#include <map>
 #include <mutex>
 #include <cstdlib>
 
@@ -567,24 +569,30 @@ __global__ void __launch_bounds__(128) k_fill_first_tma(const uint32_t* __restri
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// launch configuration of a dynamic-smem kernel for one row size on one device
+struct LaunchCfg {
+    uint64_t rb = 0;  // row size the entry was set up for (0 = not yet)
+    int tpb = 0, bps = 0;
+};
+
 void launch_fill_first(gx_ctx* ctx, const uint32_t* init, const uint32_t* first_acc, uint32_t n,
                        const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch) {
     if (!n) return;
     if (rb % 16) fail(GX_INVALID_ARGUMENT, "fused fill needs 16-byte rows");
     static const int tma = env_int("GX_FILL_TMA", 0);  // bulk-copy form: 1.85 vs 1.67 ms (LDG/STG) at papers shape
     if (tma && (uint64_t)2 * 32 * rb <= (uint64_t)gather_smem_budget(rb)) {
-        static int tpb = 0, bpsm = 0;
-        static uint64_t last = 0;
-        static std::mutex mu;
-        std::lock_guard<std::mutex> lk(mu);
-        if (last != rb) {
-            tpb = (int)std::min<uint64_t>(128, gather_smem_budget(rb) / (2 * rb)) & ~31;
-            const int smem = tpb * 2 * (int)rb;
+        static PerDevice<LaunchCfg> cfg_dev;  // the smem attribute is per device
+        auto lk = cfg_dev.lock();
+        LaunchCfg& cf = cfg_dev.at(ctx->device);
+        if (cf.rb != rb) {
+            cf.tpb = (int)std::min<uint64_t>(128, gather_smem_budget(rb) / (2 * rb)) & ~31;
+            const int smem = cf.tpb * 2 * (int)rb;
             GX_CUDA(cudaFuncSetAttribute(k_fill_first_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, k_fill_first_tma, tpb, smem));
-            bpsm = std::max(bpsm, 1);
-            last = rb;
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cf.bps, k_fill_first_tma, cf.tpb, smem));
+            cf.bps = std::max(cf.bps, 1);
+            cf.rb = rb;
         }
+        const int tpb = cf.tpb, bpsm = cf.bps;
         const uint64_t blocks = std::min<uint64_t>((n + tpb - 1) / tpb, (uint64_t)ctx->num_sms * bpsm);
         k_fill_first_tma<<<(unsigned)blocks, tpb, (size_t)tpb * 2 * rb, lstream(ctx)>>>(init, first_acc, n, store,
                                                                                       (uint32_t)rb, cache_rows, batch);
@@ -692,6 +700,31 @@ __global__ void k_apply(const uint32_t* __restrict__ in_ids, const uint32_t* __r
     }
 }
 
+// Changesets with duplicate ids (API path). The reference accepts them and
+// runs its loops in order (feature_cache.hpp:103-129): a duplicated out id
+// frees the same slot twice, a duplicated in id is rewritten by its later
+// entry. One warp replays exactly that sequence (rows lane-strided, so a
+// later copy into the same slot lands after the earlier one).
+template <int VEC>
+__global__ void k_apply_serial(const uint32_t* __restrict__ in_ids, const uint32_t* __restrict__ in_pos,
+                               uint32_t n_in, const uint32_t* __restrict__ out_ids, uint32_t n_out, int32_t* table,
+                               uint32_t* free_list, uint64_t top, const uint8_t* __restrict__ batch,
+                               uint8_t* cache_rows, uint64_t row_bytes, uint32_t* freed) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t k = lane; k < n_out; k += 32) freed[k] = (uint32_t)table[out_ids[k]];  // pre-update state
+    __syncwarp();
+    for (uint32_t k = lane; k < n_out; k += 32) table[out_ids[k]] = -1;
+    __syncwarp();
+    uint64_t t = top;
+    for (uint32_t k = 0; k < n_in; ++k) {
+        const uint32_t s = k < n_out ? freed[k] : free_list[--t];
+        warp_copy_row<VEC>(batch + (uint64_t)in_pos[k] * row_bytes, cache_rows + (uint64_t)s * row_bytes, row_bytes);
+        if (lane == 0) table[in_ids[k]] = (int32_t)s;
+        __syncwarp();
+    }
+    for (uint32_t k = n_in + lane; k < n_out; k += 32) free_list[t + (k - n_in)] = freed[k];
+}
+
 __global__ void k_iota_desc(uint32_t* p, uint64_t n, uint64_t K) {
     // free list [K-1, K-2, ..., K-n]: back() pops ascending from K-n
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -705,15 +738,19 @@ __global__ void k_reset_table(const uint32_t* nodes, uint64_t n, int32_t* table)
         table[nodes[i]] = -1;
 }
 
-__global__ void k_resident(const int32_t* table, uint64_t N, uint32_t* out, unsigned int* cnt) {
+__global__ void k_resident(const int32_t* table, uint64_t N, uint32_t* out, uint64_t cap, unsigned int* cnt) {
     // compaction in id order via a two-level approach is not needed for a test
-    // hook: emit (unordered) and let the host sort.
+    // hook: emit (unordered, at most cap) and let the host sort.
     for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < N;
          v += (uint64_t)gridDim.x * blockDim.x)
-        if (table[v] >= 0) out[atomicAdd(cnt, 1u)] = (uint32_t)v;
+        if (table[v] >= 0) {
+            const unsigned int k = atomicAdd(cnt, 1u);
+            if (k < cap) out[k] = (uint32_t)v;
+        }
 }
 
 static bool vec16(uint64_t row_bytes) { return row_bytes % 16 == 0; }
+
 
 // digest = sum over u32 words x of (word[x] + 1) * mix64(x)  (mod 2^64)
 __global__ void k_digest(const uint32_t* __restrict__ w, uint64_t nwords, unsigned long long* out) {
@@ -790,19 +827,21 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
     static const int ring = env_int("GX_GATHER_D", 0);  // 3/4/6: k_gather_ring<D> (experimental)
     static std::mutex cfg_mu;  // launch-config caches below are shared by every context / host thread
     std::lock_guard<std::mutex> cfg_lock(cfg_mu);
+    const int dev = ctx->device;  // dynamic-smem attributes are per device
     if (!staged && vec16(rb) && R == 1 && (ring == 3 || ring == 4 || ring == 6) &&
         (uint64_t)ring * 32 * rb <= (uint64_t)budget) {
-        static int tpb = 0, bpsm = 0;
-        static uint64_t last = 0;
+        static std::map<int, LaunchCfg> ring_cfg;  // per device
+        LaunchCfg& cf = ring_cfg[dev];
         auto kfn = ring == 3 ? k_gather_ring<3> : ring == 4 ? k_gather_ring<4> : k_gather_ring<6>;
-        if (last != rb) {
-            last = rb;
-            tpb = (int)std::min<uint64_t>(256, budget / (ring * rb)) & ~31;
-            const int smem = tpb * ring * (int)rb;
+        if (cf.rb != rb) {
+            cf.rb = rb;
+            cf.tpb = (int)std::min<uint64_t>(256, budget / (ring * rb)) & ~31;
+            const int smem = cf.tpb * ring * (int)rb;
             GX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bpsm, kfn, tpb, smem));
-            bpsm = std::max(bpsm, 1);
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cf.bps, kfn, cf.tpb, smem));
+            cf.bps = std::max(cf.bps, 1);
         }
+        const int tpb = cf.tpb, bpsm = cf.bps;
         static const int ctas_knob = env_int("GX_GATHER_CTAS", 0);
         const uint64_t cap = ctas_knob > 0 ? (uint64_t)ctas_knob : (uint64_t)ctx->num_sms * bpsm;
         const uint64_t blocks = std::min<uint64_t>((n + tpb - 1) / tpb, cap);
@@ -817,8 +856,8 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         fail(GX_LOGIC_ERROR, "the fused all-fit gather needs the bulk-copy kernel");
     if (vec16(rb) && R <= 1 && (uint64_t)depth * 32 * rb <= (uint64_t)budget) {
         // launch config per (depth, staged), cached for the last row size
-        static int tpb[6] = {0, 0, 0, 0, 0, 0}, bps[6] = {0, 0, 0, 0, 0, 0};
-        static uint64_t last_rb[6] = {0, 0, 0, 0, 0, 0};
+        static std::map<int, std::array<LaunchCfg, 6>> tma_cfg;  // per device
+        std::array<LaunchCfg, 6>& cfs = tma_cfg[dev];
         const bool skip = skip_first && depth == 2 && !staged;
         const int d = skip ? 4 : (depth - 1) + 2 * (int)staged;
         using KFn = void (*)(const uint32_t*, const uint32_t*, uint32_t, const uint8_t*, const uint8_t*, uint32_t,
@@ -826,18 +865,19 @@ void launch_gather_resolved(gx_ctx* ctx, const uint32_t* ids, const uint32_t* sl
         const KFn kfn = skip ? (KFn)k_gather_tma2<false, true>
                         : depth == 2 ? (staged ? (KFn)k_gather_tma2<true> : (KFn)k_gather_tma2<false>)
                                      : (staged ? (KFn)k_gather_tma<true> : (KFn)k_gather_tma<false>);
-        if (last_rb[d] != rb) {  // threads per CTA: one (or two) row buffers per thread
-            tpb[d] = (int)std::min<uint64_t>(128, budget / (depth * rb)) & ~31;
-            const int smem = tpb[d] * depth * (int)rb;
+        LaunchCfg& cf = cfs[d];
+        if (cf.rb != rb) {  // threads per CTA: one (or two) row buffers per thread
+            cf.tpb = (int)std::min<uint64_t>(128, budget / (depth * rb)) & ~31;
+            const int smem = cf.tpb * depth * (int)rb;
             GX_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps[d], kfn, tpb[d], smem));
-            bps[d] = std::max(bps[d], 1);
-            last_rb[d] = rb;
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cf.bps, kfn, cf.tpb, smem));
+            cf.bps = std::max(cf.bps, 1);
+            cf.rb = rb;
         }
         static const int ctas_knob = env_int("GX_GATHER_CTAS", 0);  // cap on CTAs (0 = all resident)
-        const uint64_t cap = ctas_knob > 0 ? (uint64_t)ctas_knob : (uint64_t)ctx->num_sms * bps[d];
-        const uint64_t blocks = std::min<uint64_t>((n + tpb[d] - 1) / tpb[d], cap);
-        kfn<<<(unsigned)blocks, tpb[d], (size_t)tpb[d] * depth * rb, lstream(ctx)>>>(
+        const uint64_t cap = ctas_knob > 0 ? (uint64_t)ctas_knob : (uint64_t)ctx->num_sms * cf.bps;
+        const uint64_t blocks = std::min<uint64_t>((n + cf.tpb - 1) / cf.tpb, cap);
+        kfn<<<(unsigned)blocks, cf.tpb, (size_t)cf.tpb * depth * rb, lstream(ctx)>>>(
             ids, slots, (uint32_t)n, cache_rows, store, (uint32_t)rb, out, counters, sg);
         GX_CHECK_LAUNCH();
     } else if (vec16(rb)) {
@@ -1075,7 +1115,16 @@ gx_status gx_cache_apply(gx_cache* c, const gx_batch* batch, const uint64_t* ids
             if (out_ids[k] >= c->f->n) fail(GX_LOGIC_ERROR, "evicted node is not cached");
         for (uint64_t k = 0; k < n_in; ++k)
             if (in_ids[k] >= c->f->n) fail(GX_LOGIC_ERROR, "changeset position does not match ids");
-        const uint64_t tot = n_ids + 2 * n_in + n_out;
+        // duplicate ids inside the changeset take the exact sequential replay
+        // (k_apply_serial); the parallel kernel assumes distinct in and out ids
+        auto has_dup = [](const uint64_t* v, uint64_t n) {
+            if (n < 2) return false;
+            std::vector<uint64_t> t(v, v + n);
+            std::sort(t.begin(), t.end());
+            return std::adjacent_find(t.begin(), t.end()) != t.end();
+        };
+        const bool dup = has_dup(in_ids, n_in) || has_dup(out_ids, n_out);
+        const uint64_t tot = n_ids + 2 * n_in + n_out + (dup ? n_out : 0);
         c->scratch.reserve(std::max<uint64_t>(tot, 1));
         upload_u32(ctx, c->scratch, 0, ids, n_ids);
         upload_u32(ctx, c->scratch, n_ids, in_ids, n_in);
@@ -1098,7 +1147,18 @@ gx_status gx_cache_apply(gx_cache* c, const gx_batch* batch, const uint64_t* ids
         if (e) fail(GX_LOGIC_ERROR, "invalid changeset for the current cache state");
         if (n_in > n_out + c->free_top) fail(GX_LOGIC_ERROR, "changeset overflows cache capacity");
         const uint32_t m = (uint32_t)std::max(n_in, n_out);
-        if (m) {
+        if (m && dup) {
+            uint32_t* freed = c->scratch.p + n_ids + 2 * n_in + n_out;
+            if (vec16(c->f->row_bytes))
+                k_apply_serial<16><<<1, 32, 0, ctx->stream>>>(d_in, d_pos, (uint32_t)n_in, d_out, (uint32_t)n_out,
+                                                             c->table.p, c->free_list.p, c->free_top, batch->data.p,
+                                                             c->rows.p, c->f->row_bytes, freed);
+            else
+                k_apply_serial<4><<<1, 32, 0, ctx->stream>>>(d_in, d_pos, (uint32_t)n_in, d_out, (uint32_t)n_out,
+                                                            c->table.p, c->free_list.p, c->free_top, batch->data.p,
+                                                            c->rows.p, c->f->row_bytes, freed);
+            GX_CHECK_LAUNCH();
+        } else if (m) {
             const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)m * 32 + 255) / 256, ctx->num_sms * 8);
             if (vec16(c->f->row_bytes))
                 k_apply<16><<<blocks, 256, 0, ctx->stream>>>(d_in, d_pos, (uint32_t)n_in, d_out, (uint32_t)n_out,
@@ -1139,14 +1199,23 @@ gx_status gx_cache_cached_row(const gx_cache* c, uint64_t v, void* out) {
 gx_status gx_cache_resident_set(const gx_cache* c, uint64_t* out, uint64_t cap, uint64_t* n) {
     return guard([&] {
         gx_ctx* ctx = c->ctx;
-        DevBuf<uint32_t> tmp(std::max<uint64_t>(c->K, 1));
+        // more residents than slots is possible after a changeset with
+        // duplicate out ids (two nodes share a freed slot, as in the reference):
+        // size by the count and retry once
+        uint64_t cap = std::max<uint64_t>(c->K, 1);
+        DevBuf<uint32_t> tmp(cap);
         DevBuf<unsigned int> cnt(1);
-        GX_CUDA(cudaMemsetAsync(cnt.p, 0, 4, ctx->stream));
-        k_resident<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(c->table.p, c->f->n, tmp.p, cnt.p);
-        GX_CHECK_LAUNCH();
         unsigned int hc = 0;
-        GX_CUDA(cudaMemcpyAsync(&hc, cnt.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        GX_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int pass = 0; pass < 2; ++pass) {
+            GX_CUDA(cudaMemsetAsync(cnt.p, 0, 4, ctx->stream));
+            k_resident<<<ctx->num_sms * 4, 256, 0, ctx->stream>>>(c->table.p, c->f->n, tmp.p, cap, cnt.p);
+            GX_CHECK_LAUNCH();
+            GX_CUDA(cudaMemcpyAsync(&hc, cnt.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+            GX_CUDA(cudaStreamSynchronize(ctx->stream));
+            if (hc <= cap) break;
+            cap = hc;
+            tmp.alloc(cap);
+        }
         std::vector<uint32_t> h(hc);
         if (hc) GX_CUDA(cudaMemcpy(h.data(), tmp.p, hc * 4, cudaMemcpyDeviceToHost));
         std::sort(h.begin(), h.end());
@@ -1175,12 +1244,14 @@ gx_status gx_features_read_rows(gx_features* f, const uint64_t* ids, uint64_t n,
         DevBuf<uint32_t> d(std::max<uint64_t>(n, 1));
         upload_u32(ctx, d, 0, ids, n);
         DevBuf<uint8_t> o(std::max<uint64_t>(n * f->row_bytes, 16));
-        DevBuf<int32_t> none(1);  // table lookup is skipped via an all-miss table below
-        DevBuf<int32_t> table(std::max<uint64_t>(f->n, 1));
-        GX_CUDA(cudaMemsetAsync(table.p, 0xff, std::max<uint64_t>(f->n, 1) * 4, ctx->stream));
         DevBuf<unsigned long long> cnt(8);
         GX_CUDA(cudaMemsetAsync(cnt.p, 0, 64, ctx->stream));
-        launch_gather(ctx, d.p, n, table.p, nullptr, f, o.p, cnt.p);
+        // every row is a backing-store read: the all-miss form (no slots, no
+        // address table), charging pages like FeatureFile::read_row
+        const cudaStream_t saved = ctx->launch_stream;
+        ctx->launch_stream = nullptr;
+        launch_gather_resolved(ctx, d.p, nullptr, n, nullptr, f->rows_dev_view, f->row_bytes, o.p, cnt.p);
+        ctx->launch_stream = saved;
         unsigned long long h[5];
         GX_CUDA(cudaMemcpyAsync(h, cnt.p, 40, cudaMemcpyDeviceToHost, ctx->stream));
         GX_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -12,6 +12,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -32,6 +34,24 @@ __device__ __forceinline__ unsigned long long gtimer() {
 inline int env_int(const char* name, int def) {
     const char* e = std::getenv(name);
     return (e && *e) ? std::atoi(e) : def;
+}
+
+// Kernel attributes (cudaFuncSetAttribute) and occupancy results are per
+// device: launch-configuration caches are kept per device ordinal so a second
+// context on another GPU of the same process sets them up again.
+template <class T>
+struct PerDevice {
+    std::mutex mu;
+    std::map<int, T> m;
+    // the entry of `dev`, value-initialised on first use; callers that fill it
+    // lazily hold lock() while they do
+    T& at(int dev) { return m[dev]; }
+    std::unique_lock<std::mutex> lock() { return std::unique_lock<std::mutex>(mu); }
+};
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
 }
 
 // Persistent grid-barrier kernels (sampler, inspector) are sized to be fully

@@ -96,6 +96,8 @@ struct gx_ctx {
     gx::DevBuf<uint32_t> resolve_slots;  // executor API path scratch
     gx::DevBuf<uint32_t> stage_ids;      // API path: miss ids staged from storage
     gx::DevBuf<uint8_t> stage_rows;      // API path: their rows
+    gx::DevBuf<uint32_t> miss_flags, miss_ranks;  // stage_misses scan scratch (storage.cu)
+    gx::DevBuf<uint8_t> miss_tmp;
     cudaStream_t launch_stream = nullptr;  // executor launches go here when set (pipeline stream)
 };
 
@@ -126,6 +128,7 @@ struct gx_samples {
     gx::DevBuf<uint32_t> n_ids;           // S
     gx::DevBuf<uint2> edges;              // S * cap_e_batch  (src_local, dst_local)
     gx::DevBuf<uint32_t> layer_count;     // S * L
+    bool dup_seed = false;                // a batch had a duplicate seed (set by samples_sync_host)
     std::vector<uint32_t> h_n_ids;        // host mirrors, valid after the call
     std::vector<uint32_t> h_layer_count;
     std::vector<uint64_t> h_n_seeds;

@@ -27,6 +27,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <array>
 #include <mutex>
 #include <unordered_set>
 
@@ -1379,10 +1380,13 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     void* const kfns[3] = {(void*)k_inspect<128>, (void*)k_inspect<512>, (void*)k_inspect<kMaxIters>};
     void* const rfns[3] = {(void*)k_inspect_rec<128>, (void*)k_inspect_rec<512>, (void*)k_inspect_rec<kMaxIters>};
     const size_t smems[3] = {sizeof(ISmem<128>), sizeof(ISmem<512>), sizeof(ISmem<kMaxIters>)};
-    static int bps0[3] = {0, 0, 0};
-    static std::mutex attr_mu;
+    // attributes and occupancy are per device: cached per device ordinal
+    static PerDevice<std::array<int, 3>> bps0_dev;
+    GX_CUDA(cudaSetDevice(ctx->device));
+    int bps0_ci = 0;
     {
-        std::lock_guard<std::mutex> lk(attr_mu);
+        auto lk = bps0_dev.lock();
+        std::array<int, 3>& bps0 = bps0_dev.at(ctx->device);
         if (!bps0[ci]) {
             int b1 = 0, b0 = 0;
             GX_CUDA(cudaFuncSetAttribute(kfns[ci], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smems[ci]));
@@ -1392,8 +1396,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
             if (b1 < 1 || b0 < 1) fail(GX_CUDA_ERROR, "inspector kernel cannot be resident");
             bps0[ci] = std::min(b0, GX_IN_FRONT_BPS);
         }
+        bps0_ci = bps0[ci];
     }
-    const int g0 = std::min(grid0, ctx->num_sms * bps0[ci]);
+    const int g0 = std::min(grid0, ctx->num_sms * bps0_ci);
     void* args[] = {&a};
     for (int part = 0; part < 2; ++part) {
         void* fn = part ? rfns[ci] : kfns[ci];

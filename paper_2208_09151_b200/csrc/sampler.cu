@@ -206,8 +206,10 @@ __device__ __forceinline__ uint32_t tile_offset(const uint32_t* tsum, uint32_t f
     return r;
 }
 
+// *dup (optional) is set when the key was already present: at layer 0 that
+// is a duplicate seed, which the reference rejects (sampler.hpp:83)
 __device__ __forceinline__ uint32_t table_insert(unsigned long long* tab, uint32_t H, uint32_t key,
-                                                 uint32_t val) {
+                                                 uint32_t val, bool* dup = nullptr) {
     const unsigned long long ent = ((unsigned long long)key << 32) | val;
     uint32_t s = hash32(key) & (H - 1);
     while (true) {
@@ -219,6 +221,7 @@ __device__ __forceinline__ uint32_t table_insert(unsigned long long* tab, uint32
         }
         if ((uint32_t)(cur >> 32) == key) {
             if (cur > ent) atomicMin(&tab[s], ent);
+            if (dup) *dup = true;
             return s;
         }
         s = (s + 1) & (H - 1);
@@ -399,7 +402,9 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 } else {
                     v = a.ids[gi];
                 }
-                table_insert(tnew + (uint64_t)b * a.tab_cap, newH, v, k);
+                bool dup = false;
+                table_insert(tnew + (uint64_t)b * a.tab_cap, newH, v, k, l == 0 ? &dup : nullptr);
+                if (dup) atomicOr(&a.io[3], 1ull);  // duplicate seed: the host fails the call
             }
             if (l > 0) {  // the previous layer's table is dead: bulk-clear its used region
                 clear_region(told, a.tab_cap, H, S);
@@ -840,7 +845,9 @@ __global__ void __launch_bounds__(SC_THREADS) k_sample_cl(SampArgs a) {
                     } else {
                         v = __ldcg(a.ids + ibase + k);
                     }
-                    table_insert(tnew, newH, v, k);
+                    bool dup = false;
+                    table_insert(tnew, newH, v, k, l == 0 ? &dup : nullptr);
+                    if (dup) atomicOr(&a.io[3], 1ull);
                 }
                 if (l > 0) cur ^= 1;
                 H = newH;
@@ -1101,14 +1108,22 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     }
 
     const size_t smem = sizeof(SampSmem);
-    static int blocks_per_sm = -1;
-    if (blocks_per_sm < 0) {
-        GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        static const int carve = env_int("GX_SAMPLER_CARVEOUT", -1);  // % of the array as shared memory
-        if (carve >= 0)
-            GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_sample, SB_THREADS, smem));
-        if (blocks_per_sm < 1) fail(GX_CUDA_ERROR, "sampler kernel cannot be resident");
+    // attributes and occupancy are per device: cached per device ordinal
+    static PerDevice<int> bps_dev;
+    GX_CUDA(cudaSetDevice(ctx->device));
+    int blocks_per_sm = 0;
+    {
+        auto lk = bps_dev.lock();
+        int& cached = bps_dev.at(ctx->device);
+        if (cached < 1) {
+            GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            static const int carve = env_int("GX_SAMPLER_CARVEOUT", -1);  // % of the array as shared memory
+            if (carve >= 0)
+                GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+            GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cached, k_sample, SB_THREADS, smem));
+            if (cached < 1) fail(GX_CUDA_ERROR, "sampler kernel cannot be resident");
+        }
+        blocks_per_sm = cached;
     }
     // CTAs per SM (GX_SAMPLER_BPS, default GX_SB_MINB): all that fit
     static const int bps_use = [] {
@@ -1125,10 +1140,14 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         return (v == 8 || v == 16) ? v : 0;
     }();
     if (cs) {
-        static bool attr = false;
-        if (!attr) {
-            GX_CUDA(cudaFuncSetAttribute(k_sample_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            attr = true;
+        static PerDevice<bool> attr_dev;
+        {
+            auto lk = attr_dev.lock();
+            bool& attr = attr_dev.at(ctx->device);
+            if (!attr) {
+                GX_CUDA(cudaFuncSetAttribute(k_sample_cl<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                attr = true;
+            }
         }
         const uint32_t ncl = std::max(1, ctx->num_sms / cs);
         for (uint64_t c0 = 0; c0 < S; c0 += CH) {
@@ -1205,16 +1224,17 @@ void samples_sync_host(gx_samples* s) {
     // one pinned landing area [io u64 x3 | n_ids S | layer_count S*L]: the
     // copies stay asynchronous and the host waits once
     const size_t nl = s->S * s->L;
-    s->h_pin.reserve(6 + s->S + nl);
+    s->h_pin.reserve(8 + s->S + nl);
     uint32_t* hp = s->h_pin.p;
-    GX_CUDA(cudaMemcpyAsync(hp, s->ctx->ss.io.p, 3 * 8, cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(hp + 6, s->n_ids.p, s->S * 4, cudaMemcpyDeviceToHost, st));
-    if (nl) GX_CUDA(cudaMemcpyAsync(hp + 6 + s->S, s->layer_count.p, nl * 4, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp, s->ctx->ss.io.p, 4 * 8, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp + 8, s->n_ids.p, s->S * 4, cudaMemcpyDeviceToHost, st));
+    if (nl) GX_CUDA(cudaMemcpyAsync(hp + 8 + s->S, s->layer_count.p, nl * 4, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
-    unsigned long long io[3];
+    unsigned long long io[4];
     std::memcpy(io, hp, sizeof(io));
-    std::memcpy(s->h_n_ids.data(), hp + 6, s->S * 4);
-    if (nl) std::memcpy(s->h_layer_count.data(), hp + 6 + s->S, nl * 4);
+    std::memcpy(s->h_n_ids.data(), hp + 8, s->S * 4);
+    if (nl) std::memcpy(s->h_layer_count.data(), hp + 8 + s->S, nl * 4);
+    s->dup_seed = io[3] != 0;
     s->io.pages_read = io[0];
     s->io.neighbor_lists_read = io[1];
     s->io.bytes_read = io[2];

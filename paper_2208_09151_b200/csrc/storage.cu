@@ -297,8 +297,9 @@ uint64_t stage_misses(gx_ctx* ctx, const uint32_t* ids, uint32_t* slots, uint64_
                       cudaStream_t s) {
     if (!n) return 0;
     if (n >= kStageFlag) fail(GX_OVERFLOW, "too many accesses for the staging index");
-    static thread_local DevBuf<uint32_t> flags, ranks;
-    static thread_local DevBuf<uint8_t> tmp;
+    // per-context scratch (allocated on this context's device, freed with it)
+    DevBuf<uint32_t>&flags = ctx->miss_flags, &ranks = ctx->miss_ranks;
+    DevBuf<uint8_t>& tmp = ctx->miss_tmp;
     flags.reserve(n);
     ranks.reserve(n);
     const unsigned g = ctx->num_sms * 4;

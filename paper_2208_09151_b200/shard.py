@@ -10,7 +10,7 @@ box, gloo in the CPU tests).
 """
 from __future__ import annotations
 
-from typing import List, Sequence
+from typing import List, NamedTuple, Optional, Sequence
 
 
 def assign_superbatches(num_superbatches: int, rank: int, world: int, steps: int,
@@ -23,9 +23,41 @@ def assign_superbatches(num_superbatches: int, rank: int, world: int, steps: int
     return [(rank + (start + k) * world) % num_superbatches for k in range(steps)]
 
 
-def first_global_batch(sb_index: int, superbatch_size: int) -> int:
-    """Global index of the first batch of a superbatch (TrainingRunner::run, pipeline.hpp:214-228)."""
-    return sb_index * superbatch_size
+class Job(NamedTuple):
+    """One (epoch, superbatch) job of TrainingRunner::run (pipeline.hpp:206-228)."""
+    epoch: int
+    seq: int                 # position in the flattened job list
+    first_global_batch: int  # batches of all earlier jobs, short final superbatches included
+    lo: int                  # batch range [lo, hi) of the epoch's seed plan
+    hi: int
+
+
+def superbatch_jobs(batches_per_epoch: Sequence[int], superbatch_size: int) -> List[Job]:
+    """The flattened job list of TrainingRunner::run (pipeline.hpp:212-228):
+    every epoch's plan is cut into superbatches of `superbatch_size` batches
+    (the last one may be short) and first_global_batch counts the batches of
+    all earlier jobs, so batch seeds stay the reference's across epochs."""
+    if superbatch_size < 1:
+        raise ValueError("superbatch_size must be >= 1")
+    jobs: List[Job] = []
+    g = 0
+    for e, nb in enumerate(batches_per_epoch):
+        for off in range(0, nb, superbatch_size):
+            end = min(off + superbatch_size, nb)
+            jobs.append(Job(e, len(jobs), g, off, end))
+            g += end - off
+    return jobs
+
+
+def first_global_batch(sb_index: int, superbatch_size: int,
+                       batches_per_epoch: Optional[Sequence[int]] = None) -> int:
+    """Global index of the first batch of job `sb_index` (pipeline.hpp:214-228).
+    Without `batches_per_epoch` the job is taken from epoch 0 (sb_index * S);
+    with it, from the flattened multi-epoch job list (short final superbatches
+    of earlier epochs counted as the reference counts them)."""
+    if batches_per_epoch is None:
+        return sb_index * superbatch_size
+    return superbatch_jobs(batches_per_epoch, superbatch_size)[sb_index].first_global_batch
 
 
 def reduce_stats(values: Sequence[float], ops: Sequence[str], device=None) -> List[float]:

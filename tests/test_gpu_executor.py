@@ -345,3 +345,67 @@ def test_allfit_fan_out_forms(gx, oracle, fanout, S):
     assert res["ok"] and res["fused"] and res["fan"] == bool(fanout), res
     assert res["misses"] == 0 and res["init"] == res["distinct"], res
     assert res["hub"] > 32 or S < 64, res                      # S = 1: no access besides the first uses
+
+
+def test_apply_duplicate_ids_match_reference(gx, ref, tmp_path):
+    """apply_changeset with duplicate ids (feature_cache.hpp:103-129): the
+    reference accepts them -- a duplicated out id frees its slot twice (two
+    inserted nodes then share it, the later row wins), a duplicated in id is
+    rewritten by its later entry. The device path replays exactly that."""
+    dim = 8
+    rows = _feat(12, dim, 5)
+    path = str(tmp_path / "features.bin")
+    ref.write_features(path, rows)
+    rf = ref.open_features(path)
+    f = gx.FeatureFile.from_array(rows)
+    cases = [
+        ([2, 5], [0, 0], [1, 2]),        # duplicated out: 2 and 5 share slot(0)
+        ([2, 2], [0], [1, 1]),           # duplicated in: 2 written twice
+        ([2, 5, 2], [0, 6, 6], [1, 2, 1]),
+        ([2], [0, 0, 6], [1]),           # surplus freed slots pushed twice
+    ]
+    for in_ids, out_ids, in_pos in cases:
+        init = [0, 1, 4, 6, 7]
+        c = gx.FeatureCache(f, init, 6)
+        rc = rf.cache(init, 6)
+        ids = [0, 2, 5, 7]
+        b, _ = c.gather(f, ids)
+        rb, _, _, _ = rc.gather(ids, dim)
+        assert b.numpy().tobytes() == rb.tobytes()
+        c.apply_changeset(b, ids, gx.Changeset(in_ids, out_ids, in_pos))
+        rc.apply(rb, ids, in_ids, in_pos, out_ids)
+        res = rc.resident(12)
+        assert list(c.resident_set()) == list(res)
+        for v in res:
+            assert c.cached_row(int(v)).tobytes() == rc.row(int(v), dim).tobytes()
+        # later traffic goes through the same (shared / re-pushed) slots
+        ids2 = [3, 8, 9, 10]
+        b2, _ = c.gather(f, ids2)
+        rb2, _, _, _ = rc.gather(ids2, dim)
+        assert b2.numpy().tobytes() == rb2.tobytes()
+        c.apply_changeset(b2, ids2, gx.Changeset([3, 8], [], [0, 1]))
+        rc.apply(rb2, ids2, [3, 8], [0, 1], [])
+        assert list(c.resident_set()) == list(rc.resident(12))
+        for v in rc.resident(12):
+            assert c.cached_row(int(v)).tobytes() == rc.row(int(v), dim).tobytes()
+
+
+def test_pipeline_rejects_duplicate_seeds(gx, oracle):
+    """superbatch_sample rethrows sample_batch's duplicate-seed
+    invalid_argument as runtime_error (sampler.hpp:83, 236); the fused
+    pipeline reports the same, and stays usable afterwards."""
+    ip, ind = oracle.rmat_graph(3000, 5.0, 21)
+    g = gx.GraphFile.from_csc(ip, ind)
+    f = gx.FeatureFile.from_array(_feat(3000, 16, 2))
+    p = gx.Pipeline(g, f, [4, 4], 500)
+    good = [np.arange(10, 40, dtype=np.uint64), np.arange(100, 130, dtype=np.uint64)]
+    bad = [good[0], np.array([7, 8, 9, 8], np.uint64)]
+    with pytest.raises(RuntimeError) as e1:
+        p.run_superbatch(bad, 1, 0)
+    with pytest.raises(RuntimeError) as e2:
+        gx.sample_superbatch(g, None, bad, [4, 4], 1, 0)
+    assert type(e1.value) is RuntimeError and type(e2.value) is RuntimeError  # not a CudaError
+    st = p.run_superbatch(good, 1, 0)
+    ref_edges = sum(sum(len(l) for l in oracle.sample_batch(ip, ind, b, [4, 4], oracle.derive_seed(1, i))[1])
+                    for i, b in enumerate(good))
+    assert st.sampled_edges == ref_edges

@@ -143,3 +143,17 @@ def test_partitioned_exchange_protocol_gloo():
     assert all(ok for _, ok, _, _, _ in res)
     assert sum(r[2] for r in res) == sum(r[3] for r in res)   # every request served exactly once
     assert all(r[4] > 0 for r in res)                          # rows did cross ranks
+
+
+def test_superbatch_jobs_multi_epoch():
+    """TrainingRunner::run (pipeline.hpp:212-228): each epoch's plan is cut
+    into superbatches (short last one kept) and first_global_batch counts every
+    earlier job's batches -- 7 batches per epoch at S = 3 give jobs of
+    3, 3, 1 batches per epoch."""
+    from paper_2208_09151_b200.shard import first_global_batch, superbatch_jobs
+    jobs = superbatch_jobs([7, 7], 3)
+    assert [(j.epoch, j.lo, j.hi, j.first_global_batch) for j in jobs] == [
+        (0, 0, 3, 0), (0, 3, 6, 3), (0, 6, 7, 6), (1, 0, 3, 7), (1, 3, 6, 10), (1, 6, 7, 13)]
+    assert [j.seq for j in jobs] == list(range(6))
+    assert first_global_batch(4, 3, [7, 7]) == 10   # not 4 * 3
+    assert first_global_batch(4, 3) == 12           # epoch-0-only form
