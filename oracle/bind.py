@@ -472,6 +472,18 @@ class _Ref:
             r["state_off"] = st_off
         return r
 
+    def precompute_changesets(self, d, sb, S, N, K):
+        """precompute_changesets (changeset.hpp:468-484) over ids_{sb}_{i}.bin
+        already in d; writes init_{sb}.bin + update_{sb}_{i}.bin there.
+        -> (misses per iteration, init size)"""
+        m = np.zeros(max(S, 1), np.uint64)
+        n = u64()
+        secs = C_.c_double()
+        self._chk(self.lib.gxr_precompute_changesets(os.fspath(d).encode(), sb, S, N, K, m.ctypes.data,
+                                                     C_.addressof(n),
+                                                     C_.byref(secs)))
+        return m[:S].copy(), n.value
+
     def dp_optimal_misses(self, trace, K):
         flat, off = _trace(trace)
         o = u64()
@@ -628,8 +640,44 @@ class _RefCache:
         return out
 
 
+gen_lib_path = os.path.join(HERE, "_build", "libgx_gen.so")
+
+
+class _Gen:
+    """oracle/gen_dataset.cpp: threaded writer of generate_dataset's files
+    (graph.bin + features.bin, byte-identical to graphgen.hpp:82-108)."""
+
+    def __init__(self, path):
+        self.path = path
+        self._lib = None
+
+    @property
+    def lib(self):
+        if self._lib is None:
+            if not os.path.exists(self.path):
+                build(ref=False)
+            L = C_.CDLL(self.path)
+            L.gxg_graph_file.argtypes = [C_.c_char_p, u64, C_.c_double, C_.c_double, C_.c_double,
+                                         C_.c_double, u64, C_.c_int, C_.POINTER(u64)]
+            L.gxg_features_file.argtypes = [C_.c_char_p, u64, u32, u64, C_.c_int]
+            self._lib = L
+        return self._lib
+
+    def graph_file(self, path, n, avg_deg, edge_seed, threads=None, a=0.57, b=0.19, c=0.19):
+        """-> number of edges after dedup"""
+        e = u64()
+        _raise(self.lib.gxg_graph_file(os.fspath(path).encode(), n, avg_deg, a, b, c, edge_seed,
+                                       threads or os.cpu_count() or 1, C_.byref(e)))
+        return e.value
+
+    def features_file(self, path, n, dim, value_seed, threads=None):
+        _raise(self.lib.gxg_features_file(os.fspath(path).encode(), n, dim, value_seed,
+                                          threads or os.cpu_count() or 1))
+
+
 C = _Oracle(oracle_lib_path)
 REF = _Ref(ref_lib_path)
+GEN = _Gen(gen_lib_path)
 
 
 def ref_available():

@@ -277,6 +277,14 @@ class Samples:
         os.makedirs(out_dir, exist_ok=True)
         check(lib.gx_samples_write_files(self.h, os.fspath(out_dir).encode(), sb_index))
 
+    def precompute(self, num_nodes: int, num_entries: int) -> "Changesets":
+        """precompute_changesets over this superbatch's device-resident trace
+        (changeset.hpp:468-484 minus the file reads): the inspector path the
+        fused pipeline runs (trusted sampler trace, gx_precompute_samples)."""
+        h = C.c_void_p()
+        check(lib.gx_precompute_samples(self.h, num_nodes, num_entries, C.byref(h)))
+        return Changesets(h)
+
 
 class NeighborCache:
     """Static neighbor cache (neighbor_cache.hpp). The CSC is HBM-resident, so

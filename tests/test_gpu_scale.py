@@ -82,3 +82,52 @@ def test_papers_superbatch_properties(gx, papers, kfrac):
     dig = p.digests()
     for i in rng.choice(S, 3, replace=False):
         assert int(dig[i]) == gx.batch_digest(_feature_rows(trace[i], DIM, vseed))
+
+
+def test_papers_sampler_matches_oracle(gx, oracle, papers):
+    """Bit-exact sampled batches of the bench superbatch vs the oracle's
+    sample_batch (sampler.hpp:69-117) on the host copy of the papers-shape
+    CSC: ids, per-layer (src, dst) edges and the IoStats charge."""
+    g, f, sb, vseed = papers
+    ip, ind = g.to_csc()                                   # u64, 13.8 GB of host memory
+    samples = gx.sample_superbatch(g, None, sb, FAN, 1, 0)
+    for i in (0, 1, 2, 3, 50, 97, 98, 99):
+        ids, layers, io = oracle.sample_batch(ip, ind, sb[i], FAN, oracle.derive_seed(1, i))
+        b = samples.batch(i)
+        assert np.array_equal(b.ids, ids), i
+        for l in range(len(FAN)):
+            assert np.array_equal(b.layers[l], layers[l]), (i, l)
+        st = gx.IoStats()
+        gx.sample_batch(g, None, sb[i], FAN, gx.derive_seed(1, i), st)
+        assert (st.pages_read, st.neighbor_lists_read, st.bytes_read) == (int(io[0]), int(io[2]), int(io[3])), i
+
+
+def test_papers_changesets_match_oracle(gx, oracle, papers):
+    """Belady changesets of a papers-shape superbatch under cache pressure
+    (K = 2 % of N = 2.2M slots) vs the oracle's simulate_changesets
+    (changeset.hpp:228-295): init, misses, in/out/pos per iteration. At this
+    size the device recurrence takes its large-cache slot scan (>= 8 slots
+    per thread, inspector.cu `nres >= 8u * G`) and its two-level-bitmap out
+    ordering (4096 < |out| < N/1024), which smaller tests cannot reach.
+    The pipeline's observed misses agree as well."""
+    g, f, sb, vseed = papers
+    K = int(0.02 * N)
+    samples = gx.sample_superbatch(g, None, sb, FAN, 1, 0)
+    cs = samples.precompute(N, K)
+    trace = [samples.batch(i).ids for i in range(S)]
+    init = oracle.compute_init_set(trace, K, N)
+    assert len(init) == K
+    assert np.array_equal(cs.init_set(), init)
+    sim = oracle.simulate(trace, N, K, init)
+    assert np.array_equal(cs.misses(), sim["misses"])
+    n_out = np.diff(sim["out_off"].astype(np.int64))
+    assert ((n_out > 4096) & (n_out < N // 1024)).any(), n_out.max()   # the sparse-out branch ran
+    for i in range(S):
+        c = cs.changeset(i)
+        a, b = int(sim["in_off"][i]), int(sim["in_off"][i + 1])
+        o0, o1 = int(sim["out_off"][i]), int(sim["out_off"][i + 1])
+        assert np.array_equal(c.in_ids, sim["in_ids"][a:b]), i
+        assert np.array_equal(c.in_positions, sim["in_pos"][a:b]), i
+        assert np.array_equal(c.out_ids, sim["out_ids"][o0:o1]), i
+    st = gx.Pipeline(g, f, FAN, K).run_superbatch(sb, 1, 0)
+    assert np.array_equal(st.misses, sim["misses"]) and st.total_misses == st.predicted_misses

@@ -213,3 +213,21 @@ def test_feature_cache_oracle_vs_reference(oracle, ref):
                 oc.apply(ob, *args)
                 assert np.array_equal(rc.resident(60), oc.resident())
         f.close()
+
+
+@pytest.mark.parametrize("n,avg,dim,threads", [(1, 3.0, 4, 2), (2000, 8.0, 16, 3), (70_000, 10.0, 8, 8),
+                                               (5000, 0.0, 4, 4), (33_333, 14.67, 3, 5)])
+def test_threaded_generator_matches_reference(ref, tmp_path, n, avg, dim, threads):
+    """oracle/gen_dataset.cpp (the bench reference arm's input writer) is
+    byte-identical to the reference's generate_dataset (graphgen.hpp:82-108)
+    at any thread count."""
+    import oracle as o
+    es, vs = o.C.derive_seed(7, 0xED6E5), o.C.derive_seed(7, 0xFEA7)
+    rd = tmp_path / "ref"
+    rd.mkdir()
+    e_ref = ref.generate_dataset(str(rd), n, avg, dim, es, vs)
+    e = o.GEN.graph_file(tmp_path / "graph.bin", n, avg, es, threads)
+    o.GEN.features_file(tmp_path / "features.bin", n, dim, vs, threads)
+    assert e == e_ref
+    for name in ("graph.bin", "features.bin"):
+        assert (tmp_path / name).read_bytes() == (rd / name).read_bytes(), name
