@@ -229,6 +229,11 @@ def ref_prepare(gx, g, f, cfg, samples, workdir, log):
 
 
 def ref_run(batches, cfg, gpath, fpath, workdir, workers, global_seed=SEED_RUN, first_batch=0):
+    """One superbatch through the reference's own stages (oracle/_ref,
+    gxr_run_superbatch): superbatch_sample with `workers` threads writing the
+    ids/adj files -> precompute_changesets (init/update files) -> FeatureCache
+    ctor -> per iteration read files, gather, apply_changeset. The files are
+    opened before the clock starts; `seconds` is the sum of the four stages."""
     import oracle
     L = oracle.REF.lib
     import ctypes as C
@@ -242,15 +247,38 @@ def ref_run(batches, cfg, gpath, fpath, workdir, workers, global_seed=SEED_RUN, 
     times = np.zeros(4, np.float64)
     e, r, m = C.c_uint64(), C.c_uint64(), C.c_uint64()
     K = int(cfg["cache_frac"] * cfg["N"])
-    t0 = time.perf_counter()
     oracle.REF._chk(L.gxr_run_superbatch(gpath.encode(), fpath.encode(), rt.encode(), flat, off,
                                          len(batches), fan, len(fan), global_seed, first_batch, K,
                                          workers, times, C.byref(e), C.byref(r), C.byref(m)))
-    wall = time.perf_counter() - t0
     shutil.rmtree(rt, ignore_errors=True)
-    return dict(edges=e.value, rows=r.value, misses=m.value, seconds=wall,
+    return dict(edges=e.value, rows=r.value, misses=m.value, seconds=float(times.sum()),
                 stages={"sample_s": times[0], "precompute_s": times[1], "switch_s": times[2],
                         "main_loop_s": times[3]})
+
+
+def ref_inputs(cfg, workdir, log):
+    """graph.bin + features.bin of the bench workload, written on the host
+    cores by oracle/gen_dataset.cpp -- byte-identical to the reference's
+    generate_dataset (tests/test_oracle.py::test_threaded_generator_matches_reference)
+    -- into tmpfs, so the reference reads page-cache-warm files. No CUDA."""
+    import oracle
+    os.makedirs(workdir, exist_ok=True)
+    gpath = os.path.join(workdir, "graph.bin")
+    fpath = os.path.join(workdir, "features.bin")
+    es = oracle.C.derive_seed(SEED_GEN, 0xED6E5)
+    vs = oracle.C.derive_seed(SEED_GEN, 0xFEA7)
+    t0 = time.time()
+    E = oracle.GEN.graph_file(gpath, cfg["N"], cfg["avg_degree"], es, cpu_cores())
+    t1 = time.time()
+    oracle.GEN.features_file(fpath, cfg["N"], cfg["dim"], vs, cpu_cores())
+    t2 = time.time()
+    log(f"reference inputs in {workdir}: N={cfg['N']} E={E} (graph.bin {t1 - t0:.1f}s, "
+        f"features.bin {t2 - t1:.1f}s, {cpu_cores()} threads)")
+    train = oracle.REF.train_ids(gpath, fpath, SEED_RUN, cfg["train_fraction"])
+    plan = oracle.REF.plan_seed_batches(train, cfg["batch"], oracle.C.epoch_seed(SEED_RUN, 0))
+    S = cfg["S"]
+    sbs = [plan[o:o + S] for o in range(0, len(plan), S)]
+    return gpath, fpath, sbs, E
 
 
 def cpu_cores():
@@ -261,6 +289,12 @@ def cpu_cores():
 
 
 def run_reference_arm(args, cfg, log):
+    """--impl reference: the UNMODIFIED reference (oracle/_ref/libgx_ref.so, its
+    headers compiled in this container) on the host cores, on the same workload
+    and config as the GPU arm. Neither torch nor the CUDA library is loaded:
+    inputs come from the host-side writer, the seed plan from the reference's
+    own TrainingRunner / plan_seed_batches. One step = one full superbatch
+    (S batches, cache K) through the reference's stages."""
     rank, world, local = env_rank()
     if rank != 0:
         return
@@ -268,18 +302,11 @@ def run_reference_arm(args, cfg, log):
     if not oracle.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libgx_ref.so was not built"}))
         return
-    import paper_2208_09151_b200 as gx
-    ctx = gx.Context(local)
-    g, f = build_dataset(gx, cfg, ctx, log)
-    sbs = make_plan(gx, cfg)
-    nb = args.ref_batches
     workdir = f"/dev/shm/gx_bench_ref_{os.getpid()}"
     cores = cpu_cores()
+    nb = args.ref_batches or cfg["S"]
     try:
-        gpath, fpath = ref_prepare(gx, g, f, cfg,
-                                   [(sbs[k % len(sbs)][:nb], (k % len(sbs)) * cfg["S"])
-                                    for k in range(args.warmup + args.steps)], workdir, log)
-        del g, f
+        gpath, fpath, sbs, E = ref_inputs(cfg, workdir, log)
         res = []
         for k in range(args.warmup + args.steps):
             j = k % len(sbs)
@@ -292,16 +319,18 @@ def run_reference_arm(args, cfg, log):
     edges = sum(r["edges"] for r in res)
     secs = sum(r["seconds"] for r in res)
     v = edges / secs
-    sample = (f"first {nb} of the {cfg['S']} batches of superbatch k per step (full stages: "
-              f"superbatch_sample with {cores} workers + files, precompute_changesets, FeatureCache "
-              f"init with K={int(cfg['cache_frac'] * cfg['N'])}, gather+apply)")
+    K = int(cfg["cache_frac"] * cfg["N"])
+    sample = (f"{'every' if nb == cfg['S'] else f'first {nb} of the'} {cfg['S']} batches of superbatch k per "
+              f"step through the reference's stages (superbatch_sample with {cores} workers + files, "
+              f"precompute_changesets, FeatureCache init with K={K}, gather+apply); files opened "
+              "outside the timed stages")
     print(json.dumps({
         "metric": METRIC, "value": v, "unit": "sampled_edges/s", "impl": "reference",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * secs / max(len(res), 1), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32/u64 ids, f32 rows (byte copies)", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * nb,
-                   "superbatch": nb, "parallelism": "cpu"},
+        "vs_baseline": None, "dtype": "u32 ids / f32 rows (byte copies)",
+        "data": "synthetic (reference generator output, written by oracle/gen_dataset.cpp)",
+        "config": bench_config(args, cfg, 1, K, E),   # one superbatch per step on the host
         "cpu_baseline": {"value": v, "unit": "sampled_edges/s", "cores": cores, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": v, "unit": "sampled_edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -309,8 +338,33 @@ def run_reference_arm(args, cfg, log):
     }))
 
 
+def bench_config(args, cfg, world, K, E):
+    """The `config` object both arms print (same workload keys)."""
+    S = cfg["S"]
+    sb_per_step = world if args.split == "superbatch" else 1   # superbatches all ranks run per step
+    return {"workload": cfg["workload"], "global_batch": cfg["batch"] * S * sb_per_step,
+            "superbatch": S, "cache_entries": K, "num_edges": E,
+            "features": args.features, "backing": args.backing,
+            "l2": "inputs larger than L2 (57 GB table, 6.6 GB CSC)" if args.config == "papers"
+            else "inputs larger than L2"}
+
+
 METRIC = ("sampled edges/s through the full data-prep step (sample + Belady inspect + feature "
           "gather/cache update); gathered feature GB/s and HBM fraction in `stages`/`roofline`")
+
+
+def relaunch(n):
+    """`bench.py --gpus N` without a launcher: start N ranks on this node with
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1)."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    raise SystemExit(subprocess.call(cmd))
 
 
 def main():
@@ -323,8 +377,8 @@ def main():
     ap.add_argument("--avg-degree", type=float, default=None)
     ap.add_argument("--superbatch", type=int, default=None)
     ap.add_argument("--cache-frac", type=float, default=None, help="cache entries as a fraction of the nodes")
-    ap.add_argument("--ref-batches", type=int, default=16,
-                    help="batches per step for the reference / cpu_baseline sample")
+    ap.add_argument("--ref-batches", type=int, default=0,
+                    help="batches per step for the reference / cpu_baseline sample (default: the whole superbatch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--overlap", action="store_true",
                     help="two superbatches in flight: superbatch k's executor overlaps k+1's sampler/"
@@ -339,7 +393,16 @@ def main():
                     help="replicated: every rank holds the whole table (no data-path collective); "
                          "partitioned: rows split over the ranks, cache init + misses fetched from "
                          "their owners by NCCL all-to-all (SURVEY.md 8e)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "replicated", "partitioned"],
+                    help="CSC layout: replicated on every rank, or row-partitioned with the sampler "
+                         "loading remote lists from their owner's HBM over NVLink (CUDA IPC); auto = "
+                         "partitioned when N > 1")
+    ap.add_argument("--split", default="superbatch", choices=["superbatch", "batches"],
+                    help="superbatch: rank r runs superbatches r, r+N, ... (weak scaling); batches: every "
+                         "superbatch's batches are split into N contiguous rank blocks (strong scaling)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "gx":
+        return relaunch(args.gpus)
     cfg = dict(CONFIGS[args.config])
     if args.avg_degree is not None:
         cfg["avg_degree"] = args.avg_degree
@@ -356,11 +419,24 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args, cfg, log)
 
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
     import torch
+    # GX_BENCH_SHARE_GPU=1 (tests on a one-GPU box): ranks share the visible
+    # GPUs and talk over gloo, since NCCL refuses two ranks on one device
+    share = os.environ.get("GX_BENCH_SHARE_GPU") == "1"
+    local = local % torch.cuda.device_count() if share else local
+    red_dev = "cpu" if share else f"cuda:{local}"
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        log(f"world {world}: torch.distributed {dist.get_backend()}"
+            f"{' NCCL ' + '.'.join(map(str, torch.cuda.nccl.version())) if not share else ''}, "
+            f"rank 0 on cuda:{local}")
     import paper_2208_09151_b200 as gx
     ctx = gx.Context(local)
     comm = None
@@ -383,25 +459,40 @@ def main():
             print(json.dumps({"metric": METRIC, "value": None, "unavailable": msg}))
         return
     g, f = build_dataset(gx, cfg, ctx, log, args.backing, args.ssd_dir, comm)
+    from paper_2208_09151_b200.shard import assign_superbatches, batch_block, partition_graph
+    graph_layout = args.graph if args.graph != "auto" else ("partitioned" if world > 1 else "replicated")
+    if graph_layout == "partitioned":
+        try:
+            partition_graph(g, rank, world)
+            log(f"CSC row-partitioned over {world} ranks: this rank holds nodes "
+                f"{g.partition_bounds(world)[rank:rank + 2].tolist()}, peers mapped over CUDA IPC")
+        except Exception as e:   # e.g. no peer access between the GPUs: keep the whole CSC
+            if g.partition_info()[0]:
+                raise
+            graph_layout = f"replicated (partitioning failed: {e})"
+            log(f"CSC partitioning failed ({e}); every rank keeps the whole CSC")
     sbs = make_plan(gx, cfg)
     K_entries = int(cfg["cache_frac"] * cfg["N"])
     pipe = gx.Pipeline(g, f, cfg["fanouts"], K_entries, overlap=args.overlap)
     stream = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
 
-    from paper_2208_09151_b200.shard import assign_superbatches
-
-    def sb_index(k):  # rank r takes superbatches r, r+world, ... of the epoch plan
+    def sb_index(k):  # rank r takes superbatches r, r+world, ... of the epoch plan (split=superbatch)
+        if args.split == "batches":
+            return k % len(sbs)
         return assign_superbatches(len(sbs), rank, world, 1, start=k)[0]
 
-    def step(k):
-        j = sb_index(k)
-        return pipe.run_superbatch(sbs[j], SEED_RUN, j * cfg["S"])
+    def rank_batches(j):
+        """-> (this rank's batches of superbatch j, their first global batch index)"""
+        if args.split == "batches":
+            blk = batch_block(len(sbs[j]), rank, world)
+            return sbs[j][blk.start:blk.stop], j * cfg["S"] + blk.start
+        return sbs[j], j * cfg["S"]
 
     exec_stream = torch.cuda.ExternalStream(pipe.exec_stream, device=torch.device("cuda", local))
 
     def submit(k):
-        j = sb_index(k)
-        return pipe.submit(sbs[j], SEED_RUN, j * cfg["S"])
+        b, first = rank_batches(sb_index(k))
+        return pipe.submit(b, SEED_RUN, first)
 
     def run_steps(k0, n, on_stats, ev_start=None, ev_end=None):
         """Two superbatches in flight: superbatch k+1 is submitted before k is
@@ -445,10 +536,10 @@ def main():
     dev_s = ev0.elapsed_time(ev1) / 1e3
     edges = sum(s.sampled_edges for s in stats)
     if world > 1:
-        t = torch.tensor([dev_s, wall_s], device=f"cuda:{local}", dtype=torch.float64)
+        t = torch.tensor([dev_s, wall_s], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         dev_s, wall_s = t.tolist()
-        e = torch.tensor([edges], device=f"cuda:{local}", dtype=torch.float64)
+        e = torch.tensor([edges], device=red_dev, dtype=torch.float64)
         torch.distributed.all_reduce(e)
         edges_all = int(e.item())
     else:
@@ -570,20 +661,21 @@ def main():
     out = {
         "metric": METRIC, "value": edges_all / dev_s, "unit": "sampled_edges/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.split == "batches" else "weak",
+        "vs_baseline": None,
         "dtype": "u32 ids / f32 rows (byte copies)", "data": "synthetic (device R-MAT, bit-exact to the "
         "reference generator; feature_value table)",
-        "config": {"workload": cfg["workload"], "global_batch": cfg["batch"] * S * world,
-                   "superbatch": S, "cache_entries": K_entries, "num_edges": g.num_edges(),
-                   "pipeline": ("2 superbatches in flight, GPU stages concurrent" if args.overlap else
-                                "2 superbatches in flight, GPU stages back to back"),
-                   "backing": args.backing,
-                   "parallelism": (f"dp{world} (superbatches per rank, no collective)" if comm is None else
-                                   f"dp{world} superbatches x {world}-way row-partitioned features "
-                                   "(NCCL all-to-all for cache init + misses)"),
-                   "features": args.features,
-                   "l2": "inputs larger than L2 (57 GB table, 6.6 GB CSC)" if args.config == "papers"
-                   else "inputs larger than L2"},
+        "config": bench_config(args, cfg, world, K_entries, g.num_edges()),
+        "pipeline": ("2 superbatches in flight, GPU stages concurrent" if args.overlap else
+                     "2 superbatches in flight, GPU stages back to back"),
+        "parallelism": {
+            "ranks": world,
+            "split": ("superbatches r, r+N, ... per rank (weak scaling)" if args.split == "superbatch" else
+                      "each superbatch's batches split into N contiguous rank blocks (strong scaling)"),
+            "graph": graph_layout + (" (sampler loads remote lists over NVLink, CUDA IPC)"
+                                     if graph_layout == "partitioned" and world > 1 else ""),
+            "features": ("replicated (no data-path collective)" if comm is None else
+                         f"{world}-way row-partitioned (NCCL all-to-all for cache init + misses)")},
         "e2e": {"value": edges_all / wall_s, "unit": "sampled_edges/s",
                 "h2d_bytes_per_step": int(8 * sum(len(b) for b in sbs[0]) + 8 * (S + 1)),
                 "d2h_bytes_per_step": int(8 * S + 8 * 16)},
@@ -614,7 +706,7 @@ def main():
         try:
             import oracle
             if oracle.ref_available():
-                nb = args.ref_batches
+                nb = args.ref_batches or cfg["S"]
                 workdir = f"/dev/shm/gx_bench_cpu_{os.getpid()}"
                 try:
                     gpath, fpath = ref_prepare(gx, g, f, cfg, [(sbs[0][:nb], 0)], workdir, log)
@@ -625,7 +717,8 @@ def main():
                 out["cpu_baseline"] = {
                     "value": r["edges"] / r["seconds"], "unit": "sampled_edges/s", "cores": cores,
                     "kind": "reference",
-                    "sample": f"first {nb} batches of superbatch 0 through the reference's stages "
+                    "sample": f"{'all' if nb == cfg['S'] else f'the first {nb} of the'} {cfg['S']} batches of "
+                              "superbatch 0 through the reference's stages "
                               f"(superbatch_sample {cores} workers, precompute_changesets, FeatureCache "
                               f"K={K_entries}, gather+apply); {r['edges']} edges in {r['seconds']:.2f}s",
                     "stages": r["stages"]}

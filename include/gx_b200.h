@@ -97,6 +97,35 @@ gx_status gx_graph_copy_csc(const gx_graph* g, uint64_t* indptr, uint64_t* indic
 /* persist_graph (graph_store.hpp:83-98): writes graph.bin byte-identically */
 gx_status gx_graph_write(const gx_graph* g, const char* path);
 
+/* ---- row-partitioned CSC over the GPUs of one box -----------
+ * The reference reads every in-neighbour list of sample_batch's layer loop
+ * from one graph.bin (sampler.hpp:89-115 -> GraphFile::read_in_neighbors,
+ * graph_store.hpp:145-154). Here rank r of P keeps the lists of nodes
+ * [bounds[r], bounds[r+1]) -- bounds balanced by edge count, no list split --
+ * and the replicated indptr. The per-layer request/response exchange is fused
+ * into the sampler kernel: a draw's child id is loaded from the owner's HBM
+ * through a CUDA IPC peer mapping (NVLink/NVSwitch), so sampled output is
+ * bit-identical to the whole-CSC path (the draws depend only on degrees, which
+ * indptr gives every rank). Collective use: every rank partitions, exports its
+ * handle, and attaches all handles in rank order.
+ * After gx_graph_partition, copy_csc / write / neighbor-cache build / static
+ * degree policy fail with GX_LOGIC_ERROR; sampling fails until attached. */
+#define GX_IPC_HANDLE_BYTES 64
+#define GX_MAX_PARTS 16
+/* node bounds[nranks + 1] of the edge-balanced partition */
+gx_status gx_graph_partition_bounds(const gx_graph* g, int nranks, uint64_t* node_bounds);
+/* keep only rank `rank`'s lists (frees the others' share of indices) */
+gx_status gx_graph_partition(gx_graph* g, int nranks, int rank);
+/* this rank's edge range and the IPC handle of its indices allocation */
+gx_status gx_graph_ipc_handle(const gx_graph* g, void* handle, uint64_t* edge_lo, uint64_t* edge_hi);
+/* map every peer's partition: handles[q * GX_IPC_HANDLE_BYTES] and edge_lo_hi[2q..2q+1]
+ * from rank q (this rank's own entry is ignored); the edge ranges must match */
+gx_status gx_graph_attach_peers(gx_graph* g, const void* handles, const uint64_t* edge_lo_hi);
+/* in-process form (P ranks on one device in one process, tests): parts[q] is rank q's graph */
+gx_status gx_graph_attach_local(gx_graph* g, gx_graph* const* parts, int nranks);
+/* partition count (0 = whole CSC) and this graph's rank */
+gx_status gx_graph_partition_info(const gx_graph* g, int* nranks, int* rank, int* attached);
+
 /* ---- static neighbor cache (neighbor_cache.hpp) --------------------------
  * The CSC is HBM-resident, so the cache changes only the sampler's IoStats (a
  * cached list charges nothing, sampler.hpp:91-97), exactly as in the

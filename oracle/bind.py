@@ -420,6 +420,24 @@ class _Ref:
         self._chk(self.lib.gxr_write_features(path.encode(), rows.shape[0], rows.shape[1],
                                               rows.reshape(-1)))
 
+    def train_ids(self, graph_path, feature_path, seed, train_fraction):
+        """TrainingRunner::train_ids (pipeline.hpp:384-399) on the given files."""
+        n = u64()
+        self._chk(self.lib.gxr_train_ids(os.fspath(graph_path).encode(), os.fspath(feature_path).encode(),
+                                         seed, train_fraction, np.zeros(1, np.uint64), 0, C_.byref(n)))
+        out = np.zeros(max(n.value, 1), np.uint64)
+        self._chk(self.lib.gxr_train_ids(os.fspath(graph_path).encode(), os.fspath(feature_path).encode(),
+                                         seed, train_fraction, out, len(out), C_.byref(n)))
+        return out[:n.value].copy()
+
+    def plan_seed_batches(self, train, batch_size, epoch_seed):
+        """plan_seed_batches (sampler.hpp:46-62) -> list of batches"""
+        train = _a64(train)
+        out = np.zeros(max(len(train), 1), np.uint64)
+        self._chk(self.lib.gxr_plan_seed_batches(train if len(train) else out, len(train), batch_size,
+                                                 epoch_seed, out))
+        return [out[o:o + batch_size].copy() for o in range(0, len(train), batch_size)]
+
     def generate_dataset(self, d, n, avg_deg, dim, edge_seed, value_seed):
         e = u64()
         self._chk(self.lib.gxr_generate_dataset(d.encode(), n, avg_deg, dim, edge_seed, value_seed,

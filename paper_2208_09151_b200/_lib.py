@@ -82,6 +82,12 @@ SIGNATURES = {
     "gx_graph_in_degree": (i32, [vp, u64, P64]),
     "gx_graph_copy_csc": (i32, [vp, vp, vp]),
     "gx_graph_write": (i32, [vp, cstr]),
+    "gx_graph_partition_bounds": (i32, [vp, i32, vp]),
+    "gx_graph_partition": (i32, [vp, i32, i32]),
+    "gx_graph_ipc_handle": (i32, [vp, vp, P64, P64]),
+    "gx_graph_attach_peers": (i32, [vp, vp, vp]),
+    "gx_graph_attach_local": (i32, [vp, vp, i32]),
+    "gx_graph_partition_info": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
     "gx_sample_superbatch": (i32, [vp, vp, vp, u64, vp, u32, u64, u64, PVP, PIO]),
     "gx_sample_batch": (i32, [vp, vp, u64, vp, u32, u64, PVP, PIO]),
     "gx_samples_destroy": (None, [vp]),

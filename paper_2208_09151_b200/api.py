@@ -193,6 +193,46 @@ class GraphFile:
         """persist_graph (graph_store.hpp:83-98)"""
         check(lib.gx_graph_write(self.h, os.fspath(path).encode()))
 
+    # -- row-partitioned CSC over the GPUs of one box (SURVEY 8e; include/gx_b200.h)
+    def partition_bounds(self, nranks: int) -> np.ndarray:
+        """node bounds[nranks + 1] of the edge-balanced partition (no list is split)"""
+        out = np.zeros(nranks + 1, np.uint64)
+        check(lib.gx_graph_partition_bounds(self.h, nranks, out.ctypes.data))
+        return out
+
+    def partition(self, nranks: int, rank: int) -> "GraphFile":
+        """keep only rank's in-neighbour lists (indptr stays replicated)"""
+        check(lib.gx_graph_partition(self.h, nranks, rank))
+        return self
+
+    def ipc_handle(self) -> tuple:
+        """-> (CUDA IPC handle bytes of this rank's lists, edge_lo, edge_hi)"""
+        h = (C.c_uint8 * 64)()
+        lo, hi = C.c_uint64(), C.c_uint64()
+        check(lib.gx_graph_ipc_handle(self.h, h, C.byref(lo), C.byref(hi)))
+        return bytes(h), lo.value, hi.value
+
+    def attach_peers(self, handles: Sequence[tuple]) -> "GraphFile":
+        """map every rank's partition (handles[q] = rank q's ipc_handle())"""
+        buf = b"".join(h[0] for h in handles)
+        lohi = np.array([x for h in handles for x in h[1:]], np.uint64)
+        check(lib.gx_graph_attach_peers(self.h, buf, lohi.ctypes.data))
+        self._peers = handles
+        return self
+
+    def attach_local(self, parts: Sequence["GraphFile"]) -> "GraphFile":
+        """in-process form: parts[q] is rank q's graph (kept alive with this one)"""
+        arr = (C.c_void_p * len(parts))(*[p.h.value if isinstance(p.h, C.c_void_p) else p.h for p in parts])
+        check(lib.gx_graph_attach_local(self.h, arr, len(parts)))
+        self._parts = list(parts)
+        return self
+
+    def partition_info(self) -> tuple:
+        """-> (nranks (0 = whole CSC), rank, attached)"""
+        n, r, a = C.c_int(), C.c_int(), C.c_int()
+        check(lib.gx_graph_partition_info(self.h, C.byref(n), C.byref(r), C.byref(a)))
+        return n.value, r.value, bool(a.value)
+
 
 open_graph = GraphFile.open
 

@@ -64,6 +64,7 @@ extern "C" {
 gx_status gx_static_degree_set(gx_graph* g, uint64_t K, uint64_t* out) {
     return guard([&] {
         if (!g) fail(GX_INVALID_ARGUMENT, "null graph");
+        require_whole_csc(g, "static_degree policy");
         const uint64_t n = g->n;
         if (K > n) fail(GX_INVALID_ARGUMENT, "static set larger than node count");
         gx_ctx* ctx = g->ctx;
@@ -95,6 +96,7 @@ gx_status gx_simulate_static_degree(gx_graph* g, const uint64_t* ids_flat, const
                                     uint64_t K, uint64_t* misses) {
     return guard([&] {
         if (!g) fail(GX_INVALID_ARGUMENT, "null graph");
+        require_whole_csc(g, "static_degree policy");
         const uint64_t n = g->n;
         if (K > n) fail(GX_INVALID_ARGUMENT, "static set larger than node count");
         gx_ctx* ctx = g->ctx;

@@ -386,6 +386,7 @@ gx_status gx_graph_in_degree(const gx_graph* g, uint64_t v, uint64_t* deg) {
 
 gx_status gx_graph_copy_csc(const gx_graph* g, uint64_t* indptr, uint64_t* indices) {
     return guard([&] {
+        require_whole_csc(g, "copy_csc");
         GX_CUDA(cudaMemcpy(indptr, g->indptr.p, (g->n + 1) * 8, cudaMemcpyDeviceToHost));
         const uint64_t CH = 1ull << 24;
         DevBuf<uint64_t> tmp(std::min(g->e, CH) + 1);
@@ -401,6 +402,7 @@ gx_status gx_graph_copy_csc(const gx_graph* g, uint64_t* indptr, uint64_t* indic
 
 gx_status gx_graph_write(const gx_graph* g, const char* path) {
     return guard([&] {
+        require_whole_csc(g, "persist_graph");
         File f(path, O_WRONLY | O_CREAT | O_TRUNC);
         unsigned char hdr[36];
         std::memcpy(hdr, kGraphMagic, 8);
@@ -429,6 +431,144 @@ gx_status gx_graph_write(const gx_graph* g, const char* path) {
             GX_CUDA(cudaStreamSynchronize(g->ctx->stream));
             f.write_all(pin.p, c * 8);
         }
+    });
+}
+
+// ---- row-partitioned CSC --------------------------------------
+
+namespace gx {
+GraphParts::~GraphParts() {
+    for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
+}
+}  // namespace gx
+
+// bounds[q] = the first node whose list starts at or after E*q/P (lower bound
+// on indptr), so every rank owns about E/P edges and no list is split
+__global__ void k_part_bounds(const uint64_t* __restrict__ indptr, uint64_t N, uint64_t E, int P,
+                              uint64_t* __restrict__ bounds) {
+    const int q = threadIdx.x;
+    if (q > P) return;
+    if (q == 0 || q == P) {
+        bounds[q] = q == 0 ? 0 : N;
+        return;
+    }
+    const uint64_t want = (uint64_t)((unsigned __int128)E * (unsigned)q / (unsigned)P);
+    uint64_t lo = 0, hi = N;  // first v in [0, N] with indptr[v] >= want
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) / 2;
+        if (indptr[mid] < want) lo = mid + 1;
+        else hi = mid;
+    }
+    bounds[q] = lo;
+}
+
+static void part_bounds(const gx_graph* g, int P, uint64_t* nb, uint64_t* eb) {
+    if (P < 1 || P > kMaxParts) fail(GX_INVALID_ARGUMENT, "partition count must be in [1, " +
+                                                           std::to_string(kMaxParts) + "]");
+    DevBuf<uint64_t> d(P + 1);
+    k_part_bounds<<<1, 32, 0, g->ctx->stream>>>(g->indptr.p, g->n, g->e, P, d.p);
+    GX_CHECK_LAUNCH();
+    GX_CUDA(cudaMemcpyAsync(nb, d.p, (P + 1) * 8, cudaMemcpyDeviceToHost, g->ctx->stream));
+    GX_CUDA(cudaStreamSynchronize(g->ctx->stream));
+    for (int q = 0; q <= P; ++q)
+        GX_CUDA(cudaMemcpy(eb + q, g->indptr.p + nb[q], 8, cudaMemcpyDeviceToHost));
+}
+
+gx_status gx_graph_partition_bounds(const gx_graph* g, int P, uint64_t* node_bounds) {
+    return guard([&] {
+        std::vector<uint64_t> eb(P + 1);
+        if (g->part.P) {
+            if (P != g->part.P) fail(GX_INVALID_ARGUMENT, "graph is already partitioned differently");
+            std::copy(g->part.node_bounds, g->part.node_bounds + P + 1, node_bounds);
+            return;
+        }
+        part_bounds(g, P, node_bounds, eb.data());
+    });
+}
+
+gx_status gx_graph_partition(gx_graph* g, int P, int rank) {
+    return guard([&] {
+        if (g->part.P) fail(GX_LOGIC_ERROR, "graph is already partitioned");
+        if (rank < 0 || rank >= P) fail(GX_INVALID_ARGUMENT, "rank out of range");
+        GraphParts& pt = g->part;
+        part_bounds(g, P, pt.node_bounds, pt.ebound);
+        const uint64_t lo = pt.ebound[rank], hi = pt.ebound[rank + 1];
+        DevBuf<uint32_t> mine(std::max<uint64_t>(hi - lo, 1));
+        if (hi > lo)
+            GX_CUDA(cudaMemcpyAsync(mine.p, g->indices.p + lo, (hi - lo) * 4, cudaMemcpyDeviceToDevice,
+                                    g->ctx->stream));
+        GX_CUDA(cudaStreamSynchronize(g->ctx->stream));
+        g->indices = std::move(mine);   // the other ranks' share is freed
+        pt.P = P;
+        pt.rank = rank;
+        pt.ptr[rank] = g->indices.p;
+        pt.attached = P == 1;
+    });
+}
+
+gx_status gx_graph_ipc_handle(const gx_graph* g, void* handle, uint64_t* edge_lo, uint64_t* edge_hi) {
+    return guard([&] {
+        if (!g->part.P) fail(GX_LOGIC_ERROR, "graph is not partitioned");
+        static_assert(sizeof(cudaIpcMemHandle_t) == GX_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        GX_CUDA(cudaIpcGetMemHandle(&h, g->indices.p));
+        std::memcpy(handle, &h, sizeof(h));
+        *edge_lo = g->part.ebound[g->part.rank];
+        *edge_hi = g->part.ebound[g->part.rank + 1];
+    });
+}
+
+gx_status gx_graph_attach_peers(gx_graph* g, const void* handles, const uint64_t* lohi) {
+    return guard([&] {
+        GraphParts& pt = g->part;
+        if (!pt.P) fail(GX_LOGIC_ERROR, "graph is not partitioned");
+        if (pt.attached) fail(GX_LOGIC_ERROR, "peers are already attached");
+        for (int q = 0; q < pt.P; ++q)
+            if (lohi[2 * q] != pt.ebound[q] || lohi[2 * q + 1] != pt.ebound[q + 1])
+                fail(GX_INVALID_ARGUMENT, "peer " + std::to_string(q) + " holds a different edge range");
+        std::vector<void*> opened;
+        try {
+            for (int q = 0; q < pt.P; ++q) {
+                if (q == pt.rank) continue;
+                cudaIpcMemHandle_t h;
+                std::memcpy(&h, static_cast<const uint8_t*>(handles) + (size_t)q * GX_IPC_HANDLE_BYTES, sizeof(h));
+                void* p = nullptr;
+                GX_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+                opened.push_back(p);
+                pt.ptr[q] = static_cast<const uint32_t*>(p);
+            }
+        } catch (...) {
+            for (void* p : opened) cudaIpcCloseMemHandle(p);
+            throw;
+        }
+        pt.ipc_opened = std::move(opened);
+        pt.attached = true;
+    });
+}
+
+gx_status gx_graph_attach_local(gx_graph* g, gx_graph* const* parts, int P) {
+    return guard([&] {
+        GraphParts& pt = g->part;
+        if (!pt.P) fail(GX_LOGIC_ERROR, "graph is not partitioned");
+        if (pt.attached && P > 1) fail(GX_LOGIC_ERROR, "peers are already attached");
+        if (P != pt.P) fail(GX_INVALID_ARGUMENT, "partition count mismatch");
+        for (int q = 0; q < P; ++q) {
+            const GraphParts& o = parts[q]->part;
+            if (o.P != P || o.rank != q || parts[q]->n != g->n || parts[q]->e != g->e ||
+                o.ebound[q] != pt.ebound[q] || o.ebound[q + 1] != pt.ebound[q + 1])
+                fail(GX_INVALID_ARGUMENT, "part " + std::to_string(q) + " is not rank " + std::to_string(q) +
+                                              " of the same partition");
+            pt.ptr[q] = parts[q]->indices.p;
+        }
+        pt.attached = true;
+    });
+}
+
+gx_status gx_graph_partition_info(const gx_graph* g, int* nranks, int* rank, int* attached) {
+    return guard([&] {
+        *nranks = g->part.P;
+        *rank = g->part.rank;
+        *attached = g->part.attached ? 1 : 0;
     });
 }
 

@@ -104,13 +104,38 @@ struct gx_ctx {
 // stream the executor launchers use
 inline cudaStream_t lstream(const gx_ctx* c) { return c->launch_stream ? c->launch_stream : c->stream; }
 
+namespace gx {
+constexpr int kMaxParts = 16;  // ranks of one box that can share a row-partitioned CSC
+// Row-partitioned CSC: rank r holds the in-neighbour lists of
+// nodes [node_bounds[r], node_bounds[r+1]) = edges [ebound[r], ebound[r+1])
+// (bounds balanced by edge count, lists never split); indptr stays replicated.
+// ptr[q] addresses rank q's edges (ptr[q][e - ebound[q]]): this rank's own
+// buffer, or a peer's HBM mapped over NVLink through CUDA IPC.
+struct GraphParts {
+    int P = 0, rank = 0;
+    bool attached = false;
+    uint64_t node_bounds[kMaxParts + 1] = {};
+    uint64_t ebound[kMaxParts + 1] = {};
+    const uint32_t* ptr[kMaxParts] = {};
+    std::vector<void*> ipc_opened;  // peer mappings to close
+    ~GraphParts();
+};
+}  // namespace gx
+
 struct gx_graph {
     gx_ctx* ctx = nullptr;
     uint64_t n = 0, e = 0;
     gx::DevBuf<uint64_t> indptr;   // N+1
-    gx::DevBuf<uint32_t> indices;  // E (u32 device ids)
+    gx::DevBuf<uint32_t> indices;  // E (u32 device ids); partitioned: only this rank's edges
     const uint32_t* ncache_bits = nullptr;  // neighbor cache in use (bit v: list cached, charges no I/O)
+    gx::GraphParts part;           // P == 0: not partitioned
 };
+namespace gx {
+// operations that need every list on this device refuse a partitioned graph
+inline void require_whole_csc(const gx_graph* g, const char* what) {
+    if (g->part.P) fail(GX_LOGIC_ERROR, std::string(what) + " needs the whole CSC; the graph is row-partitioned");
+}
+}  // namespace gx
 
 // Sampler output for S batches (SampleOutput x S, sampler.hpp:36-40).
 // Per-batch regions have fixed capacities so every batch can be written in

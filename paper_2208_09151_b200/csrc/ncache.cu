@@ -172,6 +172,7 @@ extern "C" {
 gx_status gx_ncache_build(gx_graph* g, uint64_t budget_bytes, gx_iostats* io, gx_ncache** out) {
     return guard([&] {
         if (!g) fail(GX_INVALID_ARGUMENT, "null graph");
+        require_whole_csc(g, "build_neighbor_cache");
         const uint64_t n = g->n, E = g->e;
         if (budget_bytes < n * 8) fail(GX_INVALID_ARGUMENT, "neighbor cache budget is smaller than the address table");
         gx_ctx* ctx = g->ctx;

@@ -82,6 +82,11 @@ constexpr int kPickCache = 32;
 struct SampArgs {
     const uint64_t* __restrict__ indptr;
     const uint32_t* __restrict__ indices;
+    // row-partitioned CSC (nparts > 0): edge e of rank q's range lives at
+    // part[q][e - ebound[q]] -- this rank's HBM or a peer's over NVLink (IPC)
+    uint32_t nparts;
+    const uint32_t* part[kMaxParts];
+    uint64_t ebound[kMaxParts + 1];
     uint64_t N;
     uint32_t S, L;
     uint32_t fan[kMaxLayers];
@@ -126,6 +131,22 @@ struct SampArgs {
         if ((a).trace && blockIdx.x == 0 && threadIdx.x == 0)                  \
             (a).trace[1 + (l) * 8 + (ph)] = gtimer() - (a).trace[0];           \
     } while (0)
+
+// indices[e]: the whole CSC, or the owner's partition (peer loads over NVLink
+// fuse the per-layer request/response exchange of sampler.hpp:89-115 into the
+// draw loop; every index in the parameter bank is static, no local copies)
+__device__ __forceinline__ uint32_t ld_index(const SampArgs& a, uint64_t e) {
+    if (a.nparts == 0) return __ldg(a.indices + e);
+    const uint32_t* base = a.part[0];
+    uint64_t lo = 0;
+#pragma unroll
+    for (int q = 1; q < kMaxParts; ++q)
+        if (q < (int)a.nparts && e >= a.ebound[q]) {
+            base = a.part[q];
+            lo = a.ebound[q];
+        }
+    return __ldg(base + (e - lo));
+}
 
 struct SampSmem {
     uint32_t scan[34];
@@ -553,7 +574,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
                         const uint32_t p = q0 + j * blockDim.x;
-                        if (p < tile_d1) child[j] = __ldg(a.indices + sm.plo_s[st[j].y - tile_k0] + st[j].x);
+                        if (p < tile_d1) child[j] = ld_index(a, sm.plo_s[st[j].y - tile_k0] + st[j].x);
                     }
                     // first probes of all U draws back to back, then resolve
                     uint32_t slot[U];
@@ -909,7 +930,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_sample_cl(SampArgs a) {
                 __syncthreads();
                 for (uint32_t p = d0 + tid; p < d0 + tot; p += T) {
                     const uint2 st = bedge[p];
-                    const uint32_t child = __ldg(a.indices + a.plo[ibase + st.y] + st.x);
+                    const uint32_t child = ld_index(a, a.plo[ibase + st.y] + st.x);
                     bedge[p] = make_uint2(child, st.y);
                     bdslot[p] = table_insert(tab, H, child, kNewBit | p);
                 }
@@ -1067,6 +1088,12 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
     SampArgs a{};
     a.indptr = g->indptr.p;
     a.indices = g->indices.p;
+    if (g->part.P) {
+        if (!g->part.attached) fail(GX_LOGIC_ERROR, "partitioned graph: peers are not attached");
+        a.nparts = (uint32_t)g->part.P;
+        for (int q = 0; q < g->part.P; ++q) a.part[q] = g->part.ptr[q];
+        for (int q = 0; q <= g->part.P; ++q) a.ebound[q] = g->part.ebound[q];
+    }
     a.N = N;
     a.L = L;
     for (uint32_t l = 0; l < L; ++l) {

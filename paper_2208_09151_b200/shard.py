@@ -72,3 +72,32 @@ def reduce_stats(values: Sequence[float], ops: Sequence[str], device=None) -> Li
         dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
         out.append(float(t.item()))
     return out
+
+
+def batch_block(num_batches: int, rank: int, world: int) -> range:
+    """Contiguous block of a superbatch's batches that rank `rank` samples when
+    the superbatch's batches are split by rank (north_star / SURVEY §8e):
+    [S*r/P, S*(r+1)/P). Batch i of the block keeps its global index
+    first_global_batch + i, so its RNG stream is the single-GPU one
+    (sampler.hpp:216)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return range(num_batches * rank // world, num_batches * (rank + 1) // world)
+
+
+def partition_graph(graph, rank: int, world: int, group=None):
+    """Row-partition a GraphFile over the ranks of `group` (collective): every
+    rank keeps its edge-balanced share of the in-neighbour lists, exports the
+    CUDA IPC handle of that share, and maps every peer's share, so the sampler
+    reads remote lists straight from the owner's HBM over NVLink
+    (gx_graph_partition / gx_graph_attach_peers, include/gx_b200.h). Handles
+    travel through torch.distributed (all_gather_object)."""
+    import torch.distributed as dist
+    graph.partition(world, rank)
+    if world == 1:
+        return graph
+    mine = graph.ipc_handle()
+    handles = [None] * world
+    dist.all_gather_object(handles, mine, group=group)
+    graph.attach_peers(handles)
+    return graph
