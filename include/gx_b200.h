@@ -291,6 +291,16 @@ gx_status gx_comm_init_nccl(gx_ctx* ctx, const void* id, int nranks, int rank, g
 /* in-process transport: nranks contexts (one per host thread; they may share a
  * GPU), peer copies through the CUDA runtime; outs[r] belongs to ctxs[r] */
 gx_status gx_comm_init_local(gx_ctx* const* ctxs, int nranks, gx_comm** outs);
+/* host-staged transport: device bytes are staged through pinned host buffers and
+ * exchanged by the caller's callback (MPI / gloo / sockets) -- for ranks NCCL
+ * cannot connect (e.g. several processes sharing one GPU). The callback sends
+ * send[sum(scnt[<p]) ..] (scnt[p] bytes) to rank p and receives rcnt[p] bytes
+ * from rank p into recv (packed in rank order); returns 0 on success. It is
+ * called collectively, in the same order on every rank. */
+typedef int (*gx_host_alltoallv_fn)(void* user, const void* send, const uint64_t* scnt, void* recv,
+                                    const uint64_t* rcnt);
+gx_status gx_comm_init_host(gx_ctx* ctx, int nranks, int rank, gx_host_alltoallv_fn fn, void* user,
+                            gx_comm** out);
 void gx_comm_destroy(gx_comm* c);
 int gx_comm_rank(const gx_comm* c);
 int gx_comm_size(const gx_comm* c);

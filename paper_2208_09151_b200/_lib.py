@@ -127,6 +127,7 @@ SIGNATURES = {
     "gx_comm_unique_id": (i32, [vp]),
     "gx_comm_init_nccl": (i32, [vp, vp, i32, i32, PVP]),
     "gx_comm_init_local": (i32, [vp, i32, vp]),
+    "gx_comm_init_host": (i32, [vp, i32, i32, vp, vp, PVP]),
     "gx_comm_destroy": (None, [vp]),
     "gx_comm_rank": (i32, [vp]),
     "gx_comm_size": (i32, [vp]),

@@ -818,6 +818,10 @@ def partition_bounds(num_nodes: int, nranks: int, rank: int) -> tuple:
     return lo.value, hi.value
 
 
+_HOST_XCHG = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p,
+                         C.POINTER(C.c_uint64))
+
+
 class Comm:
     """Communicator of a row-partitioned feature table: NCCL (one process per
     GPU) or the in-process hub (one host thread per rank, for tests)."""
@@ -851,6 +855,37 @@ class Comm:
         outs = (C.c_void_p * n)()
         check(lib.gx_comm_init_local(arr, n, outs))
         return [Comm(C.c_void_p(outs[r]), ctxs[r]) for r in range(n)]
+
+    @staticmethod
+    def host(ctx: Context, nranks: int, rank: int, group=None) -> "Comm":
+        """Host-staged transport (gx_comm_init_host): the same grouping,
+        owner-gather and scatter kernels, with the bytes exchanged by
+        torch.distributed all_to_all_single over the process group (gloo) --
+        for ranks NCCL cannot connect, e.g. several processes on one GPU."""
+        import torch
+        import torch.distributed as dist
+
+        def xchg(user, send, scnt, recv, rcnt):
+            try:
+                sc = [int(scnt[p]) for p in range(nranks)]
+                rc = [int(rcnt[p]) for p in range(nranks)]
+                t_in = torch.empty(sum(sc), dtype=torch.uint8)
+                if sum(sc):
+                    C.memmove(t_in.data_ptr(), send, sum(sc))
+                t_out = torch.empty(sum(rc), dtype=torch.uint8)
+                dist.all_to_all_single(t_out, t_in, output_split_sizes=rc, input_split_sizes=sc, group=group)
+                if sum(rc):
+                    C.memmove(recv, t_out.data_ptr(), sum(rc))
+                return 0
+            except Exception:   # reported as GX_RUNTIME_ERROR by the library
+                return 1
+
+        cb = _HOST_XCHG(xchg)
+        h = C.c_void_p()
+        check(lib.gx_comm_init_host(ctx.h, nranks, rank, cb, None, C.byref(h)))
+        c = Comm(h, ctx)
+        c._cb = cb      # the callback must outlive the communicator
+        return c
 
     @property
     def rank(self) -> int:

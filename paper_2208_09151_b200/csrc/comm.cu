@@ -231,6 +231,48 @@ struct LocalTransport : Transport {
     }
 };
 
+// Host-staged transport: the exchange itself is the caller's (a callback over
+// host buffers -- MPI, gloo, sockets), for boxes or tests where NCCL cannot
+// connect the ranks (e.g. several ranks sharing one GPU). Device bytes are
+// staged through pinned buffers; the grouping, owner gathers and scatters are
+// the same kernels the NCCL path runs.
+struct HostTransport : Transport {
+    gx_host_alltoallv_fn fn = nullptr;
+    void* user = nullptr;
+    PinBuf<uint8_t> hs, hr;
+    void call(const void* send, const uint64_t* scnt, void* recv, const uint64_t* rcnt) {
+        const int rc = fn(user, send, scnt, recv, rcnt);
+        if (rc) fail(GX_RUNTIME_ERROR, "host exchange callback failed (" + std::to_string(rc) + ")");
+    }
+    void counts(const uint64_t* send, uint64_t* recv, cudaStream_t) override {
+        std::vector<uint64_t> c8(size, 8);
+        call(send, c8.data(), recv, c8.data());
+    }
+    void alltoallv(const uint8_t* send, const uint64_t* soff, const uint64_t* scnt, uint8_t* recv,
+                   const uint64_t* roff, const uint64_t* rcnt, cudaStream_t s) override {
+        uint64_t ts = 0, tr = 0;
+        for (int p = 0; p < size; ++p) {
+            ts += scnt[p];
+            tr += rcnt[p];
+        }
+        hs.reserve(std::max<uint64_t>(ts, 1));
+        hr.reserve(std::max<uint64_t>(tr, 1));
+        uint64_t o = 0;  // pack the send pieces densely in rank order
+        for (int p = 0; p < size; ++p) {
+            if (scnt[p]) GX_CUDA(cudaMemcpyAsync(hs.p + o, send + soff[p], scnt[p], cudaMemcpyDeviceToHost, s));
+            o += scnt[p];
+        }
+        GX_CUDA(cudaStreamSynchronize(s));
+        call(hs.p, scnt, hr.p, rcnt);
+        o = 0;
+        for (int p = 0; p < size; ++p) {
+            if (rcnt[p]) GX_CUDA(cudaMemcpyAsync(recv + roff[p], hr.p + o, rcnt[p], cudaMemcpyHostToDevice, s));
+            o += rcnt[p];
+        }
+        GX_CUDA(cudaStreamSynchronize(s));  // the pinned staging is reused by the next call
+    }
+};
+
 }  // namespace gx
 
 struct gx_comm {
@@ -515,6 +557,23 @@ gx_status gx_comm_init_local(gx_ctx* const* ctxs, int nranks, gx_comm** outs) {
             c->t = std::move(t);
             outs[r] = c;
         }
+    });
+}
+
+gx_status gx_comm_init_host(gx_ctx* ctx, int nranks, int rank, gx_host_alltoallv_fn fn, void* user,
+                            gx_comm** out) {
+    return guard([&] {
+        if (!ctx || !fn) fail(GX_INVALID_ARGUMENT, "null context or callback");
+        if (nranks < 1 || nranks > 64 || rank < 0 || rank >= nranks) fail(GX_INVALID_ARGUMENT, "bad rank / size");
+        auto t = std::make_unique<HostTransport>();
+        t->fn = fn;
+        t->user = user;
+        t->rank = rank;
+        t->size = nranks;
+        auto c = new gx_comm();
+        c->ctx = ctx;
+        c->t = std::move(t);
+        *out = c;
     });
 }
 

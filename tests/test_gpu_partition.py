@@ -171,3 +171,72 @@ def test_nccl_world1_matches_device_backing(gx, oracle):
     assert a.gather_io == b.gather_io
     xs = fp.exchange_stats()
     assert xs.calls == 2 and xs.rows_remote == 0 and xs.rows_requested == a.init_size + a.total_misses
+
+
+MP_WORKER = r"""
+import json, os, sys
+import numpy as np
+sys.path.insert(0, os.environ["GX_ROOT"])
+import torch.distributed as dist
+rank, P = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+dist.init_process_group("gloo")
+import oracle
+import paper_2208_09151_b200 as gx
+from paper_2208_09151_b200.shard import partition_graph
+o = oracle.C
+n, dim, K, S = 5000, 40, int(os.environ["GX_K"]), 6
+ip, ind = o.rmat_graph(n, 6.0, 31)
+rows = o.features(n, dim, 32)
+plan = o.plan_seed_batches(o.train_ids(n, 1, 0.3), 40, o.epoch_seed(1, 0))
+sbs = [plan[q:q + S] for q in range(0, len(plan), S)]
+ctx = gx.Context(0)
+comm = gx.Comm.host(ctx, P, rank)
+lo, hi = gx.partition_bounds(n, P, rank)
+g = partition_graph(gx.GraphFile.from_csc(ip, ind, ctx=ctx), rank, P)
+f = gx.FeatureFile.partitioned_from_array(rows[lo:hi], n, comm)
+p = gx.Pipeline(g, f, [5, 3], K, digest=True)
+ok = True
+for k in range(2):                      # superbatches rank, rank + P
+    j = rank + k * P
+    st = p.run_superbatch(sbs[j], 1, j * S)
+    trace = [o.sample_batch(ip, ind, b, [5, 3], o.derive_seed(1, j * S + i))[0] for i, b in enumerate(sbs[j])]
+    sim = o.simulate(trace, n, K, o.compute_init_set(trace, K, n))
+    ok &= bool(np.array_equal(st.misses, sim["misses"])) and st.storage_rows == st.init_size + st.total_misses
+    for i, ids in enumerate(trace):
+        ok &= bool(np.array_equal(p.batch(i), rows[ids.astype(np.int64)]))
+xs = f.exchange_stats()
+dist.barrier()
+print(json.dumps({"rank": rank, "ok": ok, "calls": xs.calls, "remote": xs.rows_remote,
+                  "requested": xs.rows_requested, "served": xs.rows_served}))
+dist.destroy_process_group()
+"""
+
+
+@pytest.mark.parametrize("K", [250, 4000])
+def test_partitioned_table_two_processes_host_transport(K):
+    """Two processes on the one GPU: row-partitioned table exchanged through
+    the host-staged transport (gx_comm_init_host, gloo all_to_all_single) and
+    the row-partitioned CSC mapped over CUDA IPC -- the product's grouping,
+    owner gathers and scatters with real process separation."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [subprocess.Popen([sys.executable, "-c", MP_WORKER], cwd=root, text=True,
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              env=dict(os.environ, GX_ROOT=root, RANK=str(r), WORLD_SIZE="2", GX_K=str(K),
+                                       MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), PYTHONPATH=root))
+             for r in range(2)]
+    outs = [p.communicate(timeout=300) for p in procs]
+    for p, (o, e) in zip(procs, outs):
+        assert p.returncode == 0, o + e
+    res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
+    assert all(r["ok"] for r in res), res
+    assert all(r["calls"] == 4 and 0 < r["remote"] <= r["requested"] for r in res), res
+    assert sum(r["requested"] for r in res) == sum(r["served"] for r in res)
