@@ -397,6 +397,9 @@ def main():
                     help="CSC layout: replicated on every rank, or row-partitioned with the sampler "
                          "loading remote lists from their owner's HBM over NVLink (CUDA IPC); auto = "
                          "partitioned when N > 1")
+    ap.add_argument("--pressure-frac", type=float, default=0.05,
+                    help="also time the same superbatches with a cache of this fraction of the nodes "
+                         "(the Belady recurrence + changeset executor regime; 0 = skip)")
     ap.add_argument("--split", default="superbatch", choices=["superbatch", "batches"],
                     help="superbatch: rank r runs superbatches r, r+N, ... (weak scaling); batches: every "
                          "superbatch's batches are split into N contiguous rank blocks (strong scaling)")
@@ -490,27 +493,25 @@ def main():
 
     exec_stream = torch.cuda.ExternalStream(pipe.exec_stream, device=torch.device("cuda", local))
 
-    def submit(k):
-        b, first = rank_batches(sb_index(k))
-        return pipe.submit(b, SEED_RUN, first)
-
-    def run_steps(k0, n, on_stats, ev_start=None, ev_end=None):
+    def run_steps(k0, n, on_stats, ev_start=None, ev_end=None, pp=None, xs=None):
         """Two superbatches in flight: superbatch k+1 is submitted before k is
         waited for, so the host prepares k+1 while the GPU runs k. The GPU
         stages run back to back (default) or, with --overlap, k+1's
         sampler/inspector concurrently with k's executor."""
+        pp = pp or pipe
         if ev_start is not None:
             ev_start.record(stream)
         prev = None
         for k in range(k0, k0 + n):
-            t = submit(k)
+            b, first = rank_batches(sb_index(k))
+            t = pp.submit(b, SEED_RUN, first)
             if prev is not None:
-                on_stats(pipe.wait(prev))
+                on_stats(pp.wait(prev))
             prev = t
         if ev_end is not None:
-            ev_end.record(exec_stream)
+            ev_end.record(xs or exec_stream)
         if prev is not None:
-            on_stats(pipe.wait(prev))
+            on_stats(pp.wait(prev))
 
     def log_warm(st):
         log(f"warmup: {st.sampled_edges} edges, sample {st.ms_sample:.2f} ms inspect "
@@ -546,6 +547,48 @@ def main():
         edges_all = edges
     for s in stats:
         assert s.total_misses == s.predicted_misses, "observed misses != inspector prediction"
+
+    # --- cache-pressure line: the same superbatches through a small cache, so
+    # the Belady recurrence and the changeset executor (not the all-fit path)
+    # run inside the driver's bench (same graph and table, same timing rules)
+    pressure = None
+    if args.pressure_frac > 0:
+        Kp = int(args.pressure_frac * cfg["N"])
+        del pipe
+        pp = gx.Pipeline(g, f, cfg["fanouts"], Kp, overlap=args.overlap)
+        xs_p = torch.cuda.ExternalStream(pp.exec_stream, device=torch.device("cuda", local))
+        run_steps(0, args.warmup, lambda st: None, pp=pp)
+        pst = []
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        run_steps(args.warmup, args.steps, pst.append, e0, e1, pp=pp, xs=xs_p)
+        barrier()
+        p_s = e0.elapsed_time(e1) / 1e3
+        if world > 1:
+            t = torch.tensor([p_s], device=red_dev, dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            p_s = float(t.item())
+        for s in pst:
+            assert s.total_misses == s.predicted_misses, "observed misses != inspector prediction"
+        n_p = len(pst)
+        acc = sum(s.gathered_rows for s in pst)
+        pressure = {
+            "cache_entries": Kp, "cache_frac": args.pressure_frac,
+            "ms_per_step": 1e3 * p_s / args.steps,
+            "sampled_edges_per_s_rank0": sum(s.sampled_edges for s in pst) / p_s,
+            "miss_ratio": sum(s.total_misses for s in pst) / max(acc, 1),
+            "changeset_in_per_iter": sum(s.total_in for s in pst) / (n_p * cfg["S"]),
+            "stages_ms": {"sample": sum(s.ms_sample for s in pst) / n_p,
+                          "inspect (incl. Belady recurrence)": sum(s.ms_inspect for s in pst) / n_p,
+                          "switch (cache init)": sum(s.ms_switch for s in pst) / n_p,
+                          "gather + apply": sum(s.ms_gather for s in pst) / n_p},
+            "inspect_us_per_iteration": 1e3 * sum(s.ms_inspect for s in pst) / (n_p * cfg["S"]),
+            "gather_GBps": (f.row_bytes() * sum(s.gather_kernel_rows for s in pst) /
+                            (sum(s.ms_gather_kernels for s in pst) / 1e3) / 1e9
+                            if sum(s.ms_gather_kernels for s in pst) else None),
+            "note": "same superbatches as the headline with the cache at cache_frac of the nodes: misses and "
+                    "changesets in every iteration (timed with CUDA events like the headline)"}
+        del pp
 
     # --- rooflines: the gather (the north star's bandwidth kernel) and every stage --
     w = f.row_bytes()
@@ -700,6 +743,7 @@ def main():
                                "batch row, the gather moves the other accesses" if fused else None)}),
         "rooflines": rooflines,
         "stages": stages,
+        "cache_pressure": pressure,
         "clocks": clk.summary(),
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline and comm is None:

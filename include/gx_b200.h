@@ -151,9 +151,14 @@ gx_status gx_graph_set_neighbor_cache(gx_graph* g, const gx_ncache* c);
 gx_status gx_static_degree_set(gx_graph* g, uint64_t num_entries, uint64_t* out);
 /* simulate_policy(..., static_degree) (baselines.hpp:81-96): per-iteration
  * misses of a fixed resident set over a trace of distinct-id lists. The belady
- * policy is gx_precompute_trace's misses; none = every access; LRU is not offered. */
+ * policy is gx_precompute_trace's misses; none = every access; LRU: gx_simulate_lru. */
 gx_status gx_simulate_static_degree(gx_graph* g, const uint64_t* ids_flat, const uint64_t* offsets,
                                     uint64_t n_iters, uint64_t num_entries, uint64_t* misses);
+/* LRU policy (baselines.hpp:104-128): per-iteration misses of an LRU cache of
+ * K entries over the trace, from per-access stack distances on the device
+ * (prev-access sort + a merge-sort inversion count; baselines.cu). */
+gx_status gx_simulate_lru(gx_ctx* ctx, const uint64_t* ids_flat, const uint64_t* offsets, uint64_t S,
+                          uint64_t num_nodes, uint64_t K, uint64_t* misses);
 
 /* ---- sampler (sampler.hpp) ---------------------------------------------- */
 typedef struct gx_samples gx_samples; /* S batches: ids + per-layer edges, on device */

@@ -123,6 +123,7 @@ SIGNATURES = {
     "gx_static_degree_set": (i32, [vp, u64, vp]),
     "gx_pipeline_set_overlap": (i32, [vp, i32]),
     "gx_simulate_static_degree": (i32, [vp, vp, vp, u64, u64, vp]),
+    "gx_simulate_lru": (i32, [vp, vp, vp, u64, u64, u64, vp]),
     "gx_features_generate_fp16": (i32, [vp, u64, u32, u64, PVP]),
     "gx_comm_unique_id": (i32, [vp]),
     "gx_comm_init_nccl": (i32, [vp, vp, i32, i32, PVP]),

@@ -733,7 +733,7 @@ def simulate_policy(trace, num_nodes: int, num_entries: int, policy: str,
                     graph: Optional[GraphFile] = None, ctx: Optional[Context] = None) -> PolicyResult:
     """simulate_policy (baselines.hpp:64-143). static_degree takes its
     out-degrees from `graph` (the reference takes them as a span); belady is
-    the inspector; LRU is not offered on the device."""
+    the inspector; lru the device stack-distance count (gx_simulate_lru)."""
     policy = parse_policy(policy)
     lists = _trace_lists(trace)
     total = int(sum(len(x) for x in lists))
@@ -750,8 +750,12 @@ def simulate_policy(trace, num_nodes: int, num_entries: int, policy: str,
     if policy == "belady":
         cs = precompute_trace(lists, num_nodes, num_entries, ctx=ctx)
         return PolicyResult(policy, num_entries, cs.misses().astype(np.uint64), total)
-    raise NotImplementedError("LRU is not offered on the device: its misses need the number of distinct "
-                              "nodes between consecutive accesses of a node (a sequential stack simulation)")
+    # lru: LRU stack distances on the device (gx_simulate_lru, baselines.cu)
+    flat, off = _flatten(lists)
+    m = np.zeros(max(len(lists), 1), np.uint64)
+    check(lib.gx_simulate_lru(_ctx(ctx).h, flat.ctypes.data, off.ctypes.data, len(lists), num_nodes, num_entries,
+                              m.ctypes.data))
+    return PolicyResult(policy, num_entries, m[:len(lists)].copy(), total)
 
 
 def compute_init_set(trace, num_entries: int, num_nodes: int,

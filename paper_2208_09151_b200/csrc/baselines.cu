@@ -7,10 +7,18 @@
 //                  out-degrees by a histogram over the CSC indices, the set by
 //                  a stable CUB radix sort of (~degree, id), misses by a
 //                  per-iteration count of non-resident ids;
-//  * belady        the inspector (precompute over the same trace).
-// LRU (baselines.hpp:98-128) is not offered: a miss depends on the number of
-// distinct nodes since the previous access of the same node (a 2D dominance
-// count per access), a study tool rather than part of the hot path.
+//  * belady        the inspector (precompute over the same trace);
+//  * lru           (baselines.hpp:104-128) as LRU stack distances: access t of
+//                  node v, previous access p, hits iff fewer than K distinct
+//                  nodes were accessed in (p, t). That count is
+//                  D(t) = t - p - 1 - C(t), C(t) = #{u < t : prev[u] > p}
+//                  (every access in (p, t) whose own previous access also lies
+//                  in (p, t) repeats a node already counted), and C is a
+//                  per-element inversion count over prev[] -- a bottom-up merge
+//                  sort whose merge step adds, for each element of a right run,
+//                  the left-run elements above it. prev[] comes from a stable
+//                  CUB radix sort of (node, time). Exact for any trace (also
+//                  repeats inside one list, which the reference counts as hits).
 #include <cub/cub.cuh>
 
 #include "gx_internal.cuh"
@@ -49,6 +57,71 @@ __global__ void k_count_misses(const uint32_t* __restrict__ trace, const uint64_
                 continue;
             }
             if (!((bits[v >> 5] >> (v & 31)) & 1u)) ++c;
+        }
+        c = warp_sum(c);
+        if ((threadIdx.x & 31) == 0 && c) atomicAdd(&misses[i], c);
+    }
+}
+
+// prev1[t] = 1 + previous access time of the same node, 0 = first access
+__global__ void k_lru_prev(const uint32_t* __restrict__ node_sorted, const uint32_t* __restrict__ time_sorted,
+                           uint64_t A, uint32_t* __restrict__ prev1) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < A; s += (uint64_t)gridDim.x * blockDim.x)
+        prev1[time_sorted[s]] = (s > 0 && node_sorted[s - 1] == node_sorted[s]) ? time_sorted[s - 1] + 1 : 0u;
+}
+
+__global__ void k_lru_pack(const uint32_t* __restrict__ prev1, uint64_t A, unsigned long long* __restrict__ out) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < A; t += (uint64_t)gridDim.x * blockDim.x)
+        out[t] = ((unsigned long long)prev1[t] << 32) | t;
+}
+
+// number of x in sorted run [p, p + n) with x < key
+__device__ __forceinline__ uint64_t count_below(const unsigned long long* __restrict__ p, uint64_t n,
+                                                unsigned long long key) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (p[mid] < key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// one merge level of width w over packed (prev1 << 32 | time) keys (all
+// distinct): every element lands at its merged position; a right-run element
+// adds the left-run elements with a larger prev1 to C[time]
+__global__ void k_lru_merge(const unsigned long long* __restrict__ in, unsigned long long* __restrict__ out,
+                            uint64_t A, uint64_t w, uint32_t* __restrict__ C) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < A; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t base = i / (2 * w) * (2 * w);
+        const uint64_t lmid = min(base + w, A), rend = min(base + 2 * w, A);
+        const unsigned long long x = in[i];
+        uint64_t pos;
+        if (i < lmid) {
+            pos = base + (i - base) + count_below(in + lmid, rend - lmid, x);
+        } else {
+            const uint64_t nl = lmid - base;
+            pos = base + (i - lmid) + count_below(in + base, nl, x);
+            const uint32_t v = (uint32_t)(x >> 32);
+            if (v) {  // a repeat: left elements with prev1 > v (keys >= (v + 1) << 32)
+                const uint64_t le = count_below(in + base, nl, (unsigned long long)(v + 1) << 32);
+                C[(uint32_t)x] += (uint32_t)(nl - le);
+            }
+        }
+        out[pos] = x;
+    }
+}
+
+__global__ void k_lru_misses(const uint32_t* __restrict__ prev1, const uint32_t* __restrict__ C,
+                             const uint64_t* __restrict__ off, uint32_t S, uint64_t K,
+                             unsigned long long* __restrict__ misses) {
+    for (uint32_t i = blockIdx.y; i < S; i += gridDim.y) {
+        unsigned long long c = 0;
+        for (uint64_t t = off[i] + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < off[i + 1];
+             t += (uint64_t)gridDim.x * blockDim.x) {
+            const uint32_t p1 = prev1[t];
+            const bool hit = p1 && (t - p1 - C[t]) < K;  // distinct nodes in (p, t) = t - p - 1 - C
+            c += hit ? 0 : 1;
         }
         c = warp_sum(c);
         if ((threadIdx.x & 31) == 0 && c) atomicAdd(&misses[i], c);
@@ -139,6 +212,58 @@ gx_status gx_simulate_static_degree(gx_graph* g, const uint64_t* ids_flat, const
         GX_CUDA(cudaMemcpyAsync(&he, err.p, 4, cudaMemcpyDeviceToHost, st));
         GX_CUDA(cudaStreamSynchronize(st));
         if (he) fail(GX_OUT_OF_RANGE, "trace id out of range");
+        for (uint64_t i = 0; i < S; ++i) misses[i] = hm[i];
+    });
+}
+
+gx_status gx_simulate_lru(gx_ctx* ctx, const uint64_t* ids_flat, const uint64_t* offsets, uint64_t S, uint64_t N,
+                          uint64_t K, uint64_t* misses) {
+    return guard([&] {
+        if (!ctx) fail(GX_INVALID_ARGUMENT, "null context");
+        const uint64_t A = S ? offsets[S] : 0;
+        if (A >= 0xFFFFFFFFull) fail(GX_INVALID_ARGUMENT, "trace longer than 2^32 - 1 accesses");
+        std::vector<uint32_t> h32(std::max<uint64_t>(A, 1));
+        for (uint64_t x = 0; x < A; ++x) {
+            if (ids_flat[x] >= N) fail(GX_OUT_OF_RANGE, "trace id out of range");
+            h32[x] = (uint32_t)ids_flat[x];
+        }
+        for (uint64_t i = 0; i < S; ++i) misses[i] = 0;
+        if (!A) return;
+        cudaStream_t st = ctx->stream;
+        const unsigned grid = ctx->num_sms * 8;
+        DevBuf<uint32_t> node(A), node2(A), tm(A), tm2(A), prev1(A), C(A);
+        DevBuf<unsigned long long> ka(A), kb(A);
+        DevBuf<uint64_t> doff(S + 1);
+        DevBuf<unsigned long long> dm(S);
+        GX_CUDA(cudaMemcpyAsync(node.p, h32.data(), A * 4, cudaMemcpyHostToDevice, st));
+        for (uint64_t x = 0; x < A; ++x) h32[x] = (uint32_t)x;
+        GX_CUDA(cudaMemcpyAsync(tm.p, h32.data(), A * 4, cudaMemcpyHostToDevice, st));
+        GX_CUDA(cudaMemcpyAsync(doff.p, offsets, (S + 1) * 8, cudaMemcpyHostToDevice, st));
+        int bits = 1;
+        while (bits < 32 && (1ull << bits) < N) ++bits;
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, node.p, node2.p, tm.p, tm2.p, (int64_t)A, 0, bits, st);
+        DevBuf<uint8_t> tmp(std::max<size_t>(tmp_bytes, 1));
+        GX_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, node.p, node2.p, tm.p, tm2.p, (int64_t)A, 0, bits,
+                                                st));
+        k_lru_prev<<<grid, 256, 0, st>>>(node2.p, tm2.p, A, prev1.p);
+        GX_CHECK_LAUNCH();
+        k_lru_pack<<<grid, 256, 0, st>>>(prev1.p, A, ka.p);
+        GX_CHECK_LAUNCH();
+        GX_CUDA(cudaMemsetAsync(C.p, 0, A * 4, st));
+        unsigned long long *in = ka.p, *out = kb.p;
+        for (uint64_t w = 1; w < A; w <<= 1) {
+            k_lru_merge<<<grid, 256, 0, st>>>(in, out, A, w, C.p);
+            GX_CHECK_LAUNCH();
+            std::swap(in, out);
+        }
+        GX_CUDA(cudaMemsetAsync(dm.p, 0, S * 8, st));
+        dim3 g2(16, (unsigned)std::min<uint64_t>(S, 65535));
+        k_lru_misses<<<g2, 256, 0, st>>>(prev1.p, C.p, doff.p, (uint32_t)S, K, dm.p);
+        GX_CHECK_LAUNCH();
+        std::vector<unsigned long long> hm(S);
+        GX_CUDA(cudaMemcpyAsync(hm.data(), dm.p, S * 8, cudaMemcpyDeviceToHost, st));
+        GX_CUDA(cudaStreamSynchronize(st));
         for (uint64_t i = 0; i < S; ++i) misses[i] = hm[i];
     });
 }

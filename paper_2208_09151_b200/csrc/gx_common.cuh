@@ -154,8 +154,22 @@ struct GridBarrier {
     unsigned int gen;
 };
 
+__device__ __forceinline__ unsigned cluster_ctas() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ void grid_sync(GridBarrier* b) {
     __syncthreads();
+    if (gridDim.x == 1) return;  // one-CTA launches (narrow inspector traces): the CTA barrier suffices
+    if (gridDim.x == cluster_ctas()) {
+        // the whole grid is one thread-block cluster (narrow inspector traces):
+        // the hardware cluster barrier, release/acquire at cluster scope, which
+        // orders the CTAs' global-memory writes before the other CTAs' reads
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
     if (threadIdx.x == 0) {
         volatile unsigned int* vgen = &b->gen;
         unsigned int g = *vgen;

@@ -1399,11 +1399,38 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         bps0_ci = bps0[ci];
     }
     const int g0 = std::min(grid0, ctx->num_sms * bps0_ci);
+    // recurrence as ONE thread-block cluster (GX_INSPECT_CLUSTER = 8 or 16 CTAs):
+    // hardware cluster barriers instead of the grid-wide atomic barrier
+    static const int clu = env_int("GX_INSPECT_CLUSTER", 0);
+    const int rec_cluster = (clu == 8 || clu == 16) ? clu : 0;
+    if (rec_cluster == 16) {
+        static PerDevice<std::array<bool, 3>> npc_dev;
+        auto lk = npc_dev.lock();
+        std::array<bool, 3>& done = npc_dev.at(ctx->device);
+        if (!done[ci]) {
+            GX_CUDA(cudaFuncSetAttribute(rfns[ci], cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            done[ci] = true;
+        }
+    }
     void* args[] = {&a};
     for (int part = 0; part < 2; ++part) {
         void* fn = part ? rfns[ci] : kfns[ci];
         const int g = part ? grid : g0;
-        if (coop_launch())
+        if (part && rec_cluster) {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(rec_cluster);
+            lc.blockDim = dim3(IN_THREADS);
+            lc.dynamicSmemBytes = smems[ci];
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = rec_cluster;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            GX_CUDA(cudaLaunchKernelExC(&lc, fn, args));
+        } else if (coop_launch())
             GX_CUDA(cudaLaunchCooperativeKernel(fn, dim3(g), dim3(IN_THREADS), args, smems[ci], st));
         else
             GX_CUDA(cudaLaunchKernel(fn, dim3(g), dim3(IN_THREADS), args, smems[ci], st));

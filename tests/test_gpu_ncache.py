@@ -106,16 +106,38 @@ def test_policies_match_reference(gx, ref, dataset, K):
     rng = np.random.default_rng(K)
     trace = [rg.sample_batch(rng.choice(rg.num_nodes, 40, replace=False).astype(np.uint64), [4, 3], 50 + i)[0]
              for i in range(8)]
-    for pol in ["none", "static_degree", "belady"]:
+    for pol in ["none", "static_degree", "belady", "lru"]:
         want, tot = rg.simulate_policy(trace, K, pol)
         got = gx.simulate_policy(trace, rg.num_nodes, K, pol, graph=g)
         assert np.array_equal(got.misses, want), pol
         assert got.total_accesses == tot and got.policy == pol and got.capacity == K
-    with pytest.raises(NotImplementedError):
-        gx.simulate_policy(trace, rg.num_nodes, K, "lru")
     with pytest.raises(ValueError):
         gx.simulate_policy(trace, rg.num_nodes, K, "fifo")
     with pytest.raises(ValueError):
         gx.static_degree_set(g, rg.num_nodes + 1)
     s = gx.static_degree_set(g, 10)
     assert len(s) == 10 and len(set(s.tolist())) == 10
+
+
+@pytest.mark.parametrize("K", [0, 1, 7, 64, 300, 5000])
+def test_lru_matches_reference(gx, ref, dataset, K):
+    """LRU (baselines.hpp:104-128) by device stack distances vs the reference's
+    list+map simulation: sampled traces, random lists with repeats inside one
+    iteration (the reference counts the repeat as a hit), and skewed ids."""
+    gpath = os.path.join(dataset, "graph.bin")
+    rg = ref.open_graph(gpath)
+    n = rg.num_nodes
+    rng = np.random.default_rng(100 + K)
+    traces = [
+        [rg.sample_batch(rng.choice(n, 30, replace=False).astype(np.uint64), [5, 4], 7 + i)[0] for i in range(12)],
+        [rng.integers(0, 200, rng.integers(1, 80)).astype(np.uint64) for _ in range(40)],   # repeats
+        [(rng.zipf(1.3, 150) % n).astype(np.uint64) for _ in range(25)],
+        [np.zeros(0, np.uint64), np.array([5], np.uint64), np.zeros(0, np.uint64)],
+    ]
+    for t in traces:
+        want, tot = rg.simulate_policy(t, K, "lru")
+        got = gx.simulate_policy(t, n, K, "lru")
+        assert np.array_equal(got.misses, want), (K, [len(x) for x in t][:5])
+        assert got.total_accesses == tot
+    with pytest.raises(IndexError):
+        gx.simulate_policy([np.array([n], np.uint64)], n, K, "lru")
