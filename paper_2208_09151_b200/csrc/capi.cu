@@ -6,6 +6,7 @@
 #include <unistd.h>
 #include <unordered_set>
 
+#include "files.cuh"
 #include "gx_internal.cuh"
 
 namespace gx {
@@ -17,32 +18,6 @@ static const char kIdsMagic[8] = {'G', 'X', 'I', 'D', 'S', '0', '0', '1'};
 static const char kAdjMagic[8] = {'G', 'X', 'A', 'D', 'J', '0', '0', '1'};
 static const char kInitMagic[8] = {'G', 'X', 'I', 'N', 'I', 'T', '0', '1'};
 static const char kUpdMagic[8] = {'G', 'X', 'U', 'P', 'D', '0', '0', '1'};
-
-// Little-endian buffered writer with the reference's failure semantics
-// (BinWriter, common.hpp:130-199): throws runtime_error on open/short write.
-struct Writer {
-    FILE* f = nullptr;
-    std::string path;
-    explicit Writer(const std::string& p) : path(p) {
-        f = std::fopen(p.c_str(), "wb");
-        if (!f) fail(GX_RUNTIME_ERROR, "cannot open for write: " + p);
-    }
-    ~Writer() {
-        if (f) std::fclose(f);
-    }
-    void raw(const void* p, size_t n) {
-        if (n && std::fwrite(p, 1, n, f) != n) fail(GX_RUNTIME_ERROR, "short write: " + path);
-    }
-    void u32(uint32_t v) { raw(&v, 4); }
-    void u64(uint64_t v) { raw(&v, 8); }
-    void close() {
-        if (f && std::fclose(f) != 0) {
-            f = nullptr;
-            fail(GX_RUNTIME_ERROR, "close failed: " + path);
-        }
-        f = nullptr;
-    }
-};
 
 static std::string rt_path(const char* dir, const char* stem, uint64_t sb, int64_t i) {
     std::string p = std::string(dir) + "/" + stem + "_" + std::to_string(sb);
@@ -335,67 +310,53 @@ gx_status gx_changesets_misses(const gx_changesets* cs, uint64_t* misses) {
     });
 }
 
-// init_{sb}.bin + update_{sb}_{i}.bin (changeset.hpp:409-454)
+// init_{sb}.bin + update_{sb}_{i}.bin (changeset.hpp:409-454): the byte images
+// of all S + 1 files are packed on the device and written asynchronously
+// (files.cu: side-stream D2H into pinned chunks, host writer threads)
 gx_status gx_changesets_write_files(const gx_changesets* cs, const char* dir, uint64_t sb) {
     return guard([&] {
-        std::vector<uint64_t> init(cs->n_init);
-        d2h_u32_as_u64(cs->init.p, cs->n_init, init.data());
-        {
-            Writer w(rt_path(dir, "init", sb, -1));
-            w.raw(kInitMagic, 8);
-            w.u64(init.size());
-            w.raw(init.data(), init.size() * 8);
-            w.close();
-        }
-        const uint64_t TI = cs->h_in_off[cs->S], TO = cs->h_out_off[cs->S];
-        std::vector<uint64_t> in(TI), pos(TI), outv(TO);
-        d2h_u32_as_u64(cs->in_ids.p, TI, in.data());
-        d2h_u32_as_u64(cs->in_pos.p, TI, pos.data());
-        d2h_u32_as_u64(cs->out_ids.p, TO, outv.data());
+        FileImage im;
+        im.add_file(rt_path(dir, "init", sb, -1));
+        im.header(kInitMagic, 8);
+        im.value<uint64_t>(cs->n_init);
+        im.widen(cs->init.p, cs->n_init);
         for (uint64_t i = 0; i < cs->S; ++i) {
             const uint64_t a = cs->h_in_off[i], ni = cs->h_in_off[i + 1] - a;
             const uint64_t b = cs->h_out_off[i], no = cs->h_out_off[i + 1] - b;
-            Writer w(rt_path(dir, "update", sb, (int64_t)i));
-            w.raw(kUpdMagic, 8);
-            w.u64(ni);
-            w.raw(in.data() + a, ni * 8);
-            w.u64(no);
-            w.raw(outv.data() + b, no * 8);
-            w.u64(ni);
-            w.raw(pos.data() + a, ni * 8);
-            w.close();
+            im.add_file(rt_path(dir, "update", sb, (int64_t)i));
+            im.header(kUpdMagic, 8);
+            im.value<uint64_t>(ni);
+            im.widen(cs->in_ids.p + a, ni);
+            im.value<uint64_t>(no);
+            im.widen(cs->out_ids.p + b, no);
+            im.value<uint64_t>(ni);
+            im.widen(cs->in_pos.p + a, ni);
         }
+        write_file_image(cs->ctx, im);
     });
 }
 
-// ids_{sb}_{i}.bin + adj_{sb}_{i}.bin (sampler.hpp:123-182)
+// ids_{sb}_{i}.bin + adj_{sb}_{i}.bin (sampler.hpp:123-182), written like the
+// changeset files (files.cu)
 gx_status gx_samples_write_files(const gx_samples* s, const char* dir, uint64_t sb) {
     return guard([&] {
+        FileImage im;
         for (uint64_t b = 0; b < s->S; ++b) {
             const uint64_t n = s->h_n_ids[b];
-            std::vector<uint64_t> ids(n);
-            d2h_u32_as_u64(s->ids.p + b * s->cap_ids, n, ids.data());
-            {
-                Writer w(rt_path(dir, "ids", sb, (int64_t)b));
-                w.raw(kIdsMagic, 8);
-                w.u64(n);
-                w.raw(ids.data(), n * 8);
-                w.close();
-            }
-            Writer w(rt_path(dir, "adj", sb, (int64_t)b));
-            w.raw(kAdjMagic, 8);
-            w.u32(s->L);
+            im.add_file(rt_path(dir, "ids", sb, (int64_t)b));
+            im.header(kIdsMagic, 8);
+            im.value<uint64_t>(n);
+            im.widen(s->ids.p + b * s->cap_ids, n);
+            im.add_file(rt_path(dir, "adj", sb, (int64_t)b));
+            im.header(kAdjMagic, 8);
+            im.value<uint32_t>(s->L);
             for (uint32_t l = 0; l < s->L; ++l) {
                 const uint64_t c = s->h_layer_count[b * s->L + l];
-                std::vector<uint32_t> pairs(2 * c);
-                if (c)
-                    GX_CUDA(cudaMemcpy(pairs.data(), s->edges.p + b * s->cap_e_batch + s->e_off[l], c * 8,
-                                       cudaMemcpyDeviceToHost));
-                w.u64(c);
-                w.raw(pairs.data(), c * 8);
+                im.value<uint64_t>(c);
+                im.copy8(s->edges.p + b * s->cap_e_batch + s->e_off[l], c);
             }
-            w.close();
         }
+        write_file_image(s->ctx, im);
     });
 }
 
