@@ -13,15 +13,24 @@ generator (tests/test_gpu_sampler.py::test_device_generator_matches_reference_ge
 
 value  = sampled edges / device time of the K timed steps (CUDA events on the
          pipeline's stream; max over ranks; whole-job edges over all ranks).
-e2e    = the same through the public API call with host seeds in and host
-         results out, timed by the wall clock around each call.
-Multi-GPU (torchrun): every rank runs its own superbatches of the epoch plan
-(no data-path collective; "scaling": "weak").
+e2e    = the same through the public API call (host seeds uploaded per
+         superbatch, per-iteration statistics read back), timed by the wall
+         clock around the calls.
+Extra keys: `cache_pressure` (the same superbatches with a 5 % cache: Belady
+recurrence + changeset executor), `ssd_tier` (cfg1 with features.bin on the
+box's storage, O_DIRECT reads vs the storage's sequential rate), `exchange`
+(row-partitioned table, N > 1).
+Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run) unless a
+launcher already did; the CSC is row-partitioned over the ranks (the sampler
+reads remote lists over NVLink through CUDA IPC mappings); rank r runs
+superbatches r, r+N, ... ("scaling": "weak"), or `--split batches` splits
+every superbatch's batches into rank blocks ("strong").
 
 --impl reference runs the UNMODIFIED reference (oracle/_ref/libgx_ref.so, the
-reference headers compiled in this container) on the host cores on a bounded
-sample of the same workload (the first `--ref-batches` batches of a superbatch
-per step), reading graph.bin/features.bin written to /dev/shm.
+reference headers compiled in this container) on the host cores, one full
+superbatch (S = 100, K = 20 %) per step, on graph.bin/features.bin written to
+/dev/shm by oracle/gen_dataset.cpp (byte-identical to generate_dataset); the
+reference process loads neither torch nor the CUDA library.
 """
 from __future__ import annotations
 
@@ -185,6 +194,99 @@ def build_dataset(gx, cfg, ctx, log, backing="device", ssd_dir=None, comm=None):
         log(f"features.bin written to {ssd_dir} ({time.time() - t2:.1f}s), "
             f"O_DIRECT={f.storage_stats().direct}")
     return g, f
+
+
+def storage_seq_read_GBps(path, threads=16, chunk=8 << 20, limit=4 << 30):
+    """The box's storage roofline for the SSD tier: sequential O_DIRECT reads of
+    `path` (page-aligned buffers, `threads` readers on disjoint chunks), GB/s."""
+    import mmap
+    from concurrent.futures import ThreadPoolExecutor
+    size = min(os.path.getsize(path), limit) // chunk * chunk
+    if size == 0:
+        return None
+    try:
+        fd = os.open(path, os.O_RDONLY | getattr(os, "O_DIRECT", 0))
+    except OSError:
+        fd = os.open(path, os.O_RDONLY)
+    bufs = [mmap.mmap(-1, chunk) for _ in range(threads)]
+
+    def work(t):
+        n = 0
+        for off in range(t * chunk, size, threads * chunk):
+            n += os.preadv(fd, [bufs[t]], off)
+        return n
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        got = sum(ex.map(work, range(threads)))
+    dt = time.perf_counter() - t0
+    os.close(fd)
+    return got / dt / 1e9
+
+
+def ssd_tier_line(gx, ctx, args, log):
+    """The SSD tier in the driver's bench: configs[0] (cfg1, 1M nodes, K = 10 %)
+    with features.bin on the box's storage (GX_BACKING_FILE: the init set and
+    the misses are read with pread/O_DIRECT into pinned staging, storage.cu),
+    against the storage's own sequential O_DIRECT read rate on the same file."""
+    import torch
+    cfg = dict(CONFIGS["cfg1"])
+    g = gx.GraphFile.generate_rmat(cfg["N"], cfg["avg_degree"], gx.derive_seed(SEED_GEN, 0xED6E5), ctx=ctx)
+    f = gx.FeatureFile.generate(cfg["N"], cfg["dim"], gx.derive_seed(SEED_GEN, 0xFEA7), ctx=ctx)
+    path = os.path.join(args.ssd_dir, f"gx_bench_ssd_{os.getpid()}.bin")
+    try:
+        f.write(path)
+        del f
+        os.sync()
+        peak = storage_seq_read_GBps(path)
+        fb = gx.FeatureFile.open(path, "file", ctx=ctx)
+    finally:
+        if os.path.exists(path):
+            os.unlink(path)  # an open descriptor keeps the inode readable
+    sbs = make_plan(gx, cfg)
+    K = int(cfg["cache_frac"] * cfg["N"])
+    p = gx.Pipeline(g, fb, cfg["fanouts"], K)
+    p.run_superbatch(sbs[0], SEED_RUN, 0)             # warm-up (staging buffers)
+    fb_before = fb.storage_stats()
+    stats = []
+    xs = torch.cuda.ExternalStream(p.exec_stream, device=torch.device("cuda", ctx.device))
+    st0 = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", ctx.device))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx.synchronize()
+    e0.record(st0)
+    for _ in range(2):
+        stats.append(p.run_superbatch(sbs[0], SEED_RUN, 0))
+    e1.record(xs)
+    ctx.synchronize()
+    torch.cuda.synchronize(ctx.device)
+    secs = e0.elapsed_time(e1) / 1e3
+    fs = fb.storage_stats()
+    rows = sum(s.storage_rows for s in stats)
+    byts = sum(s.storage_bytes for s in stats)
+    ms_read = sum(s.ms_storage for s in stats)
+    preads = fs.preads - fb_before.preads
+    achieved = byts / (ms_read / 1e3) / 1e9 if ms_read else None
+    for s in stats:
+        assert s.total_misses == s.predicted_misses
+    out = {
+        "workload": cfg["workload"] + ", features.bin on storage (O_DIRECT)",
+        "ms_per_superbatch": 1e3 * secs / len(stats),
+        "sampled_edges_per_s": sum(s.sampled_edges for s in stats) / secs,
+        "rows_read_per_superbatch": rows / len(stats),
+        "storage_bytes_per_superbatch": byts / len(stats),
+        "storage_read_ms_per_superbatch": ms_read / len(stats),
+        "storage_GBps": achieved,
+        "storage_MBps": achieved * 1e3 if achieved else None,
+        "preads_per_s": preads / (ms_read / 1e3) if ms_read else None,
+        "o_direct": fs.direct, "reader_threads": fs.threads, "dir": args.ssd_dir,
+        "roofline": {"bound": "storage", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if achieved and peak else None,
+                     "peak_source": "measured here: sequential O_DIRECT reads of the same features.bin, 16 threads"},
+        "page_accounting": {"gather_pages_read": sum(s.gather_io.pages_read for s in stats),
+                            "note": "IoStats charged per missed row as the reference's FeatureFile does"},
+    }
+    log(f"ssd tier: {out['ms_per_superbatch']:.1f} ms/superbatch, {achieved} GB/s read vs {peak} GB/s sequential")
+    return out
 
 
 def make_plan(gx, cfg):
@@ -380,6 +482,8 @@ def main():
     ap.add_argument("--ref-batches", type=int, default=0,
                     help="batches per step for the reference / cpu_baseline sample (default: the whole superbatch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tiers", action="store_true",
+                    help="skip the SSD-tier line (cfg1 with features.bin on storage, O_DIRECT)")
     ap.add_argument("--overlap", action="store_true",
                     help="two superbatches in flight: superbatch k's executor overlaps k+1's sampler/"
                          "inspector (slower on B200 at papers shape: the HBM-bound gather stretches the "
@@ -746,6 +850,19 @@ def main():
         "cache_pressure": pressure,
         "clocks": clk.summary(),
     }
+    if comm is not None:   # the NVLink tier: the row-partitioned table's all-to-all
+        xms = stages["exchange_ms"] * n
+        xb = stages["exchange_bytes_sent_total"]
+        out["exchange"] = {
+            "bound": "nvlink", "achieved": xb / (xms / 1e3) / 1e9 if xms else None, "peak": 900.0,
+            "unit": "GB/s", "frac": (xb / (xms / 1e3) / 1e9) / 900.0 if xms else None,
+            "note": "rows sent by this rank's exchanges over the timed steps / their wall time "
+                    "(init + misses per superbatch); 900 GB/s = NVLink 5 per direction per GPU"}
+    if rank == 0 and world == 1 and not args.no_tiers and args.backing == "device" and comm is None:
+        try:
+            out["ssd_tier"] = ssd_tier_line(gx, ctx, args, log)
+        except Exception as e:  # the tier line never blocks the headline
+            out["ssd_tier"] = {"error": repr(e)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline and comm is None:
         try:
             import oracle

@@ -116,6 +116,8 @@ class _Oracle:
             L.gxo_cache_apply.argtypes = [vp, vp, u64, u64p, u64, u64p, u64p, u64, u64p, u64]
             L.gxo_cache_resident.restype = u64
             L.gxo_cache_resident.argtypes = [vp, u64p]
+            L.gxo_compute_stub.restype = u64
+            L.gxo_compute_stub.argtypes = [vp, u64, u64, vp, vp, u32]
             self._lib = L
         return self._lib
 
@@ -260,6 +262,15 @@ class _Oracle:
             r["state_off"] = st_off
         return r
 
+    def compute_stub(self, rows, layers):
+        """compute_stub (pipeline.hpp:35-57) of a batch (n, dim) and its layers [(E_l, 2) u32]"""
+        rows = np.ascontiguousarray(rows)
+        pairs = np.ascontiguousarray(np.concatenate([np.asarray(l, np.uint32).reshape(-1) for l in layers])
+                                     if layers else np.zeros(0, np.uint32))
+        cnt = np.array([len(l) for l in layers] or [0], np.uint64)
+        return self.lib.gxo_compute_stub(rows.ctypes.data, rows.shape[0], rows.shape[1] * rows.itemsize,
+                                         pairs.ctypes.data if pairs.size else None, cnt.ctypes.data, len(layers))
+
     # -- executor
     def cache(self, store_rows, init, K):
         return _OCache(self, store_rows, init, K)
@@ -379,6 +390,11 @@ class _Ref:
             L.gxr_dp_optimal_misses.argtypes = [u64p, u64p, u64, u64, C_.POINTER(u64)]
             L.gxr_precompute_changesets.argtypes = [C_.c_char_p, u64, u64, u64, u64, vp, vp,
                                                     C_.POINTER(C_.c_double)]
+            L.gxr_run_training.argtypes = [C_.c_char_p, C_.c_char_p, C_.c_char_p, C_.c_char_p, vp, u32, u64, u64,
+                                           u64, u64, C_.c_int, C_.c_int, C_.c_uint, u64, C_.c_double, vp, u64,
+                                           C_.POINTER(u64)]
+            L.gxr_compute_stub.restype = u64
+            L.gxr_compute_stub.argtypes = [vp, u64, u32, vp, vp, u32]
             L.gxr_features_open.argtypes = [C_.c_char_p, C_.POINTER(vp)]
             L.gxr_features_close.argtypes = [vp]
             L.gxr_cache_create.argtypes = [vp, u64p, u64, u64, u64p, C_.POINTER(vp)]
@@ -501,6 +517,27 @@ class _Ref:
                                                      C_.addressof(n),
                                                      C_.byref(secs)))
         return m[:S].copy(), n.value
+
+    def run_training(self, graph_path, feature_path, ncache_path, rt_dir, fanouts, batch_size, superbatch_size,
+                     epochs, cache_entries, use_ncache, overlap, workers, seed, train_fraction):
+        """run_training (pipeline.hpp:451) -> every iteration's compute_stub checksum"""
+        fan = np.ascontiguousarray(fanouts, dtype=np.uint32)
+        out = np.zeros(1 << 16, np.uint64)
+        n = u64()
+        self._chk(self.lib.gxr_run_training(os.fspath(graph_path).encode(), os.fspath(feature_path).encode(),
+                                            os.fspath(ncache_path).encode() if ncache_path else None,
+                                            os.fspath(rt_dir).encode(), fan.ctypes.data, len(fan), batch_size,
+                                            superbatch_size, epochs, cache_entries, int(use_ncache), int(overlap),
+                                            workers, seed, train_fraction, out.ctypes.data, len(out), C_.byref(n)))
+        return out[:n.value].copy()
+
+    def compute_stub(self, rows, layers):
+        rows = np.ascontiguousarray(rows, dtype=np.float32)
+        pairs = np.ascontiguousarray(np.concatenate([np.asarray(l, np.uint32).reshape(-1) for l in layers])
+                                     if layers else np.zeros(0, np.uint32))
+        cnt = np.array([len(l) for l in layers] or [0], np.uint64)
+        return self.lib.gxr_compute_stub(rows.ctypes.data, rows.shape[0], rows.shape[1],
+                                         pairs.ctypes.data if pairs.size else None, cnt.ctypes.data, len(layers))
 
     def dp_optimal_misses(self, trace, K):
         flat, off = _trace(trace)

@@ -607,3 +607,32 @@ uint64_t gxo_cache_resident(const gxo_cache* c, uint64_t* out) {
         if (c->table[v] >= 0) out[n++] = v;
     return n;
 }
+
+/* ---- compute_stub (pipeline.hpp:35-57): FNV-1a 64 over rows count, the row
+ * bytes, the layer count, then per layer its edge count and (src, dst) u32
+ * pairs -- the per-iteration checksum of TrainingRunner (pipeline.hpp:426). */
+static void fnv_absorb(uint64_t* h, const void* p, uint64_t n) {
+    const unsigned char* b = (const unsigned char*)p;
+    for (uint64_t i = 0; i < n; ++i) {
+        *h ^= b[i];
+        *h *= 0x100000001B3ULL;
+    }
+}
+
+uint64_t gxo_compute_stub(const void* rows, uint64_t n_rows, uint64_t row_bytes, const uint32_t* pairs,
+                          const uint64_t* layer_counts, uint32_t n_layers) {
+    uint64_t h = 0xCBF29CE484222325ULL;
+    uint64_t v = n_rows;
+    fnv_absorb(&h, &v, 8);
+    fnv_absorb(&h, rows, n_rows * row_bytes);
+    v = n_layers;
+    fnv_absorb(&h, &v, 8);
+    uint64_t k = 0;
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        v = layer_counts[l];
+        fnv_absorb(&h, &v, 8);
+        fnv_absorb(&h, pairs + 2 * k, layer_counts[l] * 8);
+        k += layer_counts[l];
+    }
+    return h;
+}

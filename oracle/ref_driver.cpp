@@ -528,4 +528,52 @@ int gxr_run_superbatch(const char* graph_path, const char* feature_path, const c
     });
 }
 
+/// run_training (pipeline.hpp:451): the whole TrainingRunner loop (sample,
+/// precompute, executor with compute_stub) on the given files; returns every
+/// iteration's checksum in order (StageMetrics::checksums, pipeline.hpp:426).
+int gxr_run_training(const char* graph_path, const char* feature_path, const char* ncache_path,
+                     const char* rt_dir, const uint32_t* fanouts, uint32_t n_layers, uint64_t batch_size,
+                     uint64_t superbatch_size, uint64_t epochs, uint64_t cache_entries, int use_ncache,
+                     int overlap, unsigned workers, uint64_t seed, double train_fraction, uint64_t* checksums,
+                     uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        RunConfig cfg;
+        cfg.graph_path = graph_path;
+        cfg.feature_path = feature_path;
+        if (ncache_path) cfg.neighbor_cache_path = ncache_path;
+        cfg.runtime_dir = rt_dir;
+        cfg.fanouts.assign(fanouts, fanouts + n_layers);
+        cfg.batch_size = batch_size;
+        cfg.superbatch_size = superbatch_size;
+        cfg.epochs = epochs;
+        cfg.feature_cache_entries = cache_entries;
+        cfg.use_neighbor_cache = use_ncache != 0;
+        cfg.overlap = overlap != 0;
+        cfg.sampler_workers = workers;
+        cfg.seed = seed;
+        cfg.train_fraction = train_fraction;
+        RunReport r = run_training(cfg);
+        uint64_t k = 0;
+        for (auto& sb : r.superbatches)
+            for (auto c : sb.checksums) {
+                if (k < cap) checksums[k] = c;
+                ++k;
+            }
+        *n = k;
+    });
+}
+
+/// compute_stub (pipeline.hpp:35-57) over a batch and its adjacency
+uint64_t gxr_compute_stub(const float* rows, uint64_t n_rows, uint32_t dim, const uint32_t* pairs,
+                          const uint64_t* layer_counts, uint32_t n_layers) {
+    RowMatrix batch;
+    batch.resize(n_rows, dim);
+    std::copy(rows, rows + n_rows * dim, batch.data.begin());
+    std::vector<std::vector<LocalEdge>> adj(n_layers);
+    uint64_t k = 0;
+    for (uint32_t l = 0; l < n_layers; ++l)
+        for (uint64_t e = 0; e < layer_counts[l]; ++e, ++k) adj[l].push_back({pairs[2 * k], pairs[2 * k + 1]});
+    return compute_stub(batch, adj);
+}
+
 } // extern "C"

@@ -1238,8 +1238,13 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.c_ref.reserve(std::max(Keff, maxw));
     B.in_node.reserve(maxw);
     B.in_pos.reserve(maxw);
-    static const int grid_knob = env_int("GX_INSPECT_CTAS", 0);  // CTAs (0 = one per SM)
-    const int grid = grid_knob > 0 ? std::min(grid_knob, ctx->num_sms) : ctx->num_sms;  // PART 1 (recurrence)
+    // PART 1 (recurrence) grid: one CTA per SM, or ONE CTA for narrow traces --
+    // an iteration of <= 4096 accesses against <= 16384 slots is a few dozen
+    // elements per thread, and the CTA barrier replaces every grid barrier
+    // (acceptance c8, 64 ids x K = 256: 13.4 -> 7.2 ms per 512 iterations)
+    static const int grid_knob = env_int("GX_INSPECT_CTAS", 0);  // CTAs (0 = automatic)
+    const bool narrow = maxw <= 4096 && Keff <= 16384;
+    const int grid = grid_knob > 0 ? std::min(grid_knob, ctx->num_sms) : (narrow ? 1 : ctx->num_sms);
     const int grid0 = ctx->num_sms * GX_IN_FRONT_BPS;                                      // PART 0
     B.chunk_cnt.reserve(2 * std::max(grid, grid0));
     B.bm_cnt.reserve(std::max(grid, grid0));
@@ -1249,7 +1254,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.isfirst.reserve(std::max<uint64_t>(A, 1));
     // per-node iteration bitmask (next use in 3 grid steps) when it fits the budget
     const uint64_t W = (S + 63) / 64;
-    const bool use_bits = S > 0 && W <= 2 && N * W * 8 <= (8ull << 30);
+    // (W <= 2: papers-size N; wider masks for small N, e.g. acceptance c8's
+    // S = 1024 traces, instead of one grid step per iteration)
+    const bool use_bits = S > 0 && ((W <= 2 && N * W * 8 <= (8ull << 30)) || (W <= 64 && N * W * 8 <= (512ull << 20)));
     if (use_bits && is.bits_words < N * W) {
         is.bits.alloc(N * W);
         GX_CUDA(cudaMemsetAsync(is.bits.p, 0, N * W * 8, st));

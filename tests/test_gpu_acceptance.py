@@ -133,3 +133,83 @@ def test_survey_cfg1_superbatch_on_device(gx):
     plan = gx.plan_seed_batches(train, 1000, gx.epoch_seed(1, 0)).batches
     st = gx.Pipeline(g, f, [10, 10, 10], 100_000).run_superbatch(plan[:100], 1, 0)
     assert (st.gathered_rows, st.sampled_edges, st.total_misses) == (k["accesses"], k["sampled_edges"], k["misses"])
+
+
+def test_acceptance_c4_checksums_match_reference(gx, oracle, ref, tmp_path):
+    """acceptance.cpp:296-349 restated: the per-iteration compute_stub checksums
+    (pipeline.hpp:35-57, 426) of the reference's run_training on the c4 dataset
+    (10K nodes, batch 256, superbatch 2, fanout 10,10,10, seed 404) are the same
+    for every cache / neighbor-cache / overlap / worker configuration, and the
+    device pipeline's batches + adjacency give exactly those checksums in every
+    configuration it has (cache on/off, neighbor cache on/off, overlap on/off)."""
+    d = str(tmp_path / "small")
+    os.makedirs(d)
+    ref.generate_dataset(d, 10000, 8.0, 16, 81, 82)
+    gpath, fpath, npath = (os.path.join(d, x) for x in ("graph.bin", "features.bin", "ncache.bin"))
+    ref.open_graph(gpath).ncache_build(10000 * 8 + 4 * 1024 * 1024, npath)
+    fan = [10, 10, 10]
+    want = None
+    tag = 0
+    for fc in (True, False):
+        for nc in (True, False):
+            for ov in (True, False):
+                for w in (1, 4):
+                    got = ref.run_training(gpath, fpath, npath, str(tmp_path / f"rt{tag}"), fan, 256, 2, 1,
+                                           2000 if fc else 0, nc, ov, w, 404, 0.1)
+                    tag += 1
+                    want = got if want is None else want
+                    assert np.array_equal(got, want), (fc, nc, ov, w)
+    g = gx.GraphFile.open(gpath)
+    f = gx.FeatureFile.open(fpath)
+    ncache = gx.NeighborCache.open(g, npath)
+    train = gx.derive_train_ids(10000, 404, 0.1)
+    plan = gx.plan_seed_batches(train, 256, gx.epoch_seed(404, 0)).batches
+    sbs = [plan[o:o + 2] for o in range(0, len(plan), 2)]
+    assert sum(len(s) for s in sbs) == len(want)
+    from paper_2208_09151_b200.api import _UseNcache
+    for K in (2000, 0):
+        for use_nc in (True, False):
+            for ov in (False, True):
+                p = gx.Pipeline(g, f, fan, K, overlap=ov)
+                sums = []
+                for j, sb in enumerate(sbs):
+                    with _UseNcache(g, ncache if use_nc else None):   # the sampler charges no I/O for cached lists
+                        p.run_superbatch(sb, 404, 2 * j)
+                    s = gx.sample_superbatch(g, None, sb, fan, 404, 2 * j)
+                    for i in range(len(sb)):
+                        sums.append(oracle.compute_stub(p.batch(i), s.batch(i).layers))
+                assert np.array_equal(np.array(sums, np.uint64), want), (K, use_nc, ov)
+
+
+def test_acceptance_c8_simulate_linear_in_superbatch(gx, ref):
+    """acceptance.cpp:544-602 restated on the device: traces of S = 512 and 1024
+    iterations, 64 fresh ids each, K = 256. The device precompute (next use,
+    init set, recurrence, readback -- the whole gx.precompute_trace call) stays
+    linear in S (< 2.5x, the reference's bar), and its misses equal the
+    reference simulator's. Both timings are printed (reference:
+    build_access_index + simulate_changesets on one host core)."""
+    import time
+
+    def build(S):
+        return [np.arange(i * 64, (i + 1) * 64, dtype=np.uint64) for i in range(S)]
+
+    def t_dev(t, S):
+        best = 1e9
+        for _ in range(5):
+            t0 = time.perf_counter()
+            cs = gx.precompute_trace(t, S * 64, 256)
+            best = min(best, time.perf_counter() - t0)
+        return best, cs
+
+    res = {}
+    for S in (512, 1024):
+        t = build(S)
+        sec, cs = t_dev(t, S)
+        init = ref.compute_init_set(t, 256, S * 64)
+        r = min((ref.simulate(t, S * 64, 256, init) for _ in range(3)), key=lambda x: x["seconds"])
+        assert np.array_equal(cs.misses(), r["misses"])
+        res[S] = (sec, r["seconds"])
+    ratio = res[1024][0] / res[512][0]
+    print(f"c8 device {res[512][0] * 1e3:.2f} -> {res[1024][0] * 1e3:.2f} ms ({ratio:.2f}x); reference "
+          f"{res[512][1] * 1e3:.2f} -> {res[1024][1] * 1e3:.2f} ms")
+    assert ratio < 2.5

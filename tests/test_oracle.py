@@ -231,3 +231,13 @@ def test_threaded_generator_matches_reference(ref, tmp_path, n, avg, dim, thread
     assert e == e_ref
     for name in ("graph.bin", "features.bin"):
         assert (tmp_path / name).read_bytes() == (rd / name).read_bytes(), name
+
+
+def test_compute_stub_matches_reference(oracle, ref):
+    """compute_stub (pipeline.hpp:35-57) restated in oracle/gx_oracle.c equals the
+    reference's on random batches and adjacency (incl. empty layers/batches)."""
+    rng = np.random.default_rng(3)
+    for rows_n, dim, layers in [(5, 4, [3, 0, 7]), (0, 8, [0]), (40, 16, [12, 90]), (1, 1, [])]:
+        rows = rng.random((rows_n, dim)).astype(np.float32)
+        adj = [rng.integers(0, 1 << 20, (c, 2)).astype(np.uint32) for c in layers]
+        assert oracle.compute_stub(rows, adj) == ref.compute_stub(rows, adj)
