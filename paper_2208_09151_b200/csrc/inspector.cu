@@ -714,12 +714,16 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         }
         if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[31] += 1;
 
-        // CUT: threshold bucket b* over keys in (i, S] (every CTA, redundantly)
+        // CUT: threshold bucket b* over keys in (i, S] (every CTA, redundantly),
+        // blockDim buckets per step: one block scan instead of a warp walking
+        // S - i buckets (acceptance c8: every key is NEVER, so the walk spans
+        // the whole tail every iteration -- quadratic in S)
         uint32_t bstar = 0, r = 0, inc_b = 0, new_b = 0;
-        if (tid < 32) {
+        {
+            if (tid == 0) sm.bc[0] = 0xFFFFFFFFu;
+            __syncthreads();
             uint32_t cum = 0;
-            bool done = false;
-            for (uint32_t b0 = i + 1; b0 <= S && !done; b0 += 32) {
+            for (uint32_t b0 = i + 1; b0 <= S; b0 += blockDim.x) {  // CTA-uniform
                 const uint32_t b = b0 + tid;
                 uint32_t ci = 0, cn = 0;
                 if (b <= S) {
@@ -727,19 +731,18 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     cn = ((volatile uint32_t*)a.hist_new)[b];
                 }
                 const uint32_t v = ci + cn;
-                const uint32_t incl = warp_incl_scan(v) + cum;
-                const unsigned hit = __ballot_sync(0xffffffffu, b <= S && incl >= K);
-                if (hit) {
-                    const int ln = __ffs(hit) - 1;
-                    if ((int)tid == ln) {
-                        sm.bc[0] = b;
-                        sm.bc[1] = K - (incl - v);
-                        sm.bc[2] = ci;
-                        sm.bc[3] = cn;
-                    }
-                    done = true;
+                uint32_t tot;
+                const uint32_t before = cum + block_excl_scan(v, sm.scan, tot);
+                // the one bucket that crosses K (K = 0: the first bucket, nothing kept)
+                if (b <= S && (K == 0 ? b == i + 1 : (before < K && before + v >= K))) {
+                    sm.bc[0] = b;
+                    sm.bc[1] = K - before;
+                    sm.bc[2] = ci;
+                    sm.bc[3] = cn;
                 }
-                cum = __shfl_sync(0xffffffffu, incl, 31);
+                __syncthreads();
+                if (sm.bc[0] != 0xFFFFFFFFu) break;
+                cum += tot;
             }
         }
         __syncthreads();
