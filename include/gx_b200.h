@@ -435,6 +435,10 @@ gx_status gx_pipeline_batch(gx_pipeline* p, uint64_t ticket, uint64_t i, const v
  * over the u32 words w_kj (W per row) of row k of iteration i's batch. */
 gx_status gx_pipeline_set_digest(gx_pipeline* p, int enable);
 gx_status gx_pipeline_digests(const gx_pipeline* p, uint64_t* digests_per_iter);
+/* test hook: the feature cache's K slot rows (K x row_bytes) after the last
+ * waited-for superbatch -- FeatureCache's rows after its last apply_changeset
+ * (feature_cache.hpp:114-129); slots never filled are unspecified */
+gx_status gx_pipeline_cache_rows(gx_pipeline* p, void* host_out);
 
 #ifdef __cplusplus
 }

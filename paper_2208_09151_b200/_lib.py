@@ -168,6 +168,7 @@ SIGNATURES = {
     "gx_pipeline_batch": (i32, [vp, u64, u64, C.POINTER(vp), P64, vp]),
     "gx_pipeline_set_digest": (i32, [vp, i32]),
     "gx_pipeline_digests": (i32, [vp, vp]),
+    "gx_pipeline_cache_rows": (i32, [vp, vp]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

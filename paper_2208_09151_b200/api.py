@@ -1207,6 +1207,7 @@ class Pipeline:
         check(lib.gx_pipeline_create(graph.h, features.h, _ptr(f), len(f), num_entries, C.byref(h)))
         self.h = h
         self.graph, self.features = graph, features
+        self._K = num_entries
         if digest:
             check(lib.gx_pipeline_set_digest(h, 1))
         if overlap:
@@ -1265,6 +1266,16 @@ class Pipeline:
     @property
     def exec_stream(self) -> int:
         return lib.gx_pipeline_exec_stream(self.h)
+
+    def cache_rows(self) -> np.ndarray:
+        """Test hook: the feature cache's K slot rows after the last waited-for
+        superbatch (gx_pipeline_cache_rows); never-filled slots are unspecified."""
+        f = self.features
+        K = self._K
+        out = np.empty((K, f.dim()), dtype=f.dtype)
+        if K:
+            check(lib.gx_pipeline_cache_rows(self.h, out.ctypes.data))
+        return out
 
     def digests(self) -> np.ndarray:
         out = np.zeros(max(self._S, 1), np.uint64)

@@ -53,6 +53,10 @@ struct PipeSlot {
     bool full = false;
     gx::DevBuf<uint32_t> d_off;  // o[] on the device (segment-mode miss charging)
     gx::PinBuf<uint32_t> h_off;
+    // one-launch executor: insert offsets per iteration, per-slot last-insert marks (K, kept zeroed)
+    gx::DevBuf<uint32_t> d_in_off, last_ins;
+    gx::PinBuf<uint32_t> h_in_off32;
+    uint64_t last_ins_n = 0;
     uint64_t nseg = 0;     // gather launches (segments of iterations)
     uint64_t ticket = ~0ull;
     uint64_t sampled_edges = 0;
@@ -418,6 +422,16 @@ gx_status gx_pipeline_digests(const gx_pipeline* p, uint64_t* d) {
     });
 }
 
+gx_status gx_pipeline_cache_rows(gx_pipeline* p, void* host_out) {
+    return guard([&] {
+        if (!p) fail(GX_INVALID_ARGUMENT, "null pipeline");
+        for (const auto& sl : p->slot)
+            if (sl.pending) fail(GX_LOGIC_ERROR, "cache rows are readable when no superbatch is in flight");
+        const uint64_t n = p->K * p->f->row_bytes;
+        if (n) GX_CUDA(cudaMemcpy(host_out, p->cache_rows.p, n, cudaMemcpyDeviceToHost));
+    });
+}
+
 void* gx_pipeline_exec_stream(gx_pipeline* p) { return p ? (void*)p->exec : nullptr; }
 
 gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const uint64_t* batch_off, uint64_t S,
@@ -507,9 +521,9 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         sl.d_off.reserve(S + 1);
         for (uint64_t i = 0; i <= S; ++i) sl.h_off.p[i] = (uint32_t)sl.o[i];
         GX_CUDA(cudaMemcpyAsync(sl.d_off.p, sl.h_off.p, (S + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, B));
-        sl.counters.reserve(8 * (S + 1));
+        sl.counters.reserve(8 * (S + 2));  // S iterations, the cache init, a scratch block
         sl.h_cnt.reserve(8 * (S + 1));
-        GX_CUDA(cudaMemsetAsync(sl.counters.p, 0, 8 * (S + 1) * 8, B));
+        GX_CUDA(cudaMemsetAsync(sl.counters.p, 0, 8 * (S + 2) * 8, B));
         if (p->digest) {
             sl.digests.reserve(S);
             sl.h_dig.reserve(S);
@@ -572,6 +586,49 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             };
             auto rows_of = [&](uint64_t i) { return sl.batch.p + (sl.full ? sl.o[i] * rb : 0); };
             uint64_t nseg = 0;
+            // device-backed table, whole superbatch resident, changesets: the
+            // gathers of all S iterations are ONE bulk-copy launch (k_gather_sb).
+            // The cache keeps its init rows during the launch (the changesets
+            // are applied after it, in iteration order, so the cache ends in the
+            // reference's state): a hit whose slot still holds its init node
+            // reads the cache, every other access the same bytes from the
+            // HBM-resident table (a slot is a copy of the table row,
+            // feature_cache.hpp:115-126), so iteration i's hits no longer wait
+            // for the applies of iterations < i. The per-iteration miss / page
+            // counters come from the inspector's resolved slots.
+            // GX_ONE_GATHER=0: per-segment gathers + applies.
+            static const bool one_gather = gx::env_int("GX_ONE_GATHER", 1) != 0;
+            const bool single = !fused && !file && sl.full && one_gather && p->f->rows_dev_view != nullptr;
+            if (single) {
+                GX_CUDA(cudaEventRecord(sl.kev[0], B));
+                if (!launch_gather_superbatch(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p,
+                                              (uint32_t)sl.cs.n_init, p->cache_rows.p, p->f->rows_dev_view, rb,
+                                              sl.batch.p))
+                    launch_gather_resolved(ctx, sl.trace.p, nullptr, sl.o[S], nullptr, p->f->rows_dev_view, rb,
+                                           sl.batch.p, sl.counters.p + 8 * (S + 1), nullptr, 0, false, false);
+                launch_count_iter_misses(ctx, sl.trace.p, sl.acc_slot.p, sl.d_off.p, (uint32_t)S, maxw, rb,
+                                         sl.counters.p);
+                GX_CUDA(cudaEventRecord(sl.kev[1], B));
+                if (p->digest)
+                    for (uint64_t k = 0; k < S; ++k)
+                        launch_digest(ctx, rows_of(k), sl.o[k + 1] - sl.o[k], rb, sl.digests.p + k);
+                // all changesets at once: each slot takes its last insert's row
+                const uint64_t n_in = sl.cs.h_in_off[S];
+                if (n_in) {
+                    sl.d_in_off.reserve(S + 1);
+                    sl.h_in_off32.reserve(S + 1);
+                    for (uint64_t i = 0; i <= S; ++i) sl.h_in_off32.p[i] = (uint32_t)sl.cs.h_in_off[i];
+                    GX_CUDA(cudaMemcpyAsync(sl.d_in_off.p, sl.h_in_off32.p, (S + 1) * 4, cudaMemcpyHostToDevice, B));
+                    if (sl.last_ins_n < p->K + 1) {
+                        sl.last_ins.alloc(p->K + 1);
+                        GX_CUDA(cudaMemsetAsync(sl.last_ins.p, 0, (p->K + 1) * 4, B));
+                        sl.last_ins_n = p->K + 1;
+                    }
+                    launch_apply_all(ctx, sl.cs.in_pos.p, sl.cs.in_slot.p, sl.d_in_off.p, (uint32_t)S, (uint32_t)n_in,
+                                     sl.d_off.p, sl.last_ins.p, sl.batch.p, p->cache_rows.p, rb);
+                }
+                GX_CUDA(cudaEventRecord(sl.kev[2], B));
+            }
             if (fused) {  // one launch: every access that is not a first use
                 GX_CUDA(cudaEventRecord(sl.kev[0], B));
                 if (sl.cs.fan) {
@@ -590,7 +647,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                         launch_digest(ctx, rows_of(k), sl.o[k + 1] - sl.o[k], rb, sl.digests.p + k);
                 GX_CUDA(cudaEventRecord(sl.kev[2], B));
             }
-            for (uint64_t i = fused ? S : 0; i < S;) {
+            for (uint64_t i = fused || single ? S : 0; i < S;) {
                 uint64_t e = i;  // segment [i, e]
                 if (sl.full)
                     while (e + 1 < S && empty_cs(e)) ++e;
@@ -619,7 +676,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 ++nseg;
                 i = e + 1;
             }
-            sl.nseg = fused ? 1 : nseg;
+            sl.nseg = fused || single ? 1 : nseg;
         } catch (...) {
             ctx->launch_stream = nullptr;
             throw;

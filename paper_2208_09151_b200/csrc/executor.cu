@@ -333,6 +333,59 @@ __global__ void __launch_bounds__(128) k_gather_tma2(const uint32_t* __restrict_
     }
 }
 
+// One launch over a whole resident superbatch with changesets (the pipeline's
+// device-backed executor): the cache holds exactly its init rows for the
+// duration of the launch (the changesets are applied after it), so an access
+// whose resolved slot still holds its init node (slot < n_init and
+// init[slot] == node) reads the cache slot -- a small, TLB-friendly region --
+// and every other access (misses, nodes inserted by a changeset) reads the
+// same bytes from the HBM-resident table. No counting here: the per-iteration
+// miss counters come from k_count_iter_misses over the same resolved slots.
+__global__ void __launch_bounds__(128) k_gather_sb(const uint32_t* __restrict__ ids,
+                                                   const uint32_t* __restrict__ slots, uint32_t n,
+                                                   const uint32_t* __restrict__ init, uint32_t n_init,
+                                                   const uint8_t* __restrict__ cache_rows,
+                                                   const uint8_t* __restrict__ store, uint32_t row_bytes,
+                                                   uint8_t* __restrict__ out) {
+    extern __shared__ __align__(128) unsigned char sbuf[];
+    __shared__ __align__(8) unsigned long long bars[2 * 128];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t bar0 = smem_u32(&bars[2 * tid]), bar1 = bar0 + 8;
+    const uint32_t buf0 = smem_u32(sbuf + (size_t)(2 * tid) * row_bytes), buf1 = buf0 + row_bytes;
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncthreads();
+    auto src = [&](uint32_t r) -> const uint8_t* {
+        const uint32_t v = __ldg(ids + r), sl = __ldg(slots + r);
+        if (sl < n_init && __ldg(init + sl) == v) return cache_rows + (uint64_t)sl * row_bytes;
+        return store + (uint64_t)v * row_bytes;
+    };
+    const uint32_t step = gridDim.x * blockDim.x;
+    uint32_t r = blockIdx.x * blockDim.x + tid;
+    uint32_t ph0 = 0, ph1 = 0;
+    if (r < n) bulk_load(buf0, src(r), row_bytes, bar0);
+    for (uint32_t j = 0; r < n; ++j) {
+        const uint32_t nx = r + step;
+        const bool odd = j & 1;
+        if (nx < n) {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            bulk_load(odd ? buf0 : buf1, src(nx), row_bytes, odd ? bar0 : bar1);
+        }
+        if (odd) {
+            bar_wait(bar1, ph1);
+            ph1 ^= 1;
+            bulk_store(out + (uint64_t)r * row_bytes, buf1, row_bytes);
+        } else {
+            bar_wait(bar0, ph0);
+            ph0 ^= 1;
+            bulk_store(out + (uint64_t)r * row_bytes, buf0, row_bytes);
+        }
+        r = nx;
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 // D-stage ring of bulk copies per thread: D-1 row loads stay in flight while
 // the previous row's bulk store drains; a buffer is refilled once its store has
 // read shared memory (wait_group.read 1 = all but the newest store).
@@ -938,6 +991,140 @@ void launch_apply_slots(gx_ctx* ctx, const uint32_t* in_ids, const uint32_t* in_
 __global__ void k_set_table(const uint32_t* __restrict__ init, uint32_t n, int32_t* table) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
         table[init[k]] = (int32_t)k;
+}
+
+// Per-iteration miss and page counts of a resolved access list (slot kNever =
+// miss; a miss charges page_count_for_row, feature_cache.hpp:66-71): grid
+// (chunks, iterations), one block reduction and two atomics per block.
+__global__ void k_count_iter_misses(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ slots,
+                                    const uint32_t* __restrict__ off, uint32_t S, uint64_t rb,
+                                    unsigned long long* __restrict__ counters) {
+    __shared__ unsigned long long red[2][32];
+    for (uint32_t i = blockIdx.y; i < S; i += gridDim.y) {
+        unsigned long long m = 0, pg = 0;
+        for (uint32_t x = off[i] + blockIdx.x * blockDim.x + threadIdx.x; x < off[i + 1]; x += gridDim.x * blockDim.x) {
+            if (__ldg(slots + x) == kNever) {
+                const uint64_t v = __ldg(ids + x);
+                ++m;
+                pg += pages_touched(v * rb, v * rb + rb);
+            }
+        }
+        m = warp_sum(m);
+        pg = warp_sum(pg);
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = m;
+            red[1][threadIdx.x >> 5] = pg;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long tm = 0, tp = 0;
+            for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) {
+                tm += red[0][w];
+                tp += red[1][w];
+            }
+            if (tm) {
+                atomicAdd(&counters[8 * i + 1], tm);
+                atomicAdd(&counters[8 * i + 2], tp);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+void launch_count_iter_misses(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, const uint32_t* d_off,
+                              uint32_t S, uint64_t maxw, uint64_t rb, unsigned long long* counters) {
+    if (!S) return;
+    const dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((maxw + 1023) / 1024, 16)),
+                    (unsigned)std::min<uint32_t>(S, 65535));
+    k_count_iter_misses<<<grid, 256, 0, lstream(ctx)>>>(ids, slots, d_off, S, rb, counters);
+    GX_CHECK_LAUNCH();
+}
+
+bool launch_gather_superbatch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
+                              const uint32_t* init, uint32_t n_init, const uint8_t* cache_rows, const uint8_t* store,
+                              uint64_t rb, uint8_t* out) {
+    const int budget = gather_smem_budget(rb);
+    if (!vec16(rb) || 2ull * 32 * rb > (uint64_t)budget) return false;  // the caller falls back
+    if (!n) return true;
+    static std::mutex mu;
+    static std::map<int, LaunchCfg> cfgs;  // per device
+    std::lock_guard<std::mutex> lk(mu);
+    LaunchCfg& cf = cfgs[ctx->device];
+    if (cf.rb != rb) {
+        cf.tpb = (int)std::min<uint64_t>(128, budget / (2 * rb)) & ~31;
+        const int smem = cf.tpb * 2 * (int)rb;
+        GX_CUDA(cudaFuncSetAttribute(k_gather_sb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cf.bps, k_gather_sb, cf.tpb, smem));
+        cf.bps = std::max(cf.bps, 1);
+        cf.rb = rb;
+    }
+    const uint64_t blocks = std::min<uint64_t>((n + cf.tpb - 1) / cf.tpb, (uint64_t)ctx->num_sms * cf.bps);
+    k_gather_sb<<<(unsigned)blocks, cf.tpb, (size_t)cf.tpb * 2 * rb, lstream(ctx)>>>(
+        ids, slots, (uint32_t)n, init, n_init, cache_rows, store, (uint32_t)rb, out);
+    GX_CHECK_LAUNCH();
+    return true;
+}
+
+// All changesets of a superbatch applied at once, in effect (the pipeline's
+// one-launch executor; nothing reads the cache in between): a slot ends with
+// the row of its LAST insert (feature_cache.hpp:114-129 applied in iteration
+// order), so pass 1 records each slot's last inserting iteration (+1), pass 2
+// copies only those rows (batch row o[i] + pos -> slot), pass 3 clears the
+// marks. Insert k's iteration comes from the insert offsets in_off[S + 1].
+__device__ __forceinline__ uint32_t iter_of_insert(const uint32_t* in_off, uint32_t S, uint32_t k) {
+    uint32_t lo = 0, hi = S;  // in_off[lo] <= k < in_off[lo + 1]
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(in_off + mid) <= k) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void k_apply_last(const uint32_t* __restrict__ in_slot, const uint32_t* __restrict__ in_off, uint32_t S,
+                             uint32_t n, uint32_t* __restrict__ last) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        atomicMax(&last[__ldg(in_slot + k)], iter_of_insert(in_off, S, k) + 1);
+}
+
+template <int VEC>
+__global__ void k_apply_copy(const uint32_t* __restrict__ in_pos, const uint32_t* __restrict__ in_slot,
+                             const uint32_t* __restrict__ in_off, uint32_t S, uint32_t n,
+                             const uint32_t* __restrict__ bat_off, const uint32_t* __restrict__ last,
+                             const uint8_t* __restrict__ batch, uint8_t* __restrict__ cache_rows, uint32_t rb) {
+    using V = typename VecT<VEC>::T;
+    const uint32_t lane = threadIdx.x & 31, nv = rb / VEC;
+    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n; k += (gridDim.x * blockDim.x) >> 5) {
+        const uint32_t i = iter_of_insert(in_off, S, k), sl = __ldg(in_slot + k);
+        if (__ldg(last + sl) != i + 1) continue;  // a later iteration overwrites this slot
+        const V* src = reinterpret_cast<const V*>(batch + (uint64_t)(__ldg(bat_off + i) + __ldg(in_pos + k)) * rb);
+        V* dst = reinterpret_cast<V*>(cache_rows + (uint64_t)sl * rb);
+        for (uint32_t c = lane; c < nv; c += 32) dst[c] = src[c];
+    }
+}
+
+__global__ void k_apply_clear(const uint32_t* __restrict__ in_slot, uint32_t n, uint32_t* __restrict__ last) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
+        last[__ldg(in_slot + k)] = 0;
+}
+
+void launch_apply_all(gx_ctx* ctx, const uint32_t* in_pos, const uint32_t* in_slot, const uint32_t* in_off,
+                      uint32_t S, uint32_t n, const uint32_t* bat_off, uint32_t* last, const uint8_t* batch,
+                      uint8_t* cache_rows, uint64_t rb) {
+    if (!n) return;
+    const unsigned g = std::min<unsigned>((n + 255) / 256, ctx->num_sms * 8);
+    k_apply_last<<<g, 256, 0, lstream(ctx)>>>(in_slot, in_off, S, n, last);
+    GX_CHECK_LAUNCH();
+    const unsigned gw = std::min<unsigned>((n + 7) / 8, ctx->num_sms * 16);  // a warp per insert
+    if (vec16(rb))
+        k_apply_copy<16><<<gw, 256, 0, lstream(ctx)>>>(in_pos, in_slot, in_off, S, n, bat_off, last, batch, cache_rows,
+                                                      (uint32_t)rb);
+    else
+        k_apply_copy<4><<<gw, 256, 0, lstream(ctx)>>>(in_pos, in_slot, in_off, S, n, bat_off, last, batch, cache_rows,
+                                                     (uint32_t)rb);
+    GX_CHECK_LAUNCH();
+    k_apply_clear<<<g, 256, 0, lstream(ctx)>>>(in_slot, n, last);
+    GX_CHECK_LAUNCH();
 }
 
 void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* table, gx_features* f,

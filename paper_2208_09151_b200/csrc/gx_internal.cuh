@@ -260,6 +260,22 @@ void launch_cache_init(gx_ctx* ctx, const uint32_t* init, uint32_t n, int32_t* t
 void launch_reset_table(gx_ctx* ctx, const uint32_t* nodes, uint64_t n, int32_t* table);
 void launch_digest(gx_ctx* ctx, const uint8_t* batch, uint64_t rows, uint64_t row_bytes,
                    unsigned long long* out);
+// whole resident superbatch in one bulk-copy launch (k_gather_sb): accesses
+// whose slot still holds its init node read the cache, the rest the table;
+// false if the row size does not suit the bulk-copy kernel
+bool launch_gather_superbatch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, uint64_t n,
+                              const uint32_t* init, uint32_t n_init, const uint8_t* cache_rows, const uint8_t* store,
+                              uint64_t rb, uint8_t* out);
+// every changeset of a superbatch applied at once (the cache is not read in
+// between): each slot gets its last insert's batch row; `last` = K zeroed u32
+// marks (left zeroed), in_off / bat_off = insert / batch-row offsets per iteration
+void launch_apply_all(gx_ctx* ctx, const uint32_t* in_pos, const uint32_t* in_slot, const uint32_t* in_off,
+                      uint32_t S, uint32_t n, const uint32_t* bat_off, uint32_t* last, const uint8_t* batch,
+                      uint8_t* cache_rows, uint64_t rb);
+// counters[8 i + 1 / + 2] += misses / pages of iteration i of a resolved access
+// list (slot kNever = miss), d_off = the S + 1 iteration offsets on the device
+void launch_count_iter_misses(gx_ctx* ctx, const uint32_t* ids, const uint32_t* slots, const uint32_t* d_off,
+                              uint32_t S, uint64_t maxw, uint64_t rb, unsigned long long* counters);
 
 // Storage tier (storage.cu). A slot value with kStageFlag set (and != kNever)
 // is a miss whose row was staged: the gather reads row (slot & ~kStageFlag)

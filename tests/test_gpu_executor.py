@@ -422,3 +422,49 @@ def test_pipeline_rejects_duplicate_seeds(gx, oracle):
     ref_edges = sum(sum(len(l) for l in oracle.sample_batch(ip, ind, b, [4, 4], oracle.derive_seed(1, i))[1])
                     for i, b in enumerate(good))
     assert st.sampled_edges == ref_edges
+
+
+@pytest.mark.parametrize("one_gather", [1, 0])
+def test_pipeline_cache_state_matches_reference_replay(gx, oracle, one_gather):
+    """The fused pipeline's executor leaves the feature cache in the state the
+    reference's FeatureCache reaches after S x (gather, apply_changeset)
+    (feature_cache.hpp:58-130): every occupied slot holds its node's row. Run
+    with the one-launch executor (GX_ONE_GATHER=1: one gather, changesets
+    applied at once, last insert per slot) and the per-segment one."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import json, sys, numpy as np
+sys.path.insert(0, %r)
+import oracle, paper_2208_09151_b200 as gx
+o = oracle.C
+n, dim, K = 4000, 16, 300
+ip, ind = o.rmat_graph(n, 7.0, 44)
+rows = o.features(n, dim, 45)
+plan = o.plan_seed_batches(o.train_ids(n, 1, 0.3), 40, o.epoch_seed(1, 0))[:9]
+p = gx.Pipeline(gx.GraphFile.from_csc(ip, ind), gx.FeatureFile.from_array(rows), [4, 3], K)
+st = p.run_superbatch(plan, 1, 0)
+trace = [o.sample_batch(ip, ind, b, [4, 3], o.derive_seed(1, i))[0] for i, b in enumerate(plan)]
+init = o.compute_init_set(trace, K, n)
+sim = o.simulate(trace, n, K, init)
+c = o.cache(rows, init, K)
+for i, ids in enumerate(trace):
+    b, _, _, _ = c.gather(ids)
+    a, e = int(sim["in_off"][i]), int(sim["in_off"][i + 1])
+    q, w = int(sim["out_off"][i]), int(sim["out_off"][i + 1])
+    c.apply(b, ids, sim["in_ids"][a:e], sim["in_pos"][a:e], sim["out_ids"][q:w])
+got = p.cache_rows()
+ok, occ = True, 0
+for v in c.resident():
+    s = c.slot(int(v))
+    occ += 1
+    ok &= bool(np.array_equal(got[s], rows[int(v)]))
+print(json.dumps({"ok": ok, "occupied": occ, "inserts": int(st.total_in), "misses": int(st.total_misses)}))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GX_ONE_GATHER=str(one_gather))
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    assert res["ok"] and res["occupied"] == 300 and res["inserts"] > 0, res
