@@ -147,11 +147,17 @@ __device__ __forceinline__ uint32_t hash32(uint32_t x) {
 
 // ---------------------------------------------------------------------------
 // Grid-wide barrier for persistent kernels launched cooperatively (all CTAs
-// co-resident). Sense via a monotonically increasing generation counter.
+// co-resident). Default: one monotonically increasing 64-bit arrival count
+// (zeroed by the host before each launch, `barrier_reset`): barrier k of a
+// launch completes when the count reaches k x gridDim, so a CTA's arrival is
+// one atomic and the waiters poll the same word -- no second hop through a
+// generation flag written by the last arriver. GX_BARRIER=0 (host knob,
+// `count64` left at ~0): the previous count + generation barrier.
 // ---------------------------------------------------------------------------
 struct GridBarrier {
     unsigned int count;
     unsigned int gen;
+    unsigned long long count64;
 };
 
 __device__ __forceinline__ unsigned cluster_ctas() {
@@ -171,24 +177,44 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b) {
         return;
     }
     if (threadIdx.x == 0) {
-        volatile unsigned int* vgen = &b->gen;
-        unsigned int g = *vgen;
-        __threadfence();
-        unsigned int arrived = atomicAdd(&b->count, 1u);
-        if (arrived == gridDim.x - 1) {
-            b->count = 0;
+        volatile unsigned long long* vc = &b->count64;
+        if (*vc != ~0ull) {  // monotonic arrival count (host-zeroed per launch)
             __threadfence();
-            atomicAdd(&b->gen, 1u);
-        } else {
-            unsigned ns = 32;
-            while (*vgen == g) {
-                __nanosleep(ns);
-                if (ns < 256) ns <<= 1;
+            const unsigned long long old = atomicAdd(&b->count64, 1ull);
+            const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+            while (*vc < target) {
             }
+            __threadfence();
+        } else {
+            volatile unsigned int* vgen = &b->gen;
+            unsigned int g = *vgen;
+            __threadfence();
+            unsigned int arrived = atomicAdd(&b->count, 1u);
+            if (arrived == gridDim.x - 1) {
+                b->count = 0;
+                __threadfence();
+                atomicAdd(&b->gen, 1u);
+            } else {
+                unsigned ns = 32;
+                while (*vgen == g) {
+                    __nanosleep(ns);
+                    if (ns < 256) ns <<= 1;
+                }
+            }
+            __threadfence();
         }
-        __threadfence();
     }
     __syncthreads();
+}
+
+// host: before every launch that synchronises through `b` on stream `st`
+inline void barrier_reset(GridBarrier* b, cudaStream_t st) {
+    static const bool mono = [] {
+        const char* e = std::getenv("GX_BARRIER");
+        return !e || std::atoi(e) != 0;
+    }();
+    // count64 = 0 selects the monotonic barrier, ~0 the generation barrier
+    GX_CUDA(cudaMemsetAsync(&b->count64, mono ? 0 : 0xff, sizeof(unsigned long long), st));
 }
 
 // ---------------------------------------------------------------------------

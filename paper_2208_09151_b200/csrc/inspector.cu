@@ -1426,6 +1426,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     for (int part = 0; part < 2; ++part) {
         void* fn = part ? rfns[ci] : kfns[ci];
         const int g = part ? grid : g0;
+        barrier_reset(a.bar, st);
         if (part && rec_cluster) {
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3(rec_cluster);

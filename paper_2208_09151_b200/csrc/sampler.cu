@@ -1215,6 +1215,7 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         a.layer_count = out->layer_count.p + c0 * L;
         a.batch0 = (uint32_t)c0;
         void* args[] = {&a};
+        barrier_reset(a.bar, st);
         if (coop_launch()) GX_CUDA(cudaLaunchCooperativeKernel((void*)k_sample, grid, block, args, smem, st));
         else GX_CUDA(cudaLaunchKernel((void*)k_sample, grid, block, args, smem, st));
         GX_CHECK_LAUNCH();
