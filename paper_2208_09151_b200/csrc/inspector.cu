@@ -173,8 +173,11 @@ __device__ __forceinline__ void stage_put(Stage st, bool pred, uint32_t a, uint3
 }
 // Called by the whole CTA after __syncthreads; flushes when `force` or when
 // another round could overflow the 2048-entry stage.
+// bm_words / bm_top (out lists): also mark every flushed node in the
+// two-level out bitmap, so the ordered out walk of P5 needs no marking pass.
 __device__ __forceinline__ void stage_flush(Stage st, uint32_t* gcnt, uint32_t* ga, uint32_t* gb, bool force,
-                                            uint32_t* bcast) {
+                                            uint32_t* bcast, uint32_t* bm_words = nullptr,
+                                            uint32_t* bm_top = nullptr) {
     const uint32_t n = *st.cnt;
     __syncthreads();  // every thread has read n before anyone appends again
     if (n == 0 || (!force && n < 1024)) return;
@@ -185,6 +188,11 @@ __device__ __forceinline__ void stage_flush(Stage st, uint32_t* gcnt, uint32_t* 
         const unsigned long long e = st.buf[k];
         ga[base + k] = (uint32_t)(e >> 32);
         gb[base + k] = (uint32_t)e;
+        if (bm_words) {
+            const uint32_t v = (uint32_t)(e >> 32);
+            atomicOr(&bm_words[v >> 5], 1u << (v & 31));
+            atomicOr(&bm_top[v >> 10], 1u << ((v >> 5) & 31));
+        }
     }
     __syncthreads();
     if (threadIdx.x == 0) *st.cnt = 0;
@@ -794,7 +802,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 stage_put(st_ev, ev, v, s);
                 if (j & 1) {
                     __syncthreads();
-                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10], a.bm_words, a.bm_top);
                 }
             }
         }
@@ -811,7 +819,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             }
             stage_put(st_ev, ev, v, s);
             __syncthreads();
-            stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+            stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10], a.bm_words, a.bm_top);
         }
         }
         if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
@@ -830,7 +838,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
             }
         }
         __syncthreads();
-        stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
+        stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10], a.bm_words, a.bm_top);
         stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         if (sel) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
         grid_sync(a.bar);
@@ -864,7 +872,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         stage_put(st_c, c, v, s);
                         if (j & 1) {
                             __syncthreads();
-                            stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                            stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10], a.bm_words, a.bm_top);
                             stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
                         }
                     }
@@ -883,12 +891,12 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     stage_put(st_ev, ev, v, s);
                     stage_put(st_c, c, v, s);
                     __syncthreads();
-                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10], a.bm_words, a.bm_top);
                     stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
                 }
                 }
                 __syncthreads();
-                stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
+                stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10], a.bm_words, a.bm_top);
                 stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
             } else {
                 const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
@@ -935,10 +943,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     const bool ev = k < nc && a.c_id[k] > thr;
                     stage_put(st_ev, ev, ev ? a.c_id[k] : 0, ev ? a.c_ref[k] : 0);
                     __syncthreads();
-                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10]);
+                    stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, false, &sm.bc[10], a.bm_words, a.bm_top);
                 }
                 __syncthreads();
-                stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10]);
+                stage_flush(st_ev, &cs->n_out, a.out_node, a.out_slot, true, &sm.bc[10], a.bm_words, a.bm_top);
             }
         }
         grid_sync(a.bar);
@@ -999,18 +1007,21 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     a.out_slot[k] = (uint32_t)sm.sortbuf[k];
                 }
             }
+            if (blockIdx.x == 0) {  // clear the bitmap marks made while staging
+                __syncthreads();
+                for (uint32_t k = tid; k < n_out; k += blockDim.x) {
+                    const uint32_t v = a.out_node[k];
+                    a.bm_words[v >> 5] = 0;
+                    a.bm_top[v >> 10] = 0;
+                }
+            }
             grid_sync(a.bar);
         } else if ((uint64_t)n_out * 32 < a.nwords) {
             // sparse outs (large N): two-level bitmap -- bit v of bm_words per
             // out node, bit w of bm_top per non-empty word, so the ordered walk
             // touches N/1024 summary words plus the occupied words instead of
             // all N/32 words (S = 500 at 5 %: P5 67 -> ~45 us per cut iteration)
-            for (uint32_t k = gtid; k < n_out; k += G) {
-                const uint32_t v = a.out_node[k];
-                atomicOr(&a.bm_words[v >> 5], 1u << (v & 31));
-                atomicOr(&a.bm_top[v >> 10], 1u << ((v >> 5) & 31));
-            }
-            grid_sync(a.bar);
+            // (every out node was marked when its stage was flushed, P3 / P4)
             const uint32_t tch = (a.ntop + gridDim.x - 1) / gridDim.x;
             const uint32_t t0 = min(a.ntop, blockIdx.x * tch), t1 = min(a.ntop, t0 + tch);
             uint32_t c = 0;
@@ -1046,12 +1057,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 pre += tot;
             }
             grid_sync(a.bar);
-        } else {  // dense outs: one flat pass over the N-bit bitmap
-            for (uint32_t k = gtid; k < n_out; k += G) {
-                const uint32_t v = a.out_node[k];
-                atomicOr(&a.bm_words[v >> 5], 1u << (v & 31));
-            }
-            grid_sync(a.bar);
+        } else {  // dense outs: one flat pass over the N-bit bitmap (marked while staging)
             const uint32_t wch = (a.nwords + gridDim.x - 1) / gridDim.x;
             const uint32_t w0 = min(a.nwords, blockIdx.x * wch), w1 = min(a.nwords, w0 + wch);
             uint32_t c = 0;
@@ -1067,7 +1073,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 uint32_t bits = w < w1 ? a.bm_words[w] : 0;
                 uint32_t tot;
                 uint32_t k = pre + block_excl_scan((uint32_t)__popc(bits), sm.scan, tot);
-                if (bits) a.bm_words[w] = 0;
+                if (bits) {
+                    a.bm_words[w] = 0;
+                    a.bm_top[w >> 5] = 0;  // (marked while staging; only the sparse walk reads it)
+                }
                 while (bits) {
                     const int b = __ffs(bits) - 1;
                     bits &= bits - 1;
