@@ -652,6 +652,33 @@ def main():
     for s in stats:
         assert s.total_misses == s.predicted_misses, "observed misses != inspector prediction"
 
+    # --- e2e with the gathered rows returned to the host: a caller that consumes
+    # batches on the CPU (the reference's RowMatrix) gets every iteration's rows
+    # in pinned memory; submit + wait + one D2H per superbatch, wall clock
+    e2e_rows = None
+    if rank == 0 and world == 1 and not args.no_tiers:
+        try:
+            k0 = args.warmup + args.steps
+            b0, f0 = rank_batches(sb_index(k0))
+            pipe.wait(pipe.submit(b0, SEED_RUN, f0))
+            nbytes = pipe.copy_superbatch(0, 0)
+            host = torch.empty(int(nbytes * 1.25) + (1 << 20), dtype=torch.uint8, pin_memory=True)
+            t0 = time.perf_counter()
+            e_sum, b_sum = 0, 0
+            for k in range(k0 + 1, k0 + 3):
+                bk, fk = rank_batches(sb_index(k))
+                stk = pipe.wait(pipe.submit(bk, SEED_RUN, fk))
+                b_sum += pipe.copy_superbatch(host.data_ptr(), host.numel())
+                e_sum += stk.sampled_edges
+            dt = time.perf_counter() - t0
+            e2e_rows = {"value": e_sum / dt, "unit": "sampled_edges/s", "d2h_GBps": b_sum / dt / 1e9,
+                        "d2h_bytes_per_step": b_sum // 2, "h2d_bytes_per_step": int(8 * sum(len(b) for b in bk)),
+                        "note": "2 superbatches, each: seeds in, sample + inspect + gather, then every "
+                                "iteration's gathered rows copied to pinned host memory (one D2H); wall clock"}
+            del host
+        except Exception as e:
+            e2e_rows = {"error": repr(e)}
+
     # --- cache-pressure line: the same superbatches through a small cache, so
     # the Belady recurrence and the changeset executor (not the all-fit path)
     # run inside the driver's bench (same graph and table, same timing rules)
@@ -848,6 +875,7 @@ def main():
         "rooflines": rooflines,
         "stages": stages,
         "cache_pressure": pressure,
+        "e2e_host_rows": e2e_rows,
         "clocks": clk.summary(),
     }
     if comm is not None:   # the NVLink tier: the row-partitioned table's all-to-all

@@ -428,6 +428,12 @@ void* gx_pipeline_exec_stream(gx_pipeline* p);
  * receives a copy of the rows. */
 gx_status gx_pipeline_batch(gx_pipeline* p, uint64_t ticket, uint64_t i, const void** rows,
                             uint64_t* n_rows, void* host_out);
+/* Every iteration's rows of a waited-for, HBM-resident superbatch copied to
+ * host memory in one D2H (the S RowMatrix objects of the reference's executor
+ * back to back; pinned host_out streams at PCIe rate). *bytes = rows x
+ * row_bytes; host_out == NULL only reports the size. */
+gx_status gx_pipeline_copy_superbatch(gx_pipeline* p, uint64_t ticket, void* host_out, uint64_t cap_bytes,
+                                      uint64_t* bytes);
 
 /* Optional per-iteration digest of each gathered batch (for end-to-end parity
  * checks; off by default, costs one extra read of every batch):

@@ -169,6 +169,7 @@ SIGNATURES = {
     "gx_pipeline_set_digest": (i32, [vp, i32]),
     "gx_pipeline_digests": (i32, [vp, vp]),
     "gx_pipeline_cache_rows": (i32, [vp, vp]),
+    "gx_pipeline_copy_superbatch": (i32, [vp, u64, vp, u64, P64]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

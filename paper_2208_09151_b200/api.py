@@ -1267,6 +1267,15 @@ class Pipeline:
     def exec_stream(self) -> int:
         return lib.gx_pipeline_exec_stream(self.h)
 
+    def copy_superbatch(self, host_ptr: int, cap_bytes: int, ticket: Optional[int] = None) -> int:
+        """All iterations' rows of a waited-for superbatch into host memory at
+        host_ptr (pinned for PCIe rate) in one D2H -> bytes copied
+        (gx_pipeline_copy_superbatch)."""
+        ticket = self._last if ticket is None else ticket
+        n = C.c_uint64()
+        check(lib.gx_pipeline_copy_superbatch(self.h, ticket, host_ptr, cap_bytes, C.byref(n)))
+        return n.value
+
     def cache_rows(self) -> np.ndarray:
         """Test hook: the feature cache's K slot rows after the last waited-for
         superbatch (gx_pipeline_cache_rows); never-filled slots are unspecified."""

@@ -780,6 +780,23 @@ gx_status gx_pipeline_batch(gx_pipeline* p, uint64_t ticket, uint64_t i, const v
     });
 }
 
+gx_status gx_pipeline_copy_superbatch(gx_pipeline* p, uint64_t ticket, void* host_out, uint64_t cap,
+                                      uint64_t* bytes) {
+    return guard([&] {
+        if (!p) fail(GX_INVALID_ARGUMENT, "null pipeline");
+        const PipeSlot& sl = p->slot[ticket & 1];
+        if (sl.ticket != ticket || sl.pending)
+            fail(GX_LOGIC_ERROR, "batches are readable after wait(ticket) until that slot is resubmitted");
+        if (!sl.full) fail(GX_LOGIC_ERROR, "superbatch exceeded GX_BATCH_BUDGET_MB: not resident");
+        const uint64_t n = sl.o[sl.S] * p->f->row_bytes;
+        if (bytes) *bytes = n;
+        if (!host_out || !n) return;
+        if (cap < n) fail(GX_INVALID_ARGUMENT, "host buffer smaller than the superbatch's rows");
+        GX_CUDA(cudaMemcpyAsync(host_out, sl.batch.p, n, cudaMemcpyDeviceToHost, p->exec));
+        GX_CUDA(cudaStreamSynchronize(p->exec));
+    });
+}
+
 gx_status gx_pipeline_superbatch(gx_pipeline* p, const uint64_t* seeds_flat, const uint64_t* batch_off,
                                  uint64_t S, uint64_t global_seed, uint64_t first_global_batch,
                                  uint64_t* misses_per_iter, gx_pipeline_stats* stats) {
