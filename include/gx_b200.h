@@ -422,7 +422,7 @@ void* gx_pipeline_exec_stream(gx_pipeline* p);
  * RowMatrix of feature_cache.hpp:58 kept in HBM) of a waited-for superbatch.
  * Valid until the slot is resubmitted (ticket + 2). The executor keeps the whole
  * superbatch's batches resident (rows of iteration i at row offset
- * sum_{j<i}|ids_j|) when they fit GX_BATCH_BUDGET_MB (default 24 GiB per slot);
+ * sum_{j<i}|ids_j|) when they fit the free HBM (or GX_BATCH_BUDGET_MB per slot);
  * otherwise it reuses one iteration-sized buffer and only the last iteration is
  * readable (GX_LOGIC_ERROR for the others). host_out (nullable) additionally
  * receives a copy of the rows. */

@@ -481,8 +481,23 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         // all-fit superbatches fuse the cache fill with the first uses when the
         // whole superbatch is resident in HBM and the backing table is too
         const uint64_t rb = p->f->row_bytes;
-        static const uint64_t budget = (uint64_t)std::max(0, gx::env_int("GX_BATCH_BUDGET_MB", 24576)) << 20;
-        const bool resident = sl.o[S] * rb <= budget;
+        // the whole superbatch's rows stay in HBM when they fit: GX_BATCH_BUDGET_MB
+        // caps a slot explicitly; by default whatever the device has free (the
+        // slot's current buffer included) minus a margin for the inspector's
+        // trace-sized scratch (S = 500 at papers shape: 46 GB per slot)
+        const uint64_t need = sl.o[S] * rb;
+        static const int budget_mb = gx::env_int("GX_BATCH_BUDGET_MB", -1);
+        bool resident;
+        if (budget_mb >= 0) {
+            resident = need <= ((uint64_t)budget_mb << 20);
+        } else if (need <= sl.batch.n) {
+            resident = true;
+        } else {
+            size_t fr = 0, total = 0;
+            GX_CUDA(cudaMemGetInfo(&fr, &total));
+            const uint64_t margin = (4ull << 30) + 16ull * sl.o[S];
+            resident = need + margin <= (uint64_t)fr + sl.batch.n;
+        }
         // fan-out form (default): each init row read once, written to its slot
         // and every batch row of its node; GX_FANOUT=0: fill + first use, then
         // a gather of the other accesses from the cache
