@@ -589,6 +589,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 #else
                             got[j] = atomicCAS(&btab[slot[j]], kEmptySlot,
                                                ((unsigned long long)child[j] << 32) | (kNewBit | p));
+#endif
                         }
                     }
 #if GX_E_LOADFIRST
@@ -636,7 +637,6 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                     atomicAdd(&a.trace[101 + 2 * l], (unsigned long long)(clock64() - c_e2));
             }
         }
-#endif
         grid_sync(a.bar);
         TRACE_STAMP(a, l, 2);
 
