@@ -491,6 +491,7 @@ gx_status gx_graph_partition(gx_graph* g, int P, int rank) {
         if (g->part.P) fail(GX_LOGIC_ERROR, "graph is already partitioned");
         if (rank < 0 || rank >= P) fail(GX_INVALID_ARGUMENT, "rank out of range");
         GraphParts& pt = g->part;
+        GX_CUDA(cudaSetDevice(g->ctx->device));
         part_bounds(g, P, pt.node_bounds, pt.ebound);
         const uint64_t lo = pt.ebound[rank], hi = pt.ebound[rank + 1];
         DevBuf<uint32_t> mine(std::max<uint64_t>(hi - lo, 1));
@@ -510,6 +511,7 @@ gx_status gx_graph_ipc_handle(const gx_graph* g, void* handle, uint64_t* edge_lo
     return guard([&] {
         if (!g->part.P) fail(GX_LOGIC_ERROR, "graph is not partitioned");
         static_assert(sizeof(cudaIpcMemHandle_t) == GX_IPC_HANDLE_BYTES, "IPC handle size");
+        GX_CUDA(cudaSetDevice(g->ctx->device));
         cudaIpcMemHandle_t h;
         GX_CUDA(cudaIpcGetMemHandle(&h, g->indices.p));
         std::memcpy(handle, &h, sizeof(h));
@@ -523,6 +525,7 @@ gx_status gx_graph_attach_peers(gx_graph* g, const void* handles, const uint64_t
         GraphParts& pt = g->part;
         if (!pt.P) fail(GX_LOGIC_ERROR, "graph is not partitioned");
         if (pt.attached) fail(GX_LOGIC_ERROR, "peers are already attached");
+        GX_CUDA(cudaSetDevice(g->ctx->device));  // the mappings belong to this graph's device
         for (int q = 0; q < pt.P; ++q)
             if (lohi[2 * q] != pt.ebound[q] || lohi[2 * q + 1] != pt.ebound[q + 1])
                 fail(GX_INVALID_ARGUMENT, "peer " + std::to_string(q) + " holds a different edge range");
