@@ -123,6 +123,10 @@ struct SampArgs {
     uint32_t fx_epoch, batch0;
     GridBarrier* bar;
     uint32_t* tctr;             // dynamic tile counters, 4 per layer (zeroed at kernel start)
+    // phase E stages a tile's (position, parent) draws in shared memory (after
+    // SampSmem, SB_TILE x max fanout entries) instead of the edge slots, so the
+    // draw loop's first load is an smem read, not an L2 round trip
+    uint32_t stage_smem;
     unsigned long long* trace;  // optional phase timestamps (GX_SAMPLER_TRACE)
 };
 
@@ -355,6 +359,7 @@ __device__ __forceinline__ void clear_region(unsigned long long* tab, uint64_t t
 __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
     extern __shared__ unsigned char smem_raw[];
     SampSmem& sm = *reinterpret_cast<SampSmem*>(smem_raw);
+    uint2* const sm_stage = reinterpret_cast<uint2*>(smem_raw + ((sizeof(SampSmem) + 15) & ~size_t(15)));
     __shared__ uint32_t bcast;
     const uint32_t S = a.S;
     const uint32_t tid = threadIdx.x;
@@ -547,7 +552,8 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                     if (tk) {
                         const uint64_t gi = (uint64_t)b * a.cap_ids + k0 + j;
                         sm.plo_s[tid * SB_IPT + j] = a.plo[gi];
-                        draw_positions(tk, seed, dbase + off, a.pdeg[gi], bedge + off, k0 + j);
+                        draw_positions(tk, seed, dbase + off, a.pdeg[gi],
+                                       a.stage_smem ? sm_stage + (off - toff) : bedge + off, k0 + j);
                     }
                     off += tk;
                 }
@@ -569,7 +575,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
                         const uint32_t p = q0 + j * blockDim.x;
-                        if (p < tile_d1) st[j] = bedge[p];
+                        if (p < tile_d1) st[j] = a.stage_smem ? sm_stage[p - tile_d0] : bedge[p];
                     }
 #pragma unroll
                     for (int j = 0; j < U; ++j) {
@@ -1134,16 +1140,28 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         a.trace = tbuf.p;
     }
 
-    const size_t smem = sizeof(SampSmem);
-    // attributes and occupancy are per device: cached per device ordinal
-    static PerDevice<int> bps_dev;
+    // phase-E draw staging in shared memory when a tile's draws fit 32 KB
+    // (SB_TILE parents x max fanout; GX_SAMPLER_STAGE_SMEM=0 keeps the edge slots)
+    uint32_t maxf = 0;
+    for (uint32_t l = 0; l < L; ++l) maxf = std::max(maxf, fanouts[l]);
+    const size_t stage_bytes = (size_t)SB_TILE * maxf * sizeof(uint2);
+    static const bool stage_knob = env_int("GX_SAMPLER_STAGE_SMEM", 1) != 0;
+    a.stage_smem = stage_knob && maxf > 0 && stage_bytes <= (32u << 10) ? 1u : 0u;
+    const size_t smem = ((sizeof(SampSmem) + 15) & ~size_t(15)) + (a.stage_smem ? stage_bytes : 0);
+    // attributes and occupancy are per device (and per shared-memory size)
+    static PerDevice<std::map<size_t, int>> bps_dev;
     GX_CUDA(cudaSetDevice(ctx->device));
     int blocks_per_sm = 0;
     {
         auto lk = bps_dev.lock();
-        int& cached = bps_dev.at(ctx->device);
-        if (cached < 1) {
+        int& cached = bps_dev.at(ctx->device)[smem];
+        // the attribute is per kernel: keep it at the largest size used on this device
+        int& attr = bps_dev.at(ctx->device)[0];
+        if ((int)smem > attr) {
             GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = (int)smem;
+        }
+        if (cached < 1) {
             static const int carve = env_int("GX_SAMPLER_CARVEOUT", -1);  // % of the array as shared memory
             if (carve >= 0)
                 GX_CUDA(cudaFuncSetAttribute(k_sample, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
