@@ -179,12 +179,24 @@ __device__ __forceinline__ void grid_sync(GridBarrier* b) {
     if (threadIdx.x == 0) {
         volatile unsigned long long* vc = &b->count64;
         if (*vc != ~0ull) {  // monotonic arrival count (host-zeroed per launch)
+#ifndef GX_BARRIER_FENCES
+            // release on the arrival (cumulative over the CTA's writes ordered
+            // before it by the __syncthreads above), acquire on the polls
+            unsigned long long old;
+            asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(&b->count64) : "memory");
+            const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
+            unsigned long long cur;
+            do {
+                asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(&b->count64) : "memory");
+            } while (cur < target);
+#else
             __threadfence();
             const unsigned long long old = atomicAdd(&b->count64, 1ull);
             const unsigned long long target = (old / gridDim.x + 1) * gridDim.x;
             while (*vc < target) {
             }
             __threadfence();
+#endif
         } else {
             volatile unsigned int* vgen = &b->gen;
             unsigned int g = *vgen;
