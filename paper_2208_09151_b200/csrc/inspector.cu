@@ -94,6 +94,10 @@ struct IArgs {
     uint32_t nwords;
     uint32_t* bm_top;    // ntop = ceil(nwords / 32): bit w set iff bm_words[w] != 0
     uint32_t ntop;
+    // radix select over node ids in b*: digit 1 = id >> sh1 (<= 2048 values),
+    // digit 2 = (id >> sh2) & m2, digit 3 = id & (2^sh2 - 1); sh2 == 0 (N <= 2^22):
+    // two passes -- one histogram and one grid barrier fewer per cut iteration
+    uint32_t sh1, sh2, m2;
     uint32_t* bm_cnt;    // gridDim
     const uint32_t* init_ext;
     uint32_t n_init_ext;
@@ -798,7 +802,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 const bool mem = s < nres && sel == 1 && bk[j] == bstar;
                 uint32_t v = 0;
                 if (ev || mem) v = a.slot_node[s];
-                if (mem) atomicAdd(&sm.rh[v >> 21], 1);
+                if (mem) atomicAdd(&sm.rh[v >> a.sh1], 1);
                 stage_put(st_ev, ev, v, s);
                 if (j & 1) {
                     __syncthreads();
@@ -815,7 +819,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 const uint32_t bk = bucket_of(a.slot_key[s], S);
                 ev = bk > bstar || (bk == bstar && keep_inc == 0);
                 if (ev || (sel == 1 && bk == bstar)) v = a.slot_node[s];
-                if (sel == 1 && bk == bstar) atomicAdd(&sm.rh[v >> 21], 1);
+                if (sel == 1 && bk == bstar) atomicAdd(&sm.rh[v >> a.sh1], 1);
             }
             stage_put(st_ev, ev, v, s);
             __syncthreads();
@@ -830,7 +834,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 if (pos < ni && a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar) {
                     c = true;
                     v = a.trace[base + pos];
-                    atomicAdd(&sm.rh[v >> 21], 1);
+                    atomicAdd(&sm.rh[v >> a.sh1], 1);
                 }
                 stage_put(st_c, c, v, pos);
                 __syncthreads();
@@ -864,9 +868,9 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         uint32_t v = 0;
                         if (inb[j]) {
                             v = a.slot_node[s];
-                            ev = (v >> 21) > d1;
-                            c = (v >> 21) == d1;
-                            if (c) atomicAdd(&sm.rh[(v >> 10) & 2047], 1);
+                            ev = (v >> a.sh1) > d1;
+                            c = (v >> a.sh1) == d1;
+                            if (c) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
                         }
                         stage_put(st_ev, ev, v, s);
                         stage_put(st_c, c, v, s);
@@ -884,9 +888,9 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     uint32_t v = 0;
                     if (s < nres && bucket_of(a.slot_key[s], S) == bstar) {
                         v = a.slot_node[s];
-                        ev = (v >> 21) > d1;
-                        c = (v >> 21) == d1;
-                        if (c) atomicAdd(&sm.rh[(v >> 10) & 2047], 1);
+                        ev = (v >> a.sh1) > d1;
+                        c = (v >> a.sh1) == d1;
+                        if (c) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
                     }
                     stage_put(st_ev, ev, v, s);
                     stage_put(st_c, c, v, s);
@@ -902,22 +906,27 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
                 for (uint32_t k = gtid; k < nc; k += G) {
                     const uint32_t v = a.c_id[k];
-                    if ((v >> 21) == d1) atomicAdd(&sm.rh[(v >> 10) & 2047], 1);
+                    if ((v >> a.sh1) == d1) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
                 }
             }
             hist_flush(sm.rh, (int32_t*)a.rh + 2048, 2048);
             grid_sync(a.bar);
             const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
             const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
-            const uint32_t pre = (d1 << 11) | d2;
-            for (uint32_t k = gtid; k < nc; k += G) {
-                const uint32_t v = a.c_id[k];
-                if ((v >> 10) == pre) atomicAdd(&sm.rh[v & 1023], 1);
+            const uint32_t pre = (d1 << (a.sh1 - a.sh2)) | d2;  // id >> sh2 of the cut
+            if (a.sh2 == 0) {
+                thr = pre;
+            } else {
+                (void)nc;
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const uint32_t v = a.c_id[k];
+                    if ((v >> a.sh2) == pre) atomicAdd(&sm.rh[v & ((1u << a.sh2) - 1)], 1);
+                }
+                hist_flush(sm.rh, (int32_t*)a.rh + 4096, 1024);
+                grid_sync(a.bar);
+                const uint32_t d3 = hist_select(a.rh + 4096, 1u << a.sh2, left, &left, sm);
+                thr = (pre << a.sh2) | d3;
             }
-            hist_flush(sm.rh, (int32_t*)a.rh + 4096, 1024);
-            grid_sync(a.bar);
-            const uint32_t d3 = hist_select(a.rh + 4096, 1024, left, &left, sm);
-            thr = (pre << 10) | d3;
         }
         IPHASE(a, 4);
 
@@ -1354,6 +1363,13 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.nwords = (uint32_t)((N + 31) / 32);
     a.bm_top = B.bm_top.p;
     a.ntop = (uint32_t)((N + 1023) / 1024);
+    {
+        uint32_t D = 1;
+        while (D < 32 && (1ull << D) < N) ++D;  // ids < N need D bits
+        a.sh1 = D > 11 ? D - 11 : 0;
+        a.sh2 = a.sh1 > 11 ? a.sh1 - 11 : 0;
+        a.m2 = (1u << (a.sh1 - a.sh2)) - 1;
+    }
     a.bm_cnt = B.bm_cnt.p;
     a.init_ext = n_init_explicit >= 0 ? B.init_ext.p : nullptr;
     a.n_init_ext = n_init_explicit >= 0 ? (uint32_t)n_init_explicit : 0;
