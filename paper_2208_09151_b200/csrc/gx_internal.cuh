@@ -75,6 +75,9 @@ struct InspectScratch {
         c_ref, in_node, in_pos, chunk_cnt, bm_words, bm_top, bm_cnt, init_ext, toff, st;
     DevBuf<int32_t> hist_inc;
     DevBuf<uint8_t> pmiss;
+    // deferred-ordering recurrence (inspector.cu: recurrence_deferred, k_finish_changesets)
+    DevBuf<uint32_t> slot_tag, out_raw, out_tagraw, tag_sorted, ev_slot, ins_x, fin_unres;
+    DevBuf<uint8_t> sort_tmp;
     DevBuf<uint32_t> o_misses, o_in_off, o_out_off;  // per-iteration outputs (S+1)
     DevBuf<unsigned long long> bits;  // N * ceil(S/64) iteration bitmask, clean between calls
     uint64_t bits_words = 0;

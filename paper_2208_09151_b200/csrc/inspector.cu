@@ -46,13 +46,15 @@ constexpr uint32_t kMaxIters = 4096;
 
 struct IState {
     uint32_t n_res;
-    uint32_t miss;
+    uint32_t n_ins;  // deferred recurrence: insertion tickets of the iteration
     uint32_t n_out;
     uint32_t n_c;
     uint32_t in_total;
     uint32_t out_total;
     uint32_t n_first;
     uint32_t err;
+    uint32_t exp_out;  // deferred recurrence: the iteration's eviction / insertion counts
+    uint32_t exp_in;   // from the histograms (checked against the tickets handed out)
 };
 
 struct IArgs {
@@ -116,7 +118,18 @@ struct IArgs {
     uint32_t* o_out_off;  // S+1
     IState* st;
     GridBarrier* bar;
+    // deferred ordering (GX_INSPECT_DEFER, default on): the recurrence keeps an
+    // internal slot layout and unordered in/out sets; k_finish_changesets
+    // derives the reference's ordered lists and FeatureCache slots afterwards
+    int defer;
+    uint32_t* slot_tag;    // K: occupancy tag of each internal slot (init rank r, or kEv | access)
+    uint32_t* out_raw;     // A: evicted node per out ticket (iteration-major, unordered)
+    uint32_t* out_tagraw;  // A: the evicted occupancy's tag
+    uint32_t* ev_slot;     // maxw: internal slot freed by eviction ticket t (kNever = not yet)
+    uint32_t* ins_x;       // maxw: access of a certain insertion whose eviction comes later
 };
+
+constexpr uint32_t kEv = 0x80000000u;  // tag bit: the occupancy began at access (tag & ~kEv)
 
 // block 0 / thread 0 records the time since kernel start into slot k (after a grid barrier)
 #define ISTAMP(a, k)                                                         \
@@ -214,6 +227,7 @@ struct ISmem {
     static_assert(kSort >= 4096, "two 2048-entry Stage buffers live in sortbuf");
     uint32_t scan[34];
     uint32_t bc[16];
+    unsigned long long scan64[34];
     unsigned long long sortbuf[kSort];
     uint32_t toff[CAP + 1];
     int32_t hinc[CAP + 1];  // per-CTA histogram deltas, flushed with one atomic per bin
@@ -381,6 +395,441 @@ __device__ bool next_use_pass(const IArgs& a, SM& sm, bool firsts) {
     return true;
 }
 
+// ---------------------------------------------------------------------------
+// Deferred-ordering recurrence (default; GX_INSPECT_DEFER=0 keeps the ordered
+// one below). The Belady recurrence only needs the resident SET and its keys:
+// the order of in_ids (positions), out_ids (ids) and the FeatureCache slot each
+// insertion lands in (in[k] takes out[k]'s slot, feature_cache.hpp:114-129)
+// are functions of the sets, so they are derived after the loop, for every
+// iteration at once (k_finish_changesets). Inside the loop a node sits in an
+// internal slot: insertion ticket t takes the slot freed by eviction ticket t
+// (published through ev_slot by the evicting CTA) or a fresh one. Every count
+// of the cut follows from the key histograms right after P1:
+//   n_out = nres - (incumbents below b*) - keep_inc,
+//   n_in  = (new candidates below b*) + admit_new,
+// so a cut iteration is P1 | P3 (+ radix digits of b*) | final: 3-5 grid
+// barriers instead of 6-8, and no ordered list is built inside the loop.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// slot freed by eviction ticket t; its producer (a CTA that finished its own
+// evictions before consuming anything) never waits, so the spin ends
+__device__ __forceinline__ uint32_t take_slot(uint32_t* ev_slot, uint32_t t) {
+    uint32_t s;
+    while ((s = ld_acquire_u32(ev_slot + t)) == kNever) {
+    }
+    ev_slot[t] = kNever;  // each ticket is consumed once: clean for the next iteration
+    return s;
+}
+
+// Flush staged evictions (internal slots): each takes the next out ticket t,
+// its node and occupancy tag go to the iteration's raw out list, the node
+// leaves the cache, and slot s is published as ev_slot[t].
+__device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, uint32_t out_total, bool force,
+                                         uint32_t* bcast) {
+    const uint32_t n = *st.cnt;
+    __syncthreads();
+    if (n == 0 || (!force && n < 1024)) return;
+    if (threadIdx.x == 0) *bcast = atomicAdd(&cs->n_out, n);
+    __syncthreads();
+    const uint32_t base = *bcast;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint32_t s = (uint32_t)st.buf[k];
+        const uint32_t t = base + k;
+        const uint32_t u = a.slot_node[s];
+        a.out_raw[out_total + t] = u;
+        a.out_tagraw[out_total + t] = a.slot_tag[s];
+        a.node_slot[u] = -1;
+        st_release_u32(a.ev_slot + t, s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *st.cnt = 0;
+    __syncthreads();
+}
+
+// a missed access x enters internal slot s with key `key`
+template <class SM>
+__device__ __forceinline__ void place_ins(const IArgs& a, SM& sm, uint32_t x, uint32_t key, uint32_t s, uint32_t S) {
+    const uint32_t v = a.trace[x];
+    a.slot_node[s] = v;
+    a.slot_key[s] = key;
+    a.slot_tag[s] = kEv | x;
+    a.node_slot[v] = (int32_t)s;
+    atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
+    a.isfirst[x] = 1;  // (isfirst doubles as the inserted-access flag in PART 1)
+}
+
+// P3 slot scan: evict every incumbent above b* (and b* itself when none of it
+// is kept); sel 1: first radix digit of b*'s incumbents. PI slots per thread
+// per pass with their keys loaded together.
+template <int PI, class SM>
+__device__ __forceinline__ void p3_scan(const IArgs& a, SM& sm, uint32_t nres, uint32_t bstar, bool evict_b,
+                                        bool memb, Stage st_ev, IState* cs, uint32_t out_total, uint32_t S) {
+    const uint32_t G = gridDim.x * blockDim.x;
+    for (uint32_t s0 = blockIdx.x * blockDim.x * PI; s0 < nres; s0 += G * PI) {  // CTA-uniform trip count
+        uint32_t bk[PI];
+#pragma unroll
+        for (int j = 0; j < PI; ++j) {
+            const uint32_t s = s0 + j * blockDim.x + threadIdx.x;
+            bk[j] = s < nres ? bucket_of(a.slot_key[s], S) : 0u;  // bucket 0 <= i < b*: kept
+        }
+#pragma unroll
+        for (int j = 0; j < PI; ++j) {
+            const uint32_t s = s0 + j * blockDim.x + threadIdx.x;
+            const bool ev = s < nres && (bk[j] > bstar || (bk[j] == bstar && evict_b));
+            if (s < nres && memb && bk[j] == bstar) atomicAdd(&sm.rh[a.slot_node[s] >> a.sh1], 1);
+            if (ev) atomicSub(&sm.hinc[bk[j]], 1);
+            stage_put(st_ev, ev, 0, s);
+            if (PI == 1 || (j & 1)) {
+                __syncthreads();
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10]);
+            }
+        }
+    }
+}
+
+// P3b (sel 1): b*'s incumbents whose first digit is above the cut digit leave,
+// the ones on it become candidates (c_id / c_ref = slot) with their 2nd digit
+template <int PI, class SM>
+__device__ __forceinline__ void p3b_scan(const IArgs& a, SM& sm, uint32_t nres, uint32_t bstar, uint32_t d1,
+                                         Stage st_ev, Stage st_c, IState* cs, uint32_t out_total, uint32_t S) {
+    const uint32_t G = gridDim.x * blockDim.x;
+    for (uint32_t s0 = blockIdx.x * blockDim.x * PI; s0 < nres; s0 += G * PI) {  // CTA-uniform trip count
+        bool inb[PI];
+#pragma unroll
+        for (int j = 0; j < PI; ++j) {
+            const uint32_t s = s0 + j * blockDim.x + threadIdx.x;
+            inb[j] = s < nres && bucket_of(a.slot_key[s], S) == bstar;
+        }
+#pragma unroll
+        for (int j = 0; j < PI; ++j) {
+            const uint32_t s = s0 + j * blockDim.x + threadIdx.x;
+            const uint32_t v = inb[j] ? a.slot_node[s] : 0u;
+            const bool ev = inb[j] && (v >> a.sh1) > d1;
+            const bool c = inb[j] && (v >> a.sh1) == d1;
+            if (c) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
+            if (ev) atomicSub(&sm.hinc[bstar], 1);
+            stage_put(st_ev, ev, 0, s);
+            stage_put(st_c, c, v, s);
+            if (PI == 1 || (j & 1)) {
+                __syncthreads();
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10]);
+                stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
+            }
+        }
+    }
+}
+
+template <uint32_t CAP>
+__device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
+    const uint32_t S = a.S, K = a.K;
+    const uint32_t tid = threadIdx.x;
+    const uint32_t G = gridDim.x * blockDim.x;
+    const uint32_t gtid = blockIdx.x * blockDim.x + tid;
+    for (uint32_t i = 0; i < S; ++i) {
+        IPHASE(a, 0);
+        IState* cs = a.st + (i & 1);
+        IState* ns = a.st + ((i + 1) & 1);  // = the previous iteration's state until the final phase
+        const uint32_t base = sm.toff[i];
+        const uint32_t ni = sm.toff[i + 1] - base;
+        const uint32_t chunk = (ni + gridDim.x - 1) / gridDim.x;
+        const uint32_t c0 = min(ni, blockIdx.x * chunk), c1 = min(ni, c0 + chunk);
+        const uint32_t nres = *(volatile uint32_t*)&cs->n_res;
+        const uint32_t in_total = *(volatile uint32_t*)&cs->in_total;
+        const uint32_t out_total = *(volatile uint32_t*)&cs->out_total;
+        if (i > 0 && gtid == 0) {  // the previous iteration handed out exactly its histogram counts
+            const volatile IState* ps = ns;
+            if (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in) atomicOr(&a.st->err, 8u);
+        }
+        for (uint32_t b = gtid; b < 3 * 2048; b += G) a.rh[b] = 0;  // last read before the previous barrier
+
+        // P1: hits refresh their key and record their occupancy tag; misses
+        // become candidates; per-chunk miss counts
+        {
+            uint32_t miss = 0, hits = 0;
+            for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) {
+                const uint32_t x = base + pos;
+                const uint32_t v = a.trace[x];
+                const uint32_t nu = a.next_use[x];
+                const int32_t s = a.node_slot[v];
+                a.isfirst[x] = 0;
+                if (s >= 0) {
+                    a.slot_key[s] = nu;
+                    a.acc_slot[x] = a.slot_tag[s];
+                    atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
+                    ++hits;
+                    a.pmiss[pos] = 0;
+                } else {
+                    a.pmiss[pos] = 1;
+                    a.pkey[pos] = nu;
+                    a.acc_slot[x] = kNever;
+                    atomicAdd(&sm.hnew[bucket_of(nu, S)], 1);
+                    ++miss;
+                }
+            }
+            miss = block_sum(miss, sm.scan);
+            hits = block_sum(hits, sm.scan);
+            if (tid == 0) {
+                a.chunk_miss[blockIdx.x] = miss;
+                sm.hinc[i] -= (int32_t)hits;  // all incumbents keyed i are exactly the hits
+            }
+            hist_flush(sm.hinc, a.hist_inc, S + 1);
+            hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
+        }
+        grid_sync(a.bar);
+        IPHASE(a, 1);
+
+        uint32_t m, mpre;  // misses this iteration, misses in earlier chunks
+        {
+            uint32_t pre = 0, tot = 0;
+            for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
+                const uint32_t v = a.chunk_miss[c];
+                if (c < blockIdx.x) pre += v;
+                tot += v;
+            }
+            mpre = block_sum(pre, sm.scan);
+            m = block_sum(tot, sm.scan);
+        }
+        if ((uint64_t)nres + m <= K) {
+            // ALLIN: every miss enters, in position order, the next fresh slots
+            uint32_t k = mpre;
+            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {
+                const uint32_t pos = p0 + tid;
+                const uint32_t f = pos < c1 ? a.pmiss[pos] : 0;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan(f, sm.scan, tot);
+                if (f) place_ins(a, sm, base + pos, a.pkey[pos], nres + k + ex, S);
+                k += tot;
+            }
+            hist_flush(sm.hinc, a.hist_inc, S + 1);
+            for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+            if (gtid == 0) {
+                a.o_misses[i] = m;
+                cs->exp_out = 0;
+                cs->exp_in = 0;
+                ns->n_res = nres + m;
+                ns->in_total = in_total + m;
+                ns->out_total = out_total;
+                ns->n_out = 0;
+                ns->n_c = 0;
+                ns->n_ins = 0;
+                a.o_in_off[i + 1] = in_total + m;
+                a.o_out_off[i + 1] = out_total;
+            }
+            grid_sync(a.bar);
+            IPHASE(a, 2);
+            if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[30] += 1;
+            continue;
+        }
+        if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[31] += 1;
+
+        // CUT: threshold bucket b* over keys in (i, S] (every CTA, redundantly),
+        // scanning (incumbents, new candidates) pairs so that the counts below
+        // b* come out of the same block scan
+        {
+            if (tid == 0) sm.bc[0] = 0xFFFFFFFFu;
+            __syncthreads();
+            unsigned long long cum = 0;
+            for (uint32_t b0 = i + 1; b0 <= S; b0 += blockDim.x) {  // CTA-uniform
+                const uint32_t b = b0 + tid;
+                uint32_t ci = 0, cn = 0;
+                if (b <= S) {
+                    ci = (uint32_t)((volatile int32_t*)a.hist_inc)[b];
+                    cn = ((volatile uint32_t*)a.hist_new)[b];
+                }
+                unsigned long long tot;
+                const unsigned long long bef =
+                    cum + block_excl_scan(((unsigned long long)ci << 32) | cn, sm.scan64, tot);
+                const uint32_t before = (uint32_t)(bef >> 32) + (uint32_t)bef, v = ci + cn;
+                if (b <= S && (K == 0 ? b == i + 1 : (before < K && before + v >= K))) {
+                    sm.bc[0] = b;
+                    sm.bc[1] = K - before;
+                    sm.bc[2] = ci;
+                    sm.bc[3] = cn;
+                    sm.bc[4] = (uint32_t)(bef >> 32);  // incumbents in (i, b*)
+                    sm.bc[5] = (uint32_t)bef;          // new candidates in (i, b*)
+                }
+                __syncthreads();
+                if (sm.bc[0] != 0xFFFFFFFFu) break;
+                cum += tot;
+            }
+        }
+        __syncthreads();
+        const uint32_t bstar = sm.bc[0], r = sm.bc[1], inc_b = sm.bc[2], new_b = sm.bc[3];
+        const uint32_t inc_before = sm.bc[4], new_before = sm.bc[5];
+        __syncthreads();
+        int sel = 0;  // 1: select among incumbents of b*, 2: among new candidates of b*
+        if (r <= inc_b) sel = (r > 0 && r < inc_b) ? 1 : 0;
+        else sel = (r - inc_b < new_b) ? 2 : 0;
+        const uint32_t keep_inc = min(r, inc_b);
+        const uint32_t admit_new = r > inc_b ? r - inc_b : 0;
+        const bool evict_b = keep_inc == 0;  // none of b*'s incumbents kept: they leave in P3
+        const uint32_t n_out = nres - inc_before - keep_inc;
+        const uint32_t n_in = new_before + admit_new;
+        const uint32_t n_out_p3 = nres - inc_before - (evict_b ? 0u : inc_b);  // eviction tickets issued in P3
+
+        // P3: evictions above b*; b*'s members for the radix select; certain
+        // insertions (keys below b*) in tickets -- placed now when their
+        // eviction was issued in this phase (or they take a fresh slot)
+        const Stage st_ev{sm.sortbuf, &sm.bc[8]}, st_c{sm.sortbuf + 2048, &sm.bc[9]};
+        if (tid == 0) {
+            sm.bc[8] = 0;
+            sm.bc[9] = 0;
+        }
+        __syncthreads();
+        if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S);
+        else p3_scan<1>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S);
+        __syncthreads();
+        ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10]);
+        if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
+            for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < ni; p0 += G) {
+                const uint32_t pos = p0 + tid;
+                bool c = false;
+                uint32_t v = 0;
+                if (pos < ni && a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar) {
+                    c = true;
+                    v = a.trace[base + pos];
+                    atomicAdd(&sm.rh[v >> a.sh1], 1);
+                }
+                stage_put(st_c, c, v, pos);
+                __syncthreads();
+                stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
+            }
+            __syncthreads();
+            stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
+        }
+        if (new_before) {
+            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {  // CTA-uniform
+                const uint32_t pos = p0 + tid;
+                bool f = false;
+                uint32_t key = 0;
+                if (pos < c1 && a.pmiss[pos]) {
+                    key = a.pkey[pos];
+                    f = bucket_of(key, S) < bstar;
+                }
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan((uint32_t)f, sm.scan, tot);
+                if (tid == 0 && tot) sm.bc[11] = atomicAdd(&cs->n_ins, tot);
+                __syncthreads();
+                if (f) {
+                    const uint32_t t = sm.bc[11] + ex;
+                    if (t < n_out_p3) place_ins(a, sm, base + pos, key, take_slot(a.ev_slot, t), S);
+                    else if (t < n_out) a.ins_x[t] = base + pos;  // its slot is freed after the select
+                    else place_ins(a, sm, base + pos, key, nres + (t - n_out), S);
+                }
+            }
+        }
+        if (sel) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
+        // (hinc deltas stay in shared memory until the final phase: other CTAs
+        // may still be reading hist_inc for b*)
+        grid_sync(a.bar);
+        IPHASE(a, 3);
+
+        uint32_t thr = 0xFFFFFFFFu;
+        if (sel) {
+            const uint32_t want = sel == 1 ? keep_inc : admit_new;
+            uint32_t left;
+            const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
+            if (sel == 1) {
+                if (nres >= 8u * G) p3b_scan<8>(a, sm, nres, bstar, d1, st_ev, st_c, cs, out_total, S);
+                else p3b_scan<1>(a, sm, nres, bstar, d1, st_ev, st_c, cs, out_total, S);
+                __syncthreads();
+                ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10]);
+                stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
+            } else {
+                const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const uint32_t v = a.c_id[k];
+                    if ((v >> a.sh1) == d1) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
+                }
+            }
+            hist_flush(sm.rh, (int32_t*)a.rh + 2048, 2048);
+            grid_sync(a.bar);
+            const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
+            const uint32_t pre = (d1 << (a.sh1 - a.sh2)) | d2;  // id >> sh2 of the cut
+            if (a.sh2 == 0) {
+                thr = pre;
+            } else {
+                const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+                for (uint32_t k = gtid; k < nc; k += G) {
+                    const uint32_t v = a.c_id[k];
+                    if ((v >> a.sh2) == pre) atomicAdd(&sm.rh[v & ((1u << a.sh2) - 1)], 1);
+                }
+                hist_flush(sm.rh, (int32_t*)a.rh + 4096, 1024);
+                grid_sync(a.bar);
+                const uint32_t d3 = hist_select(a.rh + 4096, 1u << a.sh2, left, &left, sm);
+                thr = (pre << a.sh2) | d3;
+            }
+        }
+        IPHASE(a, 4);
+
+        // final: b*'s last evictions (sel 1: ids above the cut), then every
+        // insertion still without a slot -- b*'s admissions (tickets after the
+        // certain ones) and the certain insertions deferred in P3
+        if (sel == 1) {
+            const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+            for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < nc; k0 += G) {  // CTA-uniform
+                const uint32_t k = k0 + tid;
+                const bool ev = k < nc && a.c_id[k] > thr;
+                if (ev) atomicSub(&sm.hinc[bstar], 1);
+                stage_put(st_ev, ev, 0, ev ? a.c_ref[k] : 0u);
+                __syncthreads();
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10]);
+            }
+            __syncthreads();
+            ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10]);
+        }
+        if (admit_new) {
+            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {  // CTA-uniform
+                const uint32_t pos = p0 + tid;
+                bool f = false;
+                if (pos < c1 && a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar)
+                    f = sel != 2 || a.trace[base + pos] <= thr;
+                uint32_t tot;
+                const uint32_t ex = block_excl_scan((uint32_t)f, sm.scan, tot);
+                if (tid == 0 && tot) sm.bc[11] = atomicAdd(&cs->n_ins, tot);
+                __syncthreads();
+                if (f) {
+                    const uint32_t t = sm.bc[11] + ex;
+                    place_ins(a, sm, base + pos, a.pkey[pos], t < n_out ? take_slot(a.ev_slot, t) : nres + (t - n_out), S);
+                }
+            }
+        }
+        for (uint32_t t = n_out_p3 + gtid; t < min(new_before, n_out); t += G) {
+            const uint32_t x = a.ins_x[t];
+            place_ins(a, sm, x, a.pkey[x - base], take_slot(a.ev_slot, t), S);
+        }
+        hist_flush(sm.hinc, a.hist_inc, S + 1);
+        for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+        if (gtid == 0) {
+            if (n_out > n_in) atomicOr(&a.st->err, 4u);
+            cs->exp_out = n_out;
+            cs->exp_in = n_in;
+            a.o_misses[i] = m;
+            ns->n_res = nres + n_in - n_out;
+            ns->in_total = in_total + n_in;
+            ns->out_total = out_total + n_out;
+            ns->n_out = 0;
+            ns->n_c = 0;
+            ns->n_ins = 0;
+            a.o_in_off[i + 1] = in_total + n_in;
+            a.o_out_off[i + 1] = out_total + n_out;
+        }
+        grid_sync(a.bar);
+        IPHASE(a, 5);
+    }
+    if (S > 0 && gtid == 0) {
+        const volatile IState* ls = a.st + ((S - 1) & 1);
+        if (ls->n_out != ls->exp_out || ls->n_ins != ls->exp_in) atomicOr(&a.st->err, 8u);
+    }
+}
+
 // The inspector is two cooperative launches over one body. PART 0 (first uses,
 // init set, and the whole all-fit case) runs two 512-thread CTAs per SM: its
 // passes are random node-array accesses that want warps in flight (1.04 vs
@@ -504,6 +953,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                             const uint32_t it = iter_of(sm, S, x);
                             a.slot_node[r] = v;
                             a.slot_key[r] = it;
+                            if (a.slot_tag) a.slot_tag[r] = r;  // occupancy tag of an init slot: the slot
                             atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                         }
                         if (fit) {
@@ -534,6 +984,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         const uint32_t it = iter_of(sm, S, x);
                         a.slot_node[k] = v;
                         a.slot_key[k] = it;
+                        if (a.slot_tag) a.slot_tag[k] = (uint32_t)k;
                         a.node_slot[v] = k;
                         a.o_init[k] = v;
                         atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
@@ -625,7 +1076,8 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     // ---- the recurrence -------------------------------------------------------
     // State counters are double-buffered by iteration parity: iteration i reads
     // st[i&1] and CTA 0 writes st[(i+1)&1] in the iteration's last grid step.
-    for (uint32_t i = 0; i < S; ++i) {
+    if (a.defer) recurrence_deferred<CAP>(a, sm);
+    for (uint32_t i = 0; !a.defer && i < S; ++i) {
         IPHASE(a, 0);
         IState* cs = a.st + (i & 1);
         IState* ns = a.st + ((i + 1) & 1);
@@ -1157,6 +1609,126 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect_rec(IArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_finish_changesets: the ordered changesets of a deferred recurrence.
+//  1. in-lists: the inserted accesses in trace order ARE the reference's
+//     in_ids / in_positions (iteration-major, position order within an
+//     iteration, finish_selection changeset.hpp:211-216) -- one compaction.
+//  2. out-lists were sorted by id per iteration before this kernel (segmented
+//     sort of the raw out tickets, carrying each evicted occupancy's tag).
+//  3. slots (feature_cache.hpp:114-129): the k-th insertion of iteration i
+//     reuses the slot of out_i[k] -- the slot its occupancy got when it was
+//     inserted (a pointer to an earlier insertion) or its init slot -- and
+//     the rest take n_res_i, n_res_i + 1, ...; the pointers are resolved by
+//     pointer jumping (chains are at most S long: log2 S rounds).
+//  4. every hit's occupancy tag becomes that occupancy's slot (acc_slot).
+// ---------------------------------------------------------------------------
+struct FArgs {
+    const uint32_t* trace;
+    const uint32_t* toff;     // S+1
+    const uint8_t* isin;      // A
+    uint32_t* acc_slot;       // A: tags of hits -> slots
+    uint32_t* R;              // A: per inserted access, its slot (or kEv | parent access)
+    const uint32_t* in_off;   // S+1
+    const uint32_t* out_off;  // S+1
+    const uint32_t* out_tag;  // sorted out tags
+    uint32_t* o_in_ids;
+    uint32_t* o_in_pos;
+    uint32_t* o_in_slot;
+    uint32_t* tile_cnt;
+    uint32_t* unres;          // 64 per-round unresolved counters (host-zeroed)
+    uint32_t S, A, n_in, n0;
+    GridBarrier* bar;
+};
+constexpr int FIN_THREADS = 512;
+constexpr uint32_t FIN_TILE = FIN_THREADS * 4;
+
+__global__ void __launch_bounds__(FIN_THREADS) k_finish_changesets(FArgs f) {
+    __shared__ uint32_t scan[34];
+    __shared__ uint32_t toff[kMaxIters + 1];
+    const uint32_t tid = threadIdx.x, G = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + tid;
+    for (uint32_t i = tid; i <= f.S; i += blockDim.x) toff[i] = f.toff[i];
+    const uint32_t ntiles = (f.A + FIN_TILE - 1) / FIN_TILE;
+    // 1. inserted accesses per tile
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint32_t c = 0;
+        const uint32_t x0 = t * FIN_TILE + tid * 4;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) c += x0 + j < f.A ? f.isin[x0 + j] : 0u;
+        c = block_sum(c, scan);
+        if (tid == 0) f.tile_cnt[t] = c;
+    }
+    grid_sync(f.bar);
+    if (blockIdx.x == 0) {  // exclusive scan of the tile counts
+        uint32_t carry = 0;
+        for (uint32_t b0 = 0; b0 < ntiles; b0 += blockDim.x) {
+            const uint32_t t = b0 + tid;
+            const uint32_t v = t < ntiles ? f.tile_cnt[t] : 0u;
+            uint32_t tot;
+            const uint32_t ex = block_excl_scan(v, scan, tot);
+            if (t < ntiles) f.tile_cnt[t] = carry + ex;
+            carry += tot;
+        }
+    }
+    grid_sync(f.bar);
+    // 2. in-list entries and the slot (or parent) of every insertion
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint32_t x0 = t * FIN_TILE + tid * 4;
+        uint32_t fl[4], c = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            fl[j] = x0 + j < f.A ? f.isin[x0 + j] : 0u;
+            c += fl[j];
+        }
+        uint32_t tot;
+        uint32_t g = f.tile_cnt[t] + block_excl_scan(c, scan, tot);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            if (!fl[j]) continue;
+            const uint32_t x = x0 + j;
+            uint32_t lo = 0, hi = f.S;  // iteration of x: toff[lo] <= x < toff[lo + 1]
+            while (hi - lo > 1) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if (toff[mid] <= x) lo = mid;
+                else hi = mid;
+            }
+            const uint32_t i = lo;
+            const uint32_t ib = f.in_off[i], ob = f.out_off[i], nout = f.out_off[i + 1] - ob;
+            const uint32_t k = g - ib;
+            f.o_in_ids[g] = f.trace[x];
+            f.o_in_pos[g] = x - toff[i];
+            f.o_in_slot[g] = x;  // the access, until the slots are resolved
+            f.R[x] = k < nout ? f.out_tag[ob + k] : f.n0 + ib - ob + (k - nout);
+            ++g;
+        }
+    }
+    grid_sync(f.bar);
+    // 3. pointer jumping: R[x] always points at an ancestor on x's chain (or is
+    // the root's slot), so concurrent updates stay valid
+    for (uint32_t round = 0; round < 64; ++round) {
+        uint32_t open = 0;
+        for (uint32_t g = gtid; g < f.n_in; g += G) {
+            const uint32_t x = f.o_in_slot[g];
+            const uint32_t r = f.R[x];
+            if (r & kEv) {
+                const uint32_t r2 = f.R[r & ~kEv];
+                f.R[x] = r2;
+                open |= (r2 & kEv) ? 1u : 0u;
+            }
+        }
+        open = __syncthreads_or(open);
+        if (tid == 0 && open) atomicAdd(&f.unres[round], 1u);
+        grid_sync(f.bar);
+        if (*(volatile uint32_t*)&f.unres[round] == 0) break;
+    }
+    // 4. in-list slots; hits' tags -> slots
+    for (uint32_t g = gtid; g < f.n_in; g += G) f.o_in_slot[g] = f.R[f.o_in_slot[g]];
+    for (uint32_t x = gtid; x < f.A; x += G) {
+        const uint32_t t = f.acc_slot[x];
+        if (t != kNever && (t & kEv)) f.acc_slot[x] = f.R[t & ~kEv];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
 
@@ -1259,6 +1831,16 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.c_ref.reserve(std::max(Keff, maxw));
     B.in_node.reserve(maxw);
     B.in_pos.reserve(maxw);
+    static const bool defer = env_int("GX_INSPECT_DEFER", 1) != 0;
+    if (defer) {
+        B.slot_tag.reserve(Keff + 1);
+        B.out_raw.reserve(A + 1);
+        B.out_tagraw.reserve(A + 1);
+        B.tag_sorted.reserve(A + 1);
+        B.ev_slot.reserve(maxw);
+        GX_CUDA(cudaMemsetAsync(B.ev_slot.p, 0xff, maxw * 4, st));  // every ticket "not yet published"
+        B.ins_x.reserve(maxw);
+    }
     // PART 1 (recurrence) grid: one CTA per SM, or ONE CTA for narrow traces --
     // an iteration of <= 4096 accesses against <= 16384 slots is a few dozen
     // elements per thread, and the CTA barrier replaces every grid barrier
@@ -1269,9 +1851,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     const int grid0 = ctx->num_sms * GX_IN_FRONT_BPS;                                      // PART 0
     B.chunk_cnt.reserve(2 * std::max(grid, grid0));
     B.bm_cnt.reserve(std::max(grid, grid0));
-    B.st.reserve(16);
+    B.st.reserve(32);
     GX_CUDA(cudaMemsetAsync(B.st.p, 0, 2 * sizeof(IState), st));
-    static_assert(2 * sizeof(IState) <= 16 * sizeof(uint32_t), "2 IStates fit the scratch words");
+    static_assert(2 * sizeof(IState) <= 32 * sizeof(uint32_t), "2 IStates fit the scratch words");
     B.isfirst.reserve(std::max<uint64_t>(A, 1));
     // per-node iteration bitmask (next use in 3 grid steps) when it fits the budget
     const uint64_t W = (S + 63) / 64;
@@ -1399,6 +1981,12 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.o_out_off = d_out_off.p;
     a.st = reinterpret_cast<IState*>(B.st.p);
     a.bar = ctx->barrier.p;
+    a.defer = defer;
+    a.slot_tag = defer ? B.slot_tag.p : nullptr;
+    a.out_raw = B.out_raw.p;
+    a.out_tagraw = B.out_tagraw.p;
+    a.ev_slot = B.ev_slot.p;
+    a.ins_x = B.ins_x.p;
     static const bool tracing = std::getenv("GX_INSPECT_TRACE") != nullptr;
     static DevBuf<unsigned long long> tbuf;
     static PinBuf<unsigned long long> htb;
@@ -1504,6 +2092,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         if (htb.p[30] + htb.p[31]) {
             std::fprintf(stderr, " | allin=%llu cut=%llu phases(us):", htb.p[30], htb.p[31]);
             const char* nm[8] = {"", "P1", "allin", "P3", "select", "P4", "P5", "P6"};
+            if (defer) nm[5] = "final";
             for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.1f", nm[k], htb.p[16 + k] / 1e3);
         }
         std::fprintf(stderr, "\n");
@@ -1517,6 +2106,60 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         host_trace_error(flat, off, N);
     }
     if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");
+    const bool recurrence_ran = !(n_init_explicit < 0 && hs.n_first <= Keff);
+    if (defer && recurrence_ran && io32[S] > 0) {
+        // ordered out lists: segmented sort of the raw out tickets by node id
+        const uint32_t n_out_all = oo32[S];
+        if (n_out_all) {
+            size_t tb = 0;
+            GX_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, B.out_raw.p, out->out_ids.p, B.out_tagraw.p,
+                                                        B.tag_sorted.p, (int)n_out_all, (int)S, d_out_off.p,
+                                                        d_out_off.p + 1, st));
+            B.sort_tmp.reserve(tb + 16);
+            GX_CUDA(cub::DeviceSegmentedSort::SortPairs(B.sort_tmp.p, tb, B.out_raw.p, out->out_ids.p,
+                                                        B.out_tagraw.p, B.tag_sorted.p, (int)n_out_all, (int)S,
+                                                        d_out_off.p, d_out_off.p + 1, st));
+        }
+        B.fin_unres.reserve(64);
+        GX_CUDA(cudaMemsetAsync(B.fin_unres.p, 0, 64 * 4, st));
+        FArgs fa{};
+        fa.trace = is.trace.p;
+        fa.toff = B.toff.p;
+        fa.isin = B.isfirst.p;
+        fa.acc_slot = is.acc_slot.p;
+        fa.R = is.next_use.p;  // next use is dead after the recurrence
+        fa.in_off = d_in_off.p;
+        fa.out_off = d_out_off.p;
+        fa.out_tag = B.tag_sorted.p;
+        fa.o_in_ids = out->in_ids.p;
+        fa.o_in_pos = out->in_pos.p;
+        fa.o_in_slot = out->in_slot.p;
+        fa.tile_cnt = B.tile_cnt.p;
+        fa.unres = B.fin_unres.p;
+        fa.S = (uint32_t)S;
+        fa.A = (uint32_t)A;
+        fa.n_in = io32[S];
+        fa.n0 = n_init_explicit >= 0 ? (uint32_t)n_init_explicit : (uint32_t)std::min<uint64_t>(hs.n_first, Keff);
+        fa.bar = ctx->barrier.p;
+        static PerDevice<int> fin_bps;
+        int bps = 0;
+        {
+            auto lk = fin_bps.lock();
+            int& c = fin_bps.at(ctx->device);
+            if (c < 1) GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c, k_finish_changesets, FIN_THREADS, 0));
+            if (c < 1) fail(GX_CUDA_ERROR, "finish kernel cannot be resident");
+            bps = std::min(c, 2);
+        }
+        const uint32_t need = (uint32_t)((A + FIN_TILE - 1) / FIN_TILE);
+        B.tile_cnt.reserve(need + 1);
+        fa.tile_cnt = B.tile_cnt.p;
+        void* fargs[] = {&fa};
+        barrier_reset(fa.bar, st);
+        const dim3 fg(ctx->num_sms * bps);
+        if (coop_launch()) GX_CUDA(cudaLaunchCooperativeKernel((void*)k_finish_changesets, fg, dim3(FIN_THREADS), fargs, 0, st));
+        else GX_CUDA(cudaLaunchKernel((void*)k_finish_changesets, fg, dim3(FIN_THREADS), fargs, 0, st));
+        GX_CHECK_LAUNCH();
+    }
     out->n_init = n_init_explicit >= 0 ? (uint64_t)n_init_explicit : std::min<uint64_t>(hs.n_first, Keff);
     // all-fit with marks: first_acc and the rest lists (or the fan-out lists) are valid
     out->first_marked = (a.o_first != nullptr || a.o_fan_cnt != nullptr) && hs.n_first <= Keff;
