@@ -127,6 +127,14 @@ struct IArgs {
     uint32_t* out_tagraw;  // A: the evicted occupancy's tag
     uint32_t* ev_slot;     // maxw: internal slot freed by eviction ticket t (kNever = not yet)
     uint32_t* ins_x;       // maxw: access of a certain insertion whose eviction comes later
+    // dense node keys (trusted traces, deferred recurrence): a node is keyed by
+    // the rank of its first access among first accesses (< n_first, the init
+    // order), so node_slot / the next-use bitmask / `last` touch an n_first-sized
+    // prefix (L2-sized) instead of N-sized arrays. PART 0 leaves the key of each
+    // first access in acc_slot; PART 1 spreads it to every access.
+    int dense;
+    uint32_t* slot_nk;     // K: node key of each internal slot's occupant (node id when !dense)
+    uint32_t* pnk;         // maxw: node key of each missed position of the iteration
 };
 
 constexpr uint32_t kEv = 0x80000000u;  // tag bit: the occupancy began at access (tag & ~kEv)
@@ -442,10 +450,9 @@ __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, u
     for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
         const uint32_t s = (uint32_t)st.buf[k];
         const uint32_t t = base + k;
-        const uint32_t u = a.slot_node[s];
-        a.out_raw[out_total + t] = u;
+        a.out_raw[out_total + t] = a.slot_node[s];
         a.out_tagraw[out_total + t] = a.slot_tag[s];
-        a.node_slot[u] = -1;
+        a.node_slot[a.slot_nk[s]] = -1;
         st_release_u32(a.ev_slot + t, s);
     }
     __syncthreads();
@@ -455,12 +462,13 @@ __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, u
 
 // a missed access x enters internal slot s with key `key`
 template <class SM>
-__device__ __forceinline__ void place_ins(const IArgs& a, SM& sm, uint32_t x, uint32_t key, uint32_t s, uint32_t S) {
-    const uint32_t v = a.trace[x];
-    a.slot_node[s] = v;
+__device__ __forceinline__ void place_ins(const IArgs& a, SM& sm, uint32_t x, uint32_t key, uint32_t nk, uint32_t s,
+                                          uint32_t S) {
+    a.slot_node[s] = a.trace[x];
     a.slot_key[s] = key;
     a.slot_tag[s] = kEv | x;
-    a.node_slot[v] = (int32_t)s;
+    a.slot_nk[s] = nk;
+    a.node_slot[nk] = (int32_t)s;
     atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
     a.isfirst[x] = 1;  // (isfirst doubles as the inserted-access flag in PART 1)
 }
@@ -555,9 +563,9 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             uint32_t miss = 0, hits = 0;
             for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) {
                 const uint32_t x = base + pos;
-                const uint32_t v = a.trace[x];
+                const uint32_t nk = a.dense ? a.acc_slot[x] : a.trace[x];
                 const uint32_t nu = a.next_use[x];
-                const int32_t s = a.node_slot[v];
+                const int32_t s = a.node_slot[nk];
                 a.isfirst[x] = 0;
                 if (s >= 0) {
                     a.slot_key[s] = nu;
@@ -568,6 +576,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 } else {
                     a.pmiss[pos] = 1;
                     a.pkey[pos] = nu;
+                    a.pnk[pos] = nk;
                     a.acc_slot[x] = kNever;
                     atomicAdd(&sm.hnew[bucket_of(nu, S)], 1);
                     ++miss;
@@ -604,7 +613,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 const uint32_t f = pos < c1 ? a.pmiss[pos] : 0;
                 uint32_t tot;
                 const uint32_t ex = block_excl_scan(f, sm.scan, tot);
-                if (f) place_ins(a, sm, base + pos, a.pkey[pos], nres + k + ex, S);
+                if (f) place_ins(a, sm, base + pos, a.pkey[pos], a.pnk[pos], nres + k + ex, S);
                 k += tot;
             }
             hist_flush(sm.hinc, a.hist_inc, S + 1);
@@ -719,9 +728,10 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 __syncthreads();
                 if (f) {
                     const uint32_t t = sm.bc[11] + ex;
-                    if (t < n_out_p3) place_ins(a, sm, base + pos, key, take_slot(a.ev_slot, t), S);
+                    const uint32_t nk = a.pnk[pos];
+                    if (t < n_out_p3) place_ins(a, sm, base + pos, key, nk, take_slot(a.ev_slot, t), S);
                     else if (t < n_out) a.ins_x[t] = base + pos;  // its slot is freed after the select
-                    else place_ins(a, sm, base + pos, key, nres + (t - n_out), S);
+                    else place_ins(a, sm, base + pos, key, nk, nres + (t - n_out), S);
                 }
             }
         }
@@ -797,13 +807,14 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 __syncthreads();
                 if (f) {
                     const uint32_t t = sm.bc[11] + ex;
-                    place_ins(a, sm, base + pos, a.pkey[pos], t < n_out ? take_slot(a.ev_slot, t) : nres + (t - n_out), S);
+                    place_ins(a, sm, base + pos, a.pkey[pos], a.pnk[pos],
+                              t < n_out ? take_slot(a.ev_slot, t) : nres + (t - n_out), S);
                 }
             }
         }
         for (uint32_t t = n_out_p3 + gtid; t < min(new_before, n_out); t += G) {
             const uint32_t x = a.ins_x[t];
-            place_ins(a, sm, x, a.pkey[x - base], take_slot(a.ev_slot, t), S);
+            place_ins(a, sm, x, a.pkey[x - base], a.pnk[x - base], take_slot(a.ev_slot, t), S);
         }
         hist_flush(sm.hinc, a.hist_inc, S + 1);
         for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
@@ -827,6 +838,59 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
     if (S > 0 && gtid == 0) {
         const volatile IState* ls = a.st + ((S - 1) & 1);
         if (ls->n_out != ls->exp_out || ls->n_ins != ls->exp_in) atomicOr(&a.st->err, 8u);
+    }
+}
+
+// PART 1 next use of a trusted trace with dense node keys: every access takes
+// its key from its first access (next_use holds that access index after PART
+// 0), then the next use comes from an n_first x W iteration bitmask (or the
+// backward pass over `last`), both indexed by the key -- an L2-sized footprint
+// instead of N x W words.
+template <class SM>
+__device__ void next_use_dense(const IArgs& a, SM& sm) {
+    const uint32_t S = a.S;
+    const uint32_t G = gridDim.x * blockDim.x;
+    const uint32_t gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t x = gtid; x < a.A; x += G) {
+        const uint32_t fx = a.next_use[x];
+        const uint32_t d = a.acc_slot[fx];
+        if (fx != x) a.acc_slot[x] = d;
+        if (a.use_bits == 1) {
+            const uint32_t i = iter_of(sm, S, x);
+            atomicOr(&a.bits[(uint64_t)d * a.W + (i >> 6)], 1ull << (i & 63));
+        }
+    }
+    grid_sync(a.bar);
+    if (a.use_bits == 1) {
+        for (uint32_t x = gtid; x < a.A; x += G) {
+            const uint32_t i = iter_of(sm, S, x);
+            const unsigned long long* w = a.bits + (uint64_t)a.acc_slot[x] * a.W;
+            uint32_t nu = kNever;
+            for (uint32_t q = i >> 6; q < a.W; ++q) {
+                const unsigned long long word = w[q];
+                const unsigned long long above =
+                    q == (i >> 6) ? ((i & 63) == 63 ? 0ull : word & (~0ull << ((i & 63) + 1))) : word;
+                if (above) {
+                    nu = q * 64 + __ffsll((long long)above) - 1;
+                    break;
+                }
+            }
+            a.next_use[x] = nu;
+        }
+        grid_sync(a.bar);
+        for (uint32_t x = gtid; x < a.A; x += G) {  // leave the bitmask clean (once per node)
+            if (!a.isfirst[x]) continue;
+            unsigned long long* w = a.bits + (uint64_t)a.acc_slot[x] * a.W;
+            for (uint32_t q = 0; q < a.W; ++q) w[q] = 0;
+        }
+    } else {
+        for (int i = (int)S - 1; i >= 0; --i) {  // one grid step per iteration
+            for (uint32_t x = sm.toff[i] + gtid; x < sm.toff[i + 1]; x += G)
+                a.next_use[x] = atomicExch(&a.last[a.acc_slot[x]], (uint32_t)i);
+            grid_sync(a.bar);
+        }
+        for (uint32_t x = gtid; x < a.A; x += G)
+            if (a.isfirst[x]) a.last[a.acc_slot[x]] = kNever;  // leave clean
     }
 }
 
@@ -948,12 +1012,16 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                 if (fl[j]) {
                     const uint32_t x = x0 + j;
                     const uint32_t v = a.trace[x];
+                    if (a.dense && !fit) a.acc_slot[x] = r;  // dense node key (every first access)
                     if (r < K) {
                         if (!(fit && a.trusted)) {  // recurrence state (and the untrusted cleanup)
                             const uint32_t it = iter_of(sm, S, x);
                             a.slot_node[r] = v;
                             a.slot_key[r] = it;
-                            if (a.slot_tag) a.slot_tag[r] = r;  // occupancy tag of an init slot: the slot
+                            if (a.slot_tag) {
+                                a.slot_tag[r] = r;  // occupancy tag of an init slot: the slot
+                                a.slot_nk[r] = a.dense ? r : v;
+                            }
                             atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
                         }
                         if (fit) {
@@ -961,7 +1029,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                             if (a.o_first) a.o_first[r] = x;
                             if (a.o_fan_cnt) a.o_fan_cnt[r] = 0;  // the other accesses are counted below
                         } else {
-                            a.node_slot[v] = (int32_t)r;
+                            a.node_slot[a.dense ? r : v] = (int32_t)r;
                         }
                         a.o_init[r] = v;
                     }
@@ -984,7 +1052,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                         const uint32_t it = iter_of(sm, S, x);
                         a.slot_node[k] = v;
                         a.slot_key[k] = it;
-                        if (a.slot_tag) a.slot_tag[k] = (uint32_t)k;
+                        if (a.slot_tag) {
+                            a.slot_tag[k] = (uint32_t)k;
+                            a.slot_nk[k] = v;
+                        }
                         a.node_slot[v] = k;
                         a.o_init[k] = v;
                         atomicAdd(&sm.hinc[bucket_of(it, S)], 1);
@@ -1067,7 +1138,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     if (*(volatile uint32_t*)&a.st->err) return;  // PART 0 found a bad trace (the host reports it)
     if (!a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K) return;  // all-fit: done
     const bool have_next = !a.trusted;  // untrusted traces computed next use in PART 0
-    if (!have_next) next_use_pass(a, sm, false);
+    if (!have_next) {
+        if (a.dense) next_use_dense(a, sm);
+        else next_use_pass(a, sm, false);
+    }
     if (a.tstamp) {  // tracing only: the recurrence needs no barrier here
         grid_sync(a.bar);
         ISTAMP(a, 6);
@@ -1595,7 +1669,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     ISTAMP(a, 7);
     // leave node_slot clean
     const uint32_t nfin = a.st[S & 1].n_res;
-    for (uint32_t s = gtid; s < nfin; s += G) a.node_slot[a.slot_node[s]] = -1;
+    for (uint32_t s = gtid; s < nfin; s += G) a.node_slot[a.defer ? a.slot_nk[s] : a.slot_node[s]] = -1;
     if (gtid == 0) a.st->n_res = nfin;  // final resident count for the host
 }
 
@@ -1840,6 +1914,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         B.ev_slot.reserve(maxw);
         GX_CUDA(cudaMemsetAsync(B.ev_slot.p, 0xff, maxw * 4, st));  // every ticket "not yet published"
         B.ins_x.reserve(maxw);
+        B.slot_nk.reserve(Keff + 1);
+        B.pnk.reserve(maxw);
     }
     // PART 1 (recurrence) grid: one CTA per SM, or ONE CTA for narrow traces --
     // an iteration of <= 4096 accesses against <= 16384 slots is a few dozen
@@ -1987,6 +2063,18 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.out_tagraw = B.out_tagraw.p;
     a.ev_slot = B.ev_slot.p;
     a.ins_x = B.ins_x.p;
+    a.slot_nk = B.slot_nk.p;
+    a.pnk = B.pnk.p;
+    a.dense = defer && a.trusted;
+    // dense keys: the bitmask (3 grid passes over an n_first x W prefix) by
+    // default; GX_DENSE_NEXT=last: one grid step per iteration over the
+    // L2-resident `last` prefix (measured cfg1 357 vs 220 us, papers@5 % 905 vs
+    // 931 us: not kept as the default)
+    static const bool dense_last = [] {
+        const char* e = std::getenv("GX_DENSE_NEXT");
+        return e && std::string(e) == "last";
+    }();
+    if (a.dense && dense_last) a.use_bits = 0;
     static const bool tracing = std::getenv("GX_INSPECT_TRACE") != nullptr;
     static DevBuf<unsigned long long> tbuf;
     static PinBuf<unsigned long long> htb;
