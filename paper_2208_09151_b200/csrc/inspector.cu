@@ -135,6 +135,14 @@ struct IArgs {
     int dense;
     uint32_t* slot_nk;     // K: node key of each internal slot's occupant (node id when !dense)
     uint32_t* pnk;         // maxw: node key of each missed position of the iteration
+    // NEVER members (occupancies keyed "no further access"; they only leave by
+    // eviction, largest ids first when b* is the NEVER bucket): their top-digit
+    // histogram and, per 16-slot block, 1 + the largest NEVER id (stale-high
+    // allowed) are maintained across iterations, so a cut inside NEVER knows its
+    // first digit after P1 and scans only the blocks that can hold ids >= it
+    int nv;
+    int32_t* never_hist;   // 2048
+    uint32_t* blk_max;     // ceil(K / 16)
 };
 
 constexpr uint32_t kEv = 0x80000000u;  // tag bit: the occupancy began at access (tag & ~kEv)
@@ -241,6 +249,8 @@ struct ISmem {
     int32_t hinc[CAP + 1];  // per-CTA histogram deltas, flushed with one atomic per bin
     int32_t hnew[CAP + 1];
     int32_t rh[2048];       // per-CTA radix-select digit histogram
+    int32_t nh[2048];       // deferred recurrence: NEVER-member digit-histogram deltas
+    uint32_t fbl[IN_THREADS];  // flagged slot blocks of one pass (NEVER fast path)
 };
 
 __device__ __forceinline__ void hist_flush(int32_t* loc, int32_t* glob, uint32_t n) {
@@ -440,7 +450,7 @@ __device__ __forceinline__ uint32_t take_slot(uint32_t* ev_slot, uint32_t t) {
 // its node and occupancy tag go to the iteration's raw out list, the node
 // leaves the cache, and slot s is published as ev_slot[t].
 __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, uint32_t out_total, bool force,
-                                         uint32_t* bcast) {
+                                         uint32_t* bcast, int32_t* nh) {
     const uint32_t n = *st.cnt;
     __syncthreads();
     if (n == 0 || (!force && n < 1024)) return;
@@ -450,9 +460,11 @@ __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, u
     for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
         const uint32_t s = (uint32_t)st.buf[k];
         const uint32_t t = base + k;
-        a.out_raw[out_total + t] = a.slot_node[s];
+        const uint32_t u = a.slot_node[s];
+        a.out_raw[out_total + t] = u;
         a.out_tagraw[out_total + t] = a.slot_tag[s];
         a.node_slot[a.slot_nk[s]] = -1;
+        if (nh && a.slot_key[s] == kNever) atomicSub(&nh[u >> a.sh1], 1);
         st_release_u32(a.ev_slot + t, s);
     }
     __syncthreads();
@@ -464,11 +476,16 @@ __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, u
 template <class SM>
 __device__ __forceinline__ void place_ins(const IArgs& a, SM& sm, uint32_t x, uint32_t key, uint32_t nk, uint32_t s,
                                           uint32_t S) {
-    a.slot_node[s] = a.trace[x];
+    const uint32_t v = a.trace[x];
+    a.slot_node[s] = v;
     a.slot_key[s] = key;
     a.slot_tag[s] = kEv | x;
     a.slot_nk[s] = nk;
     a.node_slot[nk] = (int32_t)s;
+    if (a.nv && key == kNever) {
+        atomicAdd(&sm.nh[v >> a.sh1], 1);
+        atomicMax(&a.blk_max[s >> 4], v + 1);
+    }
     atomicAdd(&sm.hinc[bucket_of(key, S)], 1);
     a.isfirst[x] = 1;  // (isfirst doubles as the inserted-access flag in PART 1)
 }
@@ -478,7 +495,8 @@ __device__ __forceinline__ void place_ins(const IArgs& a, SM& sm, uint32_t x, ui
 // per pass with their keys loaded together.
 template <int PI, class SM>
 __device__ __forceinline__ void p3_scan(const IArgs& a, SM& sm, uint32_t nres, uint32_t bstar, bool evict_b,
-                                        bool memb, Stage st_ev, IState* cs, uint32_t out_total, uint32_t S) {
+                                        bool memb, Stage st_ev, IState* cs, uint32_t out_total, uint32_t S,
+                                        bool collect = false, Stage st_c = Stage{}) {
     const uint32_t G = gridDim.x * blockDim.x;
     for (uint32_t s0 = blockIdx.x * blockDim.x * PI; s0 < nres; s0 += G * PI) {  // CTA-uniform trip count
         uint32_t bk[PI];
@@ -491,12 +509,18 @@ __device__ __forceinline__ void p3_scan(const IArgs& a, SM& sm, uint32_t nres, u
         for (int j = 0; j < PI; ++j) {
             const uint32_t s = s0 + j * blockDim.x + threadIdx.x;
             const bool ev = s < nres && (bk[j] > bstar || (bk[j] == bstar && evict_b));
-            if (s < nres && memb && bk[j] == bstar) atomicAdd(&sm.rh[a.slot_node[s] >> a.sh1], 1);
+            const bool mem = s < nres && memb && bk[j] == bstar;
             if (ev) atomicSub(&sm.hinc[bk[j]], 1);
             stage_put(st_ev, ev, 0, s);
+            if (collect) {  // small b*: every member to c_id (the select runs locally)
+                stage_put(st_c, mem, mem ? a.slot_node[s] : 0u, s);
+            } else if (mem) {
+                atomicAdd(&sm.rh[a.slot_node[s] >> a.sh1], 1);
+            }
             if (PI == 1 || (j & 1)) {
                 __syncthreads();
-                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10]);
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], a.nv ? sm.nh : nullptr);
+                if (collect) stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
             }
         }
     }
@@ -527,10 +551,101 @@ __device__ __forceinline__ void p3b_scan(const IArgs& a, SM& sm, uint32_t nres, 
             stage_put(st_c, c, v, s);
             if (PI == 1 || (j & 1)) {
                 __syncthreads();
-                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10]);
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], a.nv ? sm.nh : nullptr);
                 stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
             }
         }
+    }
+}
+
+// Local radix select (every CTA redundantly, no grid barrier): the rank-th
+// smallest (1-based) id among c_id[0..nc), nc <= kLocalSel -- all candidates of
+// a small b* (from_d1 = false), or those of the NEVER fast path, which all share
+// the first digit d1 (from_d1 = true, rank counted inside d1). The ids sit in
+// the candidate stage's area (free once P3 flushed it).
+constexpr uint32_t kLocalSel = 4096;
+template <class SM>
+__device__ uint32_t local_select(const IArgs& a, SM& sm, uint32_t nc, uint32_t rank, bool from_d1, uint32_t d1) {
+    uint32_t* ids = reinterpret_cast<uint32_t*>(sm.sortbuf + 2048);
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t k = tid; k < nc; k += blockDim.x) ids[k] = __ldcg(a.c_id + k);
+    for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+    __syncthreads();
+    uint32_t left = rank;
+    if (!from_d1) {
+        for (uint32_t k = tid; k < nc; k += blockDim.x) atomicAdd(&sm.rh[ids[k] >> a.sh1], 1);
+        __syncthreads();
+        d1 = hist_select((const uint32_t*)sm.rh, 2048, rank, &left, sm);
+        for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+        __syncthreads();
+    }
+    for (uint32_t k = tid; k < nc; k += blockDim.x) {
+        const uint32_t v = ids[k];
+        if ((v >> a.sh1) == d1) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
+    }
+    __syncthreads();
+    const uint32_t d2 = hist_select((const uint32_t*)sm.rh, 2048, left, &left, sm);
+    const uint32_t pre = (d1 << (a.sh1 - a.sh2)) | d2;
+    for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+    __syncthreads();
+    if (a.sh2 == 0) return pre;
+    for (uint32_t k = tid; k < nc; k += blockDim.x) {
+        const uint32_t v = ids[k];
+        if ((v >> a.sh2) == pre) atomicAdd(&sm.rh[v & ((1u << a.sh2) - 1)], 1);
+    }
+    __syncthreads();
+    const uint32_t d3 = hist_select((const uint32_t*)sm.rh, 1u << a.sh2, left, &left, sm);
+    for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+    __syncthreads();
+    return (pre << a.sh2) | d3;
+}
+
+// NEVER fast path of P3 (b* = NEVER, sel 1): NEVER members whose first digit
+// is above d1 leave, those on d1 become candidates; only 16-slot blocks whose
+// summary max can reach d1 are read, and each read block's summary is
+// refreshed (no NEVER-keyed placement runs in such an iteration: certain
+// insertions key below b* = NEVER and nothing of b* is admitted).
+template <class SM>
+__device__ __forceinline__ void never_scan(const IArgs& a, SM& sm, uint32_t nres, uint32_t d1, Stage st_ev,
+                                           Stage st_c, IState* cs, uint32_t out_total, uint32_t S) {
+    const uint32_t G = gridDim.x * blockDim.x, tid = threadIdx.x;
+    const uint32_t nblk = (nres + 15) / 16;
+    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < nblk; b0 += G) {  // CTA-uniform
+        const uint32_t blk = b0 + tid;
+        bool f = false;
+        if (blk < nblk) {
+            const uint32_t mx = a.blk_max[blk];
+            f = mx && ((mx - 1) >> a.sh1) >= d1;
+        }
+        uint32_t tot;
+        const uint32_t ex = block_excl_scan((uint32_t)f, sm.scan, tot);
+        if (f) sm.fbl[ex] = blk;
+        __syncthreads();
+        for (uint32_t g0 = 0; g0 < tot; g0 += blockDim.x / 16) {  // CTA-uniform: 16 lanes per block
+            const uint32_t gi = g0 + tid / 16;
+            bool ev = false, c = false;
+            uint32_t v = 0, sl = 0, keep = 0;
+            if (gi < tot) {
+                sl = sm.fbl[gi] * 16 + (tid & 15);
+                if (sl < nres && a.slot_key[sl] == kNever) {
+                    v = a.slot_node[sl];
+                    const uint32_t dg = v >> a.sh1;
+                    ev = dg > d1;
+                    c = dg == d1;
+                    if (!ev) keep = v + 1;
+                }
+            }
+#pragma unroll
+            for (int o = 8; o > 0; o >>= 1) keep = max(keep, __shfl_xor_sync(0xffffffffu, keep, o));
+            if (gi < tot && (tid & 15) == 0) a.blk_max[sm.fbl[gi]] = keep;
+            if (ev) atomicSub(&sm.hinc[S], 1);
+            stage_put(st_ev, ev, 0, sl);
+            stage_put(st_c, c, v, sl);
+            __syncthreads();
+            ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], sm.nh);
+            stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, false, &sm.bc[10]);
+        }
+        __syncthreads();  // fbl is rewritten by the next pass
     }
 }
 
@@ -540,6 +655,18 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x * blockDim.x;
     const uint32_t gtid = blockIdx.x * blockDim.x + tid;
+    // one CTA (narrow traces, acceptance c8): the key histograms live in shared
+    // memory (no flushes, no global reads for b*) and the resident / list
+    // counters in registers -- the grid barriers are __syncthreads already
+    const bool one = gridDim.x == 1;
+    uint32_t l_nres = a.st->n_res, l_in = 0, l_out = 0;
+    if (one) {
+        for (uint32_t b = tid; b <= S; b += blockDim.x) {
+            sm.hinc[b] = ((volatile int32_t*)a.hist_inc)[b];
+            sm.hnew[b] = 0;
+        }
+        __syncthreads();
+    }
     for (uint32_t i = 0; i < S; ++i) {
         IPHASE(a, 0);
         IState* cs = a.st + (i & 1);
@@ -548,14 +675,19 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         const uint32_t ni = sm.toff[i + 1] - base;
         const uint32_t chunk = (ni + gridDim.x - 1) / gridDim.x;
         const uint32_t c0 = min(ni, blockIdx.x * chunk), c1 = min(ni, c0 + chunk);
-        const uint32_t nres = *(volatile uint32_t*)&cs->n_res;
-        const uint32_t in_total = *(volatile uint32_t*)&cs->in_total;
-        const uint32_t out_total = *(volatile uint32_t*)&cs->out_total;
+        const uint32_t nres = one ? l_nres : *(volatile uint32_t*)&cs->n_res;
+        const uint32_t in_total = one ? l_in : *(volatile uint32_t*)&cs->in_total;
+        const uint32_t out_total = one ? l_out : *(volatile uint32_t*)&cs->out_total;
+        uint32_t m_one = 0;
         if (i > 0 && gtid == 0) {  // the previous iteration handed out exactly its histogram counts
             const volatile IState* ps = ns;
             if (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in) atomicOr(&a.st->err, 8u);
         }
-        for (uint32_t b = gtid; b < 3 * 2048; b += G) a.rh[b] = 0;  // last read before the previous barrier
+        if (one) {
+            for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+        } else {
+            for (uint32_t b = gtid; b < 3 * 2048; b += G) a.rh[b] = 0;  // last read before the previous barrier
+        }
 
         // P1: hits refresh their key and record their occupancy tag; misses
         // become candidates; per-chunk miss counts
@@ -571,6 +703,11 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                     a.slot_key[s] = nu;
                     a.acc_slot[x] = a.slot_tag[s];
                     atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
+                    if (a.nv && nu == kNever) {  // a new NEVER member
+                        const uint32_t v = a.trace[x];
+                        atomicAdd(&sm.nh[v >> a.sh1], 1);
+                        atomicMax(&a.blk_max[s >> 4], v + 1);
+                    }
                     ++hits;
                     a.pmiss[pos] = 0;
                 } else {
@@ -585,17 +722,23 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             miss = block_sum(miss, sm.scan);
             hits = block_sum(hits, sm.scan);
             if (tid == 0) {
-                a.chunk_miss[blockIdx.x] = miss;
+                if (!one) a.chunk_miss[blockIdx.x] = miss;
                 sm.hinc[i] -= (int32_t)hits;  // all incumbents keyed i are exactly the hits
             }
-            hist_flush(sm.hinc, a.hist_inc, S + 1);
-            hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
+            if (!one) {
+                hist_flush(sm.hinc, a.hist_inc, S + 1);
+                hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
+                if (a.nv) hist_flush(sm.nh, a.never_hist, 2048);
+            }
+            if (one) {
+                m_one = miss;
+            }
         }
         grid_sync(a.bar);
         IPHASE(a, 1);
 
-        uint32_t m, mpre;  // misses this iteration, misses in earlier chunks
-        {
+        uint32_t m = m_one, mpre = 0;  // misses this iteration, misses in earlier chunks
+        if (!one) {
             uint32_t pre = 0, tot = 0;
             for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
                 const uint32_t v = a.chunk_miss[c];
@@ -616,8 +759,16 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 if (f) place_ins(a, sm, base + pos, a.pkey[pos], a.pnk[pos], nres + k + ex, S);
                 k += tot;
             }
-            hist_flush(sm.hinc, a.hist_inc, S + 1);
-            for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+            if (one) {
+                __syncthreads();
+                for (uint32_t b = tid; b <= S; b += blockDim.x) sm.hnew[b] = 0;
+                l_nres = nres + m;
+                l_in = in_total + m;
+            } else {
+                hist_flush(sm.hinc, a.hist_inc, S + 1);
+                if (a.nv) hist_flush(sm.nh, a.never_hist, 2048);
+                for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+            }
             if (gtid == 0) {
                 a.o_misses[i] = m;
                 cs->exp_out = 0;
@@ -649,8 +800,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 const uint32_t b = b0 + tid;
                 uint32_t ci = 0, cn = 0;
                 if (b <= S) {
-                    ci = (uint32_t)((volatile int32_t*)a.hist_inc)[b];
-                    cn = ((volatile uint32_t*)a.hist_new)[b];
+                    ci = one ? (uint32_t)sm.hinc[b] : (uint32_t)((volatile int32_t*)a.hist_inc)[b];
+                    cn = one ? (uint32_t)sm.hnew[b] : ((volatile uint32_t*)a.hist_new)[b];
                 }
                 unsigned long long tot;
                 const unsigned long long bef =
@@ -681,7 +832,29 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         const bool evict_b = keep_inc == 0;  // none of b*'s incumbents kept: they leave in P3
         const uint32_t n_out = nres - inc_before - keep_inc;
         const uint32_t n_in = new_before + admit_new;
-        const uint32_t n_out_p3 = nres - inc_before - (evict_b ? 0u : inc_b);  // eviction tickets issued in P3
+        // small b* (<= kLocalSel candidates): P3 collects all of them and every
+        // CTA selects locally -- no digit barriers, no second slot scan.
+        // NEVER fast path: the first digit comes from the maintained NEVER
+        // histogram and P3 reads only the summary-flagged slot blocks.
+        const bool small = sel != 0 && (sel == 1 ? inc_b : new_b) <= kLocalSel;
+        const bool fastnv = !small && a.nv && sel == 1 && bstar == S && !one;
+        uint32_t d1_nv = 0, left_nv = 0;
+        uint32_t n_out_p3 = nres - inc_before - (evict_b ? 0u : inc_b);  // eviction tickets issued in P3
+        if (fastnv) {
+            d1_nv = hist_select((const uint32_t*)a.never_hist, 2048, keep_inc, &left_nv, sm);
+            const uint32_t eq = (uint32_t)((volatile int32_t*)a.never_hist)[d1_nv];
+            n_out_p3 = inc_b - (keep_inc - left_nv) - eq;  // members above the cut digit
+        }
+        if (a.tstamp && gtid == 0) {  // GX_INSPECT_TRACE: the first 256 cut iterations' shape
+            const uint32_t c = (uint32_t)a.tstamp[31] - 1;
+            if (c < 256) {
+                unsigned long long* e = a.tstamp + 64 + 4 * c;
+                e[0] = ((unsigned long long)i << 32) | nres;
+                e[1] = ((unsigned long long)bstar << 32) | (uint32_t)sel;
+                e[2] = ((unsigned long long)inc_b << 32) | new_b;
+                e[3] = ((unsigned long long)n_out << 32) | n_in;
+            }
+        }
 
         // P3: evictions above b*; b*'s members for the radix select; certain
         // insertions (keys below b*) in tickets -- placed now when their
@@ -692,10 +865,13 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             sm.bc[9] = 0;
         }
         __syncthreads();
-        if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S);
-        else p3_scan<1>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S);
+        const bool coll = small && sel == 1;
+        if (fastnv) never_scan(a, sm, nres, d1_nv, st_ev, st_c, cs, out_total, S);
+        else if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
+        else p3_scan<1>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
         __syncthreads();
-        ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10]);
+        ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10], a.nv ? sm.nh : nullptr);
+        if (fastnv || coll) stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
             for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < ni; p0 += G) {
                 const uint32_t pos = p0 + tid;
@@ -735,22 +911,37 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 }
             }
         }
-        if (sel) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
+        if (sel && !one && !small && !fastnv) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
+        if (small && sel == 2) {  // (the digit histogram of the materialisation is not needed)
+            __syncthreads();
+            for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+        }
         // (hinc deltas stay in shared memory until the final phase: other CTAs
         // may still be reading hist_inc for b*)
         grid_sync(a.bar);
         IPHASE(a, 3);
 
         uint32_t thr = 0xFFFFFFFFu;
-        if (sel) {
+        const uint32_t nc_sel = *(volatile uint32_t*)&cs->n_c;
+        if (small) {
+            thr = local_select(a, sm, nc_sel, sel == 1 ? keep_inc : admit_new, false, 0);
+        } else if (fastnv && nc_sel <= kLocalSel) {
+            thr = local_select(a, sm, nc_sel, left_nv, true, d1_nv);
+        } else if (sel) {
             const uint32_t want = sel == 1 ? keep_inc : admit_new;
-            uint32_t left;
-            const uint32_t d1 = hist_select(a.rh, 2048, want, &left, sm);
-            if (sel == 1) {
+            uint32_t left = left_nv, d1 = d1_nv;
+            if (!fastnv) {
+                d1 = hist_select(one ? (const uint32_t*)sm.rh : a.rh, 2048, want, &left, sm);
+                if (one) {  // the shared histogram takes the next digit
+                    for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+                    __syncthreads();
+                }
+            }
+            if (sel == 1 && !fastnv) {
                 if (nres >= 8u * G) p3b_scan<8>(a, sm, nres, bstar, d1, st_ev, st_c, cs, out_total, S);
                 else p3b_scan<1>(a, sm, nres, bstar, d1, st_ev, st_c, cs, out_total, S);
                 __syncthreads();
-                ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10]);
+                ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10], a.nv ? sm.nh : nullptr);
                 stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
             } else {
                 const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
@@ -759,21 +950,25 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                     if ((v >> a.sh1) == d1) atomicAdd(&sm.rh[(v >> a.sh2) & a.m2], 1);
                 }
             }
-            hist_flush(sm.rh, (int32_t*)a.rh + 2048, 2048);
+            if (!one) hist_flush(sm.rh, (int32_t*)a.rh + 2048, 2048);
             grid_sync(a.bar);
-            const uint32_t d2 = hist_select(a.rh + 2048, 2048, left, &left, sm);
+            const uint32_t d2 = hist_select(one ? (const uint32_t*)sm.rh : a.rh + 2048, 2048, left, &left, sm);
             const uint32_t pre = (d1 << (a.sh1 - a.sh2)) | d2;  // id >> sh2 of the cut
             if (a.sh2 == 0) {
                 thr = pre;
             } else {
                 const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+                if (one) {
+                    for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
+                    __syncthreads();
+                }
                 for (uint32_t k = gtid; k < nc; k += G) {
                     const uint32_t v = a.c_id[k];
                     if ((v >> a.sh2) == pre) atomicAdd(&sm.rh[v & ((1u << a.sh2) - 1)], 1);
                 }
-                hist_flush(sm.rh, (int32_t*)a.rh + 4096, 1024);
+                if (!one) hist_flush(sm.rh, (int32_t*)a.rh + 4096, 1024);
                 grid_sync(a.bar);
-                const uint32_t d3 = hist_select(a.rh + 4096, 1u << a.sh2, left, &left, sm);
+                const uint32_t d3 = hist_select(one ? (const uint32_t*)sm.rh : a.rh + 4096, 1u << a.sh2, left, &left, sm);
                 thr = (pre << a.sh2) | d3;
             }
         }
@@ -790,10 +985,10 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 if (ev) atomicSub(&sm.hinc[bstar], 1);
                 stage_put(st_ev, ev, 0, ev ? a.c_ref[k] : 0u);
                 __syncthreads();
-                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10]);
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], a.nv ? sm.nh : nullptr);
             }
             __syncthreads();
-            ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10]);
+            ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10], a.nv ? sm.nh : nullptr);
         }
         if (admit_new) {
             for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {  // CTA-uniform
@@ -816,8 +1011,17 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             const uint32_t x = a.ins_x[t];
             place_ins(a, sm, x, a.pkey[x - base], a.pnk[x - base], take_slot(a.ev_slot, t), S);
         }
-        hist_flush(sm.hinc, a.hist_inc, S + 1);
-        for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+        if (one) {
+            __syncthreads();
+            for (uint32_t b = tid; b <= S; b += blockDim.x) sm.hnew[b] = 0;
+            l_nres = nres + n_in - n_out;
+            l_in = in_total + n_in;
+            l_out = out_total + n_out;
+        } else {
+            hist_flush(sm.hinc, a.hist_inc, S + 1);
+            if (a.nv) hist_flush(sm.nh, a.never_hist, 2048);
+            for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
+        }
         if (gtid == 0) {
             if (n_out > n_in) atomicOr(&a.st->err, 4u);
             cs->exp_out = n_out;
@@ -917,7 +1121,10 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
         sm.hinc[i] = 0;
         sm.hnew[i] = 0;
     }
-    for (uint32_t i = tid; i < 2048; i += blockDim.x) sm.rh[i] = 0;
+    for (uint32_t i = tid; i < 2048; i += blockDim.x) {
+        sm.rh[i] = 0;
+        sm.nh[i] = 0;
+    }
     if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[0] = gtimer();
     __syncthreads();
     const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
@@ -1916,6 +2123,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         B.ins_x.reserve(maxw);
         B.slot_nk.reserve(Keff + 1);
         B.pnk.reserve(maxw);
+        B.never_hist.reserve(2048);
+        B.blk_max.reserve(Keff / 16 + 1);
     }
     // PART 1 (recurrence) grid: one CTA per SM, or ONE CTA for narrow traces --
     // an iteration of <= 4096 accesses against <= 16384 slots is a few dozen
@@ -2066,6 +2275,17 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.slot_nk = B.slot_nk.p;
     a.pnk = B.pnk.p;
     a.dense = defer && a.trusted;
+    // NEVER-member bookkeeping pays where a cut would otherwise scan a large
+    // resident set (>= 8 slots per recurrence thread); GX_INSPECT_NEVER=0 disables
+    // (2 = on for every multi-CTA recurrence: the tests' small-scale coverage)
+    static const int never_knob = env_int("GX_INSPECT_NEVER", 1);
+    a.nv = defer && never_knob && grid > 1 && (never_knob == 2 || Keff >= 8ull * (uint64_t)grid * IN_THREADS);
+    a.never_hist = B.never_hist.p;
+    a.blk_max = B.blk_max.p;
+    if (a.nv) {
+        GX_CUDA(cudaMemsetAsync(B.never_hist.p, 0, 2048 * 4, st));
+        GX_CUDA(cudaMemsetAsync(B.blk_max.p, 0, (Keff / 16 + 1) * 4, st));
+    }
     // dense keys: the bitmask (3 grid passes over an n_first x W prefix) by
     // default; GX_DENSE_NEXT=last: one grid step per iteration over the
     // L2-resident `last` prefix (measured cfg1 357 vs 220 us, papers@5 % 905 vs
@@ -2080,9 +2300,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     static PinBuf<unsigned long long> htb;
     a.tstamp = nullptr;
     if (tracing) {
-        tbuf.reserve(64);
-        htb.reserve(64);
-        GX_CUDA(cudaMemsetAsync(tbuf.p, 0, 64 * 8, st));
+        tbuf.reserve(64 + 4 * 256);
+        htb.reserve(64 + 4 * 256);
+        GX_CUDA(cudaMemsetAsync(tbuf.p, 0, (64 + 4 * 256) * 8, st));
         a.tstamp = tbuf.p;
     }
 
@@ -2166,7 +2386,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     GX_CUDA(cudaMemcpyAsync(hp + hs_bytes, d_misses.p, arr_bytes, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(hp + hs_bytes + arr_bytes, d_in_off.p, arr_bytes, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaMemcpyAsync(hp + hs_bytes + 2 * arr_bytes, d_out_off.p, arr_bytes, cudaMemcpyDeviceToHost, st));
-    if (tracing) GX_CUDA(cudaMemcpyAsync(htb.p, tbuf.p, 64 * 8, cudaMemcpyDeviceToHost, st));
+    if (tracing) GX_CUDA(cudaMemcpyAsync(htb.p, tbuf.p, (64 + 4 * 256) * 8, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
     IState hs;
     std::memcpy(&hs, hp, sizeof(IState));
@@ -2182,6 +2402,15 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
             const char* nm[8] = {"", "P1", "allin", "P3", "select", "P4", "P5", "P6"};
             if (defer) nm[5] = "final";
             for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.1f", nm[k], htb.p[16 + k] / 1e3);
+            if (defer && std::getenv("GX_INSPECT_TRACE_CUTS")) {
+                std::fprintf(stderr, "\n[inspect cuts] i:nres:b*:sel:inc_b:new_b:n_out:n_in");
+                for (unsigned long long c = 0; c < std::min<unsigned long long>(htb.p[31], 256); ++c) {
+                    const unsigned long long* e = htb.p + 64 + 4 * c;
+                    std::fprintf(stderr, " %u:%u:%u:%u:%u:%u:%u:%u", (unsigned)(e[0] >> 32), (unsigned)e[0],
+                                 (unsigned)(e[1] >> 32), (unsigned)e[1], (unsigned)(e[2] >> 32), (unsigned)e[2],
+                                 (unsigned)(e[3] >> 32), (unsigned)e[3]);
+                }
+            }
         }
         std::fprintf(stderr, "\n");
     }
