@@ -55,6 +55,8 @@ struct IState {
     uint32_t err;
     uint32_t exp_out;  // deferred recurrence: the iteration's eviction / insertion counts
     uint32_t exp_in;   // from the histograms (checked against the tickets handed out)
+    uint32_t n_pool;   // free slots published to the pool (leftover evictions + fresh slots)
+    uint32_t n_take;   // pool slots taken by leftover insertions
 };
 
 struct IArgs {
@@ -446,26 +448,35 @@ __device__ __forceinline__ uint32_t take_slot(uint32_t* ev_slot, uint32_t t) {
     return s;
 }
 
-// Flush staged evictions (internal slots): each takes the next out ticket t,
-// its node and occupancy tag go to the iteration's raw out list, the node
-// leaves the cache, and slot s is published as ev_slot[t].
+// The evicted slot s leaves: out record (node, occupancy tag) at position t of
+// the iteration's raw out list, node_slot cleared, NEVER histogram delta.
+__device__ __forceinline__ void ev_record(const IArgs& a, uint32_t s, uint32_t t, int32_t* nh) {
+    const uint32_t u = a.slot_node[s];
+    a.out_raw[t] = u;
+    a.out_tagraw[t] = a.slot_tag[s];
+    a.node_slot[a.slot_nk[s]] = -1;
+    if (nh && a.slot_key[s] == kNever) atomicSub(&nh[u >> a.sh1], 1);
+}
+
+// Spill a CTA's staged evictions (its list E) once it passes 1024 entries (or
+// when forced): out records, then every slot is published to the free-slot
+// pool (ev_slot[pool ticket]) for insertions of any CTA. Below that, E stays in
+// shared memory for the final phase, where the CTA's own insertions take it.
 __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, uint32_t out_total, bool force,
                                          uint32_t* bcast, int32_t* nh) {
     const uint32_t n = *st.cnt;
     __syncthreads();
     if (n == 0 || (!force && n < 1024)) return;
-    if (threadIdx.x == 0) *bcast = atomicAdd(&cs->n_out, n);
+    if (threadIdx.x == 0) {
+        bcast[0] = atomicAdd(&cs->n_out, n);
+        bcast[1] = atomicAdd(&cs->n_pool, n);
+    }
     __syncthreads();
-    const uint32_t base = *bcast;
+    const uint32_t base = bcast[0], pbase = bcast[1];
     for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) {
         const uint32_t s = (uint32_t)st.buf[k];
-        const uint32_t t = base + k;
-        const uint32_t u = a.slot_node[s];
-        a.out_raw[out_total + t] = u;
-        a.out_tagraw[out_total + t] = a.slot_tag[s];
-        a.node_slot[a.slot_nk[s]] = -1;
-        if (nh && a.slot_key[s] == kNever) atomicSub(&nh[u >> a.sh1], 1);
-        st_release_u32(a.ev_slot + t, s);
+        ev_record(a, s, out_total + base + k, nh);
+        st_release_u32(a.ev_slot + pbase + k, s);
     }
     __syncthreads();
     if (threadIdx.x == 0) *st.cnt = 0;
@@ -681,7 +692,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         uint32_t m_one = 0;
         if (i > 0 && gtid == 0) {  // the previous iteration handed out exactly its histogram counts
             const volatile IState* ps = ns;
-            if (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in) atomicOr(&a.st->err, 8u);
+            if (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in || ps->n_pool != ps->n_take)
+                atomicOr(&a.st->err, 8u);
         }
         if (one) {
             for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
@@ -693,30 +705,55 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         // become candidates; per-chunk miss counts
         {
             uint32_t miss = 0, hits = 0;
-            for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) {
-                const uint32_t x = base + pos;
-                const uint32_t nk = a.dense ? a.acc_slot[x] : a.trace[x];
-                const uint32_t nu = a.next_use[x];
-                const int32_t s = a.node_slot[nk];
-                a.isfirst[x] = 0;
-                if (s >= 0) {
-                    a.slot_key[s] = nu;
-                    a.acc_slot[x] = a.slot_tag[s];
-                    atomicAdd(&sm.hinc[bucket_of(nu, S)], 1);
-                    if (a.nv && nu == kNever) {  // a new NEVER member
-                        const uint32_t v = a.trace[x];
-                        atomicAdd(&sm.nh[v >> a.sh1], 1);
-                        atomicMax(&a.blk_max[s >> 4], v + 1);
+            // PU positions per thread at a time: their key, node_slot and tag
+            // loads overlap (the chain is latency-bound otherwise)
+            constexpr int PU = 4;
+            for (uint32_t p0 = c0 + tid; p0 < c1; p0 += PU * blockDim.x) {
+                uint32_t nk[PU], nu[PU], tg[PU], vv[PU];
+                int32_t sl[PU];
+#pragma unroll
+                for (int j = 0; j < PU; ++j) {
+                    const uint32_t pos = p0 + j * blockDim.x;
+                    nk[j] = 0;
+                    nu[j] = 0;
+                    if (pos < c1) {
+                        nk[j] = a.dense ? a.acc_slot[base + pos] : a.trace[base + pos];
+                        nu[j] = a.next_use[base + pos];
                     }
-                    ++hits;
-                    a.pmiss[pos] = 0;
-                } else {
-                    a.pmiss[pos] = 1;
-                    a.pkey[pos] = nu;
-                    a.pnk[pos] = nk;
-                    a.acc_slot[x] = kNever;
-                    atomicAdd(&sm.hnew[bucket_of(nu, S)], 1);
-                    ++miss;
+                }
+#pragma unroll
+                for (int j = 0; j < PU; ++j) sl[j] = p0 + j * blockDim.x < c1 ? a.node_slot[nk[j]] : -1;
+#pragma unroll
+                for (int j = 0; j < PU; ++j) {
+                    const bool hit = sl[j] >= 0;
+                    tg[j] = hit ? a.slot_tag[sl[j]] : 0u;
+                    vv[j] = hit && a.nv && nu[j] == kNever ? a.trace[base + p0 + j * blockDim.x] : 0u;
+                }
+#pragma unroll
+                for (int j = 0; j < PU; ++j) {
+                    const uint32_t pos = p0 + j * blockDim.x;
+                    if (pos >= c1) continue;
+                    const uint32_t x = base + pos;
+                    a.isfirst[x] = 0;
+                    const int32_t s = sl[j];
+                    if (s >= 0) {
+                        a.slot_key[s] = nu[j];
+                        a.acc_slot[x] = tg[j];
+                        atomicAdd(&sm.hinc[bucket_of(nu[j], S)], 1);
+                        if (a.nv && nu[j] == kNever) {  // a new NEVER member
+                            atomicAdd(&sm.nh[vv[j] >> a.sh1], 1);
+                            atomicMax(&a.blk_max[s >> 4], vv[j] + 1);
+                        }
+                        ++hits;
+                        a.pmiss[pos] = 0;
+                    } else {
+                        a.pmiss[pos] = 1;
+                        a.pkey[pos] = nu[j];
+                        a.pnk[pos] = nk[j];
+                        a.acc_slot[x] = kNever;
+                        atomicAdd(&sm.hnew[bucket_of(nu[j], S)], 1);
+                        ++miss;
+                    }
                 }
             }
             miss = block_sum(miss, sm.scan);
@@ -779,6 +816,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 ns->n_out = 0;
                 ns->n_c = 0;
                 ns->n_ins = 0;
+                ns->n_pool = 0;
+                ns->n_take = 0;
                 a.o_in_off[i + 1] = in_total + m;
                 a.o_out_off[i + 1] = out_total;
             }
@@ -839,12 +878,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         const bool small = sel != 0 && (sel == 1 ? inc_b : new_b) <= kLocalSel;
         const bool fastnv = !small && a.nv && sel == 1 && bstar == S && !one;
         uint32_t d1_nv = 0, left_nv = 0;
-        uint32_t n_out_p3 = nres - inc_before - (evict_b ? 0u : inc_b);  // eviction tickets issued in P3
-        if (fastnv) {
-            d1_nv = hist_select((const uint32_t*)a.never_hist, 2048, keep_inc, &left_nv, sm);
-            const uint32_t eq = (uint32_t)((volatile int32_t*)a.never_hist)[d1_nv];
-            n_out_p3 = inc_b - (keep_inc - left_nv) - eq;  // members above the cut digit
-        }
+        if (fastnv) d1_nv = hist_select((const uint32_t*)a.never_hist, 2048, keep_inc, &left_nv, sm);
         if (a.tstamp && gtid == 0) {  // GX_INSPECT_TRACE: the first 256 cut iterations' shape
             const uint32_t c = (uint32_t)a.tstamp[31] - 1;
             if (c < 256) {
@@ -856,21 +890,21 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             }
         }
 
-        // P3: evictions above b*; b*'s members for the radix select; certain
-        // insertions (keys below b*) in tickets -- placed now when their
-        // eviction was issued in this phase (or they take a fresh slot)
+        // P3: evictions above b* (into this CTA's list E, kept in shared memory
+        // until the final phase; spilled to the pool past 1024), b*'s members /
+        // candidates for the select
         const Stage st_ev{sm.sortbuf, &sm.bc[8]}, st_c{sm.sortbuf + 2048, &sm.bc[9]};
         if (tid == 0) {
             sm.bc[8] = 0;
             sm.bc[9] = 0;
         }
         __syncthreads();
+        int32_t* const nhp = a.nv ? sm.nh : nullptr;
         const bool coll = small && sel == 1;
         if (fastnv) never_scan(a, sm, nres, d1_nv, st_ev, st_c, cs, out_total, S);
         else if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
         else p3_scan<1>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
         __syncthreads();
-        ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10], a.nv ? sm.nh : nullptr);
         if (fastnv || coll) stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
             for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < ni; p0 += G) {
@@ -880,7 +914,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 if (pos < ni && a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar) {
                     c = true;
                     v = a.trace[base + pos];
-                    atomicAdd(&sm.rh[v >> a.sh1], 1);
+                    if (!small) atomicAdd(&sm.rh[v >> a.sh1], 1);
                 }
                 stage_put(st_c, c, v, pos);
                 __syncthreads();
@@ -889,40 +923,14 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             __syncthreads();
             stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         }
-        if (new_before) {
-            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {  // CTA-uniform
-                const uint32_t pos = p0 + tid;
-                bool f = false;
-                uint32_t key = 0;
-                if (pos < c1 && a.pmiss[pos]) {
-                    key = a.pkey[pos];
-                    f = bucket_of(key, S) < bstar;
-                }
-                uint32_t tot;
-                const uint32_t ex = block_excl_scan((uint32_t)f, sm.scan, tot);
-                if (tid == 0 && tot) sm.bc[11] = atomicAdd(&cs->n_ins, tot);
-                __syncthreads();
-                if (f) {
-                    const uint32_t t = sm.bc[11] + ex;
-                    const uint32_t nk = a.pnk[pos];
-                    if (t < n_out_p3) place_ins(a, sm, base + pos, key, nk, take_slot(a.ev_slot, t), S);
-                    else if (t < n_out) a.ins_x[t] = base + pos;  // its slot is freed after the select
-                    else place_ins(a, sm, base + pos, key, nk, nres + (t - n_out), S);
-                }
-            }
-        }
         if (sel && !one && !small && !fastnv) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
-        if (small && sel == 2) {  // (the digit histogram of the materialisation is not needed)
-            __syncthreads();
-            for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
-        }
         // (hinc deltas stay in shared memory until the final phase: other CTAs
         // may still be reading hist_inc for b*)
         grid_sync(a.bar);
         IPHASE(a, 3);
 
         uint32_t thr = 0xFFFFFFFFu;
-        const uint32_t nc_sel = *(volatile uint32_t*)&cs->n_c;
+        const uint32_t nc_sel = small || fastnv ? *(volatile uint32_t*)&cs->n_c : 0u;
         if (small) {
             thr = local_select(a, sm, nc_sel, sel == 1 ? keep_inc : admit_new, false, 0);
         } else if (fastnv && nc_sel <= kLocalSel) {
@@ -941,7 +949,6 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 if (nres >= 8u * G) p3b_scan<8>(a, sm, nres, bstar, d1, st_ev, st_c, cs, out_total, S);
                 else p3b_scan<1>(a, sm, nres, bstar, d1, st_ev, st_c, cs, out_total, S);
                 __syncthreads();
-                ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10], a.nv ? sm.nh : nullptr);
                 stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
             } else {
                 const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
@@ -974,9 +981,12 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         }
         IPHASE(a, 4);
 
-        // final: b*'s last evictions (sel 1: ids above the cut), then every
-        // insertion still without a slot -- b*'s admissions (tickets after the
-        // certain ones) and the certain insertions deferred in P3
+        // final: b*'s last evictions (sel 1: ids above the cut) join this CTA's
+        // list E; this CTA's insertions (keys below b*, and b*'s admissions)
+        // take E's slots in order. Only leftovers meet through the pool: E
+        // beyond the insertions and the n_in - n_out fresh slots are published,
+        // insertions beyond E take pool tickets -- every CTA publishes before it
+        // takes, so the waits end.
         if (sel == 1) {
             const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
             for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < nc; k0 += G) {  // CTA-uniform
@@ -985,31 +995,74 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 if (ev) atomicSub(&sm.hinc[bstar], 1);
                 stage_put(st_ev, ev, 0, ev ? a.c_ref[k] : 0u);
                 __syncthreads();
-                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], a.nv ? sm.nh : nullptr);
+                ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], nhp);
+            }
+        }
+        if (n_in) {  // (n_out <= n_in: nothing leaves either when nothing enters)
+            __syncthreads();
+            const uint32_t nE = *st_ev.cnt;
+            auto ins_flag = [&](uint32_t pos, uint32_t& key) -> bool {
+                if (pos >= c1) return false;
+                const uint8_t pm = a.pmiss[pos];
+                key = a.pkey[pos];
+                if (!pm) return false;
+                const uint32_t bk = bucket_of(key, S);
+                if (bk != bstar) return bk < bstar;
+                return admit_new != 0 && (sel != 2 || a.trace[base + pos] <= thr);
+            };
+            // this CTA's insertions: flags and keys in registers when the chunk
+            // is at most FQ positions per thread, else recounted below
+            constexpr int FQ = 4;
+            const bool reg = c1 - c0 <= FQ * blockDim.x;
+            uint32_t fkey[FQ], fmask = 0, cnt = 0;
+            if (reg) {
+#pragma unroll
+                for (int j = 0; j < FQ; ++j)
+                    if (ins_flag(c0 + tid + j * blockDim.x, fkey[j])) fmask |= 1u << j;
+                cnt = __popc(fmask);
+            } else {
+                uint32_t key;
+                for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) cnt += ins_flag(pos, key);
+            }
+            uint32_t nI;
+            const uint32_t ex = block_excl_scan(cnt, sm.scan, nI);
+            const uint32_t F = n_in - n_out;  // fresh slots, spread over the CTAs
+            const uint32_t fr0 = (uint32_t)((uint64_t)F * blockIdx.x / gridDim.x);
+            const uint32_t fr1 = (uint32_t)((uint64_t)F * (blockIdx.x + 1) / gridDim.x);
+            // the CTA's ticket ranges, one atomic per warp so they overlap
+            if ((tid & 31) == 0) {
+                const uint32_t w = tid >> 5;
+                if (w == 0) sm.bc[12] = nE ? atomicAdd(&cs->n_out, nE) : 0u;
+                if (w == 1) sm.bc[13] = nE > nI ? atomicAdd(&cs->n_pool, nE - nI) : 0u;
+                if (w == 2) sm.bc[14] = fr1 > fr0 ? atomicAdd(&cs->n_pool, fr1 - fr0) : 0u;
+                if (w == 3) sm.bc[15] = nI > nE ? atomicAdd(&cs->n_take, nI - nE) : 0u;
+                if (w == 4 && nI) atomicAdd(&cs->n_ins, nI);
             }
             __syncthreads();
-            ev_flush(a, st_ev, cs, out_total, true, &sm.bc[10], a.nv ? sm.nh : nullptr);
-        }
-        if (admit_new) {
-            for (uint32_t p0 = c0; p0 < c1; p0 += blockDim.x) {  // CTA-uniform
-                const uint32_t pos = p0 + tid;
-                bool f = false;
-                if (pos < c1 && a.pmiss[pos] && bucket_of(a.pkey[pos], S) == bstar)
-                    f = sel != 2 || a.trace[base + pos] <= thr;
-                uint32_t tot;
-                const uint32_t ex = block_excl_scan((uint32_t)f, sm.scan, tot);
-                if (tid == 0 && tot) sm.bc[11] = atomicAdd(&cs->n_ins, tot);
-                __syncthreads();
-                if (f) {
-                    const uint32_t t = sm.bc[11] + ex;
-                    place_ins(a, sm, base + pos, a.pkey[pos], a.pnk[pos],
-                              t < n_out ? take_slot(a.ev_slot, t) : nres + (t - n_out), S);
-                }
+            for (uint32_t k = tid; k < nE; k += blockDim.x) {
+                const uint32_t sl = (uint32_t)st_ev.buf[k];
+                ev_record(a, sl, out_total + sm.bc[12] + k, nhp);
+                if (k >= nI) st_release_u32(a.ev_slot + sm.bc[13] + (k - nI), sl);
             }
-        }
-        for (uint32_t t = n_out_p3 + gtid; t < min(new_before, n_out); t += G) {
-            const uint32_t x = a.ins_x[t];
-            place_ins(a, sm, x, a.pkey[x - base], a.pnk[x - base], take_slot(a.ev_slot, t), S);
+            for (uint32_t j = fr0 + tid; j < fr1; j += blockDim.x)
+                st_release_u32(a.ev_slot + sm.bc[14] + (j - fr0), nres + j);
+            __syncthreads();  // E's out records read their slots before any placement rewrites them
+            // the k-th insertion of the CTA takes E[k], or pool ticket k - nE
+            uint32_t k = ex;
+            auto place_k = [&](uint32_t pos, uint32_t key) {
+                const uint32_t sl = k < nE ? (uint32_t)st_ev.buf[k] : take_slot(a.ev_slot, sm.bc[15] + (k - nE));
+                place_ins(a, sm, base + pos, key, a.pnk[pos], sl, S);
+                ++k;
+            };
+            if (reg) {
+#pragma unroll
+                for (int j = 0; j < FQ; ++j)
+                    if (fmask & (1u << j)) place_k(c0 + tid + j * blockDim.x, fkey[j]);
+            } else {
+                uint32_t key;
+                for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x)
+                    if (ins_flag(pos, key)) place_k(pos, key);
+            }
         }
         if (one) {
             __syncthreads();
@@ -1033,6 +1086,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             ns->n_out = 0;
             ns->n_c = 0;
             ns->n_ins = 0;
+            ns->n_pool = 0;
+            ns->n_take = 0;
             a.o_in_off[i + 1] = in_total + n_in;
             a.o_out_off[i + 1] = out_total + n_out;
         }
@@ -1041,7 +1096,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
     }
     if (S > 0 && gtid == 0) {
         const volatile IState* ls = a.st + ((S - 1) & 1);
-        if (ls->n_out != ls->exp_out || ls->n_ins != ls->exp_in) atomicOr(&a.st->err, 8u);
+        if (ls->n_out != ls->exp_out || ls->n_ins != ls->exp_in || ls->n_pool != ls->n_take)
+            atomicOr(&a.st->err, 8u);
     }
 }
 
