@@ -1946,19 +1946,70 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect_rec(IArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_finish_changesets: the ordered changesets of a deferred recurrence.
+// The ordered changesets of a deferred recurrence, for every iteration at once.
+//  k_sort_outs: each iteration's raw out list sorted by node id (carrying the
+//     evicted occupancy's tag) in shared memory, one CTA per iteration
+//     (bitonic over <= kSortSeg entries; longer lists are left to k_finish,
+//     which orders them through the N-bit bitmap).
+//  k_finish_changesets:
 //  1. in-lists: the inserted accesses in trace order ARE the reference's
 //     in_ids / in_positions (iteration-major, position order within an
-//     iteration, finish_selection changeset.hpp:211-216) -- one compaction.
-//  2. out-lists were sorted by id per iteration before this kernel (segmented
-//     sort of the raw out tickets, carrying each evicted occupancy's tag).
-//  3. slots (feature_cache.hpp:114-129): the k-th insertion of iteration i
+//     iteration, finish_selection changeset.hpp:211-216) -- one compaction
+//     (each CTA owns a contiguous range of the trace).
+//  2. slots (feature_cache.hpp:114-129): the k-th insertion of iteration i
 //     reuses the slot of out_i[k] -- the slot its occupancy got when it was
 //     inserted (a pointer to an earlier insertion) or its init slot -- and
 //     the rest take n_res_i, n_res_i + 1, ...; the pointers are resolved by
 //     pointer jumping (chains are at most S long: log2 S rounds).
-//  4. every hit's occupancy tag becomes that occupancy's slot (acc_slot).
+//  3. every hit's occupancy tag becomes that occupancy's slot (acc_slot).
 // ---------------------------------------------------------------------------
+constexpr int kSortThreads = 512, kSortItems = 32;
+constexpr uint32_t kSortSeg = kSortThreads * kSortItems;  // entries one k_sort_outs CTA sorts
+
+// one CTA per iteration: block radix sort of (node id, tag) over the id bits
+// (ids are distinct within an iteration's out list); padding sorts last
+__global__ void __launch_bounds__(kSortThreads) k_sort_outs(const uint32_t* __restrict__ out_off, uint32_t S,
+                                                            const uint32_t* __restrict__ raw,
+                                                            const uint32_t* __restrict__ rawtag, uint32_t* out_ids,
+                                                            uint32_t* tag_sorted, uint32_t* big, uint32_t* nbig,
+                                                            int id_bits) {
+    using BRS = cub::BlockRadixSort<uint32_t, kSortThreads, kSortItems, uint32_t>;
+    extern __shared__ unsigned char sort_smem[];  // (66 KB: dynamic)
+    typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(sort_smem);
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t i = blockIdx.x; i < S; i += gridDim.x) {  // CTA-uniform
+        const uint32_t lo = out_off[i], n = out_off[i + 1] - lo;
+        if (n <= 1) {
+            if (n == 1 && tid == 0) {
+                out_ids[lo] = raw[lo];
+                tag_sorted[lo] = rawtag[lo];
+            }
+            continue;
+        }
+        if (n > kSortSeg) {
+            if (tid == 0) big[atomicAdd(nbig, 1u)] = i;
+            continue;
+        }
+        uint32_t k[kSortItems], v[kSortItems];
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {  // blocked arrangement: thread t holds [t * items, ...)
+            const uint32_t e = tid * kSortItems + j;
+            k[j] = e < n ? raw[lo + e] : 0xFFFFFFFFu;
+            v[j] = e < n ? rawtag[lo + e] : 0u;
+        }
+        BRS(tmp).Sort(k, v, 0, id_bits < 32 ? id_bits + 1 : 32);  // (+1: the padding key sorts after every id)
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            const uint32_t e = tid * kSortItems + j;
+            if (e < n) {
+                out_ids[lo + e] = k[j];
+                tag_sorted[lo + e] = v[j];
+            }
+        }
+        __syncthreads();  // tmp is reused by the next iteration
+    }
+}
+
 struct FArgs {
     const uint32_t* trace;
     const uint32_t* toff;     // S+1
@@ -1967,61 +2018,104 @@ struct FArgs {
     uint32_t* R;              // A: per inserted access, its slot (or kEv | parent access)
     const uint32_t* in_off;   // S+1
     const uint32_t* out_off;  // S+1
-    const uint32_t* out_tag;  // sorted out tags
+    uint32_t* out_ids;        // sorted out ids (the oversize lists are written here)
+    uint32_t* out_tag;        // sorted out tags
+    const uint32_t* out_raw;  // raw out lists (oversize lists)
+    const uint32_t* out_tagraw;
+    const uint32_t* big;      // iterations whose out list k_sort_outs left (> kSortSeg)
+    const uint32_t* nbig;
+    uint32_t* bm_words;       // N-bit bitmap, clean
+    uint32_t nwords;
+    uint32_t* last;           // N, kNever when clean: tag of a marked node
     uint32_t* o_in_ids;
     uint32_t* o_in_pos;
     uint32_t* o_in_slot;
-    uint32_t* tile_cnt;
+    uint32_t* cta_cnt;        // gridDim
     uint32_t* unres;          // 64 per-round unresolved counters (host-zeroed)
     uint32_t S, A, n_in, n0;
     GridBarrier* bar;
 };
 constexpr int FIN_THREADS = 512;
-constexpr uint32_t FIN_TILE = FIN_THREADS * 4;
 
 __global__ void __launch_bounds__(FIN_THREADS) k_finish_changesets(FArgs f) {
     __shared__ uint32_t scan[34];
     __shared__ uint32_t toff[kMaxIters + 1];
     const uint32_t tid = threadIdx.x, G = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + tid;
     for (uint32_t i = tid; i <= f.S; i += blockDim.x) toff[i] = f.toff[i];
-    const uint32_t ntiles = (f.A + FIN_TILE - 1) / FIN_TILE;
-    // 1. inserted accesses per tile
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    // 0. out lists longer than kSortSeg: mark their nodes in the bitmap (tag
+    // parked in `last`), count per word range, walk in id order
+    const uint32_t nbig = *f.nbig;
+    const uint32_t wch = (f.nwords + gridDim.x - 1) / gridDim.x;
+    const uint32_t w0 = min(f.nwords, blockIdx.x * wch), w1 = min(f.nwords, w0 + wch);
+    for (uint32_t b = 0; b < nbig; ++b) {
+        const uint32_t i = f.big[b], lo = f.out_off[i], n = f.out_off[i + 1] - lo;
+        for (uint32_t k = gtid; k < n; k += G) {
+            const uint32_t u = f.out_raw[lo + k];
+            f.last[u] = f.out_tagraw[lo + k];
+            atomicOr(&f.bm_words[u >> 5], 1u << (u & 31));
+        }
+        grid_sync(f.bar);
         uint32_t c = 0;
-        const uint32_t x0 = t * FIN_TILE + tid * 4;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) c += x0 + j < f.A ? f.isin[x0 + j] : 0u;
+        for (uint32_t w = w0 + tid; w < w1; w += blockDim.x) c += __popc(f.bm_words[w]);
         c = block_sum(c, scan);
-        if (tid == 0) f.tile_cnt[t] = c;
-    }
-    grid_sync(f.bar);
-    if (blockIdx.x == 0) {  // exclusive scan of the tile counts
-        uint32_t carry = 0;
-        for (uint32_t b0 = 0; b0 < ntiles; b0 += blockDim.x) {
-            const uint32_t t = b0 + tid;
-            const uint32_t v = t < ntiles ? f.tile_cnt[t] : 0u;
+        if (tid == 0) f.cta_cnt[blockIdx.x] = c;
+        grid_sync(f.bar);
+        uint32_t pre = 0;
+        for (uint32_t cc = tid; cc < blockIdx.x; cc += blockDim.x) pre += f.cta_cnt[cc];
+        pre = block_sum(pre, scan);
+        for (uint32_t p0 = w0; p0 < w1; p0 += blockDim.x) {  // CTA-uniform
+            const uint32_t w = p0 + tid;
+            uint32_t bits = w < w1 ? f.bm_words[w] : 0u;
             uint32_t tot;
-            const uint32_t ex = block_excl_scan(v, scan, tot);
-            if (t < ntiles) f.tile_cnt[t] = carry + ex;
-            carry += tot;
+            uint32_t k = pre + block_excl_scan((uint32_t)__popc(bits), scan, tot);
+            if (bits) f.bm_words[w] = 0;
+            while (bits) {
+                const uint32_t u = w * 32 + (__ffs(bits) - 1);
+                bits &= bits - 1;
+                f.out_ids[lo + k] = u;
+                f.out_tag[lo + k] = f.last[u];
+                f.last[u] = kNever;
+                ++k;
+            }
+            pre += tot;
         }
+        grid_sync(f.bar);
+    }
+    // 1. inserted accesses of this CTA's contiguous range of the trace (16-byte
+    // aligned ranges, 16 flags per thread per pass)
+    const uint32_t A16 = (f.A + 15) / 16;
+    const uint32_t x0 = 16 * (uint32_t)((uint64_t)A16 * blockIdx.x / gridDim.x);
+    const uint32_t x1 = min(f.A, 16 * (uint32_t)((uint64_t)A16 * (blockIdx.x + 1) / gridDim.x));
+    auto flags16 = [&](uint32_t x) -> uint4 {  // flags of x .. x + 15 (zero past x1)
+        if (x + 16 <= x1) return *reinterpret_cast<const uint4*>(f.isin + x);
+        uint32_t w[4] = {0, 0, 0, 0};
+        for (uint32_t j = 0; x + j < x1 && j < 16; ++j) w[j >> 2] |= (uint32_t)f.isin[x + j] << (8 * (j & 3));
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    };
+    auto pop16 = [](uint4 q) -> uint32_t {  // flags are 0 / 1 bytes
+        return __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);
+    };
+    {
+        uint32_t c = 0;
+        for (uint32_t x = x0 + 16 * tid; x < x1; x += 16 * blockDim.x) c += pop16(flags16(x));
+        c = block_sum(c, scan);
+        if (tid == 0) f.cta_cnt[blockIdx.x] = c;
     }
     grid_sync(f.bar);
+    uint32_t g0 = 0;
+    for (uint32_t cc = tid; cc < blockIdx.x; cc += blockDim.x) g0 += f.cta_cnt[cc];
+    g0 = block_sum(g0, scan);
     // 2. in-list entries and the slot (or parent) of every insertion
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint32_t x0 = t * FIN_TILE + tid * 4;
-        uint32_t fl[4], c = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            fl[j] = x0 + j < f.A ? f.isin[x0 + j] : 0u;
-            c += fl[j];
-        }
+    for (uint32_t p0 = x0; p0 < x1; p0 += 16 * blockDim.x) {  // CTA-uniform
+        const uint32_t xb = p0 + 16 * tid;
+        const uint4 q = xb < x1 ? flags16(xb) : make_uint4(0, 0, 0, 0);
         uint32_t tot;
-        uint32_t g = f.tile_cnt[t] + block_excl_scan(c, scan, tot);
+        uint32_t g = g0 + block_excl_scan(pop16(q), scan, tot);
+        const uint32_t wq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if (!fl[j]) continue;
-            const uint32_t x = x0 + j;
+        for (int j = 0; j < 16; ++j) {
+            if (!((wq[j >> 2] >> (8 * (j & 3))) & 1u)) continue;
+            const uint32_t x = xb + j;
             uint32_t lo = 0, hi = f.S;  // iteration of x: toff[lo] <= x < toff[lo + 1]
             while (hi - lo > 1) {
                 const uint32_t mid = (lo + hi) >> 1;
@@ -2037,6 +2131,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish_changesets(FArgs f) {
             f.R[x] = k < nout ? f.out_tag[ob + k] : f.n0 + ib - ob + (k - nout);
             ++g;
         }
+        g0 += tot;
     }
     grid_sync(f.bar);
     // 3. pointer jumping: R[x] always points at an ancestor on x's chain (or is
@@ -2059,9 +2154,24 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish_changesets(FArgs f) {
     }
     // 4. in-list slots; hits' tags -> slots
     for (uint32_t g = gtid; g < f.n_in; g += G) f.o_in_slot[g] = f.R[f.o_in_slot[g]];
-    for (uint32_t x = gtid; x < f.A; x += G) {
-        const uint32_t t = f.acc_slot[x];
-        if (t != kNever && (t & kEv)) f.acc_slot[x] = f.R[t & ~kEv];
+    for (uint32_t x0 = 4 * gtid; x0 < f.A; x0 += 4 * G) {  // 4 accesses per thread in flight
+        if (x0 + 4 <= f.A) {
+            uint4 t = *reinterpret_cast<const uint4*>(f.acc_slot + x0);
+            const bool c0 = t.x != kNever && (t.x & kEv), c1 = t.y != kNever && (t.y & kEv);
+            const bool c2 = t.z != kNever && (t.z & kEv), c3 = t.w != kNever && (t.w & kEv);
+            if (c0 | c1 | c2 | c3) {
+                if (c0) t.x = f.R[t.x & ~kEv];
+                if (c1) t.y = f.R[t.y & ~kEv];
+                if (c2) t.z = f.R[t.z & ~kEv];
+                if (c3) t.w = f.R[t.w & ~kEv];
+                *reinterpret_cast<uint4*>(f.acc_slot + x0) = t;
+            }
+        } else {
+            for (uint32_t x = x0; x < f.A; ++x) {
+                const uint32_t t = f.acc_slot[x];
+                if (t != kNever && (t & kEv)) f.acc_slot[x] = f.R[t & ~kEv];
+            }
+        }
     }
 }
 
@@ -2481,17 +2591,28 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     if (hs.err) fail(GX_RUNTIME_ERROR, "inspector: internal consistency error");
     const bool recurrence_ran = !(n_init_explicit < 0 && hs.n_first <= Keff);
     if (defer && recurrence_ran && io32[S] > 0) {
-        // ordered out lists: segmented sort of the raw out tickets by node id
+        // ordered out lists: each iteration's raw out list sorted by node id
         const uint32_t n_out_all = oo32[S];
+        B.fin_big.reserve(S + 1);
+        GX_CUDA(cudaMemsetAsync(B.fin_big.p + S, 0, 4, st));  // oversize-list count
         if (n_out_all) {
-            size_t tb = 0;
-            GX_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, B.out_raw.p, out->out_ids.p, B.out_tagraw.p,
-                                                        B.tag_sorted.p, (int)n_out_all, (int)S, d_out_off.p,
-                                                        d_out_off.p + 1, st));
-            B.sort_tmp.reserve(tb + 16);
-            GX_CUDA(cub::DeviceSegmentedSort::SortPairs(B.sort_tmp.p, tb, B.out_raw.p, out->out_ids.p,
-                                                        B.out_tagraw.p, B.tag_sorted.p, (int)n_out_all, (int)S,
-                                                        d_out_off.p, d_out_off.p + 1, st));
+            int id_bits = 1;
+            while (id_bits < 32 && (1ull << id_bits) < N) ++id_bits;
+            using BRS = cub::BlockRadixSort<uint32_t, kSortThreads, kSortItems, uint32_t>;
+            constexpr int sort_smem = (int)sizeof(typename BRS::TempStorage);
+            static PerDevice<bool> sort_attr;
+            {
+                auto lk = sort_attr.lock();
+                bool& done = sort_attr.at(ctx->device);
+                if (!done) {
+                    GX_CUDA(cudaFuncSetAttribute(k_sort_outs, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem));
+                    done = true;
+                }
+            }
+            k_sort_outs<<<(unsigned)std::min<uint64_t>(S, 2ull * ctx->num_sms), kSortThreads, sort_smem, st>>>(
+                d_out_off.p, (uint32_t)S, B.out_raw.p, B.out_tagraw.p, out->out_ids.p, B.tag_sorted.p,
+                B.fin_big.p, B.fin_big.p + S, id_bits);
+            GX_CHECK_LAUNCH();
         }
         B.fin_unres.reserve(64);
         GX_CUDA(cudaMemsetAsync(B.fin_unres.p, 0, 64 * 4, st));
@@ -2503,11 +2624,18 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         fa.R = is.next_use.p;  // next use is dead after the recurrence
         fa.in_off = d_in_off.p;
         fa.out_off = d_out_off.p;
+        fa.out_ids = out->out_ids.p;
         fa.out_tag = B.tag_sorted.p;
+        fa.out_raw = B.out_raw.p;
+        fa.out_tagraw = B.out_tagraw.p;
+        fa.big = B.fin_big.p;
+        fa.nbig = B.fin_big.p + S;
+        fa.bm_words = B.bm_words.p;
+        fa.nwords = (uint32_t)((N + 31) / 32);
+        fa.last = is.last.p;
         fa.o_in_ids = out->in_ids.p;
         fa.o_in_pos = out->in_pos.p;
         fa.o_in_slot = out->in_slot.p;
-        fa.tile_cnt = B.tile_cnt.p;
         fa.unres = B.fin_unres.p;
         fa.S = (uint32_t)S;
         fa.A = (uint32_t)A;
@@ -2523,9 +2651,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
             if (c < 1) fail(GX_CUDA_ERROR, "finish kernel cannot be resident");
             bps = std::min(c, 2);
         }
-        const uint32_t need = (uint32_t)((A + FIN_TILE - 1) / FIN_TILE);
-        B.tile_cnt.reserve(need + 1);
-        fa.tile_cnt = B.tile_cnt.p;
+        B.chunk_cnt.reserve(2 * (uint64_t)ctx->num_sms * bps + 1);
+        fa.cta_cnt = B.chunk_cnt.p;
         void* fargs[] = {&fa};
         barrier_reset(fa.bar, st);
         const dim3 fg(ctx->num_sms * bps);
