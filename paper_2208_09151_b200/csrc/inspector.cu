@@ -678,6 +678,27 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         }
         __syncthreads();
     }
+    // P1's static loads (node key, next use) of the next iteration are issued
+    // before the end-of-iteration barrier when the chunk is one pass
+    constexpr int PU = 4;
+    uint32_t pf_nk[PU], pf_nu[PU];
+    bool pf = false;
+    auto prefetch = [&](uint32_t i1) {
+        pf = false;
+        if (i1 >= S) return;
+        const uint32_t b1 = sm.toff[i1], n1 = sm.toff[i1 + 1] - b1;
+        const uint32_t ch1 = (n1 + gridDim.x - 1) / gridDim.x;
+        const uint32_t d0 = min(n1, blockIdx.x * ch1), d1 = min(n1, d0 + ch1);
+        if (d1 - d0 > PU * blockDim.x) return;
+#pragma unroll
+        for (int j = 0; j < PU; ++j) {
+            const uint32_t pos = d0 + tid + j * blockDim.x;
+            pf_nk[j] = pos < d1 ? (a.dense ? a.acc_slot[b1 + pos] : a.trace[b1 + pos]) : 0u;
+            pf_nu[j] = pos < d1 ? a.next_use[b1 + pos] : 0u;
+        }
+        pf = true;
+    };
+    prefetch(0);
     for (uint32_t i = 0; i < S; ++i) {
         IPHASE(a, 0);
         IState* cs = a.st + (i & 1);
@@ -695,10 +716,15 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             if (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in || ps->n_pool != ps->n_take)
                 atomicOr(&a.st->err, 8u);
         }
+        // this iteration's new-candidate histogram (double-buffered: the other
+        // buffer was last read by the previous iteration's b* scans and is
+        // reset here for the next one)
+        uint32_t* const hn = a.hist_new + (i & 1) * (S + 1);
         if (one) {
             for (uint32_t b = tid; b < 2048; b += blockDim.x) sm.rh[b] = 0;
         } else {
             for (uint32_t b = gtid; b < 3 * 2048; b += G) a.rh[b] = 0;  // last read before the previous barrier
+            for (uint32_t b = gtid; b <= S; b += G) a.hist_new[((i + 1) & 1) * (S + 1) + b] = 0;
         }
 
         // P1: hits refresh their key and record their occupancy tag; misses
@@ -707,18 +733,25 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             uint32_t miss = 0, hits = 0;
             // PU positions per thread at a time: their key, node_slot and tag
             // loads overlap (the chain is latency-bound otherwise)
-            constexpr int PU = 4;
             for (uint32_t p0 = c0 + tid; p0 < c1; p0 += PU * blockDim.x) {
                 uint32_t nk[PU], nu[PU], tg[PU], vv[PU];
                 int32_t sl[PU];
+                if (pf) {  // (one pass: the values were loaded during the previous barrier)
 #pragma unroll
-                for (int j = 0; j < PU; ++j) {
-                    const uint32_t pos = p0 + j * blockDim.x;
-                    nk[j] = 0;
-                    nu[j] = 0;
-                    if (pos < c1) {
-                        nk[j] = a.dense ? a.acc_slot[base + pos] : a.trace[base + pos];
-                        nu[j] = a.next_use[base + pos];
+                    for (int j = 0; j < PU; ++j) {
+                        nk[j] = pf_nk[j];
+                        nu[j] = pf_nu[j];
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < PU; ++j) {
+                        const uint32_t pos = p0 + j * blockDim.x;
+                        nk[j] = 0;
+                        nu[j] = 0;
+                        if (pos < c1) {
+                            nk[j] = a.dense ? a.acc_slot[base + pos] : a.trace[base + pos];
+                            nu[j] = a.next_use[base + pos];
+                        }
                     }
                 }
 #pragma unroll
@@ -762,9 +795,9 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 if (!one) a.chunk_miss[blockIdx.x] = miss;
                 sm.hinc[i] -= (int32_t)hits;  // all incumbents keyed i are exactly the hits
             }
-            if (!one) {
+            if (!one) {  // (hinc / NEVER deltas of the previous iteration's P3 and final go too)
                 hist_flush(sm.hinc, a.hist_inc, S + 1);
-                hist_flush(sm.hnew, (int32_t*)a.hist_new, S + 1);
+                hist_flush(sm.hnew, (int32_t*)hn, S + 1);
                 if (a.nv) hist_flush(sm.nh, a.never_hist, 2048);
             }
             if (one) {
@@ -801,11 +834,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 for (uint32_t b = tid; b <= S; b += blockDim.x) sm.hnew[b] = 0;
                 l_nres = nres + m;
                 l_in = in_total + m;
-            } else {
-                hist_flush(sm.hinc, a.hist_inc, S + 1);
-                if (a.nv) hist_flush(sm.nh, a.never_hist, 2048);
-                for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
             }
+            // (shared-memory histogram deltas are flushed by the next P1)
             if (gtid == 0) {
                 a.o_misses[i] = m;
                 cs->exp_out = 0;
@@ -821,6 +851,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 a.o_in_off[i + 1] = in_total + m;
                 a.o_out_off[i + 1] = out_total;
             }
+            prefetch(i + 1);
             grid_sync(a.bar);
             IPHASE(a, 2);
             if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[30] += 1;
@@ -840,7 +871,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 uint32_t ci = 0, cn = 0;
                 if (b <= S) {
                     ci = one ? (uint32_t)sm.hinc[b] : (uint32_t)((volatile int32_t*)a.hist_inc)[b];
-                    cn = one ? (uint32_t)sm.hnew[b] : ((volatile uint32_t*)a.hist_new)[b];
+                    cn = one ? (uint32_t)sm.hnew[b] : ((volatile uint32_t*)hn)[b];
                 }
                 unsigned long long tot;
                 const unsigned long long bef =
@@ -901,8 +932,11 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         __syncthreads();
         int32_t* const nhp = a.nv ? sm.nh : nullptr;
         const bool coll = small && sel == 1;
+        // (no slot scan when nothing above b* leaves and b* needs no members)
+        const bool scan_slots = sel == 1 || evict_b || nres - inc_before - inc_b > 0;
         if (fastnv) never_scan(a, sm, nres, d1_nv, st_ev, st_c, cs, out_total, S);
-        else if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
+        else if (!scan_slots) {
+        } else if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
         else p3_scan<1>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
         __syncthreads();
         if (fastnv || coll) stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
@@ -924,9 +958,12 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         }
         if (sel && !one && !small && !fastnv) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
-        // (hinc deltas stay in shared memory until the final phase: other CTAs
-        // may still be reading hist_inc for b*)
-        grid_sync(a.bar);
+        // (hinc deltas stay in shared memory until the next P1: other CTAs may
+        // still be reading hist_inc for b*). Without a select nothing of P3 is
+        // read across CTAs before the final phase (leftover evictions meet
+        // through the pool), so the barrier is only for c_id / the digit
+        // histogram.
+        if (sel) grid_sync(a.bar);
         IPHASE(a, 3);
 
         uint32_t thr = 0xFFFFFFFFu;
@@ -1070,11 +1107,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             l_nres = nres + n_in - n_out;
             l_in = in_total + n_in;
             l_out = out_total + n_out;
-        } else {
-            hist_flush(sm.hinc, a.hist_inc, S + 1);
-            if (a.nv) hist_flush(sm.nh, a.never_hist, 2048);
-            for (uint32_t b = gtid; b <= S; b += G) a.hist_new[b] = 0;
         }
+        // (shared-memory histogram deltas are flushed by the next P1)
         if (gtid == 0) {
             if (n_out > n_in) atomicOr(&a.st->err, 4u);
             cs->exp_out = n_out;
@@ -1091,6 +1125,7 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             a.o_in_off[i + 1] = in_total + n_in;
             a.o_out_off[i + 1] = out_total + n_out;
         }
+        prefetch(i + 1);
         grid_sync(a.bar);
         IPHASE(a, 5);
     }
@@ -2265,9 +2300,9 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.slot_node.reserve(Keff + 1);
     B.slot_key.reserve(Keff + 1);
     B.hist_inc.reserve(S + 1);
-    B.hist_new.reserve(S + 1);
+    B.hist_new.reserve(2 * (S + 1));  // (double-buffered by the deferred recurrence)
     GX_CUDA(cudaMemsetAsync(B.hist_inc.p, 0, (S + 1) * 4, st));
-    GX_CUDA(cudaMemsetAsync(B.hist_new.p, 0, (S + 1) * 4, st));
+    GX_CUDA(cudaMemsetAsync(B.hist_new.p, 0, 2 * (S + 1) * 4, st));
     B.rh.reserve(3 * 2048);
     GX_CUDA(cudaMemsetAsync(B.rh.p, 0, 3 * 2048 * 4, st));
     B.pkey.reserve(maxw);
