@@ -661,7 +661,7 @@ __device__ __forceinline__ void never_scan(const IArgs& a, SM& sm, uint32_t nres
 }
 
 template <uint32_t CAP>
-__device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
+__device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
     const uint32_t S = a.S, K = a.K;
     const uint32_t tid = threadIdx.x;
     const uint32_t G = gridDim.x * blockDim.x;
@@ -670,7 +670,9 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
     // memory (no flushes, no global reads for b*) and the resident / list
     // counters in registers -- the grid barriers are __syncthreads already
     const bool one = gridDim.x == 1;
-    uint32_t l_nres = a.st->n_res, l_in = 0, l_out = 0;
+    // resident count and list totals: every CTA derives them from values it
+    // has after the iteration's barriers (no state round trip through memory)
+    uint32_t l_nres = *(volatile uint32_t*)&a.st->n_res, l_in = 0, l_out = 0;
     if (one) {
         for (uint32_t b = tid; b <= S; b += blockDim.x) {
             sm.hinc[b] = ((volatile int32_t*)a.hist_inc)[b];
@@ -707,15 +709,24 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         const uint32_t ni = sm.toff[i + 1] - base;
         const uint32_t chunk = (ni + gridDim.x - 1) / gridDim.x;
         const uint32_t c0 = min(ni, blockIdx.x * chunk), c1 = min(ni, c0 + chunk);
-        const uint32_t nres = one ? l_nres : *(volatile uint32_t*)&cs->n_res;
-        const uint32_t in_total = one ? l_in : *(volatile uint32_t*)&cs->in_total;
-        const uint32_t out_total = one ? l_out : *(volatile uint32_t*)&cs->out_total;
+        const uint32_t nres = l_nres, in_total = l_in, out_total = l_out;
         uint32_t m_one = 0;
-        if (i > 0 && gtid == 0) {  // the previous iteration handed out exactly its histogram counts
-            const volatile IState* ps = ns;
-            if (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in || ps->n_pool != ps->n_take)
+        if (gtid == 0) {
+            // the previous iteration handed out exactly its histogram counts;
+            // its counters are then free for the next iteration
+            volatile IState* ps = ns;
+            if (i > 0 && (ps->n_out != ps->exp_out || ps->n_ins != ps->exp_in || ps->n_pool != ps->n_take))
                 atomicOr(&a.st->err, 8u);
+            ps->n_out = 0;
+            ps->n_c = 0;
+            ps->n_ins = 0;
+            ps->n_pool = 0;
+            ps->n_take = 0;
         }
+        // certain ALLIN (even if every access missed, everything fits): the
+        // misses take fresh slots right in P1 and the iteration ends at P1's barrier
+        const bool sure = (uint64_t)nres + ni <= K;
+        uint32_t* const cmiss = (i & 1) ? a.chunk_in : a.chunk_miss;  // (parity: read after the barrier)
         // this iteration's new-candidate histogram (double-buffered: the other
         // buffer was last read by the previous iteration's b* scans and is
         // reset here for the next one)
@@ -733,7 +744,8 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             uint32_t miss = 0, hits = 0;
             // PU positions per thread at a time: their key, node_slot and tag
             // loads overlap (the chain is latency-bound otherwise)
-            for (uint32_t p0 = c0 + tid; p0 < c1; p0 += PU * blockDim.x) {
+            for (uint32_t q0 = c0; q0 < c1; q0 += PU * blockDim.x) {  // CTA-uniform (the sure path syncs)
+                const uint32_t p0 = q0 + tid;
                 uint32_t nk[PU], nu[PU], tg[PU], vv[PU];
                 int32_t sl[PU];
                 if (pf) {  // (one pass: the values were loaded during the previous barrier)
@@ -788,11 +800,26 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                         ++miss;
                     }
                 }
+                if (sure) {  // this pass's misses: slot tickets (the internal layout is free)
+                    uint32_t c = 0;
+#pragma unroll
+                    for (int j = 0; j < PU; ++j) c += p0 + j * blockDim.x < c1 && sl[j] < 0;
+                    uint32_t tot;
+                    uint32_t k = block_excl_scan(c, sm.scan, tot);
+                    if (tid == 0 && tot) sm.bc[11] = atomicAdd(&cs->n_ins, tot);
+                    __syncthreads();
+#pragma unroll
+                    for (int j = 0; j < PU; ++j) {
+                        const uint32_t pos = p0 + j * blockDim.x;
+                        if (pos < c1 && sl[j] < 0) place_ins(a, sm, base + pos, nu[j], nk[j], nres + sm.bc[11] + k++, S);
+                    }
+                    __syncthreads();  // bc[11] is rewritten by the next pass
+                }
             }
             miss = block_sum(miss, sm.scan);
             hits = block_sum(hits, sm.scan);
             if (tid == 0) {
-                if (!one) a.chunk_miss[blockIdx.x] = miss;
+                if (!one) cmiss[blockIdx.x] = miss;
                 sm.hinc[i] -= (int32_t)hits;  // all incumbents keyed i are exactly the hits
             }
             if (!one) {  // (hinc / NEVER deltas of the previous iteration's P3 and final go too)
@@ -811,12 +838,31 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         if (!one) {
             uint32_t pre = 0, tot = 0;
             for (uint32_t c = tid; c < gridDim.x; c += blockDim.x) {
-                const uint32_t v = a.chunk_miss[c];
+                const uint32_t v = cmiss[c];
                 if (c < blockIdx.x) pre += v;
                 tot += v;
             }
             mpre = block_sum(pre, sm.scan);
             m = block_sum(tot, sm.scan);
+        }
+        if (sure) {  // (placed in P1; P1's barrier ended the iteration)
+            l_nres = nres + m;
+            l_in = in_total + m;
+            if (one) {
+                for (uint32_t b = tid; b <= S; b += blockDim.x) sm.hnew[b] = 0;
+                __syncthreads();
+            }
+            if (gtid == 0) {
+                a.o_misses[i] = m;
+                cs->exp_out = 0;
+                cs->exp_in = m;
+                a.o_in_off[i + 1] = in_total + m;
+                a.o_out_off[i + 1] = out_total;
+            }
+            prefetch(i + 1);
+            IPHASE(a, 2);
+            if (a.tstamp && blockIdx.x == 0 && tid == 0) a.tstamp[30] += 1;
+            continue;
         }
         if ((uint64_t)nres + m <= K) {
             // ALLIN: every miss enters, in position order, the next fresh slots
@@ -832,22 +878,14 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             if (one) {
                 __syncthreads();
                 for (uint32_t b = tid; b <= S; b += blockDim.x) sm.hnew[b] = 0;
-                l_nres = nres + m;
-                l_in = in_total + m;
             }
+            l_nres = nres + m;
+            l_in = in_total + m;
             // (shared-memory histogram deltas are flushed by the next P1)
             if (gtid == 0) {
                 a.o_misses[i] = m;
                 cs->exp_out = 0;
                 cs->exp_in = 0;
-                ns->n_res = nres + m;
-                ns->in_total = in_total + m;
-                ns->out_total = out_total;
-                ns->n_out = 0;
-                ns->n_c = 0;
-                ns->n_ins = 0;
-                ns->n_pool = 0;
-                ns->n_take = 0;
                 a.o_in_off[i + 1] = in_total + m;
                 a.o_out_off[i + 1] = out_total;
             }
@@ -1104,24 +1142,16 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         if (one) {
             __syncthreads();
             for (uint32_t b = tid; b <= S; b += blockDim.x) sm.hnew[b] = 0;
-            l_nres = nres + n_in - n_out;
-            l_in = in_total + n_in;
-            l_out = out_total + n_out;
         }
+        l_nres = nres + n_in - n_out;
+        l_in = in_total + n_in;
+        l_out = out_total + n_out;
         // (shared-memory histogram deltas are flushed by the next P1)
         if (gtid == 0) {
             if (n_out > n_in) atomicOr(&a.st->err, 4u);
             cs->exp_out = n_out;
             cs->exp_in = n_in;
             a.o_misses[i] = m;
-            ns->n_res = nres + n_in - n_out;
-            ns->in_total = in_total + n_in;
-            ns->out_total = out_total + n_out;
-            ns->n_out = 0;
-            ns->n_c = 0;
-            ns->n_ins = 0;
-            ns->n_pool = 0;
-            ns->n_take = 0;
             a.o_in_off[i + 1] = in_total + n_in;
             a.o_out_off[i + 1] = out_total + n_out;
         }
@@ -1129,11 +1159,15 @@ __device__ void recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         grid_sync(a.bar);
         IPHASE(a, 5);
     }
-    if (S > 0 && gtid == 0) {
-        const volatile IState* ls = a.st + ((S - 1) & 1);
-        if (ls->n_out != ls->exp_out || ls->n_ins != ls->exp_in || ls->n_pool != ls->n_take)
-            atomicOr(&a.st->err, 8u);
+    if (S > 0) {
+        grid_sync(a.bar);  // (a certain-ALLIN last iteration ends without its own barrier)
+        if (gtid == 0) {
+            const volatile IState* ls = a.st + ((S - 1) & 1);
+            if (ls->n_out != ls->exp_out || ls->n_ins != ls->exp_in || ls->n_pool != ls->n_take)
+                atomicOr(&a.st->err, 8u);
+        }
     }
+    return l_nres;
 }
 
 // PART 1 next use of a trusted trace with dense node keys: every access takes
@@ -1448,7 +1482,8 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     // ---- the recurrence -------------------------------------------------------
     // State counters are double-buffered by iteration parity: iteration i reads
     // st[i&1] and CTA 0 writes st[(i+1)&1] in the iteration's last grid step.
-    if (a.defer) recurrence_deferred<CAP>(a, sm);
+    uint32_t nfin_def = 0;
+    if (a.defer) nfin_def = recurrence_deferred<CAP>(a, sm);
     for (uint32_t i = 0; !a.defer && i < S; ++i) {
         IPHASE(a, 0);
         IState* cs = a.st + (i & 1);
@@ -1966,7 +2001,7 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     }
     ISTAMP(a, 7);
     // leave node_slot clean
-    const uint32_t nfin = a.st[S & 1].n_res;
+    const uint32_t nfin = a.defer ? nfin_def : a.st[S & 1].n_res;
     for (uint32_t s = gtid; s < nfin; s += G) a.node_slot[a.defer ? a.slot_nk[s] : a.slot_node[s]] = -1;
     if (gtid == 0) a.st->n_res = nfin;  // final resident count for the host
 }
