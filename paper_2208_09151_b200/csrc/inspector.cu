@@ -486,8 +486,8 @@ __device__ __forceinline__ void ev_flush(const IArgs& a, Stage st, IState* cs, u
 // a missed access x enters internal slot s with key `key`
 template <class SM>
 __device__ __forceinline__ void place_ins(const IArgs& a, SM& sm, uint32_t x, uint32_t key, uint32_t nk, uint32_t s,
-                                          uint32_t S) {
-    const uint32_t v = a.trace[x];
+                                          uint32_t S, uint32_t v = kNever) {
+    if (v == kNever) v = a.trace[x];
     a.slot_node[s] = v;
     a.slot_key[s] = key;
     a.slot_tag[s] = kEv | x;
@@ -1062,6 +1062,37 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         // beyond the insertions and the n_in - n_out fresh slots are published,
         // insertions beyond E take pool tickets -- every CTA publishes before it
         // takes, so the waits end.
+        // this CTA's insertions first (their loads overlap the evictions below):
+        // flags, keys, node keys and ids in registers when the chunk is at most
+        // FQ positions per thread, else recounted in the placement loop
+        auto ins_flag = [&](uint32_t pos, uint32_t& key, uint32_t& v) -> bool {
+            if (pos >= c1) return false;
+            const uint8_t pm = a.pmiss[pos];
+            key = a.pkey[pos];
+            v = a.trace[base + pos];
+            if (!pm) return false;
+            const uint32_t bk = bucket_of(key, S);
+            if (bk != bstar) return bk < bstar;
+            return admit_new != 0 && (sel != 2 || v <= thr);
+        };
+        constexpr int FQ = 4;
+        const bool reg = c1 - c0 <= FQ * blockDim.x;
+        uint32_t fkey[FQ], fv[FQ], fnk[FQ], fmask = 0, cnt = 0;
+        if (n_in) {
+            if (reg) {
+#pragma unroll
+                for (int j = 0; j < FQ; ++j) {
+                    const uint32_t pos = c0 + tid + j * blockDim.x;
+                    fnk[j] = pos < c1 ? a.pnk[pos] : 0u;
+                    if (ins_flag(pos, fkey[j], fv[j])) fmask |= 1u << j;
+                }
+                cnt = __popc(fmask);
+            } else {
+                uint32_t key, v;
+                for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) cnt += ins_flag(pos, key, v);
+            }
+        }
+        // b*'s last evictions (sel 1: ids above the cut) join this CTA's list E
         if (sel == 1) {
             const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
             for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < nc; k0 += G) {  // CTA-uniform
@@ -1073,32 +1104,13 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], nhp);
             }
         }
+        // this CTA's k-th insertion takes E[k]; only leftovers meet through the
+        // pool: E beyond the insertions and the n_in - n_out fresh slots are
+        // published, insertions beyond E take pool tickets -- every CTA
+        // publishes before it takes, so the waits end
         if (n_in) {  // (n_out <= n_in: nothing leaves either when nothing enters)
             __syncthreads();
             const uint32_t nE = *st_ev.cnt;
-            auto ins_flag = [&](uint32_t pos, uint32_t& key) -> bool {
-                if (pos >= c1) return false;
-                const uint8_t pm = a.pmiss[pos];
-                key = a.pkey[pos];
-                if (!pm) return false;
-                const uint32_t bk = bucket_of(key, S);
-                if (bk != bstar) return bk < bstar;
-                return admit_new != 0 && (sel != 2 || a.trace[base + pos] <= thr);
-            };
-            // this CTA's insertions: flags and keys in registers when the chunk
-            // is at most FQ positions per thread, else recounted below
-            constexpr int FQ = 4;
-            const bool reg = c1 - c0 <= FQ * blockDim.x;
-            uint32_t fkey[FQ], fmask = 0, cnt = 0;
-            if (reg) {
-#pragma unroll
-                for (int j = 0; j < FQ; ++j)
-                    if (ins_flag(c0 + tid + j * blockDim.x, fkey[j])) fmask |= 1u << j;
-                cnt = __popc(fmask);
-            } else {
-                uint32_t key;
-                for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x) cnt += ins_flag(pos, key);
-            }
             uint32_t nI;
             const uint32_t ex = block_excl_scan(cnt, sm.scan, nI);
             const uint32_t F = n_in - n_out;  // fresh slots, spread over the CTAs
@@ -1122,21 +1134,20 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             for (uint32_t j = fr0 + tid; j < fr1; j += blockDim.x)
                 st_release_u32(a.ev_slot + sm.bc[14] + (j - fr0), nres + j);
             __syncthreads();  // E's out records read their slots before any placement rewrites them
-            // the k-th insertion of the CTA takes E[k], or pool ticket k - nE
             uint32_t k = ex;
-            auto place_k = [&](uint32_t pos, uint32_t key) {
+            auto place_k = [&](uint32_t pos, uint32_t key, uint32_t nk, uint32_t v) {
                 const uint32_t sl = k < nE ? (uint32_t)st_ev.buf[k] : take_slot(a.ev_slot, sm.bc[15] + (k - nE));
-                place_ins(a, sm, base + pos, key, a.pnk[pos], sl, S);
+                place_ins(a, sm, base + pos, key, nk, sl, S, v);
                 ++k;
             };
             if (reg) {
 #pragma unroll
                 for (int j = 0; j < FQ; ++j)
-                    if (fmask & (1u << j)) place_k(c0 + tid + j * blockDim.x, fkey[j]);
+                    if (fmask & (1u << j)) place_k(c0 + tid + j * blockDim.x, fkey[j], fnk[j], fv[j]);
             } else {
-                uint32_t key;
+                uint32_t key, v;
                 for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x)
-                    if (ins_flag(pos, key)) place_k(pos, key);
+                    if (ins_flag(pos, key, v)) place_k(pos, key, a.pnk[pos], v);
             }
         }
         if (one) {
