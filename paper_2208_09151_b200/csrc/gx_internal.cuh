@@ -76,7 +76,7 @@ struct InspectScratch {
     DevBuf<int32_t> hist_inc;
     DevBuf<uint8_t> pmiss;
     // deferred-ordering recurrence (inspector.cu: recurrence_deferred, k_finish_changesets)
-    DevBuf<uint32_t> slot_tag, slot_nk, pnk, out_raw, out_tagraw, tag_sorted, ev_slot, ins_x, fin_unres, blk_max, fin_big;
+    DevBuf<uint32_t> slot_tag, slot_nk, pnk, out_raw, out_tagraw, tag_sorted, ev_slot, fin_unres, blk_max, fin_big;
     DevBuf<int32_t> never_hist;
     DevBuf<uint8_t> sort_tmp;
     DevBuf<uint32_t> o_misses, o_in_off, o_out_off;  // per-iteration outputs (S+1)

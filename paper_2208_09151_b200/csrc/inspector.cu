@@ -128,7 +128,6 @@ struct IArgs {
     uint32_t* out_raw;     // A: evicted node per out ticket (iteration-major, unordered)
     uint32_t* out_tagraw;  // A: the evicted occupancy's tag
     uint32_t* ev_slot;     // maxw: internal slot freed by eviction ticket t (kNever = not yet)
-    uint32_t* ins_x;       // maxw: access of a certain insertion whose eviction comes later
     // dense node keys (trusted traces, deferred recurrence): a node is keyed by
     // the rank of its first access among first accesses (< n_first, the init
     // order), so node_slot / the next-use bitmask / `last` touch an n_first-sized
@@ -2367,7 +2366,6 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         B.tag_sorted.reserve(A + 1);
         B.ev_slot.reserve(maxw);
         GX_CUDA(cudaMemsetAsync(B.ev_slot.p, 0xff, maxw * 4, st));  // every ticket "not yet published"
-        B.ins_x.reserve(maxw);
         B.slot_nk.reserve(Keff + 1);
         B.pnk.reserve(maxw);
         B.never_hist.reserve(2048);
@@ -2518,7 +2516,6 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.out_raw = B.out_raw.p;
     a.out_tagraw = B.out_tagraw.p;
     a.ev_slot = B.ev_slot.p;
-    a.ins_x = B.ins_x.p;
     a.slot_nk = B.slot_nk.p;
     a.pnk = B.pnk.p;
     a.dense = defer && a.trusted;
