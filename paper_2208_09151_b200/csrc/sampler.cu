@@ -71,6 +71,14 @@ constexpr uint32_t SB_TILE = SB_THREADS * SB_IPT;
 #endif
 constexpr int SB_DIPT = GX_SB_DIPT;
 constexpr uint32_t SB_DTILE = SB_THREADS * SB_DIPT;
+// F/H move a thread's SB_DIPT = 4 consecutive draws as 16-byte words (dslot,
+// drank: one uint4; edges: two uint4) -- the per-batch draw / edge regions are
+// padded to multiples of 4 draws so these are aligned and stay inside the
+// region (GX_SB_VEC=0: the scalar per-draw form, 4 words per warp sector)
+#ifndef GX_SB_VEC
+#define GX_SB_VEC 1
+#endif
+static_assert(!GX_SB_VEC || SB_DIPT == 4, "vectorised F/H phases move 4 draws per thread");
 constexpr uint32_t kNewBit = 0x80000000u;
 constexpr unsigned long long kEmptySlot = ~0ull;
 // batches per launch cap: sizes SampSmem's prefix arrays, and a small SampSmem
@@ -656,6 +664,26 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 const unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
                 const uint2* bedge = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
                 uint32_t s = 0;
+#if GX_SB_VEC
+                if (p0 < Tb) {
+                    const uint64_t gd0 = (uint64_t)b * a.cap_draw + p0;
+                    const uint4 d4 = *reinterpret_cast<const uint4*>(a.dslot + gd0);
+                    const uint4 e01 = *reinterpret_cast<const uint4*>(bedge + p0);
+                    const uint4 e23 = *reinterpret_cast<const uint4*>(bedge + p0 + 2);
+                    const uint32_t ds[4] = {d4.x, d4.y, d4.z, d4.w}, ch[4] = {e01.x, e01.z, e23.x, e23.z};
+                    uint32_t fl[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        fl[j] = 0;
+                        if (p0 + j < Tb && !(ds[j] & kResolved)) {
+                            const unsigned long long e = btab[ds[j]];
+                            fl[j] = e == (((unsigned long long)ch[j] << 32) | (kNewBit | (p0 + j))) ? 1u : 0u;
+                        }
+                        s += fl[j];
+                    }
+                    *reinterpret_cast<uint4*>(a.drank + gd0) = make_uint4(fl[0], fl[1], fl[2], fl[3]);
+                }
+#else
 #pragma unroll
                 for (int j = 0; j < SB_DIPT; ++j) {
                     const uint32_t p = p0 + j;
@@ -672,6 +700,7 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                         s += fl;
                     }
                 }
+#endif
                 uint32_t tot = block_sum(s, sm.scan);
                 if (tid == 0) a.tsum2[t] = tot;
             }
@@ -697,17 +726,61 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 const uint32_t p0 = (t - first) * SB_DTILE + tid * SB_DIPT;
                 uint32_t fl[SB_DIPT];
                 uint32_t s = 0;
+#if GX_SB_VEC
+                const uint64_t gd0 = (uint64_t)b * a.cap_draw + p0;
+                uint4 r4 = make_uint4(0, 0, 0, 0);
+                if (p0 < Tb) r4 = *reinterpret_cast<const uint4*>(a.drank + gd0);
+                fl[0] = r4.x;
+                fl[1] = p0 + 1 < Tb ? r4.y : 0u;
+                fl[2] = p0 + 2 < Tb ? r4.z : 0u;
+                fl[3] = p0 + 3 < Tb ? r4.w : 0u;
+                s = fl[0] + fl[1] + fl[2] + fl[3];
+#else
 #pragma unroll
                 for (int j = 0; j < SB_DIPT; ++j) {
                     const uint32_t p = p0 + j;
                     fl[j] = p < Tb ? a.drank[(uint64_t)b * a.cap_draw + p] : 0;
                     s += fl[j];
                 }
+#endif
                 uint32_t tot;
                 uint32_t r = toff + block_excl_scan(s, sm.scan, tot);
                 unsigned long long* btab = tab + (uint64_t)b * a.tab_cap;
                 uint2* bedge_w = a.edges + (uint64_t)b * a.cap_e_batch + a.e_off[l];
                 const uint2* bedge = bedge_w;
+#if GX_SB_VEC
+                if (s) {  // winners: the thread's 4 edges (and rank words) rewritten as 16-byte words
+                    uint4 e01 = *reinterpret_cast<const uint4*>(bedge + p0);
+                    uint4 e23 = *reinterpret_cast<const uint4*>(bedge + p0 + 2);
+                    uint32_t ch[4] = {e01.x, e01.z, e23.x, e23.z}, rk[4] = {r4.x, r4.y, r4.z, r4.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        if (fl[j]) {
+                            const uint32_t child = ch[j];
+                            const uint32_t local = Fb + r;
+                            a.ids[(uint64_t)b * a.cap_ids + local] = child;
+                            if (a.firstx)  // fire-and-forget: overlaps the latency-bound phases
+                                atomicMax(&a.firstx[child], a.fx_epoch - (((a.batch0 + b) << 21) | local));
+                            if (last_layer) {
+                                rk[j] = local;  // phase I follows the table's winning position here
+                            } else {
+                                const uint32_t slot = a.dslot[gd0 + j];
+                                btab[slot] = ((unsigned long long)child << 32) | local;
+                            }
+                            ch[j] = local;
+                            ++r;
+                        }
+                    }
+                    e01.x = ch[0];
+                    e01.z = ch[1];
+                    e23.x = ch[2];
+                    e23.z = ch[3];
+                    *reinterpret_cast<uint4*>(bedge_w + p0) = e01;
+                    *reinterpret_cast<uint4*>(bedge_w + p0 + 2) = e23;
+                    if (last_layer) *reinterpret_cast<uint4*>(a.drank + gd0) = make_uint4(rk[0], rk[1], rk[2], rk[3]);
+                }
+                if (false)
+#endif
 #pragma unroll
                 for (int j = 0; j < SB_DIPT; ++j) {
                     if (fl[j]) {
@@ -1035,8 +1108,8 @@ bool sample_run(gx_graph* g, const uint64_t* seeds_flat, const uint64_t* batch_o
         if (c >= (1ull << 31)) fail(GX_INVALID_ARGUMENT, "batch too large: > 2^31 draws per layer");
         out->e_off[l] = ce;
         out->cap_e[l] = c;
-        ce += c;
-        cap_draw = std::max(cap_draw, c);
+        ce += (c + 3) & ~3ull;  // (layer regions in multiples of 4 edges: 16-byte aligned, see GX_SB_VEC)
+        cap_draw = std::max<uint64_t>(cap_draw, (c + 3) & ~3ull);
     }
     out->cap_e_batch = std::max<uint64_t>(ce, 1);
     out->ids.reserve(S * cap_ids);
