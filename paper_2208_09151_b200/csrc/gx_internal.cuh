@@ -79,7 +79,7 @@ struct InspectScratch {
     DevBuf<uint32_t> slot_tag, slot_nk, pnk, out_raw, out_tagraw, tag_sorted, ev_slot, fin_unres, blk_max, fin_big;
     DevBuf<int32_t> never_hist;
     DevBuf<uint8_t> sort_tmp;
-    DevBuf<uint32_t> o_misses, o_in_off, o_out_off;  // per-iteration outputs (S+1)
+    DevBuf<uint32_t> o_pack;  // 2 IStates (32 words), then misses / in_off / out_off (S+1 each)
     DevBuf<unsigned long long> bits;  // N * ceil(S/64) iteration bitmask, clean between calls
     uint64_t bits_words = 0;
     DevBuf<uint8_t> isfirst;

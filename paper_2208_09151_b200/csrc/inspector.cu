@@ -144,6 +144,7 @@ struct IArgs {
     int nv;
     int32_t* never_hist;   // 2048
     uint32_t* blk_max;     // ceil(K / 16)
+    uint32_t n_blk;        // its length
 };
 
 constexpr uint32_t kEv = 0x80000000u;  // tag bit: the occupancy began at access (tag & ~kEv)
@@ -1264,6 +1265,16 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     __syncthreads();
     const uint32_t ntiles = (a.A + IN_TILE - 1) / IN_TILE;
     if (PART == 0) {
+    // recurrence histograms start clean (first flushed after several grid
+    // barriers below; in-kernel instead of four memsets per call)
+    for (uint32_t b = gtid; b <= S; b += G) {
+        a.hist_inc[b] = 0;
+        a.hist_new[b] = 0;
+        a.hist_new[S + 1 + b] = 0;
+    }
+    for (uint32_t b = gtid; b < 3 * 2048; b += G) a.rh[b] = 0;
+    if (a.never_hist)
+        for (uint32_t b = gtid; b < 2048; b += G) a.never_hist[b] = 0;
 
     // ---- first occurrences, next use ---------------------------------------
     bool have_next = false;
@@ -1480,6 +1491,11 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
     if (*(volatile uint32_t*)&a.st->err) return;  // PART 0 found a bad trace (the host reports it)
     if (!a.explicit_init && *(volatile uint32_t*)&a.st->n_first <= K) return;  // all-fit: done
     const bool have_next = !a.trusted;  // untrusted traces computed next use in PART 0
+    if (a.defer) {  // the recurrence's pool and NEVER summary start clean (first used after barriers)
+        for (uint32_t k = gtid; k < a.maxw; k += G) a.ev_slot[k] = kNever;
+        if (a.nv)
+            for (uint32_t k = gtid; k < a.n_blk; k += G) a.blk_max[k] = 0;
+    }
     if (!have_next) {
         if (a.dense) next_use_dense(a, sm);
         else next_use_pass(a, sm, false);
@@ -2346,10 +2362,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     B.slot_key.reserve(Keff + 1);
     B.hist_inc.reserve(S + 1);
     B.hist_new.reserve(2 * (S + 1));  // (double-buffered by the deferred recurrence)
-    GX_CUDA(cudaMemsetAsync(B.hist_inc.p, 0, (S + 1) * 4, st));
-    GX_CUDA(cudaMemsetAsync(B.hist_new.p, 0, 2 * (S + 1) * 4, st));
     B.rh.reserve(3 * 2048);
-    GX_CUDA(cudaMemsetAsync(B.rh.p, 0, 3 * 2048 * 4, st));
     B.pkey.reserve(maxw);
     B.pmiss.reserve(maxw);
     B.out_node.reserve(maxw);
@@ -2365,7 +2378,6 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         B.out_tagraw.reserve(A + 1);
         B.tag_sorted.reserve(A + 1);
         B.ev_slot.reserve(maxw);
-        GX_CUDA(cudaMemsetAsync(B.ev_slot.p, 0xff, maxw * 4, st));  // every ticket "not yet published"
         B.slot_nk.reserve(Keff + 1);
         B.pnk.reserve(maxw);
         B.never_hist.reserve(2048);
@@ -2381,9 +2393,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     const int grid0 = ctx->num_sms * GX_IN_FRONT_BPS;                                      // PART 0
     B.chunk_cnt.reserve(2 * std::max(grid, grid0));
     B.bm_cnt.reserve(std::max(grid, grid0));
-    B.st.reserve(32);
-    GX_CUDA(cudaMemsetAsync(B.st.p, 0, 2 * sizeof(IState), st));
-    static_assert(2 * sizeof(IState) <= 32 * sizeof(uint32_t), "2 IStates fit the scratch words");
+
     B.isfirst.reserve(std::max<uint64_t>(A, 1));
     // per-node iteration bitmask (next use in 3 grid steps) when it fits the budget
     const uint64_t W = (S + 63) / 64;
@@ -2405,10 +2415,14 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     out->in_pos.reserve(A + 1);
     out->in_slot.reserve(A + 1);
     out->out_ids.reserve(A + 1);
-    B.o_misses.reserve(S + 1);
-    B.o_in_off.reserve(S + 1);
-    B.o_out_off.reserve(S + 1);
-    DevBuf<uint32_t>&d_misses = B.o_misses, &d_in_off = B.o_in_off, &d_out_off = B.o_out_off;
+    // the two IStates and the per-iteration outputs in one buffer: one readback
+    constexpr uint32_t kStWords = 32;
+    static_assert(2 * sizeof(IState) <= kStWords * sizeof(uint32_t), "2 IStates fit the packed header");
+    B.o_pack.reserve(kStWords + 3 * (S + 1));
+    struct {
+        uint32_t* p;
+    } d_misses{B.o_pack.p + kStWords}, d_in_off{B.o_pack.p + kStWords + (S + 1)},
+        d_out_off{B.o_pack.p + kStWords + 2 * (S + 1)};
 
     if (n_init_explicit >= 0) {
         std::vector<uint32_t> i32(std::max<int64_t>(n_init_explicit, 1));
@@ -2509,7 +2523,8 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.o_misses = d_misses.p;
     a.o_in_off = d_in_off.p;
     a.o_out_off = d_out_off.p;
-    a.st = reinterpret_cast<IState*>(B.st.p);
+    a.st = reinterpret_cast<IState*>(B.o_pack.p);
+    GX_CUDA(cudaMemsetAsync(B.o_pack.p, 0, 2 * sizeof(IState), st));
     a.bar = ctx->barrier.p;
     a.defer = defer;
     a.slot_tag = defer ? B.slot_tag.p : nullptr;
@@ -2526,10 +2541,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.nv = defer && never_knob && grid > 1 && (never_knob == 2 || Keff >= 8ull * (uint64_t)grid * IN_THREADS);
     a.never_hist = B.never_hist.p;
     a.blk_max = B.blk_max.p;
-    if (a.nv) {
-        GX_CUDA(cudaMemsetAsync(B.never_hist.p, 0, 2048 * 4, st));
-        GX_CUDA(cudaMemsetAsync(B.blk_max.p, 0, (Keff / 16 + 1) * 4, st));
-    }
+    a.n_blk = (uint32_t)(Keff / 16 + 1);
     // dense keys: the bitmask (3 grid passes over an n_first x W prefix) by
     // default; GX_DENSE_NEXT=last: one grid step per iteration over the
     // L2-resident `last` prefix (measured cfg1 357 vs 220 us, papers@5 % 905 vs
@@ -2623,13 +2635,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     m32.resize(S + 1);
     io32.resize(S + 1);
     oo32.resize(S + 1);
-    const size_t hs_bytes = (sizeof(IState) + 15) / 16 * 16, arr_bytes = (S + 1) * 4;
+    const size_t hs_bytes = kStWords * 4, arr_bytes = (S + 1) * 4;
     B.h_pin.reserve(hs_bytes + 3 * arr_bytes);
     uint8_t* hp = B.h_pin.p;
-    GX_CUDA(cudaMemcpyAsync(hp, a.st, sizeof(IState), cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(hp + hs_bytes, d_misses.p, arr_bytes, cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(hp + hs_bytes + arr_bytes, d_in_off.p, arr_bytes, cudaMemcpyDeviceToHost, st));
-    GX_CUDA(cudaMemcpyAsync(hp + hs_bytes + 2 * arr_bytes, d_out_off.p, arr_bytes, cudaMemcpyDeviceToHost, st));
+    GX_CUDA(cudaMemcpyAsync(hp, B.o_pack.p, hs_bytes + 3 * arr_bytes, cudaMemcpyDeviceToHost, st));
     if (tracing) GX_CUDA(cudaMemcpyAsync(htb.p, tbuf.p, (64 + 4 * 256) * 8, cudaMemcpyDeviceToHost, st));
     GX_CUDA(cudaStreamSynchronize(st));
     IState hs;
