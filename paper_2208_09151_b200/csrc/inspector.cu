@@ -111,6 +111,8 @@ struct IArgs {
     uint32_t* o_rest_x;  // all-fit + mark_first: accesses that are not a first use (dense) ...
     uint32_t* o_rest_slot;  // ... and their cache slots
     uint32_t* o_fan_cnt;    // all-fit + fan-out marks: accesses per init slot (K + 1)
+    uint32_t* o_fan_off;    // ... their list offsets (K + 1) and the lists (A), built in PART 0
+    uint32_t* o_fan_list;
     uint32_t* o_in_ids;
     uint32_t* o_in_pos;
     uint32_t* o_in_slot;
@@ -1460,6 +1462,39 @@ __device__ __forceinline__ void inspect_body(IArgs& a) {
                     }
                 }
             }
+            if (a.o_fan_off) {
+                // per-slot access lists right here (no scan / placement launches
+                // after a host round trip): counts -> offsets by a scan over the
+                // init slots (contiguous slot range per CTA), then every rest
+                // access takes the next entry of its slot's range; fan_off[s]
+                // ends as the range end = the start of slot s + 1 (k_fan_rows
+                // reads slot s as [fan_off[s - 1], fan_off[s]))
+                grid_sync(a.bar);
+                const uint32_t n = *(volatile uint32_t*)&a.st->n_first;  // all-fit: every first use has a slot
+                const uint32_t r0 = (uint32_t)((uint64_t)n * blockIdx.x / gridDim.x);
+                const uint32_t r1 = (uint32_t)((uint64_t)n * (blockIdx.x + 1) / gridDim.x);
+                uint32_t c = 0;
+                for (uint32_t r = r0 + tid; r < r1; r += blockDim.x) c += a.o_fan_cnt[r];
+                c = block_sum(c, sm.scan);
+                if (tid == 0) a.bm_cnt[blockIdx.x] = c;
+                grid_sync(a.bar);
+                uint32_t pre = 0;
+                for (uint32_t cc = tid; cc < blockIdx.x; cc += blockDim.x) pre += a.bm_cnt[cc];
+                pre = block_sum(pre, sm.scan);
+                for (uint32_t q0 = r0; q0 < r1; q0 += blockDim.x) {  // CTA-uniform
+                    const uint32_t r = q0 + tid;
+                    const uint32_t v = r < r1 ? a.o_fan_cnt[r] : 0u;
+                    uint32_t tot;
+                    const uint32_t ex = block_excl_scan(v, sm.scan, tot);
+                    if (r < r1) a.o_fan_off[r] = pre + ex;
+                    pre += tot;
+                }
+                if (blockIdx.x == gridDim.x - 1 && tid == 0) a.o_fan_off[n] = pre;
+                grid_sync(a.bar);
+                const uint32_t nr = a.A - n;
+                for (uint32_t k = gtid; k < nr; k += G)
+                    a.o_fan_list[atomicAdd(&a.o_fan_off[a.o_rest_slot[k]], 1u)] = a.o_rest_x[k];  // (written by this launch: no __ldg)
+            }
         } else if (a.trusted) {
             // the first occurrence of each access's node already holds the slot
             // (init pass); the lookups stay inside the A-sized acc_slot array
@@ -2504,9 +2539,16 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     a.o_first = nullptr;
     a.o_rest_x = a.o_rest_slot = nullptr;
     a.o_fan_cnt = nullptr;
+    a.o_fan_off = a.o_fan_list = nullptr;
     if (mark_first == 2 && a.trusted) {
         out->fan_cnt.reserve(Keff + 1);
         a.o_fan_cnt = out->fan_cnt.p;
+        // the lists are built inside PART 0 (sized by K and A: n_first is
+        // not known before the launch)
+        out->fan_off.reserve(Keff + 1);
+        out->fan_list.reserve(A + 1);
+        a.o_fan_off = out->fan_off.p;
+        a.o_fan_list = out->fan_list.p;
     }
     if (mark_first && a.trusted) {
         out->first_acc.reserve(Keff + 1);
@@ -2752,7 +2794,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     out->first_marked = (a.o_first != nullptr || a.o_fan_cnt != nullptr) && hs.n_first <= Keff;
     out->fan = out->first_marked && a.o_fan_cnt != nullptr;
     out->n_rest = out->first_marked ? A - hs.n_first : 0;
-    if (out->fan) {  // slot -> its other accesses: offsets by a scan of the counts, then placement
+    if (out->fan && !a.o_fan_off) {  // slot -> its other accesses: offsets by a scan of the counts, then placement
         const uint32_t n = (uint32_t)hs.n_first;
         const uint64_t nr = out->n_rest;
         out->fan_off.reserve((uint64_t)n + 1);
