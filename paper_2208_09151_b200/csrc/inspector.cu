@@ -2352,17 +2352,6 @@ uint32_t inspect_reserve_epoch(gx_ctx* ctx, uint64_t N, uint64_t keyrange) {
     return (uint32_t)is.fx_base;
 }
 
-// fan-out lists: each access that is not a first use (the dense rest list)
-// takes the next position of its slot's range; off[s] (the range start after
-// the scan) ends as the range end, i.e. the start of slot s + 1 -- the fan-out
-// kernel reads slot s as [off[s - 1], off[s]). The order inside a range is
-// arbitrary: every entry is a distinct batch row that receives the same bytes.
-__global__ void k_fan_place(const uint32_t* __restrict__ rest_x, const uint32_t* __restrict__ rest_slot,
-                            uint32_t* __restrict__ off, uint32_t n, uint32_t* __restrict__ list) {
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x)
-        list[atomicAdd(off + __ldg(rest_slot + k), 1u)] = __ldg(rest_x + k);
-}
-
 void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint64_t K,
                  const uint64_t* h_init, int64_t n_init_explicit, gx_changesets* out, bool trusted,
                  int mark_first, uint32_t presampled_epoch) {
@@ -2794,22 +2783,6 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     out->first_marked = (a.o_first != nullptr || a.o_fan_cnt != nullptr) && hs.n_first <= Keff;
     out->fan = out->first_marked && a.o_fan_cnt != nullptr;
     out->n_rest = out->first_marked ? A - hs.n_first : 0;
-    if (out->fan && !a.o_fan_off) {  // slot -> its other accesses: offsets by a scan of the counts, then placement
-        const uint32_t n = (uint32_t)hs.n_first;
-        const uint64_t nr = out->n_rest;
-        out->fan_off.reserve((uint64_t)n + 1);
-        out->fan_list.reserve(nr + 1);
-        GX_CUDA(cudaMemsetAsync(out->fan_cnt.p + n, 0, 4, st));  // scan sentinel
-        size_t tb = 0;
-        GX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
-        out->cub_tmp.reserve(tb + 16);
-        GX_CUDA(cub::DeviceScan::ExclusiveSum(out->cub_tmp.p, tb, out->fan_cnt.p, out->fan_off.p, (int)n + 1, st));
-        if (nr) {
-            k_fan_place<<<ctx->num_sms * 4, 256, 0, st>>>(out->rest_x.p, out->rest_slot.p, out->fan_off.p,
-                                                         (uint32_t)nr, out->fan_list.p);
-            GX_CHECK_LAUNCH();
-        }
-    }
     out->h_misses.assign(m32.begin(), m32.begin() + S);
     out->h_in_off.assign(S + 1, 0);
     out->h_out_off.assign(S + 1, 0);
