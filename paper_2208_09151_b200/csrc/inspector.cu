@@ -901,8 +901,22 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
 
         // CUT: threshold bucket b* over keys in (i, S] (every CTA, redundantly),
         // scanning (incumbents, new candidates) pairs so that the counts below
-        // b* come out of the same block scan
-        {
+        // b* come out of the same block scan. Shortcut: when the candidates
+        // keyed below NEVER are fewer than K, b* is NEVER and its counts follow
+        // from the NEVER bins alone (every cut at papers scale; acceptance c8)
+        const uint32_t inc_S = one ? (uint32_t)sm.hinc[S] : (uint32_t)((volatile int32_t*)a.hist_inc)[S];
+        const uint32_t new_S = one ? (uint32_t)sm.hnew[S] : ((volatile uint32_t*)hn)[S];
+        const uint32_t below_S = nres + m - inc_S - new_S;
+        if (K > 0 && below_S < K) {
+            if (tid == 0) {
+                sm.bc[0] = S;
+                sm.bc[1] = K - below_S;
+                sm.bc[2] = inc_S;
+                sm.bc[3] = new_S;
+                sm.bc[4] = nres - inc_S;
+                sm.bc[5] = m - new_S;
+            }
+        } else {
             if (tid == 0) sm.bc[0] = 0xFFFFFFFFu;
             __syncthreads();
             unsigned long long cum = 0;
@@ -2713,7 +2727,20 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         const uint32_t n_out_all = oo32[S];
         B.fin_big.reserve(S + 1);
         GX_CUDA(cudaMemsetAsync(B.fin_big.p + S, 0, 4, st));  // oversize-list count
-        if (n_out_all) {
+        uint32_t max_seg = 0;
+        for (uint64_t i = 0; i < S; ++i) max_seg = std::max<uint32_t>(max_seg, oo32[i + 1] - oo32[i]);
+        if (n_out_all && max_seg > kSortSeg) {
+            // an iteration evicts more than one block sort holds (e.g. S = 500
+            // at 5 %: 20-27K per cut): a device segmented sort of every list
+            size_t tb = 0;
+            GX_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, B.out_raw.p, out->out_ids.p, B.out_tagraw.p,
+                                                        B.tag_sorted.p, (int)n_out_all, (int)S, d_out_off.p,
+                                                        d_out_off.p + 1, st));
+            B.sort_tmp.reserve(tb + 16);
+            GX_CUDA(cub::DeviceSegmentedSort::SortPairs(B.sort_tmp.p, tb, B.out_raw.p, out->out_ids.p,
+                                                        B.out_tagraw.p, B.tag_sorted.p, (int)n_out_all, (int)S,
+                                                        d_out_off.p, d_out_off.p + 1, st));
+        } else if (n_out_all) {
             int id_bits = 1;
             while (id_bits < 32 && (1ull << id_bits) < N) ++id_bits;
             using BRS = cub::BlockRadixSort<uint32_t, kSortThreads, kSortItems, uint32_t>;
