@@ -2,11 +2,15 @@
 hot-path kernels: the persistent grid-barrier sampler (k_sample), the inspector
 with the Belady recurrence cutting every iteration (k_inspect, k_inspect_rec),
 the changeset executor (k_gather_tma2, k_apply_slots, k_gather_rows), the
-all-fit fan-out executor (k_fan_place, k_fan_rows) and the LRU policy kernels.
-Each case checks its result against the oracle, so a run that passes the
-sanitizer also passed parity.
+all-fit fan-out executor (k_fan_rows; the per-slot lists are built in
+k_inspect), the deferred-ordering post-pass (k_sort_outs, k_finish_changesets)
+and the LRU policy kernels. Each case checks its result against the oracle, so a
+run that passes the sanitizer also passed parity.
 
     compute-sanitizer --tool memcheck python profiles/sanitize_cases.py
+    GX_INSPECT_CTAS=8 GX_INSPECT_NEVER=2 compute-sanitizer ...   # the multi-CTA
+        recurrence (eviction pool, ticket spins, NEVER fast path) on the same
+        small traces, which otherwise run on one CTA
 """
 import os
 import sys
