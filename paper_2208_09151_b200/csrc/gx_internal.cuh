@@ -76,7 +76,7 @@ struct InspectScratch {
     DevBuf<int32_t> hist_inc;
     DevBuf<uint8_t> pmiss;
     // deferred-ordering recurrence (inspector.cu: recurrence_deferred, k_finish_changesets)
-    DevBuf<uint32_t> slot_tag, slot_nk, pnk, out_raw, out_tagraw, tag_sorted, ev_slot, fin_unres, blk_max, fin_big;
+    DevBuf<uint32_t> slot_tag, slot_nk, pnk, out_raw, out_tagraw, tag_sorted, ev_slot, fin_unres, blk_max;
     DevBuf<int32_t> never_hist;
     DevBuf<uint8_t> sort_tmp;
     DevBuf<uint32_t> o_pack;  // 2 IStates (32 words), then misses / in_off / out_off (S+1 each)

@@ -442,9 +442,15 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
 }
 // slot freed by eviction ticket t; its producer (a CTA that finished its own
 // evictions before consuming anything) never waits, so the spin ends
-__device__ __forceinline__ uint32_t take_slot(uint32_t* ev_slot, uint32_t t) {
+// (watchdog: a ticket never published -- an internal counting error -- fails
+// the call through st->err after ~2^26 polls instead of hanging the device)
+__device__ __forceinline__ uint32_t take_slot(uint32_t* ev_slot, uint32_t t, uint32_t* err) {
     uint32_t s;
+    uint32_t polls = 0;
     while ((s = ld_acquire_u32(ev_slot + t)) == kNever) {
+        ++polls;
+        if (polls == (1u << 26)) atomicOr(err, 16u);
+        if ((polls & 4095u) == 0 && (*(volatile uint32_t*)err & 16u)) return 0;  // (sticky: later waits end at once)
     }
     ev_slot[t] = kNever;  // each ticket is consumed once: clean for the next iteration
     return s;
@@ -990,10 +996,14 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         const bool scan_slots = sel == 1 || evict_b || nres - inc_before - inc_b > 0;
         if (fastnv) never_scan(a, sm, nres, d1_nv, st_ev, st_c, cs, out_total, S);
         else if (!scan_slots) {
-        } else if (nres >= 8u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
+        } else if (nres > 4u * G) p3_scan<8>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
+        else if (nres > 2u * G) p3_scan<4>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
+        else if (nres > G) p3_scan<2>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
         else p3_scan<1>(a, sm, nres, bstar, evict_b, sel == 1, st_ev, cs, out_total, S, coll, st_c);
+        IPHASE(a, 8);
         __syncthreads();
         if (fastnv || coll) stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
+        IPHASE(a, 9);
         if (sel == 2) {  // new candidates of b* (at most |ids_i|): materialise all
             for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < ni; p0 += G) {
                 const uint32_t pos = p0 + tid;
@@ -1011,6 +1021,7 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             __syncthreads();
             stage_flush(st_c, &cs->n_c, a.c_id, a.c_ref, true, &sm.bc[10]);
         }
+        IPHASE(a, 10);
         if (sel && !one && !small && !fastnv) hist_flush(sm.rh, (int32_t*)a.rh, 2048);
         // (hinc deltas stay in shared memory until the next P1: other CTAs may
         // still be reading hist_inc for b*). Without a select nothing of P3 is
@@ -1019,6 +1030,34 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         // histogram.
         if (sel) grid_sync(a.bar);
         IPHASE(a, 3);
+
+        // the final phase's loads (independent of the cut threshold) are issued
+        // before the select so their latency overlaps it: this CTA's missed
+        // positions (miss flag, key, node id, node key) and, sel 1, the first
+        // c_id entry of this thread
+        // (only when the candidate list is final here: small b* / NEVER path;
+        // the digit path materialises its candidates during the select)
+        const bool cid_final = sel == 1 && (small || fastnv);
+        const uint32_t nc_pre = cid_final ? *(volatile uint32_t*)&cs->n_c : 0u;
+        uint32_t cid0 = 0, cref0 = 0;
+        if (gtid < nc_pre) {
+            cid0 = a.c_id[gtid];
+            cref0 = a.c_ref[gtid];
+        }
+        constexpr int FQ = 4;
+        const bool reg = c1 - c0 <= FQ * blockDim.x;
+        uint32_t fkey[FQ], fv[FQ], fnk[FQ], fmask = 0, cnt = 0;
+        uint8_t fpm[FQ];
+        if (n_in && reg) {
+#pragma unroll
+            for (int j = 0; j < FQ; ++j) {
+                const uint32_t pos = c0 + tid + j * blockDim.x;
+                fpm[j] = pos < c1 ? a.pmiss[pos] : 0;
+                fkey[j] = pos < c1 ? a.pkey[pos] : 0u;
+                fv[j] = pos < c1 ? a.trace[base + pos] : 0u;
+                fnk[j] = pos < c1 ? a.pnk[pos] : 0u;
+            }
+        }
 
         uint32_t thr = 0xFFFFFFFFu;
         const uint32_t nc_sel = small || fastnv ? *(volatile uint32_t*)&cs->n_c : 0u;
@@ -1078,30 +1117,25 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         // beyond the insertions and the n_in - n_out fresh slots are published,
         // insertions beyond E take pool tickets -- every CTA publishes before it
         // takes, so the waits end.
-        // this CTA's insertions first (their loads overlap the evictions below):
-        // flags, keys, node keys and ids in registers when the chunk is at most
-        // FQ positions per thread, else recounted in the placement loop
+        auto ins_flag2 = [&](uint32_t pos, uint8_t pm, uint32_t key, uint32_t v) -> bool {
+            if (pos >= c1 || !pm) return false;
+            const uint32_t bk = bucket_of(key, S);
+            if (bk != bstar) return bk < bstar;
+            return admit_new != 0 && (sel != 2 || v <= thr);
+        };
         auto ins_flag = [&](uint32_t pos, uint32_t& key, uint32_t& v) -> bool {
             if (pos >= c1) return false;
             const uint8_t pm = a.pmiss[pos];
             key = a.pkey[pos];
             v = a.trace[base + pos];
-            if (!pm) return false;
-            const uint32_t bk = bucket_of(key, S);
-            if (bk != bstar) return bk < bstar;
-            return admit_new != 0 && (sel != 2 || v <= thr);
+            return ins_flag2(pos, pm, key, v);
         };
-        constexpr int FQ = 4;
-        const bool reg = c1 - c0 <= FQ * blockDim.x;
-        uint32_t fkey[FQ], fv[FQ], fnk[FQ], fmask = 0, cnt = 0;
+        // this CTA's insertion flags from the values loaded before the select
         if (n_in) {
             if (reg) {
 #pragma unroll
-                for (int j = 0; j < FQ; ++j) {
-                    const uint32_t pos = c0 + tid + j * blockDim.x;
-                    fnk[j] = pos < c1 ? a.pnk[pos] : 0u;
-                    if (ins_flag(pos, fkey[j], fv[j])) fmask |= 1u << j;
-                }
+                for (int j = 0; j < FQ; ++j)
+                    if (ins_flag2(c0 + tid + j * blockDim.x, fpm[j], fkey[j], fv[j])) fmask |= 1u << j;
                 cnt = __popc(fmask);
             } else {
                 uint32_t key, v;
@@ -1110,12 +1144,14 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         }
         // b*'s last evictions (sel 1: ids above the cut) join this CTA's list E
         if (sel == 1) {
-            const uint32_t nc = *(volatile uint32_t*)&cs->n_c;
+            const uint32_t nc = cid_final ? nc_pre : *(volatile uint32_t*)&cs->n_c;
             for (uint32_t k0 = blockIdx.x * blockDim.x; k0 < nc; k0 += G) {  // CTA-uniform
                 const uint32_t k = k0 + tid;
-                const bool ev = k < nc && a.c_id[k] > thr;
+                const bool first_pass = cid_final && k0 == blockIdx.x * blockDim.x;
+                const uint32_t id = k < nc ? (first_pass ? cid0 : a.c_id[k]) : 0u;
+                const bool ev = k < nc && id > thr;
                 if (ev) atomicSub(&sm.hinc[bstar], 1);
-                stage_put(st_ev, ev, 0, ev ? a.c_ref[k] : 0u);
+                stage_put(st_ev, ev, 0, ev ? (first_pass ? cref0 : a.c_ref[k]) : 0u);
                 __syncthreads();
                 ev_flush(a, st_ev, cs, out_total, false, &sm.bc[10], nhp);
             }
@@ -1124,6 +1160,7 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
         // pool: E beyond the insertions and the n_in - n_out fresh slots are
         // published, insertions beyond E take pool tickets -- every CTA
         // publishes before it takes, so the waits end
+        IPHASE(a, 11);
         if (n_in) {  // (n_out <= n_in: nothing leaves either when nothing enters)
             __syncthreads();
             const uint32_t nE = *st_ev.cnt;
@@ -1150,9 +1187,10 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
             for (uint32_t j = fr0 + tid; j < fr1; j += blockDim.x)
                 st_release_u32(a.ev_slot + sm.bc[14] + (j - fr0), nres + j);
             __syncthreads();  // E's out records read their slots before any placement rewrites them
+            IPHASE(a, 12);
             uint32_t k = ex;
             auto place_k = [&](uint32_t pos, uint32_t key, uint32_t nk, uint32_t v) {
-                const uint32_t sl = k < nE ? (uint32_t)st_ev.buf[k] : take_slot(a.ev_slot, sm.bc[15] + (k - nE));
+                const uint32_t sl = k < nE ? (uint32_t)st_ev.buf[k] : take_slot(a.ev_slot, sm.bc[15] + (k - nE), &a.st->err);
                 place_ins(a, sm, base + pos, key, nk, sl, S, v);
                 ++k;
             };
@@ -1165,6 +1203,7 @@ __device__ uint32_t recurrence_deferred(IArgs& a, ISmem<CAP>& sm) {
                 for (uint32_t pos = c0 + tid; pos < c1; pos += blockDim.x)
                     if (ins_flag(pos, key, v)) place_k(pos, key, a.pnk[pos], v);
             }
+            IPHASE(a, 13);
         }
         if (one) {
             __syncthreads();
@@ -2094,8 +2133,8 @@ __global__ void __launch_bounds__(IN_THREADS, 1) k_inspect_rec(IArgs a) {
 // The ordered changesets of a deferred recurrence, for every iteration at once.
 //  k_sort_outs: each iteration's raw out list sorted by node id (carrying the
 //     evicted occupancy's tag) in shared memory, one CTA per iteration
-//     (bitonic over <= kSortSeg entries; longer lists are left to k_finish,
-//     which orders them through the N-bit bitmap).
+//     (block radix sort, <= kSortSeg entries; the host sends every list
+//     through a device segmented sort when one is longer).
 //  k_finish_changesets:
 //  1. in-lists: the inserted accesses in trace order ARE the reference's
 //     in_ids / in_positions (iteration-major, position order within an
@@ -2116,8 +2155,7 @@ constexpr uint32_t kSortSeg = kSortThreads * kSortItems;  // entries one k_sort_
 __global__ void __launch_bounds__(kSortThreads) k_sort_outs(const uint32_t* __restrict__ out_off, uint32_t S,
                                                             const uint32_t* __restrict__ raw,
                                                             const uint32_t* __restrict__ rawtag, uint32_t* out_ids,
-                                                            uint32_t* tag_sorted, uint32_t* big, uint32_t* nbig,
-                                                            int id_bits) {
+                                                            uint32_t* tag_sorted, int id_bits) {
     using BRS = cub::BlockRadixSort<uint32_t, kSortThreads, kSortItems, uint32_t>;
     extern __shared__ unsigned char sort_smem[];  // (66 KB: dynamic)
     typename BRS::TempStorage& tmp = *reinterpret_cast<typename BRS::TempStorage*>(sort_smem);
@@ -2131,10 +2169,7 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_outs(const uint32_t* __re
             }
             continue;
         }
-        if (n > kSortSeg) {
-            if (tid == 0) big[atomicAdd(nbig, 1u)] = i;
-            continue;
-        }
+        if (n > kSortSeg) continue;  // (never: the host sorts such lists with a segmented sort)
         uint32_t k[kSortItems], v[kSortItems];
 #pragma unroll
         for (int j = 0; j < kSortItems; ++j) {  // blocked arrangement: thread t holds [t * items, ...)
@@ -2163,15 +2198,7 @@ struct FArgs {
     uint32_t* R;              // A: per inserted access, its slot (or kEv | parent access)
     const uint32_t* in_off;   // S+1
     const uint32_t* out_off;  // S+1
-    uint32_t* out_ids;        // sorted out ids (the oversize lists are written here)
-    uint32_t* out_tag;        // sorted out tags
-    const uint32_t* out_raw;  // raw out lists (oversize lists)
-    const uint32_t* out_tagraw;
-    const uint32_t* big;      // iterations whose out list k_sort_outs left (> kSortSeg)
-    const uint32_t* nbig;
-    uint32_t* bm_words;       // N-bit bitmap, clean
-    uint32_t nwords;
-    uint32_t* last;           // N, kNever when clean: tag of a marked node
+    const uint32_t* out_tag;  // sorted out tags
     uint32_t* o_in_ids;
     uint32_t* o_in_pos;
     uint32_t* o_in_slot;
@@ -2187,45 +2214,6 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish_changesets(FArgs f) {
     __shared__ uint32_t toff[kMaxIters + 1];
     const uint32_t tid = threadIdx.x, G = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + tid;
     for (uint32_t i = tid; i <= f.S; i += blockDim.x) toff[i] = f.toff[i];
-    // 0. out lists longer than kSortSeg: mark their nodes in the bitmap (tag
-    // parked in `last`), count per word range, walk in id order
-    const uint32_t nbig = *f.nbig;
-    const uint32_t wch = (f.nwords + gridDim.x - 1) / gridDim.x;
-    const uint32_t w0 = min(f.nwords, blockIdx.x * wch), w1 = min(f.nwords, w0 + wch);
-    for (uint32_t b = 0; b < nbig; ++b) {
-        const uint32_t i = f.big[b], lo = f.out_off[i], n = f.out_off[i + 1] - lo;
-        for (uint32_t k = gtid; k < n; k += G) {
-            const uint32_t u = f.out_raw[lo + k];
-            f.last[u] = f.out_tagraw[lo + k];
-            atomicOr(&f.bm_words[u >> 5], 1u << (u & 31));
-        }
-        grid_sync(f.bar);
-        uint32_t c = 0;
-        for (uint32_t w = w0 + tid; w < w1; w += blockDim.x) c += __popc(f.bm_words[w]);
-        c = block_sum(c, scan);
-        if (tid == 0) f.cta_cnt[blockIdx.x] = c;
-        grid_sync(f.bar);
-        uint32_t pre = 0;
-        for (uint32_t cc = tid; cc < blockIdx.x; cc += blockDim.x) pre += f.cta_cnt[cc];
-        pre = block_sum(pre, scan);
-        for (uint32_t p0 = w0; p0 < w1; p0 += blockDim.x) {  // CTA-uniform
-            const uint32_t w = p0 + tid;
-            uint32_t bits = w < w1 ? f.bm_words[w] : 0u;
-            uint32_t tot;
-            uint32_t k = pre + block_excl_scan((uint32_t)__popc(bits), scan, tot);
-            if (bits) f.bm_words[w] = 0;
-            while (bits) {
-                const uint32_t u = w * 32 + (__ffs(bits) - 1);
-                bits &= bits - 1;
-                f.out_ids[lo + k] = u;
-                f.out_tag[lo + k] = f.last[u];
-                f.last[u] = kNever;
-                ++k;
-            }
-            pre += tot;
-        }
-        grid_sync(f.bar);
-    }
     // 1. inserted accesses of this CTA's contiguous range of the trace (16-byte
     // aligned ranges, 16 flags per thread per pass)
     const uint32_t A16 = (f.A + 15) / 16;
@@ -2697,9 +2685,10 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
             if (htb.p[k]) std::fprintf(stderr, " s%d=%.1f", k, htb.p[k] / 1e3);
         if (htb.p[30] + htb.p[31]) {
             std::fprintf(stderr, " | allin=%llu cut=%llu phases(us):", htb.p[30], htb.p[31]);
-            const char* nm[8] = {"", "P1", "allin", "P3", "select", "P4", "P5", "P6"};
+            const char* nm[14] = {"", "P1", "allin", "P3", "select", "P4", "P5", "P6",
+                                  "p3scan", "p3flush", "p3mat", "fin_ev", "fin_rec", "fin_place"};
             if (defer) nm[5] = "final";
-            for (int k = 1; k < 8; ++k) std::fprintf(stderr, " %s=%.1f", nm[k], htb.p[16 + k] / 1e3);
+            for (int k = 1; k < (defer ? 14 : 8); ++k) std::fprintf(stderr, " %s=%.1f", nm[k], htb.p[16 + k] / 1e3);
             if (defer && std::getenv("GX_INSPECT_TRACE_CUTS")) {
                 std::fprintf(stderr, "\n[inspect cuts] i:nres:b*:sel:inc_b:new_b:n_out:n_in");
                 for (unsigned long long c = 0; c < std::min<unsigned long long>(htb.p[31], 256); ++c) {
@@ -2725,8 +2714,6 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
     if (defer && recurrence_ran && io32[S] > 0) {
         // ordered out lists: each iteration's raw out list sorted by node id
         const uint32_t n_out_all = oo32[S];
-        B.fin_big.reserve(S + 1);
-        GX_CUDA(cudaMemsetAsync(B.fin_big.p + S, 0, 4, st));  // oversize-list count
         uint32_t max_seg = 0;
         for (uint64_t i = 0; i < S; ++i) max_seg = std::max<uint32_t>(max_seg, oo32[i + 1] - oo32[i]);
         if (n_out_all && max_seg > kSortSeg) {
@@ -2756,7 +2743,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
             }
             k_sort_outs<<<(unsigned)std::min<uint64_t>(S, 2ull * ctx->num_sms), kSortThreads, sort_smem, st>>>(
                 d_out_off.p, (uint32_t)S, B.out_raw.p, B.out_tagraw.p, out->out_ids.p, B.tag_sorted.p,
-                B.fin_big.p, B.fin_big.p + S, id_bits);
+                id_bits);
             GX_CHECK_LAUNCH();
         }
         B.fin_unres.reserve(64);
@@ -2769,15 +2756,7 @@ void inspect_run(gx_ctx* ctx, const std::vector<uint64_t>& off, uint64_t N, uint
         fa.R = is.next_use.p;  // next use is dead after the recurrence
         fa.in_off = d_in_off.p;
         fa.out_off = d_out_off.p;
-        fa.out_ids = out->out_ids.p;
         fa.out_tag = B.tag_sorted.p;
-        fa.out_raw = B.out_raw.p;
-        fa.out_tagraw = B.out_tagraw.p;
-        fa.big = B.fin_big.p;
-        fa.nbig = B.fin_big.p + S;
-        fa.bm_words = B.bm_words.p;
-        fa.nwords = (uint32_t)((N + 31) / 32);
-        fa.last = is.last.p;
         fa.o_in_ids = out->in_ids.p;
         fa.o_in_pos = out->in_pos.p;
         fa.o_in_slot = out->in_slot.p;
