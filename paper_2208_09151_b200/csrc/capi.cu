@@ -495,8 +495,11 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         } else {
             size_t fr = 0, total = 0;
             GX_CUDA(cudaMemGetInfo(&fr, &total));
-            const uint64_t margin = (4ull << 30) + 16ull * sl.o[S];
-            resident = need + margin <= (uint64_t)fr + sl.batch.n;
+            // (the deferred recurrence keeps ~12 A-sized u32 arrays: trace,
+            // next use, acc_slot, raw/sorted out lists, in lists, ...)
+            const uint64_t margin = (4ull << 30) + 48ull * sl.o[S];
+            // (what the grow-only buffer would actually allocate, headroom included)
+            resident = (uint64_t)sl.batch.reserved_after(need) + margin <= (uint64_t)fr + sl.batch.n;
         }
         // fan-out form (default): each init row read once, written to its slot
         // and every batch row of its node; GX_FANOUT=0: fill + first use, then

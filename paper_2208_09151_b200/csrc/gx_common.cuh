@@ -315,9 +315,19 @@ struct DevBuf {
         n = count;
     }
     // grow-only, with 25% headroom so per-superbatch size jitter does not
-    // re-allocate (cudaMalloc/cudaFree stall the stream)
+    // re-allocate (cudaMalloc/cudaFree stall the stream); buffers of 4 GiB and
+    // more get 1/32 (a resident S = 500 superbatch is 46 GB of rows: 25 % would
+    // be 11 GB of HBM for jitter of about 1 %)
+    static size_t grow_to(size_t count, size_t cur) {
+        const size_t big = (size_t(4) << 30) / sizeof(T);
+        const size_t c = count + (count >= big ? count / 32 : count / 4);
+        const size_t g = cur + (cur >= big ? cur / 32 : cur / 4);
+        return std::max(c, g) + 64;
+    }
+    // elements reserve(count) would hold afterwards
+    size_t reserved_after(size_t count) const { return count > n ? grow_to(count, n) : n; }
     void reserve(size_t count) {
-        if (count > n) alloc(std::max(count + count / 4, n + n / 4) + 64);
+        if (count > n) alloc(grow_to(count, n));
     }
     void release() {
         if (p) cudaFree(p);
