@@ -48,7 +48,7 @@ constexpr int SB_IPT = GX_SB_IPT;
 #define GX_TABLE_SLACK 1
 #endif
 #ifndef GX_TABLE_BY_DRAWS
-#define GX_TABLE_BY_DRAWS 0
+#define GX_TABLE_BY_DRAWS 1
 #endif
 #ifndef GX_I_UNROLL
 #define GX_I_UNROLL 4
@@ -457,10 +457,14 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
             TRACE_STAMP(a, l, 0);
         }
         };
-        // GX_TABLE_BY_DRAWS=1 sizes layers >= 1 by the actual draw count (phase A
-        // first): tables about half as large, but measured slower at papers shape
-        // (phase E 1.22 vs 1.11 ms: the higher load costs more probes than the
-        // smaller footprint saves), so the default sizes by F_b * (1 + f).
+        // GX_TABLE_BY_DRAWS=1 (default) sizes layers >= 1 by the actual draw count
+        // (phase A first): the last layer's tables are half as large (0.39 vs
+        // 0.78 GB per papers superbatch, load <= 0.42). The sampler is bound by
+        // random DRAM accesses, so the smaller footprint wins: k_sample 1.84 ->
+        // 1.78 ms (2 A/B pairs, profiles/r02z_ab_table_by_draws.txt; round 1 had
+        // measured it slower before the F/H vectorisation). Load ~0.7 (slack 0)
+        // is far slower (2.80 ms): the probe chains grow. GX_TABLE_BY_DRAWS=0
+        // sizes by F_b * (1 + f).
         if (l == 0 || !GX_TABLE_BY_DRAWS) phase_d(false);
         if (a.L == 0) break;
         const uint32_t f = a.fan[l];
