@@ -354,6 +354,15 @@ __device__ __forceinline__ void draw_positions(uint32_t tk, uint64_t seed, uint6
 }
 
 // Clear the first H entries of each of the S per-batch tables (16-byte stores).
+// phase F's per-draw word for an unresolved draw whose table entry is e: 1 for
+// the winner (the entry holds this draw's position), 0 for a loser, or on the
+// last layer kNewBit | the winner's position so phase I finds the winner's
+// local id without re-reading the table (another random DRAM sector per loser)
+__device__ __forceinline__ uint32_t loser_code(unsigned long long e, uint32_t child, uint32_t p, bool last) {
+    if (e == (((unsigned long long)child << 32) | (kNewBit | p))) return 1u;
+    return last ? (kNewBit | ((uint32_t)e & ~kNewBit)) : 0u;
+}
+
 __device__ __forceinline__ void clear_region(unsigned long long* tab, uint64_t tab_cap, uint32_t H, uint32_t S) {
     const uint64_t total_threads = (uint64_t)gridDim.x * blockDim.x;
     const uint64_t per = H / 2;  // ulonglong2 per batch (H is a power of two >= 1024)
@@ -681,9 +690,9 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                         fl[j] = 0;
                         if (p0 + j < Tb && !(ds[j] & kResolved)) {
                             const unsigned long long e = btab[ds[j]];
-                            fl[j] = e == (((unsigned long long)ch[j] << 32) | (kNewBit | (p0 + j))) ? 1u : 0u;
+                            fl[j] = loser_code(e, ch[j], p0 + j, last_layer);
                         }
-                        s += fl[j];
+                        s += fl[j] == 1u;
                     }
                     *reinterpret_cast<uint4*>(a.drank + gd0) = make_uint4(fl[0], fl[1], fl[2], fl[3]);
                 }
@@ -698,10 +707,10 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                         if (!(ds & kResolved)) {
                             const unsigned long long e = btab[ds];
                             const uint32_t child = bedge[p].x;
-                            fl = e == (((unsigned long long)child << 32) | (kNewBit | p)) ? 1u : 0u;
+                            fl = loser_code(e, child, p, last_layer);
                         }
                         a.drank[gd] = fl;
-                        s += fl;
+                        s += fl == 1u;
                     }
                 }
 #endif
@@ -734,16 +743,16 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                 const uint64_t gd0 = (uint64_t)b * a.cap_draw + p0;
                 uint4 r4 = make_uint4(0, 0, 0, 0);
                 if (p0 < Tb) r4 = *reinterpret_cast<const uint4*>(a.drank + gd0);
-                fl[0] = r4.x;
-                fl[1] = p0 + 1 < Tb ? r4.y : 0u;
-                fl[2] = p0 + 2 < Tb ? r4.z : 0u;
-                fl[3] = p0 + 3 < Tb ? r4.w : 0u;
+                fl[0] = r4.x == 1u;
+                fl[1] = p0 + 1 < Tb && r4.y == 1u;
+                fl[2] = p0 + 2 < Tb && r4.z == 1u;
+                fl[3] = p0 + 3 < Tb && r4.w == 1u;
                 s = fl[0] + fl[1] + fl[2] + fl[3];
 #else
 #pragma unroll
                 for (int j = 0; j < SB_DIPT; ++j) {
                     const uint32_t p = p0 + j;
-                    fl[j] = p < Tb ? a.drank[(uint64_t)b * a.cap_draw + p] : 0;
+                    fl[j] = p < Tb && a.drank[(uint64_t)b * a.cap_draw + p] == 1u;
                     s += fl[j];
                 }
 #endif
@@ -840,19 +849,27 @@ __global__ void GX_SB_BOUNDS k_sample(SampArgs a) {
                     }
                 }
                 uint32_t val[IU];
+                if (last_layer) {
+                    // a loser's drank holds kNewBit | the winner's draw position
+                    // (phase F), and the winner's drank its local id (phase H):
+                    // no table read
 #pragma unroll
-                for (int j = 0; j < IU; ++j)  // resolved at insert time or a winner: nothing to do
-                    if (!(ds[j] & kResolved) && !rk[j]) val[j] = (uint32_t)tab[(uint64_t)bb[j] * a.tab_cap + ds[j]];
-                if (last_layer) {  // val = the winner's draw position: its local id sits in drank
+                    for (int j = 0; j < IU; ++j)
+                        if (!(ds[j] & kResolved) && (rk[j] & kNewBit))
+                            val[j] = a.drank[(uint64_t)bb[j] * a.cap_draw + (rk[j] & ~kNewBit)];
+#pragma unroll
+                    for (int j = 0; j < IU; ++j)
+                        if (!(ds[j] & kResolved) && (rk[j] & kNewBit))
+                            a.edges[(uint64_t)bb[j] * a.cap_e_batch + a.e_off[l] + pp[j]].x = val[j];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < IU; ++j)  // resolved at insert time or a winner: nothing to do
+                        if (!(ds[j] & kResolved) && !rk[j]) val[j] = (uint32_t)tab[(uint64_t)bb[j] * a.tab_cap + ds[j]];
 #pragma unroll
                     for (int j = 0; j < IU; ++j)
                         if (!(ds[j] & kResolved) && !rk[j])
-                            val[j] = a.drank[(uint64_t)bb[j] * a.cap_draw + (val[j] & ~kNewBit)];
+                            a.edges[(uint64_t)bb[j] * a.cap_e_batch + a.e_off[l] + pp[j]].x = val[j];
                 }
-#pragma unroll
-                for (int j = 0; j < IU; ++j)
-                    if (!(ds[j] & kResolved) && !rk[j])
-                        a.edges[(uint64_t)bb[j] * a.cap_e_batch + a.e_off[l] + pp[j]].x = val[j];
             }
             for (uint32_t b = blockIdx.x * blockDim.x + tid; b < S; b += total_threads) {
                 a.layer_count[(uint64_t)b * a.L + l] = a.T[b];
