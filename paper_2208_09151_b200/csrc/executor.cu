@@ -559,7 +559,7 @@ void launch_fan_rows(gx_ctx* ctx, const uint32_t* idx, uint32_t n, const uint8_t
                      uint8_t* batch) {
     if (!n) return;
     if (rb % 16) fail(GX_INVALID_ARGUMENT, "fan-out fill needs 16-byte rows");
-    static const int rr = env_int("GX_FAN_R", 8);  // slots per warp: 4, 8 or 16
+    static const int rr = env_int("GX_FAN_R", 16);  // slots per warp: 4, 8 or 16 (16: 2.83 vs 2.89 ms for 8, r02z_ab_fan_r.txt)
     auto go = [&](auto kfn, int R) {
         int bps = 0;
         GX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kfn, GA_THREADS, 0));
