@@ -42,7 +42,7 @@ constexpr int SB_THREADS = GX_SB_THREADS;
 #endif
 constexpr int SB_IPT = GX_SB_IPT;
 #ifndef GX_E_UNROLL
-#define GX_E_UNROLL 3  // draws in flight per thread in phase E (swept 2-6 at 64 registers: 3 best)
+#define GX_E_UNROLL 2  // draws in flight per thread in phase E (round 1: 3 best of 2-6; with the tables sized by draws 2 is: 1.758 vs 1.770 ms, 4: 1.808, r02z_ab_sampler_e.txt)
 #endif
 #ifndef GX_TABLE_SLACK  // table slots >= entry bound << SLACK (1: load <= 1/2)
 #define GX_TABLE_SLACK 1
