@@ -751,10 +751,22 @@ def main():
     lists = sum(s.sample_io.neighbor_lists_read for s in stats)
     C = sum(s.total_in + s.total_out for s in stats)
     fills = sum(s.fill_rows for s in stats)
+    samp = line("k_sample (stage: sampler)", sum(s.ms_sample for s in stats),
+                24 * lists + 16 * edges + 8 * rows, "24*P + 16*E + 8*U (SURVEY 8d; P = parents expanded)",
+                "random accesses (one scattered index read + one dedup-table probe/claim per draw)")
+    # the sampler's own ceiling is a rate of scattered accesses, not bytes: one
+    # draw = a random 4-byte index read + a dependent 8-byte table load/CAS,
+    # measured alone at 21.4 G draws/s (profiles/random_sectors.cu ->
+    # r02z_random_sectors.txt; 36.6 G/s for the index reads alone)
+    ceil_dps = 21.4e9
+    dps = edges / (sum(s.ms_sample for s in stats) / 1e3) if edges else None
+    samp["random_access"] = {"achieved_draws_per_s": dps, "ceiling_draws_per_s": ceil_dps,
+                             "frac": dps / ceil_dps if dps else None,
+                             "ceiling_source": "profiles/r02z_random_sectors.txt (draw: idx4 -> probe8)",
+                             "note": "whole sampler (every phase and layer) per draw; the draw loop alone "
+                                     "(last-layer phase E) runs at ~1.2x the ceiling (hub repeats hit L2)"}
     rooflines = [
-        line("k_sample (stage: sampler)", sum(s.ms_sample for s in stats),
-             24 * lists + 16 * edges + 8 * rows, "24*P + 16*E + 8*U (SURVEY 8d; P = parents expanded)",
-             "latency (dependent indptr -> indices -> dedup-table chains, grid barriers)"),
+        samp,
         line("k_flatten + k_inspect (stage: inspector)", sum(s.ms_inspect for s in stats),
              24 * rows + 16 * C + 8 * fills, "24*A + 16*C + 8*|init| (SURVEY 8d)",
              "latency (random node-array atomics, grid barriers)"),
