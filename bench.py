@@ -711,7 +711,9 @@ def main():
             "changeset_in_per_iter": sum(s.total_in for s in pst) / (n_p * cfg["S"]),
             "stages_ms": {"sample": sum(s.ms_sample for s in pst) / n_p,
                           "inspect (incl. Belady recurrence)": sum(s.ms_inspect for s in pst) / n_p,
-                          "switch (cache init)": sum(s.ms_switch for s in pst) / n_p,
+                          ("switch (init rows fanned out to the accesses they serve)"
+                           if any(s.init_fan for s in pst) else "switch (cache init)"):
+                              sum(s.ms_switch for s in pst) / n_p,
                           "gather + apply": sum(s.ms_gather for s in pst) / n_p},
             "inspect_us_per_iteration": 1e3 * sum(s.ms_inspect for s in pst) / (n_p * cfg["S"]),
             "gather_GBps": (f.row_bytes() * sum(s.gather_kernel_rows for s in pst) /
@@ -747,6 +749,7 @@ def main():
 
     fused = any(s.fused_fill for s in stats)
     fan = any(s.fan_out for s in stats)
+    ifan = any(getattr(s, "init_fan", False) for s in stats)
     staged = args.backing == "file" or comm is not None
     lists = sum(s.sample_io.neighbor_lists_read for s in stats)
     C = sum(s.total_in + s.total_out for s in stats)
@@ -789,6 +792,18 @@ def main():
         rooflines.append(line(fan_kernel, fan_ms, fan_bytes,
                               "<= (w + 4) per init row (read slot row if it has other accesses, range end) + "
                               "(w + 4) per other access (write batch row, list entry)"))
+    elif ifan:                  # changesets: the init rows fanned out in the switch
+        served = rows - rows_g  # accesses the init rows served
+        fan_kernel = "switch: init rows fanned out (k_ifan_count + scan + k_ifan_place + k_fan_rows)"
+        fan_ms = sum(s.ms_switch for s in stats)
+        fan_bytes = (2 * w + 12) * fills + (w + 4) * served + 16 * rows
+        rooflines += [
+            line(fan_kernel, fan_ms, fan_bytes,
+                 "(2w + 12) per init row (read row, write slot, id, count, range end) + (w + 4) per served "
+                 "access (write batch row, list entry) + 16 per access (trace + slot, two passes)"),
+            line("k_gather_rest (accesses the init rows do not serve) + miss counts", gk_ms,
+                 (2 * w + 4) * rows_g + 8 * rows, "(2w + 4) per copied row + 8 per access (trace + slot)"),
+        ]
     else:
         rooflines += [
             line("k_fill_first (switch fused with first uses)" if fused else "k_gather_rows<16,8> (switch: cache init)",
@@ -798,10 +813,10 @@ def main():
             line("k_gather_tma2 (bulk-copy row gather)", gk_ms, alg_bytes,
                  "(2w + 8) per row: read row, write row, u32 id + u32 slot"),
         ]
-    if fan:                     # the headline roofline is the fan-out kernel
+    if fan or ifan:             # the headline roofline is the fan-out kernel
         achieved = fan_bytes / (fan_ms / 1e3) / 1e9
         traffic = None
-        if os.path.exists(tp) and not staged:   # captured on the device-backed fan-out
+        if os.path.exists(tp) and not staged and not ifan:   # captured on the device-backed all-fit fan-out
             with open(tp) as fh:
                 traffic = json.load(fh).get("k_fan_dram_bytes_per_launch")
     S = cfg["S"]
@@ -871,11 +886,14 @@ def main():
                       "peak_source": peak_src,
                       "init_rows_per_launch": fills / n, "accesses_per_launch": rows / n,
                       "alg_bytes_per_launch": fan_bytes / n,
-                      "note": "all-fit superbatches: one launch per superbatch reads each init row once and "
-                              "writes it to its cache slot and to the batch row of every access of its node"
-                              if not staged else "staged tier: the scatter filled slots + first-use rows; the "
-                              "cache rows fan out to the other accesses"}
-                     if fan else
+                      "note": ("changeset superbatches: each init row is read once and written to its cache "
+                               "slot and to every access it serves; the other accesses are copied from the table"
+                               if ifan else
+                               "all-fit superbatches: one launch per superbatch reads each init row once and "
+                               "writes it to its cache slot and to the batch row of every access of its node"
+                               if not staged else "staged tier: the scatter filled slots + first-use rows; the "
+                               "cache rows fan out to the other accesses")}
+                     if fan or ifan else
                      {"kernel": "k_gather_tma2 (bulk-copy row gather)", "bound": "hbm", "achieved": achieved,
                       "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                       "peak_source": peak_src,

@@ -385,10 +385,13 @@ typedef struct gx_pipeline_stats {
     uint64_t fill_rows;        /* rows the switch wrote into cache slots (= init_size) */
     uint64_t gather_kernel_rows; /* rows the gather launches moved (all accesses; fused_fill 1:
                                     the accesses that are not an init node's first use; fused_fill 2:
-                                    0, or all accesses fanned out from the cache on staged tiers) */
+                                    0, or all accesses fanned out from the cache on staged tiers;
+                                    fused_fill 3: the accesses the init rows do not serve) */
     uint32_t fused_fill;       /* all-fit superbatch: 1 = the switch also wrote each init node's
                                   first-use batch row; 2 = fan-out: each init row was read once and
-                                  written to its slot and to every batch row of its node */
+                                  written to its slot and to every batch row of its node;
+                                  changeset superbatch: 3 = each init row was read once and written
+                                  to its slot and to every access it serves (slot still holding it) */
     uint32_t reserved0;
 } gx_pipeline_stats;
 gx_status gx_pipeline_create(gx_graph* g, gx_features* f, const uint32_t* fanouts,

@@ -1188,6 +1188,7 @@ class PipelineStats:
     gather_kernel_rows: int = 0  # rows the gather launches moved
     fused_fill: bool = False     # all-fit: the switch also wrote each init node's first batch row
     fan_out: bool = False        # all-fit, fan-out form: each init row written to all its batch rows
+    init_fan: bool = False       # changesets: each init row written to its slot + every access it serves
 
 
 def _io(c: IoStatsC) -> IoStats:
@@ -1247,8 +1248,8 @@ class Pipeline:
                              _io(st.gather_io), st.ms_sample, st.ms_inspect, st.ms_switch,
                              st.ms_gather, st.ms_gather_kernels, st.ms_apply_kernels, st.kernel_launches,
                              st.gather_launches, misses[:S].copy(), st.ms_storage, st.storage_rows,
-                             st.storage_bytes, st.fill_rows, st.gather_kernel_rows, bool(st.fused_fill),
-                             st.fused_fill == 2)
+                             st.storage_bytes, st.fill_rows, st.gather_kernel_rows, st.fused_fill in (1, 2),
+                             st.fused_fill == 2, st.fused_fill == 3)
 
     def batch(self, i: int, ticket: Optional[int] = None) -> np.ndarray:
         """Iteration i's gathered rows of a waited-for superbatch (default: the

@@ -68,6 +68,9 @@ struct PipeSlot {
     double ms_storage = 0;
     uint64_t storage_rows = 0, storage_bytes = 0;
     bool fused = false;
+    bool ifan = false;  // changeset regime: init rows fanned out in the switch (launch_init_fan)
+    gx::DevBuf<uint32_t> ifan_cnt, ifan_off, ifan_list;
+    gx::DevBuf<uint8_t> ifan_tmp;
     uint64_t gather_rows = 0;
     cudaEvent_t ev[6] = {};  // A: start, sampled, inspected; B: exec start, switched, done
     std::vector<cudaEvent_t> kev;
@@ -552,6 +555,19 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             GX_CUDA(cudaEventCreate(&e));
             sl.kev.push_back(e);
         }
+        // device-backed table, whole superbatch resident, changesets: the
+        // gathers of all S iterations are ONE launch (see (4)), and when the
+        // init rows serve most accesses (few inserts against the init set:
+        // papers @5 %, 25K inserts for 5.55M init slots) the switch fans each
+        // init row out to the accesses it serves and k_gather_rest copies the
+        // rest; with many inserts (cfg1: 540K for 100K slots) most rows would
+        // go through the rest copy, and k_gather_sb serves every access.
+        // GX_INIT_FAN: 0 off, 1 by that rule (default), 2 always.
+        static const bool one_gather = gx::env_int("GX_ONE_GATHER", 1) != 0;
+        static const int init_fan = gx::env_int("GX_INIT_FAN", 1);
+        const bool single = !fused && !file && sl.full && one_gather && p->f->rows_dev_view != nullptr;
+        sl.ifan = single && rb % 16 == 0 && sl.cs.n_init > 0 &&
+                  (init_fan == 2 || (init_fan == 1 && 4 * sl.cs.h_in_off[S] <= sl.cs.n_init));
         ctx->launch_stream = B;
         try {
             // (3) switch: the init rows into slots 0..n_init-1 (the inspector
@@ -591,6 +607,11 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 launch_fill_first(ctx, sl.cs.init.p, sl.cs.first_acc.p, (uint32_t)sl.cs.n_init, p->f->rows_dev_view,
                                   rb, p->cache_rows.p, sl.batch.p);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
+            } else if (sl.ifan) {
+                launch_init_fan(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p, (uint32_t)sl.cs.n_init,
+                                p->f->rows_dev_view, rb, p->cache_rows.p, sl.batch.p, sl.ifan_cnt, sl.ifan_off,
+                                sl.ifan_list, sl.ifan_tmp);
+                GX_CUDA(cudaEventRecord(sl.ev[4], B));
             } else {
                 launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
                                   sl.counters.p + 8 * S);
@@ -615,13 +636,14 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             // for the applies of iterations < i. The per-iteration miss / page
             // counters come from the inspector's resolved slots.
             // GX_ONE_GATHER=0: per-segment gathers + applies.
-            static const bool one_gather = gx::env_int("GX_ONE_GATHER", 1) != 0;
-            const bool single = !fused && !file && sl.full && one_gather && p->f->rows_dev_view != nullptr;
             if (single) {
                 GX_CUDA(cudaEventRecord(sl.kev[0], B));
-                if (!launch_gather_superbatch(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p,
-                                              (uint32_t)sl.cs.n_init, p->cache_rows.p, p->f->rows_dev_view, rb,
-                                              sl.batch.p))
+                if (sl.ifan)  // the init-served accesses were written by the switch
+                    launch_gather_rest(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p, (uint32_t)sl.cs.n_init,
+                                       p->f->rows_dev_view, rb, sl.batch.p, sl.counters.p + 8 * S + 5);
+                else if (!launch_gather_superbatch(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p,
+                                                   (uint32_t)sl.cs.n_init, p->cache_rows.p, p->f->rows_dev_view, rb,
+                                                   sl.batch.p))
                     launch_gather_resolved(ctx, sl.trace.p, nullptr, sl.o[S], nullptr, p->f->rows_dev_view, rb,
                                            sl.batch.p, sl.counters.p + 8 * (S + 1), nullptr, 0, false, false);
                 launch_count_iter_misses(ctx, sl.trace.p, sl.acc_slot.p, sl.d_off.p, (uint32_t)S, maxw, rb,
@@ -767,8 +789,10 @@ gx_status gx_pipeline_wait(gx_pipeline* p, uint64_t ticket, uint64_t* misses_per
             stats->kernel_launches = sl.launches;
             stats->gather_launches = sl.nseg;
             stats->fill_rows = sl.cs.n_init;
-            stats->gather_kernel_rows = sl.gather_rows;
-            stats->fused_fill = sl.fused ? (sl.cs.fan ? 2u : 1u) : 0u;
+            // init fan-out: the gather copies only the accesses the init rows
+            // do not serve (counted by k_gather_rest in the unused init block)
+            stats->gather_kernel_rows = sl.ifan ? cnt[8 * S + 5] : sl.gather_rows;
+            stats->fused_fill = sl.fused ? (sl.cs.fan ? 2u : 1u) : (sl.ifan ? 3u : 0u);
             stats->reserved0 = 0;
             stats->ms_storage = sl.ms_storage;
             stats->storage_rows = sl.storage_rows;

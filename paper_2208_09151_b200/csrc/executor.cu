@@ -17,6 +17,8 @@
 #include <mutex>
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "gx_internal.cuh"
 
 struct gx_cache {
@@ -1063,6 +1065,151 @@ bool launch_gather_superbatch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* 
         ids, slots, (uint32_t)n, init, n_init, cache_rows, store, (uint32_t)rb, out);
     GX_CHECK_LAUNCH();
     return true;
+}
+
+// Changeset regime, device-backed table, whole superbatch resident: the switch
+// fanned out to every access its init rows serve (the all-fit fan-out,
+// generalised). Access x is init-served when its serving slot s = acc_slot[x]
+// is an init slot still holding init[s] == trace[x] -- a slot is a copy of the
+// table row (feature_cache.hpp:115-126), so an init node evicted and later
+// re-inserted into its own slot serves the same bytes. Each init row is read
+// once and written to its slot and to the batch rows of those accesses; the
+// other accesses (misses, hits on inserted nodes) are copied from the table by
+// k_gather_rest; the changesets' rows land in their slots afterwards
+// (launch_apply_all), so the cache ends in the reference's state.
+__device__ __forceinline__ bool init_served(uint32_t s, uint32_t v, const uint32_t* __restrict__ init,
+                                            uint32_t n_init) {
+    return s < n_init && __ldg(init + s) == v;
+}
+
+__global__ void __launch_bounds__(256) k_ifan_count(const uint32_t* __restrict__ trace,
+                                                    const uint32_t* __restrict__ acc_slot, uint32_t A,
+                                                    const uint32_t* __restrict__ init, uint32_t n_init,
+                                                    uint32_t* cnt) {
+    const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < A; x0 += 4 * G) {
+        uint32_t s[4], v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t x = x0 + j * G;
+            s[j] = x < A ? __ldg(acc_slot + x) : kNever;
+            v[j] = x < A ? __ldg(trace + x) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (init_served(s[j], v[j], init, n_init)) atomicAdd(&cnt[s[j]], 1u);
+    }
+}
+
+// off[s] = start of slot s's list on entry, its end on exit (k_fan_rows reads
+// slot s as [off[s - 1], off[s]))
+__global__ void __launch_bounds__(256) k_ifan_place(const uint32_t* __restrict__ trace,
+                                                    const uint32_t* __restrict__ acc_slot, uint32_t A,
+                                                    const uint32_t* __restrict__ init, uint32_t n_init,
+                                                    uint32_t* off, uint32_t* list) {
+    const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t x0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < A; x0 += 4 * G) {
+        uint32_t s[4], v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint64_t x = x0 + j * G;
+            s[j] = x < A ? __ldg(acc_slot + x) : kNever;
+            v[j] = x < A ? __ldg(trace + x) : 0u;
+        }
+        bool f[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            f[j] = init_served(s[j], v[j], init, n_init);
+            if (f[j]) s[j] = atomicAdd(&off[s[j]], 1u);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (f[j]) list[s[j]] = (uint32_t)(x0 + j * G);
+    }
+}
+
+// every access that is not init-served: its row from the table. A warp takes
+// 32 consecutive accesses and copies the selected rows 4 at a time (16 bytes
+// per lane per row).
+__global__ void __launch_bounds__(256) k_gather_rest(const uint32_t* __restrict__ trace,
+                                                     const uint32_t* __restrict__ acc_slot, uint32_t A,
+                                                     const uint32_t* __restrict__ init, uint32_t n_init,
+                                                     const uint8_t* __restrict__ store, uint32_t row_bytes,
+                                                     uint8_t* __restrict__ out, unsigned long long* nrows) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t nvec = row_bytes / 16;
+    uint32_t copied = 0;
+    for (uint64_t b0 = warp * 32; b0 < A; b0 += nwarps * 32) {
+        const uint64_t x = b0 + lane;
+        uint32_t v = 0;
+        bool rest = false;
+        if (x < A) {
+            v = __ldg(trace + x);
+            rest = !init_served(__ldg(acc_slot + x), v, init, n_init);
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, rest);
+        copied += __popc(m);
+        while (m) {
+            uint32_t q[4];
+            int k = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                q[j] = 0;
+                if (m) {
+                    q[j] = __ffs(m) - 1;
+                    m &= m - 1;
+                    k = j + 1;
+                }
+            }
+            uint32_t vq[4];  // (shuffles before the lane-dependent copy loop: rows < 512 B idle lanes)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) vq[j] = __shfl_sync(0xffffffffu, v, q[j]);
+            for (uint32_t c = lane; c < nvec; c += 32) {
+                uint4 t[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j < k) t[j] = ld_nc(reinterpret_cast<const uint4*>(store + (uint64_t)vq[j] * row_bytes) + c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (j < k) st_na(reinterpret_cast<uint4*>(out + (b0 + q[j]) * row_bytes) + c, t[j]);
+            }
+        }
+    }
+    if (lane == 0 && copied) atomicAdd(nrows, (unsigned long long)copied);
+}
+
+void launch_init_fan(gx_ctx* ctx, const uint32_t* trace, const uint32_t* acc_slot, uint64_t A, const uint32_t* init,
+                     uint32_t n_init, const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch,
+                     DevBuf<uint32_t>& cnt, DevBuf<uint32_t>& off, DevBuf<uint32_t>& list, DevBuf<uint8_t>& tmp) {
+    if (rb % 16) fail(GX_INVALID_ARGUMENT, "init fan-out needs 16-byte rows");
+    if (!n_init) return;
+    cudaStream_t st = lstream(ctx);
+    cnt.reserve(n_init + 1);
+    off.reserve(n_init + 1);
+    list.reserve(std::max<uint64_t>(A, 1));
+    GX_CUDA(cudaMemsetAsync(cnt.p, 0, (n_init + 1) * sizeof(uint32_t), st));
+    const unsigned g = std::min<uint64_t>((A + 1023) / 1024 + 1, (uint64_t)ctx->num_sms * 8);
+    k_ifan_count<<<g, 256, 0, st>>>(trace, acc_slot, (uint32_t)A, init, n_init, cnt.p);
+    GX_CHECK_LAUNCH();
+    size_t tb = 0;
+    GX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, (int)(n_init + 1), st));
+    tmp.reserve(std::max<size_t>(tb, 16));
+    GX_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, (int)(n_init + 1), st));
+    k_ifan_place<<<g, 256, 0, st>>>(trace, acc_slot, (uint32_t)A, init, n_init, off.p, list.p);
+    GX_CHECK_LAUNCH();
+    launch_fan_rows(ctx, init, n_init, store, rb, cache_rows, nullptr, off.p, list.p, batch);
+}
+
+void launch_gather_rest(gx_ctx* ctx, const uint32_t* trace, const uint32_t* acc_slot, uint64_t A,
+                        const uint32_t* init, uint32_t n_init, const uint8_t* store, uint64_t rb, uint8_t* batch,
+                        unsigned long long* nrows) {
+    if (!A) return;
+    const unsigned g = (unsigned)std::min<uint64_t>((A + 255) / 256, (uint64_t)ctx->num_sms * 8);
+    k_gather_rest<<<g, 256, 0, lstream(ctx)>>>(trace, acc_slot, (uint32_t)A, init, n_init, store, (uint32_t)rb,
+                                               batch, nrows);
+    GX_CHECK_LAUNCH();
 }
 
 // All changesets of a superbatch applied at once, in effect (the pipeline's

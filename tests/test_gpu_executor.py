@@ -424,13 +424,16 @@ def test_pipeline_rejects_duplicate_seeds(gx, oracle):
     assert st.sampled_edges == ref_edges
 
 
-@pytest.mark.parametrize("one_gather", [1, 0])
-def test_pipeline_cache_state_matches_reference_replay(gx, oracle, one_gather):
+@pytest.mark.parametrize("one_gather,init_fan", [(1, 2), (1, 0), (0, 0)])
+def test_pipeline_cache_state_matches_reference_replay(gx, oracle, one_gather, init_fan):
     """The fused pipeline's executor leaves the feature cache in the state the
     reference's FeatureCache reaches after S x (gather, apply_changeset)
-    (feature_cache.hpp:58-130): every occupied slot holds its node's row. Run
-    with the one-launch executor (GX_ONE_GATHER=1: one gather, changesets
-    applied at once, last insert per slot) and the per-segment one."""
+    (feature_cache.hpp:58-130): every occupied slot holds its node's row, and
+    every iteration's batch holds the rows of its ids. Run with the one-launch
+    executor (GX_ONE_GATHER=1: one gather, changesets applied at once, last
+    insert per slot) with and without the init fan-out (GX_INIT_FAN=2 forces
+    it: the switch writes each init row to every access it serves, the gather
+    copies the rest), and with the per-segment one."""
     import json
     import os
     import subprocess
@@ -457,13 +460,16 @@ for i, ids in enumerate(trace):
     c.apply(b, ids, sim["in_ids"][a:e], sim["in_pos"][a:e], sim["out_ids"][q:w])
 got = p.cache_rows()
 ok, occ = True, 0
+for i, ids in enumerate(trace):
+    ok &= bool(np.array_equal(p.batch(i), rows[ids.astype(np.int64)]))
+ok &= bool(st.init_fan) == (%d == 1 and %d == 2)
 for v in c.resident():
     s = c.slot(int(v))
     occ += 1
     ok &= bool(np.array_equal(got[s], rows[int(v)]))
 print(json.dumps({"ok": ok, "occupied": occ, "inserts": int(st.total_in), "misses": int(st.total_misses)}))
-""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GX_ONE_GATHER=str(one_gather))
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))), one_gather, init_fan)
+    env = dict(os.environ, GX_ONE_GATHER=str(one_gather), GX_INIT_FAN=str(init_fan))
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     res = json.loads(r.stdout.strip().splitlines()[-1])
