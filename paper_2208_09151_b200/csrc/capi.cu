@@ -69,7 +69,7 @@ struct PipeSlot {
     uint64_t storage_rows = 0, storage_bytes = 0;
     bool fused = false;
     bool ifan = false;  // changeset regime: init rows fanned out in the switch (launch_init_fan)
-    gx::DevBuf<uint32_t> ifan_cnt, ifan_off, ifan_list;
+    gx::DevBuf<uint32_t> ifan_cnt, ifan_off, ifan_list, ifan_rank;
     gx::DevBuf<uint8_t> ifan_tmp;
     uint64_t gather_rows = 0;
     cudaEvent_t ev[6] = {};  // A: start, sampled, inspected; B: exec start, switched, done
@@ -610,7 +610,7 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             } else if (sl.ifan) {
                 launch_init_fan(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p, (uint32_t)sl.cs.n_init,
                                 p->f->rows_dev_view, rb, p->cache_rows.p, sl.batch.p, sl.ifan_cnt, sl.ifan_off,
-                                sl.ifan_list, sl.ifan_tmp);
+                                sl.ifan_list, sl.ifan_rank, sl.ifan_tmp);
                 GX_CUDA(cudaEventRecord(sl.ev[4], B));
             } else {
                 launch_cache_init(ctx, sl.cs.init.p, (uint32_t)sl.cs.n_init, nullptr, p->f, p->cache_rows.p,
@@ -639,8 +639,8 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             if (single) {
                 GX_CUDA(cudaEventRecord(sl.kev[0], B));
                 if (sl.ifan)  // the init-served accesses were written by the switch
-                    launch_gather_rest(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p, (uint32_t)sl.cs.n_init,
-                                       p->f->rows_dev_view, rb, sl.batch.p, sl.counters.p + 8 * S + 5);
+                    launch_gather_rest(ctx, sl.trace.p, sl.ifan_rank.p, sl.o[S], p->f->rows_dev_view, rb, sl.batch.p,
+                                       sl.counters.p + 8 * S + 5);
                 else if (!launch_gather_superbatch(ctx, sl.trace.p, sl.acc_slot.p, sl.o[S], sl.cs.init.p,
                                                    (uint32_t)sl.cs.n_init, p->cache_rows.p, p->f->rows_dev_view, rb,
                                                    sl.batch.p))

@@ -1082,10 +1082,12 @@ __device__ __forceinline__ bool init_served(uint32_t s, uint32_t v, const uint32
     return s < n_init && __ldg(init + s) == v;
 }
 
-__global__ void __launch_bounds__(256) k_ifan_count(const uint32_t* __restrict__ trace,
-                                                    const uint32_t* __restrict__ acc_slot, uint32_t A,
-                                                    const uint32_t* __restrict__ init, uint32_t n_init,
-                                                    uint32_t* cnt) {
+// rank[x] = x's index in its init slot's list (ticket of a per-slot count),
+// kNever when x is not init-served
+__global__ void __launch_bounds__(256) k_ifan_rank(const uint32_t* __restrict__ trace,
+                                                   const uint32_t* __restrict__ acc_slot, uint32_t A,
+                                                   const uint32_t* __restrict__ init, uint32_t n_init,
+                                                   uint32_t* cnt, uint32_t* rank) {
     const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t x0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < A; x0 += 4 * G) {
         uint32_t s[4], v[4];
@@ -1096,35 +1098,32 @@ __global__ void __launch_bounds__(256) k_ifan_count(const uint32_t* __restrict__
             v[j] = x < A ? __ldg(trace + x) : 0u;
         }
 #pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = init_served(s[j], v[j], init, n_init) ? atomicAdd(&cnt[s[j]], 1u) : kNever;
+#pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (init_served(s[j], v[j], init, n_init)) atomicAdd(&cnt[s[j]], 1u);
+            if (x0 + j * G < A) rank[x0 + j * G] = v[j];
     }
 }
 
-// off[s] = start of slot s's list on entry, its end on exit (k_fan_rows reads
-// slot s as [off[s - 1], off[s]))
-__global__ void __launch_bounds__(256) k_ifan_place(const uint32_t* __restrict__ trace,
-                                                    const uint32_t* __restrict__ acc_slot, uint32_t A,
-                                                    const uint32_t* __restrict__ init, uint32_t n_init,
-                                                    uint32_t* off, uint32_t* list) {
+// list[start[s] + rank[x]] = x for every init-served access (no atomics)
+__global__ void __launch_bounds__(256) k_ifan_place(const uint32_t* __restrict__ acc_slot,
+                                                    const uint32_t* __restrict__ rank, uint32_t A,
+                                                    const uint32_t* __restrict__ start, uint32_t* list) {
     const uint64_t G = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t x0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x0 < A; x0 += 4 * G) {
-        uint32_t s[4], v[4];
+        uint32_t s[4], r[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint64_t x = x0 + j * G;
-            s[j] = x < A ? __ldg(acc_slot + x) : kNever;
-            v[j] = x < A ? __ldg(trace + x) : 0u;
-        }
-        bool f[4];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            f[j] = init_served(s[j], v[j], init, n_init);
-            if (f[j]) s[j] = atomicAdd(&off[s[j]], 1u);
+            r[j] = x < A ? __ldg(rank + x) : kNever;
+            s[j] = r[j] != kNever ? __ldg(acc_slot + x) : 0u;
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-            if (f[j]) list[s[j]] = (uint32_t)(x0 + j * G);
+            if (r[j] != kNever) r[j] += __ldg(start + s[j]);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (r[j] != kNever) list[r[j]] = (uint32_t)(x0 + j * G);
     }
 }
 
@@ -1132,8 +1131,7 @@ __global__ void __launch_bounds__(256) k_ifan_place(const uint32_t* __restrict__
 // 32 consecutive accesses and copies the selected rows 4 at a time (16 bytes
 // per lane per row).
 __global__ void __launch_bounds__(256) k_gather_rest(const uint32_t* __restrict__ trace,
-                                                     const uint32_t* __restrict__ acc_slot, uint32_t A,
-                                                     const uint32_t* __restrict__ init, uint32_t n_init,
+                                                     const uint32_t* __restrict__ rank, uint32_t A,
                                                      const uint8_t* __restrict__ store, uint32_t row_bytes,
                                                      uint8_t* __restrict__ out, unsigned long long* nrows) {
     const uint32_t lane = threadIdx.x & 31;
@@ -1147,7 +1145,7 @@ __global__ void __launch_bounds__(256) k_gather_rest(const uint32_t* __restrict_
         bool rest = false;
         if (x < A) {
             v = __ldg(trace + x);
-            rest = !init_served(__ldg(acc_slot + x), v, init, n_init);
+            rest = __ldg(rank + x) == kNever;
         }
         uint32_t m = __ballot_sync(0xffffffffu, rest);
         copied += __popc(m);
@@ -1182,33 +1180,35 @@ __global__ void __launch_bounds__(256) k_gather_rest(const uint32_t* __restrict_
 
 void launch_init_fan(gx_ctx* ctx, const uint32_t* trace, const uint32_t* acc_slot, uint64_t A, const uint32_t* init,
                      uint32_t n_init, const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch,
-                     DevBuf<uint32_t>& cnt, DevBuf<uint32_t>& off, DevBuf<uint32_t>& list, DevBuf<uint8_t>& tmp) {
+                     DevBuf<uint32_t>& cnt, DevBuf<uint32_t>& off, DevBuf<uint32_t>& list, DevBuf<uint32_t>& rank,
+                     DevBuf<uint8_t>& tmp) {
     if (rb % 16) fail(GX_INVALID_ARGUMENT, "init fan-out needs 16-byte rows");
     if (!n_init) return;
     cudaStream_t st = lstream(ctx);
     cnt.reserve(n_init + 1);
     off.reserve(n_init + 1);
     list.reserve(std::max<uint64_t>(A, 1));
+    rank.reserve(std::max<uint64_t>(A, 1));
     GX_CUDA(cudaMemsetAsync(cnt.p, 0, (n_init + 1) * sizeof(uint32_t), st));
     const unsigned g = std::min<uint64_t>((A + 1023) / 1024 + 1, (uint64_t)ctx->num_sms * 8);
-    k_ifan_count<<<g, 256, 0, st>>>(trace, acc_slot, (uint32_t)A, init, n_init, cnt.p);
+    k_ifan_rank<<<g, 256, 0, st>>>(trace, acc_slot, (uint32_t)A, init, n_init, cnt.p, rank.p);
     GX_CHECK_LAUNCH();
     size_t tb = 0;
     GX_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, off.p, (int)(n_init + 1), st));
     tmp.reserve(std::max<size_t>(tb, 16));
     GX_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, off.p, (int)(n_init + 1), st));
-    k_ifan_place<<<g, 256, 0, st>>>(trace, acc_slot, (uint32_t)A, init, n_init, off.p, list.p);
+    k_ifan_place<<<g, 256, 0, st>>>(acc_slot, rank.p, (uint32_t)A, off.p, list.p);
     GX_CHECK_LAUNCH();
-    launch_fan_rows(ctx, init, n_init, store, rb, cache_rows, nullptr, off.p, list.p, batch);
+    // off = list starts (n_init + 1 entries); k_fan_rows reads slot s as
+    // [o[s - 1], o[s]) with o[-1] = 0, i.e. o = off + 1
+    launch_fan_rows(ctx, init, n_init, store, rb, cache_rows, nullptr, off.p + 1, list.p, batch);
 }
 
-void launch_gather_rest(gx_ctx* ctx, const uint32_t* trace, const uint32_t* acc_slot, uint64_t A,
-                        const uint32_t* init, uint32_t n_init, const uint8_t* store, uint64_t rb, uint8_t* batch,
-                        unsigned long long* nrows) {
+void launch_gather_rest(gx_ctx* ctx, const uint32_t* trace, const uint32_t* rank, uint64_t A, const uint8_t* store,
+                        uint64_t rb, uint8_t* batch, unsigned long long* nrows) {
     if (!A) return;
     const unsigned g = (unsigned)std::min<uint64_t>((A + 255) / 256, (uint64_t)ctx->num_sms * 8);
-    k_gather_rest<<<g, 256, 0, lstream(ctx)>>>(trace, acc_slot, (uint32_t)A, init, n_init, store, (uint32_t)rb,
-                                               batch, nrows);
+    k_gather_rest<<<g, 256, 0, lstream(ctx)>>>(trace, rank, (uint32_t)A, store, (uint32_t)rb, batch, nrows);
     GX_CHECK_LAUNCH();
 }
 

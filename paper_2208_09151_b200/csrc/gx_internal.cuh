@@ -271,15 +271,16 @@ bool launch_gather_superbatch(gx_ctx* ctx, const uint32_t* ids, const uint32_t* 
                               const uint32_t* init, uint32_t n_init, const uint8_t* cache_rows, const uint8_t* store,
                               uint64_t rb, uint8_t* out);
 // changeset regime, device-backed, whole superbatch resident: the switch fans
-// each init row out to its slot and to every access it serves (init_served:
-// acc_slot[x] = s < n_init with init[s] == trace[x]); launch_gather_rest copies
-// every other access from the table. Scratch buffers are the caller's.
+// each init row out to its slot and to every access it serves (init-served:
+// acc_slot[x] = s < n_init with init[s] == trace[x]; rank[x] = its index in
+// slot s's list, kNever otherwise); launch_gather_rest copies every access
+// with rank kNever from the table. Scratch buffers are the caller's.
 void launch_init_fan(gx_ctx* ctx, const uint32_t* trace, const uint32_t* acc_slot, uint64_t A, const uint32_t* init,
                      uint32_t n_init, const uint8_t* store, uint64_t rb, uint8_t* cache_rows, uint8_t* batch,
-                     DevBuf<uint32_t>& cnt, DevBuf<uint32_t>& off, DevBuf<uint32_t>& list, DevBuf<uint8_t>& tmp);
-void launch_gather_rest(gx_ctx* ctx, const uint32_t* trace, const uint32_t* acc_slot, uint64_t A,
-                        const uint32_t* init, uint32_t n_init, const uint8_t* store, uint64_t rb, uint8_t* batch,
-                        unsigned long long* nrows);  // += rows copied
+                     DevBuf<uint32_t>& cnt, DevBuf<uint32_t>& off, DevBuf<uint32_t>& list, DevBuf<uint32_t>& rank,
+                     DevBuf<uint8_t>& tmp);
+void launch_gather_rest(gx_ctx* ctx, const uint32_t* trace, const uint32_t* rank, uint64_t A, const uint8_t* store,
+                        uint64_t rb, uint8_t* batch, unsigned long long* nrows);  // += rows copied
 // every changeset of a superbatch applied at once (the cache is not read in
 // between): each slot gets its last insert's batch row; `last` = K zeroed u32
 // marks (left zeroed), in_off / bat_off = insert / batch-row offsets per iteration
