@@ -499,8 +499,9 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             size_t fr = 0, total = 0;
             GX_CUDA(cudaMemGetInfo(&fr, &total));
             // (the deferred recurrence keeps ~12 A-sized u32 arrays: trace,
-            // next use, acc_slot, raw/sorted out lists, in lists, ...)
-            const uint64_t margin = (4ull << 30) + 48ull * sl.o[S];
+            // next use, acc_slot, raw/sorted out lists, in lists, ...; the init
+            // fan-out two more: per-access ranks and the slot lists)
+            const uint64_t margin = (4ull << 30) + 56ull * sl.o[S];
             // (what the grow-only buffer would actually allocate, headroom included)
             resident = (uint64_t)sl.batch.reserved_after(need) + margin <= (uint64_t)fr + sl.batch.n;
         }
