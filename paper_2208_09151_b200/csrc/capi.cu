@@ -69,6 +69,7 @@ struct PipeSlot {
     uint64_t storage_rows = 0, storage_bytes = 0;
     bool fused = false;
     bool ifan = false;  // changeset regime: init rows fanned out in the switch (launch_init_fan)
+    uint64_t last_row = 0;  // not resident: row of the last iteration in the batch window
     gx::DevBuf<uint32_t> ifan_cnt, ifan_off, ifan_list, ifan_rank;
     gx::DevBuf<uint8_t> ifan_tmp;
     uint64_t gather_rows = 0;
@@ -538,7 +539,12 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
         const bool fused = sl.cs.first_marked;  // implies all-fit (no changesets) and resident
         sl.fused = fused;
         sl.gather_rows = fused ? (sl.cs.fan ? (file ? sl.cs.n_rest : 0) : sl.cs.n_rest) : sl.o[S];
-        sl.batch.reserve(std::max<uint64_t>((sl.full ? sl.o[S] : maxw) * rb, 16));
+        // not resident: a window of up to GX_BATCH_WINDOW iterations' rows, so a
+        // run of iterations without changesets is still one gather launch
+        // (S = 500 all-fit at 35-50 % cache: 500 launches of ~30 us -> 32)
+        static const uint64_t win_iters = (uint64_t)std::max(1, gx::env_int("GX_BATCH_WINDOW", 16));
+        const uint64_t win_rows = sl.full ? sl.o[S] : std::max(maxw, std::min(sl.o[S], win_iters * maxw));
+        sl.batch.reserve(std::max<uint64_t>(win_rows * rb, 16));
         sl.h_off.reserve(S + 1);
         sl.d_off.reserve(S + 1);
         for (uint64_t i = 0; i <= S; ++i) sl.h_off.p[i] = (uint32_t)sl.o[i];
@@ -624,7 +630,8 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
             auto empty_cs = [&](uint64_t i) {
                 return sl.cs.h_in_off[i + 1] == sl.cs.h_in_off[i] && sl.cs.h_out_off[i + 1] == sl.cs.h_out_off[i];
             };
-            auto rows_of = [&](uint64_t i) { return sl.batch.p + (sl.full ? sl.o[i] * rb : 0); };
+            uint64_t seg0 = 0;  // first iteration of the current segment (the window's row 0 when not resident)
+            auto rows_of = [&](uint64_t i) { return sl.batch.p + (sl.full ? sl.o[i] : sl.o[i] - sl.o[seg0]) * rb; };
             uint64_t nseg = 0;
             // device-backed table, whole superbatch resident, changesets: the
             // gathers of all S iterations are ONE bulk-copy launch (k_gather_sb).
@@ -692,6 +699,10 @@ gx_status gx_pipeline_submit(gx_pipeline* p, const uint64_t* seeds_flat, const u
                 uint64_t e = i;  // segment [i, e]
                 if (sl.full)
                     while (e + 1 < S && empty_cs(e)) ++e;
+                else
+                    while (e + 1 < S && empty_cs(e) && sl.o[e + 2] - sl.o[i] <= win_rows) ++e;
+                seg0 = i;
+                if (e + 1 == S) sl.last_row = sl.full ? sl.o[S - 1] : sl.o[S - 1] - sl.o[i];
                 GX_CUDA(cudaEventRecord(sl.kev[3 * nseg], B));
                 // a one-iteration segment charges its misses through the kernel's
                 // per-warp counters (the iteration's counter block has the same
@@ -812,7 +823,7 @@ gx_status gx_pipeline_batch(gx_pipeline* p, uint64_t ticket, uint64_t i, const v
         if (i >= sl.S) fail(GX_OUT_OF_RANGE, "iteration index out of range");
         if (!sl.full && i + 1 != sl.S)
             fail(GX_LOGIC_ERROR, "superbatch exceeded GX_BATCH_BUDGET_MB: only the last iteration's rows are resident");
-        const uint8_t* src = sl.batch.p + (sl.full ? sl.o[i] * p->f->row_bytes : 0);
+        const uint8_t* src = sl.batch.p + (sl.full ? sl.o[i] : sl.last_row) * p->f->row_bytes;
         const uint64_t n = sl.o[i + 1] - sl.o[i];
         if (rows) *rows = src;
         if (n_rows) *n_rows = n;

@@ -240,9 +240,13 @@ def test_pipeline_segments_resident_batches(gx, oracle, K):
         p.batch(len(trace))
 
 
-def test_pipeline_batch_budget_fallback(oracle):
-    """GX_BATCH_BUDGET_MB=0: one iteration-sized buffer reused per iteration;
-    results identical, only the last iteration stays readable."""
+@pytest.mark.parametrize("K,window", [(300, 16), (5000, 16), (5000, 3)])
+def test_pipeline_batch_budget_fallback(oracle, K, window):
+    """GX_BATCH_BUDGET_MB=0: the superbatch is not resident; a window of up to
+    GX_BATCH_WINDOW iterations' rows is reused (runs of iterations without
+    changesets -- all of them when everything fits, K = 5000 -- gather in one
+    launch per window); results identical, only the last iteration stays
+    readable."""
     import subprocess
     import sys
     import textwrap
@@ -257,7 +261,7 @@ def test_pipeline_batch_budget_fallback(oracle):
         g, f = gx.GraphFile.from_csc(ip, ind), gx.FeatureFile.from_array(rows)
         plan = o.plan_seed_batches(o.train_ids(n, 2, 0.3), 30, o.epoch_seed(2, 0))[:8]
         trace = [o.sample_batch(ip, ind, b, [4, 3], o.derive_seed(2, i))[0] for i, b in enumerate(plan)]
-        K = 300
+        K = %d
         sim = o.simulate(trace, n, K, o.compute_init_set(trace, K, n))
         p = gx.Pipeline(g, f, [4, 3], K, digest=True)
         st = p.run_superbatch(plan, 2, 0)
@@ -271,10 +275,10 @@ def test_pipeline_batch_budget_fallback(oracle):
         except gx.LogicError:
             pass
         print("OK")
-    """)
+    """) % K
     import os
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, GX_BATCH_BUDGET_MB="0", PYTHONPATH=root)
+    env = dict(os.environ, GX_BATCH_BUDGET_MB="0", GX_BATCH_WINDOW=str(window), PYTHONPATH=root)
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
 
