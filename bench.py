@@ -330,6 +330,64 @@ def ref_prepare(gx, g, f, cfg, samples, workdir, log):
     return gpath, fpath
 
 
+def dropin_run(gx, ctx, g, cfg, batches, fpath, workdir, K, first_batch=0):
+    """The reference's stage sequence (TrainingRunner::run_superbatch,
+    pipeline.hpp:338-377) through this library's drop-in API: superbatch_sample
+    writing the ids/adj runtime files -> precompute_changesets (init/update
+    files) -> FeatureCache ctor on features.bin through the file tier (pread, as
+    the reference's FeatureFile) -> per iteration read the ids/update files,
+    gather into a host RowMatrix (pinned) and apply_changeset. Same inputs and
+    files as the reference arm; the graph is the bench's (graph.bin was written
+    from it) and the feature file is opened before the clock starts."""
+    import torch
+    f2 = gx.FeatureFile.open(fpath, "file", ctx=ctx)
+    rt = os.path.join(workdir, "rt_dropin")
+    shutil.rmtree(rt, ignore_errors=True)
+    os.makedirs(rt)
+    S = len(batches)
+    t = [time.perf_counter()]
+    res = gx.superbatch_sample(g, None, batches, cfg["fanouts"], SEED_RUN, first_batch, 0, rt)
+    t.append(time.perf_counter())
+    trace = gx.FileTrace([gx.api.ids_file_path(rt, 0, i) for i in range(S)])
+    gx.precompute_changesets(trace, cfg["N"], K, rt, 0, ctx=ctx)
+    t.append(time.perf_counter())
+    cache = gx.FeatureCache(f2, gx.read_init_file(gx.api.init_file_path(rt, 0)), K)
+    t.append(time.perf_counter())
+    host = None
+    rows = d2h = 0
+    b = gx.Batch(ctx, f2.dim(), f2.dtype)  # one RowMatrix reused by every gather (as the reference's loop)
+    loop = np.zeros(4)  # read files, gather, rows to host, apply
+    for i in range(S):
+        c0 = time.perf_counter()
+        ids = gx.read_ids_file(gx.api.ids_file_path(rt, 0, i))
+        cs = gx.read_update_file(gx.api.update_file_path(rt, 0, i))
+        c1 = time.perf_counter()
+        b, _ = cache.gather(f2, ids, out=b)
+        n = b.rows
+        c2 = time.perf_counter()
+        if host is None or host.shape[0] < n:
+            host = torch.empty((max(n, 1) * 5 // 4, f2.dim()), dtype=torch.float32, pin_memory=True).numpy()
+        gx.api.check(gx.api.lib.gx_batch_copy_to_host(b.h, host.ctypes.data))
+        c3 = time.perf_counter()
+        rows += n
+        d2h += n * f2.row_bytes()
+        cache.apply_changeset(b, ids, cs)
+        loop += np.diff([c0, c1, c2, c3, time.perf_counter()])
+    ctx.synchronize()
+    t.append(time.perf_counter())
+    edges = sum(res_edges(gx.read_adj_file(gx.api.adj_file_path(rt, 0, i))) for i in range(S))
+    shutil.rmtree(rt, ignore_errors=True)
+    return dict(edges=edges, seconds=t[-1] - t[0], rows=rows, d2h=d2h,
+                stages={"sample_files_s": t[1] - t[0], "precompute_files_s": t[2] - t[1],
+                        "cache_ctor_s": t[3] - t[2], "main_loop_s": t[4] - t[3],
+                        "loop_read_files_s": loop[0], "loop_gather_s": loop[1], "loop_rows_to_host_s": loop[2],
+                        "loop_apply_s": loop[3]})
+
+
+def res_edges(layers):
+    return sum(len(e) for e in layers)
+
+
 def ref_run(batches, cfg, gpath, fpath, workdir, workers, global_seed=SEED_RUN, first_batch=0):
     """One superbatch through the reference's own stages (oracle/_ref,
     gxr_run_superbatch): superbatch_sample with `workers` threads writing the
@@ -931,6 +989,23 @@ def main():
                     gpath, fpath = ref_prepare(gx, g, f, cfg, [(sbs[0][:nb], 0)], workdir, log)
                     cores = cpu_cores()
                     r = ref_run(sbs[0][:nb], cfg, gpath, fpath, workdir, cores)
+                    # the same superbatch and files through the drop-in API (host rows out)
+                    try:
+                        dropin_run(gx, ctx, g, cfg, sbs[0][:nb], fpath, workdir, K_entries)  # warm-up
+                        dr = dropin_run(gx, ctx, g, cfg, sbs[0][:nb], fpath, workdir, K_entries)
+                        out["e2e_dropin"] = {
+                            "value": dr["edges"] / dr["seconds"], "unit": "sampled_edges/s",
+                            "seconds_per_superbatch": dr["seconds"], "stages": dr["stages"],
+                            "d2h_bytes_per_step": dr["d2h"], "rows": dr["rows"],
+                            "vs_reference_same_sample": r["seconds"] / dr["seconds"],
+                            "note": "the reference's stage sequence through the drop-in API on the same "
+                                    "superbatch and files as cpu_baseline: superbatch_sample -> ids/adj files -> "
+                                    "precompute_changesets -> init/update files -> FeatureCache on features.bin "
+                                    "(file tier, pread) -> per iteration gather into pinned host rows + "
+                                    "apply_changeset; wall clock, one superbatch after one untimed pass"}
+                        log(f"drop-in API: {dr['edges']} edges in {dr['seconds']:.2f}s {dr['stages']}")
+                    except Exception as e:  # never blocks the headline
+                        out["e2e_dropin"] = {"error": repr(e)}
                 finally:
                     shutil.rmtree(workdir, ignore_errors=True)
                 out["cpu_baseline"] = {
